@@ -1,0 +1,17 @@
+"""CPU ORACLE for the fractal-encoder search (TEST INFRASTRUCTURE ONLY).
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference legs may
+import this package.  It shares no code with the CUDA path (paper_1501_04140_b200/), and
+neither imports the other; both read their inputs from fic_inputs/.
+
+  fic_oracle.c  -- O1: plain C (int64 + binary64, -ffp-contract=off, OpenMP over ranges)
+  exact.py      -- O2: literal Eq. (1)/(3)/(5) in exact rationals for tiny images
+  oracle.py     -- ctypes wrapper + build() for O1
+
+Parity status per function: see DESIGN.md §"Oracle pins".  None is "parity unpinned" except
+the decoded-image PSNR sanity report, which the oracle does not compute.
+"""
+from .oracle import (  # noqa: F401
+    build, lib, lut, threshold, axis_candidates, entropy_keys, kept_list, isometry,
+    decimate, o_code, encode_level, encode, RECORD_DTYPE, num_threads,
+)
