@@ -1,0 +1,147 @@
+/*
+ * fic.h -- C ABI of the B200 fractal-encoder search library (libfic.so, sm_100a).
+ *
+ * Method: H. Miar Naimi, M. Salarian, "A Fast Fractal Image Compression Algorithm Using
+ * Predefined Values for Contrast Scaling", arXiv 1501.04140 (/root/reference/PAPER.md, cited as
+ * P:<line>).  Readings of the points the paper leaves open are DESIGN.md §"Readings" [Rn].
+ *
+ * Conventions for every call
+ *   - Pointers are DEVICE pointers unless the argument name starts with h_ (host memory).
+ *   - Images are N x N uint8, row-major, pixel (x, y) = img[y * N + x].
+ *   - Work is enqueued on the context's CUDA stream.  Calls that return host-visible counts
+ *     (fic_build_domain_pool, fic_encode, fic_encode_host) synchronise that stream before
+ *     returning; fic_encode_level is stream-asynchronous.
+ *   - No call throws.  Every call returns a fic_status; on failure fic_last_error(ctx) holds a
+ *     one-line message (valid until the next call on that ctx).
+ *   - Ownership: the caller owns img, ranges and out buffers; the library owns the context's
+ *     scratch memory and fic_pool storage (release with fic_pool_destroy / fic_ctx_destroy).
+ *   - A context is not thread-safe; use one context per host thread / stream.
+ */
+#ifndef FIC_H_
+#define FIC_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct fic_ctx fic_ctx;   /* per-device: stream, scratch arena, LUTs, level pools   */
+typedef struct fic_pool fic_pool; /* one level's entropy-filtered domain pool (device data) */
+
+typedef enum {
+    FIC_OK = 0,
+    FIC_ERR_ARG = 1,        /* bad scalar argument (B not a power of two, s outside [0,1], ...) */
+    FIC_ERR_SHAPE = 2,      /* N not a multiple of B_max, 2B > N, ...                          */
+    FIC_ERR_EMPTY_POOL = 3, /* no domain block survives the entropy filter                     */
+    FIC_ERR_CAPACITY = 4,   /* output buffer too small; *h_n_out holds the required count       */
+    FIC_ERR_CUDA = 5,       /* CUDA runtime error (message in fic_last_error)                  */
+    FIC_ERR_NCCL = 6,       /* reserved for the native collective path                         */
+    FIC_ERR_NOMEM = 7       /* device or host allocation failed                                */
+} fic_status;
+
+/* One affine map of the partitioned IFS = one coded range block.  40 bytes. */
+typedef struct {
+    int32_t rx, ry;   /* range origin (pixels)                                               */
+    int32_t B;        /* range size (pixels per side)                                        */
+    int32_t dom;      /* rank of the domain in the level's kept list (row-major order) [R18] */
+    int32_t dx, dy;   /* domain origin (pixels), multiples of the step L               */
+    uint8_t iso;      /* isometry k in 0..7 applied to the decimated domain [R2]             */
+    uint8_t s_idx;    /* index of s in the level's s list (listed order)                     */
+    uint8_t o_code;   /* 8-bit quantised offset o (Eq. 3) [R11]                        */
+    uint8_t accepted; /* E <= t_B^2 * B^2 ("acceptable error") or B == B_min [R14,R15]  */
+    double err;       /* E = sum_i (s d_i + o - r_i)^2, Eq. 1, unquantised o, binary64 */
+} fic_record;
+
+/* ------------------------------------------------------------------------------------ context */
+
+/* Create a context on CUDA device `device` that enqueues on `cuda_stream` (a cudaStream_t;
+ * NULL = legacy default stream).  *out receives the handle. */
+fic_status fic_ctx_create(int32_t device, void *cuda_stream, fic_ctx **out);
+fic_status fic_ctx_set_stream(fic_ctx *ctx, void *cuda_stream);
+fic_status fic_ctx_destroy(fic_ctx *ctx);
+const char *fic_last_error(const fic_ctx *ctx);
+
+/* Per-level counters and device times of the last fic_encode / fic_encode_level on ctx.
+ * Times are CUDA-event durations on the ctx stream (ms); enable with fic_ctx_set_timing. */
+typedef struct {
+    int32_t B;
+    int64_t n_candidates, n_kept, n_ranges, n_accepted;
+    int64_t pairs;          /* n_ranges * n_kept * 8 range-domain-isometry pairs scored      */
+    int64_t exact_evals;    /* (range, domain) pairs that took the exact binary64 path       */
+    float ms_pool, ms_search, ms_finalize;
+} fic_level_stats;
+
+fic_status fic_ctx_set_timing(fic_ctx *ctx, int32_t enable);
+fic_status fic_get_stats(const fic_ctx *ctx, fic_level_stats *h_out, int32_t max_levels,
+                         int32_t *h_n_levels);
+
+/* --------------------------------------------------------------------------- domain pool */
+
+/* Build one level's domain pool (Abstract P:14):
+ *   candidates: 2B x 2B blocks at (x, y) = (aL, bL), x + 2B <= N, y + 2B <= N, row-major;
+ *   entropy key of the raw block, keep iff tau < 0 or H > tau (nats, strict) [R3-R6];
+ *   kept blocks decimated by 2x2 sums (D' = 4d) [R1] and their moments.
+ * img: device [N*N]; B in {2,4,8,16,32}; L >= 1; 2B <= N.
+ * Errors: ARG, SHAPE, EMPTY_POOL (the pool is still returned for inspection), CUDA, NOMEM.
+ * Synchronises the ctx stream (the kept count is returned on the host). */
+fic_status fic_build_domain_pool(fic_ctx *ctx, const uint8_t *img, int32_t N, int32_t B,
+                                 int32_t L, double tau_nats, fic_pool **out);
+
+/* Host view of a pool.  keep_mask [n_candidates] u8, kept [n_kept] int32 (ascending candidate
+ * indices), keys [n_candidates] int64 entropy keys (m * H_bits * 2^32 fixed point) -- all
+ * device pointers owned by the pool.  Any output pointer may be NULL. */
+fic_status fic_pool_info(const fic_pool *pool, int64_t *h_n_candidates, int64_t *h_n_kept,
+                         const uint8_t **keep_mask, const int32_t **kept, const int64_t **keys);
+fic_status fic_pool_destroy(fic_pool *pool);
+
+/* ------------------------------------------------------------------------------ search */
+
+/* Match every range of `ranges` (device int32 [n_r][2] = (rx, ry), each a multiple of the
+ * pool's B) against every kept domain x 8 isometries x every s of h_s (host double [n_s],
+ * each in [0,1]; 1 <= n_s <= 16), scoring Eq. 1 with o from Eq. 3, and write the
+ * lexicographically first minimiser (E; dom, iso, s_idx) of each range to out[r] (device
+ * fic_record [n_r]).  accepted = is_min_level || E <= rms_tol^2 * B^2.
+ * Stream-asynchronous.  Errors: ARG, SHAPE, EMPTY_POOL, CUDA. */
+fic_status fic_encode_level(fic_ctx *ctx, const uint8_t *img, int32_t N, const fic_pool *pool,
+                            const int32_t *ranges, int64_t n_r, const double *h_s, int32_t n_s,
+                            double rms_tol, int32_t is_min_level, fic_record *out);
+
+/* Full quadtree encode: levels B = B_max, B_max/2, ..., B_min; level i uses step L,
+ * entropy threshold h_tau[i] (nats, < 0 keeps all), the s list h_s[off_i .. off_i+h_n_s[i])
+ * (off_i = sum of earlier h_n_s), and RMS tolerance h_rms_tol[i].  Level B_max starts from
+ * all (uB, vB) blocks; rejected ranges are split into their 4 children.
+ * Sharding (multi-GPU, DESIGN.md §"Multi-GPU"): only top-level blocks t (row-major index) with
+ * t % n_shards == shard, and their descendants, are encoded; n_shards = 1 is the whole image.
+ * out: device fic_record [capacity]; accepted leaves sorted by B descending, then (ry, rx).
+ * *h_n_out receives the number of records (also on FIC_ERR_CAPACITY).  Synchronous. */
+fic_status fic_encode(fic_ctx *ctx, const uint8_t *img, int32_t N, int32_t B_max, int32_t B_min,
+                      int32_t L, const double *h_tau, const double *h_s, const int32_t *h_n_s,
+                      const double *h_rms_tol, int32_t shard, int32_t n_shards, fic_record *out,
+                      int64_t capacity, int64_t *h_n_out);
+
+/* Same as fic_encode with HOST buffers: h_img [N*N] is copied to the device, h_out [capacity]
+ * receives the records (device->host copy inside the call).  Synchronous. */
+fic_status fic_encode_host(fic_ctx *ctx, const uint8_t *h_img, int32_t N, int32_t B_max,
+                           int32_t B_min, int32_t L, const double *h_tau, const double *h_s,
+                           const int32_t *h_n_s, const double *h_rms_tol, int32_t shard,
+                           int32_t n_shards, fic_record *h_out, int64_t capacity,
+                           int64_t *h_n_out);
+
+/* Merge per-shard record lists (each sorted by B desc, ry, rx) into one canonical list.
+ * in: device fic_record [n_shards][stride]; h_counts: host int64 [n_shards]; out: device
+ * fic_record [sum(h_counts)].  Stream-asynchronous. */
+fic_status fic_merge_shards(fic_ctx *ctx, const fic_record *in, const int64_t *h_counts,
+                            int32_t n_shards, int64_t stride, fic_record *out);
+
+/* Host-only: the entropy fixed-point table lut[c] = round-half-even(c log2(c) 2^32),
+ * c = 0..mmax (h_lut host int64 [mmax+1]).  No device work. */
+fic_status fic_entropy_lut(int64_t *h_lut, int32_t mmax);
+
+/* Library version string (host-only). */
+const char *fic_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FIC_H_ */

@@ -1,0 +1,544 @@
+// fic_api.cu -- the C ABI of include/fic.h: contexts, pools, the per-level driver and the
+// quadtree loop (§2 line 40).
+#include <cuda_runtime.h>
+#include <quadmath.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "fic_internal.cuh"
+
+using fic::Buf;
+using fic::Pool;
+
+struct fic_pool {
+    Pool P;
+};
+
+struct fic_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    int num_sms = 148;
+    std::string err;
+    int timing = 0;
+    int64_t lut[4097];
+    int64_t *d_delta = nullptr;  // delta[t] = lut[t+1] - lut[t], t < 4096
+    Pool levels[fic::kMaxLevels];
+    Buf b_blocksum, b_counts, b_rng[2], b_rec, b_acc, b_child, b_part, b_t2f, b_img, b_out,
+        b_scounts;
+    unsigned long long *h_counts = nullptr;  // pinned [64]
+    std::vector<fic_level_stats> stats;
+    cudaEvent_t ev[fic::kMaxLevels][5] = {};  // pool start, search start, search end, finalize end, pool end
+};
+
+namespace {
+
+// ---------------------------------------------------------------------------- host helpers
+fic_status cuda_fail(fic_ctx *ctx, cudaError_t e, const char *what, int line) {
+    if (ctx) {
+        char buf[512];
+        snprintf(buf, sizeof buf, "CUDA error %d (%s) at fic_api.cu:%d in %s", (int)e,
+                 cudaGetErrorString(e), line, what);
+        ctx->err = buf;
+    }
+    return e == cudaErrorMemoryAllocation ? FIC_ERR_NOMEM : FIC_ERR_CUDA;
+}
+fic_status fail(fic_ctx *ctx, fic_status st, const std::string &msg) {
+    if (ctx) ctx->err = msg;
+    return st;
+}
+#define CK(x)                                                               \
+    do {                                                                    \
+        cudaError_t e_ = (x);                                               \
+        if (e_ != cudaSuccess) return cuda_fail(ctx, e_, #x, __LINE__);     \
+    } while (0)
+#define CKS(x)                                   \
+    do {                                         \
+        fic_status s_ = (x);                     \
+        if (s_ != FIC_OK) return s_;             \
+    } while (0)
+
+cudaError_t grow(fic_ctx *ctx, Buf &b, size_t bytes) {
+    if (bytes == 0) bytes = 16;
+    if (b.cap >= bytes) return cudaSuccess;
+    if (b.p) {
+        if (ctx) cudaStreamSynchronize(ctx->stream);
+        cudaFree(b.p);
+        b.p = nullptr;
+        b.cap = 0;
+    }
+    const size_t nb = bytes + bytes / 4 + 256;
+    cudaError_t e = cudaMalloc(&b.p, nb);
+    if (e != cudaSuccess) return e;
+    b.cap = nb;
+    return cudaSuccess;
+}
+template <class T>
+T *ptr(Buf &b) {
+    return reinterpret_cast<T *>(b.p);
+}
+
+void free_buf(Buf &b) {
+    if (b.p) cudaFree(b.p);
+    b.p = nullptr;
+    b.cap = 0;
+}
+void free_pool(Pool &P) {
+    free_buf(P.b_keys); free_buf(P.b_keep); free_buf(P.b_kept); free_buf(P.b_Dt);
+    free_buf(P.b_SDf); free_buf(P.b_SD); free_buf(P.b_C); free_buf(P.b_misc);
+}
+
+bool pow2(int32_t v) { return v > 0 && (v & (v - 1)) == 0; }
+
+// round-half-even(c log2(c) 2^32) in binary128, via the natural log (reading R6)
+void make_lut(int64_t *lut, int32_t mmax) {
+    const __float128 inv_ln2 = 1 / logq((__float128)2);
+    for (int32_t c = 0; c <= mmax; ++c) {
+        if (c < 2) {
+            lut[c] = 0;
+            continue;
+        }
+        const __float128 v = (__float128)c * logq((__float128)c) * inv_ln2 * (__float128)4294967296.0;
+        lut[c] = (int64_t)nearbyintq(v);
+    }
+}
+
+// T = floor(((tau log2(e)) m) 2^32), binary64 left to right (readings R5, R6)
+int64_t entropy_threshold(double tau, int32_t m) {
+    volatile double t = tau * 1.4426950408889634;
+    t = t * (double)m;
+    t = t * 4294967296.0;
+    return (int64_t)std::floor(t);
+}
+
+// ------------------------------------------------------------------------- pool building
+fic_status pool_enqueue(fic_ctx *ctx, Pool &P, const uint8_t *img, int32_t N, int32_t B,
+                        int32_t L, double tau) {
+    P.device = ctx->device;
+    P.N = N; P.B = B; P.L = L; P.n = B * B;
+    P.A = (N - 2 * B) / L + 1;
+    P.n_c = (int64_t)P.A * P.A;
+    const int64_t tiles_max = (P.n_c + fic::kTileD - 1) / fic::kTileD;
+    const int64_t slots = tiles_max * fic::kTileD;
+    CK(grow(ctx, P.b_keys, sizeof(int64_t) * P.n_c));
+    CK(grow(ctx, P.b_keep, P.n_c + 16));
+    CK(grow(ctx, P.b_kept, sizeof(int32_t) * P.n_c));
+    CK(grow(ctx, P.b_Dt, sizeof(float) * slots * P.n));
+    CK(grow(ctx, P.b_SDf, sizeof(float) * slots));
+    CK(grow(ctx, P.b_SD, sizeof(int32_t) * slots));
+    CK(grow(ctx, P.b_C, sizeof(int64_t) * slots));
+    CK(grow(ctx, P.b_misc, 2 * sizeof(unsigned long long)));
+    CK(grow(ctx, ctx->b_blocksum, sizeof(int64_t) * fic::select_blocksum_len(P.n_c)));
+    P.keys = ptr<int64_t>(P.b_keys); P.keep = ptr<uint8_t>(P.b_keep);
+    P.kept = ptr<int32_t>(P.b_kept); P.Dt = ptr<float>(P.b_Dt); P.SDf = ptr<float>(P.b_SDf);
+    P.SD = ptr<int32_t>(P.b_SD); P.C = ptr<int64_t>(P.b_C);
+    P.d_misc = ptr<unsigned long long>(P.b_misc);
+    cudaStream_t st = ctx->stream;
+    CK(cudaMemsetAsync(P.d_misc, 0, 2 * sizeof(unsigned long long), st));
+    const int32_t m = 4 * B * B;
+    const int use_tau = tau >= 0.0;
+    const int64_t T = use_tau ? entropy_threshold(tau, m) : 0;
+    CK(fic::launch_entropy_keys(img, N, B, L, P.A, ctx->d_delta, ctx->lut[m], T, use_tau, P.keys,
+                                P.keep, st));
+    CK(fic::launch_select_index(P.keep, P.n_c, ptr<int64_t>(ctx->b_blocksum), P.kept, &P.d_misc[0],
+                                st));
+    CK(fic::launch_pool_gather(img, N, B, L, P.A, P.kept, &P.d_misc[0], tiles_max, P.Dt, st));
+    CK(fic::launch_pool_moments(img, N, B, L, P.A, P.kept, &P.d_misc[0], slots, P.SD, P.SDf, P.C,
+                                &P.d_misc[1], st));
+    return FIC_OK;
+}
+
+// after a stream sync: copy the pool's counters into the host struct
+void pool_take_counts(Pool &P, const unsigned long long *h) {
+    P.n_k = (int64_t)h[0];
+    P.cmax = (int64_t)h[1];
+    P.n_tiles = (P.n_k + fic::kTileD - 1) / fic::kTileD;
+}
+
+fic_status check_level(fic_ctx *ctx, int32_t N, int32_t B, int32_t L) {
+    if (!pow2(B) || B < 2) return fail(ctx, FIC_ERR_ARG, "B must be a power of two >= 2");
+    if (B > 16)
+        return fail(ctx, FIC_ERR_ARG, "B > 16 is not supported by the CUDA search kernel yet");
+    if (L < 1) return fail(ctx, FIC_ERR_ARG, "L must be >= 1");
+    if (N < 1 || 2 * B > N) return fail(ctx, FIC_ERR_SHAPE, "2B > N: no domain block fits");
+    return FIC_OK;
+}
+
+fic_status check_s(fic_ctx *ctx, const double *h_s, int32_t n_s) {
+    if (!h_s || n_s < 1 || n_s > fic::kMaxS)
+        return fail(ctx, FIC_ERR_ARG, "need 1 <= n_s <= 16 contrast values");
+    for (int j = 0; j < n_s; ++j)
+        if (!(h_s[j] >= 0.0 && h_s[j] <= 1.0))
+            return fail(ctx, FIC_ERR_ARG, "contrast values s must lie in [0,1]");
+    return FIC_OK;
+}
+
+// --------------------------------------------------------------------------- one level
+// ranges: device int2 [n_r]; writes rec [n_r], acc [n_r], and child marks (if child != null).
+fic_status level_enqueue(fic_ctx *ctx, const Pool &P, const uint8_t *img, const int2 *ranges,
+                         int64_t n_r, const double *h_s, int32_t n_s, double rms_tol, int is_min,
+                         fic_record *rec, uint8_t *acc, uint8_t *child, int level_slot) {
+    cudaStream_t st = ctx->stream;
+    fic::SearchParams sp;
+    memset(&sp, 0, sizeof sp);
+    sp.img = img;
+    sp.N = P.N;
+    sp.ranges = ranges;
+    sp.n_r = (int32_t)n_r;
+    sp.Dt = P.Dt; sp.SDf = P.SDf; sp.SD = P.SD; sp.C = P.C;
+    sp.n_k = (int32_t)P.n_k;
+    sp.n_tiles = (int32_t)P.n_tiles;
+    sp.has_zero = 0;
+    sp.j_zero = 0;
+    sp.smax = 0.0;
+    for (int j = 0; j < n_s; ++j) {
+        if (h_s[j] == 0.0) {
+            if (!sp.has_zero) { sp.has_zero = 1; sp.j_zero = j; }
+        } else {
+            sp.spos[sp.nsp] = h_s[j];
+            sp.jpos[sp.nsp] = j;
+            ++sp.nsp;
+        }
+        if (h_s[j] > sp.smax) sp.smax = h_s[j];
+    }
+    sp.cmax = (double)P.cmax;
+    const int64_t slots = P.n_tiles * fic::kTileD;
+    sp.nsplit = fic::search_nsplit_hint(P.B, n_r, P.n_tiles, ctx->num_sms);
+    sp.tiles_per_split = (int32_t)((P.n_tiles + sp.nsplit - 1) / sp.nsplit);
+    sp.nsplit = (int32_t)((P.n_tiles + sp.tiles_per_split - 1) / sp.tiles_per_split);
+    CK(grow(ctx, ctx->b_t2f, sizeof(float) * (size_t)slots * (sp.nsp ? sp.nsp : 1)));
+    CK(grow(ctx, ctx->b_part, sizeof(fic::Partial) * (size_t)n_r * sp.nsplit));
+    sp.t2f = ptr<float>(ctx->b_t2f);
+    sp.part = ptr<fic::Partial>(ctx->b_part);
+    sp.exact_count = ptr<unsigned long long>(ctx->b_counts) + 8 + level_slot;
+    fic::SList sl;
+    memcpy(sl.s, sp.spos, sizeof sl.s);
+    CK(fic::launch_t2f(P.C, (int32_t)P.n_k, slots, sl, sp.nsp, ptr<float>(ctx->b_t2f), st));
+    if (ctx->timing) CK(cudaEventRecord(ctx->ev[level_slot][1], st));
+    if (sp.nsp > 0) CK(fic::launch_search(P.B, sp.nsp, sp, st));
+    if (ctx->timing) CK(cudaEventRecord(ctx->ev[level_slot][2], st));
+    fic::FinalizeParams fp;
+    memset(&fp, 0, sizeof fp);
+    fp.img = img; fp.N = P.N; fp.B = P.B; fp.L = P.L; fp.A = P.A;
+    fp.ranges = ranges;
+    fp.n_r = (int32_t)n_r;
+    fp.nsplit = sp.nsp > 0 ? sp.nsplit : 0;
+    fp.part = sp.part;
+    fp.SD = P.SD; fp.kept = P.kept; fp.n_k = (int32_t)P.n_k;
+    for (int j = 0; j < n_s; ++j) fp.s[j] = h_s[j];
+    fp.n_s = n_s; fp.has_zero = sp.has_zero; fp.j_zero = sp.j_zero;
+    fp.rms_tol = rms_tol; fp.is_min = is_min;
+    fp.rec = rec; fp.accepted = acc; fp.child = child;
+    CK(fic::launch_finalize(fp, st));
+    if (ctx->timing) CK(cudaEventRecord(ctx->ev[level_slot][3], st));
+    return FIC_OK;
+}
+
+fic_status ctx_check(fic_ctx *ctx) {
+    if (!ctx) return FIC_ERR_ARG;
+    ctx->err.clear();
+    CK(cudaSetDevice(ctx->device));
+    return FIC_OK;
+}
+
+}  // namespace
+
+// =============================================================================== C ABI
+extern "C" {
+
+const char *fic_version(void) { return "fic-b200 0.1 (sm_100a; fp32-exact CUDA-core search)"; }
+
+fic_status fic_entropy_lut(int64_t *h_lut, int32_t mmax) {
+    if (!h_lut || mmax < 0 || mmax > (1 << 20)) return FIC_ERR_ARG;
+    make_lut(h_lut, mmax);
+    return FIC_OK;
+}
+
+fic_status fic_ctx_create(int32_t device, void *cuda_stream, fic_ctx **out) {
+    if (!out) return FIC_ERR_ARG;
+    *out = nullptr;
+    fic_ctx *ctx = new (std::nothrow) fic_ctx();
+    if (!ctx) return FIC_ERR_NOMEM;
+    ctx->device = device;
+    ctx->stream = (cudaStream_t)cuda_stream;
+    cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) {
+        delete ctx;
+        return FIC_ERR_CUDA;
+    }
+    cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
+    make_lut(ctx->lut, 4096);
+    std::vector<int64_t> delta(4096);
+    for (int t = 0; t < 4096; ++t) delta[t] = ctx->lut[t + 1] - ctx->lut[t];
+    e = cudaMalloc(&ctx->d_delta, sizeof(int64_t) * 4096);
+    if (e == cudaSuccess)
+        e = cudaMemcpy(ctx->d_delta, delta.data(), sizeof(int64_t) * 4096, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMallocHost(&ctx->h_counts, 64 * sizeof(unsigned long long));
+    if (e == cudaSuccess) e = grow(nullptr, ctx->b_counts, 64 * sizeof(unsigned long long));
+    for (int l = 0; l < fic::kMaxLevels && e == cudaSuccess; ++l)
+        for (int q = 0; q < 5 && e == cudaSuccess; ++q) e = cudaEventCreate(&ctx->ev[l][q]);
+    if (e != cudaSuccess) {
+        fic_ctx_destroy(ctx);
+        return FIC_ERR_CUDA;
+    }
+    *out = ctx;
+    return FIC_OK;
+}
+
+fic_status fic_ctx_set_stream(fic_ctx *ctx, void *cuda_stream) {
+    if (!ctx) return FIC_ERR_ARG;
+    ctx->stream = (cudaStream_t)cuda_stream;
+    return FIC_OK;
+}
+
+fic_status fic_ctx_set_timing(fic_ctx *ctx, int32_t enable) {
+    if (!ctx) return FIC_ERR_ARG;
+    ctx->timing = enable != 0;
+    return FIC_OK;
+}
+
+fic_status fic_ctx_destroy(fic_ctx *ctx) {
+    if (!ctx) return FIC_ERR_ARG;
+    cudaSetDevice(ctx->device);
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    for (auto &P : ctx->levels) free_pool(P);
+    Buf *bufs[] = {&ctx->b_blocksum, &ctx->b_counts, &ctx->b_rng[0], &ctx->b_rng[1], &ctx->b_rec,
+                   &ctx->b_acc, &ctx->b_child, &ctx->b_part, &ctx->b_t2f, &ctx->b_img, &ctx->b_out,
+                   &ctx->b_scounts};
+    for (Buf *b : bufs) free_buf(*b);
+    if (ctx->d_delta) cudaFree(ctx->d_delta);
+    if (ctx->h_counts) cudaFreeHost(ctx->h_counts);
+    for (auto &row : ctx->ev)
+        for (auto &e : row)
+            if (e) cudaEventDestroy(e);
+    delete ctx;
+    return FIC_OK;
+}
+
+const char *fic_last_error(const fic_ctx *ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+fic_status fic_get_stats(const fic_ctx *ctx, fic_level_stats *h_out, int32_t max_levels,
+                         int32_t *h_n_levels) {
+    if (!ctx) return FIC_ERR_ARG;
+    const int32_t n = (int32_t)ctx->stats.size();
+    if (h_n_levels) *h_n_levels = n;
+    for (int32_t i = 0; i < n && i < max_levels && h_out; ++i) h_out[i] = ctx->stats[i];
+    return FIC_OK;
+}
+
+fic_status fic_build_domain_pool(fic_ctx *ctx, const uint8_t *img, int32_t N, int32_t B, int32_t L,
+                                 double tau_nats, fic_pool **out) {
+    CKS(ctx_check(ctx));
+    if (!img || !out) return fail(ctx, FIC_ERR_ARG, "null argument");
+    *out = nullptr;
+    CKS(check_level(ctx, N, B, L));
+    fic_pool *pool = new (std::nothrow) fic_pool();
+    if (!pool) return fail(ctx, FIC_ERR_NOMEM, "host allocation failed");
+    fic_status st = pool_enqueue(ctx, pool->P, img, N, B, L, tau_nats);
+    if (st == FIC_OK) {
+        cudaError_t e = cudaMemcpyAsync(ctx->h_counts, pool->P.d_misc, 2 * sizeof(unsigned long long),
+                                        cudaMemcpyDeviceToHost, ctx->stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+        if (e != cudaSuccess) st = cuda_fail(ctx, e, "pool counts", __LINE__);
+    }
+    if (st != FIC_OK) {
+        free_pool(pool->P);
+        delete pool;
+        return st;
+    }
+    pool_take_counts(pool->P, ctx->h_counts);
+    *out = pool;
+    if (pool->P.n_k == 0) return fail(ctx, FIC_ERR_EMPTY_POOL, "no domain block passed the entropy filter");
+    return FIC_OK;
+}
+
+fic_status fic_pool_info(const fic_pool *pool, int64_t *h_n_candidates, int64_t *h_n_kept,
+                         const uint8_t **keep_mask, const int32_t **kept, const int64_t **keys) {
+    if (!pool) return FIC_ERR_ARG;
+    if (h_n_candidates) *h_n_candidates = pool->P.n_c;
+    if (h_n_kept) *h_n_kept = pool->P.n_k;
+    if (keep_mask) *keep_mask = pool->P.keep;
+    if (kept) *kept = pool->P.kept;
+    if (keys) *keys = pool->P.keys;
+    return FIC_OK;
+}
+
+fic_status fic_pool_destroy(fic_pool *pool) {
+    if (!pool) return FIC_ERR_ARG;
+    cudaSetDevice(pool->P.device);
+    cudaDeviceSynchronize();
+    free_pool(pool->P);
+    delete pool;
+    return FIC_OK;
+}
+
+fic_status fic_encode_level(fic_ctx *ctx, const uint8_t *img, int32_t N, const fic_pool *pool,
+                            const int32_t *ranges, int64_t n_r, const double *h_s, int32_t n_s,
+                            double rms_tol, int32_t is_min_level, fic_record *out) {
+    CKS(ctx_check(ctx));
+    if (!img || !pool || (!ranges && n_r) || (!out && n_r) || n_r < 0)
+        return fail(ctx, FIC_ERR_ARG, "null argument");
+    if (pool->P.N != N) return fail(ctx, FIC_ERR_SHAPE, "pool was built for another N");
+    if (n_r > (int64_t)1 << 30) return fail(ctx, FIC_ERR_ARG, "too many ranges");
+    CKS(check_s(ctx, h_s, n_s));
+    if (pool->P.n_k < 1) return fail(ctx, FIC_ERR_EMPTY_POOL, "empty domain pool");
+    if (reinterpret_cast<uintptr_t>(ranges) & 7) return fail(ctx, FIC_ERR_ARG, "ranges must be 8-byte aligned");
+    CK(grow(ctx, ctx->b_acc, n_r + 16));
+    ctx->stats.clear();
+    fic_level_stats ls;
+    memset(&ls, 0, sizeof ls);
+    CK(cudaMemsetAsync(ptr<unsigned long long>(ctx->b_counts) + 8, 0, sizeof(unsigned long long),
+                       ctx->stream));
+    if (ctx->timing) CK(cudaEventRecord(ctx->ev[0][0], ctx->stream));
+    CKS(level_enqueue(ctx, pool->P, img, reinterpret_cast<const int2 *>(ranges), n_r, h_s, n_s,
+                      rms_tol, is_min_level, out, ptr<uint8_t>(ctx->b_acc), nullptr, 0));
+    ls.B = pool->P.B; ls.n_candidates = pool->P.n_c; ls.n_kept = pool->P.n_k; ls.n_ranges = n_r;
+    ls.pairs = n_r * pool->P.n_k * 8;
+    ctx->stats.push_back(ls);
+    return FIC_OK;
+}
+
+fic_status fic_encode(fic_ctx *ctx, const uint8_t *img, int32_t N, int32_t B_max, int32_t B_min,
+                      int32_t L, const double *h_tau, const double *h_s, const int32_t *h_n_s,
+                      const double *h_rms_tol, int32_t shard, int32_t n_shards, fic_record *out,
+                      int64_t capacity, int64_t *h_n_out) {
+    CKS(ctx_check(ctx));
+    if (h_n_out) *h_n_out = 0;
+    if (!img || !h_tau || !h_s || !h_n_s || !h_rms_tol || !h_n_out || (!out && capacity > 0) ||
+        capacity < 0)
+        return fail(ctx, FIC_ERR_ARG, "null argument");
+    if (!pow2(B_max) || !pow2(B_min) || B_min < 2 || B_min > B_max)
+        return fail(ctx, FIC_ERR_ARG, "B_max, B_min must be powers of two with 2 <= B_min <= B_max");
+    if (n_shards < 1 || shard < 0 || shard >= n_shards) return fail(ctx, FIC_ERR_ARG, "bad shard");
+    if (N < 1 || N % B_max) return fail(ctx, FIC_ERR_SHAPE, "N must be a multiple of B_max");
+    int nl = 0;
+    for (int32_t B = B_max; B >= B_min; B /= 2) ++nl;
+    if (nl > fic::kMaxLevels) return fail(ctx, FIC_ERR_ARG, "too many levels");
+    std::vector<int64_t> s_off(nl + 1, 0);
+    for (int l = 0; l < nl; ++l) {
+        CKS(check_level(ctx, N, B_max >> l, L));
+        CKS(check_s(ctx, h_s + s_off[l], h_n_s[l]));
+        s_off[l + 1] = s_off[l] + h_n_s[l];
+    }
+    cudaStream_t st = ctx->stream;
+    ctx->stats.assign(nl, fic_level_stats{});
+    unsigned long long *d_counts = ptr<unsigned long long>(ctx->b_counts);
+    CK(cudaMemsetAsync(d_counts, 0, 64 * sizeof(unsigned long long), st));
+
+    // 1. every level's pool (independent of the quadtree), all enqueued back to back
+    for (int l = 0; l < nl; ++l) {
+        if (ctx->timing) CK(cudaEventRecord(ctx->ev[l][0], st));
+        CKS(pool_enqueue(ctx, ctx->levels[l], img, N, B_max >> l, L, h_tau[l]));
+        if (ctx->timing) CK(cudaEventRecord(ctx->ev[l][4], st));
+        CK(cudaMemcpyAsync(ctx->h_counts + 2 * l, ctx->levels[l].d_misc, 2 * sizeof(unsigned long long),
+                           cudaMemcpyDeviceToHost, st));
+    }
+    // 2. top-level ranges of this shard (row-major)
+    const int64_t G = N / B_max;
+    const int64_t Gmin = N / B_min;
+    CK(grow(ctx, ctx->b_child, (size_t)(Gmin * Gmin) + 16));
+    CK(grow(ctx, ctx->b_rng[0], sizeof(int2) * (size_t)(Gmin * Gmin)));
+    CK(grow(ctx, ctx->b_rng[1], sizeof(int2) * (size_t)(Gmin * Gmin)));
+    CK(grow(ctx, ctx->b_rec, sizeof(fic_record) * (size_t)(Gmin * Gmin)));
+    CK(grow(ctx, ctx->b_acc, (size_t)(Gmin * Gmin) + 16));
+    CK(grow(ctx, ctx->b_blocksum, sizeof(int64_t) * fic::select_blocksum_len(Gmin * Gmin)));
+    uint8_t *child = ptr<uint8_t>(ctx->b_child);
+    CK(fic::launch_top_flags(child, G, shard, n_shards, st));
+    CK(fic::launch_select_grid(child, G, B_max, ptr<int64_t>(ctx->b_blocksum), ptr<int2>(ctx->b_rng[0]),
+                               d_counts + 2, st));
+    int64_t n_r = G * G > shard ? (G * G - shard + n_shards - 1) / n_shards : 0;
+    CK(cudaStreamSynchronize(st));
+    for (int l = 0; l < nl; ++l) pool_take_counts(ctx->levels[l], ctx->h_counts + 2 * l);
+
+    // 3. the quadtree, one level at a time
+    int64_t total = 0;
+    int cur = 0;
+    for (int l = 0; l < nl && n_r > 0; ++l) {
+        const int32_t B = B_max >> l;
+        const Pool &P = ctx->levels[l];
+        if (P.n_k < 1) return fail(ctx, FIC_ERR_EMPTY_POOL, "empty domain pool at B=" + std::to_string(B));
+        const bool last = (l == nl - 1);
+        const int64_t Gc = N / (B / 2 > 0 ? B / 2 : 1);
+        if (!last) CK(cudaMemsetAsync(child, 0, (size_t)(Gc * Gc), st));
+        CKS(level_enqueue(ctx, P, img, ptr<int2>(ctx->b_rng[cur]), n_r, h_s + s_off[l], h_n_s[l],
+                          h_rms_tol[l], last, ptr<fic_record>(ctx->b_rec), ptr<uint8_t>(ctx->b_acc),
+                          last ? nullptr : child, l));
+        CK(fic::launch_select_records(ptr<uint8_t>(ctx->b_acc), n_r, ptr<int64_t>(ctx->b_blocksum),
+                                      ptr<fic_record>(ctx->b_rec), out, total, capacity, d_counts + 0,
+                                      st));
+        if (!last)
+            CK(fic::launch_select_grid(child, Gc, B / 2, ptr<int64_t>(ctx->b_blocksum),
+                                       ptr<int2>(ctx->b_rng[cur ^ 1]), d_counts + 1, st));
+        CK(cudaMemcpyAsync(ctx->h_counts + 32, d_counts, 2 * sizeof(unsigned long long),
+                           cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(ctx->h_counts + 40 + l, d_counts + 8 + l, sizeof(unsigned long long),
+                           cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        const int64_t n_acc = (int64_t)ctx->h_counts[32];
+        const int64_t n_next = last ? 0 : (int64_t)ctx->h_counts[33];
+        fic_level_stats &ls = ctx->stats[l];
+        ls.B = B; ls.n_candidates = P.n_c; ls.n_kept = P.n_k; ls.n_ranges = n_r;
+        ls.n_accepted = n_acc; ls.pairs = n_r * P.n_k * 8;
+        ls.exact_evals = (int64_t)ctx->h_counts[40 + l];
+        total += n_acc;
+        n_r = n_next;
+        cur ^= 1;
+    }
+    if (ctx->timing) {
+        for (int l = 0; l < nl; ++l) {
+            fic_level_stats &ls = ctx->stats[l];
+            if (ls.n_ranges == 0) continue;
+            float a = 0, b = 0, c = 0;
+            cudaEventElapsedTime(&a, ctx->ev[l][0], ctx->ev[l][4]);
+            cudaEventElapsedTime(&b, ctx->ev[l][1], ctx->ev[l][2]);
+            cudaEventElapsedTime(&c, ctx->ev[l][2], ctx->ev[l][3]);
+            ls.ms_pool = a; ls.ms_search = b; ls.ms_finalize = c;
+        }
+    }
+    *h_n_out = total;
+    if (total > capacity) return fail(ctx, FIC_ERR_CAPACITY, "output capacity too small");
+    return FIC_OK;
+}
+
+fic_status fic_encode_host(fic_ctx *ctx, const uint8_t *h_img, int32_t N, int32_t B_max,
+                           int32_t B_min, int32_t L, const double *h_tau, const double *h_s,
+                           const int32_t *h_n_s, const double *h_rms_tol, int32_t shard,
+                           int32_t n_shards, fic_record *h_out, int64_t capacity, int64_t *h_n_out) {
+    CKS(ctx_check(ctx));
+    if (!h_img || !h_n_out || (!h_out && capacity > 0) || N < 1) return fail(ctx, FIC_ERR_ARG, "null argument");
+    CK(grow(ctx, ctx->b_img, (size_t)N * N));
+    CK(grow(ctx, ctx->b_out, sizeof(fic_record) * (size_t)(capacity > 0 ? capacity : 1)));
+    CK(cudaMemcpyAsync(ctx->b_img.p, h_img, (size_t)N * N, cudaMemcpyHostToDevice, ctx->stream));
+    fic_status st = fic_encode(ctx, ptr<uint8_t>(ctx->b_img), N, B_max, B_min, L, h_tau, h_s, h_n_s,
+                               h_rms_tol, shard, n_shards, ptr<fic_record>(ctx->b_out), capacity,
+                               h_n_out);
+    if (st != FIC_OK && st != FIC_ERR_CAPACITY) return st;
+    const int64_t n = *h_n_out < capacity ? *h_n_out : capacity;
+    if (n > 0)
+        CK(cudaMemcpyAsync(h_out, ctx->b_out.p, sizeof(fic_record) * (size_t)n, cudaMemcpyDeviceToHost,
+                           ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return st;
+}
+
+fic_status fic_merge_shards(fic_ctx *ctx, const fic_record *in, const int64_t *h_counts,
+                            int32_t n_shards, int64_t stride, fic_record *out) {
+    CKS(ctx_check(ctx));
+    if (!in || !h_counts || !out || n_shards < 1) return fail(ctx, FIC_ERR_ARG, "null argument");
+    int64_t mx = 0;
+    for (int i = 0; i < n_shards; ++i) {
+        if (h_counts[i] < 0 || h_counts[i] > stride) return fail(ctx, FIC_ERR_ARG, "bad shard count");
+        if (h_counts[i] > mx) mx = h_counts[i];
+    }
+    CK(grow(ctx, ctx->b_scounts, sizeof(int64_t) * n_shards));
+    CK(cudaMemcpyAsync(ctx->b_scounts.p, h_counts, sizeof(int64_t) * n_shards, cudaMemcpyHostToDevice,
+                       ctx->stream));
+    CK(fic::launch_merge_shards(in, ptr<int64_t>(ctx->b_scounts), n_shards, stride, mx, out, ctx->stream));
+    return FIC_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,123 @@
+// fic_internal.cuh -- internal declarations of libfic (B200 / sm_100a).  Not part of the ABI.
+//
+// Layout of one level's pool in HBM (DESIGN.md §"Data layout"):
+//   Dt  float [n_tiles][n][128]   decimated domain D' (2x2 sums, exact integers <= 1020), one
+//                                 128-domain tile is one contiguous n*512-byte slab so a stage of
+//                                 the search kernel is a single cp.async.bulk copy
+//   SDf float [n_tiles*128], SD int32, C int64   domain moments (C = n*SDD - SD^2)
+// Pad domains (index >= n_kept) carry t2f = +inf, so the search filter never admits them.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "fic.h"
+
+namespace fic {
+
+constexpr int kTileD = 128;  // domains per pool tile
+constexpr int kMaxS = 16;    // s values per level
+constexpr int kMaxLevels = 8;
+
+struct Buf {
+    void *p = nullptr;
+    size_t cap = 0;
+};
+
+// One level's entropy-filtered domain pool (fic_pool).
+struct Pool {
+    int32_t N = 0, B = 0, L = 0, n = 0, A = 0;
+    int64_t n_c = 0, n_k = 0, n_tiles = 0;
+    int64_t cmax = 0;  // max C over kept domains (host copy, for the filter margin)
+    int64_t *keys = nullptr;
+    uint8_t *keep = nullptr;
+    int32_t *kept = nullptr;
+    float *Dt = nullptr, *SDf = nullptr;
+    int32_t *SD = nullptr;
+    int64_t *C = nullptr;
+    unsigned long long *d_misc = nullptr;  // [0] = n_kept, [1] = Cmax
+    Buf b_keys, b_keep, b_kept, b_Dt, b_SDf, b_SD, b_C, b_misc;
+    int device = 0;
+};
+
+// Best candidate of one range over a subset of domains (lexicographic (e; dom, iso, s_idx)).
+struct Partial {
+    double e;
+    int32_t d;
+    int32_t kj;  // iso | (s_idx << 8)
+};
+
+struct SearchParams {
+    const uint8_t *img;
+    int32_t N;
+    const int2 *ranges;
+    int32_t n_r;
+    const float *Dt;
+    const float *SDf;
+    const int32_t *SD;
+    const int64_t *C;
+    const float *t2f;  // [nsp][n_tiles*128]
+    int32_t n_k, n_tiles, tiles_per_split, nsplit;
+    int32_t nsp;                 // number of s values > 0
+    double spos[kMaxS];          // those s values
+    int32_t jpos[kMaxS];         // their indices in the level's s list
+    int32_t has_zero, j_zero;    // s = 0 present, and its first index
+    double smax;                 // max s
+    double cmax;                 // max C of the pool (margin bound)
+    Partial *part;               // [n_r][nsplit]
+    unsigned long long *exact_count;
+};
+
+struct FinalizeParams {
+    const uint8_t *img;
+    int32_t N, B, L, A;
+    const int2 *ranges;
+    int32_t n_r, nsplit;
+    const Partial *part;
+    const int32_t *SD;
+    const int32_t *kept;
+    int32_t n_k;
+    double s[kMaxS];
+    int32_t n_s, has_zero, j_zero;
+    double rms_tol;
+    int32_t is_min;
+    fic_record *rec;
+    uint8_t *accepted;
+    uint8_t *child;  // child bitmap [(N/(B/2))^2] or null
+};
+
+// ---- launchers (return cudaError_t of the launch) ---------------------------------------------
+cudaError_t launch_entropy_keys(const uint8_t *img, int32_t N, int32_t B, int32_t L, int32_t A,
+                                const int64_t *d_delta, int64_t lut_m, int64_t T, int use_tau,
+                                int64_t *keys, uint8_t *keep, cudaStream_t st);
+// order-preserving compaction of u8 flags: writes indices and *d_total
+cudaError_t launch_select_index(const uint8_t *flags, int64_t n, int64_t *blocksum, int32_t *out,
+                                unsigned long long *d_total, cudaStream_t st);
+cudaError_t launch_select_grid(const uint8_t *flags, int64_t G, int32_t B, int64_t *blocksum,
+                               int2 *out, unsigned long long *d_total, cudaStream_t st);
+cudaError_t launch_select_records(const uint8_t *flags, int64_t n, int64_t *blocksum,
+                                  const fic_record *in, fic_record *out, int64_t out_base,
+                                  int64_t capacity, unsigned long long *d_total, cudaStream_t st);
+size_t select_blocksum_len(int64_t n);
+cudaError_t launch_top_flags(uint8_t *flags, int64_t G, int32_t shard, int32_t n_shards,
+                             cudaStream_t st);
+cudaError_t launch_pool_gather(const uint8_t *img, int32_t N, int32_t B, int32_t L, int32_t A,
+                               const int32_t *kept, const unsigned long long *d_nk,
+                               int64_t n_tiles_max, float *Dt, cudaStream_t st);
+cudaError_t launch_pool_moments(const uint8_t *img, int32_t N, int32_t B, int32_t L, int32_t A,
+                                const int32_t *kept, const unsigned long long *d_nk,
+                                int64_t n_slots, int32_t *SD, float *SDf, int64_t *C,
+                                unsigned long long *d_cmax, cudaStream_t st);
+struct SList {
+    double s[kMaxS];
+};
+cudaError_t launch_t2f(const int64_t *C, int32_t n_k, int64_t n_slots, const SList &spos,
+                       int32_t nsp, float *t2f, cudaStream_t st);
+cudaError_t launch_search(int32_t B, int32_t nsp, const SearchParams &p, cudaStream_t st);
+cudaError_t launch_finalize(const FinalizeParams &p, cudaStream_t st);
+cudaError_t launch_merge_shards(const fic_record *in, const int64_t *d_counts, int32_t n_shards,
+                                int64_t stride, int64_t max_count, fic_record *out, cudaStream_t st);
+int search_nsplit_hint(int32_t B, int64_t n_r, int64_t n_tiles, int num_sms);
+
+}  // namespace fic

@@ -1,0 +1,381 @@
+// fic_pool.cu -- domain-pool construction kernels and the
+// order-preserving compactions used by the pool (kept list) and the quadtree (a8).
+//
+//   entropy_keys_kernel  P:44-56 Eq. (4)-(5) + Abstract P:14: entropy of each raw 2B x 2B candidate
+//                        as the exact fixed-point key  K = LUT[m] - sum_v LUT[h_v]  [R6]
+//   select_*             row-major compaction (kept list, next-level ranges, accepted records)
+//   pool_gather_kernel   P:30 "decimated domain block": D'(i,j) = 2x2 sum  [R1]
+//   pool_moments_kernel  SD = sum D', SDD = sum D'^2, C = n SDD - SD^2 (int64, exact)
+#include <cfloat>
+#include <cstdio>
+
+#include "fic_internal.cuh"
+
+namespace fic {
+
+// ------------------------------------------------------------------------------------ entropy
+
+// One warp per candidate (grid-stride).  Each warp owns a 256-bin histogram in shared memory.
+// The key is accumulated while the histogram is built: inserting a pixel into a bin holding
+// `old` pixels adds delta[old] = LUT[old+1] - LUT[old], so after all m insertions the sum is
+// sum_v LUT[h_v] exactly, whatever the insertion order (integer telescoping).
+__global__ void __launch_bounds__(256) entropy_keys_kernel(
+    const uint8_t *__restrict__ img, int32_t N, int32_t side, int32_t L, int32_t A,
+    const int64_t *__restrict__ g_delta, int64_t lut_m, int64_t T, int use_tau,
+    int64_t *__restrict__ keys, uint8_t *__restrict__ keep) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    const int m = side * side;
+    int64_t *delta = reinterpret_cast<int64_t *>(sm);
+    int32_t *hist_all = reinterpret_cast<int32_t *>(sm + sizeof(int64_t) * m);
+    for (int i = threadIdx.x; i < m; i += blockDim.x) delta[i] = g_delta[i];
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    int32_t *hist = hist_all + warp * 256;
+    const int64_t n_c = (int64_t)A * A;
+    const int64_t wstride = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t c = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp; c < n_c; c += wstride) {
+        for (int v = lane; v < 256; v += 32) hist[v] = 0;
+        __syncwarp();
+        const int64_t x = (c % A) * L, y = (c / A) * L;
+        int64_t acc = 0;
+        for (int idx = lane; idx < m; idx += 32) {
+            const int i = idx / side, j = idx - (idx / side) * side;
+            const int v = img[(y + i) * (int64_t)N + x + j];
+            const int old = atomicAdd(&hist[v], 1);
+            acc += delta[old];
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) {
+            const int64_t key = lut_m - acc;
+            keys[c] = key;
+            keep[c] = (uint8_t)(!use_tau || key > T);
+        }
+        __syncwarp();
+    }
+}
+
+cudaError_t launch_entropy_keys(const uint8_t *img, int32_t N, int32_t B, int32_t L, int32_t A,
+                                const int64_t *d_delta, int64_t lut_m, int64_t T, int use_tau,
+                                int64_t *keys, uint8_t *keep, cudaStream_t st) {
+    const int side = 2 * B, m = side * side;
+    const size_t smem = sizeof(int64_t) * m + 8 * 256 * sizeof(int32_t);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(entropy_keys_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             64 * 1024);
+        attr = true;
+    }
+    const int64_t n_c = (int64_t)A * A;
+    int64_t blocks = (n_c + 7) / 8;
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    if (blocks < 1) blocks = 1;
+    entropy_keys_kernel<<<(unsigned)blocks, 256, smem, st>>>(img, N, side, L, A, d_delta, lut_m, T,
+                                                             use_tau, keys, keep);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------- order-preserving select
+// Three passes: per-block counts -> single-block exclusive scan -> per-block scatter.
+constexpr int kSelThreads = 256, kSelItems = 16, kSelBlock = kSelThreads * kSelItems;
+
+size_t select_blocksum_len(int64_t n) { return (size_t)((n + kSelBlock - 1) / kSelBlock) + 1; }
+
+__device__ __forceinline__ int thread_flag_count(const uint8_t *flags, int64_t n, int64_t base) {
+    int cnt = 0;
+    if (base + kSelItems <= n && ((reinterpret_cast<uintptr_t>(flags + base) & 15) == 0)) {
+        const uint4 v = *reinterpret_cast<const uint4 *>(flags + base);
+        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) cnt += __popc(w[q] & 0x01010101u);  // flags are 0/1 bytes
+    } else {
+        for (int q = 0; q < kSelItems; ++q)
+            if (base + q < n) cnt += flags[base + q] & 1;
+    }
+    return cnt;
+}
+
+__global__ void __launch_bounds__(kSelThreads) select_count_kernel(const uint8_t *__restrict__ flags,
+                                                                   int64_t n, int64_t *blocksum) {
+    __shared__ int wsum[kSelThreads / 32];
+    const int64_t base = (int64_t)blockIdx.x * kSelBlock + (int64_t)threadIdx.x * kSelItems;
+    int cnt = base < n ? thread_flag_count(flags, n, base) : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = cnt;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int t = 0;
+        for (int w = 0; w < kSelThreads / 32; ++w) t += wsum[w];
+        blocksum[blockIdx.x] = t;
+    }
+}
+
+// exclusive scan of blocksum[0..nb) in place, total -> *d_total (single block of 1024 threads)
+__global__ void __launch_bounds__(1024) select_scan_kernel(int64_t *blocksum, int64_t nb,
+                                                           unsigned long long *d_total) {
+    __shared__ int64_t part[1024];
+    const int t = threadIdx.x;
+    const int64_t per = (nb + 1023) / 1024;
+    const int64_t b0 = t * per, b1 = min(nb, b0 + per);
+    int64_t s = 0;
+    for (int64_t b = b0; b < b1; ++b) s += blocksum[b];
+    part[t] = s;
+    __syncthreads();
+    for (int o = 1; o < 1024; o <<= 1) {
+        int64_t v = t >= o ? part[t - o] : 0;
+        __syncthreads();
+        part[t] += v;
+        __syncthreads();
+    }
+    int64_t run = t ? part[t - 1] : 0;
+    for (int64_t b = b0; b < b1; ++b) {
+        const int64_t v = blocksum[b];
+        blocksum[b] = run;
+        run += v;
+    }
+    if (t == 1023) *d_total = (unsigned long long)part[1023];
+}
+
+template <class Emit>
+__global__ void __launch_bounds__(kSelThreads) select_scatter_kernel(const uint8_t *__restrict__ flags,
+                                                                     int64_t n,
+                                                                     const int64_t *__restrict__ blockoff,
+                                                                     Emit emit) {
+    __shared__ int wsum[kSelThreads / 32];
+    const int64_t base = (int64_t)blockIdx.x * kSelBlock + (int64_t)threadIdx.x * kSelItems;
+    uint8_t f[kSelItems];
+#pragma unroll
+    for (int q = 0; q < kSelItems; ++q) f[q] = (base + q < n) ? (flags[base + q] & 1) : 0;
+    int cnt = 0;
+#pragma unroll
+    for (int q = 0; q < kSelItems; ++q) cnt += f[q];
+    // block exclusive scan of cnt
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+    }
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    int woff = 0;
+    for (int w = 0; w < warp; ++w) woff += wsum[w];
+    int64_t pos = blockoff[blockIdx.x] + woff + incl - cnt;
+#pragma unroll
+    for (int q = 0; q < kSelItems; ++q)
+        if (f[q]) emit(base + q, pos++);
+}
+
+struct EmitIndex {
+    int32_t *out;
+    __device__ void operator()(int64_t i, int64_t pos) const { out[pos] = (int32_t)i; }
+};
+struct EmitGrid {
+    int2 *out;
+    int64_t G;
+    int32_t B;
+    __device__ void operator()(int64_t i, int64_t pos) const {
+        out[pos] = make_int2((int)(i % G) * B, (int)(i / G) * B);
+    }
+};
+struct EmitRecord {
+    const fic_record *in;
+    fic_record *out;
+    int64_t base, cap;
+    __device__ void operator()(int64_t i, int64_t pos) const {
+        if (base + pos < cap) out[base + pos] = in[i];
+    }
+};
+
+template <class Emit>
+static cudaError_t select_run(const uint8_t *flags, int64_t n, int64_t *blocksum, Emit emit,
+                              unsigned long long *d_total, cudaStream_t st) {
+    const int64_t nb = (n + kSelBlock - 1) / kSelBlock;
+    if (nb == 0) return cudaMemsetAsync(d_total, 0, sizeof(unsigned long long), st);
+    select_count_kernel<<<(unsigned)nb, kSelThreads, 0, st>>>(flags, n, blocksum);
+    select_scan_kernel<<<1, 1024, 0, st>>>(blocksum, nb, d_total);
+    select_scatter_kernel<<<(unsigned)nb, kSelThreads, 0, st>>>(flags, n, blocksum, emit);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_select_index(const uint8_t *flags, int64_t n, int64_t *blocksum, int32_t *out,
+                                unsigned long long *d_total, cudaStream_t st) {
+    return select_run(flags, n, blocksum, EmitIndex{out}, d_total, st);
+}
+cudaError_t launch_select_grid(const uint8_t *flags, int64_t G, int32_t B, int64_t *blocksum,
+                               int2 *out, unsigned long long *d_total, cudaStream_t st) {
+    return select_run(flags, G * G, blocksum, EmitGrid{out, G, B}, d_total, st);
+}
+cudaError_t launch_select_records(const uint8_t *flags, int64_t n, int64_t *blocksum,
+                                  const fic_record *in, fic_record *out, int64_t out_base,
+                                  int64_t capacity, unsigned long long *d_total, cudaStream_t st) {
+    return select_run(flags, n, blocksum, EmitRecord{in, out, out_base, capacity}, d_total, st);
+}
+
+__global__ void top_flags_kernel(uint8_t *flags, int64_t n, int32_t shard, int32_t n_shards) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) flags[i] = (uint8_t)((i % n_shards) == shard);
+}
+
+cudaError_t launch_top_flags(uint8_t *flags, int64_t G, int32_t shard, int32_t n_shards,
+                             cudaStream_t st) {
+    const int64_t n = G * G;
+    top_flags_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(flags, n, shard, n_shards);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------ pool gather
+
+// Thread per (tile, p, lane128): Dt[tile][p][dl] = D'_{tile*128+dl}(p).  Consecutive threads
+// write consecutive domains of the same pixel p (coalesced 512-byte rows of the tile slab).
+__global__ void __launch_bounds__(256) pool_gather_kernel(const uint8_t *__restrict__ img, int32_t N,
+                                                          int32_t B, int32_t L, int32_t A,
+                                                          const int32_t *__restrict__ kept,
+                                                          const unsigned long long *__restrict__ d_nk,
+                                                          int64_t total, float *__restrict__ Dt) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= total) return;
+    const int n = B * B;
+    const int64_t n_k = (int64_t)*d_nk;
+    const int64_t tile = e / ((int64_t)n * kTileD);
+    const int64_t ntiles = (n_k + kTileD - 1) / kTileD;
+    if (tile >= ntiles) return;
+    const int rem = (int)(e - tile * (int64_t)n * kTileD);
+    const int p = rem / kTileD, dl = rem - p * kTileD;
+    const int64_t d = tile * kTileD + dl;
+    float v = 0.f;
+    if (d < n_k) {
+        const int32_t c = kept[d];
+        const int64_t x = (int64_t)(c % A) * L, y = (int64_t)(c / A) * L;
+        const int i = p / B, j = p - (p / B) * B;
+        const uint8_t *q = img + (y + 2 * i) * N + x + 2 * j;
+        v = (float)((int)q[0] + (int)q[1] + (int)q[N] + (int)q[N + 1]);
+    }
+    Dt[e] = v;
+}
+
+cudaError_t launch_pool_gather(const uint8_t *img, int32_t N, int32_t B, int32_t L, int32_t A,
+                               const int32_t *kept, const unsigned long long *d_nk,
+                               int64_t n_tiles_max, float *Dt, cudaStream_t st) {
+    const int64_t total = n_tiles_max * (int64_t)B * B * kTileD;
+    if (total == 0) return cudaSuccess;
+    pool_gather_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(img, N, B, L, A, kept,
+                                                                        d_nk, total, Dt);
+    return cudaGetLastError();
+}
+
+// Warp per domain slot: SD, SDD (int), C = n SDD - SD^2 (int64); pads get zeros.
+__global__ void __launch_bounds__(256) pool_moments_kernel(const uint8_t *__restrict__ img, int32_t N,
+                                                           int32_t B, int32_t L, int32_t A,
+                                                           const int32_t *__restrict__ kept,
+                                                           const unsigned long long *__restrict__ d_nk,
+                                                           int64_t n_slots, int32_t *__restrict__ SD,
+                                                           float *__restrict__ SDf,
+                                                           int64_t *__restrict__ C,
+                                                           unsigned long long *d_cmax) {
+    const int64_t d = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (d >= n_slots) return;
+    const int64_t n_k = (int64_t)*d_nk;
+    const int64_t ntiles = (n_k + kTileD - 1) / kTileD;
+    if (d >= ntiles * kTileD) return;
+    const int n = B * B;
+    int64_t sd = 0, sdd = 0;
+    if (d < n_k) {
+        const int32_t c = kept[d];
+        const int64_t x = (int64_t)(c % A) * L, y = (int64_t)(c / A) * L;
+        for (int p = lane; p < n; p += 32) {
+            const int i = p / B, j = p - (p / B) * B;
+            const uint8_t *q = img + (y + 2 * i) * N + x + 2 * j;
+            const int v = (int)q[0] + (int)q[1] + (int)q[N] + (int)q[N + 1];
+            sd += v;
+            sdd += (int64_t)v * v;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        sd += __shfl_xor_sync(0xffffffffu, sd, o);
+        sdd += __shfl_xor_sync(0xffffffffu, sdd, o);
+    }
+    if (lane == 0) {
+        const int64_t cc = (int64_t)n * sdd - sd * sd;
+        SD[d] = (int32_t)sd;
+        SDf[d] = (float)sd;
+        C[d] = cc;
+        if (d < n_k) atomicMax(d_cmax, (unsigned long long)cc);
+    }
+}
+
+cudaError_t launch_pool_moments(const uint8_t *img, int32_t N, int32_t B, int32_t L, int32_t A,
+                                const int32_t *kept, const unsigned long long *d_nk,
+                                int64_t n_slots, int32_t *SD, float *SDf, int64_t *C,
+                                unsigned long long *d_cmax, cudaStream_t st) {
+    if (n_slots == 0) return cudaSuccess;
+    const int64_t threads = n_slots * 32;
+    pool_moments_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(
+        img, N, B, L, A, kept, d_nk, n_slots, SD, SDf, C, d_cmax);
+    return cudaGetLastError();
+}
+
+// t2f[j][d] = fp32 of (s_j s_j)(C/16) for s_j > 0; +inf for pad slots (never admitted).
+__global__ void t2f_kernel(const int64_t *__restrict__ C, int32_t n_k, int64_t n_slots,
+                           const SList spos, int32_t nsp, float *__restrict__ t2f) {
+    const int64_t d = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (d >= n_slots) return;
+    const double c16 = __dmul_rn(0.0625, (double)C[d]);
+    for (int j = 0; j < nsp; ++j) {
+        const double s = spos.s[j];
+        t2f[j * n_slots + d] = d < n_k ? __double2float_rn(__dmul_rn(__dmul_rn(s, s), c16)) : INFINITY;
+    }
+}
+
+cudaError_t launch_t2f(const int64_t *C, int32_t n_k, int64_t n_slots, const SList &spos,
+                       int32_t nsp, float *t2f, cudaStream_t st) {
+    if (n_slots == 0 || nsp == 0) return cudaSuccess;
+    t2f_kernel<<<(unsigned)((n_slots + 255) / 256), 256, 0, st>>>(C, n_k, n_slots, spos, nsp, t2f);
+    return cudaGetLastError();
+}
+
+// ----------------------------------------------------------------------------- shard merge
+// Records of every shard are sorted by key (B desc, ry, rx) and the shards' range sets are
+// disjoint, so a record's output slot is its index in its own list plus, for every other shard,
+// the number of that shard's records with a smaller key (binary search).
+__device__ __forceinline__ uint64_t rec_key(const fic_record &r) {
+    const int lg = 31 - __clz(r.B);
+    return ((uint64_t)(8 - lg) << 48) | ((uint64_t)(uint32_t)r.ry << 24) | (uint64_t)(uint32_t)r.rx;
+}
+
+__global__ void merge_shards_kernel(const fic_record *__restrict__ in,
+                                    const int64_t *__restrict__ counts, int32_t n_shards,
+                                    int64_t stride, fic_record *__restrict__ out) {
+    const int32_t sh = blockIdx.y;
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= counts[sh]) return;
+    const fic_record r = in[sh * stride + i];
+    const uint64_t k = rec_key(r);
+    int64_t pos = i;
+    for (int32_t o = 0; o < n_shards; ++o) {
+        if (o == sh) continue;
+        int64_t lo = 0, hi = counts[o];
+        const fic_record *L = in + o * stride;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (rec_key(L[mid]) < k) lo = mid + 1; else hi = mid;
+        }
+        pos += lo;
+    }
+    out[pos] = r;
+}
+
+cudaError_t launch_merge_shards(const fic_record *in, const int64_t *d_counts, int32_t n_shards,
+                                int64_t stride, int64_t max_count, fic_record *out,
+                                cudaStream_t st) {
+    if (max_count == 0) return cudaSuccess;
+    dim3 grid((unsigned)((max_count + 255) / 256), (unsigned)n_shards);
+    merge_shards_kernel<<<grid, 256, 0, st>>>(in, d_counts, n_shards, stride, out);
+    return cudaGetLastError();
+}
+
+}  // namespace fic

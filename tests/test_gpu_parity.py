@@ -1,0 +1,288 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element by element.
+
+Bar (DESIGN.md §"Parity"): keep masks, entropy keys, kept lists, and every record field
+(rx, ry, B, dom, dx, dy, iso, s_idx, o_code, accepted) bit-exact; err identical (both sides
+evaluate the same binary64 expression; BASELINE.json allows 1e-12 relative, we require equality).
+Full-size configs (C3, C4, C5) run the GPU in the launch configuration bench.py times and are
+checked on seeded samples the oracle computes one by one, plus whole-output properties.
+"""
+import numpy as np
+import pytest
+
+import oracle
+from fic_inputs import (config, image_for, make_image, random_image, ramp_image, constant_image,
+                        sample_indices, PREDEFINED_S, GRID_S)
+
+pytestmark = pytest.mark.gpu
+
+FIELDS = ("rx", "ry", "B", "dom", "dx", "dy", "iso", "s_idx", "o_code", "accepted", "err")
+
+
+@pytest.fixture(scope="module")
+def fic():
+    import torch
+    from paper_1501_04140_b200 import build as b
+    b.build()
+    import paper_1501_04140_b200 as p
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    ctx = p.Context(0, timing=True)
+    yield p, ctx, torch
+    ctx.close()
+
+
+def dev(torch, a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def assert_same(gpu, orc, what=""):
+    assert len(gpu) == len(orc), f"{what}: {len(gpu)} vs {len(orc)} records"
+    for f in FIELDS:
+        g, o = gpu[f], orc[f]
+        if not np.array_equal(g, o):
+            bad = np.nonzero(g != o)[0][:5]
+            raise AssertionError(f"{what}: field {f} differs at {bad}: gpu {g[bad]} oracle {o[bad]}"
+                                 f"\n gpu rec {gpu[bad[0]]}\n orc rec {orc[bad[0]]}")
+
+
+# ------------------------------------------------------------------------------- pools
+@pytest.mark.parametrize("N,B,L,tau", [
+    (64, 4, 2, -1.0), (64, 2, 1, 2.0), (40, 8, 3, 3.0), (256, 16, 4, 5.10914), (256, 2, 4, 2.6),
+    (96, 16, 1, 4.9), (512, 8, 2, 4.753761), (33, 4, 5, -1.0)])
+def test_pool_parity(fic, N, B, L, tau):
+    p, ctx, torch = fic
+    img = make_image(N, N + B, texture=(N == 512))
+    pool = ctx.build_domain_pool(dev(torch, img), B, L, tau)
+    info = pool.info()
+    keys, keep, _ = oracle.entropy_keys(img, B, L, tau)
+    assert info["n_candidates"] == keys.size
+    assert np.array_equal(info["keys"].cpu().numpy(), keys)
+    assert np.array_equal(info["keep"].cpu().numpy(), keep)
+    assert np.array_equal(info["kept"].cpu().numpy(), oracle.kept_list(img, B, L, tau))
+
+
+def test_empty_pool_is_an_error(fic):
+    p, ctx, torch = fic
+    img = constant_image(32, 5)
+    with pytest.raises(p.FicError) as ei:
+        ctx.build_domain_pool(dev(torch, img), 4, 2, 0.5)
+    assert ei.value.status == 3
+
+
+# ------------------------------------------------------------------------------- one level
+def level_case(fic, img, B, L, tau, s, tol=8.0, is_min=True, ranges=None):
+    p, ctx, torch = fic
+    N = img.shape[0]
+    if ranges is None:
+        ranges = np.array([(u * B, v * B) for v in range(N // B) for u in range(N // B)], np.int32)
+    dimg = dev(torch, img)
+    pool = ctx.build_domain_pool(dimg, B, L, tau)
+    out = ctx.encode_level(dimg, pool, dev(torch, ranges.reshape(-1, 2)), s, tol, is_min)
+    got = p.records_to_numpy(out)
+    kept = oracle.kept_list(img, B, L, tau)
+    ref = oracle.encode_level(img, B, L, kept, ranges, s, tol, is_min)
+    assert_same(got, ref, f"B={B} L={L} tau={tau} s={s}")
+    return got, ctx.stats()
+
+
+@pytest.mark.parametrize("B", [2, 4, 8, 16])
+@pytest.mark.parametrize("smode", ["predefined", "grid"])
+def test_level_parity_synthetic(fic, B, smode):
+    img = make_image(96, 100 + B)
+    s = PREDEFINED_S[B] if smode == "predefined" else GRID_S
+    level_case(fic, img, B, 2, -1.0, s, tol=6.0, is_min=False)
+
+
+@pytest.mark.parametrize("B,N,L", [(2, 50, 3), (4, 72, 1), (8, 88, 5), (16, 80, 3)])
+def test_level_parity_ragged_random(fic, B, N, L):
+    # N not a multiple of the tile sizes, n_k not a multiple of 128, n_r not a multiple of 8
+    img = random_image(N, 7 * B + N)
+    n = (N // B) * B
+    rng = np.random.default_rng(B)
+    ranges = np.array([(u * B, v * B) for v in range(n // B) for u in range(n // B)], np.int32)
+    keep = np.sort(rng.choice(len(ranges), size=len(ranges) * 2 // 3 + 1, replace=False))
+    ranges = ranges[keep]
+    level_case(fic, img, B, L, -1.0, PREDEFINED_S[B], ranges=ranges)
+
+
+def test_level_parity_entropy_filtered(fic):
+    img = make_image(128, 5, texture=True)
+    for B, tau in ((16, 5.0), (8, 4.6), (4, 3.8), (2, 2.6)):
+        level_case(fic, img, B, 2, tau, PREDEFINED_S[B])
+
+
+def test_level_odd_s_lists(fic):
+    img = make_image(64, 17)
+    level_case(fic, img, 4, 2, -1.0, (0.0,))               # only s = 0
+    level_case(fic, img, 4, 2, -1.0, (0.7, 0.0, 0.7, 1.0))  # duplicates, zero in the middle
+    level_case(fic, img, 4, 2, -1.0, (1.0,))
+    level_case(fic, img, 2, 2, -1.0, tuple(np.linspace(0, 1, 16)))
+
+
+def test_level_zero_error_ramp(fic):
+    got, _ = level_case(fic, ramp_image(64), 2, 2, -1.0, PREDEFINED_S[2])
+    assert (got["err"] == 0.0).all() and (got["dom"] == 0).all() and (got["iso"] == 0).all()
+
+
+def test_level_single_range_and_empty(fic):
+    p, ctx, torch = fic
+    img = make_image(64, 3)
+    level_case(fic, img, 8, 2, -1.0, PREDEFINED_S[8], ranges=np.array([[24, 40]], np.int32))
+    dimg = dev(torch, img)
+    pool = ctx.build_domain_pool(dimg, 8, 2, -1.0)
+    out = ctx.encode_level(dimg, pool, torch.zeros((0, 2), dtype=torch.int32, device="cuda"),
+                           PREDEFINED_S[8], 8.0, True)
+    assert out.shape[0] == 0
+
+
+# ------------------------------------------------------------------------------- full encodes
+def encode_both(fic, cfg, img=None):
+    p, ctx, torch = fic
+    if img is None:
+        img = image_for(cfg)
+    got = p.records_to_numpy(ctx.encode_cfg(cfg, dev(torch, img)))
+    return img, got
+
+
+@pytest.mark.parametrize("smode", ["predefined", "grid"])
+def test_c1_full_parity(fic, smode):
+    cfg = config("C1", s_mode=smode)
+    img, got = encode_both(fic, cfg)
+    assert_same(got, oracle.encode_cfg(cfg, img), f"C1 {smode}")
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_c2_full_parity(fic, seed):
+    cfg = config("C2", seed=seed)
+    img, got = encode_both(fic, cfg)
+    assert_same(got, oracle.encode_cfg(cfg, img), f"C2 seed {seed}")
+
+
+@pytest.mark.parametrize("t", [0.0, 4.0, 12.0, 1e9])
+def test_quadtree_thresholds_parity(fic, t):
+    cfg = config("C2", t=t)
+    cfg["N"] = 128
+    img = make_image(128, 77, texture=True)
+    cfg["tau"] = [-1.0, 4.7, -1.0, 2.6]
+    img, got = encode_both(fic, cfg, img)
+    assert_same(got, oracle.encode_cfg(cfg, img), f"t={t}")
+
+
+def test_constant_image(fic):
+    cfg = config("C2")
+    cfg["tau"] = [-1.0] * 4
+    img = constant_image(256, 200)
+    img, got = encode_both(fic, cfg, img)
+    assert len(got) == 256 and (got["B"] == 16).all() and (got["err"] == 0.0).all()
+    assert_same(got, oracle.encode_cfg(cfg, img), "constant")
+
+
+def test_determinism_and_host_api(fic):
+    p, ctx, torch = fic
+    cfg = config("C2", seed=2)
+    img = image_for(cfg)
+    a = ctx.encode_cfg(cfg, dev(torch, img)).cpu().numpy().tobytes()
+    b = ctx.encode_cfg(cfg, dev(torch, img)).cpu().numpy().tobytes()
+    assert a == b
+    h = ctx.encode_host(img, cfg["B_max"], cfg["B_min"], cfg["L"], cfg["tau"], cfg["s"], cfg["rms_tol"])
+    assert h.tobytes() == a
+
+
+def test_shards_merge_equals_single(fic):
+    p, ctx, torch = fic
+    cfg = config("C2", seed=3)
+    img = image_for(cfg)
+    dimg = dev(torch, img)
+    full = ctx.encode_cfg(cfg, dimg).cpu().numpy().tobytes()
+    for W in (2, 3, 8):
+        parts = [ctx.encode_cfg(cfg, dimg, shard=r, n_shards=W).clone() for r in range(W)]
+        counts = [x.shape[0] for x in parts]
+        stride = max(counts)
+        buf = torch.zeros((W * stride, 40), dtype=torch.uint8, device="cuda")
+        for r, x in enumerate(parts):
+            buf[r * stride: r * stride + x.shape[0]] = x
+        merged = ctx.merge_shards(buf, counts, stride).cpu().numpy().tobytes()
+        assert merged == full, W
+
+
+def test_errors(fic):
+    p, ctx, torch = fic
+    img = dev(torch, make_image(64, 1))
+    with pytest.raises(p.FicError) as ei:  # N not a multiple of B_max
+        ctx.encode(dev(torch, make_image(72, 1)), 16, 2, 2, [-1] * 4, [(0.5,)] * 4, [8.0] * 4)
+    assert ei.value.status == 2
+    with pytest.raises(p.FicError) as ei:  # s outside [0, 1]
+        ctx.encode(img, 16, 2, 2, [-1] * 4, [(1.5,)] * 4, [8.0] * 4)
+    assert ei.value.status == 1
+    with pytest.raises(p.FicError) as ei:  # B_min not a power of two
+        ctx.encode(img, 16, 3, 2, [-1] * 4, [(0.5,)] * 4, [8.0] * 4)
+    assert ei.value.status == 1
+    with pytest.raises(p.FicError) as ei:  # empty pool
+        ctx.encode(dev(torch, constant_image(64, 3)), 16, 2, 2, [0.1] * 4, [(0.5,)] * 4, [8.0] * 4)
+    assert ei.value.status == 3
+
+
+# ------------------------------------------------------------------ full-size, sampled checks
+def sampled_level_check(fic, img, cfg, got, per_level=24, seed=0, parents=8):
+    """Sampled records of a GPU encode re-derived one by one by the oracle at their level, plus
+    sampled parents re-derived as rejected; leaves tile the image."""
+    N = img.shape[0]
+    cov = np.zeros((N, N), np.int32)
+    for r in got:
+        cov[r["ry"]:r["ry"] + r["B"], r["rx"]:r["rx"] + r["B"]] += 1
+    assert (cov == 1).all()
+    levels = [cfg["B_max"] >> i for i in range(len(cfg["s"]))]
+    for li, B in enumerate(levels):
+        sel = got[got["B"] == B]
+        if len(sel) == 0:
+            continue
+        kept = oracle.kept_list(img, B, cfg["L"], cfg["tau"][li])
+        idx = sample_indices(len(sel), per_level, seed + li)
+        ranges = np.stack([sel["rx"][idx], sel["ry"][idx]], 1).astype(np.int32)
+        ref = oracle.encode_level(img, B, cfg["L"], kept, ranges, cfg["s"][li], cfg["rms_tol"][li],
+                                  B == cfg["B_min"])
+        assert_same(sel[idx], ref, f"sampled level B={B}")
+        if li > 0 and parents:
+            P = 2 * B
+            pk = oracle.kept_list(img, P, cfg["L"], cfg["tau"][li - 1])
+            pi = sample_indices(len(sel), parents, seed + 100 + li)
+            par = np.unique(np.stack([(sel["rx"][pi] // P) * P, (sel["ry"][pi] // P) * P], 1), axis=0)
+            pref = oracle.encode_level(img, P, cfg["L"], pk, par.astype(np.int32), cfg["s"][li - 1],
+                                       cfg["rms_tol"][li - 1], False)
+            assert not pref["accepted"].any()
+
+
+@pytest.mark.parametrize("smode,t", [("predefined", 4.0), ("predefined", 8.0), ("predefined", 12.0),
+                                     ("grid", 8.0)])
+def test_c3_sampled(fic, smode, t):
+    cfg = config("C3", s_mode=smode, t=t)
+    img, got = encode_both(fic, cfg)
+    # pools: full keep masks
+    p, ctx, torch = fic
+    for li, B in enumerate([16, 8, 4, 2]):
+        pool = ctx.build_domain_pool(dev(torch, img), B, cfg["L"], cfg["tau"][li])
+        _, keep, _ = oracle.entropy_keys(img, B, cfg["L"], cfg["tau"][li])
+        assert np.array_equal(pool.info()["keep"].cpu().numpy(), keep)
+    sampled_level_check(fic, img, cfg, got, per_level=16)
+
+
+def test_c4_sampled(fic):
+    p, ctx, torch = fic
+    cfg = config("C4")
+    img = image_for(cfg)
+    B, L = 8, 1
+    dimg = dev(torch, img)
+    pool = ctx.build_domain_pool(dimg, B, L, -1.0)
+    assert pool.info()["n_kept"] == 1009 ** 2
+    ranges = np.array([(u * B, v * B) for v in range(128) for u in range(128)], np.int32)
+    got = p.records_to_numpy(ctx.encode_level(dimg, pool, dev(torch, ranges), PREDEFINED_S[8], 8.0, True))
+    idx = sample_indices(len(ranges), 8, 4)
+    kept = np.arange(1009 ** 2, dtype=np.int32)
+    ref = oracle.encode_level(img, B, L, kept, ranges[idx], PREDEFINED_S[8], 8.0, True)
+    assert_same(got[idx], ref, "C4 sampled")
+
+
+@pytest.mark.slow
+def test_c5_sampled(fic):
+    cfg = config("C5")
+    img, got = encode_both(fic, cfg)
+    sampled_level_check(fic, img, cfg, got, per_level=3, parents=2)
