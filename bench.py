@@ -1,0 +1,341 @@
+#!/usr/bin/env python3
+"""bench.py -- range-domain-isometry pair evaluations per second of the B200 fractal encoder.
+
+Workload (BASELINE.json `metric` is quoted on the 512x512 image): config C3 -- 512x512 seeded
+synthetic image with a 1/f texture layer, quadtree 16->8->4->2, domain step L = 2, entropy-
+filtered pools (~50% kept), the paper's predefined s (§3.1), RMS tolerance 8.
+One step = one full fic_encode (all four pool builds + all four level searches + quadtree),
+image already resident in HBM.  L2 (126 MB) is flushed by writing a 256 MB buffer between
+timed steps (outside the timed events).  Multi-GPU (torchrun): weak scaling -- every rank
+encodes its own C3 image (seed = rank), no collective on the data path; value = pairs of all
+ranks / max-over-ranks device time.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl fic|reference]
+
+--impl reference times the CPU oracle (oracle/, the test-infrastructure reference) on a
+bounded sample of the same workload (every S-th top-level block with its whole subtree).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "range-domain-isometry pair evals/sec (ms per 512x512 encode in ms_per_step)"
+UNIT = "pairs/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["fic", "reference"], default="fic")
+    ap.add_argument("--config", default="C3")
+    ap.add_argument("--s-mode", default="predefined", choices=["predefined", "grid"])
+    ap.add_argument("--t", type=float, default=8.0)
+    ap.add_argument("--cpu-shards", type=int, default=48,
+                    help="oracle sample = 1/cpu-shards of the top-level blocks")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(prefix="clocks_", suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        os.unlink(self.path)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        loaded = [x for x in sm if x > 0.5 * max(sm)] or sm
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": max(smax),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def load_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+def load_traffic():
+    """dram bytes per launch of the dominant kernel from the committed ncu summary (or None)."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
+        return d.get("search_dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+# ----------------------------------------------------------------------------- oracle sample
+def oracle_sample(cfg, img, shards: int, shard: int = 0):
+    """Time the oracle on every `shards`-th top-level block (+ subtree); returns (pairs, s, threads)."""
+    import oracle
+    levels = [cfg["B_max"] >> i for i in range(len(cfg["s"]))]
+    n_k = [oracle.kept_list(img, B, cfg["L"], cfg["tau"][i]).size for i, B in enumerate(levels)]
+    t0 = time.perf_counter()
+    rec = oracle.encode_cfg(cfg, img, shard=shard, n_shards=shards)
+    dt = time.perf_counter() - t0
+    pairs = 0
+    for li, B in enumerate(levels):
+        deeper = rec[rec["B"] <= B]
+        anc = {(int(x) // B, int(y) // B) for x, y in zip(deeper["rx"], deeper["ry"])}
+        pairs += len(anc) * n_k[li] * 8
+    return pairs, dt, oracle.num_threads()
+
+
+def emit(d):
+    print(json.dumps(d), flush=True)
+
+
+# ----------------------------------------------------------------------------- reference arm
+def run_reference(args, cfg_name):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from fic_inputs import config, image_for
+    cfg = config(cfg_name, s_mode=args.s_mode, t=args.t)
+    img = image_for(cfg)
+    S = args.cpu_shards
+    for w in range(args.warmup):
+        oracle_sample(cfg, img, S, w % S)
+    tot_pairs, tot_t, thr = 0, 0.0, 1
+    for k in range(args.steps):
+        p, dt, thr = oracle_sample(cfg, img, S, (args.warmup + k) % S)
+        tot_pairs += p
+        tot_t += dt
+    v = tot_pairs / tot_t
+    sample = (f"oracle encode of every {S}-th top-level block (shards {args.warmup % S}..) of "
+              f"{cfg_name}, {args.steps} steps")
+    emit({"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+          "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps,
+          "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64+f64",
+          "data": "synthetic",
+          "config": {"workload": cfg_name, "N": cfg["N"], "levels": "16->2", "L": cfg["L"],
+                     "s_mode": args.s_mode, "rms_tol": args.t, "sample": f"1/{S} of top-level blocks"},
+          "cpu_baseline": {"value": v, "unit": UNIT, "cores": thr, "kind": "oracle",
+                           "sample": sample},
+          "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}})
+    return 0
+
+
+# ----------------------------------------------------------------------------- product arm
+def main():
+    args = parse()
+    cfg_name = args.config.upper()
+    if args.impl == "reference":
+        return run_reference(args, cfg_name)
+
+    import torch
+    import torch.distributed as dist
+    from fic_inputs import config, image_for
+    from paper_1501_04140_b200 import build as pbuild
+    pbuild.build()
+    import paper_1501_04140_b200 as fic
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local if world > 1 else 0)
+    torch.cuda.set_device(dev)
+
+    cfg = config(cfg_name, s_mode=args.s_mode, t=args.t, seed=rank)
+    img_np = image_for(cfg)
+    img = torch.from_numpy(img_np).to(dev)
+    stream = torch.cuda.current_stream(dev)
+    ctx = fic.Context(dev.index, stream=stream, timing=True)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    cap = (cfg["N"] // cfg["B_min"]) ** 2
+    out = torch.empty((cap, fic.RECORD_BYTES), dtype=torch.uint8, device=dev)
+
+    def step():
+        return ctx.encode_cfg(cfg, img, out=out)
+
+    for _ in range(max(args.warmup, 0)):
+        step()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler(dev.index)
+    clocks.start()
+    times, level_acc = [], None
+    launches = 0
+    n_rec = 0
+    for _ in range(args.steps):
+        flush.fill_(1)  # L2 flush between timed steps (outside the events)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        rec = step()
+        e1.record(stream)
+        e1.synchronize()
+        times.append(e0.elapsed_time(e1))
+        n_rec = rec.shape[0]
+        st = ctx.stats()
+        launches += sum(s["kernel_launches"] for s in st)
+        if level_acc is None:
+            level_acc = [dict(s) for s in st]
+            for s in level_acc:
+                s["ms_search_list"] = [s["ms_search"]]
+        else:
+            for a, s in zip(level_acc, st):
+                a["ms_search_list"].append(s["ms_search"])
+                for k in ("ms_pool", "ms_search", "ms_finalize"):
+                    a[k] += s[k]
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    total_ms = sum(times)
+    pairs_step = sum(s["pairs"] for s in level_acc)
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    p = torch.tensor([pairs_step * args.steps], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(p, op=dist.ReduceOp.SUM)
+    max_ms = float(t.item())
+    all_pairs = float(p.item())
+    value = all_pairs / (max_ms / 1e3)
+
+    # ---- e2e: same metric through the host-buffer C-ABI call (H2D image, D2H records inside)
+    e2e = None
+    if not args.no_e2e:
+        h_img = torch.empty((cfg["N"], cfg["N"]), dtype=torch.uint8, pin_memory=True)
+        h_img.copy_(torch.from_numpy(img_np))
+        h_out_t = torch.empty((cap * fic.RECORD_BYTES,), dtype=torch.uint8, pin_memory=True)
+        h_out = h_out_t.numpy().view(fic.RECORD_DTYPE)
+        h_img_np = h_img.numpy()
+
+        def hstep():
+            return ctx.encode_host(h_img_np, cfg["B_max"], cfg["B_min"], cfg["L"], cfg["tau"],
+                                   cfg["s"], cfg["rms_tol"], out=h_out)
+        for _ in range(max(args.warmup, 1)):
+            hstep()
+        et = []
+        for _ in range(args.steps):
+            flush.fill_(1)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            r = hstep()
+            e1.record(stream)
+            e1.synchronize()
+            et.append(e0.elapsed_time(e1))
+        te = torch.tensor([sum(et)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": all_pairs / (float(te.item()) / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": cfg["N"] * cfg["N"],
+               "d2h_bytes_per_step": int(len(r)) * fic.RECORD_BYTES,
+               "ms_per_step": float(te.item()) / args.steps}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
+
+    # ---- roofline of the dominant kernel (the level search with the largest device time)
+    peaks = load_peaks()
+    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+    dom = max(level_acc, key=lambda s: s["ms_search"])
+    n = dom["B"] * dom["B"]
+    ms_launch = dom["ms_search"] / args.steps
+    achieved = 2.0 * dom["pairs"] * n / (ms_launch / 1e3) / 1e12  # fp32 FMA = 2 flop per MAC
+    peak = 2.0 * 148 * 128 * sm_max * 1e6 / 1e12  # 148 SMs x 128 FP32 lanes x max SM clock
+    traffic = load_traffic()
+
+    res = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u8->f32(exact int)+f64",
+        "data": "synthetic",
+        "config": {"workload": cfg_name, "N": cfg["N"], "levels": f"{cfg['B_max']}->{cfg['B_min']}",
+                   "L": cfg["L"], "s_mode": args.s_mode, "rms_tol": args.t,
+                   "entropy_tau": cfg["tau"], "images": "seed = rank",
+                   "l2": "flushed between timed steps (256 MB write)",
+                   "pairs_per_step": pairs_step, "records_per_step": n_rec},
+        "roofline": {"bound": "alu", "kernel": f"search_kernel<B={dom['B']}>",
+                     "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "peak_note": "FP32 FFMA: 148 SMs x 128 lanes x 2 flop x sm_max_mhz "
+                                  "(MEASURED_PEAKS.json); algorithmic work = pairs x B^2 MACs"},
+        "levels": [{"B": s["B"], "n_candidates": s["n_candidates"], "n_kept": s["n_kept"],
+                    "n_ranges": s["n_ranges"], "pairs": s["pairs"],
+                    "exact_evals": s["exact_evals"],
+                    "ms_pool": s["ms_pool"] / args.steps, "ms_search": s["ms_search"] / args.steps,
+                    "ms_finalize": s["ms_finalize"] / args.steps} for s in level_acc],
+        "gpu_launches": int(launches),
+        "clocks": clk,
+    }
+    if e2e:
+        res["e2e"] = e2e
+    if world == 1 and not args.no_cpu_baseline:
+        S = args.cpu_shards
+        pairs, dt, thr = oracle_sample(cfg, img_np, S, 0)
+        res["cpu_baseline"] = {"value": pairs / dt, "unit": UNIT, "cores": thr, "kind": "oracle",
+                               "sample": f"oracle encode of every {S}-th top-level block of "
+                                         f"{cfg_name} with its subtree ({pairs} pairs, {dt:.1f} s)"}
+    emit(res)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -74,6 +74,10 @@ def config(name: str, *, s_mode: str = "predefined", t: float = 8.0, seed: int =
                  tau=TAU.get("C5", [-1.0] * 4))
     else:
         raise ValueError(name)
+    key = f"{name}@{seed}"
+    if seed != 0 and key in TAU:
+        c["tau"] = list(TAU[key])
+    c["tau"] = list(c["tau"])
     nlev = len(levels(c["B_max"], c["B_min"]))
     c["name"] = name
     c["seed"] = seed

@@ -70,6 +70,7 @@ typedef struct {
     int64_t pairs;          /* n_ranges * n_kept * 8 range-domain-isometry pairs scored      */
     int64_t exact_evals;    /* (range, domain) pairs that took the exact binary64 path       */
     float ms_pool, ms_search, ms_finalize;
+    int64_t kernel_launches; /* libfic kernels launched for this level (pool + search + quadtree) */
 } fic_level_stats;
 
 fic_status fic_ctx_set_timing(fic_ctx *ctx, int32_t enable);

@@ -13,5 +13,5 @@ the decoded-image PSNR sanity report, which the oracle does not compute.
 """
 from .oracle import (  # noqa: F401
     build, lib, lut, threshold, axis_candidates, entropy_keys, kept_list, isometry,
-    decimate, o_code, encode_level, encode, RECORD_DTYPE, num_threads,
+    decimate, o_code, encode_level, encode, encode_cfg, RECORD_DTYPE, num_threads,
 )

@@ -5,6 +5,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -32,7 +33,10 @@ struct fic_ctx {
         b_scounts;
     unsigned long long *h_counts = nullptr;  // pinned [64]
     std::vector<fic_level_stats> stats;
-    cudaEvent_t ev[fic::kMaxLevels][5] = {};  // pool start, search start, search end, finalize end, pool end
+    cudaEvent_t ev[fic::kMaxLevels][5] = {};
+    int64_t launches = 0;
+    int force_direct = 0;  // env FIC_SEARCH=direct: direct kernel at every B (A/B checks)
+    Buf b_rc, b_meta, b_u;  // libfic kernels enqueued (for fic_level_stats.kernel_launches)  // pool start, search start, search end, finalize end, pool end
 };
 
 namespace {
@@ -89,7 +93,7 @@ void free_buf(Buf &b) {
 }
 void free_pool(Pool &P) {
     free_buf(P.b_keys); free_buf(P.b_keep); free_buf(P.b_kept); free_buf(P.b_Dt);
-    free_buf(P.b_SDf); free_buf(P.b_SD); free_buf(P.b_C); free_buf(P.b_misc);
+    free_buf(P.b_SDf); free_buf(P.b_SD); free_buf(P.b_C); free_buf(P.b_misc); free_buf(P.b_Dc);
 }
 
 bool pow2(int32_t v) { return v > 0 && (v & (v - 1)) == 0; }
@@ -127,14 +131,18 @@ fic_status pool_enqueue(fic_ctx *ctx, Pool &P, const uint8_t *img, int32_t N, in
     CK(grow(ctx, P.b_keys, sizeof(int64_t) * P.n_c));
     CK(grow(ctx, P.b_keep, P.n_c + 16));
     CK(grow(ctx, P.b_kept, sizeof(int32_t) * P.n_c));
-    CK(grow(ctx, P.b_Dt, sizeof(float) * slots * P.n));
+    P.direct = (ctx->force_direct || fic::fourier_record_stride(B) == 0) ? 1 : 0;
+    if (P.direct) CK(grow(ctx, P.b_Dt, sizeof(float) * slots * P.n));
+    else CK(grow(ctx, P.b_Dc, sizeof(float) * slots * fic::fourier_record_stride(B)));
     CK(grow(ctx, P.b_SDf, sizeof(float) * slots));
     CK(grow(ctx, P.b_SD, sizeof(int32_t) * slots));
     CK(grow(ctx, P.b_C, sizeof(int64_t) * slots));
     CK(grow(ctx, P.b_misc, 2 * sizeof(unsigned long long)));
     CK(grow(ctx, ctx->b_blocksum, sizeof(int64_t) * fic::select_blocksum_len(P.n_c)));
     P.keys = ptr<int64_t>(P.b_keys); P.keep = ptr<uint8_t>(P.b_keep);
-    P.kept = ptr<int32_t>(P.b_kept); P.Dt = ptr<float>(P.b_Dt); P.SDf = ptr<float>(P.b_SDf);
+    P.kept = ptr<int32_t>(P.b_kept); P.SDf = ptr<float>(P.b_SDf);
+    P.Dt = P.direct ? ptr<float>(P.b_Dt) : nullptr;
+    P.Dc = P.direct ? nullptr : ptr<float>(P.b_Dc);
     P.SD = ptr<int32_t>(P.b_SD); P.C = ptr<int64_t>(P.b_C);
     P.d_misc = ptr<unsigned long long>(P.b_misc);
     cudaStream_t st = ctx->stream;
@@ -146,9 +154,13 @@ fic_status pool_enqueue(fic_ctx *ctx, Pool &P, const uint8_t *img, int32_t N, in
                                 P.keep, st));
     CK(fic::launch_select_index(P.keep, P.n_c, ptr<int64_t>(ctx->b_blocksum), P.kept, &P.d_misc[0],
                                 st));
-    CK(fic::launch_pool_gather(img, N, B, L, P.A, P.kept, &P.d_misc[0], tiles_max, P.Dt, st));
+    if (P.direct)
+        CK(fic::launch_pool_gather(img, N, B, L, P.A, P.kept, &P.d_misc[0], tiles_max, P.Dt, st));
+    else
+        CK(fic::launch_pool_coeff(img, N, B, L, P.A, P.kept, &P.d_misc[0], slots, P.Dc, st));
     CK(fic::launch_pool_moments(img, N, B, L, P.A, P.kept, &P.d_misc[0], slots, P.SD, P.SDf, P.C,
                                 &P.d_misc[1], st));
+    ctx->launches += 6;  // entropy, select x3, gather, moments
     return FIC_OK;
 }
 
@@ -183,6 +195,7 @@ fic_status level_enqueue(fic_ctx *ctx, const Pool &P, const uint8_t *img, const 
                          int64_t n_r, const double *h_s, int32_t n_s, double rms_tol, int is_min,
                          fic_record *rec, uint8_t *acc, uint8_t *child, int level_slot) {
     cudaStream_t st = ctx->stream;
+    if (n_r == 0) return FIC_OK;
     fic::SearchParams sp;
     memset(&sp, 0, sizeof sp);
     sp.img = img;
@@ -207,7 +220,10 @@ fic_status level_enqueue(fic_ctx *ctx, const Pool &P, const uint8_t *img, const 
     }
     sp.cmax = (double)P.cmax;
     const int64_t slots = P.n_tiles * fic::kTileD;
-    sp.nsplit = fic::search_nsplit_hint(P.B, n_r, P.n_tiles, ctx->num_sms);
+    if (P.direct)
+        sp.nsplit = fic::search_nsplit_hint(P.B, n_r, P.n_tiles, ctx->num_sms);
+    else
+        sp.nsplit = fic::fourier_nsplit_hint(P.B, sp.nsp, n_r, P.n_tiles, ctx->num_sms);
     sp.tiles_per_split = (int32_t)((P.n_tiles + sp.nsplit - 1) / sp.nsplit);
     sp.nsplit = (int32_t)((P.n_tiles + sp.tiles_per_split - 1) / sp.tiles_per_split);
     CK(grow(ctx, ctx->b_t2f, sizeof(float) * (size_t)slots * (sp.nsp ? sp.nsp : 1)));
@@ -215,11 +231,29 @@ fic_status level_enqueue(fic_ctx *ctx, const Pool &P, const uint8_t *img, const 
     sp.t2f = ptr<float>(ctx->b_t2f);
     sp.part = ptr<fic::Partial>(ctx->b_part);
     sp.exact_count = ptr<unsigned long long>(ctx->b_counts) + 8 + level_slot;
-    fic::SList sl;
-    memcpy(sl.s, sp.spos, sizeof sl.s);
-    CK(fic::launch_t2f(P.C, (int32_t)P.n_k, slots, sl, sp.nsp, ptr<float>(ctx->b_t2f), st));
-    if (ctx->timing) CK(cudaEventRecord(ctx->ev[level_slot][1], st));
-    if (sp.nsp > 0) CK(fic::launch_search(P.B, sp.nsp, sp, st));
+    if (P.direct) {
+        fic::SList sl;
+        memcpy(sl.s, sp.spos, sizeof sl.s);
+        CK(fic::launch_t2f(P.C, (int32_t)P.n_k, slots, sl, sp.nsp, ptr<float>(ctx->b_t2f), st));
+        if (sp.nsp > 0 && slots > 0) ctx->launches += 1;
+        if (ctx->timing) CK(cudaEventRecord(ctx->ev[level_slot][1], st));
+        if (sp.nsp > 0) {
+            CK(fic::launch_search(P.B, sp.nsp, sp, st));
+            ctx->launches += 1;
+        }
+    } else {
+        const int nc = fic::fourier_record_stride(P.B);  // >= 8 nO + 1
+        const int32_t r_stride = (int32_t)((n_r + 31) / 32 * 32);
+        CK(grow(ctx, ctx->b_rc, sizeof(float) * (size_t)nc * r_stride));
+        CK(grow(ctx, ctx->b_meta, fic::fourier_meta_bytes() * (size_t)n_r));
+        CK(grow(ctx, ctx->b_u, sizeof(float) * (size_t)slots * (sp.nsp ? sp.nsp : 1)));
+        if (ctx->timing) CK(cudaEventRecord(ctx->ev[level_slot][1], st));
+        CK(fic::launch_fourier_level(P.B, img, P.N, ranges, (int32_t)n_r, P.Dc, P.C, (int32_t)P.n_k,
+                                     (int32_t)P.n_tiles, sp.nsplit, sp.tiles_per_split, sp,
+                                     ptr<float>(ctx->b_rc), r_stride, ctx->b_meta.p, ptr<float>(ctx->b_u),
+                                     st));
+        ctx->launches += 1 + (sp.nsp > 0 ? 2 : 0);
+    }
     if (ctx->timing) CK(cudaEventRecord(ctx->ev[level_slot][2], st));
     fic::FinalizeParams fp;
     memset(&fp, 0, sizeof fp);
@@ -234,6 +268,7 @@ fic_status level_enqueue(fic_ctx *ctx, const Pool &P, const uint8_t *img, const 
     fp.rms_tol = rms_tol; fp.is_min = is_min;
     fp.rec = rec; fp.accepted = acc; fp.child = child;
     CK(fic::launch_finalize(fp, st));
+    if (n_r > 0) ctx->launches += 1;
     if (ctx->timing) CK(cudaEventRecord(ctx->ev[level_slot][3], st));
     return FIC_OK;
 }
@@ -279,6 +314,11 @@ fic_status fic_ctx_create(int32_t device, void *cuda_stream, fic_ctx **out) {
         e = cudaMemcpy(ctx->d_delta, delta.data(), sizeof(int64_t) * 4096, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMallocHost(&ctx->h_counts, 64 * sizeof(unsigned long long));
     if (e == cudaSuccess) e = grow(nullptr, ctx->b_counts, 64 * sizeof(unsigned long long));
+    if (e == cudaSuccess) e = fic::fourier_init();
+    {
+        const char *env = getenv("FIC_SEARCH");
+        ctx->force_direct = env && strcmp(env, "direct") == 0;
+    }
     for (int l = 0; l < fic::kMaxLevels && e == cudaSuccess; ++l)
         for (int q = 0; q < 5 && e == cudaSuccess; ++q) e = cudaEventCreate(&ctx->ev[l][q]);
     if (e != cudaSuccess) {
@@ -308,7 +348,7 @@ fic_status fic_ctx_destroy(fic_ctx *ctx) {
     for (auto &P : ctx->levels) free_pool(P);
     Buf *bufs[] = {&ctx->b_blocksum, &ctx->b_counts, &ctx->b_rng[0], &ctx->b_rng[1], &ctx->b_rec,
                    &ctx->b_acc, &ctx->b_child, &ctx->b_part, &ctx->b_t2f, &ctx->b_img, &ctx->b_out,
-                   &ctx->b_scounts};
+                   &ctx->b_scounts, &ctx->b_rc, &ctx->b_meta, &ctx->b_u};
     for (Buf *b : bufs) free_buf(*b);
     if (ctx->d_delta) cudaFree(ctx->d_delta);
     if (ctx->h_counts) cudaFreeHost(ctx->h_counts);
@@ -431,12 +471,15 @@ fic_status fic_encode(fic_ctx *ctx, const uint8_t *img, int32_t N, int32_t B_max
 
     // 1. every level's pool (independent of the quadtree), all enqueued back to back
     for (int l = 0; l < nl; ++l) {
+        ctx->launches = 0;
         if (ctx->timing) CK(cudaEventRecord(ctx->ev[l][0], st));
         CKS(pool_enqueue(ctx, ctx->levels[l], img, N, B_max >> l, L, h_tau[l]));
         if (ctx->timing) CK(cudaEventRecord(ctx->ev[l][4], st));
         CK(cudaMemcpyAsync(ctx->h_counts + 2 * l, ctx->levels[l].d_misc, 2 * sizeof(unsigned long long),
                            cudaMemcpyDeviceToHost, st));
+        ctx->stats[l].kernel_launches = ctx->launches;
     }
+    ctx->launches = 0;
     // 2. top-level ranges of this shard (row-major)
     const int64_t G = N / B_max;
     const int64_t Gmin = N / B_min;
@@ -450,6 +493,7 @@ fic_status fic_encode(fic_ctx *ctx, const uint8_t *img, int32_t N, int32_t B_max
     CK(fic::launch_top_flags(child, G, shard, n_shards, st));
     CK(fic::launch_select_grid(child, G, B_max, ptr<int64_t>(ctx->b_blocksum), ptr<int2>(ctx->b_rng[0]),
                                d_counts + 2, st));
+    ctx->launches += 4;  // top flags + select x3
     int64_t n_r = G * G > shard ? (G * G - shard + n_shards - 1) / n_shards : 0;
     CK(cudaStreamSynchronize(st));
     for (int l = 0; l < nl; ++l) pool_take_counts(ctx->levels[l], ctx->h_counts + 2 * l);
@@ -470,9 +514,12 @@ fic_status fic_encode(fic_ctx *ctx, const uint8_t *img, int32_t N, int32_t B_max
         CK(fic::launch_select_records(ptr<uint8_t>(ctx->b_acc), n_r, ptr<int64_t>(ctx->b_blocksum),
                                       ptr<fic_record>(ctx->b_rec), out, total, capacity, d_counts + 0,
                                       st));
-        if (!last)
+        ctx->launches += n_r > 0 ? 3 : 0;
+        if (!last) {
             CK(fic::launch_select_grid(child, Gc, B / 2, ptr<int64_t>(ctx->b_blocksum),
                                        ptr<int2>(ctx->b_rng[cur ^ 1]), d_counts + 1, st));
+            ctx->launches += 3;
+        }
         CK(cudaMemcpyAsync(ctx->h_counts + 32, d_counts, 2 * sizeof(unsigned long long),
                            cudaMemcpyDeviceToHost, st));
         CK(cudaMemcpyAsync(ctx->h_counts + 40 + l, d_counts + 8 + l, sizeof(unsigned long long),
@@ -484,6 +531,8 @@ fic_status fic_encode(fic_ctx *ctx, const uint8_t *img, int32_t N, int32_t B_max
         ls.B = B; ls.n_candidates = P.n_c; ls.n_kept = P.n_k; ls.n_ranges = n_r;
         ls.n_accepted = n_acc; ls.pairs = n_r * P.n_k * 8;
         ls.exact_evals = (int64_t)ctx->h_counts[40 + l];
+        ls.kernel_launches += ctx->launches;
+        ctx->launches = 0;
         total += n_acc;
         n_r = n_next;
         cur ^= 1;

@@ -34,10 +34,12 @@ struct Pool {
     uint8_t *keep = nullptr;
     int32_t *kept = nullptr;
     float *Dt = nullptr, *SDf = nullptr;
+    float *Dc = nullptr;  // D4-Fourier domain records [slots][NCS] (B <= 8), or null
+    int direct = 0;       // 1: this pool feeds the direct kernel (Dt built), 0: Fourier (Dc)
     int32_t *SD = nullptr;
     int64_t *C = nullptr;
     unsigned long long *d_misc = nullptr;  // [0] = n_kept, [1] = Cmax
-    Buf b_keys, b_keep, b_kept, b_Dt, b_SDf, b_SD, b_C, b_misc;
+    Buf b_keys, b_keep, b_kept, b_Dt, b_SDf, b_SD, b_C, b_misc, b_Dc;
     int device = 0;
 };
 
@@ -119,5 +121,20 @@ cudaError_t launch_finalize(const FinalizeParams &p, cudaStream_t st);
 cudaError_t launch_merge_shards(const fic_record *in, const int64_t *d_counts, int32_t n_shards,
                                 int64_t stride, int64_t max_count, fic_record *out, cudaStream_t st);
 int search_nsplit_hint(int32_t B, int64_t n_r, int64_t n_tiles, int num_sms);
+
+// D4 group-Fourier search (fic_fourier.cu), B in {2, 4, 8}
+cudaError_t fourier_init();
+int fourier_record_stride(int B);  // floats per domain record (0 if B unsupported)
+size_t fourier_meta_bytes();
+int fourier_rpt(int32_t B, int32_t nsp);
+int fourier_nsplit_hint(int32_t B, int32_t nsp, int64_t n_r, int64_t n_tiles, int num_sms);
+cudaError_t launch_pool_coeff(const uint8_t *img, int32_t N, int32_t B, int32_t L, int32_t A,
+                              const int32_t *kept, const unsigned long long *d_nk, int64_t n_slots,
+                              float *Dc, cudaStream_t st);
+cudaError_t launch_fourier_level(int32_t B, const uint8_t *img, int32_t N, const int2 *ranges,
+                                 int32_t n_r, const float *Dc, const int64_t *C, int32_t n_k,
+                                 int32_t n_tiles, int32_t nsplit, int32_t tiles_per_split,
+                                 const SearchParams &sp, float *Rc, int32_t r_stride, void *meta,
+                                 float *U, cudaStream_t st);
 
 }  // namespace fic

@@ -180,12 +180,20 @@ struct EmitGrid {
         out[pos] = make_int2((int)(i % G) * B, (int)(i / G) * B);
     }
 };
+// records are moved as five 8-byte words so padding bytes (zero) are preserved
+__device__ __forceinline__ void copy_record(fic_record *dst, const fic_record *src) {
+    const uint64_t *s = reinterpret_cast<const uint64_t *>(src);
+    uint64_t *d = reinterpret_cast<uint64_t *>(dst);
+#pragma unroll
+    for (int q = 0; q < 5; ++q) d[q] = s[q];
+}
+
 struct EmitRecord {
     const fic_record *in;
     fic_record *out;
     int64_t base, cap;
     __device__ void operator()(int64_t i, int64_t pos) const {
-        if (base + pos < cap) out[base + pos] = in[i];
+        if (base + pos < cap) copy_record(out + base + pos, in + i);
     }
 };
 
@@ -353,7 +361,7 @@ __global__ void merge_shards_kernel(const fic_record *__restrict__ in,
     const int32_t sh = blockIdx.y;
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= counts[sh]) return;
-    const fic_record r = in[sh * stride + i];
+    const fic_record &r = in[sh * stride + i];
     const uint64_t k = rec_key(r);
     int64_t pos = i;
     for (int32_t o = 0; o < n_shards; ++o) {
@@ -366,7 +374,7 @@ __global__ void merge_shards_kernel(const fic_record *__restrict__ in,
         }
         pos += lo;
     }
-    out[pos] = r;
+    copy_record(out + pos, &r);
 }
 
 cudaError_t launch_merge_shards(const fic_record *in, const int64_t *d_counts, int32_t n_shards,

@@ -398,6 +398,7 @@ cudaError_t launch_search(int32_t B, int32_t nsp, const SearchParams &p, cudaStr
 int search_nsplit_hint(int32_t B, int64_t n_r, int64_t n_tiles, int num_sms) {
     const int occ = B >= 16 ? 1 : (B >= 8 ? 2 : 3);
     const int64_t gx = (n_r + 7) / 8;
+    if (gx <= 0 || n_tiles <= 0) return 1;
     const int64_t target = (int64_t)num_sms * occ * 2;
     int64_t ns = (target + gx - 1) / gx;
     if (ns < 1) ns = 1;

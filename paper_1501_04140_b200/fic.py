@@ -44,7 +44,7 @@ class LevelStats(C.Structure):
     _fields_ = [("B", C.c_int32), ("n_candidates", C.c_int64), ("n_kept", C.c_int64),
                 ("n_ranges", C.c_int64), ("n_accepted", C.c_int64), ("pairs", C.c_int64),
                 ("exact_evals", C.c_int64), ("ms_pool", C.c_float), ("ms_search", C.c_float),
-                ("ms_finalize", C.c_float)]
+                ("ms_finalize", C.c_float), ("kernel_launches", C.c_int64)]
 
 
 _lib = None
@@ -102,7 +102,7 @@ class _DevArray:
 
     def __init__(self, ptr: int, shape, typestr: str):
         self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr,
-                                         "data": (int(ptr), True), "version": 3, "strides": None}
+                                         "data": (int(ptr), False), "version": 3, "strides": None}
 
 
 def entropy_lut(mmax: int) -> np.ndarray:

@@ -8,6 +8,8 @@ the ORACLE (oracle/, the only arithmetic used here), and picks the shortest deci
 fixed-point threshold T(tau) lies strictly between two adjacent distinct keys, choosing the
 boundary that keeps the fraction closest to 50%, with no candidate within 1e-9 nats of tau.
 
+Seed 0 of C2/C3/C5 (the headline images) and extra seeds of C2 (parity runs) and C3 (one image
+per rank in the weak-scaling bench) each get their own thresholds ("C3@5" = C3, seed 5).
 Writes fic_inputs/tau.json.  Run:  python scripts/choose_tau.py
 """
 from __future__ import annotations
@@ -51,18 +53,20 @@ def choose(keys: np.ndarray, m: int):
 
 def main():
     out = {}
-    for name in ("C2", "C3", "C5"):
-        cfg = config(name)
+    jobs = [("C2", 0), ("C3", 0), ("C5", 0)] + [("C2", s) for s in range(1, 4)] + \
+           [("C3", s) for s in range(1, 8)]
+    for name, seed in jobs:
+        cfg = config(name, seed=seed)
         img = image_for(cfg)
         taus = []
         for B in levels(cfg["B_max"], cfg["B_min"]):
             keys, _, _ = oracle.entropy_keys(img, B, cfg["L"], -1.0)
             tau, frac = choose(keys, 4 * B * B)
             _, keep, _ = oracle.entropy_keys(img, B, cfg["L"], tau)
-            print(f"{name} B={B:2d} n_c={keys.size} tau={tau} kept={keep.mean():.4f} "
+            print(f"{name}@{seed} B={B:2d} n_c={keys.size} tau={tau} kept={keep.mean():.4f} "
                   f"(target boundary {frac:.4f})", flush=True)
             taus.append(tau)
-        out[name] = taus
+        out[name if seed == 0 else f"{name}@{seed}"] = taus
     path = os.path.join(ROOT, "fic_inputs", "tau.json")
     with open(path, "w") as f:
         json.dump(out, f, indent=1)
