@@ -137,7 +137,7 @@ fic_status pool_enqueue(fic_ctx *ctx, Pool &P, const uint8_t *img, int32_t N, in
     CK(grow(ctx, P.b_SDf, sizeof(float) * slots));
     CK(grow(ctx, P.b_SD, sizeof(int32_t) * slots));
     CK(grow(ctx, P.b_C, sizeof(int64_t) * slots));
-    CK(grow(ctx, P.b_misc, 2 * sizeof(unsigned long long)));
+    CK(grow(ctx, P.b_misc, 4 * sizeof(unsigned long long)));
     CK(grow(ctx, ctx->b_blocksum, sizeof(int64_t) * fic::select_blocksum_len(P.n_c)));
     P.keys = ptr<int64_t>(P.b_keys); P.keep = ptr<uint8_t>(P.b_keep);
     P.kept = ptr<int32_t>(P.b_kept); P.SDf = ptr<float>(P.b_SDf);
@@ -146,7 +146,7 @@ fic_status pool_enqueue(fic_ctx *ctx, Pool &P, const uint8_t *img, int32_t N, in
     P.SD = ptr<int32_t>(P.b_SD); P.C = ptr<int64_t>(P.b_C);
     P.d_misc = ptr<unsigned long long>(P.b_misc);
     cudaStream_t st = ctx->stream;
-    CK(cudaMemsetAsync(P.d_misc, 0, 2 * sizeof(unsigned long long), st));
+    CK(cudaMemsetAsync(P.d_misc, 0, 4 * sizeof(unsigned long long), st));
     const int32_t m = 4 * B * B;
     const int use_tau = tau >= 0.0;
     const int64_t T = use_tau ? entropy_threshold(tau, m) : 0;
@@ -157,7 +157,8 @@ fic_status pool_enqueue(fic_ctx *ctx, Pool &P, const uint8_t *img, int32_t N, in
     if (P.direct)
         CK(fic::launch_pool_gather(img, N, B, L, P.A, P.kept, &P.d_misc[0], tiles_max, P.Dt, st));
     else
-        CK(fic::launch_pool_coeff(img, N, B, L, P.A, P.kept, &P.d_misc[0], slots, P.Dc, st));
+        CK(fic::launch_pool_coeff(img, N, B, L, P.A, P.kept, &P.d_misc[0], slots, P.Dc,
+                                  reinterpret_cast<unsigned int *>(&P.d_misc[2]), st));
     CK(fic::launch_pool_moments(img, N, B, L, P.A, P.kept, &P.d_misc[0], slots, P.SD, P.SDf, P.C,
                                 &P.d_misc[1], st));
     ctx->launches += 6;  // entropy, select x3, gather, moments
@@ -168,6 +169,12 @@ fic_status pool_enqueue(fic_ctx *ctx, Pool &P, const uint8_t *img, int32_t N, in
 void pool_take_counts(Pool &P, const unsigned long long *h) {
     P.n_k = (int64_t)h[0];
     P.cmax = (int64_t)h[1];
+    {
+        const unsigned int bits = (unsigned int)(h[2] & 0xffffffffu);
+        float f;
+        memcpy(&f, &bits, 4);
+        P.dnmax = (double)f;
+    }
     P.n_tiles = (P.n_k + fic::kTileD - 1) / fic::kTileD;
 }
 
@@ -249,7 +256,7 @@ fic_status level_enqueue(fic_ctx *ctx, const Pool &P, const uint8_t *img, const 
         CK(grow(ctx, ctx->b_u, sizeof(float) * (size_t)slots * (sp.nsp ? sp.nsp : 1)));
         if (ctx->timing) CK(cudaEventRecord(ctx->ev[level_slot][1], st));
         CK(fic::launch_fourier_level(P.B, img, P.N, ranges, (int32_t)n_r, P.Dc, P.C, (int32_t)P.n_k,
-                                     (int32_t)P.n_tiles, sp.nsplit, sp.tiles_per_split, sp,
+                                     (int32_t)P.n_tiles, sp.nsplit, sp.tiles_per_split, sp, P.dnmax,
                                      ptr<float>(ctx->b_rc), r_stride, ctx->b_meta.p, ptr<float>(ctx->b_u),
                                      st));
         ctx->launches += 1 + (sp.nsp > 0 ? 2 : 0);
@@ -380,7 +387,7 @@ fic_status fic_build_domain_pool(fic_ctx *ctx, const uint8_t *img, int32_t N, in
     if (!pool) return fail(ctx, FIC_ERR_NOMEM, "host allocation failed");
     fic_status st = pool_enqueue(ctx, pool->P, img, N, B, L, tau_nats);
     if (st == FIC_OK) {
-        cudaError_t e = cudaMemcpyAsync(ctx->h_counts, pool->P.d_misc, 2 * sizeof(unsigned long long),
+        cudaError_t e = cudaMemcpyAsync(ctx->h_counts, pool->P.d_misc, 3 * sizeof(unsigned long long),
                                         cudaMemcpyDeviceToHost, ctx->stream);
         if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
         if (e != cudaSuccess) st = cuda_fail(ctx, e, "pool counts", __LINE__);
@@ -475,7 +482,7 @@ fic_status fic_encode(fic_ctx *ctx, const uint8_t *img, int32_t N, int32_t B_max
         if (ctx->timing) CK(cudaEventRecord(ctx->ev[l][0], st));
         CKS(pool_enqueue(ctx, ctx->levels[l], img, N, B_max >> l, L, h_tau[l]));
         if (ctx->timing) CK(cudaEventRecord(ctx->ev[l][4], st));
-        CK(cudaMemcpyAsync(ctx->h_counts + 2 * l, ctx->levels[l].d_misc, 2 * sizeof(unsigned long long),
+        CK(cudaMemcpyAsync(ctx->h_counts + 4 * l, ctx->levels[l].d_misc, 3 * sizeof(unsigned long long),
                            cudaMemcpyDeviceToHost, st));
         ctx->stats[l].kernel_launches = ctx->launches;
     }
@@ -496,7 +503,7 @@ fic_status fic_encode(fic_ctx *ctx, const uint8_t *img, int32_t N, int32_t B_max
     ctx->launches += 4;  // top flags + select x3
     int64_t n_r = G * G > shard ? (G * G - shard + n_shards - 1) / n_shards : 0;
     CK(cudaStreamSynchronize(st));
-    for (int l = 0; l < nl; ++l) pool_take_counts(ctx->levels[l], ctx->h_counts + 2 * l);
+    for (int l = 0; l < nl; ++l) pool_take_counts(ctx->levels[l], ctx->h_counts + 4 * l);
 
     // 3. the quadtree, one level at a time
     int64_t total = 0;

@@ -177,14 +177,17 @@ int fourier_record_stride(int B) {
 }
 
 // ----------------------------------------------------------------------- domain coefficients
-// Warp per domain slot: D' (2x2 sums) into shared memory, centred by 510, then the 8 nO
-// coefficients dh (orbit-major: q = O*8 + component) and the uncentred sum SD at slot NC.
+// Warp per domain slot: D' (2x2 sums), SD, the centred-and-scaled block Dt = n D' - SD (so that
+// sum_p R(p) Dt(f_k p) = n SRD_k - SR SD = Bq_k exactly, for any R), its 8 nO D4-Fourier
+// coefficients (orbit-major: q = O*8 + component; exact integers |.| <= 8 n 1020 < 2^24) and
+// their Euclidean norm rounded up (for the filter's Cauchy-Schwarz error bound) at slot NC.
 template <int B>
 __global__ void __launch_bounds__(256) pool_coeff_kernel(const uint8_t *__restrict__ img, int32_t N,
                                                          int32_t L, int32_t A,
                                                          const int32_t *__restrict__ kept,
                                                          const unsigned long long *__restrict__ d_nk,
-                                                         int64_t n_slots, float *__restrict__ Dc) {
+                                                         int64_t n_slots, float *__restrict__ Dc,
+                                                         unsigned int *__restrict__ d_dnmax) {
     using Cf = FCfg<B>;
     __shared__ int dsm[8][Cf::n];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -205,88 +208,91 @@ __global__ void __launch_bounds__(256) pool_coeff_kernel(const uint8_t *__restri
         const int i = p / B, j = p % B;
         const uint8_t *q = img + (y + 2 * i) * N + x + 2 * j;
         const int v = (int)q[0] + (int)q[1] + (int)q[N] + (int)q[N + 1];
-        dsm[warp][p] = v - 510;
+        dsm[warp][p] = v;
         sd += v;
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) sd += __shfl_xor_sync(0xffffffffu, sd, o);
     __syncwarp();
+    for (int p = lane; p < Cf::n; p += 32) dsm[warp][p] = Cf::n * dsm[warp][p] - sd;
+    __syncwarp();
+    double nrm = 0.0;
     for (int q = lane; q < Cf::NC; q += 32) {
         const int o = q >> 3, comp = q & 7, ob = orb_base(B) + o;
         int acc = 0;
 #pragma unroll
         for (int h = 0; h < 8; ++h) acc += c_tab[h][comp] * dsm[warp][c_orb_pts[ob][h]];
         rec[q] = (float)acc;
+        nrm += (double)acc * (double)acc;
     }
-    if (lane == 0) rec[Cf::NC] = (float)sd;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) nrm += __shfl_xor_sync(0xffffffffu, nrm, o);
+    if (lane == 0) {
+        const float dn = __double2float_ru(sqrt(nrm) * (1.0 + 1e-12));
+        rec[Cf::NC] = dn;
+        atomicMax(d_dnmax, __float_as_uint(dn));  // non-negative floats order as integers
+    }
     for (int q = Cf::NC + 1 + lane; q < Cf::NCS; q += 32) rec[q] = 0.f;
 }
 
 cudaError_t launch_pool_coeff(const uint8_t *img, int32_t N, int32_t B, int32_t L, int32_t A,
                               const int32_t *kept, const unsigned long long *d_nk, int64_t n_slots,
-                              float *Dc, cudaStream_t st) {
+                              float *Dc, unsigned int *d_dnmax, cudaStream_t st) {
     if (n_slots == 0) return cudaSuccess;
     const unsigned blocks = (unsigned)((n_slots + 7) / 8);
     switch (B) {
-    case 2: pool_coeff_kernel<2><<<blocks, 256, 0, st>>>(img, N, L, A, kept, d_nk, n_slots, Dc); break;
-    case 4: pool_coeff_kernel<4><<<blocks, 256, 0, st>>>(img, N, L, A, kept, d_nk, n_slots, Dc); break;
-    case 8: pool_coeff_kernel<8><<<blocks, 256, 0, st>>>(img, N, L, A, kept, d_nk, n_slots, Dc); break;
+    case 2: pool_coeff_kernel<2><<<blocks, 256, 0, st>>>(img, N, L, A, kept, d_nk, n_slots, Dc, d_dnmax); break;
+    case 4: pool_coeff_kernel<4><<<blocks, 256, 0, st>>>(img, N, L, A, kept, d_nk, n_slots, Dc, d_dnmax); break;
+    case 8: pool_coeff_kernel<8><<<blocks, 256, 0, st>>>(img, N, L, A, kept, d_nk, n_slots, Dc, d_dnmax); break;
     default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();
 }
 
-// U[tile][j][dl] = fp32 of (s_j^2 C/16 - (s_j/2) n 128 (SD - 510 n)); +inf on pad slots
-__global__ void fourier_u_kernel(const float *__restrict__ Dc, int32_t nc, int32_t ncs,
-                                 const int64_t *__restrict__ C, int32_t n_k, int64_t n_slots,
-                                 int32_t n, const SList spos, int32_t nsp, float *__restrict__ U) {
+// U[tile][j][dl] = fp32 of t2_j = (s_j s_j)(C/16); +inf on pad slots (never admitted)
+__global__ void fourier_u_kernel(const int64_t *__restrict__ C, int32_t n_k, int64_t n_slots,
+                                 const SList spos, int32_t nsp, float *__restrict__ U) {
     const int64_t d = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (d >= n_slots) return;
     const int64_t tile = d / kTileD, dl = d % kTileD;
     const double c16 = __dmul_rn(0.0625, (double)C[d]);
-    const double K2 = 128.0 * ((double)Dc[d * ncs + nc] - 510.0 * n);
     for (int j = 0; j < nsp; ++j) {
-        float u = INFINITY;
-        if (d < n_k) {
-            const double s = spos.s[j];
-            const double t2 = __dmul_rn(__dmul_rn(s, s), c16);
-            u = __double2float_rn(t2 - 0.5 * s * (double)n * K2);
-        }
-        U[(tile * nsp + j) * kTileD + dl] = u;
+        const double s = spos.s[j];
+        U[(tile * nsp + j) * kTileD + dl] =
+            d < n_k ? __double2float_rn(__dmul_rn(__dmul_rn(s, s), c16)) : INFINITY;
     }
 }
 
 // ------------------------------------------------------------------------------ range prep
 struct RangeMeta {
     double A;       // n SRR - SR^2 (exact)
-    double margin;  // filter margin in e units (without the K1 term)
-    double K1;      // 510 (SR - 128 n) + 65280 n
-    int32_t SR;
+    double margin;  // filter margin in e units (rounding of the fp32 score + binary64 slack)
+    float cr;       // Cauchy-Schwarz factor: |m8_f - 8 Bq_max| <= cr * |dh|_2
     int32_t pad;
 };
 
-// Thread per range: moments, centred coefficients rh (component-major over ranges: Rc[q][r]),
-// and the rigorous fp32 error margin of the search filter (DESIGN.md §"Exactness").
+// Thread per range: moments, centred coefficients rh of R - 128 (component-major over ranges:
+// Rc[q][r]) and the per-range constants of the filter's rigorous error bound (DESIGN.md
+// §"Exactness").  Because sum_p Dt = 0, sum_p (R(p) - 128) Dt(f_k p) = Bq_k.
 template <int B>
 __global__ void fourier_range_kernel(const uint8_t *__restrict__ img, int32_t N,
                                      const int2 *__restrict__ ranges, int32_t n_r, int32_t r_stride,
-                                     double smax, double cmax, float *__restrict__ Rc,
+                                     double smax, double t2max, double dnmax, float *__restrict__ Rc,
                                      RangeMeta *__restrict__ meta) {
     using Cf = FCfg<B>;
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= n_r) return;
     const int2 rr = ranges[r];
     int R[Cf::n];
-    long long sr = 0, srr = 0, sabs = 0;
+    long long sr = 0, srr = 0;
 #pragma unroll
     for (int p = 0; p < Cf::n; ++p) {
         const int v = img[(size_t)(rr.y + p / B) * N + rr.x + p % B];
         sr += v;
         srr += v * v;
         R[p] = v - 128;
-        sabs += R[p] < 0 ? -R[p] : R[p];
     }
-    double S_r = 0.0;
+    double nr2 = 0.0;
     for (int o = 0; o < Cf::nO; ++o) {
         const int ob = orb_base(B) + o;
         const int Hm = c_orb_H[ob];
@@ -297,23 +303,22 @@ __global__ void fourier_range_kernel(const uint8_t *__restrict__ img, int32_t N,
             for (int h = 0; h < 8; ++h)
                 if (Hm >> h & 1) acc += c_tab[h][comp] * R[c_orb_pts[ob][h]];
             Rc[(size_t)(o * 8 + comp) * r_stride + r] = (float)acc;
-            S_r += fabs((double)acc);
+            nr2 += (double)acc * (double)acc;
         }
     }
-    const double n = (double)Cf::n;
     const double u = 5.9604644775390625e-08;  // 2^-24
+    const double nr = sqrt(nr2) * (1.0 + 1e-12);
+    // every product feeding 8 Bq_k is rh_q dh_pi(q) with weight 1 or 2 (pi a permutation), so
+    // sum |terms| <= 2 |rh|_2 |dh|_2; fp32 dot products + combination: gamma_{2 nO + 8}
+    const double cr = (2.0 * Cf::nO + 8.0) * 1.02 * u * 2.0 * nr;
     const double hs = 0.5 * smax;
-    // |8 SRD'_f - 8 SRD'| <= (2 nO + 8) 1.01 u * 16320 S_r   (every |dh| <= 8 * 510 = 4080)
-    const double E8 = (2.0 * Cf::nO + 8.0) * 1.01 * u * 16320.0 * S_r;
-    const double beta = hs * n / 8.0;
+    const double m8max = 2.0 * nr * dnmax * 1.01 + cr * dnmax;  // |m8 + cr dn| bound
     const double A = (double)((long long)Cf::n * srr - sr * sr);
-    const double mag = beta * 8.0 * 510.0 * (double)sabs + hs * (double)sr * 1020.0 * n +
-                       smax * smax * cmax * 0.0625 + hs * n * 128.0 * 510.0 * n + A;
     RangeMeta m;
     m.A = A;
-    m.margin = beta * E8 + 8.0 * u * mag + 1e-6;
-    m.K1 = 510.0 * (double)(sr - 128 * (long long)Cf::n) + 65280.0 * n;
-    m.SR = (int32_t)sr;
+    // fp32: hs8 and t2 rounded, two FFMA roundings -> 4u (hs |m8p|/8 + t2); binary64 slack
+    m.margin = 4.0 * u * (hs * m8max * 0.125 + t2max) + 1e-12 * (A + hs * m8max * 0.125 + t2max) + 1e-30;
+    m.cr = __double2float_ru(cr);
     m.pad = 0;
     meta[r] = m;
 }
@@ -352,20 +357,9 @@ __device__ __forceinline__ void fmbar_wait(uint64_t *bar, uint32_t parity) {
     }
 }
 
-struct FBest {
-    double e;
-    int32_t d, kj;
-};
-__device__ __forceinline__ bool flex_less(double e, int32_t d, int32_t kj, const FBest &b) {
-    if (e < b.e) return true;
-    if (e > b.e) return false;
-    if (d != b.d) return d < b.d;
-    return kj < b.kj;
-}
-
 struct FSearchParams {
     const float *Dc;       // [n_slots][NCS]
-    const float *U;        // [n_tiles][nsp][128]
+    const float *U;        // [n_tiles][nsp][128]  t2_j
     const int64_t *C;      // [n_slots]
     const float *Rc;       // [NC][r_stride]
     const RangeMeta *meta; // [n_r]
@@ -378,28 +372,33 @@ struct FSearchParams {
     unsigned long long *exact_count;
 };
 
-template <int B, int NSP>
-struct FRange {
-    float rc[FCfg<B>::NC];
-    float alpha[NSP];  // (s_j / 2) SR
-    float thr[NSP];    // best - A + margin + (s_j/2) n K1, rounded up
-    FBest best;
-    double A, margin, K1;
-    int32_t SR;
-    bool valid;
+// cold per-range state, in shared memory (touched only by the exact path)
+struct FCold {
+    double A, margin, best_e;
+    int32_t best_d, best_kj;
 };
 
-// exact path of one (range, domain): all 8 SRD_k in exact integer arithmetic (binary64 on
-// integers < 2^53), lowest argmax k*, canonical binary64 score for every s > 0, lexicographic
-// update, threshold refresh.
+__device__ __forceinline__ bool flex_less(double e, int32_t d, int32_t kj, double be, int32_t bd,
+                                          int32_t bkj) {
+    if (e < be) return true;
+    if (e > be) return false;
+    if (d != bd) return d < bd;
+    return kj < bkj;
+}
+
+// Exact path of one (range, domain): the 8 values 8 Bq_k from the same coefficients in binary64
+// (exact: integers < 2^53), k* = lowest argmax, Bq = 8 Bq_{k*} / 8, canonical binary64 score
+// e = (A - (s/2) Bq) + (s s)(C/16) for every s > 0, lexicographic first-min update, and the
+// refreshed fp32 thresholds thr_j = RU(best - A + margin).
 template <int B, int NSP>
-__device__ __forceinline__ void fexact(const FSearchParams &P, FRange<B, NSP> &R, const float *rec,
-                                    int32_t d) {
+__device__ __forceinline__ void fexact(const FSearchParams &P, const float (&rc)[FCfg<B>::NC],
+                                       const float *rec, int32_t d, FCold &cold, float (&thr)[NSP]) {
     using Cf = FCfg<B>;
     double c[4] = {0, 0, 0, 0}, C2[2][2] = {{0, 0}, {0, 0}};
+#pragma unroll
     for (int o = 0; o < Cf::nO; ++o) {
         const float *dh = rec + o * 8;
-        const float *rh = R.rc + o * 8;
+        const float *rh = rc + o * 8;
 #pragma unroll
         for (int q = 0; q < 4; ++q) c[q] = fma((double)rh[q], (double)dh[q], c[q]);
 #pragma unroll
@@ -420,29 +419,28 @@ __device__ __forceinline__ void fexact(const FSearchParams &P, FRange<B, NSP> &R
 #pragma unroll
     for (int k = 1; k < 8; ++k)
         if (v[k] > vm) { vm = v[k]; ks = k; }
-    const double SD = (double)rec[Cf::NC];
-    const double K2 = 128.0 * (SD - 510.0 * Cf::n);
-    const double srd = vm * 0.125 + R.K1 + K2;  // exact integer SRD_{k*}
-    const double Bq = __dsub_rn(__dmul_rn((double)Cf::n, srd), __dmul_rn((double)R.SR, SD));
+    const double Bq = vm * 0.125;  // exact: vm = 8 Bq_{k*}
     const double c16 = __dmul_rn(0.0625, (double)P.C[d]);
+    double be = cold.best_e;
+    int32_t bd = cold.best_d, bkj = cold.best_kj;
     for (int jj = 0; jj < P.nsp; ++jj) {
         const double s = P.spos[jj];
         const double hs = __dmul_rn(0.5, s);
         const double t2 = __dmul_rn(__dmul_rn(s, s), c16);
-        const double e = __dadd_rn(__dsub_rn(R.A, __dmul_rn(hs, Bq)), t2);
+        const double e = __dadd_rn(__dsub_rn(cold.A, __dmul_rn(hs, Bq)), t2);
         const int32_t kj = (ks << 8) | P.jpos[jj];
-        if (flex_less(e, d, kj, R.best)) { R.best.e = e; R.best.d = d; R.best.kj = kj; }
+        if (flex_less(e, d, kj, be, bd, bkj)) { be = e; bd = d; bkj = kj; }
     }
-    const double base = __dadd_rn(__dsub_rn(R.best.e, R.A), R.margin);
+    cold.best_e = be;
+    cold.best_d = bd;
+    cold.best_kj = bkj;
+    const float t = fminf(__double2float_ru(__dadd_rn(__dsub_rn(be, cold.A), cold.margin)), FLT_MAX);
 #pragma unroll
-    for (int jj = 0; jj < NSP; ++jj) {
-        const double hsn = 0.5 * (jj < P.nsp ? P.spos[jj] : 0.0) * (double)Cf::n;
-        R.thr[jj] = jj < P.nsp ? fminf(__double2float_ru(base + hsn * R.K1), FLT_MAX) : -FLT_MAX;
-    }
+    for (int jj = 0; jj < NSP; ++jj) thr[jj] = jj < P.nsp ? t : -FLT_MAX;
 }
 
 template <int B, int NSP, int RPT>
-__global__ void __launch_bounds__(256, 1) fsearch_kernel(const __grid_constant__ FSearchParams P) {
+__global__ void __launch_bounds__(256, (B == 8 ? 1 : 2)) fsearch_kernel(const __grid_constant__ FSearchParams P) {
     using Cf = FCfg<B>;
     constexpr int NC = Cf::NC, NCS = Cf::NCS;
     constexpr int TILE_F = kTileD * NCS;                  // floats of one tile's records
@@ -452,7 +450,8 @@ __global__ void __launch_bounds__(256, 1) fsearch_kernel(const __grid_constant__
     extern __shared__ __align__(128) unsigned char smem[];
     float *Ds = reinterpret_cast<float *>(smem);          // [2][STAGE_F]
     float *Us = Ds + 2 * STAGE_F;                         // [2][USTAGE_F]
-    uint64_t *bar = reinterpret_cast<uint64_t *>(Us + 2 * USTAGE_F);
+    FCold *cold = reinterpret_cast<FCold *>(Us + 2 * USTAGE_F);  // [RPT][256]
+    uint64_t *bar = reinterpret_cast<uint64_t *>(cold + RPT * 256);
 
     const int split = blockIdx.y;
     const int t0 = split * P.tiles_per_split;
@@ -479,48 +478,38 @@ __global__ void __launch_bounds__(256, 1) fsearch_kernel(const __grid_constant__
         if (nstages > 1) issue(1);
     }
 
-    // ---- this thread's RPT ranges: coefficients in registers, thresholds
-    FRange<B, NSP> Rg[RPT];
+    // ---- this thread's RPT ranges: coefficients + error factor + thresholds in registers
+    float rc[RPT][NC], cr[RPT], thr[RPT][NSP];
     const int rbase = (blockIdx.x * 256 + threadIdx.x) * RPT;
 #pragma unroll
     for (int q = 0; q < RPT; ++q) {
         const int r = rbase + q;
-        FRange<B, NSP> &R = Rg[q];
-        R.valid = r < P.n_r;
-        const int rr = R.valid ? r : 0;
+        const bool valid = r < P.n_r;
+        const int rr = valid ? r : 0;
 #pragma unroll
-        for (int c = 0; c < NC; ++c) R.rc[c] = R.valid ? P.Rc[(size_t)c * P.r_stride + rr] : 0.f;
+        for (int c = 0; c < NC; ++c) rc[q][c] = valid ? P.Rc[(size_t)c * P.r_stride + rr] : 0.f;
         const RangeMeta m = P.meta[rr];
-        R.A = m.A;
-        R.margin = m.margin;
-        R.K1 = m.K1;
-        R.SR = m.SR;
-        if (P.has_zero) {
-            R.best.e = R.A;
-            R.best.d = 0;
-            R.best.kj = P.j_zero;
+        cr[q] = m.cr;
+        FCold &cd = cold[q * 256 + threadIdx.x];
+        cd.A = m.A;
+        cd.margin = m.margin;
+        if (P.has_zero) {  // s = 0 gives e = A for every (domain, isometry): first is (0, 0, j0)
+            cd.best_e = m.A;
+            cd.best_d = 0;
+            cd.best_kj = P.j_zero;
         } else {
-            R.best.e = INFINITY;
-            R.best.d = INT_MAX;
-            R.best.kj = INT_MAX;
+            cd.best_e = INFINITY;
+            cd.best_d = INT_MAX;
+            cd.best_kj = INT_MAX;
         }
+        const float t0v = P.has_zero ? fminf(__double2float_ru(m.margin), FLT_MAX) : FLT_MAX;
 #pragma unroll
-        for (int jj = 0; jj < NSP; ++jj) {
-            const double s = jj < P.nsp ? P.spos[jj] : 0.0;
-            const double hs = 0.5 * s;
-            R.alpha[jj] = __double2float_rn(hs * (double)m.SR);
-            if (!R.valid || jj >= P.nsp)
-                R.thr[jj] = -FLT_MAX;
-            else if (P.has_zero)
-                R.thr[jj] = fminf(__double2float_ru(R.margin + hs * Cf::n * R.K1), FLT_MAX);
-            else
-                R.thr[jj] = FLT_MAX;
-        }
+        for (int jj = 0; jj < NSP; ++jj) thr[q][jj] = (valid && jj < P.nsp) ? t0v : -FLT_MAX;
     }
-    float nbeta[NSP];  // -(s_j/2) n / 8
+    float nhs8[NSP];  // -(s_j / 2) / 8
 #pragma unroll
     for (int jj = 0; jj < NSP; ++jj)
-        nbeta[jj] = -__double2float_rn(0.5 * (jj < P.nsp ? P.spos[jj] : 0.0) * Cf::n * 0.125);
+        nhs8[jj] = -__double2float_rn(0.0625 * (jj < P.nsp ? P.spos[jj] : 0.0));
     unsigned n_exact = 0;
 
     for (int s = 0; s < nstages; ++s) {
@@ -548,22 +537,23 @@ __global__ void __launch_bounds__(256, 1) fsearch_kernel(const __grid_constant__
                     const float4 db = *reinterpret_cast<const float4 *>(rec + o * 8 + 4);
 #pragma unroll
                     for (int q = 0; q < RPT; ++q) {
-                        const float *rh = Rg[q].rc + o * 8;
+                        const float *rh = rc[q] + o * 8;
                         acc[q][0] = fmaf(rh[0], da.x, acc[q][0]);
                         acc[q][1] = fmaf(rh[1], da.y, acc[q][1]);
                         acc[q][2] = fmaf(rh[2], da.z, acc[q][2]);
                         acc[q][3] = fmaf(rh[3], da.w, acc[q][3]);
-                        // C2[i][j] += dh(i,0) rh(j,0) + dh(i,1) rh(j,1);  dh(0,*) = db.x,y ; dh(1,*) = db.z,w
+                        // C2[i][j] += dh(i,0) rh(j,0) + dh(i,1) rh(j,1); dh(0,*) = db.x,y; dh(1,*) = db.z,w
                         acc[q][4] = fmaf(db.x, rh[4], fmaf(db.y, rh[5], acc[q][4]));  // C00
                         acc[q][5] = fmaf(db.x, rh[6], fmaf(db.y, rh[7], acc[q][5]));  // C01
                         acc[q][6] = fmaf(db.z, rh[4], fmaf(db.w, rh[5], acc[q][6]));  // C10
                         acc[q][7] = fmaf(db.z, rh[6], fmaf(db.w, rh[7], acc[q][7]));  // C11
                     }
                 }
-                const float sd = rec[NC];
+                const float dn = rec[NC];
                 float uj[NSP];
 #pragma unroll
                 for (int jj = 0; jj < NSP; ++jj) uj[jj] = jj < P.nsp ? Ut[jj * kTileD + dl] : 0.f;
+                unsigned pass = 0;
 #pragma unroll
                 for (int q = 0; q < RPT; ++q) {
                     const float *c = acc[q];
@@ -575,17 +565,20 @@ __global__ void __launch_bounds__(256, 1) fsearch_kernel(const __grid_constant__
                     const float v1 = fmaf(2.f, fabsf(t1v), p01 - p23);
                     const float v4 = fmaf(2.f, fabsf(t4v), m01 + m23);
                     const float v5 = fmaf(2.f, fabsf(t5v), m01 - m23);
-                    const float m8 = fmaxf(fmaxf(v0, v1), fmaxf(v4, v5));
-                    bool pass = false;
+                    const float m8 = fmaxf(fmaxf(v0, v1), fmaxf(v4, v5));  // ~ 8 max_k Bq_k
+                    const float m8p = fmaf(cr[q], dn, m8);                 // >= 8 max_k Bq_k
+                    bool pq = false;
 #pragma unroll
-                    for (int jj = 0; jj < NSP; ++jj) {
-                        const float g = fmaf(nbeta[jj], m8, fmaf(Rg[q].alpha[jj], sd, uj[jj]));
-                        pass = pass || (g <= Rg[q].thr[jj]);
-                    }
-                    if (pass) {
-                        fexact<B, NSP>(P, Rg[q], rec, dbase + dl);
-                        ++n_exact;
-                    }
+                    for (int jj = 0; jj < NSP; ++jj) pq = pq || (fmaf(nhs8[jj], m8p, uj[jj]) <= thr[q][jj]);
+                    pass |= (unsigned)pq << q;
+                }
+                if (pass) {
+#pragma unroll
+                    for (int q = 0; q < RPT; ++q)
+                        if (pass >> q & 1) {
+                            fexact<B, NSP>(P, rc[q], rec, dbase + dl, cold[q * 256 + threadIdx.x], thr[q]);
+                            ++n_exact;
+                        }
                 }
             }
         }
@@ -599,10 +592,11 @@ __global__ void __launch_bounds__(256, 1) fsearch_kernel(const __grid_constant__
     for (int q = 0; q < RPT; ++q) {
         const int r = rbase + q;
         if (r < P.n_r) {
+            const FCold &cd = cold[q * 256 + threadIdx.x];
             Partial pb;
-            pb.e = Rg[q].best.e;
-            pb.d = Rg[q].best.d;
-            pb.kj = Rg[q].best.kj;
+            pb.e = cd.best_e;
+            pb.d = cd.best_d;
+            pb.kj = cd.best_kj;
             P.part[(size_t)r * P.nsplit + split] = pb;
         }
     }
@@ -618,7 +612,8 @@ static cudaError_t launch_fsearch_t(const FSearchParams &p, cudaStream_t st) {
     using Cf = FCfg<B>;
     constexpr int TILE_F = kTileD * Cf::NCS;
     constexpr int TPS = (TILE_F * 4 >= 24 * 1024) ? 1 : (24 * 1024) / (TILE_F * 4);
-    constexpr size_t SMEM = (size_t)(2 * TPS * TILE_F + 2 * TPS * NSP * kTileD) * 4 + 64;
+    constexpr size_t SMEM = (size_t)(2 * TPS * TILE_F + 2 * TPS * NSP * kTileD) * 4 +
+                            sizeof(FCold) * RPT * 256 + 64;
     static bool attr = false;
     if (!attr) {
         cudaError_t e = cudaFuncSetAttribute(fsearch_kernel<B, NSP, RPT>,
@@ -637,17 +632,12 @@ int fourier_rpt(int32_t B, int32_t nsp) {
 }
 
 template <int B>
+constexpr int rpt_of() { return B == 2 ? 4 : (B == 4 ? 2 : 1); }
+
+template <int B>
 static cudaError_t launch_fsearch_b(const FSearchParams &p, cudaStream_t st) {
-    if (p.nsp <= 1) {
-        if (fourier_rpt(B, 1) == 4) return launch_fsearch_t<B, 1, 4>(p, st);
-        if (fourier_rpt(B, 1) == 2) return launch_fsearch_t<B, 1, 2>(p, st);
-        return launch_fsearch_t<B, 1, 1>(p, st);
-    }
-    if (p.nsp <= 2) {
-        if (fourier_rpt(B, 2) == 4) return launch_fsearch_t<B, 2, 4>(p, st);
-        if (fourier_rpt(B, 2) == 2) return launch_fsearch_t<B, 2, 2>(p, st);
-        return launch_fsearch_t<B, 2, 1>(p, st);
-    }
+    if (p.nsp <= 1) return launch_fsearch_t<B, 1, rpt_of<B>()>(p, st);
+    if (p.nsp <= 2) return launch_fsearch_t<B, 2, rpt_of<B>()>(p, st);
     return launch_fsearch_t<B, 16, 1>(p, st);
 }
 
@@ -655,27 +645,26 @@ static cudaError_t launch_fsearch_b(const FSearchParams &p, cudaStream_t st) {
 cudaError_t launch_fourier_level(int32_t B, const uint8_t *img, int32_t N, const int2 *ranges,
                                  int32_t n_r, const float *Dc, const int64_t *C, int32_t n_k,
                                  int32_t n_tiles, int32_t nsplit, int32_t tiles_per_split,
-                                 const SearchParams &sp, float *Rc, int32_t r_stride, void *meta,
-                                 float *U, cudaStream_t st) {
+                                 const SearchParams &sp, double dnmax, float *Rc, int32_t r_stride,
+                                 void *meta, float *U, cudaStream_t st) {
     if (n_r == 0) return cudaSuccess;
+    const double t2max = sp.smax * sp.smax * sp.cmax * 0.0625 * (1.0 + 1e-12);
     const int64_t n_slots = (int64_t)n_tiles * kTileD;
     SList sl;
     memcpy(sl.s, sp.spos, sizeof sl.s);
-    const int ncs = fourier_record_stride(B);
-    const int nc = 8 * n_orbits(B);
     RangeMeta *m = reinterpret_cast<RangeMeta *>(meta);
     const unsigned rb = (unsigned)((n_r + 127) / 128);
     switch (B) {
-    case 2: fourier_range_kernel<2><<<rb, 128, 0, st>>>(img, N, ranges, n_r, r_stride, sp.smax, sp.cmax, Rc, m); break;
-    case 4: fourier_range_kernel<4><<<rb, 128, 0, st>>>(img, N, ranges, n_r, r_stride, sp.smax, sp.cmax, Rc, m); break;
-    case 8: fourier_range_kernel<8><<<rb, 128, 0, st>>>(img, N, ranges, n_r, r_stride, sp.smax, sp.cmax, Rc, m); break;
+    case 2: fourier_range_kernel<2><<<rb, 128, 0, st>>>(img, N, ranges, n_r, r_stride, sp.smax, t2max, dnmax, Rc, m); break;
+    case 4: fourier_range_kernel<4><<<rb, 128, 0, st>>>(img, N, ranges, n_r, r_stride, sp.smax, t2max, dnmax, Rc, m); break;
+    case 8: fourier_range_kernel<8><<<rb, 128, 0, st>>>(img, N, ranges, n_r, r_stride, sp.smax, t2max, dnmax, Rc, m); break;
     default: return cudaErrorInvalidValue;
     }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     if (sp.nsp > 0 && n_slots > 0) {
-        fourier_u_kernel<<<(unsigned)((n_slots + 255) / 256), 256, 0, st>>>(
-            Dc, nc, ncs, C, n_k, n_slots, B * B, sl, sp.nsp, U);
+        fourier_u_kernel<<<(unsigned)((n_slots + 255) / 256), 256, 0, st>>>(C, n_k, n_slots, sl,
+                                                                            sp.nsp, U);
         e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }

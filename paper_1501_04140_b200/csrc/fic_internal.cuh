@@ -38,7 +38,8 @@ struct Pool {
     int direct = 0;       // 1: this pool feeds the direct kernel (Dt built), 0: Fourier (Dc)
     int32_t *SD = nullptr;
     int64_t *C = nullptr;
-    unsigned long long *d_misc = nullptr;  // [0] = n_kept, [1] = Cmax
+    unsigned long long *d_misc = nullptr;  // [0] = n_kept, [1] = Cmax, [2] = max |dh|_2 (float bits)
+    double dnmax = 0.0;
     Buf b_keys, b_keep, b_kept, b_Dt, b_SDf, b_SD, b_C, b_misc, b_Dc;
     int device = 0;
 };
@@ -130,11 +131,11 @@ int fourier_rpt(int32_t B, int32_t nsp);
 int fourier_nsplit_hint(int32_t B, int32_t nsp, int64_t n_r, int64_t n_tiles, int num_sms);
 cudaError_t launch_pool_coeff(const uint8_t *img, int32_t N, int32_t B, int32_t L, int32_t A,
                               const int32_t *kept, const unsigned long long *d_nk, int64_t n_slots,
-                              float *Dc, cudaStream_t st);
+                              float *Dc, unsigned int *d_dnmax, cudaStream_t st);
 cudaError_t launch_fourier_level(int32_t B, const uint8_t *img, int32_t N, const int2 *ranges,
                                  int32_t n_r, const float *Dc, const int64_t *C, int32_t n_k,
                                  int32_t n_tiles, int32_t nsplit, int32_t tiles_per_split,
-                                 const SearchParams &sp, float *Rc, int32_t r_stride, void *meta,
-                                 float *U, cudaStream_t st);
+                                 const SearchParams &sp, double dnmax, float *Rc, int32_t r_stride,
+                                 void *meta, float *U, cudaStream_t st);
 
 }  // namespace fic
