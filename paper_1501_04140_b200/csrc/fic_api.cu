@@ -35,7 +35,7 @@ struct fic_ctx {
     std::vector<fic_level_stats> stats;
     cudaEvent_t ev[fic::kMaxLevels][5] = {};
     int64_t launches = 0;
-    int force_direct = 0;  // env FIC_SEARCH=direct: direct kernel at every B (A/B checks)
+    int search_mode = 0;  // env FIC_SEARCH = tc (default) | fourier | direct (A/B checks)
     Buf b_rc, b_meta, b_u;  // libfic kernels enqueued (for fic_level_stats.kernel_launches)  // pool start, search start, search end, finalize end, pool end
 };
 
@@ -94,6 +94,7 @@ void free_buf(Buf &b) {
 void free_pool(Pool &P) {
     free_buf(P.b_keys); free_buf(P.b_keep); free_buf(P.b_kept); free_buf(P.b_Dt);
     free_buf(P.b_SDf); free_buf(P.b_SD); free_buf(P.b_C); free_buf(P.b_misc); free_buf(P.b_Dc);
+    free_buf(P.b_Dtc);
 }
 
 bool pow2(int32_t v) { return v > 0 && (v & (v - 1)) == 0; }
@@ -131,9 +132,12 @@ fic_status pool_enqueue(fic_ctx *ctx, Pool &P, const uint8_t *img, int32_t N, in
     CK(grow(ctx, P.b_keys, sizeof(int64_t) * P.n_c));
     CK(grow(ctx, P.b_keep, P.n_c + 16));
     CK(grow(ctx, P.b_kept, sizeof(int32_t) * P.n_c));
-    P.direct = (ctx->force_direct || fic::fourier_record_stride(B) == 0) ? 1 : 0;
-    if (P.direct) CK(grow(ctx, P.b_Dt, sizeof(float) * slots * P.n));
-    else CK(grow(ctx, P.b_Dc, sizeof(float) * slots * fic::fourier_record_stride(B)));
+    P.mode = ctx->search_mode;
+    if (P.mode == 0 && !fic::tc_supported(B)) P.mode = 2;
+    if (P.mode == 1 && fic::fourier_record_stride(B) == 0) P.mode = 2;
+    if (P.mode == 2) CK(grow(ctx, P.b_Dt, sizeof(float) * slots * P.n));
+    if (P.mode == 1) CK(grow(ctx, P.b_Dc, sizeof(float) * slots * fic::fourier_record_stride(B)));
+    if (P.mode == 0) CK(grow(ctx, P.b_Dtc, fic::tc_pool_bytes(B, tiles_max)));
     CK(grow(ctx, P.b_SDf, sizeof(float) * slots));
     CK(grow(ctx, P.b_SD, sizeof(int32_t) * slots));
     CK(grow(ctx, P.b_C, sizeof(int64_t) * slots));
@@ -141,8 +145,9 @@ fic_status pool_enqueue(fic_ctx *ctx, Pool &P, const uint8_t *img, int32_t N, in
     CK(grow(ctx, ctx->b_blocksum, sizeof(int64_t) * fic::select_blocksum_len(P.n_c)));
     P.keys = ptr<int64_t>(P.b_keys); P.keep = ptr<uint8_t>(P.b_keep);
     P.kept = ptr<int32_t>(P.b_kept); P.SDf = ptr<float>(P.b_SDf);
-    P.Dt = P.direct ? ptr<float>(P.b_Dt) : nullptr;
-    P.Dc = P.direct ? nullptr : ptr<float>(P.b_Dc);
+    P.Dt = P.mode == 2 ? ptr<float>(P.b_Dt) : nullptr;
+    P.Dc = P.mode == 1 ? ptr<float>(P.b_Dc) : nullptr;
+    P.Dtc = P.mode == 0 ? ptr<uint8_t>(P.b_Dtc) : nullptr;
     P.SD = ptr<int32_t>(P.b_SD); P.C = ptr<int64_t>(P.b_C);
     P.d_misc = ptr<unsigned long long>(P.b_misc);
     cudaStream_t st = ctx->stream;
@@ -154,8 +159,10 @@ fic_status pool_enqueue(fic_ctx *ctx, Pool &P, const uint8_t *img, int32_t N, in
                                 P.keep, st));
     CK(fic::launch_select_index(P.keep, P.n_c, ptr<int64_t>(ctx->b_blocksum), P.kept, &P.d_misc[0],
                                 st));
-    if (P.direct)
+    if (P.mode == 2)
         CK(fic::launch_pool_gather(img, N, B, L, P.A, P.kept, &P.d_misc[0], tiles_max, P.Dt, st));
+    else if (P.mode == 0)
+        CK(fic::launch_pool_tc(img, N, B, L, P.A, P.kept, &P.d_misc[0], tiles_max, P.Dtc, st));
     else
         CK(fic::launch_pool_coeff(img, N, B, L, P.A, P.kept, &P.d_misc[0], slots, P.Dc,
                                   reinterpret_cast<unsigned int *>(&P.d_misc[2]), st));
@@ -227,8 +234,10 @@ fic_status level_enqueue(fic_ctx *ctx, const Pool &P, const uint8_t *img, const 
     }
     sp.cmax = (double)P.cmax;
     const int64_t slots = P.n_tiles * fic::kTileD;
-    if (P.direct)
+    if (P.mode == 2)
         sp.nsplit = fic::search_nsplit_hint(P.B, n_r, P.n_tiles, ctx->num_sms);
+    else if (P.mode == 0)
+        sp.nsplit = fic::tc_nsplit_hint(P.B, n_r, P.n_tiles, ctx->num_sms);
     else
         sp.nsplit = fic::fourier_nsplit_hint(P.B, sp.nsp, n_r, P.n_tiles, ctx->num_sms);
     sp.tiles_per_split = (int32_t)((P.n_tiles + sp.nsplit - 1) / sp.nsplit);
@@ -238,14 +247,16 @@ fic_status level_enqueue(fic_ctx *ctx, const Pool &P, const uint8_t *img, const 
     sp.t2f = ptr<float>(ctx->b_t2f);
     sp.part = ptr<fic::Partial>(ctx->b_part);
     sp.exact_count = ptr<unsigned long long>(ctx->b_counts) + 8 + level_slot;
-    if (P.direct) {
+    if (P.mode == 2 || P.mode == 0) {
         fic::SList sl;
         memcpy(sl.s, sp.spos, sizeof sl.s);
         CK(fic::launch_t2f(P.C, (int32_t)P.n_k, slots, sl, sp.nsp, ptr<float>(ctx->b_t2f), st));
         if (sp.nsp > 0 && slots > 0) ctx->launches += 1;
         if (ctx->timing) CK(cudaEventRecord(ctx->ev[level_slot][1], st));
+        sp.t2f = ptr<float>(ctx->b_t2f);
         if (sp.nsp > 0) {
-            CK(fic::launch_search(P.B, sp.nsp, sp, st));
+            if (P.mode == 2) CK(fic::launch_search(P.B, sp.nsp, sp, st));
+            else CK(fic::launch_tc_search(P.B, sp, P.Dtc, slots, st));
             ctx->launches += 1;
         }
     } else {
@@ -324,7 +335,9 @@ fic_status fic_ctx_create(int32_t device, void *cuda_stream, fic_ctx **out) {
     if (e == cudaSuccess) e = fic::fourier_init();
     {
         const char *env = getenv("FIC_SEARCH");
-        ctx->force_direct = env && strcmp(env, "direct") == 0;
+        ctx->search_mode = 0;
+        if (env && strcmp(env, "fourier") == 0) ctx->search_mode = 1;
+        if (env && strcmp(env, "direct") == 0) ctx->search_mode = 2;
     }
     for (int l = 0; l < fic::kMaxLevels && e == cudaSuccess; ++l)
         for (int q = 0; q < 5 && e == cudaSuccess; ++q) e = cudaEventCreate(&ctx->ev[l][q]);

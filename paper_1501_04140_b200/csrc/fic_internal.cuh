@@ -34,13 +34,14 @@ struct Pool {
     uint8_t *keep = nullptr;
     int32_t *kept = nullptr;
     float *Dt = nullptr, *SDf = nullptr;
-    float *Dc = nullptr;  // D4-Fourier domain records [slots][NCS] (B <= 8), or null
-    int direct = 0;       // 1: this pool feeds the direct kernel (Dt built), 0: Fourier (Dc)
+    float *Dc = nullptr;    // D4-Fourier domain records [slots][NCS] (B <= 8), or null
+    uint8_t *Dtc = nullptr; // tcgen05 A operand: [tiles][chunks][128 x KCH] core-matrix u8, or null
+    int mode = 0;           // 0: tcgen05 (Dtc), 1: D4-Fourier CUDA cores (Dc), 2: direct FFMA (Dt)
     int32_t *SD = nullptr;
     int64_t *C = nullptr;
     unsigned long long *d_misc = nullptr;  // [0] = n_kept, [1] = Cmax, [2] = max |dh|_2 (float bits)
     double dnmax = 0.0;
-    Buf b_keys, b_keep, b_kept, b_Dt, b_SDf, b_SD, b_C, b_misc, b_Dc;
+    Buf b_keys, b_keep, b_kept, b_Dt, b_SDf, b_SD, b_C, b_misc, b_Dc, b_Dtc;
     int device = 0;
 };
 
@@ -122,6 +123,16 @@ cudaError_t launch_finalize(const FinalizeParams &p, cudaStream_t st);
 cudaError_t launch_merge_shards(const fic_record *in, const int64_t *d_counts, int32_t n_shards,
                                 int64_t stride, int64_t max_count, fic_record *out, cudaStream_t st);
 int search_nsplit_hint(int32_t B, int64_t n_r, int64_t n_tiles, int num_sms);
+
+// tcgen05 search (fic_tc.cu), B in {2, 4, 8, 16}
+int tc_supported(int B);
+size_t tc_pool_bytes(int B, int64_t n_tiles);
+int tc_nsplit_hint(int32_t B, int64_t n_r, int64_t n_tiles, int num_sms);
+cudaError_t launch_pool_tc(const uint8_t *img, int32_t N, int32_t B, int32_t L, int32_t A,
+                           const int32_t *kept, const unsigned long long *d_nk, int64_t n_tiles_max,
+                           uint8_t *Dtc, cudaStream_t st);
+cudaError_t launch_tc_search(int32_t B, const SearchParams &sp, const uint8_t *Dtc, int64_t n_slots,
+                             cudaStream_t st);
 
 // D4 group-Fourier search (fic_fourier.cu), B in {2, 4, 8}
 cudaError_t fourier_init();

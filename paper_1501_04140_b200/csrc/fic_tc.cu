@@ -1,0 +1,589 @@
+// fic_tc.cu -- the range x (domain, isometry) cross terms on the 5th-generation tensor cores
+// (tcgen05.mma kind::i8, accumulators in TMEM), fused with the score filter and the exact
+// first-min update.
+//
+// Contraction (exact, integer): SRD_k(r, d) = sum_p R_r(p) D'_d(f_k p)  (§2 lines 28-30)
+//   D'(p) = sum of the 4 pixels of the 2x2 cell p, so with the four polyphase sub-images
+//   P_ab(p) = I(y + 2i + a, x + 2j + b) of the raw 2B x 2B domain block:
+//   SRD_k = sum_{ab} sum_p Rperm_k(p) P_ab(p),  Rperm_k(f_k p) = R(p)   (scatter through f_k)
+//   i.e. one GEMM   S[m = domain][n = (range, k)] = sum_K A[m][K] B[n][K]
+//   with A = the 4 u8 polyphase planes of each domain (K = 4 B^2, zero-padded to a multiple of
+//   32) and B = the range scattered through the 8 isometries, replicated over the 4 planes.
+//   u8 x u8 products accumulate exactly in s32 (max 4 B^2 255^2 < 2^31 for B <= 16).
+// Epilogue (per TMEM lane = domain, per range): the 8 exact SRD_k, Bq = n max_k SRD_k - SR SD,
+//   an fp32 lower bound of every binary64 score with a rigorous margin, and -- only when the
+//   bound does not exclude the pair -- the canonical binary64 score and the lexicographic
+//   (e; dom, k, j) first-min update; the running best of each range is shared by the CTA's
+//   128 domain lanes through a shared-memory atomic threshold.
+//
+// Roles (10 warps): warp 0 = TMEM allocator + bulk-copy producer, warp 1 = MMA issuer (one
+// elected thread), warps 2..9 = epilogue (two warpgroups, each half of the ranges; warp w reads
+// TMEM lanes 32 (w % 4) ..).  Pipelines: A stages full/empty (producer <-> MMA), TMEM buffers
+// full/empty (MMA <-> epilogue), two accumulator buffers of N columns.
+#include <cfloat>
+#include <climits>
+#include <cstring>
+
+#include "fic_internal.cuh"
+
+namespace fic {
+
+// ------------------------------------------------------------------------------ configuration
+template <int B>
+struct TCfg {
+    static constexpr int n = B * B;
+    static constexpr int KP = ((4 * n + 31) / 32) * 32;    // K bytes (padded)
+    static constexpr int NR = (B == 16) ? 16 : 32;         // ranges per CTA
+    static constexpr int N = 8 * NR;                       // MMA N (columns per accumulator)
+    static constexpr int KCH = KP < 256 ? KP : 256;        // K bytes per pipeline stage
+    static constexpr int CH = KP / KCH;                    // stages per domain tile
+    static constexpr int STAGE_BYTES = kTileD * KCH;       // A bytes per stage
+    static constexpr int STAGES = (B == 16) ? 2 : (B == 8 ? 3 : 4);
+    static constexpr int B_BYTES = N * KP;                 // resident range operand
+    static constexpr int THREADS = 320;
+};
+
+constexpr uint32_t kTmemCols = 512;
+
+// ------------------------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t su32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void tmbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void tmbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void tmbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(bar)) : "memory");
+}
+__device__ __forceinline__ void tmbar_wait(uint64_t *bar, uint32_t parity) {
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+            : "=r"(done)
+            : "r"(su32(bar)), "r"(parity)
+            : "memory");
+    }
+}
+__device__ __forceinline__ void tbulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            su32(dst)),
+        "l"(src), "r"(bytes), "r"(su32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_commit(uint64_t *bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void tc_mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                          uint32_t accum) {
+    asm volatile(
+        "{ .reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p; }" ::"r"(
+            tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
+        : "memory");
+}
+__device__ __forceinline__ void tc_ld8(uint32_t taddr, uint32_t (&v)[8]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+        : "r"(taddr));
+}
+template <int O>
+__device__ __forceinline__ void tc_ld32(uint32_t taddr, uint32_t (&w)[64]) {
+    uint32_t *v = w + O;
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+        "%14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+          "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+          "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+        : "r"(taddr));
+}
+__device__ __forceinline__ void tc_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// K-major, no-swizzle canonical layout: 8-row x 16-byte core matrices; LBO = distance between
+// the two 16-byte K halves of one MMA (128 B here), SBO = distance between 8-row groups.
+__device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+    d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+    d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+    d |= (uint64_t)1 << 46;  // descriptor version (sm_100)
+    return d;                // base offset 0, lbo mode 0, layout SWIZZLE_NONE
+}
+// kind::i8 instruction descriptor: D s32, A u8, B u8, both K-major, M = 128, N
+__host__ __device__ constexpr uint32_t idesc_i8(int N) {
+    return (2u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+}
+// byte offset of element (row, kb) in a K-major no-swizzle operand with K bytes per row
+__host__ __device__ __forceinline__ uint32_t cm_off(int row, int kb, int K) {
+    return (uint32_t)((row >> 3) * (K / 16) * 128 + (kb >> 4) * 128 + (row & 7) * 16 + (kb & 15));
+}
+
+// GPU-side isometry source map (same derivation as fic_search.cu, reading R2)
+__device__ __forceinline__ void tiso_src(int B, int k, int i, int j, int &si, int &sj) {
+    const int b = B - 1;
+    if (k >= 4) j = b - j;
+    for (int r = 0; r < (k & 3); ++r) {
+        const int t = i;
+        i = b - j;
+        j = t;
+    }
+    si = i;
+    sj = j;
+}
+
+// orderable encoding of fp32 for atomicMin
+__device__ __forceinline__ uint32_t f2ord(float f) {
+    const uint32_t u = __float_as_uint(f);
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float ord2f(uint32_t o) {
+    return __uint_as_float((o & 0x80000000u) ? (o & 0x7fffffffu) : ~o);
+}
+
+// ------------------------------------------------------------------------------ pool (A operand)
+// Tile t, chunk c: 128 domains x KCH bytes in the core-matrix layout (one bulk copy per stage).
+// K byte kb of domain d = plane (kb / n) = (a, b) = (plane >> 1, plane & 1), pixel p = kb % n:
+// I(y + 2i + a, x + 2j + b); zero for kb >= 4n.
+template <int B>
+__global__ void __launch_bounds__(256) pool_tc_kernel(const uint8_t *__restrict__ img, int32_t N, int32_t L,
+                                                      int32_t A, const int32_t *__restrict__ kept,
+                                                      const unsigned long long *__restrict__ d_nk,
+                                                      int64_t total16, uint8_t *__restrict__ Dtc) {
+    using Cf = TCfg<B>;
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // one 16-byte group
+    if (e >= total16) return;
+    const int64_t n_k = (int64_t)*d_nk;
+    const int64_t ntiles = (n_k + kTileD - 1) / kTileD;
+    constexpr int G16 = Cf::KP / 16;  // 16-byte groups per row
+    const int64_t tile = e / ((int64_t)kTileD * G16);
+    if (tile >= ntiles) return;
+    const int rem = (int)(e - tile * kTileD * G16);
+    const int m = rem / G16, g = rem % G16;
+    const int64_t d = tile * kTileD + m;
+    uint32_t w[4] = {0, 0, 0, 0};
+    if (d < n_k) {
+        const int32_t c = kept[d];
+        const int64_t x = (int64_t)(c % A) * L, y = (int64_t)(c / A) * L;
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+            const int kb = g * 16 + q;
+            uint32_t v = 0;
+            if (kb < 4 * Cf::n) {
+                const int plane = kb / Cf::n, p = kb % Cf::n;
+                const int i = p / B, j = p % B;
+                v = img[(y + 2 * i + (plane >> 1)) * N + x + 2 * j + (plane & 1)];
+            }
+            w[q >> 2] |= v << (8 * (q & 3));
+        }
+    }
+    // chunk layout: [tile][chunk][128 x KCH]
+    const int kb0 = g * 16;
+    const int ch = kb0 / Cf::KCH, kc = kb0 % Cf::KCH;
+    uint8_t *dst = Dtc + ((size_t)tile * Cf::CH + ch) * Cf::STAGE_BYTES + cm_off(m, kc, Cf::KCH);
+    *reinterpret_cast<uint4 *>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+int tc_supported(int B) { return B == 2 || B == 4 || B == 8 || B == 16; }
+
+size_t tc_pool_bytes(int B, int64_t n_tiles) {
+    switch (B) {
+    case 2: return (size_t)n_tiles * TCfg<2>::CH * TCfg<2>::STAGE_BYTES;
+    case 4: return (size_t)n_tiles * TCfg<4>::CH * TCfg<4>::STAGE_BYTES;
+    case 8: return (size_t)n_tiles * TCfg<8>::CH * TCfg<8>::STAGE_BYTES;
+    case 16: return (size_t)n_tiles * TCfg<16>::CH * TCfg<16>::STAGE_BYTES;
+    default: return 0;
+    }
+}
+
+cudaError_t launch_pool_tc(const uint8_t *img, int32_t N, int32_t B, int32_t L, int32_t A,
+                           const int32_t *kept, const unsigned long long *d_nk, int64_t n_tiles_max,
+                           uint8_t *Dtc, cudaStream_t st) {
+    int kp = 0;
+    switch (B) {
+    case 2: kp = TCfg<2>::KP; break;
+    case 4: kp = TCfg<4>::KP; break;
+    case 8: kp = TCfg<8>::KP; break;
+    case 16: kp = TCfg<16>::KP; break;
+    default: return cudaErrorInvalidValue;
+    }
+    const int64_t total16 = n_tiles_max * kTileD * (kp / 16);
+    if (total16 == 0) return cudaSuccess;
+    const unsigned blocks = (unsigned)((total16 + 255) / 256);
+    switch (B) {
+    case 2: pool_tc_kernel<2><<<blocks, 256, 0, st>>>(img, N, L, A, kept, d_nk, total16, Dtc); break;
+    case 4: pool_tc_kernel<4><<<blocks, 256, 0, st>>>(img, N, L, A, kept, d_nk, total16, Dtc); break;
+    case 8: pool_tc_kernel<8><<<blocks, 256, 0, st>>>(img, N, L, A, kept, d_nk, total16, Dtc); break;
+    case 16: pool_tc_kernel<16><<<blocks, 256, 0, st>>>(img, N, L, A, kept, d_nk, total16, Dtc); break;
+    }
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------ search kernel
+struct TCParams {
+    const uint8_t *img;
+    int32_t N;
+    const int2 *ranges;
+    int32_t n_r;
+    const uint8_t *Dtc;
+    const int32_t *SD;
+    const int64_t *C;
+    const float *t2f;  // [nsp][n_slots]
+    int64_t n_slots;
+    int32_t n_tiles, tiles_per_split, nsplit;
+    int32_t nsp;
+    double spos[kMaxS];
+    int32_t jpos[kMaxS];
+    int32_t has_zero, j_zero;
+    double smax, cmax;
+    Partial *part;
+    unsigned long long *exact_count;
+};
+
+struct TCRange {
+    double A, margin;
+    int32_t SR;
+    int32_t valid;
+};
+
+template <int B, int NSP>
+__global__ void __launch_bounds__(320, 1) tcsearch_kernel(const __grid_constant__ TCParams P) {
+    using Cf = TCfg<B>;
+    constexpr int n = Cf::n, KP = Cf::KP, NR = Cf::NR, NN = Cf::N, KCH = Cf::KCH, CH = Cf::CH;
+    constexpr int STAGES = Cf::STAGES;
+    constexpr int HALF = NR / 2;  // ranges per epilogue warpgroup
+    extern __shared__ __align__(1024) uint8_t smem[];
+    uint8_t *sA = smem;                                        // [STAGES][128 x KCH]
+    uint8_t *sB = sA + STAGES * Cf::STAGE_BYTES;               // [N x KP]
+    TCRange *sR = reinterpret_cast<TCRange *>(sB + Cf::B_BYTES);   // [NR]
+    uint32_t *sThr = reinterpret_cast<uint32_t *>(sR + NR);    // [NR] orderable (best - A + margin)
+    float *sHsn = reinterpret_cast<float *>(sThr + NR);        // [NSP]
+    Partial *sRed = reinterpret_cast<Partial *>(sHsn + 16);    // [NR][4]
+    uint64_t *bar = reinterpret_cast<uint64_t *>(sRed + NR * 4);  // full[S], empty[S], tfull[2], tempty[2]
+    uint64_t *full = bar, *empty = bar + STAGES, *tfull = bar + 2 * STAGES, *tempty = tfull + 2;
+    uint32_t *sTmem = reinterpret_cast<uint32_t *>(tempty + 2);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int r0 = blockIdx.x * NR;
+    const int split = blockIdx.y;
+    const int t0 = split * P.tiles_per_split;
+    const int t1 = min(P.n_tiles, t0 + P.tiles_per_split);
+    const int ntl = max(0, t1 - t0);
+    const int nsteps = ntl * CH;
+
+    // ---- setup: barriers, TMEM, per-range constants, the resident range operand
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            tmbar_init(&full[s], 1);
+            tmbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            tmbar_init(&tfull[b], 1);
+            tmbar_init(&tempty[b], 8);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(sTmem)),
+                     "r"(kTmemCols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    // range operand: row (rl, k) = Rperm_k replicated over the 4 planes; zero padding
+    for (int idx = threadIdx.x; idx < NN * (KP / 4); idx += blockDim.x) {
+        const int row = idx / (KP / 4), kw = idx % (KP / 4);
+        const int rl = row >> 3, k = row & 7;
+        const int r = r0 + rl;
+        uint32_t w = 0;
+        if (r < P.n_r) {
+            const int2 rr = P.ranges[r];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int kb = kw * 4 + q;
+                if (kb < 4 * n) {
+                    // Rperm_k(p) = R(f_k^{-1}(p)); under this numbering f_k^{-1} = f_{k'} with
+                    // k' = [0,3,2,1,4,5,6,7][k] (rotations by 90/270 swap, the rest are involutions)
+                    const int p = kb % n;
+                    const int kinv = (k == 1) ? 3 : (k == 3 ? 1 : k);
+                    int si, sj;
+                    tiso_src(B, kinv, p / B, p % B, si, sj);
+                    const uint32_t v = P.img[(size_t)(rr.y + si) * P.N + rr.x + sj];
+                    w |= v << (8 * q);
+                }
+            }
+        }
+        *reinterpret_cast<uint32_t *>(sB + cm_off(row, kw * 4, KP)) = w;
+    }
+    if (threadIdx.x < NR) {
+        const int r = r0 + threadIdx.x;
+        TCRange R;
+        long long sr = 0, srr = 0;
+        R.valid = r < P.n_r;
+        if (R.valid) {
+            const int2 rr = P.ranges[r];
+            for (int i = 0; i < B; ++i)
+                for (int j = 0; j < B; ++j) {
+                    const int v = P.img[(size_t)(rr.y + i) * P.N + rr.x + j];
+                    sr += v;
+                    srr += v * v;
+                }
+        }
+        R.A = (double)((long long)n * srr - sr * sr);
+        R.SR = (int32_t)sr;
+        // fp32 filter error: |Bq| <= sqrt(A C) (Cauchy-Schwarz); conversions, hs and t2 roundings,
+        // two FFMA roundings, SR*SD rounding at B = 16 -> 8u (hs (sqrt(A Cmax) + n 1020 SR) + t2max)
+        const double u = 5.9604644775390625e-08;
+        const double hs = 0.5 * P.smax;
+        // B <= 8: Bq is exact in int32 and |Bq| <= sqrt(A C); B = 16: fp32 n max SRD - SR SD
+        const double bq = sqrt(R.A * P.cmax) * 1.01 + (B > 8 ? (double)n * 1020.0 * (double)sr : 0.0);
+        const double t2m = P.smax * P.smax * P.cmax * 0.0625;
+        R.margin = 8.0 * u * (hs * bq + t2m) + 1e-12 * (R.A + hs * bq + t2m) + 1e-30;
+        sR[threadIdx.x] = R;
+        const float th = P.has_zero ? fminf(__double2float_ru(R.margin), FLT_MAX) : FLT_MAX;
+        sThr[threadIdx.x] = R.valid ? f2ord(th) : f2ord(-FLT_MAX);
+    }
+    if (threadIdx.x < 16) sHsn[threadIdx.x] = threadIdx.x < P.nsp ? -__double2float_rn(0.5 * P.spos[threadIdx.x]) : 0.f;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes of sB -> tensor core
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *sTmem;
+
+    if (warp == 0) {
+        // ================= producer: one bulk copy per (tile, chunk) stage
+        if (lane == 0) {
+            for (int i = 0; i < nsteps; ++i) {
+                const int s = i % STAGES;
+                if (i >= STAGES) tmbar_wait(&empty[s], (uint32_t)(((i / STAGES) + 1) & 1));
+                const int tile = t0 + i / CH, ch = i % CH;
+                tmbar_expect_tx(&full[s], Cf::STAGE_BYTES);
+                tbulk_g2s(sA + s * Cf::STAGE_BYTES, P.Dtc + ((size_t)tile * CH + ch) * Cf::STAGE_BYTES,
+                          Cf::STAGE_BYTES, &full[s]);
+            }
+        }
+    } else if (warp == 1) {
+        // ================= MMA issuer
+        constexpr uint32_t idesc = idesc_i8(NN);
+        for (int i = 0; i < nsteps; ++i) {
+            const int s = i % STAGES;
+            const int tl = i / CH, ch = i % CH;
+            const int buf = tl & 1;
+            tmbar_wait(&full[s], (uint32_t)((i / STAGES) & 1));
+            if (ch == 0 && tl >= 2) tmbar_wait(&tempty[buf], (uint32_t)(((tl >> 1) + 1) & 1));
+            tc_fence_after();
+            if (lane == 0) {
+                const uint32_t a0 = su32(sA + s * Cf::STAGE_BYTES);
+                const uint32_t b0 = su32(sB) + ch * (KCH / 16) * 128;
+#pragma unroll
+                for (int kk = 0; kk < KCH / 32; ++kk) {
+                    const uint64_t ad = smem_desc(a0 + kk * 256, 128, (KCH / 16) * 128);
+                    const uint64_t bd = smem_desc(b0 + kk * 256, 128, (KP / 16) * 128);
+                    tc_mma_i8(tmem + buf * NN, ad, bd, idesc, (ch > 0 || kk > 0) ? 1u : 0u);
+                }
+                tc_commit(&empty[s]);
+                if (ch == CH - 1) tc_commit(&tfull[buf]);
+            }
+            __syncwarp();
+        }
+    } else {
+        // ================= epilogue: lane = domain (TMEM lane), warpgroup = half of the ranges
+        const int eg = (warp - 2) >> 2;   // 0 or 1
+        const int lq = warp & 3;          // TMEM lane quarter accessible by this warp
+        const int m = lq * 32 + lane;     // domain lane within the tile
+        float nhs[NSP];
+#pragma unroll
+        for (int jj = 0; jj < NSP; ++jj) nhs[jj] = sHsn[jj];
+        double be[HALF];
+        int32_t bd[HALF], bkj[HALF];
+#pragma unroll
+        for (int q = 0; q < HALF; ++q) {
+            const TCRange &R = sR[eg * HALF + q];
+            if (P.has_zero) { be[q] = R.A; bd[q] = 0; bkj[q] = P.j_zero; }
+            else { be[q] = INFINITY; bd[q] = INT_MAX; bkj[q] = INT_MAX; }
+        }
+        unsigned n_exact = 0;
+        for (int tl = 0; tl < ntl; ++tl) {
+            const int buf = tl & 1;
+            const int d = (t0 + tl) * kTileD + m;
+            const int32_t sd = P.SD[d];
+            float t2[NSP];
+#pragma unroll
+            for (int jj = 0; jj < NSP; ++jj) t2[jj] = jj < P.nsp ? P.t2f[(int64_t)jj * P.n_slots + d] : 0.f;
+            tmbar_wait(&tfull[buf], (uint32_t)((tl >> 1) & 1));
+            tc_fence_after();
+            const uint32_t tbase = tmem + ((uint32_t)(lq * 32) << 16) + buf * NN + eg * HALF * 8;
+            // four ranges (32 columns) per tcgen05.ld, the next group in flight while one is scored
+            constexpr int G = HALF / 4;
+            uint32_t vv[64];
+            tc_ld32<0>(tbase, vv);
+            tc_wait_ld();
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                if (g + 1 < G) {
+                    if ((g & 1) == 0) tc_ld32<32>(tbase + (g + 1) * 32, vv);
+                    else tc_ld32<0>(tbase + (g + 1) * 32, vv);
+                }
+#pragma unroll
+                for (int q4 = 0; q4 < 4; ++q4) {
+                    const int q = g * 4 + q4;
+                    const uint32_t *v = vv + (g & 1) * 32 + q4 * 8;
+                    const int mx = max(__vimax3_s32((int)v[0], (int)v[1], (int)v[2]),
+                                       __vimax3_s32((int)v[3], (int)v[4], __vimax3_s32((int)v[5], (int)v[6], (int)v[7])));
+                    const TCRange &R = sR[eg * HALF + q];
+                    float bq;
+                    if constexpr (B == 2) {
+                        // |Bq| <= sqrt(A C) < 2^22: exact int -> float by the 1.5 * 2^23 magic
+                        bq = __int_as_float(n * mx - R.SR * sd + 0x4B400000) - 12582912.0f;
+                    } else if constexpr (B <= 8) {
+                        bq = (float)(n * mx - R.SR * sd);  // exact int32 (|.| < 2^31)
+                    } else {
+                        bq = fmaf((float)n, (float)mx, -((float)R.SR * (float)sd));
+                    }
+                    const float thr = ord2f(sThr[eg * HALF + q]);
+                    bool pass = false;
+#pragma unroll
+                    for (int jj = 0; jj < NSP; ++jj) pass = pass || (fmaf(nhs[jj], bq, t2[jj]) <= thr);
+                    if (pass) {
+                        // ---- exact path: canonical binary64 score, lexicographic first-min
+                        ++n_exact;
+                        int ks = 7;
+#pragma unroll
+                        for (int k = 6; k >= 0; --k)
+                            if ((int)v[k] == mx) ks = k;  // lowest index attaining the max
+                        const double Bq = __dsub_rn(__dmul_rn((double)n, (double)mx),
+                                                    __dmul_rn((double)R.SR, (double)sd));
+                        const double c16 = __dmul_rn(0.0625, (double)P.C[d]);
+                        double e0 = be[q];
+                        int32_t d0 = bd[q], kj0 = bkj[q];
+                        for (int jj = 0; jj < P.nsp; ++jj) {
+                            const double s = P.spos[jj];
+                            const double e = __dadd_rn(__dsub_rn(R.A, __dmul_rn(__dmul_rn(0.5, s), Bq)),
+                                                       __dmul_rn(__dmul_rn(s, s), c16));
+                            const int32_t kj = (ks << 8) | P.jpos[jj];
+                            if (e < e0 || (e == e0 && (d < d0 || (d == d0 && kj < kj0)))) { e0 = e; d0 = d; kj0 = kj; }
+                        }
+                        be[q] = e0; bd[q] = d0; bkj[q] = kj0;
+                        const float t = fminf(__double2float_ru(__dadd_rn(__dsub_rn(e0, R.A), R.margin)), FLT_MAX);
+                        atomicMin(&sThr[eg * HALF + q], f2ord(t));
+                    }
+                }
+                if (g + 1 < G) tc_wait_ld();
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) tmbar_arrive(&tempty[buf]);
+        }
+        // ---- reduce each range's best over the 128 domain lanes (lexicographic)
+#pragma unroll
+        for (int q = 0; q < HALF; ++q) {
+            double e0 = be[q];
+            int32_t d0 = bd[q], kj0 = bkj[q];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const double oe = __shfl_xor_sync(0xffffffffu, e0, o);
+                const int od = __shfl_xor_sync(0xffffffffu, d0, o);
+                const int okj = __shfl_xor_sync(0xffffffffu, kj0, o);
+                if (oe < e0 || (oe == e0 && (od < d0 || (od == d0 && okj < kj0)))) { e0 = oe; d0 = od; kj0 = okj; }
+            }
+            if (lane == 0) {
+                Partial pb;
+                pb.e = e0; pb.d = d0; pb.kj = kj0;
+                sRed[(eg * HALF + q) * 4 + lq] = pb;
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) n_exact += __shfl_xor_sync(0xffffffffu, n_exact, o);
+        if (lane == 0 && n_exact && P.exact_count) atomicAdd(P.exact_count, (unsigned long long)n_exact);
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (threadIdx.x < NR) {
+        const int r = r0 + threadIdx.x;
+        Partial b = sRed[threadIdx.x * 4];
+        for (int w = 1; w < 4; ++w) {
+            const Partial c = sRed[threadIdx.x * 4 + w];
+            if (c.e < b.e || (c.e == b.e && (c.d < b.d || (c.d == b.d && c.kj < b.kj)))) b = c;
+        }
+        if (r < P.n_r) P.part[(size_t)r * P.nsplit + split] = b;
+    }
+    if (warp == 0) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
+    }
+}
+
+template <int B, int NSP>
+static size_t tc_smem_bytes() {
+    using Cf = TCfg<B>;
+    return (size_t)Cf::STAGES * Cf::STAGE_BYTES + Cf::B_BYTES + sizeof(TCRange) * Cf::NR + 4 * Cf::NR +
+           4 * 16 + sizeof(Partial) * Cf::NR * 4 + 8 * (2 * Cf::STAGES + 4) + 16 + 1024;
+}
+
+template <int B, int NSP>
+static cudaError_t launch_tc_t(const TCParams &p, cudaStream_t st) {
+    using Cf = TCfg<B>;
+    const size_t smem = tc_smem_bytes<B, NSP>();
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(tcsearch_kernel<B, NSP>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    dim3 grid((unsigned)((p.n_r + Cf::NR - 1) / Cf::NR), (unsigned)p.nsplit);
+    tcsearch_kernel<B, NSP><<<grid, Cf::THREADS, smem, st>>>(p);
+    return cudaGetLastError();
+}
+
+template <int B>
+static cudaError_t launch_tc_b(const TCParams &p, cudaStream_t st) {
+    if (p.nsp <= 1) return launch_tc_t<B, 1>(p, st);
+    if (p.nsp <= 2) return launch_tc_t<B, 2>(p, st);
+    return launch_tc_t<B, 16>(p, st);
+}
+
+int tc_ranges_per_cta(int B) { return B == 16 ? 16 : 32; }
+
+cudaError_t launch_tc_search(int32_t B, const SearchParams &sp, const uint8_t *Dtc, int64_t n_slots,
+                             cudaStream_t st) {
+    if (sp.n_r == 0 || sp.nsp == 0) return cudaSuccess;
+    TCParams p;
+    memset(&p, 0, sizeof p);
+    p.img = sp.img; p.N = sp.N; p.ranges = sp.ranges; p.n_r = sp.n_r;
+    p.Dtc = Dtc; p.SD = sp.SD; p.C = sp.C; p.t2f = sp.t2f; p.n_slots = n_slots;
+    p.n_tiles = sp.n_tiles; p.tiles_per_split = sp.tiles_per_split; p.nsplit = sp.nsplit;
+    p.nsp = sp.nsp;
+    memcpy(p.spos, sp.spos, sizeof p.spos);
+    memcpy(p.jpos, sp.jpos, sizeof p.jpos);
+    p.has_zero = sp.has_zero; p.j_zero = sp.j_zero;
+    p.smax = sp.smax; p.cmax = sp.cmax;
+    p.part = sp.part; p.exact_count = sp.exact_count;
+    switch (B) {
+    case 2: return launch_tc_b<2>(p, st);
+    case 4: return launch_tc_b<4>(p, st);
+    case 8: return launch_tc_b<8>(p, st);
+    case 16: return launch_tc_b<16>(p, st);
+    default: return cudaErrorInvalidValue;
+    }
+}
+
+int tc_nsplit_hint(int32_t B, int64_t n_r, int64_t n_tiles, int num_sms) {
+    const int64_t nr = tc_ranges_per_cta(B);
+    const int64_t gx = (n_r + nr - 1) / nr;
+    if (gx <= 0 || n_tiles <= 0) return 1;
+    int64_t ns = ((int64_t)num_sms * 2 + gx - 1) / gx;
+    const int64_t max_ns = (n_tiles + 3) / 4;  // at least ~4 tiles per split
+    if (ns > max_ns) ns = max_ns;
+    if (ns < 1) ns = 1;
+    if (ns > 65535) ns = 65535;
+    return (int)ns;
+}
+
+}  // namespace fic
