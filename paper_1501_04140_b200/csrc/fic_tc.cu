@@ -35,12 +35,13 @@ struct TCfg {
     static constexpr int KP = ((4 * n + 31) / 32) * 32;    // K bytes (padded)
     static constexpr int NR = (B == 16) ? 16 : 32;         // ranges per CTA
     static constexpr int N = 8 * NR;                       // MMA N (columns per accumulator)
-    static constexpr int KCH = KP < 256 ? KP : 256;        // K bytes per pipeline stage
+    static constexpr int KCH = KP < 256 ? KP : (B == 16 ? 128 : 256);  // K bytes per pipeline stage
     static constexpr int CH = KP / KCH;                    // stages per domain tile
     static constexpr int STAGE_BYTES = kTileD * KCH;       // A bytes per stage
-    static constexpr int STAGES = (B == 16) ? 2 : (B == 8 ? 3 : 4);
+    static constexpr int STAGES = (B >= 8) ? 2 : 4;
     static constexpr int B_BYTES = N * KP;                 // resident range operand
-    static constexpr int THREADS = 320;
+    static constexpr int EWG = 4;                          // epilogue warpgroups
+    static constexpr int THREADS = 64 + 128 * EWG;
 };
 
 constexpr uint32_t kTmemCols = 512;
@@ -255,21 +256,23 @@ struct TCRange {
 };
 
 template <int B, int NSP>
-__global__ void __launch_bounds__(320, 1) tcsearch_kernel(const __grid_constant__ TCParams P) {
+__global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __grid_constant__ TCParams P) {
     using Cf = TCfg<B>;
     constexpr int n = Cf::n, KP = Cf::KP, NR = Cf::NR, NN = Cf::N, KCH = Cf::KCH, CH = Cf::CH;
     constexpr int STAGES = Cf::STAGES;
-    constexpr int HALF = NR / 2;  // ranges per epilogue warpgroup
+    constexpr int HALF = NR / Cf::EWG;  // ranges per epilogue warpgroup
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t *sA = smem;                                        // [STAGES][128 x KCH]
     uint8_t *sB = sA + STAGES * Cf::STAGE_BYTES;               // [N x KP]
     TCRange *sR = reinterpret_cast<TCRange *>(sB + Cf::B_BYTES);   // [NR]
-    uint32_t *sThr = reinterpret_cast<uint32_t *>(sR + NR);    // [NR] orderable (best - A + margin)
+    float *sThr = reinterpret_cast<float *>(sR + NR);          // [NR] RU(best - A + margin), CAS-min
     float *sHsn = reinterpret_cast<float *>(sThr + NR);        // [NSP]
     Partial *sRed = reinterpret_cast<Partial *>(sHsn + 16);    // [NR][4]
     uint64_t *bar = reinterpret_cast<uint64_t *>(sRed + NR * 4);  // full[S], empty[S], tfull[2], tempty[2]
     uint64_t *full = bar, *empty = bar + STAGES, *tfull = bar + 2 * STAGES, *tempty = tfull + 2;
     uint32_t *sTmem = reinterpret_cast<uint32_t *>(tempty + 2);
+    Partial *sBest = reinterpret_cast<Partial *>(sTmem + 4);  // [NR][128] per (range, domain lane)
+    int2 *sQ = reinterpret_cast<int2 *>(sBest + NR * kTileD);  // [epilogue threads][4] exact queue
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int r0 = blockIdx.x * NR;
@@ -287,7 +290,7 @@ __global__ void __launch_bounds__(320, 1) tcsearch_kernel(const __grid_constant_
         }
         for (int b = 0; b < 2; ++b) {
             tmbar_init(&tfull[b], 1);
-            tmbar_init(&tempty[b], 8);
+            tmbar_init(&tempty[b], 4 * Cf::EWG);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -347,7 +350,7 @@ __global__ void __launch_bounds__(320, 1) tcsearch_kernel(const __grid_constant_
         R.margin = 8.0 * u * (hs * bq + t2m) + 1e-12 * (R.A + hs * bq + t2m) + 1e-30;
         sR[threadIdx.x] = R;
         const float th = P.has_zero ? fminf(__double2float_ru(R.margin), FLT_MAX) : FLT_MAX;
-        sThr[threadIdx.x] = R.valid ? f2ord(th) : f2ord(-FLT_MAX);
+        sThr[threadIdx.x] = R.valid ? th : -FLT_MAX;
     }
     if (threadIdx.x < 16) sHsn[threadIdx.x] = threadIdx.x < P.nsp ? -__double2float_rn(0.5 * P.spos[threadIdx.x]) : 0.f;
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes of sB -> tensor core
@@ -394,28 +397,47 @@ __global__ void __launch_bounds__(320, 1) tcsearch_kernel(const __grid_constant_
         }
     } else {
         // ================= epilogue: lane = domain (TMEM lane), warpgroup = half of the ranges
-        const int eg = (warp - 2) >> 2;   // 0 or 1
+        const int eg = (warp - 2) >> 2;   // epilogue warpgroup
         const int lq = warp & 3;          // TMEM lane quarter accessible by this warp
         const int m = lq * 32 + lane;     // domain lane within the tile
         float nhs[NSP];
 #pragma unroll
         for (int jj = 0; jj < NSP; ++jj) nhs[jj] = sHsn[jj];
-        double be[HALF];
-        int32_t bd[HALF], bkj[HALF];
-#pragma unroll
         for (int q = 0; q < HALF; ++q) {
-            const TCRange &R = sR[eg * HALF + q];
-            if (P.has_zero) { be[q] = R.A; bd[q] = 0; bkj[q] = P.j_zero; }
-            else { be[q] = INFINITY; bd[q] = INT_MAX; bkj[q] = INT_MAX; }
+            Partial pb;
+            if (P.has_zero) { pb.e = sR[eg * HALF + q].A; pb.d = 0; pb.kj = P.j_zero; }
+            else { pb.e = INFINITY; pb.d = INT_MAX; pb.kj = INT_MAX; }
+            sBest[(eg * HALF + q) * kTileD + m] = pb;
         }
         unsigned n_exact = 0;
+        int rSR[HALF];
+#pragma unroll
+        for (int q = 0; q < HALF; ++q) rSR[q] = sR[eg * HALF + q].SR;
+        int qn = 0;
+        const int qbase = (threadIdx.x - 64) * 4;
+        int32_t sd_n = 0;
+        float t2_n[NSP];
+        {
+            const int d = t0 * kTileD + m;
+            if (ntl > 0) {
+                sd_n = P.SD[d];
+#pragma unroll
+                for (int jj = 0; jj < NSP; ++jj) t2_n[jj] = jj < P.nsp ? P.t2f[(int64_t)jj * P.n_slots + d] : 0.f;
+            }
+        }
         for (int tl = 0; tl < ntl; ++tl) {
             const int buf = tl & 1;
             const int d = (t0 + tl) * kTileD + m;
-            const int32_t sd = P.SD[d];
+            const int32_t sd = sd_n;
             float t2[NSP];
 #pragma unroll
-            for (int jj = 0; jj < NSP; ++jj) t2[jj] = jj < P.nsp ? P.t2f[(int64_t)jj * P.n_slots + d] : 0.f;
+            for (int jj = 0; jj < NSP; ++jj) t2[jj] = t2_n[jj];
+            if (tl + 1 < ntl) {  // prefetch the next tile's per-domain data
+                sd_n = P.SD[d + kTileD];
+#pragma unroll
+                for (int jj = 0; jj < NSP; ++jj)
+                    t2_n[jj] = jj < P.nsp ? P.t2f[(int64_t)jj * P.n_slots + d + kTileD] : 0.f;
+            }
             tmbar_wait(&tfull[buf], (uint32_t)((tl >> 1) & 1));
             tc_fence_after();
             const uint32_t tbase = tmem + ((uint32_t)(lq * 32) << 16) + buf * NN + eg * HALF * 8;
@@ -430,50 +452,77 @@ __global__ void __launch_bounds__(320, 1) tcsearch_kernel(const __grid_constant_
                     if ((g & 1) == 0) tc_ld32<32>(tbase + (g + 1) * 32, vv);
                     else tc_ld32<0>(tbase + (g + 1) * 32, vv);
                 }
+                unsigned pm = 0;
+                int mxs[4];
 #pragma unroll
-                for (int q4 = 0; q4 < 4; ++q4) {
+                for (int q4 = 0; q4 < 4; ++q4) {  // branch-free filter of four ranges
                     const int q = g * 4 + q4;
                     const uint32_t *v = vv + (g & 1) * 32 + q4 * 8;
                     const int mx = max(__vimax3_s32((int)v[0], (int)v[1], (int)v[2]),
                                        __vimax3_s32((int)v[3], (int)v[4], __vimax3_s32((int)v[5], (int)v[6], (int)v[7])));
-                    const TCRange &R = sR[eg * HALF + q];
+                    mxs[q4] = mx;
+                    const int rsr = rSR[q];
                     float bq;
                     if constexpr (B == 2) {
                         // |Bq| <= sqrt(A C) < 2^22: exact int -> float by the 1.5 * 2^23 magic
-                        bq = __int_as_float(n * mx - R.SR * sd + 0x4B400000) - 12582912.0f;
+                        bq = __int_as_float(n * mx - rsr * sd + 0x4B400000) - 12582912.0f;
                     } else if constexpr (B <= 8) {
-                        bq = (float)(n * mx - R.SR * sd);  // exact int32 (|.| < 2^31)
+                        bq = (float)(n * mx - rsr * sd);  // exact int32 (|.| < 2^31)
                     } else {
-                        bq = fmaf((float)n, (float)mx, -((float)R.SR * (float)sd));
+                        bq = fmaf((float)n, (float)mx, -((float)rsr * (float)sd));
                     }
-                    const float thr = ord2f(sThr[eg * HALF + q]);
-                    bool pass = false;
+                    float g0 = fmaf(nhs[0], bq, t2[0]);
 #pragma unroll
-                    for (int jj = 0; jj < NSP; ++jj) pass = pass || (fmaf(nhs[jj], bq, t2[jj]) <= thr);
-                    if (pass) {
-                        // ---- exact path: canonical binary64 score, lexicographic first-min
-                        ++n_exact;
-                        int ks = 7;
+                    for (int jj = 1; jj < NSP; ++jj) g0 = fminf(g0, fmaf(nhs[jj], bq, t2[jj]));
+                    pm |= (g0 <= sThr[eg * HALF + q]) ? (1u << q4) : 0u;
+                }
+                if (pm) {  // queue (q, k*, max SRD) of the passing ranges for the exact path
 #pragma unroll
-                        for (int k = 6; k >= 0; --k)
-                            if ((int)v[k] == mx) ks = k;  // lowest index attaining the max
-                        const double Bq = __dsub_rn(__dmul_rn((double)n, (double)mx),
-                                                    __dmul_rn((double)R.SR, (double)sd));
-                        const double c16 = __dmul_rn(0.0625, (double)P.C[d]);
-                        double e0 = be[q];
-                        int32_t d0 = bd[q], kj0 = bkj[q];
-                        for (int jj = 0; jj < P.nsp; ++jj) {
-                            const double s = P.spos[jj];
-                            const double e = __dadd_rn(__dsub_rn(R.A, __dmul_rn(__dmul_rn(0.5, s), Bq)),
-                                                       __dmul_rn(__dmul_rn(s, s), c16));
-                            const int32_t kj = (ks << 8) | P.jpos[jj];
-                            if (e < e0 || (e == e0 && (d < d0 || (d == d0 && kj < kj0)))) { e0 = e; d0 = d; kj0 = kj; }
+                    for (int q4 = 0; q4 < 4; ++q4) {
+                        if (pm >> q4 & 1) {
+                            const uint32_t *v = vv + (g & 1) * 32 + q4 * 8;
+                            int ks = 7;
+#pragma unroll
+                            for (int k = 6; k >= 0; --k)
+                                if ((int)v[k] == mxs[q4]) ks = k;  // lowest index attaining the max
+                            sQ[qbase + qn] = make_int2((g * 4 + q4) | (ks << 8), mxs[q4]);
+                            ++qn;
                         }
-                        be[q] = e0; bd[q] = d0; bkj[q] = kj0;
-                        const float t = fminf(__double2float_ru(__dadd_rn(__dsub_rn(e0, R.A), R.margin)), FLT_MAX);
-                        atomicMin(&sThr[eg * HALF + q], f2ord(t));
                     }
                 }
+                // ---- exact path (rare, one rolled copy): canonical binary64 score for every s > 0,
+                // lexicographic first-min update of this lane's best, CAS-min of the shared threshold
+                for (int i = 0; i < qn; ++i) {
+                    const int2 ent = sQ[qbase + i];
+                    const int q = ent.x & 255, ks = ent.x >> 8, mx = ent.y;
+                    const TCRange &R = sR[eg * HALF + q];
+                    Partial *bp = &sBest[(eg * HALF + q) * kTileD + m];
+                    const double Bq = __dsub_rn(__dmul_rn((double)n, (double)mx),
+                                                __dmul_rn((double)R.SR, (double)sd));
+                    const double c16 = __dmul_rn(0.0625, (double)P.C[d]);
+                    double e0 = bp->e;
+                    int32_t d0 = bp->d, kj0 = bp->kj;
+                    for (int jj = 0; jj < P.nsp; ++jj) {
+                        const double sj = P.spos[jj];
+                        const double e = __dadd_rn(__dsub_rn(R.A, __dmul_rn(__dmul_rn(0.5, sj), Bq)),
+                                                   __dmul_rn(__dmul_rn(sj, sj), c16));
+                        const int32_t kj = (ks << 8) | P.jpos[jj];
+                        if (e < e0 || (e == e0 && (d < d0 || (d == d0 && kj < kj0)))) { e0 = e; d0 = d; kj0 = kj; }
+                    }
+                    bp->e = e0;
+                    bp->d = d0;
+                    bp->kj = kj0;
+                    const float t = fminf(__double2float_ru(__dadd_rn(__dsub_rn(e0, R.A), R.margin)), FLT_MAX);
+                    int *ti = reinterpret_cast<int *>(&sThr[eg * HALF + q]);
+                    int old = *ti;
+                    while (t < __int_as_float(old)) {
+                        const int prev = atomicCAS(ti, old, __float_as_int(t));
+                        if (prev == old) break;
+                        old = prev;
+                    }
+                }
+                n_exact += qn;
+                qn = 0;
                 if (g + 1 < G) tc_wait_ld();
             }
             tc_fence_before();
@@ -481,10 +530,11 @@ __global__ void __launch_bounds__(320, 1) tcsearch_kernel(const __grid_constant_
             if (lane == 0) tmbar_arrive(&tempty[buf]);
         }
         // ---- reduce each range's best over the 128 domain lanes (lexicographic)
-#pragma unroll
+#pragma unroll 1
         for (int q = 0; q < HALF; ++q) {
-            double e0 = be[q];
-            int32_t d0 = bd[q], kj0 = bkj[q];
+            const Partial mine = sBest[(eg * HALF + q) * kTileD + m];
+            double e0 = mine.e;
+            int32_t d0 = mine.d, kj0 = mine.kj;
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) {
                 const double oe = __shfl_xor_sync(0xffffffffu, e0, o);
@@ -523,7 +573,8 @@ template <int B, int NSP>
 static size_t tc_smem_bytes() {
     using Cf = TCfg<B>;
     return (size_t)Cf::STAGES * Cf::STAGE_BYTES + Cf::B_BYTES + sizeof(TCRange) * Cf::NR + 4 * Cf::NR +
-           4 * 16 + sizeof(Partial) * Cf::NR * 4 + 8 * (2 * Cf::STAGES + 4) + 16 + 1024;
+           4 * 16 + sizeof(Partial) * Cf::NR * 4 + 8 * (2 * Cf::STAGES + 4) + 16 +
+           sizeof(Partial) * Cf::NR * kTileD + sizeof(int2) * 128 * Cf::EWG * 4 + 1024;
 }
 
 template <int B, int NSP>
