@@ -45,8 +45,10 @@ def parse():
     ap.add_argument("--config", default="C3")
     ap.add_argument("--s-mode", default="predefined", choices=["predefined", "grid"])
     ap.add_argument("--t", type=float, default=8.0)
-    ap.add_argument("--cpu-shards", type=int, default=48,
-                    help="oracle sample = 1/cpu-shards of the top-level blocks")
+    ap.add_argument("--cpu-shards", type=int, default=1,
+                    help="cpu_baseline sample = 1/cpu-shards of the top-level blocks (1 = whole C3)")
+    ap.add_argument("--ref-shards", type=int, default=4,
+                    help="--impl reference: each step encodes 1/ref-shards of the top-level blocks")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     return ap.parse_args()
@@ -149,7 +151,7 @@ def run_reference(args, cfg_name):
     from fic_inputs import config, image_for
     cfg = config(cfg_name, s_mode=args.s_mode, t=args.t)
     img = image_for(cfg)
-    S = args.cpu_shards
+    S = args.ref_shards
     for w in range(args.warmup):
         oracle_sample(cfg, img, S, w % S)
     tot_pairs, tot_t, thr = 0, 0.0, 1
@@ -290,14 +292,20 @@ def main():
             dist.destroy_process_group()
         return 0
 
-    # ---- roofline of the dominant kernel (the level search with the largest device time)
+    # ---- roofline of the dominant kernel (the level search with the largest device time),
+    # SURVEY.md §8(d) / BASELINE.md:  T_roof = pairs * max(4n / P_int8, 2 / P_int32 + 0.5 |S| / P_fp64)
     peaks = load_peaks()
-    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+    sm_max = float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
+    p_int8 = 2.0 * float(peaks.get("bf16_tflops", 1640.9)) * 1e12  # measured bf16 x nominal int8 ratio
+    p_int32 = 148 * 128 * sm_max                                   # fma + alu pipes, 64 lanes each
+    p_fp64 = 148 * 64 * sm_max                                     # B200 fp64 (37 TF)
     dom = max(level_acc, key=lambda s: s["ms_search"])
     n = dom["B"] * dom["B"]
+    nS = len(cfg["s"][[lv["B"] for lv in level_acc].index(dom["B"])])
+    t_pair = max(4.0 * n / p_int8, 2.0 / p_int32 + 0.5 * nS / p_fp64)
     ms_launch = dom["ms_search"] / args.steps
-    achieved = 2.0 * dom["pairs"] * n / (ms_launch / 1e3) / 1e12  # fp32 FMA = 2 flop per MAC
-    peak = 2.0 * 148 * 128 * sm_max * 1e6 / 1e12  # 148 SMs x 128 FP32 lanes x max SM clock
+    achieved = dom["pairs"] / (ms_launch / 1e3) / 1e9
+    peak = 1.0 / t_pair / 1e9
     traffic = load_traffic()
 
     res = {
@@ -310,11 +318,13 @@ def main():
                    "entropy_tau": cfg["tau"], "images": "seed = rank",
                    "l2": "flushed between timed steps (256 MB write)",
                    "pairs_per_step": pairs_step, "records_per_step": n_rec},
-        "roofline": {"bound": "alu", "kernel": f"search_kernel<B={dom['B']}>",
-                     "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+        "roofline": {"bound": "alu" if 4.0 * n / p_int8 < 2.0 / p_int32 + 0.5 * nS / p_fp64 else "tensor",
+                     "kernel": f"tcsearch_kernel<B={dom['B']}>",
+                     "achieved": achieved, "peak": peak, "unit": "Gpairs/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "peak_note": "FP32 FFMA: 148 SMs x 128 lanes x 2 flop x sm_max_mhz "
-                                  "(MEASURED_PEAKS.json); algorithmic work = pairs x B^2 MACs"},
+                     "peak_note": "SURVEY 8(d): 1/max(4n/P_int8, 2/P_int32 + 0.5|S|/P_fp64) pairs/s; "
+                                  "P_int8 = 2 x measured bf16 burst, P_int32 = 148x128xf_max, "
+                                  "P_fp64 = 148x64xf_max (DESIGN.md 7)"},
         "levels": [{"B": s["B"], "n_candidates": s["n_candidates"], "n_kept": s["n_kept"],
                     "n_ranges": s["n_ranges"], "pairs": s["pairs"],
                     "exact_evals": s["exact_evals"],
