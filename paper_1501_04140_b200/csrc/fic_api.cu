@@ -35,8 +35,8 @@ struct fic_ctx {
     std::vector<fic_level_stats> stats;
     cudaEvent_t ev[fic::kMaxLevels][5] = {};
     int64_t launches = 0;
-    int search_mode = 0;  // env FIC_SEARCH = tc (default) | fourier | direct (A/B checks)
-    Buf b_rc, b_meta, b_u;  // libfic kernels enqueued (for fic_level_stats.kernel_launches)  // pool start, search start, search end, finalize end, pool end
+    int search_mode = 0;  // env FIC_SEARCH: auto (default: B=2 closed form, else tcgen05) | fourier | direct | tc
+    Buf b_rc, b_meta, b_u, b_gthr;  // libfic kernels enqueued (for fic_level_stats.kernel_launches)  // pool start, search start, search end, finalize end, pool end
 };
 
 namespace {
@@ -94,7 +94,7 @@ void free_buf(Buf &b) {
 void free_pool(Pool &P) {
     free_buf(P.b_keys); free_buf(P.b_keep); free_buf(P.b_kept); free_buf(P.b_Dt);
     free_buf(P.b_SDf); free_buf(P.b_SD); free_buf(P.b_C); free_buf(P.b_misc); free_buf(P.b_Dc);
-    free_buf(P.b_Dtc);
+    free_buf(P.b_Dtc); free_buf(P.b_F2);
 }
 
 bool pow2(int32_t v) { return v > 0 && (v & (v - 1)) == 0; }
@@ -132,12 +132,14 @@ fic_status pool_enqueue(fic_ctx *ctx, Pool &P, const uint8_t *img, int32_t N, in
     CK(grow(ctx, P.b_keys, sizeof(int64_t) * P.n_c));
     CK(grow(ctx, P.b_keep, P.n_c + 16));
     CK(grow(ctx, P.b_kept, sizeof(int32_t) * P.n_c));
-    P.mode = ctx->search_mode;
+    P.mode = ctx->search_mode == 4 ? 0 : ctx->search_mode;
+    if (ctx->search_mode == 0 && B == 2) P.mode = 3;
     if (P.mode == 0 && !fic::tc_supported(B)) P.mode = 2;
     if (P.mode == 1 && fic::fourier_record_stride(B) == 0) P.mode = 2;
     if (P.mode == 2) CK(grow(ctx, P.b_Dt, sizeof(float) * slots * P.n));
     if (P.mode == 1) CK(grow(ctx, P.b_Dc, sizeof(float) * slots * fic::fourier_record_stride(B)));
     if (P.mode == 0) CK(grow(ctx, P.b_Dtc, fic::tc_pool_bytes(B, tiles_max)));
+    if (P.mode == 3) CK(grow(ctx, P.b_F2, sizeof(float4) * slots));
     CK(grow(ctx, P.b_SDf, sizeof(float) * slots));
     CK(grow(ctx, P.b_SD, sizeof(int32_t) * slots));
     CK(grow(ctx, P.b_C, sizeof(int64_t) * slots));
@@ -148,6 +150,7 @@ fic_status pool_enqueue(fic_ctx *ctx, Pool &P, const uint8_t *img, int32_t N, in
     P.Dt = P.mode == 2 ? ptr<float>(P.b_Dt) : nullptr;
     P.Dc = P.mode == 1 ? ptr<float>(P.b_Dc) : nullptr;
     P.Dtc = P.mode == 0 ? ptr<uint8_t>(P.b_Dtc) : nullptr;
+    P.F2 = P.mode == 3 ? ptr<float4>(P.b_F2) : nullptr;
     P.SD = ptr<int32_t>(P.b_SD); P.C = ptr<int64_t>(P.b_C);
     P.d_misc = ptr<unsigned long long>(P.b_misc);
     cudaStream_t st = ctx->stream;
@@ -163,6 +166,8 @@ fic_status pool_enqueue(fic_ctx *ctx, Pool &P, const uint8_t *img, int32_t N, in
         CK(fic::launch_pool_gather(img, N, B, L, P.A, P.kept, &P.d_misc[0], tiles_max, P.Dt, st));
     else if (P.mode == 0)
         CK(fic::launch_pool_tc(img, N, B, L, P.A, P.kept, &P.d_misc[0], tiles_max, P.Dtc, st));
+    else if (P.mode == 3)
+        CK(fic::launch_b2_pool(img, N, L, P.A, P.kept, &P.d_misc[0], slots, P.F2, st));
     else
         CK(fic::launch_pool_coeff(img, N, B, L, P.A, P.kept, &P.d_misc[0], slots, P.Dc,
                                   reinterpret_cast<unsigned int *>(&P.d_misc[2]), st));
@@ -238,6 +243,8 @@ fic_status level_enqueue(fic_ctx *ctx, const Pool &P, const uint8_t *img, const 
         sp.nsplit = fic::search_nsplit_hint(P.B, n_r, P.n_tiles, ctx->num_sms);
     else if (P.mode == 0)
         sp.nsplit = fic::tc_nsplit_hint(P.B, n_r, P.n_tiles, ctx->num_sms);
+    else if (P.mode == 3)
+        sp.nsplit = fic::b2_nsplit_hint(n_r, P.n_tiles, ctx->num_sms);
     else
         sp.nsplit = fic::fourier_nsplit_hint(P.B, sp.nsp, n_r, P.n_tiles, ctx->num_sms);
     sp.tiles_per_split = (int32_t)((P.n_tiles + sp.nsplit - 1) / sp.nsplit);
@@ -259,6 +266,15 @@ fic_status level_enqueue(fic_ctx *ctx, const Pool &P, const uint8_t *img, const 
             else CK(fic::launch_tc_search(P.B, sp, P.Dtc, slots, st));
             ctx->launches += 1;
         }
+    } else if (P.mode == 3) {
+        fic::SList sl;
+        memcpy(sl.s, sp.spos, sizeof sl.s);
+        CK(grow(ctx, ctx->b_u, sizeof(float) * (size_t)slots * (sp.nsp ? sp.nsp : 1)));
+        CK(fic::launch_fourier_u(P.C, (int32_t)P.n_k, slots, sl, sp.nsp, ptr<float>(ctx->b_u), st));
+        if (ctx->timing) CK(cudaEventRecord(ctx->ev[level_slot][1], st));
+        CK(grow(ctx, ctx->b_gthr, sizeof(float) * (size_t)n_r));
+        CK(fic::launch_b2_search(sp, P.F2, ptr<float>(ctx->b_u), P.kept, P.L, P.A, ptr<float>(ctx->b_gthr), st));
+        ctx->launches += sp.nsp > 0 ? 2 : 0;
     } else {
         const int nc = fic::fourier_record_stride(P.B);  // >= 8 nO + 1
         const int32_t r_stride = (int32_t)((n_r + 31) / 32 * 32);
@@ -338,6 +354,7 @@ fic_status fic_ctx_create(int32_t device, void *cuda_stream, fic_ctx **out) {
         ctx->search_mode = 0;
         if (env && strcmp(env, "fourier") == 0) ctx->search_mode = 1;
         if (env && strcmp(env, "direct") == 0) ctx->search_mode = 2;
+        if (env && strcmp(env, "tc") == 0) ctx->search_mode = 4;
     }
     for (int l = 0; l < fic::kMaxLevels && e == cudaSuccess; ++l)
         for (int q = 0; q < 5 && e == cudaSuccess; ++q) e = cudaEventCreate(&ctx->ev[l][q]);
@@ -368,7 +385,7 @@ fic_status fic_ctx_destroy(fic_ctx *ctx) {
     for (auto &P : ctx->levels) free_pool(P);
     Buf *bufs[] = {&ctx->b_blocksum, &ctx->b_counts, &ctx->b_rng[0], &ctx->b_rng[1], &ctx->b_rec,
                    &ctx->b_acc, &ctx->b_child, &ctx->b_part, &ctx->b_t2f, &ctx->b_img, &ctx->b_out,
-                   &ctx->b_scounts, &ctx->b_rc, &ctx->b_meta, &ctx->b_u};
+                   &ctx->b_scounts, &ctx->b_rc, &ctx->b_meta, &ctx->b_u, &ctx->b_gthr};
     for (Buf *b : bufs) free_buf(*b);
     if (ctx->d_delta) cudaFree(ctx->d_delta);
     if (ctx->h_counts) cudaFreeHost(ctx->h_counts);

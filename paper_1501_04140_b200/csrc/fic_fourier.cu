@@ -263,6 +263,13 @@ __global__ void fourier_u_kernel(const int64_t *__restrict__ C, int32_t n_k, int
     }
 }
 
+cudaError_t launch_fourier_u(const int64_t *C, int32_t n_k, int64_t n_slots, const SList &sl, int32_t nsp,
+                             float *U, cudaStream_t st) {
+    if (n_slots == 0 || nsp == 0) return cudaSuccess;
+    fourier_u_kernel<<<(unsigned)((n_slots + 255) / 256), 256, 0, st>>>(C, n_k, n_slots, sl, nsp, U);
+    return cudaGetLastError();
+}
+
 // ------------------------------------------------------------------------------ range prep
 struct RangeMeta {
     double A;       // n SRR - SR^2 (exact)

@@ -36,12 +36,13 @@ struct Pool {
     float *Dt = nullptr, *SDf = nullptr;
     float *Dc = nullptr;    // D4-Fourier domain records [slots][NCS] (B <= 8), or null
     uint8_t *Dtc = nullptr; // tcgen05 A operand: [tiles][chunks][128 x KCH] core-matrix u8, or null
-    int mode = 0;           // 0: tcgen05 (Dtc), 1: D4-Fourier CUDA cores (Dc), 2: direct FFMA (Dt)
+    float4 *F2 = nullptr;   // B = 2 closed-form domain features (Y2, yr, yi, 0)
+    int mode = 0;           // 0: tcgen05 (Dtc), 1: D4-Fourier (Dc), 2: direct FFMA (Dt), 3: B=2 closed form (F2)
     int32_t *SD = nullptr;
     int64_t *C = nullptr;
     unsigned long long *d_misc = nullptr;  // [0] = n_kept, [1] = Cmax, [2] = max |dh|_2 (float bits)
     double dnmax = 0.0;
-    Buf b_keys, b_keep, b_kept, b_Dt, b_SDf, b_SD, b_C, b_misc, b_Dc, b_Dtc;
+    Buf b_keys, b_keep, b_kept, b_Dt, b_SDf, b_SD, b_C, b_misc, b_Dc, b_Dtc, b_F2;
     int device = 0;
 };
 
@@ -123,6 +124,15 @@ cudaError_t launch_finalize(const FinalizeParams &p, cudaStream_t st);
 cudaError_t launch_merge_shards(const fic_record *in, const int64_t *d_counts, int32_t n_shards,
                                 int64_t stride, int64_t max_count, fic_record *out, cudaStream_t st);
 int search_nsplit_hint(int32_t B, int64_t n_r, int64_t n_tiles, int num_sms);
+
+// B = 2 closed-form search (fic_b2.cu)
+cudaError_t launch_b2_pool(const uint8_t *img, int32_t N, int32_t L, int32_t A, const int32_t *kept,
+                           const unsigned long long *d_nk, int64_t n_slots, float4 *F, cudaStream_t st);
+int b2_nsplit_hint(int64_t n_r, int64_t n_tiles, int num_sms);
+cudaError_t launch_b2_search(const SearchParams &sp, const float4 *F, const float *U, const int32_t *kept,
+                             int32_t L, int32_t A, float *gthr, cudaStream_t st);
+cudaError_t launch_fourier_u(const int64_t *C, int32_t n_k, int64_t n_slots, const SList &sl, int32_t nsp,
+                             float *U, cudaStream_t st);
 
 // tcgen05 search (fic_tc.cu), B in {2, 4, 8, 16}
 int tc_supported(int B);

@@ -422,7 +422,7 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
             if (ntl > 0) {
                 sd_n = P.SD[d];
 #pragma unroll
-                for (int jj = 0; jj < NSP; ++jj) t2_n[jj] = jj < P.nsp ? P.t2f[(int64_t)jj * P.n_slots + d] : 0.f;
+                for (int jj = 0; jj < NSP; ++jj) t2_n[jj] = jj < P.nsp ? P.t2f[(int64_t)jj * P.n_slots + d] : INFINITY;
             }
         }
         for (int tl = 0; tl < ntl; ++tl) {
@@ -436,7 +436,7 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
                 sd_n = P.SD[d + kTileD];
 #pragma unroll
                 for (int jj = 0; jj < NSP; ++jj)
-                    t2_n[jj] = jj < P.nsp ? P.t2f[(int64_t)jj * P.n_slots + d + kTileD] : 0.f;
+                    t2_n[jj] = jj < P.nsp ? P.t2f[(int64_t)jj * P.n_slots + d + kTileD] : INFINITY;
             }
             tmbar_wait(&tfull[buf], (uint32_t)((tl >> 1) & 1));
             tc_fence_after();
@@ -523,6 +523,7 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
                 }
                 n_exact += qn;
                 qn = 0;
+                __syncwarp();  // reconverge after the (rare, divergent) exact path
                 if (g + 1 < G) tc_wait_ld();
             }
             tc_fence_before();
