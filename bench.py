@@ -39,8 +39,8 @@ UNIT = "pairs/s"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["fic", "reference"], default="fic")
     ap.add_argument("--config", default="C3")
     ap.add_argument("--s-mode", default="predefined", choices=["predefined", "grid"])
@@ -71,7 +71,7 @@ class ClockSampler:
             os.close(fd)
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
@@ -319,7 +319,8 @@ def main():
                    "l2": "flushed between timed steps (256 MB write)",
                    "pairs_per_step": pairs_step, "records_per_step": n_rec},
         "roofline": {"bound": "alu" if 4.0 * n / p_int8 < 2.0 / p_int32 + 0.5 * nS / p_fp64 else "tensor",
-                     "kernel": f"tcsearch_kernel<B={dom['B']}>",
+                     "kernel": ("b2search_kernel (B=2 closed form, CUDA cores)" if dom["B"] == 2
+                                else f"tcsearch_kernel<B={dom['B']}> (tcgen05 kind::i8)"),
                      "achieved": achieved, "peak": peak, "unit": "Gpairs/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "peak_note": "SURVEY 8(d): 1/max(4n/P_int8, 2/P_int32 + 0.5|S|/P_fp64) pairs/s; "

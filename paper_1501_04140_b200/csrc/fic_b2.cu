@@ -16,6 +16,7 @@
 #include <cfloat>
 #include <climits>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "fic_internal.cuh"
@@ -106,9 +107,9 @@ struct B2Cold {
     int32_t SR;
 };
 
-constexpr int kB2TPS = 8;   // tiles per stage
+constexpr int kB2TPS = 4;   // tiles per stage
 constexpr int kB2RPT = 4;   // ranges per thread
-constexpr int kB2Threads = 128;
+constexpr int kB2Threads = 256;
 
 // k* of one (range, domain): all 8 SRD_k in integers (isometry convention of the oracle,
 // reading R2), lowest index of the maximum.  Only called when the pair improves the best.
@@ -267,32 +268,49 @@ __global__ void __launch_bounds__(kB2Threads) b2search_kernel(const __grid_const
             const float4 *Ft = Fb + tt * kTileD;
             const float *Ut = Ub + tt * P.nsp * kTileD;
             const int dbase = (ta + tt) * kTileD;
-#pragma unroll 4
-            for (int dl = 0; dl < kTileD; ++dl) {
-                const float4 f = Ft[dl];
-                float t2[NSP];
+#pragma unroll 2
+            for (int dl0 = 0; dl0 < kTileD; dl0 += 2) {
+                // two domains per block: the filters of 2 x RPT pairs interleave, one branch
+                float4 f2[2];
+                float t2v[2][NSP];
+                float mn[2];
 #pragma unroll
-                for (int jj = 0; jj < NSP; ++jj) t2[jj] = jj < P.nsp ? Ut[jj * kTileD + dl] : INFINITY;
-                unsigned pm = 0;
+                for (int u2 = 0; u2 < 2; ++u2) {
+                    f2[u2] = Ft[dl0 + u2];
 #pragma unroll
-                for (int q = 0; q < RPT; ++q) {
-                    const float v1 = fmaf(X2[q], f.x, fmaf(xr2[q], f.y, xi2[q] * f.z));
-                    const float v2 = fmaf(-X2[q], f.x, fmaf(xr2[q], f.z, xi2[q] * f.y));
-                    const float bq = fmaxf(v1, v2);  // = max_k Bq_k, exact
-                    float g = fmaf(nhs[0], bq, t2[0]);
+                    for (int jj = 0; jj < NSP; ++jj)
+                        t2v[u2][jj] = jj < P.nsp ? Ut[jj * kTileD + dl0 + u2] : INFINITY;
+                    mn[u2] = 1.0f;  // min over ranges of (lower bound - threshold): <= 0 -> some pass
 #pragma unroll
-                    for (int jj = 1; jj < NSP; ++jj) g = fminf(g, fmaf(nhs[jj], bq, t2[jj]));
-                    pm |= (g <= thr[q]) ? (1u << q) : 0u;
+                    for (int q = 0; q < RPT; ++q) {
+                        const float4 f = f2[u2];
+                        const float v1 = fmaf(X2[q], f.x, fmaf(xr2[q], f.y, xi2[q] * f.z));
+                        const float v2 = fmaf(-X2[q], f.x, fmaf(xr2[q], f.z, xi2[q] * f.y));
+                        const float bq = fmaxf(v1, v2);  // = max_k Bq_k, exact
+                        float g = fmaf(nhs[0], bq, t2v[u2][0]);
+#pragma unroll
+                        for (int jj = 1; jj < NSP; ++jj) g = fminf(g, fmaf(nhs[jj], bq, t2v[u2][jj]));
+                        mn[u2] = fminf(mn[u2], g - thr[q]);
+                    }
                 }
-                if (pm) {
+                if (fminf(mn[0], mn[1]) <= 0.0f) {
 #pragma unroll
-                    for (int q = 0; q < RPT; ++q)
-                        if (pm >> q & 1) {
+                    for (int u2 = 0; u2 < 2; ++u2) {
+                        const float4 f = f2[u2];
+#pragma unroll
+                        for (int q = 0; q < RPT; ++q) {
                             const float bq = fmaxf(fmaf(X2[q], f.x, fmaf(xr2[q], f.y, xi2[q] * f.z)),
                                                    fmaf(-X2[q], f.x, fmaf(xr2[q], f.z, xi2[q] * f.y)));
-                            thr[q] = b2_exact(P, &cold[q * kB2Threads + threadIdx.x], thr[q], rbase + q, dbase + dl, bq, f.w);
-                            ++n_exact;
+                            float g = fmaf(nhs[0], bq, t2v[u2][0]);
+#pragma unroll
+                            for (int jj = 1; jj < NSP; ++jj) g = fminf(g, fmaf(nhs[jj], bq, t2v[u2][jj]));
+                            if (g <= thr[q]) {
+                                thr[q] = b2_exact(P, &cold[q * kB2Threads + threadIdx.x], thr[q], rbase + q,
+                                                  dbase + dl0 + u2, bq, f.w);
+                                ++n_exact;
+                            }
                         }
+                    }
                 }
                 __syncwarp();  // reconverge after the (rare, divergent) exact path
             }
@@ -339,7 +357,11 @@ static cudaError_t launch_b2_t(const B2Params &p, cudaStream_t st) {
 int b2_nsplit_hint(int64_t n_r, int64_t n_tiles, int num_sms) {
     const int64_t gx = (n_r + kB2Threads * kB2RPT - 1) / (kB2Threads * kB2RPT);
     if (gx <= 0 || n_tiles <= 0) return 1;
-    int64_t ns = ((int64_t)num_sms * 8 + gx - 1) / gx;
+    static int waves = [] {
+        const char *e = getenv("FIC_B2_CTAS_PER_SM");
+        return e ? atoi(e) : 8;
+    }();
+    int64_t ns = ((int64_t)num_sms * waves + gx - 1) / gx;
     const int64_t max_ns = (n_tiles + kB2TPS - 1) / kB2TPS;
     if (ns > max_ns) ns = max_ns;
     if (ns < 1) ns = 1;
