@@ -36,7 +36,7 @@ struct fic_ctx {
     cudaEvent_t ev[fic::kMaxLevels][5] = {};
     int64_t launches = 0;
     int search_mode = 0;  // env FIC_SEARCH: auto (default: B=2 closed form, else tcgen05) | fourier | direct | tc
-    Buf b_rc, b_meta, b_u, b_gthr;  // libfic kernels enqueued (for fic_level_stats.kernel_launches)  // pool start, search start, search end, finalize end, pool end
+    Buf b_rc, b_meta, b_u, b_gthr, b_rop;  // libfic kernels enqueued (for fic_level_stats.kernel_launches)  // pool start, search start, search end, finalize end, pool end
 };
 
 namespace {
@@ -263,7 +263,11 @@ fic_status level_enqueue(fic_ctx *ctx, const Pool &P, const uint8_t *img, const 
         sp.t2f = ptr<float>(ctx->b_t2f);
         if (sp.nsp > 0) {
             if (P.mode == 2) CK(fic::launch_search(P.B, sp.nsp, sp, st));
-            else CK(fic::launch_tc_search(P.B, sp, P.Dtc, slots, st));
+            else {
+                CK(grow(ctx, ctx->b_rop, fic::tc_range_bytes(P.B, n_r)));
+                CK(fic::launch_tc_search(P.B, sp, P.Dtc, slots, ptr<uint8_t>(ctx->b_rop), st));
+                ctx->launches += 2;
+            }
             ctx->launches += 1;
         }
     } else if (P.mode == 3) {
@@ -385,7 +389,7 @@ fic_status fic_ctx_destroy(fic_ctx *ctx) {
     for (auto &P : ctx->levels) free_pool(P);
     Buf *bufs[] = {&ctx->b_blocksum, &ctx->b_counts, &ctx->b_rng[0], &ctx->b_rng[1], &ctx->b_rec,
                    &ctx->b_acc, &ctx->b_child, &ctx->b_part, &ctx->b_t2f, &ctx->b_img, &ctx->b_out,
-                   &ctx->b_scounts, &ctx->b_rc, &ctx->b_meta, &ctx->b_u, &ctx->b_gthr};
+                   &ctx->b_scounts, &ctx->b_rc, &ctx->b_meta, &ctx->b_u, &ctx->b_gthr, &ctx->b_rop};
     for (Buf *b : bufs) free_buf(*b);
     if (ctx->d_delta) cudaFree(ctx->d_delta);
     if (ctx->h_counts) cudaFreeHost(ctx->h_counts);

@@ -141,8 +141,9 @@ int tc_nsplit_hint(int32_t B, int64_t n_r, int64_t n_tiles, int num_sms);
 cudaError_t launch_pool_tc(const uint8_t *img, int32_t N, int32_t B, int32_t L, int32_t A,
                            const int32_t *kept, const unsigned long long *d_nk, int64_t n_tiles_max,
                            uint8_t *Dtc, cudaStream_t st);
+size_t tc_range_bytes(int B, int64_t n_r);  // scratch for the prepared range operand + metadata
 cudaError_t launch_tc_search(int32_t B, const SearchParams &sp, const uint8_t *Dtc, int64_t n_slots,
-                             cudaStream_t st);
+                             uint8_t *scratch, cudaStream_t st);
 
 // D4 group-Fourier search (fic_fourier.cu), B in {2, 4, 8}
 cudaError_t fourier_init();

@@ -228,8 +228,91 @@ cudaError_t launch_pool_tc(const uint8_t *img, int32_t N, int32_t B, int32_t L, 
     return cudaGetLastError();
 }
 
+// ------------------------------------------------------------------------------ range operand
+// Per group of NR ranges: rows (rl, k) = Rperm_k replicated over the 4 polyphase planes, K-major
+// core-matrix layout, B_BYTES contiguous bytes (one bulk copy per CTA); zero rows past n_r.
+template <int B>
+__global__ void __launch_bounds__(256) tc_range_operand_kernel(const uint8_t *__restrict__ img, int32_t N,
+                                                               const int2 *__restrict__ ranges, int32_t n_r,
+                                                               int64_t total16, uint8_t *__restrict__ Bop) {
+    using Cf = TCfg<B>;
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // one 16-byte group
+    if (e >= total16) return;
+    constexpr int G16 = Cf::KP / 16;
+    const int64_t row_g = e / G16;  // global row = group * N + row
+    const int g = (int)(e % G16);
+    const int64_t grp = row_g / Cf::N;
+    const int row = (int)(row_g % Cf::N);
+    const int rl = row >> 3, k = row & 7;
+    const int64_t r = grp * Cf::NR + rl;
+    uint32_t w[4] = {0, 0, 0, 0};
+    if (r < n_r) {
+        const int2 rr = ranges[r];
+        // Rperm_k(p) = R(f_k^{-1}(p)); under this numbering f_k^{-1} = f_{k'} with
+        // k' = [0,3,2,1,4,5,6,7][k] (rotations by 90/270 swap, the rest are involutions)
+        const int kinv = (k == 1) ? 3 : (k == 3 ? 1 : k);
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+            const int kb = g * 16 + q;
+            uint32_t v = 0;
+            if (kb < 4 * Cf::n) {
+                const int p = kb % Cf::n;
+                int si, sj;
+                tiso_src(B, kinv, p / B, p % B, si, sj);
+                v = img[(size_t)(rr.y + si) * N + rr.x + sj];
+            }
+            w[q >> 2] |= v << (8 * (q & 3));
+        }
+    }
+    uint8_t *dst = Bop + (size_t)grp * Cf::B_BYTES + cm_off(row, g * 16, Cf::KP);
+    *reinterpret_cast<uint4 *>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+struct TCRangeG {
+    double A, margin;
+    int32_t SR;
+    int32_t valid;
+};
+
+// Thread per range: SR, A = n SRR - SR^2 and the filter margin
+template <int B>
+__global__ void tc_range_meta_kernel(const uint8_t *__restrict__ img, int32_t N, const int2 *__restrict__ ranges,
+                                     int32_t n_r, int32_t n_pad, double smax, double cmax,
+                                     TCRangeG *__restrict__ meta) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n_pad) return;
+    constexpr int n = B * B;
+    TCRangeG R;
+    long long sr = 0, srr = 0;
+    R.valid = r < n_r;
+    if (R.valid) {
+        const int2 rr = ranges[r];
+        for (int i = 0; i < B; ++i) {
+            const uint8_t *row = img + (size_t)(rr.y + i) * N + rr.x;
+#pragma unroll
+            for (int j = 0; j < B; ++j) {
+                const int v = row[j];
+                sr += v;
+                srr += v * v;
+            }
+        }
+    }
+    R.A = (double)((long long)n * srr - sr * sr);
+    R.SR = (int32_t)sr;
+    // fp32 filter error: |Bq| <= sqrt(A C) (Cauchy-Schwarz); conversions, hs and t2 roundings,
+    // two FFMA roundings, SR*SD rounding at B = 16 -> 8u (hs (sqrt(A Cmax) + n 1020 SR) + t2max)
+    const double u = 5.9604644775390625e-08;
+    const double hs = 0.5 * smax;
+    const double bq = sqrt(R.A * cmax) * 1.01 + (B > 8 ? (double)n * 1020.0 * (double)sr : 0.0);
+    const double t2m = smax * smax * cmax * 0.0625;
+    R.margin = 8.0 * u * (hs * bq + t2m) + 1e-12 * (R.A + hs * bq + t2m) + 1e-30;
+    meta[r] = R;
+}
+
 // ------------------------------------------------------------------------------ search kernel
 struct TCParams {
+    const uint8_t *Bop;        // [groups][B_BYTES] range operand
+    const TCRangeG *rmeta;     // [groups * NR]
     const uint8_t *img;
     int32_t N;
     const int2 *ranges;
@@ -249,11 +332,7 @@ struct TCParams {
     unsigned long long *exact_count;
 };
 
-struct TCRange {
-    double A, margin;
-    int32_t SR;
-    int32_t valid;
-};
+using TCRange = TCRangeG;
 
 template <int B, int NSP>
 __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __grid_constant__ TCParams P) {
@@ -268,9 +347,10 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
     float *sThr = reinterpret_cast<float *>(sR + NR);          // [NR] RU(best - A + margin), CAS-min
     float *sHsn = reinterpret_cast<float *>(sThr + NR);        // [NSP]
     Partial *sRed = reinterpret_cast<Partial *>(sHsn + 16);    // [NR][4]
-    uint64_t *bar = reinterpret_cast<uint64_t *>(sRed + NR * 4);  // full[S], empty[S], tfull[2], tempty[2]
+    uint64_t *bar = reinterpret_cast<uint64_t *>(sRed + NR * 4);  // full[S], empty[S], tfull[2], tempty[2], bop
     uint64_t *full = bar, *empty = bar + STAGES, *tfull = bar + 2 * STAGES, *tempty = tfull + 2;
-    uint32_t *sTmem = reinterpret_cast<uint32_t *>(tempty + 2);
+    uint64_t *bbar = tempty + 2;
+    uint32_t *sTmem = reinterpret_cast<uint32_t *>(bbar + 2);
     Partial *sBest = reinterpret_cast<Partial *>(sTmem + 4);  // [NR][128] per (range, domain lane)
     int2 *sQ = reinterpret_cast<int2 *>(sBest + NR * kTileD);  // [epilogue threads][4] exact queue
 
@@ -292,68 +372,22 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
             tmbar_init(&tfull[b], 1);
             tmbar_init(&tempty[b], 4 * Cf::EWG);
         }
+        tmbar_init(bbar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(sTmem)),
                      "r"(kTmemCols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
-    // range operand: row (rl, k) = Rperm_k replicated over the 4 planes; zero padding
-    for (int idx = threadIdx.x; idx < NN * (KP / 4); idx += blockDim.x) {
-        const int row = idx / (KP / 4), kw = idx % (KP / 4);
-        const int rl = row >> 3, k = row & 7;
-        const int r = r0 + rl;
-        uint32_t w = 0;
-        if (r < P.n_r) {
-            const int2 rr = P.ranges[r];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const int kb = kw * 4 + q;
-                if (kb < 4 * n) {
-                    // Rperm_k(p) = R(f_k^{-1}(p)); under this numbering f_k^{-1} = f_{k'} with
-                    // k' = [0,3,2,1,4,5,6,7][k] (rotations by 90/270 swap, the rest are involutions)
-                    const int p = kb % n;
-                    const int kinv = (k == 1) ? 3 : (k == 3 ? 1 : k);
-                    int si, sj;
-                    tiso_src(B, kinv, p / B, p % B, si, sj);
-                    const uint32_t v = P.img[(size_t)(rr.y + si) * P.N + rr.x + sj];
-                    w |= v << (8 * q);
-                }
-            }
-        }
-        *reinterpret_cast<uint32_t *>(sB + cm_off(row, kw * 4, KP)) = w;
-    }
     if (threadIdx.x < NR) {
-        const int r = r0 + threadIdx.x;
-        TCRange R;
-        long long sr = 0, srr = 0;
-        R.valid = r < P.n_r;
-        if (R.valid) {
-            const int2 rr = P.ranges[r];
-            for (int i = 0; i < B; ++i)
-                for (int j = 0; j < B; ++j) {
-                    const int v = P.img[(size_t)(rr.y + i) * P.N + rr.x + j];
-                    sr += v;
-                    srr += v * v;
-                }
-        }
-        R.A = (double)((long long)n * srr - sr * sr);
-        R.SR = (int32_t)sr;
-        // fp32 filter error: |Bq| <= sqrt(A C) (Cauchy-Schwarz); conversions, hs and t2 roundings,
-        // two FFMA roundings, SR*SD rounding at B = 16 -> 8u (hs (sqrt(A Cmax) + n 1020 SR) + t2max)
-        const double u = 5.9604644775390625e-08;
-        const double hs = 0.5 * P.smax;
-        // B <= 8: Bq is exact in int32 and |Bq| <= sqrt(A C); B = 16: fp32 n max SRD - SR SD
-        const double bq = sqrt(R.A * P.cmax) * 1.01 + (B > 8 ? (double)n * 1020.0 * (double)sr : 0.0);
-        const double t2m = P.smax * P.smax * P.cmax * 0.0625;
-        R.margin = 8.0 * u * (hs * bq + t2m) + 1e-12 * (R.A + hs * bq + t2m) + 1e-30;
+        const TCRange R = P.rmeta[r0 + threadIdx.x];
         sR[threadIdx.x] = R;
         const float th = P.has_zero ? fminf(__double2float_ru(R.margin), FLT_MAX) : FLT_MAX;
         sThr[threadIdx.x] = R.valid ? th : -FLT_MAX;
     }
     if (threadIdx.x < 16) sHsn[threadIdx.x] = threadIdx.x < P.nsp ? -__double2float_rn(0.5 * P.spos[threadIdx.x]) : 0.f;
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes of sB -> tensor core
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -362,6 +396,9 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
     if (warp == 0) {
         // ================= producer: one bulk copy per (tile, chunk) stage
         if (lane == 0) {
+            // the resident range operand of this CTA's NR ranges (prepared by tc_range_operand_kernel)
+            tmbar_expect_tx(bbar, Cf::B_BYTES);
+            tbulk_g2s(sB, P.Bop + (size_t)blockIdx.x * Cf::B_BYTES, Cf::B_BYTES, bbar);
             for (int i = 0; i < nsteps; ++i) {
                 const int s = i % STAGES;
                 if (i >= STAGES) tmbar_wait(&empty[s], (uint32_t)(((i / STAGES) + 1) & 1));
@@ -374,6 +411,7 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
     } else if (warp == 1) {
         // ================= MMA issuer
         constexpr uint32_t idesc = idesc_i8(NN);
+        if (nsteps > 0) tmbar_wait(bbar, 0);
         for (int i = 0; i < nsteps; ++i) {
             const int s = i % STAGES;
             const int tl = i / CH, ch = i % CH;
@@ -574,7 +612,7 @@ template <int B, int NSP>
 static size_t tc_smem_bytes() {
     using Cf = TCfg<B>;
     return (size_t)Cf::STAGES * Cf::STAGE_BYTES + Cf::B_BYTES + sizeof(TCRange) * Cf::NR + 4 * Cf::NR +
-           4 * 16 + sizeof(Partial) * Cf::NR * 4 + 8 * (2 * Cf::STAGES + 4) + 16 +
+           4 * 16 + sizeof(Partial) * Cf::NR * 4 + 8 * (2 * Cf::STAGES + 6) + 16 +
            sizeof(Partial) * Cf::NR * kTileD + sizeof(int2) * 128 * Cf::EWG * 4 + 1024;
 }
 
@@ -603,11 +641,49 @@ static cudaError_t launch_tc_b(const TCParams &p, cudaStream_t st) {
 
 int tc_ranges_per_cta(int B) { return B == 16 ? 16 : 32; }
 
+size_t tc_range_bytes(int B, int64_t n_r) {
+    switch (B) {
+    case 2: return (size_t)((n_r + TCfg<2>::NR - 1) / TCfg<2>::NR) * (TCfg<2>::B_BYTES + TCfg<2>::NR * sizeof(TCRangeG));
+    case 4: return (size_t)((n_r + TCfg<4>::NR - 1) / TCfg<4>::NR) * (TCfg<4>::B_BYTES + TCfg<4>::NR * sizeof(TCRangeG));
+    case 8: return (size_t)((n_r + TCfg<8>::NR - 1) / TCfg<8>::NR) * (TCfg<8>::B_BYTES + TCfg<8>::NR * sizeof(TCRangeG));
+    case 16: return (size_t)((n_r + TCfg<16>::NR - 1) / TCfg<16>::NR) * (TCfg<16>::B_BYTES + TCfg<16>::NR * sizeof(TCRangeG));
+    default: return 0;
+    }
+}
+
+template <int B>
+static cudaError_t tc_range_prep(const SearchParams &sp, uint8_t *scratch, TCParams &p, cudaStream_t st) {
+    using Cf = TCfg<B>;
+    const int64_t groups = (sp.n_r + Cf::NR - 1) / Cf::NR;
+    uint8_t *Bop = scratch;
+    TCRangeG *meta = reinterpret_cast<TCRangeG *>(scratch + (size_t)groups * Cf::B_BYTES);
+    const int64_t total16 = groups * Cf::N * (Cf::KP / 16);
+    tc_range_operand_kernel<B><<<(unsigned)((total16 + 255) / 256), 256, 0, st>>>(sp.img, sp.N, sp.ranges,
+                                                                                  sp.n_r, total16, Bop);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    const int n_pad = (int)(groups * Cf::NR);
+    tc_range_meta_kernel<B><<<(unsigned)((n_pad + 127) / 128), 128, 0, st>>>(sp.img, sp.N, sp.ranges, sp.n_r,
+                                                                              n_pad, sp.smax, sp.cmax, meta);
+    p.Bop = Bop;
+    p.rmeta = meta;
+    return cudaGetLastError();
+}
+
 cudaError_t launch_tc_search(int32_t B, const SearchParams &sp, const uint8_t *Dtc, int64_t n_slots,
-                             cudaStream_t st) {
+                             uint8_t *scratch, cudaStream_t st) {
     if (sp.n_r == 0 || sp.nsp == 0) return cudaSuccess;
     TCParams p;
     memset(&p, 0, sizeof p);
+    cudaError_t e0 = cudaSuccess;
+    switch (B) {
+    case 2: e0 = tc_range_prep<2>(sp, scratch, p, st); break;
+    case 4: e0 = tc_range_prep<4>(sp, scratch, p, st); break;
+    case 8: e0 = tc_range_prep<8>(sp, scratch, p, st); break;
+    case 16: e0 = tc_range_prep<16>(sp, scratch, p, st); break;
+    default: return cudaErrorInvalidValue;
+    }
+    if (e0 != cudaSuccess) return e0;
     p.img = sp.img; p.N = sp.N; p.ranges = sp.ranges; p.n_r = sp.n_r;
     p.Dtc = Dtc; p.SD = sp.SD; p.C = sp.C; p.t2f = sp.t2f; p.n_slots = n_slots;
     p.n_tiles = sp.n_tiles; p.tiles_per_split = sp.tiles_per_split; p.nsplit = sp.nsplit;
