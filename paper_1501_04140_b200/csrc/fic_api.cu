@@ -35,6 +35,10 @@ struct fic_ctx {
     std::vector<fic_level_stats> stats;
     cudaEvent_t ev[fic::kMaxLevels][5] = {};
     int64_t launches = 0;
+    cudaStream_t side = nullptr;                 // pool builds of levels >= 1 overlap the searches
+    int overlap_pools = 0;                       // env FIC_OVERLAP_POOLS=1
+    cudaEvent_t pool_ready[fic::kMaxLevels] = {};
+    cudaEvent_t main_ready = nullptr;
     int search_mode = 0;  // env FIC_SEARCH: auto (default: B=2 closed form, else tcgen05) | fourier | direct | tc
     Buf b_rc, b_meta, b_u, b_gthr, b_rop;  // libfic kernels enqueued (for fic_level_stats.kernel_launches)  // pool start, search start, search end, finalize end, pool end
 };
@@ -94,7 +98,7 @@ void free_buf(Buf &b) {
 void free_pool(Pool &P) {
     free_buf(P.b_keys); free_buf(P.b_keep); free_buf(P.b_kept); free_buf(P.b_Dt);
     free_buf(P.b_SDf); free_buf(P.b_SD); free_buf(P.b_C); free_buf(P.b_misc); free_buf(P.b_Dc);
-    free_buf(P.b_Dtc); free_buf(P.b_F2);
+    free_buf(P.b_Dtc); free_buf(P.b_F2); free_buf(P.b_blocksum);
 }
 
 bool pow2(int32_t v) { return v > 0 && (v & (v - 1)) == 0; }
@@ -122,7 +126,7 @@ int64_t entropy_threshold(double tau, int32_t m) {
 
 // ------------------------------------------------------------------------- pool building
 fic_status pool_enqueue(fic_ctx *ctx, Pool &P, const uint8_t *img, int32_t N, int32_t B,
-                        int32_t L, double tau) {
+                        int32_t L, double tau, cudaStream_t st) {
     P.device = ctx->device;
     P.N = N; P.B = B; P.L = L; P.n = B * B;
     P.A = (N - 2 * B) / L + 1;
@@ -144,7 +148,8 @@ fic_status pool_enqueue(fic_ctx *ctx, Pool &P, const uint8_t *img, int32_t N, in
     CK(grow(ctx, P.b_SD, sizeof(int32_t) * slots));
     CK(grow(ctx, P.b_C, sizeof(int64_t) * slots));
     CK(grow(ctx, P.b_misc, 4 * sizeof(unsigned long long)));
-    CK(grow(ctx, ctx->b_blocksum, sizeof(int64_t) * fic::select_blocksum_len(P.n_c)));
+    CK(grow(ctx, P.b_blocksum, sizeof(int64_t) * fic::select_blocksum_len(P.n_c)));
+    P.n_tiles_max = tiles_max;
     P.keys = ptr<int64_t>(P.b_keys); P.keep = ptr<uint8_t>(P.b_keep);
     P.kept = ptr<int32_t>(P.b_kept); P.SDf = ptr<float>(P.b_SDf);
     P.Dt = P.mode == 2 ? ptr<float>(P.b_Dt) : nullptr;
@@ -153,15 +158,13 @@ fic_status pool_enqueue(fic_ctx *ctx, Pool &P, const uint8_t *img, int32_t N, in
     P.F2 = P.mode == 3 ? ptr<float4>(P.b_F2) : nullptr;
     P.SD = ptr<int32_t>(P.b_SD); P.C = ptr<int64_t>(P.b_C);
     P.d_misc = ptr<unsigned long long>(P.b_misc);
-    cudaStream_t st = ctx->stream;
     CK(cudaMemsetAsync(P.d_misc, 0, 4 * sizeof(unsigned long long), st));
     const int32_t m = 4 * B * B;
     const int use_tau = tau >= 0.0;
     const int64_t T = use_tau ? entropy_threshold(tau, m) : 0;
     CK(fic::launch_entropy_keys(img, N, B, L, P.A, ctx->d_delta, ctx->lut[m], T, use_tau, P.keys,
                                 P.keep, st));
-    CK(fic::launch_select_index(P.keep, P.n_c, ptr<int64_t>(ctx->b_blocksum), P.kept, &P.d_misc[0],
-                                st));
+    CK(fic::launch_select_index(P.keep, P.n_c, ptr<int64_t>(P.b_blocksum), P.kept, &P.d_misc[0], st));
     if (P.mode == 2)
         CK(fic::launch_pool_gather(img, N, B, L, P.A, P.kept, &P.d_misc[0], tiles_max, P.Dt, st));
     else if (P.mode == 0)
@@ -209,21 +212,28 @@ fic_status check_s(fic_ctx *ctx, const double *h_s, int32_t n_s) {
 }
 
 // --------------------------------------------------------------------------- one level
-// ranges: device int2 [n_r]; writes rec [n_r], acc [n_r], and child marks (if child != null).
+// ranges: device int2 [n_r]; the range count is *d_nr (device), n_r_max a host upper bound that
+// sizes grids and buffers.  Writes rec [n_r], acc [n_r_max] (0 past n_r) and child marks.
 fic_status level_enqueue(fic_ctx *ctx, const Pool &P, const uint8_t *img, const int2 *ranges,
-                         int64_t n_r, const double *h_s, int32_t n_s, double rms_tol, int is_min,
-                         fic_record *rec, uint8_t *acc, uint8_t *child, int level_slot) {
+                         const unsigned long long *d_nr, int64_t n_r_max, const double *h_s, int32_t n_s,
+                         double rms_tol, int is_min, fic_record *rec, uint8_t *acc, uint8_t *child,
+                         int level_slot, int32_t *d_err) {
     cudaStream_t st = ctx->stream;
-    if (n_r == 0) return FIC_OK;
+    if (n_r_max == 0) return FIC_OK;
     fic::SearchParams sp;
     memset(&sp, 0, sizeof sp);
     sp.img = img;
     sp.N = P.N;
     sp.ranges = ranges;
-    sp.n_r = (int32_t)n_r;
+    sp.n_r = (int32_t)n_r_max;
+    sp.d_nr = d_nr;
+    sp.d_misc = P.d_misc;
     sp.Dt = P.Dt; sp.SDf = P.SDf; sp.SD = P.SD; sp.C = P.C;
-    sp.n_k = (int32_t)P.n_k;
-    sp.n_tiles = (int32_t)P.n_tiles;
+    const int64_t tiles = P.n_tiles_max;
+    sp.n_k = (int32_t)(tiles * fic::kTileD);
+    sp.n_tiles = (int32_t)tiles;
+    const int64_t slots = tiles * fic::kTileD;
+    sp.slot_stride = slots;
     sp.has_zero = 0;
     sp.j_zero = 0;
     sp.smax = 0.0;
@@ -237,59 +247,57 @@ fic_status level_enqueue(fic_ctx *ctx, const Pool &P, const uint8_t *img, const 
         }
         if (h_s[j] > sp.smax) sp.smax = h_s[j];
     }
-    sp.cmax = (double)P.cmax;
-    const int64_t slots = P.n_tiles * fic::kTileD;
     if (P.mode == 2)
-        sp.nsplit = fic::search_nsplit_hint(P.B, n_r, P.n_tiles, ctx->num_sms);
+        sp.nsplit = fic::search_nsplit_hint(P.B, n_r_max, tiles, ctx->num_sms);
     else if (P.mode == 0)
-        sp.nsplit = fic::tc_nsplit_hint(P.B, n_r, P.n_tiles, ctx->num_sms);
+        sp.nsplit = fic::tc_nsplit_hint(P.B, n_r_max, tiles, ctx->num_sms);
     else if (P.mode == 3)
-        sp.nsplit = fic::b2_nsplit_hint(n_r, P.n_tiles, ctx->num_sms);
+        sp.nsplit = fic::b2_nsplit_hint(n_r_max, tiles, ctx->num_sms);
     else
-        sp.nsplit = fic::fourier_nsplit_hint(P.B, sp.nsp, n_r, P.n_tiles, ctx->num_sms);
-    sp.tiles_per_split = (int32_t)((P.n_tiles + sp.nsplit - 1) / sp.nsplit);
-    sp.nsplit = (int32_t)((P.n_tiles + sp.tiles_per_split - 1) / sp.tiles_per_split);
+        sp.nsplit = fic::fourier_nsplit_hint(P.B, sp.nsp, n_r_max, tiles, ctx->num_sms);
+    if (sp.nsplit < 1) sp.nsplit = 1;
+    sp.tiles_per_split = (int32_t)((tiles + sp.nsplit - 1) / sp.nsplit);
+    // dynamic kernels (tcgen05, B=2) choose their split count on the device, up to ns_cap
+    const bool dyn = (P.mode == 0 || P.mode == 3);
+    sp.ns_cap = dyn ? (int32_t)std::min<int64_t>(4 * (int64_t)sp.nsplit, std::max<int64_t>(1, tiles)) : sp.nsplit;
+    sp.d_ns = ptr<unsigned long long>(ctx->b_counts) + 56 + level_slot;
+    if (!dyn) CK(fic::launch_set_u64(sp.d_ns, (unsigned long long)sp.nsplit, st));
     CK(grow(ctx, ctx->b_t2f, sizeof(float) * (size_t)slots * (sp.nsp ? sp.nsp : 1)));
-    CK(grow(ctx, ctx->b_part, sizeof(fic::Partial) * (size_t)n_r * sp.nsplit));
+    CK(grow(ctx, ctx->b_part, sizeof(fic::Partial) * (size_t)n_r_max * sp.ns_cap));
     sp.t2f = ptr<float>(ctx->b_t2f);
     sp.part = ptr<fic::Partial>(ctx->b_part);
     sp.exact_count = ptr<unsigned long long>(ctx->b_counts) + 8 + level_slot;
+    fic::SList sl;
+    memcpy(sl.s, sp.spos, sizeof sl.s);
     if (P.mode == 2 || P.mode == 0) {
-        fic::SList sl;
-        memcpy(sl.s, sp.spos, sizeof sl.s);
-        CK(fic::launch_t2f(P.C, (int32_t)P.n_k, slots, sl, sp.nsp, ptr<float>(ctx->b_t2f), st));
+        CK(fic::launch_t2f(P.C, &P.d_misc[0], slots, sl, sp.nsp, ptr<float>(ctx->b_t2f), st));
         if (sp.nsp > 0 && slots > 0) ctx->launches += 1;
         if (ctx->timing) CK(cudaEventRecord(ctx->ev[level_slot][1], st));
-        sp.t2f = ptr<float>(ctx->b_t2f);
         if (sp.nsp > 0) {
             if (P.mode == 2) CK(fic::launch_search(P.B, sp.nsp, sp, st));
             else {
-                CK(grow(ctx, ctx->b_rop, fic::tc_range_bytes(P.B, n_r)));
+                CK(grow(ctx, ctx->b_rop, fic::tc_range_bytes(P.B, n_r_max)));
                 CK(fic::launch_tc_search(P.B, sp, P.Dtc, slots, ptr<uint8_t>(ctx->b_rop), st));
                 ctx->launches += 2;
             }
             ctx->launches += 1;
         }
     } else if (P.mode == 3) {
-        fic::SList sl;
-        memcpy(sl.s, sp.spos, sizeof sl.s);
         CK(grow(ctx, ctx->b_u, sizeof(float) * (size_t)slots * (sp.nsp ? sp.nsp : 1)));
-        CK(fic::launch_fourier_u(P.C, (int32_t)P.n_k, slots, sl, sp.nsp, ptr<float>(ctx->b_u), st));
+        CK(fic::launch_fourier_u(P.C, &P.d_misc[0], slots, sl, sp.nsp, ptr<float>(ctx->b_u), st));
         if (ctx->timing) CK(cudaEventRecord(ctx->ev[level_slot][1], st));
-        CK(grow(ctx, ctx->b_gthr, sizeof(float) * (size_t)n_r));
+        CK(grow(ctx, ctx->b_gthr, sizeof(float) * (size_t)n_r_max));
         CK(fic::launch_b2_search(sp, P.F2, ptr<float>(ctx->b_u), P.kept, P.L, P.A, ptr<float>(ctx->b_gthr), st));
         ctx->launches += sp.nsp > 0 ? 2 : 0;
     } else {
         const int nc = fic::fourier_record_stride(P.B);  // >= 8 nO + 1
-        const int32_t r_stride = (int32_t)((n_r + 31) / 32 * 32);
+        const int32_t r_stride = (int32_t)((n_r_max + 31) / 32 * 32);
         CK(grow(ctx, ctx->b_rc, sizeof(float) * (size_t)nc * r_stride));
-        CK(grow(ctx, ctx->b_meta, fic::fourier_meta_bytes() * (size_t)n_r));
+        CK(grow(ctx, ctx->b_meta, fic::fourier_meta_bytes() * (size_t)n_r_max));
         CK(grow(ctx, ctx->b_u, sizeof(float) * (size_t)slots * (sp.nsp ? sp.nsp : 1)));
         if (ctx->timing) CK(cudaEventRecord(ctx->ev[level_slot][1], st));
-        CK(fic::launch_fourier_level(P.B, img, P.N, ranges, (int32_t)n_r, P.Dc, P.C, (int32_t)P.n_k,
-                                     (int32_t)P.n_tiles, sp.nsplit, sp.tiles_per_split, sp, P.dnmax,
-                                     ptr<float>(ctx->b_rc), r_stride, ctx->b_meta.p, ptr<float>(ctx->b_u),
-                                     st));
+        CK(fic::launch_fourier_level(P.B, sp, P.Dc, ptr<float>(ctx->b_rc), r_stride, ctx->b_meta.p,
+                                     ptr<float>(ctx->b_u), st));
         ctx->launches += 1 + (sp.nsp > 0 ? 2 : 0);
     }
     if (ctx->timing) CK(cudaEventRecord(ctx->ev[level_slot][2], st));
@@ -297,16 +305,21 @@ fic_status level_enqueue(fic_ctx *ctx, const Pool &P, const uint8_t *img, const 
     memset(&fp, 0, sizeof fp);
     fp.img = img; fp.N = P.N; fp.B = P.B; fp.L = P.L; fp.A = P.A;
     fp.ranges = ranges;
-    fp.n_r = (int32_t)n_r;
-    fp.nsplit = sp.nsp > 0 ? sp.nsplit : 0;
+    fp.n_r = (int32_t)n_r_max;
+    fp.d_nr = d_nr;
+    fp.d_misc = P.d_misc;
+    fp.d_err = d_err;
+    fp.nsplit = sp.nsp > 0 ? sp.ns_cap : 0;
+    fp.d_ns = sp.d_ns;
     fp.part = sp.part;
-    fp.SD = P.SD; fp.kept = P.kept; fp.n_k = (int32_t)P.n_k;
+    fp.SD = P.SD; fp.kept = P.kept;
     for (int j = 0; j < n_s; ++j) fp.s[j] = h_s[j];
     fp.n_s = n_s; fp.has_zero = sp.has_zero; fp.j_zero = sp.j_zero;
     fp.rms_tol = rms_tol; fp.is_min = is_min;
     fp.rec = rec; fp.accepted = acc; fp.child = child;
+    if (acc) CK(cudaMemsetAsync(acc, 0, (size_t)n_r_max, st));
     CK(fic::launch_finalize(fp, st));
-    if (n_r > 0) ctx->launches += 1;
+    ctx->launches += 1;
     if (ctx->timing) CK(cudaEventRecord(ctx->ev[level_slot][3], st));
     return FIC_OK;
 }
@@ -359,9 +372,15 @@ fic_status fic_ctx_create(int32_t device, void *cuda_stream, fic_ctx **out) {
         if (env && strcmp(env, "fourier") == 0) ctx->search_mode = 1;
         if (env && strcmp(env, "direct") == 0) ctx->search_mode = 2;
         if (env && strcmp(env, "tc") == 0) ctx->search_mode = 4;
+        const char *ov = getenv("FIC_OVERLAP_POOLS");
+        ctx->overlap_pools = ov ? atoi(ov) != 0 : 1;
     }
     for (int l = 0; l < fic::kMaxLevels && e == cudaSuccess; ++l)
         for (int q = 0; q < 5 && e == cudaSuccess; ++q) e = cudaEventCreate(&ctx->ev[l][q]);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking);
+    for (int l = 0; l < fic::kMaxLevels && e == cudaSuccess; ++l)
+        e = cudaEventCreateWithFlags(&ctx->pool_ready[l], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->main_ready, cudaEventDisableTiming);
     if (e != cudaSuccess) {
         fic_ctx_destroy(ctx);
         return FIC_ERR_CUDA;
@@ -396,6 +415,13 @@ fic_status fic_ctx_destroy(fic_ctx *ctx) {
     for (auto &row : ctx->ev)
         for (auto &e : row)
             if (e) cudaEventDestroy(e);
+    for (auto &e : ctx->pool_ready)
+        if (e) cudaEventDestroy(e);
+    if (ctx->main_ready) cudaEventDestroy(ctx->main_ready);
+    if (ctx->side) {
+        cudaStreamSynchronize(ctx->side);
+        cudaStreamDestroy(ctx->side);
+    }
     delete ctx;
     return FIC_OK;
 }
@@ -419,7 +445,7 @@ fic_status fic_build_domain_pool(fic_ctx *ctx, const uint8_t *img, int32_t N, in
     CKS(check_level(ctx, N, B, L));
     fic_pool *pool = new (std::nothrow) fic_pool();
     if (!pool) return fail(ctx, FIC_ERR_NOMEM, "host allocation failed");
-    fic_status st = pool_enqueue(ctx, pool->P, img, N, B, L, tau_nats);
+    fic_status st = pool_enqueue(ctx, pool->P, img, N, B, L, tau_nats, ctx->stream);
     if (st == FIC_OK) {
         cudaError_t e = cudaMemcpyAsync(ctx->h_counts, pool->P.d_misc, 3 * sizeof(unsigned long long),
                                         cudaMemcpyDeviceToHost, ctx->stream);
@@ -472,17 +498,25 @@ fic_status fic_encode_level(fic_ctx *ctx, const uint8_t *img, int32_t N, const f
     ctx->stats.clear();
     fic_level_stats ls;
     memset(&ls, 0, sizeof ls);
-    CK(cudaMemsetAsync(ptr<unsigned long long>(ctx->b_counts) + 8, 0, sizeof(unsigned long long),
-                       ctx->stream));
+    unsigned long long *d_counts = ptr<unsigned long long>(ctx->b_counts);
+    // device range count for the level kernels (slot 20), exact-path counter (slot 8)
+    CK(fic::launch_set_u64(d_counts + 20, (unsigned long long)n_r, ctx->stream));
+    CK(cudaMemsetAsync(d_counts + 8, 0, sizeof(unsigned long long), ctx->stream));
+    CK(cudaMemsetAsync(d_counts + 30, 0, sizeof(unsigned long long), ctx->stream));
     if (ctx->timing) CK(cudaEventRecord(ctx->ev[0][0], ctx->stream));
-    CKS(level_enqueue(ctx, pool->P, img, reinterpret_cast<const int2 *>(ranges), n_r, h_s, n_s,
-                      rms_tol, is_min_level, out, ptr<uint8_t>(ctx->b_acc), nullptr, 0));
+    CKS(level_enqueue(ctx, pool->P, img, reinterpret_cast<const int2 *>(ranges), d_counts + 20, n_r, h_s, n_s,
+                      rms_tol, is_min_level, out, ptr<uint8_t>(ctx->b_acc), nullptr, 0,
+                      reinterpret_cast<int32_t *>(d_counts + 30)));
     ls.B = pool->P.B; ls.n_candidates = pool->P.n_c; ls.n_kept = pool->P.n_k; ls.n_ranges = n_r;
     ls.pairs = n_r * pool->P.n_k * 8;
     ctx->stats.push_back(ls);
     return FIC_OK;
 }
 
+// Device counters (b_counts, 64 x u64):
+//   [0] running output total  [1] level accepted count  [2] next-level range count (scratch)
+//   [8 + l] exact evaluations of level l   [16 + l] accepted at level l   [24..] error flag (int)
+//   [32 + l] range count of level l
 fic_status fic_encode(fic_ctx *ctx, const uint8_t *img, int32_t N, int32_t B_max, int32_t B_min,
                       int32_t L, const double *h_tau, const double *h_s, const int32_t *h_n_s,
                       const double *h_rms_tol, int32_t shard, int32_t n_shards, fic_record *out,
@@ -508,20 +542,9 @@ fic_status fic_encode(fic_ctx *ctx, const uint8_t *img, int32_t N, int32_t B_max
     cudaStream_t st = ctx->stream;
     ctx->stats.assign(nl, fic_level_stats{});
     unsigned long long *d_counts = ptr<unsigned long long>(ctx->b_counts);
+    int32_t *d_err = reinterpret_cast<int32_t *>(d_counts + 24);
     CK(cudaMemsetAsync(d_counts, 0, 64 * sizeof(unsigned long long), st));
 
-    // 1. every level's pool (independent of the quadtree), all enqueued back to back
-    for (int l = 0; l < nl; ++l) {
-        ctx->launches = 0;
-        if (ctx->timing) CK(cudaEventRecord(ctx->ev[l][0], st));
-        CKS(pool_enqueue(ctx, ctx->levels[l], img, N, B_max >> l, L, h_tau[l]));
-        if (ctx->timing) CK(cudaEventRecord(ctx->ev[l][4], st));
-        CK(cudaMemcpyAsync(ctx->h_counts + 4 * l, ctx->levels[l].d_misc, 3 * sizeof(unsigned long long),
-                           cudaMemcpyDeviceToHost, st));
-        ctx->stats[l].kernel_launches = ctx->launches;
-    }
-    ctx->launches = 0;
-    // 2. top-level ranges of this shard (row-major)
     const int64_t G = N / B_max;
     const int64_t Gmin = N / B_min;
     CK(grow(ctx, ctx->b_child, (size_t)(Gmin * Gmin) + 16));
@@ -530,58 +553,91 @@ fic_status fic_encode(fic_ctx *ctx, const uint8_t *img, int32_t N, int32_t B_max
     CK(grow(ctx, ctx->b_rec, sizeof(fic_record) * (size_t)(Gmin * Gmin)));
     CK(grow(ctx, ctx->b_acc, (size_t)(Gmin * Gmin) + 16));
     CK(grow(ctx, ctx->b_blocksum, sizeof(int64_t) * fic::select_blocksum_len(Gmin * Gmin)));
+    // 1. pools: level 0 on the main stream; levels >= 1 on the side stream, overlapping the
+    //    level-0 search (pools depend only on the image)
+    CK(cudaEventRecord(ctx->main_ready, st));  // the image is ready (caller's stream order)
+    CK(cudaStreamWaitEvent(ctx->side, ctx->main_ready, 0));
+    for (int l = 0; l < nl; ++l) {
+        cudaStream_t ps = (l == 0 || !ctx->overlap_pools) ? st : ctx->side;
+        ctx->launches = 0;
+        if (ctx->timing) CK(cudaEventRecord(ctx->ev[l][0], ps));
+        CKS(pool_enqueue(ctx, ctx->levels[l], img, N, B_max >> l, L, h_tau[l], ps));
+        if (ctx->timing) CK(cudaEventRecord(ctx->ev[l][4], ps));
+        if (l > 0) CK(cudaEventRecord(ctx->pool_ready[l], ps));
+        ctx->stats[l].kernel_launches = ctx->launches;
+    }
+    ctx->launches = 0;
+    // 2. top-level ranges of this shard (row-major)
     uint8_t *child = ptr<uint8_t>(ctx->b_child);
     CK(fic::launch_top_flags(child, G, shard, n_shards, st));
     CK(fic::launch_select_grid(child, G, B_max, ptr<int64_t>(ctx->b_blocksum), ptr<int2>(ctx->b_rng[0]),
-                               d_counts + 2, st));
+                               d_counts + 32, st));
     ctx->launches += 4;  // top flags + select x3
-    int64_t n_r = G * G > shard ? (G * G - shard + n_shards - 1) / n_shards : 0;
-    CK(cudaStreamSynchronize(st));
-    for (int l = 0; l < nl; ++l) pool_take_counts(ctx->levels[l], ctx->h_counts + 4 * l);
+    int64_t n_r_max = G * G > shard ? (G * G - shard + n_shards - 1) / n_shards : 0;
+    std::vector<int64_t> bound(nl, 0);
 
-    // 3. the quadtree, one level at a time
-    int64_t total = 0;
+    // 3. the quadtree, one level at a time, sizes carried on the device
     int cur = 0;
-    for (int l = 0; l < nl && n_r > 0; ++l) {
+    for (int l = 0; l < nl && n_r_max > 0; ++l) {
         const int32_t B = B_max >> l;
         const Pool &P = ctx->levels[l];
-        if (P.n_k < 1) return fail(ctx, FIC_ERR_EMPTY_POOL, "empty domain pool at B=" + std::to_string(B));
         const bool last = (l == nl - 1);
         const int64_t Gc = N / (B / 2 > 0 ? B / 2 : 1);
+        bound[l] = n_r_max;
+        if (l > 0) CK(cudaStreamWaitEvent(st, ctx->pool_ready[l], 0));
         if (!last) CK(cudaMemsetAsync(child, 0, (size_t)(Gc * Gc), st));
-        CKS(level_enqueue(ctx, P, img, ptr<int2>(ctx->b_rng[cur]), n_r, h_s + s_off[l], h_n_s[l],
-                          h_rms_tol[l], last, ptr<fic_record>(ctx->b_rec), ptr<uint8_t>(ctx->b_acc),
-                          last ? nullptr : child, l));
-        CK(fic::launch_select_records(ptr<uint8_t>(ctx->b_acc), n_r, ptr<int64_t>(ctx->b_blocksum),
-                                      ptr<fic_record>(ctx->b_rec), out, total, capacity, d_counts + 0,
+        CKS(level_enqueue(ctx, P, img, ptr<int2>(ctx->b_rng[cur]), d_counts + 32 + l, n_r_max, h_s + s_off[l],
+                          h_n_s[l], h_rms_tol[l], last, ptr<fic_record>(ctx->b_rec), ptr<uint8_t>(ctx->b_acc),
+                          last ? nullptr : child, l, d_err));
+        CK(fic::launch_select_records(ptr<uint8_t>(ctx->b_acc), n_r_max, ptr<int64_t>(ctx->b_blocksum),
+                                      ptr<fic_record>(ctx->b_rec), out, d_counts + 0, capacity, d_counts + 16 + l,
                                       st));
-        ctx->launches += n_r > 0 ? 3 : 0;
+        CK(fic::launch_accumulate(d_counts + 0, d_counts + 16 + l, st));
+        ctx->launches += 4;
         if (!last) {
             CK(fic::launch_select_grid(child, Gc, B / 2, ptr<int64_t>(ctx->b_blocksum),
-                                       ptr<int2>(ctx->b_rng[cur ^ 1]), d_counts + 1, st));
+                                       ptr<int2>(ctx->b_rng[cur ^ 1]), d_counts + 33 + l, st));
             ctx->launches += 3;
+            n_r_max = std::min<int64_t>(4 * n_r_max, Gc * Gc);
         }
-        CK(cudaMemcpyAsync(ctx->h_counts + 32, d_counts, 2 * sizeof(unsigned long long),
-                           cudaMemcpyDeviceToHost, st));
-        CK(cudaMemcpyAsync(ctx->h_counts + 40 + l, d_counts + 8 + l, sizeof(unsigned long long),
-                           cudaMemcpyDeviceToHost, st));
-        CK(cudaStreamSynchronize(st));
-        const int64_t n_acc = (int64_t)ctx->h_counts[32];
-        const int64_t n_next = last ? 0 : (int64_t)ctx->h_counts[33];
-        fic_level_stats &ls = ctx->stats[l];
-        ls.B = B; ls.n_candidates = P.n_c; ls.n_kept = P.n_k; ls.n_ranges = n_r;
-        ls.n_accepted = n_acc; ls.pairs = n_r * P.n_k * 8;
-        ls.exact_evals = (int64_t)ctx->h_counts[40 + l];
-        ls.kernel_launches += ctx->launches;
+        ctx->stats[l].kernel_launches += ctx->launches;
         ctx->launches = 0;
-        total += n_acc;
-        n_r = n_next;
         cur ^= 1;
+    }
+    // 4. join the side stream (pools of levels the quadtree never reached), then one device -> host
+    //    read of every counter and one synchronisation
+    for (int l = 1; l < nl; ++l) CK(cudaStreamWaitEvent(st, ctx->pool_ready[l], 0));
+    CK(cudaMemcpyAsync(ctx->h_counts, d_counts, 64 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    const unsigned long long *h = ctx->h_counts;
+    if (*reinterpret_cast<const int32_t *>(h + 24) == FIC_ERR_EMPTY_POOL)
+        return fail(ctx, FIC_ERR_EMPTY_POOL, "empty domain pool at a level that has ranges");
+    for (int l = 0; l < nl; ++l) {
+        fic_level_stats &ls = ctx->stats[l];
+        const Pool &P = ctx->levels[l];
+        ls.B = B_max >> l;
+        ls.n_candidates = P.n_c;
+        ls.n_ranges = bound[l] > 0 ? (int64_t)h[32 + l] : 0;
+        ls.n_accepted = (int64_t)h[16 + l];
+        ls.exact_evals = (int64_t)h[8 + l];
+        ls.n_kept = -1;  // filled below from the pool counters
+    }
+    // pool counters (n_kept) of the levels
+    for (int l = 0; l < nl; ++l) {
+        CK(cudaMemcpyAsync(ctx->h_counts + 48 + l, ctx->levels[l].d_misc, sizeof(unsigned long long),
+                           cudaMemcpyDeviceToHost, st));
+    }
+    CK(cudaStreamSynchronize(st));
+    for (int l = 0; l < nl; ++l) {
+        fic_level_stats &ls = ctx->stats[l];
+        ls.n_kept = (int64_t)ctx->h_counts[48 + l];
+        ctx->levels[l].n_k = ls.n_kept;
+        ls.pairs = ls.n_ranges * ls.n_kept * 8;
     }
     if (ctx->timing) {
         for (int l = 0; l < nl; ++l) {
             fic_level_stats &ls = ctx->stats[l];
-            if (ls.n_ranges == 0) continue;
+            if (bound[l] == 0) continue;
             float a = 0, b = 0, c = 0;
             cudaEventElapsedTime(&a, ctx->ev[l][0], ctx->ev[l][4]);
             cudaEventElapsedTime(&b, ctx->ev[l][1], ctx->ev[l][2]);
@@ -589,6 +645,7 @@ fic_status fic_encode(fic_ctx *ctx, const uint8_t *img, int32_t N, int32_t B_max
             ls.ms_pool = a; ls.ms_search = b; ls.ms_finalize = c;
         }
     }
+    const int64_t total = (int64_t)ctx->h_counts[0];
     *h_n_out = total;
     if (total > capacity) return fail(ctx, FIC_ERR_CAPACITY, "output capacity too small");
     return FIC_OK;

@@ -89,15 +89,18 @@ struct B2Params {
     const float *U;        // [n_tiles][nsp][128] t2_j
     const int64_t *C;      // [n_slots]
     const int32_t *kept;
-    int32_t n_tiles, tiles_per_split, nsplit;
+    const unsigned long long *d_nr, *d_misc;  // device sizes: n_r; n_kept, Cmax
+    int32_t nsplit;
     int32_t nsp;
     double spos[kMaxS];
     int32_t jpos[kMaxS];
     int32_t has_zero, j_zero;
-    double smax, cmax;
+    double smax;
     Partial *part;
     unsigned long long *exact_count;
     float *gthr;  // [n_r] threshold shared by all domain splits (CAS-min), initialised to ~FLT_MAX
+    unsigned long long *d_ns;
+    int32_t ns_cap;
 };
 
 struct B2Cold {
@@ -196,9 +199,14 @@ __global__ void __launch_bounds__(kB2Threads) b2search_kernel(const __grid_const
     B2Cold *cold = reinterpret_cast<B2Cold *>(Us + 2 * TPS * NSP * kTileD);  // [RPT][threads]
     uint64_t *bar = reinterpret_cast<uint64_t *>(cold + RPT * kB2Threads);
 
-    const int split = blockIdx.y;
-    const int t0 = split * P.tiles_per_split;
-    const int t1 = min(P.n_tiles, t0 + P.tiles_per_split);
+    const int n_r = (int)*P.d_nr;
+    const int n_tiles = (int)((P.d_misc[0] + kTileD - 1) / kTileD);
+    const double cmax = (double)P.d_misc[1];
+    int group, split, ns;
+    if (!cta_work(n_r, kB2Threads * RPT, n_tiles, 2 * TPS, P.ns_cap, group, split, ns)) return;
+    if (group == 0 && split == 0 && threadIdx.x == 0) *P.d_ns = (unsigned long long)ns;
+    const int t0 = (int)(((int64_t)split * n_tiles) / ns);
+    const int t1 = (int)(((int64_t)(split + 1) * n_tiles) / ns);
     const int nstages = (max(0, t1 - t0) + TPS - 1) / TPS;
     auto issue = [&](int s) {
         const int buf = s & 1;
@@ -222,14 +230,14 @@ __global__ void __launch_bounds__(kB2Threads) b2search_kernel(const __grid_const
     }
 
     float X2[RPT], xr2[RPT], xi2[RPT], thr[RPT];
-    const int rbase = (blockIdx.x * kB2Threads + threadIdx.x) * RPT;
+    const int rbase = (group * kB2Threads + threadIdx.x) * RPT;
     const double u = 5.9604644775390625e-08;
 #pragma unroll
     for (int q = 0; q < RPT; ++q) {
         const int r = rbase + q;
         B2Cold &cd = cold[q * kB2Threads + threadIdx.x];
         int a = 0, b = 0, c = 0, d = 0;
-        if (r < P.n_r) {
+        if (r < n_r) {
             const int2 rr = P.ranges[r];
             const uint8_t *p0 = P.img + (size_t)rr.y * P.N + rr.x;
             a = p0[0]; b = p0[1]; d = p0[P.N]; c = p0[P.N + 1];
@@ -242,12 +250,12 @@ __global__ void __launch_bounds__(kB2Threads) b2search_kernel(const __grid_const
         cd.SR = sr;
         cd.px = a | (b << 8) | (c << 16) | (d << 24);
         // |Bq| <= sqrt(A C); fp32: -hs and t2 roundings and one FFMA -> 4u (hs |Bq| + t2)
-        const double hs = 0.5 * P.smax, t2m = P.smax * P.smax * P.cmax * 0.0625;
-        cd.margin = 4.0 * u * (hs * sqrt(cd.A * P.cmax) * 1.01 + t2m) + 1e-12 * (cd.A + t2m) + 1e-30;
+        const double hs = 0.5 * P.smax, t2m = P.smax * P.smax * cmax * 0.0625;
+        cd.margin = 4.0 * u * (hs * sqrt(cd.A * cmax) * 1.01 + t2m) + 1e-12 * (cd.A + t2m) + 1e-30;
         if (P.has_zero) { cd.best_e = cd.A; cd.best_d = 0; cd.best_kj = P.j_zero; }
         else { cd.best_e = INFINITY; cd.best_d = INT_MAX; cd.best_kj = INT_MAX; }
         float th = P.has_zero ? fminf(__double2float_ru(cd.margin), FLT_MAX) : FLT_MAX;
-        thr[q] = r < P.n_r ? th : -FLT_MAX;
+        thr[q] = r < n_r ? th : -FLT_MAX;
     }
     float nhs[NSP];
 #pragma unroll
@@ -259,7 +267,7 @@ __global__ void __launch_bounds__(kB2Threads) b2search_kernel(const __grid_const
         b2_wait(&bar[buf], (uint32_t)((s >> 1) & 1));
 #pragma unroll
         for (int q = 0; q < RPT; ++q)
-            if (rbase + q < P.n_r) thr[q] = fminf(thr[q], P.gthr[rbase + q]);
+            if (rbase + q < n_r) thr[q] = fminf(thr[q], P.gthr[rbase + q]);
         const float4 *Fb = Fs + buf * FST;
         const float *Ub = Us + buf * TPS * NSP * kTileD;
         const int ta = t0 + s * TPS;
@@ -324,13 +332,13 @@ __global__ void __launch_bounds__(kB2Threads) b2search_kernel(const __grid_const
 #pragma unroll
     for (int q = 0; q < RPT; ++q) {
         const int r = rbase + q;
-        if (r < P.n_r) {
+        if (r < n_r) {
             const B2Cold &cd = cold[q * kB2Threads + threadIdx.x];
             Partial pb;
             pb.e = cd.best_e;
             pb.d = cd.best_d;
             pb.kj = cd.best_kj;
-            P.part[(size_t)r * P.nsplit + split] = pb;
+            P.part[(size_t)r * P.ns_cap + split] = pb;
         }
     }
 #pragma unroll
@@ -376,12 +384,12 @@ cudaError_t launch_b2_search(const SearchParams &sp, const float4 *F, const floa
     memset(&p, 0, sizeof p);
     p.img = sp.img; p.N = sp.N; p.L = L; p.A = A; p.ranges = sp.ranges; p.n_r = sp.n_r;
     p.F = F; p.U = U; p.C = sp.C; p.kept = kept;
-    p.n_tiles = sp.n_tiles; p.tiles_per_split = sp.tiles_per_split; p.nsplit = sp.nsplit;
+    p.d_nr = sp.d_nr; p.d_misc = sp.d_misc; p.nsplit = sp.nsplit; p.d_ns = sp.d_ns; p.ns_cap = sp.ns_cap;
     p.nsp = sp.nsp;
     memcpy(p.spos, sp.spos, sizeof p.spos);
     memcpy(p.jpos, sp.jpos, sizeof p.jpos);
     p.has_zero = sp.has_zero; p.j_zero = sp.j_zero;
-    p.smax = sp.smax; p.cmax = sp.cmax;
+    p.smax = sp.smax;
     p.part = sp.part; p.exact_count = sp.exact_count;
     p.gthr = gthr;
     cudaError_t e = cudaMemsetAsync(gthr, 0x7f, sizeof(float) * (size_t)sp.n_r, st);  // ~3.4e38

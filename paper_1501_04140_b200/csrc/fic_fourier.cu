@@ -250,10 +250,12 @@ cudaError_t launch_pool_coeff(const uint8_t *img, int32_t N, int32_t B, int32_t 
 }
 
 // U[tile][j][dl] = fp32 of t2_j = (s_j s_j)(C/16); +inf on pad slots (never admitted)
-__global__ void fourier_u_kernel(const int64_t *__restrict__ C, int32_t n_k, int64_t n_slots,
-                                 const SList spos, int32_t nsp, float *__restrict__ U) {
+__global__ void fourier_u_kernel(const int64_t *__restrict__ C, const unsigned long long *__restrict__ d_nk,
+                                 int64_t n_slots, const SList spos, int32_t nsp, float *__restrict__ U) {
     const int64_t d = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (d >= n_slots) return;
+    const int64_t n_k = (int64_t)*d_nk;
+    if (d >= ((n_k + kTileD - 1) / kTileD) * kTileD) return;
     const int64_t tile = d / kTileD, dl = d % kTileD;
     const double c16 = __dmul_rn(0.0625, (double)C[d]);
     for (int j = 0; j < nsp; ++j) {
@@ -263,10 +265,10 @@ __global__ void fourier_u_kernel(const int64_t *__restrict__ C, int32_t n_k, int
     }
 }
 
-cudaError_t launch_fourier_u(const int64_t *C, int32_t n_k, int64_t n_slots, const SList &sl, int32_t nsp,
-                             float *U, cudaStream_t st) {
+cudaError_t launch_fourier_u(const int64_t *C, const unsigned long long *d_nk, int64_t n_slots, const SList &sl,
+                             int32_t nsp, float *U, cudaStream_t st) {
     if (n_slots == 0 || nsp == 0) return cudaSuccess;
-    fourier_u_kernel<<<(unsigned)((n_slots + 255) / 256), 256, 0, st>>>(C, n_k, n_slots, sl, nsp, U);
+    fourier_u_kernel<<<(unsigned)((n_slots + 255) / 256), 256, 0, st>>>(C, d_nk, n_slots, sl, nsp, U);
     return cudaGetLastError();
 }
 
@@ -283,12 +285,19 @@ struct RangeMeta {
 // §"Exactness").  Because sum_p Dt = 0, sum_p (R(p) - 128) Dt(f_k p) = Bq_k.
 template <int B>
 __global__ void fourier_range_kernel(const uint8_t *__restrict__ img, int32_t N,
-                                     const int2 *__restrict__ ranges, int32_t n_r, int32_t r_stride,
-                                     double smax, double t2max, double dnmax, float *__restrict__ Rc,
+                                     const int2 *__restrict__ ranges, const unsigned long long *__restrict__ d_nr,
+                                     int32_t r_stride, double smax,
+                                     const unsigned long long *__restrict__ d_misc, float *__restrict__ Rc,
                                      RangeMeta *__restrict__ meta) {
     using Cf = FCfg<B>;
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= n_r) return;
+    if (r >= (int)*d_nr) return;
+    const double t2max = smax * smax * (double)d_misc[1] * 0.0625 * (1.0 + 1e-12);
+    double dnmax;
+    {
+        const unsigned int bits = (unsigned int)(d_misc[2] & 0xffffffffu);
+        dnmax = (double)__uint_as_float(bits);
+    }
     const int2 rr = ranges[r];
     int R[Cf::n];
     long long sr = 0, srr = 0;
@@ -370,7 +379,8 @@ struct FSearchParams {
     const int64_t *C;      // [n_slots]
     const float *Rc;       // [NC][r_stride]
     const RangeMeta *meta; // [n_r]
-    int32_t n_r, r_stride, n_tiles, tiles_per_split, nsplit;
+    const unsigned long long *d_nr, *d_misc;  // device sizes
+    int32_t r_stride, nsplit;
     int32_t nsp;
     double spos[kMaxS];
     int32_t jpos[kMaxS];
@@ -461,8 +471,10 @@ __global__ void __launch_bounds__(256, (B == 8 ? 1 : 2)) fsearch_kernel(const __
     uint64_t *bar = reinterpret_cast<uint64_t *>(cold + RPT * 256);
 
     const int split = blockIdx.y;
-    const int t0 = split * P.tiles_per_split;
-    const int t1 = min(P.n_tiles, t0 + P.tiles_per_split);
+    const int n_r = (int)*P.d_nr;
+    const int n_tiles = (int)((P.d_misc[0] + kTileD - 1) / kTileD);
+    const int t0 = (int)(((int64_t)split * n_tiles) / P.nsplit);
+    const int t1 = (int)(((int64_t)(split + 1) * n_tiles) / P.nsplit);
     const int ntl = max(0, t1 - t0);
     const int nstages = (ntl + TPS - 1) / TPS;
     auto issue = [&](int s) {
@@ -491,7 +503,7 @@ __global__ void __launch_bounds__(256, (B == 8 ? 1 : 2)) fsearch_kernel(const __
 #pragma unroll
     for (int q = 0; q < RPT; ++q) {
         const int r = rbase + q;
-        const bool valid = r < P.n_r;
+        const bool valid = r < n_r;
         const int rr = valid ? r : 0;
 #pragma unroll
         for (int c = 0; c < NC; ++c) rc[q][c] = valid ? P.Rc[(size_t)c * P.r_stride + rr] : 0.f;
@@ -598,7 +610,7 @@ __global__ void __launch_bounds__(256, (B == 8 ? 1 : 2)) fsearch_kernel(const __
 #pragma unroll
     for (int q = 0; q < RPT; ++q) {
         const int r = rbase + q;
-        if (r < P.n_r) {
+        if (r < n_r) {
             const FCold &cd = cold[q * 256 + threadIdx.x];
             Partial pb;
             pb.e = cd.best_e;
@@ -615,7 +627,7 @@ __global__ void __launch_bounds__(256, (B == 8 ? 1 : 2)) fsearch_kernel(const __
 
 // ------------------------------------------------------------------------------ launchers
 template <int B, int NSP, int RPT>
-static cudaError_t launch_fsearch_t(const FSearchParams &p, cudaStream_t st) {
+static cudaError_t launch_fsearch_t(const FSearchParams &p, int32_t n_r_max, cudaStream_t st) {
     using Cf = FCfg<B>;
     constexpr int TILE_F = kTileD * Cf::NCS;
     constexpr int TPS = (TILE_F * 4 >= 24 * 1024) ? 1 : (24 * 1024) / (TILE_F * 4);
@@ -628,7 +640,7 @@ static cudaError_t launch_fsearch_t(const FSearchParams &p, cudaStream_t st) {
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    dim3 grid((unsigned)((p.n_r + 256 * RPT - 1) / (256 * RPT)), (unsigned)p.nsplit);
+    dim3 grid((unsigned)((n_r_max + 256 * RPT - 1) / (256 * RPT)), (unsigned)p.nsplit);
     fsearch_kernel<B, NSP, RPT><<<grid, 256, SMEM, st>>>(p);
     return cudaGetLastError();
 }
@@ -642,35 +654,31 @@ template <int B>
 constexpr int rpt_of() { return B == 2 ? 4 : (B == 4 ? 2 : 1); }
 
 template <int B>
-static cudaError_t launch_fsearch_b(const FSearchParams &p, cudaStream_t st) {
-    if (p.nsp <= 1) return launch_fsearch_t<B, 1, rpt_of<B>()>(p, st);
-    if (p.nsp <= 2) return launch_fsearch_t<B, 2, rpt_of<B>()>(p, st);
-    return launch_fsearch_t<B, 16, 1>(p, st);
+static cudaError_t launch_fsearch_b(const FSearchParams &p, int32_t n_r_max, cudaStream_t st) {
+    if (p.nsp <= 1) return launch_fsearch_t<B, 1, rpt_of<B>()>(p, n_r_max, st);
+    if (p.nsp <= 2) return launch_fsearch_t<B, 2, rpt_of<B>()>(p, n_r_max, st);
+    return launch_fsearch_t<B, 16, 1>(p, n_r_max, st);
 }
 
 // Range prep + U + search for B in {2, 4, 8}.  Rc [NC][r_stride], meta [n_r], U [n_tiles][nsp][128].
-cudaError_t launch_fourier_level(int32_t B, const uint8_t *img, int32_t N, const int2 *ranges,
-                                 int32_t n_r, const float *Dc, const int64_t *C, int32_t n_k,
-                                 int32_t n_tiles, int32_t nsplit, int32_t tiles_per_split,
-                                 const SearchParams &sp, double dnmax, float *Rc, int32_t r_stride,
-                                 void *meta, float *U, cudaStream_t st) {
-    if (n_r == 0) return cudaSuccess;
-    const double t2max = sp.smax * sp.smax * sp.cmax * 0.0625 * (1.0 + 1e-12);
-    const int64_t n_slots = (int64_t)n_tiles * kTileD;
+cudaError_t launch_fourier_level(int32_t B, const SearchParams &sp, const float *Dc, float *Rc,
+                                 int32_t r_stride, void *meta, float *U, cudaStream_t st) {
+    if (sp.n_r == 0) return cudaSuccess;
+    const int64_t n_slots = sp.slot_stride;
     SList sl;
     memcpy(sl.s, sp.spos, sizeof sl.s);
     RangeMeta *m = reinterpret_cast<RangeMeta *>(meta);
-    const unsigned rb = (unsigned)((n_r + 127) / 128);
+    const unsigned rb = (unsigned)((sp.n_r + 127) / 128);
     switch (B) {
-    case 2: fourier_range_kernel<2><<<rb, 128, 0, st>>>(img, N, ranges, n_r, r_stride, sp.smax, t2max, dnmax, Rc, m); break;
-    case 4: fourier_range_kernel<4><<<rb, 128, 0, st>>>(img, N, ranges, n_r, r_stride, sp.smax, t2max, dnmax, Rc, m); break;
-    case 8: fourier_range_kernel<8><<<rb, 128, 0, st>>>(img, N, ranges, n_r, r_stride, sp.smax, t2max, dnmax, Rc, m); break;
+    case 2: fourier_range_kernel<2><<<rb, 128, 0, st>>>(sp.img, sp.N, sp.ranges, sp.d_nr, r_stride, sp.smax, sp.d_misc, Rc, m); break;
+    case 4: fourier_range_kernel<4><<<rb, 128, 0, st>>>(sp.img, sp.N, sp.ranges, sp.d_nr, r_stride, sp.smax, sp.d_misc, Rc, m); break;
+    case 8: fourier_range_kernel<8><<<rb, 128, 0, st>>>(sp.img, sp.N, sp.ranges, sp.d_nr, r_stride, sp.smax, sp.d_misc, Rc, m); break;
     default: return cudaErrorInvalidValue;
     }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     if (sp.nsp > 0 && n_slots > 0) {
-        fourier_u_kernel<<<(unsigned)((n_slots + 255) / 256), 256, 0, st>>>(C, n_k, n_slots, sl,
+        fourier_u_kernel<<<(unsigned)((n_slots + 255) / 256), 256, 0, st>>>(sp.C, &sp.d_misc[0], n_slots, sl,
                                                                             sp.nsp, U);
         e = cudaGetLastError();
         if (e != cudaSuccess) return e;
@@ -678,18 +686,18 @@ cudaError_t launch_fourier_level(int32_t B, const uint8_t *img, int32_t N, const
     if (sp.nsp == 0) return cudaSuccess;
     FSearchParams p;
     memset(&p, 0, sizeof p);
-    p.Dc = Dc; p.U = U; p.C = C; p.Rc = Rc; p.meta = m;
-    p.n_r = n_r; p.r_stride = r_stride; p.n_tiles = n_tiles;
-    p.tiles_per_split = tiles_per_split; p.nsplit = nsplit;
+    p.Dc = Dc; p.U = U; p.C = sp.C; p.Rc = Rc; p.meta = m;
+    p.d_nr = sp.d_nr; p.d_misc = sp.d_misc; p.r_stride = r_stride; p.nsplit = sp.nsplit;
     p.nsp = sp.nsp;
     memcpy(p.spos, sp.spos, sizeof p.spos);
     memcpy(p.jpos, sp.jpos, sizeof p.jpos);
     p.has_zero = sp.has_zero; p.j_zero = sp.j_zero;
     p.part = sp.part; p.exact_count = sp.exact_count;
+    // grid is sized by the host-side upper bound of n_r
     switch (B) {
-    case 2: return launch_fsearch_b<2>(p, st);
-    case 4: return launch_fsearch_b<4>(p, st);
-    case 8: return launch_fsearch_b<8>(p, st);
+    case 2: return launch_fsearch_b<2>(p, sp.n_r, st);
+    case 4: return launch_fsearch_b<4>(p, sp.n_r, st);
+    case 8: return launch_fsearch_b<8>(p, sp.n_r, st);
     default: return cudaErrorInvalidValue;
     }
 }

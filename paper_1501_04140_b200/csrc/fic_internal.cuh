@@ -28,7 +28,7 @@ struct Buf {
 // One level's entropy-filtered domain pool (fic_pool).
 struct Pool {
     int32_t N = 0, B = 0, L = 0, n = 0, A = 0;
-    int64_t n_c = 0, n_k = 0, n_tiles = 0;
+    int64_t n_c = 0, n_k = 0, n_tiles = 0, n_tiles_max = 0;
     int64_t cmax = 0;  // max C over kept domains (host copy, for the filter margin)
     int64_t *keys = nullptr;
     uint8_t *keep = nullptr;
@@ -42,7 +42,7 @@ struct Pool {
     int64_t *C = nullptr;
     unsigned long long *d_misc = nullptr;  // [0] = n_kept, [1] = Cmax, [2] = max |dh|_2 (float bits)
     double dnmax = 0.0;
-    Buf b_keys, b_keep, b_kept, b_Dt, b_SDf, b_SD, b_C, b_misc, b_Dc, b_Dtc, b_F2;
+    Buf b_keys, b_keep, b_kept, b_Dt, b_SDf, b_SD, b_C, b_misc, b_Dc, b_Dtc, b_F2, b_blocksum;
     int device = 0;
 };
 
@@ -53,11 +53,17 @@ struct Partial {
     int32_t kj;  // iso | (s_idx << 8)
 };
 
+// Level sizes live on the device (no host round trip between levels): n_r = *d_nr,
+// n_kept = d_misc[0], Cmax = d_misc[1]; host fields n_r / n_tiles are UPPER BOUNDS used only
+// to size grids and buffers; a CTA's domain tiles are [split nt / nsplit, (split+1) nt / nsplit).
 struct SearchParams {
     const uint8_t *img;
     int32_t N;
     const int2 *ranges;
-    int32_t n_r;
+    int32_t n_r;  // upper bound
+    const unsigned long long *d_nr;    // actual range count
+    const unsigned long long *d_misc;  // pool: [0] n_kept, [1] Cmax, [2] max |dh|
+    int64_t slot_stride;               // n_tiles (upper bound) * 128: stride of t2f rows
     const float *Dt;
     const float *SDf;
     const int32_t *SD;
@@ -70,15 +76,21 @@ struct SearchParams {
     int32_t has_zero, j_zero;    // s = 0 present, and its first index
     double smax;                 // max s
     double cmax;                 // max C of the pool (margin bound)
-    Partial *part;               // [n_r][nsplit]
+    Partial *part;               // [n_r][ns_cap]
     unsigned long long *exact_count;
+    unsigned long long *d_ns;    // splits actually used (written by the search kernel)
+    int32_t ns_cap;              // partial stride (max splits)
 };
 
 struct FinalizeParams {
     const uint8_t *img;
     int32_t N, B, L, A;
     const int2 *ranges;
-    int32_t n_r, nsplit;
+    int32_t n_r, nsplit;  // n_r: upper bound; nsplit: partial stride (ns_cap)
+    const unsigned long long *d_nr;
+    const unsigned long long *d_ns;  // splits actually used
+    const unsigned long long *d_misc;
+    int32_t *d_err;  // set to FIC_ERR_EMPTY_POOL if ranges meet an empty pool
     const Partial *part;
     const int32_t *SD;
     const int32_t *kept;
@@ -92,6 +104,26 @@ struct FinalizeParams {
     uint8_t *child;  // child bitmap [(N/(B/2))^2] or null
 };
 
+// Dynamic mapping of a CTA to (range group, domain split) from the actual counts: the grid is
+// sized from host upper bounds; ns = min(ns_cap, ctas / groups, tiles / min_tiles) splits.
+__device__ __forceinline__ bool cta_work(int n_r, int rpc, int n_tiles, int min_tiles, int ns_cap, int &group,
+                                         int &split, int &ns) {
+    const int groups = (n_r + rpc - 1) / rpc;
+    const int ctas = (int)(gridDim.x * gridDim.y);
+    ns = groups > 0 ? ctas / groups : 1;
+    const int tcap = (n_tiles + min_tiles - 1) / min_tiles;
+    if (ns > tcap) ns = tcap;
+    if (ns > ns_cap) ns = ns_cap;
+    if (ns < 1) ns = 1;
+    const int item = (int)(blockIdx.y * gridDim.x + blockIdx.x);
+    if (item >= groups * ns) return false;
+    // split-major: CTAs that run early cover split 0 of every group, so later splits of a range
+    // start from the thresholds its earlier splits already published (B = 2 shares them globally)
+    split = item / groups;
+    group = item % groups;
+    return true;
+}
+
 // ---- launchers (return cudaError_t of the launch) ---------------------------------------------
 cudaError_t launch_entropy_keys(const uint8_t *img, int32_t N, int32_t B, int32_t L, int32_t A,
                                 const int64_t *d_delta, int64_t lut_m, int64_t T, int use_tau,
@@ -101,9 +133,13 @@ cudaError_t launch_select_index(const uint8_t *flags, int64_t n, int64_t *blocks
                                 unsigned long long *d_total, cudaStream_t st);
 cudaError_t launch_select_grid(const uint8_t *flags, int64_t G, int32_t B, int64_t *blocksum,
                                int2 *out, unsigned long long *d_total, cudaStream_t st);
+// appends the flagged records at out[*d_base ...] (only below capacity), *d_total = count
 cudaError_t launch_select_records(const uint8_t *flags, int64_t n, int64_t *blocksum,
-                                  const fic_record *in, fic_record *out, int64_t out_base,
+                                  const fic_record *in, fic_record *out, const unsigned long long *d_base,
                                   int64_t capacity, unsigned long long *d_total, cudaStream_t st);
+cudaError_t launch_set_u64(unsigned long long *d, unsigned long long v, cudaStream_t st);
+// *d_acc += *d_add (single thread)
+cudaError_t launch_accumulate(unsigned long long *d_acc, const unsigned long long *d_add, cudaStream_t st);
 size_t select_blocksum_len(int64_t n);
 cudaError_t launch_top_flags(uint8_t *flags, int64_t G, int32_t shard, int32_t n_shards,
                              cudaStream_t st);
@@ -117,7 +153,7 @@ cudaError_t launch_pool_moments(const uint8_t *img, int32_t N, int32_t B, int32_
 struct SList {
     double s[kMaxS];
 };
-cudaError_t launch_t2f(const int64_t *C, int32_t n_k, int64_t n_slots, const SList &spos,
+cudaError_t launch_t2f(const int64_t *C, const unsigned long long *d_nk, int64_t n_slots, const SList &spos,
                        int32_t nsp, float *t2f, cudaStream_t st);
 cudaError_t launch_search(int32_t B, int32_t nsp, const SearchParams &p, cudaStream_t st);
 cudaError_t launch_finalize(const FinalizeParams &p, cudaStream_t st);
@@ -131,8 +167,8 @@ cudaError_t launch_b2_pool(const uint8_t *img, int32_t N, int32_t L, int32_t A, 
 int b2_nsplit_hint(int64_t n_r, int64_t n_tiles, int num_sms);
 cudaError_t launch_b2_search(const SearchParams &sp, const float4 *F, const float *U, const int32_t *kept,
                              int32_t L, int32_t A, float *gthr, cudaStream_t st);
-cudaError_t launch_fourier_u(const int64_t *C, int32_t n_k, int64_t n_slots, const SList &sl, int32_t nsp,
-                             float *U, cudaStream_t st);
+cudaError_t launch_fourier_u(const int64_t *C, const unsigned long long *d_nk, int64_t n_slots, const SList &sl,
+                             int32_t nsp, float *U, cudaStream_t st);
 
 // tcgen05 search (fic_tc.cu), B in {2, 4, 8, 16}
 int tc_supported(int B);
@@ -154,10 +190,7 @@ int fourier_nsplit_hint(int32_t B, int32_t nsp, int64_t n_r, int64_t n_tiles, in
 cudaError_t launch_pool_coeff(const uint8_t *img, int32_t N, int32_t B, int32_t L, int32_t A,
                               const int32_t *kept, const unsigned long long *d_nk, int64_t n_slots,
                               float *Dc, unsigned int *d_dnmax, cudaStream_t st);
-cudaError_t launch_fourier_level(int32_t B, const uint8_t *img, int32_t N, const int2 *ranges,
-                                 int32_t n_r, const float *Dc, const int64_t *C, int32_t n_k,
-                                 int32_t n_tiles, int32_t nsplit, int32_t tiles_per_split,
-                                 const SearchParams &sp, double dnmax, float *Rc, int32_t r_stride,
-                                 void *meta, float *U, cudaStream_t st);
+cudaError_t launch_fourier_level(int32_t B, const SearchParams &sp, const float *Dc, float *Rc,
+                                 int32_t r_stride, void *meta, float *U, cudaStream_t st);
 
 }  // namespace fic

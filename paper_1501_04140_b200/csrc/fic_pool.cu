@@ -191,9 +191,11 @@ __device__ __forceinline__ void copy_record(fic_record *dst, const fic_record *s
 struct EmitRecord {
     const fic_record *in;
     fic_record *out;
-    int64_t base, cap;
+    const unsigned long long *base;
+    int64_t cap;
     __device__ void operator()(int64_t i, int64_t pos) const {
-        if (base + pos < cap) copy_record(out + base + pos, in + i);
+        const int64_t o = (int64_t)*base + pos;
+        if (o < cap) copy_record(out + o, in + i);
     }
 };
 
@@ -217,9 +219,23 @@ cudaError_t launch_select_grid(const uint8_t *flags, int64_t G, int32_t B, int64
     return select_run(flags, G * G, blocksum, EmitGrid{out, G, B}, d_total, st);
 }
 cudaError_t launch_select_records(const uint8_t *flags, int64_t n, int64_t *blocksum,
-                                  const fic_record *in, fic_record *out, int64_t out_base,
+                                  const fic_record *in, fic_record *out, const unsigned long long *d_base,
                                   int64_t capacity, unsigned long long *d_total, cudaStream_t st) {
-    return select_run(flags, n, blocksum, EmitRecord{in, out, out_base, capacity}, d_total, st);
+    return select_run(flags, n, blocksum, EmitRecord{in, out, d_base, capacity}, d_total, st);
+}
+
+__global__ void set_u64_kernel(unsigned long long *p, unsigned long long v) { *p = v; }
+
+cudaError_t launch_set_u64(unsigned long long *d, unsigned long long v, cudaStream_t st) {
+    set_u64_kernel<<<1, 1, 0, st>>>(d, v);
+    return cudaGetLastError();
+}
+
+__global__ void accumulate_kernel(unsigned long long *acc, const unsigned long long *add) { *acc += *add; }
+
+cudaError_t launch_accumulate(unsigned long long *d_acc, const unsigned long long *d_add, cudaStream_t st) {
+    accumulate_kernel<<<1, 1, 0, st>>>(d_acc, d_add);
+    return cudaGetLastError();
 }
 
 __global__ void top_flags_kernel(uint8_t *flags, int64_t n, int32_t shard, int32_t n_shards) {
@@ -328,10 +344,12 @@ cudaError_t launch_pool_moments(const uint8_t *img, int32_t N, int32_t B, int32_
 }
 
 // t2f[j][d] = fp32 of (s_j s_j)(C/16) for s_j > 0; +inf for pad slots (never admitted).
-__global__ void t2f_kernel(const int64_t *__restrict__ C, int32_t n_k, int64_t n_slots,
-                           const SList spos, int32_t nsp, float *__restrict__ t2f) {
+__global__ void t2f_kernel(const int64_t *__restrict__ C, const unsigned long long *__restrict__ d_nk,
+                           int64_t n_slots, const SList spos, int32_t nsp, float *__restrict__ t2f) {
     const int64_t d = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (d >= n_slots) return;
+    const int64_t n_k = (int64_t)*d_nk;
+    if (d >= ((n_k + kTileD - 1) / kTileD) * kTileD) return;
     const double c16 = __dmul_rn(0.0625, (double)C[d]);
     for (int j = 0; j < nsp; ++j) {
         const double s = spos.s[j];
@@ -339,10 +357,10 @@ __global__ void t2f_kernel(const int64_t *__restrict__ C, int32_t n_k, int64_t n
     }
 }
 
-cudaError_t launch_t2f(const int64_t *C, int32_t n_k, int64_t n_slots, const SList &spos,
+cudaError_t launch_t2f(const int64_t *C, const unsigned long long *d_nk, int64_t n_slots, const SList &spos,
                        int32_t nsp, float *t2f, cudaStream_t st) {
     if (n_slots == 0 || nsp == 0) return cudaSuccess;
-    t2f_kernel<<<(unsigned)((n_slots + 255) / 256), 256, 0, st>>>(C, n_k, n_slots, spos, nsp, t2f);
+    t2f_kernel<<<(unsigned)((n_slots + 255) / 256), 256, 0, st>>>(C, d_nk, n_slots, spos, nsp, t2f);
     return cudaGetLastError();
 }
 

@@ -142,14 +142,17 @@ __global__ void __launch_bounds__(256, 1) search_kernel(const __grid_constant__ 
     uint64_t *bar = reinterpret_cast<uint64_t *>(Rs + Cf::RS_F);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int n_r = (int)*P.d_nr;
+    const int n_tiles = (int)((P.d_misc[0] + kTileD - 1) / kTileD);
+    const double cmax = (double)P.d_misc[1];
     const int r = blockIdx.x * 8 + warp;
-    const bool rvalid = r < P.n_r;
+    const bool rvalid = r < n_r;
     const int split = blockIdx.y;
-    const int t0 = split * P.tiles_per_split;
-    const int t1 = min(P.n_tiles, t0 + P.tiles_per_split);
+    const int t0 = (int)(((int64_t)split * n_tiles) / P.nsplit);
+    const int t1 = (int)(((int64_t)(split + 1) * n_tiles) / P.nsplit);
     const int ntl = max(0, t1 - t0);
     const int nstages = (n <= 64) ? (ntl + TPS - 1) / TPS : ntl * NCH;
-    const int64_t n_slots = (int64_t)P.n_tiles * kTileD;
+    const int64_t n_slots = P.slot_stride;
 
     auto issue = [&](int s) {
         const int buf = s & 1;
@@ -217,7 +220,7 @@ __global__ void __launch_bounds__(256, 1) search_kernel(const __grid_constant__ 
     {
         // bound on the magnitude of the fp32-evaluated terms, over every domain and s:
         // (s/2) n SRD + (s/2) SR SD <= s n 1020 SR ;  s^2 C / 16 <= smax^2 Cmax / 16
-        const double mp = P.smax * (double)n * 1020.0 * W.SR + P.smax * P.smax * P.cmax * 0.0625;
+        const double mp = P.smax * (double)n * 1020.0 * W.SR + P.smax * P.smax * cmax * 0.0625;
         W.margin = ldexp(W.A + mp, -18) + 1e-30;  // 64 ulp(fp32) of the magnitudes
     }
     Best best;
@@ -357,7 +360,7 @@ __global__ void __launch_bounds__(256, 1) search_kernel(const __grid_constant__ 
         pb.e = best.e;
         pb.d = best.d;
         pb.kj = best.kj;
-        P.part[(size_t)r * P.nsplit + split] = pb;
+        P.part[(size_t)r * P.ns_cap + split] = pb;
         if (P.exact_count && n_exact) atomicAdd(P.exact_count, (unsigned long long)n_exact);
     }
 }
@@ -385,7 +388,7 @@ static cudaError_t launch_search_b(int32_t nsp, const SearchParams &p, cudaStrea
 }
 
 cudaError_t launch_search(int32_t B, int32_t nsp, const SearchParams &p, cudaStream_t st) {
-    if (p.n_r == 0 || p.nsplit == 0) return cudaSuccess;
+    if (p.n_r == 0 || p.nsplit == 0) return cudaSuccess;  // n_r: upper bound
     switch (B) {
     case 2: return launch_search_b<2>(nsp, p, st);
     case 4: return launch_search_b<4>(nsp, p, st);
@@ -424,7 +427,11 @@ __device__ __forceinline__ int o_code_dev(double o) {
 
 __global__ void finalize_kernel(const __grid_constant__ FinalizeParams P) {
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= P.n_r) return;
+    if (r >= (int)*P.d_nr) return;
+    if (P.d_misc[0] == 0) {  // ranges but no domain block survived the entropy filter
+        if (r == 0) *P.d_err = FIC_ERR_EMPTY_POOL;
+        return;
+    }
     const int2 rr = P.ranges[r];
     const int B = P.B, n = B * B;
     long long sr = 0, srr = 0;
@@ -446,7 +453,8 @@ __global__ void finalize_kernel(const __grid_constant__ FinalizeParams P) {
         best.d = INT_MAX;
         best.kj = INT_MAX;
     }
-    for (int sp = 0; sp < P.nsplit; ++sp) {
+    const int ns = P.nsplit > 0 ? (int)*P.d_ns : 0;
+    for (int sp = 0; sp < ns; ++sp) {
         const Partial c = P.part[(size_t)r * P.nsplit + sp];
         if (lex_less(c.e, c.d, c.kj, best)) { best.e = c.e; best.d = c.d; best.kj = c.kj; }
     }

@@ -233,11 +233,14 @@ cudaError_t launch_pool_tc(const uint8_t *img, int32_t N, int32_t B, int32_t L, 
 // core-matrix layout, B_BYTES contiguous bytes (one bulk copy per CTA); zero rows past n_r.
 template <int B>
 __global__ void __launch_bounds__(256) tc_range_operand_kernel(const uint8_t *__restrict__ img, int32_t N,
-                                                               const int2 *__restrict__ ranges, int32_t n_r,
+                                                               const int2 *__restrict__ ranges,
+                                                               const unsigned long long *__restrict__ d_nr,
                                                                int64_t total16, uint8_t *__restrict__ Bop) {
     using Cf = TCfg<B>;
     const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // one 16-byte group
     if (e >= total16) return;
+    const int64_t n_r = (int64_t)*d_nr;
+    if (e / ((int64_t)Cf::N * (Cf::KP / 16)) > (n_r + Cf::NR - 1) / Cf::NR) return;  // past the last group
     constexpr int G16 = Cf::KP / 16;
     const int64_t row_g = e / G16;  // global row = group * N + row
     const int g = (int)(e % G16);
@@ -277,10 +280,13 @@ struct TCRangeG {
 // Thread per range: SR, A = n SRR - SR^2 and the filter margin
 template <int B>
 __global__ void tc_range_meta_kernel(const uint8_t *__restrict__ img, int32_t N, const int2 *__restrict__ ranges,
-                                     int32_t n_r, int32_t n_pad, double smax, double cmax,
+                                     const unsigned long long *__restrict__ d_nr, int32_t n_pad, double smax,
+                                     const unsigned long long *__restrict__ d_misc,
                                      TCRangeG *__restrict__ meta) {
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= n_pad) return;
+    const int n_r = (int)*d_nr;
+    const double cmax = (double)d_misc[1];
     constexpr int n = B * B;
     TCRangeG R;
     long long sr = 0, srr = 0;
@@ -311,6 +317,9 @@ __global__ void tc_range_meta_kernel(const uint8_t *__restrict__ img, int32_t N,
 
 // ------------------------------------------------------------------------------ search kernel
 struct TCParams {
+    const unsigned long long *d_nr, *d_misc;  // device sizes: n_r; n_kept, Cmax
+    unsigned long long *d_ns;
+    int32_t ns_cap;
     const uint8_t *Bop;        // [groups][B_BYTES] range operand
     const TCRangeG *rmeta;     // [groups * NR]
     const uint8_t *img;
@@ -355,10 +364,14 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
     int2 *sQ = reinterpret_cast<int2 *>(sBest + NR * kTileD);  // [epilogue threads][4] exact queue
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int r0 = blockIdx.x * NR;
-    const int split = blockIdx.y;
-    const int t0 = split * P.tiles_per_split;
-    const int t1 = min(P.n_tiles, t0 + P.tiles_per_split);
+    const int n_r = (int)*P.d_nr;
+    const int n_tiles = (int)((P.d_misc[0] + kTileD - 1) / kTileD);
+    int group, split, ns;  // uniform per CTA: decided before any barrier
+    if (!cta_work(n_r, NR, n_tiles, 4, P.ns_cap, group, split, ns)) return;
+    if (group == 0 && split == 0 && threadIdx.x == 0) *P.d_ns = (unsigned long long)ns;
+    const int r0 = group * NR;
+    const int t0 = (int)(((int64_t)split * n_tiles) / ns);
+    const int t1 = (int)(((int64_t)(split + 1) * n_tiles) / ns);
     const int ntl = max(0, t1 - t0);
     const int nsteps = ntl * CH;
 
@@ -398,7 +411,7 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
         if (lane == 0) {
             // the resident range operand of this CTA's NR ranges (prepared by tc_range_operand_kernel)
             tmbar_expect_tx(bbar, Cf::B_BYTES);
-            tbulk_g2s(sB, P.Bop + (size_t)blockIdx.x * Cf::B_BYTES, Cf::B_BYTES, bbar);
+            tbulk_g2s(sB, P.Bop + (size_t)group * Cf::B_BYTES, Cf::B_BYTES, bbar);
             for (int i = 0; i < nsteps; ++i) {
                 const int s = i % STAGES;
                 if (i >= STAGES) tmbar_wait(&empty[s], (uint32_t)(((i / STAGES) + 1) & 1));
@@ -600,7 +613,7 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
             const Partial c = sRed[threadIdx.x * 4 + w];
             if (c.e < b.e || (c.e == b.e && (c.d < b.d || (c.d == b.d && c.kj < b.kj)))) b = c;
         }
-        if (r < P.n_r) P.part[(size_t)r * P.nsplit + split] = b;
+        if (r < n_r) P.part[(size_t)r * P.ns_cap + split] = b;
     }
     if (warp == 0) {
         tc_fence_after();
@@ -659,12 +672,12 @@ static cudaError_t tc_range_prep(const SearchParams &sp, uint8_t *scratch, TCPar
     TCRangeG *meta = reinterpret_cast<TCRangeG *>(scratch + (size_t)groups * Cf::B_BYTES);
     const int64_t total16 = groups * Cf::N * (Cf::KP / 16);
     tc_range_operand_kernel<B><<<(unsigned)((total16 + 255) / 256), 256, 0, st>>>(sp.img, sp.N, sp.ranges,
-                                                                                  sp.n_r, total16, Bop);
+                                                                                  sp.d_nr, total16, Bop);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     const int n_pad = (int)(groups * Cf::NR);
-    tc_range_meta_kernel<B><<<(unsigned)((n_pad + 127) / 128), 128, 0, st>>>(sp.img, sp.N, sp.ranges, sp.n_r,
-                                                                              n_pad, sp.smax, sp.cmax, meta);
+    tc_range_meta_kernel<B><<<(unsigned)((n_pad + 127) / 128), 128, 0, st>>>(sp.img, sp.N, sp.ranges, sp.d_nr,
+                                                                              n_pad, sp.smax, sp.d_misc, meta);
     p.Bop = Bop;
     p.rmeta = meta;
     return cudaGetLastError();
@@ -686,12 +699,13 @@ cudaError_t launch_tc_search(int32_t B, const SearchParams &sp, const uint8_t *D
     if (e0 != cudaSuccess) return e0;
     p.img = sp.img; p.N = sp.N; p.ranges = sp.ranges; p.n_r = sp.n_r;
     p.Dtc = Dtc; p.SD = sp.SD; p.C = sp.C; p.t2f = sp.t2f; p.n_slots = n_slots;
-    p.n_tiles = sp.n_tiles; p.tiles_per_split = sp.tiles_per_split; p.nsplit = sp.nsplit;
+    p.d_nr = sp.d_nr; p.d_misc = sp.d_misc; p.nsplit = sp.nsplit; p.n_slots = sp.slot_stride;
+    p.d_ns = sp.d_ns; p.ns_cap = sp.ns_cap;
     p.nsp = sp.nsp;
     memcpy(p.spos, sp.spos, sizeof p.spos);
     memcpy(p.jpos, sp.jpos, sizeof p.jpos);
     p.has_zero = sp.has_zero; p.j_zero = sp.j_zero;
-    p.smax = sp.smax; p.cmax = sp.cmax;
+    p.smax = sp.smax;
     p.part = sp.part; p.exact_count = sp.exact_count;
     switch (B) {
     case 2: return launch_tc_b<2>(p, st);
