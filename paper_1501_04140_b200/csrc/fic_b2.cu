@@ -6,6 +6,7 @@
 // the 4-point DFT diagonalises the rotations and conjugates under the mirrors, which gives
 // (verified exhaustively in tests against the oracle and by scripts):
 //   max_k Bq_k = max( X2 Y2 + xr2 yr + xi2 yi ,  -X2 Y2 + xr2 yi + xi2 yr )
+//              = ( (xr2 + xi2)(yr + yi) + | 2 X2 Y2 + (xr2 - xi2)(yr - yi) | ) / 2      (4 flops)
 //   X2 = a - b + c - d,  xr2 = 2|a - c|,  xi2 = 2|b - d|      (range features)
 //   Y2 = w - x + y - z,  yr = |w - y|,    yi = |x - z|        (domain features)
 // with Bq_k = n SRD_k - SR SD (n = 4).  Every product and sum is an integer below 2^24, so the
@@ -49,7 +50,7 @@ __device__ __forceinline__ void b2_wait(uint64_t *bar, uint32_t parity) {
     }
 }
 
-// Domain features: float4 (Y2, yr, yi, C) per slot; zero on pads (their t2 = +inf excludes them).
+// Domain features: float4 (Y2, yr + yi, yr - yi, C) per slot; zero on pads (t2 = +inf excludes them).
 __global__ void b2_pool_kernel(const uint8_t *__restrict__ img, int32_t N, int32_t L, int32_t A,
                                const int32_t *__restrict__ kept, const unsigned long long *__restrict__ d_nk,
                                int64_t n_slots, float4 *__restrict__ F) {
@@ -70,7 +71,8 @@ __global__ void b2_pool_kernel(const uint8_t *__restrict__ img, int32_t N, int32
     const int w = dp(0, 0), x = dp(0, 1), y = dp(1, 1), z = dp(1, 0);
     const int sd = w + x + y + z;
     const int cc = 4 * (w * w + x * x + y * y + z * z) - sd * sd;  // C = n SDD - SD^2 < 2^24
-    F[d] = make_float4((float)(w - x + y - z), (float)abs(w - y), (float)abs(x - z), (float)cc);
+    const int yr = abs(w - y), yi = abs(x - z);
+    F[d] = make_float4((float)(w - x + y - z), (float)(yr + yi), (float)(yr - yi), (float)cc);
 }
 
 cudaError_t launch_b2_pool(const uint8_t *img, int32_t N, int32_t L, int32_t A, const int32_t *kept,
@@ -229,7 +231,7 @@ __global__ void __launch_bounds__(kB2Threads) b2search_kernel(const __grid_const
         if (nstages > 1) issue(1);
     }
 
-    float X2[RPT], xr2[RPT], xi2[RPT], thr[RPT];
+    float X2d[RPT], sx[RPT], dx[RPT], thr[RPT];  // 2 X2, xr2 + xi2, xr2 - xi2
     const int rbase = (group * kB2Threads + threadIdx.x) * RPT;
     const double u = 5.9604644775390625e-08;
 #pragma unroll
@@ -242,9 +244,9 @@ __global__ void __launch_bounds__(kB2Threads) b2search_kernel(const __grid_const
             const uint8_t *p0 = P.img + (size_t)rr.y * P.N + rr.x;
             a = p0[0]; b = p0[1]; d = p0[P.N]; c = p0[P.N + 1];
         }
-        X2[q] = (float)(a - b + c - d);
-        xr2[q] = (float)(2 * abs(a - c));
-        xi2[q] = (float)(2 * abs(b - d));
+        X2d[q] = (float)(2 * (a - b + c - d));
+        sx[q] = (float)(2 * abs(a - c) + 2 * abs(b - d));
+        dx[q] = (float)(2 * abs(a - c) - 2 * abs(b - d));
         const int sr = a + b + c + d, srr = a * a + b * b + c * c + d * d;
         cd.A = (double)(4 * srr - sr * sr);
         cd.SR = sr;
@@ -259,7 +261,7 @@ __global__ void __launch_bounds__(kB2Threads) b2search_kernel(const __grid_const
     }
     float nhs[NSP];
 #pragma unroll
-    for (int jj = 0; jj < NSP; ++jj) nhs[jj] = jj < P.nsp ? -__double2float_rn(0.5 * P.spos[jj]) : 0.f;
+    for (int jj = 0; jj < NSP; ++jj) nhs[jj] = jj < P.nsp ? -__double2float_rn(0.25 * P.spos[jj]) : 0.f;  // x 2 Bq
     unsigned n_exact = 0;
 
     for (int s = 0; s < nstages; ++s) {
@@ -292,9 +294,7 @@ __global__ void __launch_bounds__(kB2Threads) b2search_kernel(const __grid_const
 #pragma unroll
                     for (int q = 0; q < RPT; ++q) {
                         const float4 f = f2[u2];
-                        const float v1 = fmaf(X2[q], f.x, fmaf(xr2[q], f.y, xi2[q] * f.z));
-                        const float v2 = fmaf(-X2[q], f.x, fmaf(xr2[q], f.z, xi2[q] * f.y));
-                        const float bq = fmaxf(v1, v2);  // = max_k Bq_k, exact
+                        const float bq = fmaf(sx[q], f.y, fabsf(fmaf(X2d[q], f.x, dx[q] * f.z)));  // 2 max_k Bq_k
                         float g = fmaf(nhs[0], bq, t2v[u2][0]);
 #pragma unroll
                         for (int jj = 1; jj < NSP; ++jj) g = fminf(g, fmaf(nhs[jj], bq, t2v[u2][jj]));
@@ -307,14 +307,13 @@ __global__ void __launch_bounds__(kB2Threads) b2search_kernel(const __grid_const
                         const float4 f = f2[u2];
 #pragma unroll
                         for (int q = 0; q < RPT; ++q) {
-                            const float bq = fmaxf(fmaf(X2[q], f.x, fmaf(xr2[q], f.y, xi2[q] * f.z)),
-                                                   fmaf(-X2[q], f.x, fmaf(xr2[q], f.z, xi2[q] * f.y)));
+                            const float bq = fmaf(sx[q], f.y, fabsf(fmaf(X2d[q], f.x, dx[q] * f.z)));  // 2 Bq
                             float g = fmaf(nhs[0], bq, t2v[u2][0]);
 #pragma unroll
                             for (int jj = 1; jj < NSP; ++jj) g = fminf(g, fmaf(nhs[jj], bq, t2v[u2][jj]));
                             if (g <= thr[q]) {
                                 thr[q] = b2_exact(P, &cold[q * kB2Threads + threadIdx.x], thr[q], rbase + q,
-                                                  dbase + dl0 + u2, bq, f.w);
+                                                  dbase + dl0 + u2, 0.5f * bq, f.w);
                                 ++n_exact;
                             }
                         }
