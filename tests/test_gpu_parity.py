@@ -286,3 +286,60 @@ def test_c5_sampled(fic):
     cfg = config("C5")
     img, got = encode_both(fic, cfg)
     sampled_level_check(fic, img, cfg, got, per_level=3, parents=2)
+
+
+# ------------------------------------------------------------------ every search implementation
+@pytest.mark.parametrize("mode", ["tc", "fourier", "direct"])
+def test_search_modes_parity(fic, mode):
+    """The non-default kernels (tcgen05 at B = 2, D4-Fourier CUDA cores, direct FFMA) are
+    bit-exact too; FIC_SEARCH is read when a context is created."""
+    import os
+    p, _, torch = fic
+    old = os.environ.get("FIC_SEARCH")
+    os.environ["FIC_SEARCH"] = mode
+    try:
+        ctx = p.Context(0)
+        for smode in ("predefined", "grid"):
+            cfg = config("C2", s_mode=smode, t=6.0)
+            cfg["N"] = 128
+            cfg["tau"] = [-1.0, 4.6, 3.6, 2.6]
+            img = make_image(128, 91, texture=True)
+            got = p.records_to_numpy(ctx.encode_cfg(cfg, dev(torch, img)))
+            assert_same(got, oracle.encode_cfg(cfg, img), f"{mode} {smode}")
+        ctx.close()
+    finally:
+        if old is None:
+            os.environ.pop("FIC_SEARCH", None)
+        else:
+            os.environ["FIC_SEARCH"] = old
+
+
+def test_capacity_error_reports_count(fic):
+    p, ctx, torch = fic
+    cfg = config("C2")
+    img = image_for(cfg)
+    full = ctx.encode_cfg(cfg, dev(torch, img))
+    small = torch.empty((10, 40), dtype=torch.uint8, device="cuda")
+    import ctypes as C
+    n_out = C.c_int64()
+    tau, n_s, s_flat, tol = ctx._cfg_arrays(cfg["tau"], cfg["s"], cfg["rms_tol"])
+    from paper_1501_04140_b200.fic import _dptr, _ptr
+    st = ctx.lib.fic_encode(ctx.handle, _dptr(dev(torch, img)), cfg["N"], cfg["B_max"], cfg["B_min"], cfg["L"],
+                            _ptr(tau), _ptr(s_flat), _ptr(n_s), _ptr(tol), 0, 1, _dptr(small), 10,
+                            C.byref(n_out))
+    assert st == 4 and n_out.value == full.shape[0]
+    # the first records written are the canonical first ones
+    assert small.cpu().numpy().tobytes() == full[:10].cpu().numpy().tobytes()
+
+
+def test_b32_and_bad_args(fic):
+    p, ctx, torch = fic
+    img = dev(torch, make_image(128, 2))
+    with pytest.raises(p.FicError) as ei:  # B_max = 32 not supported on the GPU path
+        ctx.encode(img, 32, 2, 2, [-1] * 5, [(0.5,)] * 5, [8.0] * 5)
+    assert ei.value.status == 1
+    with pytest.raises(p.FicError) as ei:  # more than 16 contrast values
+        ctx.encode(img, 16, 2, 2, [-1] * 4, [tuple(np.linspace(0, 1, 17))] * 4, [8.0] * 4)
+    assert ei.value.status == 1
+    with pytest.raises(p.FicError):
+        ctx.encode(img, 16, 2, 2, [-1] * 4, [(0.5,)] * 4, [8.0] * 4, shard=3, n_shards=2)
