@@ -311,7 +311,10 @@ __global__ void tc_range_meta_kernel(const uint8_t *__restrict__ img, int32_t N,
     const double hs = 0.5 * smax;
     const double bq = sqrt(R.A * cmax) * 1.01 + (B > 8 ? (double)n * 1020.0 * (double)sr : 0.0);
     const double t2m = smax * smax * cmax * 0.0625;
-    R.margin = 8.0 * u * (hs * bq + t2m) + 1e-12 * (R.A + hs * bq + t2m) + 1e-30;
+    // + the int -> float conversion of Bq in the epilogue: exact at B = 2, |error| <= 2 at B = 4,
+    // <= 64 at B = 8 (floor of Bq / 2 and Bq / 64): hs * 64 covers both
+    R.margin = 8.0 * u * (hs * bq + t2m) + 1e-12 * (R.A + hs * bq + t2m) + (B == 4 || B == 8 ? hs * 64.0 : 0.0) +
+               1e-30;
     meta[r] = R;
 }
 
@@ -517,8 +520,12 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
                     if constexpr (B == 2) {
                         // |Bq| <= sqrt(A C) < 2^22: exact int -> float by the 1.5 * 2^23 magic
                         bq = __int_as_float(n * mx - rsr * sd + 0x4B400000) - 12582912.0f;
-                    } else if constexpr (B <= 8) {
-                        bq = (float)(n * mx - rsr * sd);  // exact int32 (|.| < 2^31)
+                    } else if constexpr (B == 4) {
+                        // |Bq| <= n^2 127.5 510 < 2^24: magic on Bq / 2, error <= 1 (margin)
+                        bq = (__int_as_float(((n * mx - rsr * sd) >> 1) + 0x4B400000) - 12582912.0f) * 2.0f;
+                    } else if constexpr (B == 8) {
+                        // |Bq| < 2^28: magic on Bq / 64, error <= 64 (margin)
+                        bq = (__int_as_float(((n * mx - rsr * sd) >> 6) + 0x4B400000) - 12582912.0f) * 64.0f;
                     } else {
                         bq = fmaf((float)n, (float)mx, -((float)rsr * (float)sd));
                     }
