@@ -112,6 +112,14 @@ struct B2Cold {
     int32_t SR;
 };
 
+// filter margin of one range (e units): |Bq| <= sqrt(A C); fp32 -hs and t2 roundings and one
+// FFMA -> 4u (hs |Bq| + t2); shared by the search and the threshold seeding (must be identical)
+__device__ __forceinline__ double b2_margin(double A, double smax, double cmax) {
+    const double u = 5.9604644775390625e-08;
+    const double hs = 0.5 * smax, t2m = smax * smax * cmax * 0.0625;
+    return 4.0 * u * (hs * sqrt(A * cmax) * 1.01 + t2m) + 1e-12 * (A + t2m) + 1e-30;
+}
+
 constexpr int kB2TPS = 4;   // tiles per stage
 constexpr int kB2RPT = 4;   // ranges per thread
 constexpr int kB2Threads = 256;
@@ -233,7 +241,6 @@ __global__ void __launch_bounds__(kB2Threads) b2search_kernel(const __grid_const
 
     float X2d[RPT], sx[RPT], dx[RPT], thr[RPT];  // 2 X2, xr2 + xi2, xr2 - xi2
     const int rbase = (group * kB2Threads + threadIdx.x) * RPT;
-    const double u = 5.9604644775390625e-08;
 #pragma unroll
     for (int q = 0; q < RPT; ++q) {
         const int r = rbase + q;
@@ -251,9 +258,7 @@ __global__ void __launch_bounds__(kB2Threads) b2search_kernel(const __grid_const
         cd.A = (double)(4 * srr - sr * sr);
         cd.SR = sr;
         cd.px = a | (b << 8) | (c << 16) | (d << 24);
-        // |Bq| <= sqrt(A C); fp32: -hs and t2 roundings and one FFMA -> 4u (hs |Bq| + t2)
-        const double hs = 0.5 * P.smax, t2m = P.smax * P.smax * cmax * 0.0625;
-        cd.margin = 4.0 * u * (hs * sqrt(cd.A * cmax) * 1.01 + t2m) + 1e-12 * (cd.A + t2m) + 1e-30;
+        cd.margin = b2_margin(cd.A, P.smax, cmax);
         if (P.has_zero) { cd.best_e = cd.A; cd.best_d = 0; cd.best_kj = P.j_zero; }
         else { cd.best_e = INFINITY; cd.best_d = INT_MAX; cd.best_kj = INT_MAX; }
         float th = P.has_zero ? fminf(__double2float_ru(cd.margin), FLT_MAX) : FLT_MAX;
@@ -284,6 +289,7 @@ __global__ void __launch_bounds__(kB2Threads) b2search_kernel(const __grid_const
                 float4 f2[2];
                 float t2v[2][NSP];
                 float mn[2];
+                float gq[2][RPT], bqq[2][RPT];
 #pragma unroll
                 for (int u2 = 0; u2 < 2; ++u2) {
                     f2[u2] = Ft[dl0 + u2];
@@ -298,22 +304,19 @@ __global__ void __launch_bounds__(kB2Threads) b2search_kernel(const __grid_const
                         float g = fmaf(nhs[0], bq, t2v[u2][0]);
 #pragma unroll
                         for (int jj = 1; jj < NSP; ++jj) g = fminf(g, fmaf(nhs[jj], bq, t2v[u2][jj]));
+                        gq[u2][q] = g;
+                        bqq[u2][q] = bq;
                         mn[u2] = fminf(mn[u2], g - thr[q]);
                     }
                 }
                 if (fminf(mn[0], mn[1]) <= 0.0f) {
 #pragma unroll
                     for (int u2 = 0; u2 < 2; ++u2) {
-                        const float4 f = f2[u2];
 #pragma unroll
                         for (int q = 0; q < RPT; ++q) {
-                            const float bq = fmaf(sx[q], f.y, fabsf(fmaf(X2d[q], f.x, dx[q] * f.z)));  // 2 Bq
-                            float g = fmaf(nhs[0], bq, t2v[u2][0]);
-#pragma unroll
-                            for (int jj = 1; jj < NSP; ++jj) g = fminf(g, fmaf(nhs[jj], bq, t2v[u2][jj]));
-                            if (g <= thr[q]) {
+                            if (gq[u2][q] <= thr[q]) {
                                 thr[q] = b2_exact(P, &cold[q * kB2Threads + threadIdx.x], thr[q], rbase + q,
-                                                  dbase + dl0 + u2, 0.5f * bq, f.w);
+                                                  dbase + dl0 + u2, 0.5f * bqq[u2][q], f2[u2].w);
                                 ++n_exact;
                             }
                         }
@@ -343,6 +346,41 @@ __global__ void __launch_bounds__(kB2Threads) b2search_kernel(const __grid_const
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) n_exact += __shfl_xor_sync(0xffffffffu, n_exact, o);
     if ((threadIdx.x & 31) == 0 && n_exact && P.exact_count) atomicAdd(P.exact_count, (unsigned long long)n_exact);
+}
+
+// Threshold seeding: each range's exact best over a strided sample of kS domains is an upper
+// bound of its final best, so RU(best - A + margin) is a valid initial shared threshold.
+constexpr int kS = 32;
+__global__ void b2_seed_kernel(const __grid_constant__ B2Params P) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    const int n_r = (int)*P.d_nr;
+    if (r >= n_r) return;
+    const int64_t n_k = (int64_t)P.d_misc[0];
+    if (n_k == 0) return;
+    const double cmax = (double)P.d_misc[1];
+    const int2 rr = P.ranges[r];
+    const uint8_t *p0 = P.img + (size_t)rr.y * P.N + rr.x;
+    const int a = p0[0], b = p0[1], d = p0[P.N], c = p0[P.N + 1];
+    const float X2d = (float)(2 * (a - b + c - d));
+    const float sx = (float)(2 * abs(a - c) + 2 * abs(b - d));
+    const float dx = (float)(2 * abs(a - c) - 2 * abs(b - d));
+    const int sr = a + b + c + d, srr = a * a + b * b + c * c + d * d;
+    const double A = (double)(4 * srr - sr * sr);
+    double best = P.has_zero ? A : INFINITY;
+    for (int i = 0; i < kS; ++i) {
+        const int64_t dd = (i * n_k) / kS;
+        const float4 f = P.F[dd];
+        const double Bq = 0.5 * (double)fmaf(sx, f.y, fabsf(fmaf(X2d, f.x, dx * f.z)));  // exact
+        const double c16 = __dmul_rn(0.0625, (double)f.w);
+        for (int jj = 0; jj < P.nsp; ++jj) {
+            const double s = P.spos[jj];
+            const double e = __dadd_rn(__dsub_rn(A, __dmul_rn(__dmul_rn(0.5, s), Bq)),
+                                       __dmul_rn(__dmul_rn(s, s), c16));
+            best = fmin(best, e);
+        }
+    }
+    if (best < INFINITY)
+        P.gthr[r] = fminf(__double2float_ru(__dadd_rn(__dsub_rn(best, A), b2_margin(A, P.smax, cmax))), FLT_MAX);
 }
 
 template <int NSP>
@@ -392,6 +430,9 @@ cudaError_t launch_b2_search(const SearchParams &sp, const float4 *F, const floa
     p.part = sp.part; p.exact_count = sp.exact_count;
     p.gthr = gthr;
     cudaError_t e = cudaMemsetAsync(gthr, 0x7f, sizeof(float) * (size_t)sp.n_r, st);  // ~3.4e38
+    if (e != cudaSuccess) return e;
+    b2_seed_kernel<<<(unsigned)((sp.n_r + 127) / 128), 128, 0, st>>>(p);
+    e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     if (sp.nsp <= 1) return launch_b2_t<1>(p, st);
     if (sp.nsp <= 2) return launch_b2_t<2>(p, st);
