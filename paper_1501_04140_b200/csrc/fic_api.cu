@@ -283,12 +283,11 @@ fic_status level_enqueue(fic_ctx *ctx, const Pool &P, const uint8_t *img, const 
             ctx->launches += 1;
         }
     } else if (P.mode == 3) {
-        CK(grow(ctx, ctx->b_u, sizeof(float) * (size_t)slots * (sp.nsp ? sp.nsp : 1)));
-        CK(fic::launch_fourier_u(P.C, &P.d_misc[0], slots, sl, sp.nsp, ptr<float>(ctx->b_u), st));
+        CK(grow(ctx, ctx->b_u, sizeof(float) * (size_t)slots * fic::b2_t2_width(sp.nsp)));
         if (ctx->timing) CK(cudaEventRecord(ctx->ev[level_slot][1], st));
-        CK(grow(ctx, ctx->b_gthr, sizeof(float) * (size_t)n_r_max));
-        CK(fic::launch_b2_search(sp, P.F2, ptr<float>(ctx->b_u), P.kept, P.L, P.A, ptr<float>(ctx->b_gthr), st));
-        ctx->launches += sp.nsp > 0 ? 2 : 0;
+        CK(grow(ctx, ctx->b_gthr, fic::b2_scratch_bytes(n_r_max, sp.ns_cap)));
+        CK(fic::launch_b2_search(sp, P.F2, ptr<float>(ctx->b_u), P.kept, P.L, P.A, ctx->b_gthr.p, st));
+        ctx->launches += sp.nsp > 0 && n_r_max > 0 ? 3 : 0;  // t2 table, pass 1 scan, pass 2 exact
     } else {
         const int nc = fic::fourier_record_stride(P.B);  // >= 8 nO + 1
         const int32_t r_stride = (int32_t)((n_r_max + 31) / 32 * 32);

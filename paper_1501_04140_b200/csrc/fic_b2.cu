@@ -82,51 +82,196 @@ cudaError_t launch_b2_pool(const uint8_t *img, int32_t N, int32_t L, int32_t A, 
     return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------------------------
+// Search, in two passes.
+//
+// Pass 1 (b2scan_kernel) is the data-parallel bulk of the level: a thread owns kB2RPT ranges
+// (registers, packed pairs, so the arithmetic issues as FFMA2/FMUL2: two fp32 FMAs per
+// fma-pipe slot), the CTA streams its split's domain features through shared memory
+// (cp.async.bulk, kB2NB buffers, released by the last warp -- no CTA barrier).  Per
+// (range, domain) it is 5 fp32 FMA lanes + one FMNMX3 and no branch:
+//     Q  = X2 Y2 + dx z,  bq = sx y + |Q|                       (= 2 max_k Bq_k, exact)
+//     g_j = -(s_j/4) bq + t2_j   (j packed in pairs)            (fp32 lower bound of e_j - A)
+//     gmin = min(gmin, g_j ...)
+// and it stores gmin per (range, split).  |g_j - (e_j - A)| <= margin for every pair, so
+//     thr = RU(min_splits gmin + 2 margin) >= best - A + margin
+// and a pair with g > thr can neither win nor tie.
+//
+// Pass 2 (b2exact_kernel), one warp per range: only the splits with gmin <= thr can hold such a
+// pair (usually the winner's split alone); the warp rescans them with the same fp32 arithmetic,
+// sends every pair with g <= thr to the canonical binary64 score, and reduces the lexicographic
+// first minimum (e; d, k, j) over its lanes.  The result equals the exhaustive loop.
 struct B2Params {
     const uint8_t *img;
     int32_t N, L, A;
     const int2 *ranges;
     int32_t n_r;
-    const float4 *F;       // [n_slots]
-    const float *U;        // [n_tiles][nsp][128] t2_j
-    const int64_t *C;      // [n_slots]
+    const float4 *F;       // [n_slots] (Y2, yr + yi, yr - yi, C)
+    const float *T;        // [n_slots][tw] t2_j = RN((s_j s_j)(C/16)), +inf on pads
+    int32_t tw;
     const int32_t *kept;
     const unsigned long long *d_nr, *d_misc;  // device sizes: n_r; n_kept, Cmax
     int32_t nsplit;
     int32_t nsp;
     double spos[kMaxS];
+    float nhs[kMaxS];  // -RN(s_j / 4) (host-rounded, identical to the device conversion)
     int32_t jpos[kMaxS];
     int32_t has_zero, j_zero;
     double smax;
     Partial *part;
     unsigned long long *exact_count;
-    float *gthr;  // [n_r] threshold shared by all domain splits (CAS-min), initialised to ~FLT_MAX
-    unsigned long long *d_ns;
+    float *gmin;                    // [n_r][ns_cap] pass-1 minimum of g per (range, split)
+    unsigned long long *d_nscan;    // splits pass 1 used
+    unsigned long long *d_ns;       // splits of the partials finalize merges (= 1 here)
     int32_t ns_cap;
 };
 
-struct B2Cold {
-    double A, margin, best_e;
-    int32_t best_d, best_kj;
-    int32_t px;  // range pixels a, b, c, d packed as bytes (TL, TR, BR, BL)
-    int32_t SR;
-};
+constexpr int kB2Threads = 256;
+constexpr int kB2RPT = 8;  // ranges per thread (4 packed pairs)
+constexpr int kB2NB = 3;   // stage buffers
+constexpr int kB2Unroll = 4;
 
 // filter margin of one range (e units): |Bq| <= sqrt(A C); fp32 -hs and t2 roundings and one
-// FFMA -> 4u (hs |Bq| + t2); shared by the search and the threshold seeding (must be identical)
+// FFMA -> 4u (hs |Bq| + t2)
 __device__ __forceinline__ double b2_margin(double A, double smax, double cmax) {
     const double u = 5.9604644775390625e-08;
     const double hs = 0.5 * smax, t2m = smax * smax * cmax * 0.0625;
     return 4.0 * u * (hs * sqrt(A * cmax) * 1.01 + t2m) + 1e-12 * (A + t2m) + 1e-30;
 }
 
-constexpr int kB2TPS = 4;   // tiles per stage
-constexpr int kB2RPT = 4;   // ranges per thread
-constexpr int kB2Threads = 256;
+__device__ __forceinline__ float2 b2_bc(float v) { return make_float2(v, v); }
+
+// range features from the 4 pixels a, b, c, d (TL, TR, BR, BL)
+struct B2Range {
+    float x2, dx, sx;  // 2 X2, xr2 - xi2, xr2 + xi2
+    int32_t A;         // n SRR - SR^2
+};
+__device__ __forceinline__ B2Range b2_range(int a, int b, int c, int d) {
+    B2Range R;
+    R.x2 = (float)(2 * (a - b + c - d));
+    R.sx = (float)(2 * abs(a - c) + 2 * abs(b - d));
+    R.dx = (float)(2 * abs(a - c) - 2 * abs(b - d));
+    const int sr = a + b + c + d, srr = a * a + b * b + c * c + d * d;
+    R.A = 4 * srr - sr * sr;
+    return R;
+}
+
+template <int NP>
+__global__ void __launch_bounds__(kB2Threads, 3) b2scan_kernel(const __grid_constant__ B2Params P) {
+    constexpr int RPT = kB2RPT, NB = kB2NB, TW = 2 * NP;
+    constexpr int TPS = NP == 1 ? 2 : 1;  // tiles per stage
+    constexpr int SDOM = TPS * kTileD;    // domains per stage
+    constexpr int NWARP = kB2Threads / 32;
+    extern __shared__ __align__(128) unsigned char smem[];
+    float4 *Fs = reinterpret_cast<float4 *>(smem);         // [NB][SDOM]
+    float *Ts = reinterpret_cast<float *>(Fs + NB * SDOM);  // [NB][SDOM][TW]
+    uint64_t *full = reinterpret_cast<uint64_t *>(Ts + NB * SDOM * TW);
+    int *relcnt = reinterpret_cast<int *>(full + NB);
+
+    const int n_r = (int)*P.d_nr;
+    const int n_tiles = (int)((P.d_misc[0] + kTileD - 1) / kTileD);
+    int group, split, ns;
+    if (!cta_work(n_r, kB2Threads * RPT, n_tiles, 2 * TPS, P.ns_cap, group, split, ns)) return;
+    if (group == 0 && split == 0 && threadIdx.x == 0) *P.d_nscan = (unsigned long long)ns;
+    const int t0 = (int)(((int64_t)split * n_tiles) / ns);
+    const int t1 = (int)(((int64_t)(split + 1) * n_tiles) / ns);
+    const int nstages = (max(0, t1 - t0) + TPS - 1) / TPS;
+    auto issue = [&](int s) {
+        const int b = s % NB;
+        const int ta = t0 + s * TPS, tb = min(t1, ta + TPS);
+        const uint32_t b1 = (uint32_t)(tb - ta) * kTileD * 16;
+        const uint32_t b2 = (uint32_t)(tb - ta) * kTileD * TW * 4;
+        b2_expect(&full[b], b1 + b2);
+        b2_bulk(Fs + b * SDOM, P.F + (size_t)ta * kTileD, b1, &full[b]);
+        b2_bulk(Ts + b * SDOM * TW, P.T + (size_t)ta * kTileD * TW, b2, &full[b]);
+    };
+    if (threadIdx.x == 0) {
+        for (int b = 0; b < NB; ++b) {
+            b2_bar_init(&full[b]);
+            relcnt[b] = 0;
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    __syncthreads();
+    if (threadIdx.x == 0)
+        for (int s = 0; s < NB && s < nstages; ++s) issue(s);
+
+    // ranges of this thread: r = group * threads * RPT + q * threads + tid (coalesced per q)
+    const int rg0 = group * kB2Threads * RPT + threadIdx.x;
+    float2 X[RPT / 2], DX[RPT / 2], SX[RPT / 2];
+    float gm[RPT];
+#pragma unroll
+    for (int q = 0; q < RPT; ++q) {
+        const int r = rg0 + q * kB2Threads;
+        int a = 0, b = 0, c = 0, d = 0;
+        if (r < n_r) {
+            const int2 rr = P.ranges[r];
+            const uint8_t *p0 = P.img + (size_t)rr.y * P.N + rr.x;
+            a = p0[0]; b = p0[1]; d = p0[P.N]; c = p0[P.N + 1];
+        }
+        const B2Range R = b2_range(a, b, c, d);
+        if (q & 1) { X[q / 2].y = R.x2; SX[q / 2].y = R.sx; DX[q / 2].y = R.dx; }
+        else { X[q / 2].x = R.x2; SX[q / 2].x = R.sx; DX[q / 2].x = R.dx; }
+        gm[q] = INFINITY;
+    }
+    float2 nh[NP];  // -(s_j / 4) (times 2 max Bq); zero on pads (t2 = +inf there)
+#pragma unroll
+    for (int jp = 0; jp < NP; ++jp) {
+        nh[jp].x = 2 * jp < P.nsp ? P.nhs[2 * jp] : 0.f;
+        nh[jp].y = 2 * jp + 1 < P.nsp ? P.nhs[2 * jp + 1] : 0.f;
+    }
+
+    for (int s = 0; s < nstages; ++s) {
+        const int b = s % NB;
+        b2_wait(&full[b], (uint32_t)((s / NB) & 1));
+        const float4 *Fb = Fs + b * SDOM;
+        const float *Tb = Ts + b * SDOM * TW;
+        const int nd = min(t1 - (t0 + s * TPS), TPS) * kTileD;
+#pragma unroll kB2Unroll
+        for (int dl = 0; dl < nd; ++dl) {
+            const float4 f = Fb[dl];
+            float2 t2[NP];
+#pragma unroll
+            for (int jp = 0; jp < NP; ++jp) t2[jp] = reinterpret_cast<const float2 *>(Tb + dl * TW)[jp];
+#pragma unroll
+            for (int p = 0; p < RPT / 2; ++p) {
+                float2 Q = __fmul2_rn(DX[p], b2_bc(f.z));
+                Q = __ffma2_rn(X[p], b2_bc(f.x), Q);
+                const float2 bq = __ffma2_rn(SX[p], b2_bc(f.y), make_float2(fabsf(Q.x), fabsf(Q.y)));
+#pragma unroll
+                for (int jp = 0; jp < NP; ++jp) {
+                    const float2 g0 = __ffma2_rn(nh[jp], b2_bc(bq.x), t2[jp]);
+                    const float2 g1 = __ffma2_rn(nh[jp], b2_bc(bq.y), t2[jp]);
+                    gm[2 * p] = fminf(gm[2 * p], fminf(g0.x, g0.y));
+                    gm[2 * p + 1] = fminf(gm[2 * p + 1], fminf(g1.x, g1.y));
+                }
+            }
+        }
+        // release the buffer: the last warp to finish it refills it (no CTA-wide barrier)
+        __syncwarp();
+        if ((threadIdx.x & 31) == 0) {
+            __threadfence_block();
+            const int old = atomicAdd(&relcnt[b], 1);
+            if (old == NWARP - 1) {
+                relcnt[b] = 0;
+                __threadfence_block();
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                if (s + NB < nstages) issue(s + NB);
+            }
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < RPT; ++q) {
+        const int r = rg0 + q * kB2Threads;
+        if (r < n_r) P.gmin[(size_t)r * P.ns_cap + split] = gm[q];
+    }
+}
 
 // k* of one (range, domain): all 8 SRD_k in integers (isometry convention of the oracle,
-// reading R2), lowest index of the maximum.  Only called when the pair improves the best.
-__device__ __noinline__ int b2_kstar(const B2Params &P, int32_t px, int32_t d) {
+// reading R2), lowest index of the maximum.  Only the rare zero-s tie needs it in the search;
+// otherwise finalize resolves it for the winner (kPendIso).
+__device__ __noinline__ int b2_kstar(const B2Params &P, int2 rr, int32_t d) {
     const int32_t c = P.kept[d];
     const int64_t x0 = (int64_t)(c % P.A) * P.L, y0 = (int64_t)(c / P.A) * P.L;
     int D[2][2];
@@ -137,8 +282,8 @@ __device__ __noinline__ int b2_kstar(const B2Params &P, int32_t px, int32_t d) {
             const uint8_t *q = P.img + (y0 + 2 * i) * P.N + x0 + 2 * j;
             D[i][j] = (int)q[0] + (int)q[1] + (int)q[P.N] + (int)q[P.N + 1];
         }
-    const int a = px & 255, b = (px >> 8) & 255, cc = (px >> 16) & 255, dd = (px >> 24) & 255;
-    const int R[2][2] = {{a, b}, {dd, cc}};
+    const uint8_t *p0 = P.img + (size_t)rr.y * P.N + rr.x;
+    const int R[2][2] = {{p0[0], p0[1]}, {p0[P.N], p0[P.N + 1]}};
     // f_k(i,j) for B = 2 (b = 1): 0 (i,j) 1 (1-j,i) 2 (1-i,1-j) 3 (j,1-i) 4 (i,1-j) 5 (j,i) 6 (1-i,j) 7 (1-j,1-i)
     int best = INT_MIN, ks = 0;
 #pragma unroll
@@ -166,236 +311,121 @@ __device__ __noinline__ int b2_kstar(const B2Params &P, int32_t px, int32_t d) {
     return ks;
 }
 
-// exact path: canonical binary64 score for every s > 0 from the exact max_k Bq_k and C
-// (no memory traffic); only a genuine lexicographic improvement fetches k* and publishes the
-// new threshold (per thread and, CAS-min, across domain splits)
-__device__ __noinline__ float b2_exact(const B2Params &P, B2Cold *cdp, float thr, int r, int32_t d,
-                                       float bqf, float cf) {
-    B2Cold &cd = *cdp;
-    const double Bq = (double)bqf, c16 = __dmul_rn(0.0625, (double)cf);
-    double e0 = INFINITY;
-    int j0 = 0;
-    for (int jj = 0; jj < P.nsp; ++jj) {
-        const double s = P.spos[jj];
-        const double e = __dadd_rn(__dsub_rn(cd.A, __dmul_rn(__dmul_rn(0.5, s), Bq)),
-                                   __dmul_rn(__dmul_rn(s, s), c16));
-        if (e < e0) { e0 = e; j0 = jj; }  // lowest j among equal e (same k* for every s > 0)
-    }
-    if (e0 > cd.best_e || (e0 == cd.best_e && d > cd.best_d)) return thr;
-    const int ks = b2_kstar(P, cd.px, d);
-    const int32_t kj = (ks << 8) | P.jpos[j0];
-    if (e0 == cd.best_e && d == cd.best_d && kj >= cd.best_kj) return thr;
-    cd.best_e = e0;
-    cd.best_d = d;
-    cd.best_kj = kj;
-    const float t = fminf(__double2float_ru(__dadd_rn(__dsub_rn(e0, cd.A), cd.margin)), FLT_MAX);
-    int *gi = reinterpret_cast<int *>(P.gthr + r);
-    int old = *gi;
-    while (t < __int_as_float(old)) {
-        const int prev = atomicCAS(gi, old, __float_as_int(t));
-        if (prev == old) break;
-        old = prev;
-    }
-    return fminf(thr, t);
+__device__ __forceinline__ bool b2_less(double e, int32_t d, int32_t kj, double be, int32_t bd, int32_t bkj) {
+    if (e != be) return e < be;
+    if (d != bd) return d < bd;
+    return kj < bkj;
 }
 
-template <int NSP>
-__global__ void __launch_bounds__(kB2Threads) b2search_kernel(const __grid_constant__ B2Params P) {
-    constexpr int RPT = kB2RPT, TPS = kB2TPS;
-    constexpr int FST = TPS * kTileD;  // float4 per stage
-    extern __shared__ __align__(128) unsigned char smem[];
-    float4 *Fs = reinterpret_cast<float4 *>(smem);             // [2][FST]
-    float *Us = reinterpret_cast<float *>(Fs + 2 * FST);        // [2][TPS][nsp][128]
-    B2Cold *cold = reinterpret_cast<B2Cold *>(Us + 2 * TPS * NSP * kTileD);  // [RPT][threads]
-    uint64_t *bar = reinterpret_cast<uint64_t *>(cold + RPT * kB2Threads);
-
-    const int n_r = (int)*P.d_nr;
-    const int n_tiles = (int)((P.d_misc[0] + kTileD - 1) / kTileD);
-    const double cmax = (double)P.d_misc[1];
-    int group, split, ns;
-    if (!cta_work(n_r, kB2Threads * RPT, n_tiles, 2 * TPS, P.ns_cap, group, split, ns)) return;
-    if (group == 0 && split == 0 && threadIdx.x == 0) *P.d_ns = (unsigned long long)ns;
-    const int t0 = (int)(((int64_t)split * n_tiles) / ns);
-    const int t1 = (int)(((int64_t)(split + 1) * n_tiles) / ns);
-    const int nstages = (max(0, t1 - t0) + TPS - 1) / TPS;
-    auto issue = [&](int s) {
-        const int buf = s & 1;
-        const int ta = t0 + s * TPS, tb = min(t1, ta + TPS);
-        const uint32_t b1 = (uint32_t)(tb - ta) * kTileD * 16;
-        const uint32_t b2 = (uint32_t)(tb - ta) * P.nsp * kTileD * 4;
-        b2_expect(&bar[buf], b1 + b2);
-        b2_bulk(Fs + buf * FST, P.F + (size_t)ta * kTileD, b1, &bar[buf]);
-        b2_bulk(Us + buf * TPS * NSP * kTileD, P.U + (size_t)ta * P.nsp * kTileD, b2, &bar[buf]);
-    };
-    if (threadIdx.x == 0) {
-        b2_bar_init(&bar[0]);
-        b2_bar_init(&bar[1]);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        if (nstages > 0) issue(0);
-        if (nstages > 1) issue(1);
-    }
-
-    float X2d[RPT], sx[RPT], dx[RPT], thr[RPT];  // 2 X2, xr2 + xi2, xr2 - xi2
-    const int rbase = (group * kB2Threads + threadIdx.x) * RPT;
-#pragma unroll
-    for (int q = 0; q < RPT; ++q) {
-        const int r = rbase + q;
-        B2Cold &cd = cold[q * kB2Threads + threadIdx.x];
-        int a = 0, b = 0, c = 0, d = 0;
-        if (r < n_r) {
-            const int2 rr = P.ranges[r];
-            const uint8_t *p0 = P.img + (size_t)rr.y * P.N + rr.x;
-            a = p0[0]; b = p0[1]; d = p0[P.N]; c = p0[P.N + 1];
-        }
-        X2d[q] = (float)(2 * (a - b + c - d));
-        sx[q] = (float)(2 * abs(a - c) + 2 * abs(b - d));
-        dx[q] = (float)(2 * abs(a - c) - 2 * abs(b - d));
-        const int sr = a + b + c + d, srr = a * a + b * b + c * c + d * d;
-        cd.A = (double)(4 * srr - sr * sr);
-        cd.SR = sr;
-        cd.px = a | (b << 8) | (c << 16) | (d << 24);
-        cd.margin = b2_margin(cd.A, P.smax, cmax);
-        if (P.has_zero) { cd.best_e = cd.A; cd.best_d = 0; cd.best_kj = P.j_zero; }
-        else { cd.best_e = INFINITY; cd.best_d = INT_MAX; cd.best_kj = INT_MAX; }
-        float th = P.has_zero ? fminf(__double2float_ru(cd.margin), FLT_MAX) : FLT_MAX;
-        thr[q] = r < n_r ? th : -FLT_MAX;
-    }
-    float nhs[NSP];
-#pragma unroll
-    for (int jj = 0; jj < NSP; ++jj) nhs[jj] = jj < P.nsp ? -__double2float_rn(0.25 * P.spos[jj]) : 0.f;  // x 2 Bq
-    unsigned n_exact = 0;
-
-    for (int s = 0; s < nstages; ++s) {
-        const int buf = s & 1;
-        b2_wait(&bar[buf], (uint32_t)((s >> 1) & 1));
-#pragma unroll
-        for (int q = 0; q < RPT; ++q)
-            if (rbase + q < n_r) thr[q] = fminf(thr[q], P.gthr[rbase + q]);
-        const float4 *Fb = Fs + buf * FST;
-        const float *Ub = Us + buf * TPS * NSP * kTileD;
-        const int ta = t0 + s * TPS;
-        const int nt = min(t1 - ta, TPS);
-        for (int tt = 0; tt < nt; ++tt) {
-            const float4 *Ft = Fb + tt * kTileD;
-            const float *Ut = Ub + tt * P.nsp * kTileD;
-            const int dbase = (ta + tt) * kTileD;
-#pragma unroll 2
-            for (int dl0 = 0; dl0 < kTileD; dl0 += 2) {
-                // two domains per block: the filters of 2 x RPT pairs interleave, one branch
-                float4 f2[2];
-                float t2v[2][NSP];
-                float mn[2];
-                float gq[2][RPT], bqq[2][RPT];
-#pragma unroll
-                for (int u2 = 0; u2 < 2; ++u2) {
-                    f2[u2] = Ft[dl0 + u2];
-#pragma unroll
-                    for (int jj = 0; jj < NSP; ++jj)
-                        t2v[u2][jj] = jj < P.nsp ? Ut[jj * kTileD + dl0 + u2] : INFINITY;
-                    mn[u2] = 1.0f;  // min over ranges of (lower bound - threshold): <= 0 -> some pass
-#pragma unroll
-                    for (int q = 0; q < RPT; ++q) {
-                        const float4 f = f2[u2];
-                        const float bq = fmaf(sx[q], f.y, fabsf(fmaf(X2d[q], f.x, dx[q] * f.z)));  // 2 max_k Bq_k
-                        float g = fmaf(nhs[0], bq, t2v[u2][0]);
-#pragma unroll
-                        for (int jj = 1; jj < NSP; ++jj) g = fminf(g, fmaf(nhs[jj], bq, t2v[u2][jj]));
-                        gq[u2][q] = g;
-                        bqq[u2][q] = bq;
-                        mn[u2] = fminf(mn[u2], g - thr[q]);
-                    }
-                }
-                if (fminf(mn[0], mn[1]) <= 0.0f) {
-#pragma unroll
-                    for (int u2 = 0; u2 < 2; ++u2) {
-#pragma unroll
-                        for (int q = 0; q < RPT; ++q) {
-                            if (gq[u2][q] <= thr[q]) {
-                                thr[q] = b2_exact(P, &cold[q * kB2Threads + threadIdx.x], thr[q], rbase + q,
-                                                  dbase + dl0 + u2, 0.5f * bqq[u2][q], f2[u2].w);
-                                ++n_exact;
-                            }
-                        }
-                    }
-                }
-                __syncwarp();  // reconverge after the (rare, divergent) exact path
-            }
-        }
-        __syncthreads();
-        if (threadIdx.x == 0 && s + 2 < nstages) {
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            issue(s + 2);
-        }
-    }
-#pragma unroll
-    for (int q = 0; q < RPT; ++q) {
-        const int r = rbase + q;
-        if (r < n_r) {
-            const B2Cold &cd = cold[q * kB2Threads + threadIdx.x];
-            Partial pb;
-            pb.e = cd.best_e;
-            pb.d = cd.best_d;
-            pb.kj = cd.best_kj;
-            P.part[(size_t)r * P.ns_cap + split] = pb;
-        }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) n_exact += __shfl_xor_sync(0xffffffffu, n_exact, o);
-    if ((threadIdx.x & 31) == 0 && n_exact && P.exact_count) atomicAdd(P.exact_count, (unsigned long long)n_exact);
-}
-
-// Threshold seeding: each range's exact best over a strided sample of kS domains is an upper
-// bound of its final best, so RU(best - A + margin) is a valid initial shared threshold.
-constexpr int kS = 32;
-__global__ void b2_seed_kernel(const __grid_constant__ B2Params P) {
-    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+// Pass 2: one warp per range (see above).
+__global__ void __launch_bounds__(256) b2exact_kernel(const __grid_constant__ B2Params P) {
+    const int lane = threadIdx.x & 31;
+    const int r = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    if (blockIdx.x == 0 && threadIdx.x == 0) *P.d_ns = 1ull;
     const int n_r = (int)*P.d_nr;
     if (r >= n_r) return;
     const int64_t n_k = (int64_t)P.d_misc[0];
-    if (n_k == 0) return;
+    const int n_tiles = (int)((n_k + kTileD - 1) / kTileD);
     const double cmax = (double)P.d_misc[1];
+    const int ns = (int)*P.d_nscan;
     const int2 rr = P.ranges[r];
     const uint8_t *p0 = P.img + (size_t)rr.y * P.N + rr.x;
-    const int a = p0[0], b = p0[1], d = p0[P.N], c = p0[P.N + 1];
-    const float X2d = (float)(2 * (a - b + c - d));
-    const float sx = (float)(2 * abs(a - c) + 2 * abs(b - d));
-    const float dx = (float)(2 * abs(a - c) - 2 * abs(b - d));
-    const int sr = a + b + c + d, srr = a * a + b * b + c * c + d * d;
-    const double A = (double)(4 * srr - sr * sr);
-    double best = P.has_zero ? A : INFINITY;
-    for (int i = 0; i < kS; ++i) {
-        const int64_t dd = (i * n_k) / kS;
-        const float4 f = P.F[dd];
-        const double Bq = 0.5 * (double)fmaf(sx, f.y, fabsf(fmaf(X2d, f.x, dx * f.z)));  // exact
-        const double c16 = __dmul_rn(0.0625, (double)f.w);
-        for (int jj = 0; jj < P.nsp; ++jj) {
-            const double s = P.spos[jj];
-            const double e = __dadd_rn(__dsub_rn(A, __dmul_rn(__dmul_rn(0.5, s), Bq)),
-                                       __dmul_rn(__dmul_rn(s, s), c16));
-            best = fmin(best, e);
+    const B2Range R = b2_range(p0[0], p0[1], p0[P.N + 1], p0[P.N]);
+    const double A = (double)R.A;
+    const double margin = b2_margin(A, P.smax, cmax);
+    float gmn = INFINITY;
+    for (int i = lane; i < ns; i += 32) gmn = fminf(gmn, P.gmin[(size_t)r * P.ns_cap + i]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) gmn = fminf(gmn, __shfl_xor_sync(0xffffffffu, gmn, o));
+    float thr = gmn < INFINITY ? fminf(__double2float_ru(__dadd_rn((double)gmn, 2.0 * margin)), FLT_MAX) : FLT_MAX;
+    double be;
+    int32_t bd, bkj;
+    if (P.has_zero) {  // s = 0: e = A for every (domain, k); first is (0, 0, j_zero)
+        be = A; bd = 0; bkj = P.j_zero;
+        thr = fminf(thr, fminf(__double2float_ru(margin), FLT_MAX));
+    } else {
+        be = INFINITY; bd = INT_MAX; bkj = INT_MAX;
+    }
+    unsigned n_exact = 0;
+    for (int sp = 0; sp < ns; ++sp) {
+        if (!(P.gmin[(size_t)r * P.ns_cap + sp] <= thr)) continue;  // warp-uniform
+        const int64_t d0 = ((int64_t)sp * n_tiles / ns) * kTileD;
+        const int64_t d1 = min(n_k, ((int64_t)(sp + 1) * n_tiles / ns) * kTileD);
+        for (int64_t d = d0 + lane; d < d1; d += 32) {
+            const float4 f = P.F[d];
+            const float bq = fmaf(R.sx, f.y, fabsf(fmaf(R.x2, f.x, R.dx * f.z)));
+            float g = INFINITY;
+            for (int jj = 0; jj < P.nsp; ++jj) g = fminf(g, fmaf(P.nhs[jj], bq, P.T[d * P.tw + jj]));
+            if (g <= thr) {
+                ++n_exact;
+                const double Bq = 0.5 * (double)bq, c16 = __dmul_rn(0.0625, (double)f.w);
+                double e0 = INFINITY;
+                int j0 = 0;
+                for (int jj = 0; jj < P.nsp; ++jj) {
+                    const double sv = P.spos[jj];
+                    const double e = __dadd_rn(__dsub_rn(A, __dmul_rn(__dmul_rn(0.5, sv), Bq)),
+                                               __dmul_rn(__dmul_rn(sv, sv), c16));
+                    if (e < e0) { e0 = e; j0 = jj; }  // lowest j among equal e (same k* for every s > 0)
+                }
+                int32_t kj = P.jpos[j0] | kPendIso;
+                if (e0 == be && (int32_t)d == bd)  // only the zero-s seed (d = 0, k = 0) ties here
+                    kj = (b2_kstar(P, rr, (int32_t)d) << 8) | P.jpos[j0];
+                if (b2_less(e0, (int32_t)d, kj, be, bd, bkj)) {
+                    be = e0; bd = (int32_t)d; bkj = kj;
+                    thr = fminf(thr, fminf(__double2float_ru(__dadd_rn(__dsub_rn(e0, A), margin)), FLT_MAX));
+                }
+            }
         }
     }
-    if (best < INFINITY)
-        P.gthr[r] = fminf(__double2float_ru(__dadd_rn(__dsub_rn(best, A), b2_margin(A, P.smax, cmax))), FLT_MAX);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double oe = __shfl_xor_sync(0xffffffffu, be, o);
+        const int32_t od = __shfl_xor_sync(0xffffffffu, bd, o);
+        const int32_t okj = __shfl_xor_sync(0xffffffffu, bkj, o);
+        if (b2_less(oe, od, okj, be, bd, bkj)) { be = oe; bd = od; bkj = okj; }
+        n_exact += __shfl_xor_sync(0xffffffffu, n_exact, o);
+    }
+    if (lane == 0) {
+        Partial pb;
+        pb.e = be;
+        pb.d = bd;
+        pb.kj = bkj;
+        P.part[(size_t)r * P.ns_cap] = pb;
+        if (n_exact && P.exact_count) atomicAdd(P.exact_count, (unsigned long long)n_exact);
+    }
 }
 
-template <int NSP>
-static cudaError_t launch_b2_t(const B2Params &p, cudaStream_t st) {
-    const size_t smem = (size_t)2 * kB2TPS * kTileD * 16 + (size_t)2 * kB2TPS * NSP * kTileD * 4 +
-                        sizeof(B2Cold) * kB2RPT * kB2Threads + 64;
+// t2_j per slot, [slot][tw]; +inf on pad slots and pad j
+__global__ void b2_t2_kernel(const int64_t *__restrict__ C, const unsigned long long *__restrict__ d_nk,
+                             int64_t n_slots, const SList spos, int32_t nsp, int32_t tw, float *__restrict__ T) {
+    const int64_t d = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (d >= n_slots) return;
+    const int64_t n_k = (int64_t)*d_nk;
+    if (d >= ((n_k + kTileD - 1) / kTileD) * kTileD) return;
+    const double c16 = __dmul_rn(0.0625, (double)C[d]);
+    for (int j = 0; j < tw; ++j) {
+        const double s = j < nsp ? spos.s[j] : 0.0;
+        T[d * tw + j] = (d < n_k && j < nsp) ? __double2float_rn(__dmul_rn(__dmul_rn(s, s), c16)) : INFINITY;
+    }
+}
+
+template <int NP>
+static size_t b2_smem() {
+    constexpr int TPS = NP == 1 ? 2 : 1;
+    return (size_t)kB2NB * TPS * kTileD * (16 + 8 * NP) + kB2NB * 12 + 64;
+}
+
+template <int NP>
+static cudaError_t launch_b2_scan(const B2Params &p, cudaStream_t st) {
+    const size_t smem = b2_smem<NP>();
     static bool attr = false;
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(b2search_kernel<NSP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem);
+        cudaError_t e = cudaFuncSetAttribute(b2scan_kernel<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         attr = true;
     }
     dim3 grid((unsigned)((p.n_r + kB2Threads * kB2RPT - 1) / (kB2Threads * kB2RPT)), (unsigned)p.nsplit);
-    b2search_kernel<NSP><<<grid, kB2Threads, smem, st>>>(p);
+    b2scan_kernel<NP><<<grid, kB2Threads, smem, st>>>(p);
     return cudaGetLastError();
 }
 
@@ -404,39 +434,50 @@ int b2_nsplit_hint(int64_t n_r, int64_t n_tiles, int num_sms) {
     if (gx <= 0 || n_tiles <= 0) return 1;
     static int waves = [] {
         const char *e = getenv("FIC_B2_CTAS_PER_SM");
-        return e ? atoi(e) : 8;
+        return e ? atoi(e) : 6;
     }();
     int64_t ns = ((int64_t)num_sms * waves + gx - 1) / gx;
-    const int64_t max_ns = (n_tiles + kB2TPS - 1) / kB2TPS;
+    const int64_t max_ns = (n_tiles + 1) / 2;
     if (ns > max_ns) ns = max_ns;
     if (ns < 1) ns = 1;
     if (ns > 65535) ns = 65535;
     return (int)ns;
 }
 
-cudaError_t launch_b2_search(const SearchParams &sp, const float4 *F, const float *U, const int32_t *kept,
-                             int32_t L, int32_t A, float *gthr, cudaStream_t st) {
+int b2_t2_width(int32_t nsp) { return nsp <= 2 ? 2 : 16; }
+
+size_t b2_scratch_bytes(int64_t n_r, int32_t ns_cap) { return 64 + sizeof(float) * (size_t)n_r * ns_cap; }
+
+cudaError_t launch_b2_search(const SearchParams &sp, const float4 *F, float *T, const int32_t *kept,
+                             int32_t L, int32_t A, void *scratch, cudaStream_t st) {
     if (sp.n_r == 0 || sp.nsp == 0) return cudaSuccess;
+    const int tw = b2_t2_width(sp.nsp);
+    const int64_t slots = sp.slot_stride;
+    SList sl;
+    memcpy(sl.s, sp.spos, sizeof sl.s);
+    if (slots > 0) {
+        b2_t2_kernel<<<(unsigned)((slots + 255) / 256), 256, 0, st>>>(sp.C, &sp.d_misc[0], slots, sl, sp.nsp, tw, T);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
     B2Params p;
     memset(&p, 0, sizeof p);
     p.img = sp.img; p.N = sp.N; p.L = L; p.A = A; p.ranges = sp.ranges; p.n_r = sp.n_r;
-    p.F = F; p.U = U; p.C = sp.C; p.kept = kept;
+    p.F = F; p.T = T; p.tw = tw; p.kept = kept;
     p.d_nr = sp.d_nr; p.d_misc = sp.d_misc; p.nsplit = sp.nsplit; p.d_ns = sp.d_ns; p.ns_cap = sp.ns_cap;
     p.nsp = sp.nsp;
     memcpy(p.spos, sp.spos, sizeof p.spos);
     memcpy(p.jpos, sp.jpos, sizeof p.jpos);
+    for (int j = 0; j < kMaxS; ++j) p.nhs[j] = j < sp.nsp ? -(float)(0.25 * sp.spos[j]) : 0.f;
     p.has_zero = sp.has_zero; p.j_zero = sp.j_zero;
     p.smax = sp.smax;
     p.part = sp.part; p.exact_count = sp.exact_count;
-    p.gthr = gthr;
-    cudaError_t e = cudaMemsetAsync(gthr, 0x7f, sizeof(float) * (size_t)sp.n_r, st);  // ~3.4e38
+    p.d_nscan = reinterpret_cast<unsigned long long *>(scratch);
+    p.gmin = reinterpret_cast<float *>(static_cast<char *>(scratch) + 64);
+    cudaError_t e = tw == 2 ? launch_b2_scan<1>(p, st) : launch_b2_scan<8>(p, st);
     if (e != cudaSuccess) return e;
-    b2_seed_kernel<<<(unsigned)((sp.n_r + 127) / 128), 128, 0, st>>>(p);
-    e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
-    if (sp.nsp <= 1) return launch_b2_t<1>(p, st);
-    if (sp.nsp <= 2) return launch_b2_t<2>(p, st);
-    return launch_b2_t<16>(p, st);
+    b2exact_kernel<<<(unsigned)((sp.n_r + 7) / 8), 256, 0, st>>>(p);
+    return cudaGetLastError();
 }
 
 }  // namespace fic

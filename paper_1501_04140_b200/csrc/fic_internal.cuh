@@ -19,6 +19,9 @@ namespace fic {
 constexpr int kTileD = 128;  // domains per pool tile
 constexpr int kMaxS = 16;    // s values per level
 constexpr int kMaxLevels = 8;
+// Partial.kj flag: s index final, isometry k* not yet evaluated (finalize computes it for the
+// winning domain; the B = 2 search defers it because the same domain never competes twice)
+constexpr int32_t kPendIso = 1 << 16;
 
 struct Buf {
     void *p = nullptr;
@@ -165,8 +168,10 @@ int search_nsplit_hint(int32_t B, int64_t n_r, int64_t n_tiles, int num_sms);
 cudaError_t launch_b2_pool(const uint8_t *img, int32_t N, int32_t L, int32_t A, const int32_t *kept,
                            const unsigned long long *d_nk, int64_t n_slots, float4 *F, cudaStream_t st);
 int b2_nsplit_hint(int64_t n_r, int64_t n_tiles, int num_sms);
-cudaError_t launch_b2_search(const SearchParams &sp, const float4 *F, const float *U, const int32_t *kept,
-                             int32_t L, int32_t A, float *gthr, cudaStream_t st);
+int b2_t2_width(int32_t nsp);  // floats per slot of the B = 2 t2 table
+size_t b2_scratch_bytes(int64_t n_r, int32_t ns_cap);  // pass-1 minima + split count
+cudaError_t launch_b2_search(const SearchParams &sp, const float4 *F, float *T, const int32_t *kept,
+                             int32_t L, int32_t A, void *scratch, cudaStream_t st);
 cudaError_t launch_fourier_u(const int64_t *C, const unsigned long long *d_nk, int64_t n_slots, const SList &sl,
                              int32_t nsp, float *U, cudaStream_t st);
 

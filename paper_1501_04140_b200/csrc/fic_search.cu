@@ -425,6 +425,41 @@ __device__ __forceinline__ int o_code_dev(double o) {
     return 127 - min(j, 127);
 }
 
+// k* of the winning (range, domain) when the search deferred it: all 8 SRD_k in integers with
+// the isometry convention of the oracle (reading R2: T_k(D)(i,j) = D(f_k(i,j)), b = B - 1),
+// lowest index of the maximum.
+__device__ __noinline__ int kstar_dev(const FinalizeParams &P, int2 rr, int32_t d) {
+    const int B = P.B, b = B - 1;
+    const int32_t c = P.kept[d];
+    const int64_t x0 = (int64_t)(c % P.A) * P.L, y0 = (int64_t)(c / P.A) * P.L;
+    auto Dp = [&](int i, int j) {  // decimated domain value D'(i, j)
+        const uint8_t *q = P.img + (y0 + 2 * i) * P.N + x0 + 2 * j;
+        return (int)q[0] + (int)q[1] + (int)q[P.N] + (int)q[P.N + 1];
+    };
+    long long best = LLONG_MIN;
+    int ks = 0;
+    for (int k = 0; k < 8; ++k) {
+        long long s = 0;
+        for (int i = 0; i < B; ++i)
+            for (int j = 0; j < B; ++j) {
+                int si = i, sj = j;
+                switch (k) {
+                case 1: si = b - j; sj = i; break;
+                case 2: si = b - i; sj = b - j; break;
+                case 3: si = j; sj = b - i; break;
+                case 4: si = i; sj = b - j; break;
+                case 5: si = j; sj = i; break;
+                case 6: si = b - i; sj = j; break;
+                case 7: si = b - j; sj = b - i; break;
+                default: break;
+                }
+                s += (long long)P.img[(size_t)(rr.y + i) * P.N + rr.x + j] * Dp(si, sj);
+            }
+        if (s > best) { best = s; ks = k; }
+    }
+    return ks;
+}
+
 __global__ void finalize_kernel(const __grid_constant__ FinalizeParams P) {
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= (int)*P.d_nr) return;
@@ -458,6 +493,7 @@ __global__ void finalize_kernel(const __grid_constant__ FinalizeParams P) {
         const Partial c = P.part[(size_t)r * P.nsplit + sp];
         if (lex_less(c.e, c.d, c.kj, best)) { best.e = c.e; best.d = c.d; best.kj = c.kj; }
     }
+    if (best.kj & kPendIso) best.kj = (kstar_dev(P, rr, best.d) << 8) | (best.kj & 255);
     const int d = best.d, k = best.kj >> 8, j = best.kj & 255;
     const double E = __ddiv_rn(best.e, (double)n);
     const double s = P.s[j];
