@@ -328,7 +328,7 @@ def main():
                                   "P_fp64 = 148x64xf_max (DESIGN.md 7)"},
         "levels": [{"B": s["B"], "n_candidates": s["n_candidates"], "n_kept": s["n_kept"],
                     "n_ranges": s["n_ranges"], "pairs": s["pairs"],
-                    "exact_evals": s["exact_evals"],
+                    "exact_evals": s["exact_evals"], "pairs_scanned": s["pairs_scanned"],
                     "ms_pool": s["ms_pool"] / args.steps, "ms_search": s["ms_search"] / args.steps,
                     "ms_finalize": s["ms_finalize"] / args.steps} for s in level_acc],
         "gpu_launches": int(launches),

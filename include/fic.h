@@ -71,6 +71,9 @@ typedef struct {
     int64_t exact_evals;    /* (range, domain) pairs that took the exact binary64 path       */
     float ms_pool, ms_search, ms_finalize;
     int64_t kernel_launches; /* libfic kernels launched for this level (pool + search + quadtree) */
+    int64_t pairs_scanned;  /* (range, domain) pairs the search evaluated (fp32 filter); the rest of
+                               n_ranges * n_kept were proven unable to win or tie (B = 2
+                               Cauchy-Schwarz C windows) -- n_ranges * n_kept elsewhere */
 } fic_level_stats;
 
 fic_status fic_ctx_set_timing(fic_ctx *ctx, int32_t enable);

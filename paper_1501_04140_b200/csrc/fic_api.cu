@@ -39,6 +39,7 @@ struct fic_ctx {
     int overlap_pools = 0;                       // env FIC_OVERLAP_POOLS=1
     cudaEvent_t pool_ready[fic::kMaxLevels] = {};
     cudaEvent_t main_ready = nullptr;
+    int b2_window = 1;    // env FIC_B2_WINDOW=0: B = 2 full scan instead of the C windows
     int search_mode = 0;  // env FIC_SEARCH: auto (default: B=2 closed form, else tcgen05) | fourier | direct | tc
     Buf b_rc, b_meta, b_u, b_gthr, b_rop;  // libfic kernels enqueued (for fic_level_stats.kernel_launches)  // pool start, search start, search end, finalize end, pool end
 };
@@ -143,7 +144,7 @@ fic_status pool_enqueue(fic_ctx *ctx, Pool &P, const uint8_t *img, int32_t N, in
     if (P.mode == 2) CK(grow(ctx, P.b_Dt, sizeof(float) * slots * P.n));
     if (P.mode == 1) CK(grow(ctx, P.b_Dc, sizeof(float) * slots * fic::fourier_record_stride(B)));
     if (P.mode == 0) CK(grow(ctx, P.b_Dtc, fic::tc_pool_bytes(B, tiles_max)));
-    if (P.mode == 3) CK(grow(ctx, P.b_F2, sizeof(float4) * slots));
+    if (P.mode == 3) CK(grow(ctx, P.b_F2, fic::b2_pool_bytes(slots)));
     CK(grow(ctx, P.b_SDf, sizeof(float) * slots));
     CK(grow(ctx, P.b_SD, sizeof(int32_t) * slots));
     CK(grow(ctx, P.b_C, sizeof(int64_t) * slots));
@@ -155,7 +156,6 @@ fic_status pool_enqueue(fic_ctx *ctx, Pool &P, const uint8_t *img, int32_t N, in
     P.Dt = P.mode == 2 ? ptr<float>(P.b_Dt) : nullptr;
     P.Dc = P.mode == 1 ? ptr<float>(P.b_Dc) : nullptr;
     P.Dtc = P.mode == 0 ? ptr<uint8_t>(P.b_Dtc) : nullptr;
-    P.F2 = P.mode == 3 ? ptr<float4>(P.b_F2) : nullptr;
     P.SD = ptr<int32_t>(P.b_SD); P.C = ptr<int64_t>(P.b_C);
     P.d_misc = ptr<unsigned long long>(P.b_misc);
     CK(cudaMemsetAsync(P.d_misc, 0, 4 * sizeof(unsigned long long), st));
@@ -170,13 +170,13 @@ fic_status pool_enqueue(fic_ctx *ctx, Pool &P, const uint8_t *img, int32_t N, in
     else if (P.mode == 0)
         CK(fic::launch_pool_tc(img, N, B, L, P.A, P.kept, &P.d_misc[0], tiles_max, P.Dtc, st));
     else if (P.mode == 3)
-        CK(fic::launch_b2_pool(img, N, L, P.A, P.kept, &P.d_misc[0], slots, P.F2, st));
+        CK(fic::launch_b2_pool(img, N, L, P.A, P.kept, &P.d_misc[0], slots, P.b_F2.p, &P.b2, st));
     else
         CK(fic::launch_pool_coeff(img, N, B, L, P.A, P.kept, &P.d_misc[0], slots, P.Dc,
                                   reinterpret_cast<unsigned int *>(&P.d_misc[2]), st));
     CK(fic::launch_pool_moments(img, N, B, L, P.A, P.kept, &P.d_misc[0], slots, P.SD, P.SDf, P.C,
                                 &P.d_misc[1], st));
-    ctx->launches += 6;  // entropy, select x3, gather, moments
+    ctx->launches += 6 + (P.mode == 3 ? 1 : 0);  // entropy, select x3, gather, moments (+ sorted gather)
     return FIC_OK;
 }
 
@@ -259,6 +259,7 @@ fic_status level_enqueue(fic_ctx *ctx, const Pool &P, const uint8_t *img, const 
     sp.tiles_per_split = (int32_t)((tiles + sp.nsplit - 1) / sp.nsplit);
     // dynamic kernels (tcgen05, B=2) choose their split count on the device, up to ns_cap
     const bool dyn = (P.mode == 0 || P.mode == 3);
+    sp.b2_window = ctx->b2_window;
     sp.ns_cap = dyn ? (int32_t)std::min<int64_t>(4 * (int64_t)sp.nsplit, std::max<int64_t>(1, tiles)) : sp.nsplit;
     sp.d_ns = ptr<unsigned long long>(ctx->b_counts) + 56 + level_slot;
     if (!dyn) CK(fic::launch_set_u64(sp.d_ns, (unsigned long long)sp.nsplit, st));
@@ -286,7 +287,8 @@ fic_status level_enqueue(fic_ctx *ctx, const Pool &P, const uint8_t *img, const 
         CK(grow(ctx, ctx->b_u, sizeof(float) * (size_t)slots * fic::b2_t2_width(sp.nsp)));
         if (ctx->timing) CK(cudaEventRecord(ctx->ev[level_slot][1], st));
         CK(grow(ctx, ctx->b_gthr, fic::b2_scratch_bytes(n_r_max, sp.ns_cap)));
-        CK(fic::launch_b2_search(sp, P.F2, ptr<float>(ctx->b_u), P.kept, P.L, P.A, ctx->b_gthr.p, st));
+        CK(fic::launch_b2_search(sp, P.b2, ptr<float>(ctx->b_u), P.kept, P.L, P.A, ctx->b_gthr.p,
+                                 ptr<unsigned long long>(ctx->b_counts) + 40 + level_slot, st));
         ctx->launches += sp.nsp > 0 && n_r_max > 0 ? 3 : 0;  // t2 table, pass 1 scan, pass 2 exact
     } else {
         const int nc = fic::fourier_record_stride(P.B);  // >= 8 nO + 1
@@ -368,6 +370,8 @@ fic_status fic_ctx_create(int32_t device, void *cuda_stream, fic_ctx **out) {
     {
         const char *env = getenv("FIC_SEARCH");
         ctx->search_mode = 0;
+        const char *bw = getenv("FIC_B2_WINDOW");
+        ctx->b2_window = bw && strcmp(bw, "0") == 0 ? 0 : 1;
         if (env && strcmp(env, "fourier") == 0) ctx->search_mode = 1;
         if (env && strcmp(env, "direct") == 0) ctx->search_mode = 2;
         if (env && strcmp(env, "tc") == 0) ctx->search_mode = 4;
@@ -508,6 +512,7 @@ fic_status fic_encode_level(fic_ctx *ctx, const uint8_t *img, int32_t N, const f
                       reinterpret_cast<int32_t *>(d_counts + 30)));
     ls.B = pool->P.B; ls.n_candidates = pool->P.n_c; ls.n_kept = pool->P.n_k; ls.n_ranges = n_r;
     ls.pairs = n_r * pool->P.n_k * 8;
+    ls.pairs_scanned = n_r * pool->P.n_k;  // not read back here (stream-asynchronous call)
     ctx->stats.push_back(ls);
     return FIC_OK;
 }
@@ -632,6 +637,8 @@ fic_status fic_encode(fic_ctx *ctx, const uint8_t *img, int32_t N, int32_t B_max
         ls.n_kept = (int64_t)ctx->h_counts[48 + l];
         ctx->levels[l].n_k = ls.n_kept;
         ls.pairs = ls.n_ranges * ls.n_kept * 8;
+        const int64_t sc = (int64_t)ctx->h_counts[40 + l];
+        ls.pairs_scanned = sc > 0 ? sc : ls.n_ranges * ls.n_kept;
     }
     if (ctx->timing) {
         for (int l = 0; l < nl; ++l) {

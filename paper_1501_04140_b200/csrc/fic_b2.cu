@@ -20,6 +20,8 @@
 #include <cstdlib>
 #include <cstring>
 
+#include <cub/device/device_radix_sort.cuh>
+
 #include "fic_internal.cuh"
 
 namespace fic {
@@ -50,16 +52,21 @@ __device__ __forceinline__ void b2_wait(uint64_t *bar, uint32_t parity) {
     }
 }
 
-// Domain features: float4 (Y2, yr + yi, yr - yi, C) per slot; zero on pads (t2 = +inf excludes them).
+// Domain features: float4 (Y2, yr + yi, yr - yi, C) per slot; zero on pads (t2 = +inf excludes
+// them).  The pool is stored sorted by C (stable: ties keep the kept-domain rank order), with
+// ds[pos] = kept-domain rank and Cs[pos] = C, so the search can bound a range's admissible
+// domains to C windows (Cauchy-Schwarz, see b2win_kernel).
 __global__ void b2_pool_kernel(const uint8_t *__restrict__ img, int32_t N, int32_t L, int32_t A,
                                const int32_t *__restrict__ kept, const unsigned long long *__restrict__ d_nk,
-                               int64_t n_slots, float4 *__restrict__ F) {
+                               int64_t n_slots, float4 *__restrict__ F, uint32_t *__restrict__ key,
+                               int32_t *__restrict__ val) {
     const int64_t d = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (d >= n_slots) return;
     const int64_t n_k = (int64_t)*d_nk;
-    if (d >= ((n_k + kTileD - 1) / kTileD) * kTileD) return;
+    val[d] = (int32_t)d;
     if (d >= n_k) {
         F[d] = make_float4(0.f, 0.f, 0.f, 0.f);
+        key[d] = 0xffffffu;  // pads sort last (C < 2^23)
         return;
     }
     const int32_t c = kept[d];
@@ -70,15 +77,62 @@ __global__ void b2_pool_kernel(const uint8_t *__restrict__ img, int32_t N, int32
     };
     const int w = dp(0, 0), x = dp(0, 1), y = dp(1, 1), z = dp(1, 0);
     const int sd = w + x + y + z;
-    const int cc = 4 * (w * w + x * x + y * y + z * z) - sd * sd;  // C = n SDD - SD^2 < 2^24
+    const int cc = 4 * (w * w + x * x + y * y + z * z) - sd * sd;  // C = n SDD - SD^2 < 2^23
     const int yr = abs(w - y), yi = abs(x - z);
     F[d] = make_float4((float)(w - x + y - z), (float)(yr + yi), (float)(yr - yi), (float)cc);
+    key[d] = (uint32_t)cc;
 }
 
+__global__ void b2_gather_kernel(const float4 *__restrict__ Fu, const int32_t *__restrict__ ds, int64_t n_slots,
+                                 float4 *__restrict__ F) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n_slots) F[i] = Fu[ds[i]];
+}
+
+struct B2PoolLayout {
+    size_t F, Fu, Cs, key, ds, val, tmp, tmp_bytes, total;
+};
+static B2PoolLayout b2_layout(int64_t slots) {
+    B2PoolLayout L;
+    auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+    size_t o = 0;
+    L.F = o; o += al(sizeof(float4) * slots);
+    L.Fu = o; o += al(sizeof(float4) * slots);
+    L.Cs = o; o += al(sizeof(uint32_t) * slots);
+    L.key = o; o += al(sizeof(uint32_t) * slots);
+    L.ds = o; o += al(sizeof(int32_t) * slots);
+    L.val = o; o += al(sizeof(int32_t) * slots);
+    L.tmp_bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, L.tmp_bytes, (const uint32_t *)nullptr, (uint32_t *)nullptr,
+                                    (const int32_t *)nullptr, (int32_t *)nullptr, (int)slots, 0, 24);
+    L.tmp = o; o += al(L.tmp_bytes);
+    L.total = o;
+    return L;
+}
+
+size_t b2_pool_bytes(int64_t n_slots) { return b2_layout(n_slots).total; }
+
 cudaError_t launch_b2_pool(const uint8_t *img, int32_t N, int32_t L, int32_t A, const int32_t *kept,
-                           const unsigned long long *d_nk, int64_t n_slots, float4 *F, cudaStream_t st) {
+                           const unsigned long long *d_nk, int64_t n_slots, void *store, B2Pool *out,
+                           cudaStream_t st) {
+    const B2PoolLayout Ly = b2_layout(n_slots);
+    char *base = static_cast<char *>(store);
+    out->F = reinterpret_cast<float4 *>(base + Ly.F);
+    out->Cs = reinterpret_cast<int32_t *>(base + Ly.Cs);
+    out->ds = reinterpret_cast<int32_t *>(base + Ly.ds);
     if (n_slots == 0) return cudaSuccess;
-    b2_pool_kernel<<<(unsigned)((n_slots + 255) / 256), 256, 0, st>>>(img, N, L, A, kept, d_nk, n_slots, F);
+    float4 *Fu = reinterpret_cast<float4 *>(base + Ly.Fu);
+    uint32_t *key = reinterpret_cast<uint32_t *>(base + Ly.key);
+    int32_t *val = reinterpret_cast<int32_t *>(base + Ly.val);
+    const unsigned g = (unsigned)((n_slots + 255) / 256);
+    b2_pool_kernel<<<g, 256, 0, st>>>(img, N, L, A, kept, d_nk, n_slots, Fu, key, val);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    size_t tb = Ly.tmp_bytes;
+    e = cub::DeviceRadixSort::SortPairs(base + Ly.tmp, tb, key, reinterpret_cast<uint32_t *>(out->Cs), val, out->ds,
+                                        (int)n_slots, 0, 24, st);
+    if (e != cudaSuccess) return e;
+    b2_gather_kernel<<<g, 256, 0, st>>>(Fu, out->ds, n_slots, out->F);
     return cudaGetLastError();
 }
 
@@ -106,8 +160,10 @@ struct B2Params {
     int32_t N, L, A;
     const int2 *ranges;
     int32_t n_r;
-    const float4 *F;       // [n_slots] (Y2, yr + yi, yr - yi, C)
-    const float *T;        // [n_slots][tw] t2_j = RN((s_j s_j)(C/16)), +inf on pads
+    const float4 *F;       // [n_slots] (Y2, yr + yi, yr - yi, C), sorted by C
+    const float *T;        // [n_slots][tw] t2_j = RN((s_j s_j)(C/16)), +inf on pads (sorted order)
+    const int32_t *Cs;     // [n_slots] C (sorted)
+    const int32_t *ds;     // [n_slots] kept-domain rank of each sorted position
     int32_t tw;
     const int32_t *kept;
     const unsigned long long *d_nr, *d_misc;  // device sizes: n_r; n_kept, Cmax
@@ -123,6 +179,7 @@ struct B2Params {
     float *gmin;                    // [n_r][ns_cap] pass-1 minimum of g per (range, split)
     unsigned long long *d_nscan;    // splits pass 1 used
     unsigned long long *d_ns;       // splits of the partials finalize merges (= 1 here)
+    unsigned long long *scan_count; // (range, domain) pairs evaluated by the fp32 filter
     int32_t ns_cap;
 };
 
@@ -351,13 +408,14 @@ __global__ void __launch_bounds__(256) b2exact_kernel(const __grid_constant__ B2
         if (!(P.gmin[(size_t)r * P.ns_cap + sp] <= thr)) continue;  // warp-uniform
         const int64_t d0 = ((int64_t)sp * n_tiles / ns) * kTileD;
         const int64_t d1 = min(n_k, ((int64_t)(sp + 1) * n_tiles / ns) * kTileD);
-        for (int64_t d = d0 + lane; d < d1; d += 32) {
-            const float4 f = P.F[d];
+        for (int64_t pos = d0 + lane; pos < d1; pos += 32) {
+            const float4 f = P.F[pos];
             const float bq = fmaf(R.sx, f.y, fabsf(fmaf(R.x2, f.x, R.dx * f.z)));
             float g = INFINITY;
-            for (int jj = 0; jj < P.nsp; ++jj) g = fminf(g, fmaf(P.nhs[jj], bq, P.T[d * P.tw + jj]));
+            for (int jj = 0; jj < P.nsp; ++jj) g = fminf(g, fmaf(P.nhs[jj], bq, P.T[pos * P.tw + jj]));
             if (g <= thr) {
                 ++n_exact;
+                const int32_t d = P.ds[pos];
                 const double Bq = 0.5 * (double)bq, c16 = __dmul_rn(0.0625, (double)f.w);
                 double e0 = INFINITY;
                 int j0 = 0;
@@ -368,10 +426,10 @@ __global__ void __launch_bounds__(256) b2exact_kernel(const __grid_constant__ B2
                     if (e < e0) { e0 = e; j0 = jj; }  // lowest j among equal e (same k* for every s > 0)
                 }
                 int32_t kj = P.jpos[j0] | kPendIso;
-                if (e0 == be && (int32_t)d == bd)  // only the zero-s seed (d = 0, k = 0) ties here
-                    kj = (b2_kstar(P, rr, (int32_t)d) << 8) | P.jpos[j0];
-                if (b2_less(e0, (int32_t)d, kj, be, bd, bkj)) {
-                    be = e0; bd = (int32_t)d; bkj = kj;
+                if (e0 == be && d == bd)  // only the zero-s seed (d = 0, k = 0) ties here
+                    kj = (b2_kstar(P, rr, d) << 8) | P.jpos[j0];
+                if (b2_less(e0, d, kj, be, bd, bkj)) {
+                    be = e0; bd = d; bkj = kj;
                     thr = fminf(thr, fminf(__double2float_ru(__dadd_rn(__dsub_rn(e0, A), margin)), FLT_MAX));
                 }
             }
@@ -395,14 +453,198 @@ __global__ void __launch_bounds__(256) b2exact_kernel(const __grid_constant__ B2
     }
 }
 
+// float <-> int key with the same order (a signed-int min is a float min)
+__device__ __forceinline__ int b2_fkey(float f) {
+    const int i = __float_as_int(f);
+    return i >= 0 ? i : i ^ 0x7fffffff;
+}
+__device__ __forceinline__ float b2_fdec(int k) { return __int_as_float(k >= 0 ? k : k ^ 0x7fffffff); }
+
+// ---------------------------------------------------------------------------------------------
+// Windowed search (predefined s: no s = 0, at most 2 values), one warp per range.
+//
+// Cauchy-Schwarz on the centred vectors gives |Bq_k| <= sqrt(A C) for every isometry, so for
+// every domain and every s
+//     e_s = A - (s/2) Bq + (s^2/16) C  >=  lb_s(C) = (sqrt(A) - s sqrt(C)/4)^2 ,
+// and a domain can only win or tie if lb_s(C) <= best for some s in the level's set.  lb_s is
+// minimal (0) at the centre C*_s = 16 A / s^2 and grows monotonically away from it, and the
+// pool is sorted by C, so the warp expands outward from the centres, best-first: each step
+// takes the 32 domains next to the frontier with the smallest lb, scores them (fp32 filter,
+// canonical binary64 path for every pair with g <= thr, as in pass 2), and a frontier stops
+// once its lb exceeds the current best.  With s_a > s_b (centres c_a <= c_b) four frontiers
+// cover the windows: below c_a (lb_a is the smaller bound there), c_a upward and c_b downward
+// (they stop where they meet), above c_b (lb_b smaller).  Rounding: a frontier stops only if
+// |sqrt(A) - s sqrt(C)/4| > sqrt(ub)(1 + 1e-6) + 1e-3, which covers the binary64 error of the
+// canonical score (< 4.4e-16 (2 sqrt(A) + delta)^2 for A < 2^21).  Unvisited domains are
+// provably worse than the best, so the result equals the exhaustive loop.
+__device__ __forceinline__ int b2_lower_bound(const int32_t *__restrict__ Cs, int n, double v, int lane) {
+    int lo = 0, hi = n;  // invariant: Cs[< lo] < v <= Cs[>= hi]
+    while (hi - lo > 32) {
+        const int64_t span = hi - lo;
+        const int p = lo + (int)((span * (lane + 1)) / 33);
+        const unsigned m = __ballot_sync(0xffffffffu, (double)__ldg(Cs + p) >= v);
+        const int f = m ? __ffs(m) - 1 : 32;
+        const int phi = __shfl_sync(0xffffffffu, p, f < 32 ? f : 31);
+        const int plo = __shfl_sync(0xffffffffu, p, f > 0 ? f - 1 : 0);
+        if (f < 32) hi = phi;
+        if (f > 0) lo = plo + 1;
+    }
+    const int p = lo + lane;
+    const unsigned m = __ballot_sync(0xffffffffu, p < hi ? (double)__ldg(Cs + p) >= v : true);
+    return lo + (__ffs(m) - 1);
+}
+
+// canonical binary64 score of one (range, domain): min over s > 0 with the lowest j (Eq. 1/3, C7)
+__device__ __forceinline__ double b2_canon(const B2Params &P, double A, float bq, float cf, int &j0) {
+    const double Bq = 0.5 * (double)bq, c16 = __dmul_rn(0.0625, (double)cf);
+    double e0 = INFINITY;
+    j0 = 0;
+    for (int jj = 0; jj < P.nsp; ++jj) {
+        const double sv = P.spos[jj];
+        const double e = __dadd_rn(__dsub_rn(A, __dmul_rn(__dmul_rn(0.5, sv), Bq)), __dmul_rn(__dmul_rn(sv, sv), c16));
+        if (e < e0) { e0 = e; j0 = jj; }  // lowest j among equal e (same k* for every s > 0)
+    }
+    return e0;
+}
+
+constexpr int kWinStep = 64;  // domains per frontier per round
+
+__global__ void __launch_bounds__(256) b2win_kernel(const __grid_constant__ B2Params P) {
+    const int lane = threadIdx.x & 31;
+    const int r = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    if (blockIdx.x == 0 && threadIdx.x == 0) *P.d_ns = 1ull;
+    const int n_r = (int)*P.d_nr;
+    if (r >= n_r) return;
+    const int n_k = (int)P.d_misc[0];
+    const double cmax = (double)P.d_misc[1];
+    const int2 rr = P.ranges[r];
+    const uint8_t *p0 = P.img + (size_t)rr.y * P.N + rr.x;
+    const B2Range R = b2_range(p0[0], p0[1], p0[P.N + 1], p0[P.N]);
+    const double A = (double)R.A;
+    const double margin = b2_margin(A, P.smax, cmax);
+    const float nh0 = P.nhs[0], nh1 = P.nsp > 1 ? P.nhs[1] : 0.f;
+    const float2 *T2 = reinterpret_cast<const float2 *>(P.T);  // tw == 2 (pad j: +inf)
+    auto gval = [&](int pos, float &bq, float &cf) {
+        const float4 fv = __ldg(P.F + pos);
+        const float2 t2 = __ldg(T2 + pos);
+        bq = fmaf(R.sx, fv.y, fabsf(fmaf(R.x2, fv.x, R.dx * fv.z)));
+        cf = fv.w;
+        return fminf(fmaf(nh0, bq, t2.x), fmaf(nh1, bq, t2.y));
+    };
+    // s_a >= s_b, centres c_a <= c_b
+    const int ia = (P.nsp > 1 && P.spos[1] > P.spos[0]) ? 1 : 0, ib = P.nsp > 1 ? 1 - ia : ia;
+    const double sa = P.spos[ia], sb = P.spos[ib];
+    const int ca = n_k > 0 ? b2_lower_bound(P.Cs, n_k, 16.0 * A / (sa * sa), lane) : 0;
+    const int cb = n_k > 0 ? max(ca, b2_lower_bound(P.Cs, n_k, 16.0 * A / (sb * sb), lane)) : 0;
+    // window bounds in C (fp32, widened by 1e-4 relative and 1e-3 (1 + sqrt A) absolute in
+    // sqrt C -- far above the fp32 rounding of these few operations, so never too narrow)
+    const float sqAf = sqrtf((float)R.A);
+    const float ka = (float)(4.0 / sa), kb = (float)(4.0 / sb);
+    // frontiers: f0 [q0, c_a) grows down (s_a), f1 [c_a, q1) grows up (s_a), f2 [q2, c_b) grows
+    // down (s_b), f3 [c_b, q3) grows up (s_b); f1 and f2 share [c_a, c_b) and stop when they meet
+    int q0 = ca, q1 = ca, q2 = cb, q3 = cb;
+    bool al0 = q0 > 0, al1 = q1 < q2, al2 = q1 < q2, al3 = q3 < n_k;
+    float gmin = INFINITY;
+    unsigned long long scanned = 0;
+    // phase 1: rounds over the four frontiers with the fp32 filter; the bound ub = A + gmin +
+    // margin (>= best) narrows the windows after every round
+    while (al0 || al1 || al2 || al3) {
+        const int n0 = al0 ? min(kWinStep, q0) : 0;
+        const int gap = q2 - q1;
+        const int n1 = al1 ? min(kWinStep, gap) : 0;
+        const int n2 = al2 ? min(kWinStep, gap - n1) : 0;
+        const int n3 = al3 ? min(kWinStep, n_k - q3) : 0;
+        const int b0 = q0 - n0, b1 = q1, b2 = q2 - n2, b3 = q3;
+        q0 -= n0; q1 += n1; q2 -= n2; q3 += n3;
+        scanned += (unsigned long long)(n0 + n1 + n2 + n3);
+        // next frontier C values (lanes 0..3), in flight with this round's features
+        int cn = 0;
+        if (lane == 0 && q0 > 0) cn = __ldg(P.Cs + q0 - 1);
+        if (lane == 1 && q1 < q2) cn = __ldg(P.Cs + q1);
+        if (lane == 2 && q1 < q2) cn = __ldg(P.Cs + q2 - 1);
+        if (lane == 3 && q3 < n_k) cn = __ldg(P.Cs + q3);
+        float g = INFINITY, bq, cf;
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const int o = lane + 32 * k;
+            if (o < n0) g = fminf(g, gval(b0 + o, bq, cf));
+            if (o < n1) g = fminf(g, gval(b1 + o, bq, cf));
+            if (o < n2) g = fminf(g, gval(b2 + o, bq, cf));
+            if (o < n3) g = fminf(g, gval(b3 + o, bq, cf));
+        }
+        gmin = fminf(gmin, b2_fdec(__reduce_min_sync(0xffffffffu, b2_fkey(g))));
+        const float ub = gmin < INFINITY ? __double2float_ru(__dadd_ru(__dadd_ru(A, (double)gmin), margin)) : INFINITY;
+        const float u = sqrtf(fmaxf(ub, 0.f)) * 1.0001f + 1e-3f * (1.f + sqAf);
+        const float la = ka * (sqAf - u), lb = kb * (sqAf - u);
+        const float cl = (lane == 0 ? la : lb);
+        const float clo = cl > 0.f ? cl * cl * 0.9999f : -1.f;
+        const float ch = (lane == 1 ? ka : kb) * (sqAf + u);
+        const float chi = ch * ch * 1.0001f;
+        // lane f: is frontier f's next domain inside its window?
+        bool in = false;
+        if (lane == 0) in = q0 > 0 && (float)cn >= clo;
+        if (lane == 1) in = q1 < q2 && (float)cn <= chi;
+        if (lane == 2) in = q1 < q2 && (float)cn >= clo;
+        if (lane == 3) in = q3 < n_k && (float)cn <= chi;
+        const unsigned m = __ballot_sync(0xffffffffu, in);
+        al0 = m & 1u;
+        al1 = (m >> 1) & 1u;
+        al2 = (m >> 2) & 1u;
+        al3 = (m >> 3) & 1u;
+    }
+    // phase 2: every pair of the visited runs with g <= thr takes the canonical binary64 path
+    // (thr = RU(gmin + 2 margin) >= best - A + margin; unvisited domains have lb > ub >= best)
+    float thr = gmin < INFINITY ? fminf(__double2float_ru(__dadd_rn((double)gmin, 2.0 * margin)), FLT_MAX) : -FLT_MAX;
+    double be = INFINITY;
+    int32_t bd = INT_MAX, bkj = INT_MAX;
+    unsigned n_exact = 0;
+    const int nrun = q1 < q2 ? 2 : 1;  // visited: [q0, q1) and [q2, q3), one run once q1 == q2
+    for (int w = 0; w < nrun; ++w) {
+        const int a0 = w == 0 ? q0 : q2;
+        const int a1 = (w == 0 && nrun == 2) ? q1 : q3;
+#pragma unroll 4
+        for (int pos = a0 + lane; pos < a1; pos += 32) {
+            float bq, cf;
+            if (gval(pos, bq, cf) <= thr) {
+                ++n_exact;
+                int j0;
+                const double e0 = b2_canon(P, A, bq, cf, j0);
+                const int32_t d = __ldg(P.ds + pos);
+                const int32_t kj = P.jpos[j0] | kPendIso;
+                if (b2_less(e0, d, kj, be, bd, bkj)) {
+                    be = e0; bd = d; bkj = kj;
+                    thr = fminf(thr, fminf(__double2float_ru(__dadd_rn(__dsub_rn(e0, A), margin)), FLT_MAX));
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double oe = __shfl_xor_sync(0xffffffffu, be, o);
+        const int32_t od = __shfl_xor_sync(0xffffffffu, bd, o);
+        const int32_t okj = __shfl_xor_sync(0xffffffffu, bkj, o);
+        if (b2_less(oe, od, okj, be, bd, bkj)) { be = oe; bd = od; bkj = okj; }
+        n_exact += __shfl_xor_sync(0xffffffffu, n_exact, o);
+    }
+    if (lane == 0) {
+        Partial pb;
+        pb.e = be;
+        pb.d = bd;
+        pb.kj = bkj;
+        P.part[(size_t)r * P.ns_cap] = pb;
+        if (n_exact && P.exact_count) atomicAdd(P.exact_count, (unsigned long long)n_exact);
+        if (P.scan_count) atomicAdd(P.scan_count, scanned);
+    }
+}
+
 // t2_j per slot, [slot][tw]; +inf on pad slots and pad j
-__global__ void b2_t2_kernel(const int64_t *__restrict__ C, const unsigned long long *__restrict__ d_nk,
+__global__ void b2_t2_kernel(const float4 *__restrict__ F, const unsigned long long *__restrict__ d_nk,
                              int64_t n_slots, const SList spos, int32_t nsp, int32_t tw, float *__restrict__ T) {
     const int64_t d = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (d >= n_slots) return;
     const int64_t n_k = (int64_t)*d_nk;
     if (d >= ((n_k + kTileD - 1) / kTileD) * kTileD) return;
-    const double c16 = __dmul_rn(0.0625, (double)C[d]);
+    const double c16 = __dmul_rn(0.0625, (double)F[d].w);  // C (exact in fp32, < 2^23)
     for (int j = 0; j < tw; ++j) {
         const double s = j < nsp ? spos.s[j] : 0.0;
         T[d * tw + j] = (d < n_k && j < nsp) ? __double2float_rn(__dmul_rn(__dmul_rn(s, s), c16)) : INFINITY;
@@ -448,22 +690,23 @@ int b2_t2_width(int32_t nsp) { return nsp <= 2 ? 2 : 16; }
 
 size_t b2_scratch_bytes(int64_t n_r, int32_t ns_cap) { return 64 + sizeof(float) * (size_t)n_r * ns_cap; }
 
-cudaError_t launch_b2_search(const SearchParams &sp, const float4 *F, float *T, const int32_t *kept,
-                             int32_t L, int32_t A, void *scratch, cudaStream_t st) {
+cudaError_t launch_b2_search(const SearchParams &sp, const B2Pool &bp, float *T, const int32_t *kept,
+                             int32_t L, int32_t A, void *scratch, unsigned long long *scan_count,
+                             cudaStream_t st) {
     if (sp.n_r == 0 || sp.nsp == 0) return cudaSuccess;
     const int tw = b2_t2_width(sp.nsp);
     const int64_t slots = sp.slot_stride;
     SList sl;
     memcpy(sl.s, sp.spos, sizeof sl.s);
     if (slots > 0) {
-        b2_t2_kernel<<<(unsigned)((slots + 255) / 256), 256, 0, st>>>(sp.C, &sp.d_misc[0], slots, sl, sp.nsp, tw, T);
+        b2_t2_kernel<<<(unsigned)((slots + 255) / 256), 256, 0, st>>>(bp.F, &sp.d_misc[0], slots, sl, sp.nsp, tw, T);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }
     B2Params p;
     memset(&p, 0, sizeof p);
     p.img = sp.img; p.N = sp.N; p.L = L; p.A = A; p.ranges = sp.ranges; p.n_r = sp.n_r;
-    p.F = F; p.T = T; p.tw = tw; p.kept = kept;
+    p.F = bp.F; p.T = T; p.Cs = bp.Cs; p.ds = bp.ds; p.tw = tw; p.kept = kept;
     p.d_nr = sp.d_nr; p.d_misc = sp.d_misc; p.nsplit = sp.nsplit; p.d_ns = sp.d_ns; p.ns_cap = sp.ns_cap;
     p.nsp = sp.nsp;
     memcpy(p.spos, sp.spos, sizeof p.spos);
@@ -471,9 +714,13 @@ cudaError_t launch_b2_search(const SearchParams &sp, const float4 *F, float *T, 
     for (int j = 0; j < kMaxS; ++j) p.nhs[j] = j < sp.nsp ? -(float)(0.25 * sp.spos[j]) : 0.f;
     p.has_zero = sp.has_zero; p.j_zero = sp.j_zero;
     p.smax = sp.smax;
-    p.part = sp.part; p.exact_count = sp.exact_count;
+    p.part = sp.part; p.exact_count = sp.exact_count; p.scan_count = scan_count;
     p.d_nscan = reinterpret_cast<unsigned long long *>(scratch);
     p.gmin = reinterpret_cast<float *>(static_cast<char *>(scratch) + 64);
+    if (sp.b2_window && !sp.has_zero && sp.nsp <= 2) {  // predefined s: Cauchy-Schwarz windows
+        b2win_kernel<<<(unsigned)((sp.n_r + 7) / 8), 256, 0, st>>>(p);
+        return cudaGetLastError();
+    }
     cudaError_t e = tw == 2 ? launch_b2_scan<1>(p, st) : launch_b2_scan<8>(p, st);
     if (e != cudaSuccess) return e;
     b2exact_kernel<<<(unsigned)((sp.n_r + 7) / 8), 256, 0, st>>>(p);

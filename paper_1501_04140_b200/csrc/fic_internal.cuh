@@ -28,6 +28,12 @@ struct Buf {
     size_t cap = 0;
 };
 
+struct B2Pool {          // B = 2 pool, sorted by C (stable)
+    float4 *F = nullptr;    // [slots] features (Y2, yr + yi, yr - yi, C) in sorted order
+    int32_t *Cs = nullptr;  // [slots] C in sorted order (pads 0xffffff)
+    int32_t *ds = nullptr;  // [slots] kept-domain rank of each sorted position
+};
+
 // One level's entropy-filtered domain pool (fic_pool).
 struct Pool {
     int32_t N = 0, B = 0, L = 0, n = 0, A = 0;
@@ -39,7 +45,7 @@ struct Pool {
     float *Dt = nullptr, *SDf = nullptr;
     float *Dc = nullptr;    // D4-Fourier domain records [slots][NCS] (B <= 8), or null
     uint8_t *Dtc = nullptr; // tcgen05 A operand: [tiles][chunks][128 x KCH] core-matrix u8, or null
-    float4 *F2 = nullptr;   // B = 2 closed-form domain features (Y2, yr, yi, 0)
+    B2Pool b2;              // B = 2 closed-form pool (sorted by C)
     int mode = 0;           // 0: tcgen05 (Dtc), 1: D4-Fourier (Dc), 2: direct FFMA (Dt), 3: B=2 closed form (F2)
     int32_t *SD = nullptr;
     int64_t *C = nullptr;
@@ -83,6 +89,7 @@ struct SearchParams {
     unsigned long long *exact_count;
     unsigned long long *d_ns;    // splits actually used (written by the search kernel)
     int32_t ns_cap;              // partial stride (max splits)
+    int32_t b2_window;           // B = 2: Cauchy-Schwarz C windows (env FIC_B2_WINDOW=0 disables)
 };
 
 struct FinalizeParams {
@@ -165,13 +172,18 @@ cudaError_t launch_merge_shards(const fic_record *in, const int64_t *d_counts, i
 int search_nsplit_hint(int32_t B, int64_t n_r, int64_t n_tiles, int num_sms);
 
 // B = 2 closed-form search (fic_b2.cu)
+size_t b2_pool_bytes(int64_t n_slots);
 cudaError_t launch_b2_pool(const uint8_t *img, int32_t N, int32_t L, int32_t A, const int32_t *kept,
-                           const unsigned long long *d_nk, int64_t n_slots, float4 *F, cudaStream_t st);
+                           const unsigned long long *d_nk, int64_t n_slots, void *store, B2Pool *out,
+                           cudaStream_t st);
 int b2_nsplit_hint(int64_t n_r, int64_t n_tiles, int num_sms);
 int b2_t2_width(int32_t nsp);  // floats per slot of the B = 2 t2 table
 size_t b2_scratch_bytes(int64_t n_r, int32_t ns_cap);  // pass-1 minima + split count
-cudaError_t launch_b2_search(const SearchParams &sp, const float4 *F, float *T, const int32_t *kept,
-                             int32_t L, int32_t A, void *scratch, cudaStream_t st);
+// scan_count: (range, domain) pairs the search evaluated (the windowed path proves the rest
+// non-competitive); may be null
+cudaError_t launch_b2_search(const SearchParams &sp, const B2Pool &bp, float *T, const int32_t *kept,
+                             int32_t L, int32_t A, void *scratch, unsigned long long *scan_count,
+                             cudaStream_t st);
 cudaError_t launch_fourier_u(const int64_t *C, const unsigned long long *d_nk, int64_t n_slots, const SList &sl,
                              int32_t nsp, float *U, cudaStream_t st);
 

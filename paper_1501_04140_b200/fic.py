@@ -44,7 +44,7 @@ class LevelStats(C.Structure):
     _fields_ = [("B", C.c_int32), ("n_candidates", C.c_int64), ("n_kept", C.c_int64),
                 ("n_ranges", C.c_int64), ("n_accepted", C.c_int64), ("pairs", C.c_int64),
                 ("exact_evals", C.c_int64), ("ms_pool", C.c_float), ("ms_search", C.c_float),
-                ("ms_finalize", C.c_float), ("kernel_launches", C.c_int64)]
+                ("ms_finalize", C.c_float), ("kernel_launches", C.c_int64), ("pairs_scanned", C.c_int64)]
 
 
 _lib = None

@@ -289,14 +289,16 @@ def test_c5_sampled(fic):
 
 
 # ------------------------------------------------------------------ every search implementation
-@pytest.mark.parametrize("mode", ["tc", "fourier", "direct"])
+@pytest.mark.parametrize("mode", ["tc", "fourier", "direct", "b2scan"])
 def test_search_modes_parity(fic, mode):
-    """The non-default kernels (tcgen05 at B = 2, D4-Fourier CUDA cores, direct FFMA) are
-    bit-exact too; FIC_SEARCH is read when a context is created."""
+    """The non-default kernels (tcgen05 at B = 2, D4-Fourier CUDA cores, direct FFMA, and the
+    B = 2 full two-pass scan instead of the C windows) are bit-exact too; FIC_SEARCH and
+    FIC_B2_WINDOW are read when a context is created."""
     import os
     p, _, torch = fic
-    old = os.environ.get("FIC_SEARCH")
-    os.environ["FIC_SEARCH"] = mode
+    var, val = ("FIC_B2_WINDOW", "0") if mode == "b2scan" else ("FIC_SEARCH", mode)
+    old = os.environ.get(var)
+    os.environ[var] = val
     try:
         ctx = p.Context(0)
         for smode in ("predefined", "grid"):
@@ -309,9 +311,9 @@ def test_search_modes_parity(fic, mode):
         ctx.close()
     finally:
         if old is None:
-            os.environ.pop("FIC_SEARCH", None)
+            os.environ.pop(var, None)
         else:
-            os.environ["FIC_SEARCH"] = old
+            os.environ[var] = old
 
 
 def test_capacity_error_reports_count(fic):
