@@ -244,6 +244,16 @@ def main():
     if world > 1:
         dist.barrier()
     clk = clocks.stop()
+    # quality sanity (outside the timed region): decode the last code (12 Jacobi passes from the
+    # constant 128 image, readings R23-R25) and its PSNR against the input (R26)
+    d0 = torch.cuda.Event(enable_timing=True)
+    d1 = torch.cuda.Event(enable_timing=True)
+    d0.record(stream)
+    decoded = ctx.decode(rec, cfg["N"], cfg["B_max"], cfg["s"], 12)
+    d1.record(stream)
+    d1.synchronize()
+    quality = {"psnr_db": ctx.psnr(decoded, img), "decode_iterations": 12,
+               "decode_ms": d0.elapsed_time(d1), "note": "sanity report on the synthetic image"}
     total_ms = sum(times)
     pairs_step = sum(s["pairs"] for s in level_acc)
     t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
@@ -299,13 +309,22 @@ def main():
     p_int8 = 2.0 * float(peaks.get("bf16_tflops", 1640.9)) * 1e12  # measured bf16 x nominal int8 ratio
     p_int32 = 148 * 128 * sm_max                                   # fma + alu pipes, 64 lanes each
     p_fp64 = 148 * 64 * sm_max                                     # B200 fp64 (37 TF)
+    def t_pair(B, nS):  # seconds per pair at the roofline
+        n = B * B
+        return max(4.0 * n / p_int8, 2.0 / p_int32 + 0.5 * nS / p_fp64)
+
+    lv_B = [lv["B"] for lv in level_acc]
+    for lv in level_acc:
+        nS_l = len(cfg["s"][lv_B.index(lv["B"])])
+        evald = lv["pairs_scanned"] * 8  # pairs the kernel evaluated (B=2 windows skip proven losers)
+        t_l = lv["ms_search"] / args.steps / 1e3
+        lv["roof_frac"] = (evald * t_pair(lv["B"], nS_l) / t_l) if t_l > 0 else None
     dom = max(level_acc, key=lambda s: s["ms_search"])
     n = dom["B"] * dom["B"]
-    nS = len(cfg["s"][[lv["B"] for lv in level_acc].index(dom["B"])])
-    t_pair = max(4.0 * n / p_int8, 2.0 / p_int32 + 0.5 * nS / p_fp64)
+    nS = len(cfg["s"][lv_B.index(dom["B"])])
     ms_launch = dom["ms_search"] / args.steps
-    achieved = dom["pairs"] / (ms_launch / 1e3) / 1e9
-    peak = 1.0 / t_pair / 1e9
+    achieved = dom["pairs_scanned"] * 8 / (ms_launch / 1e3) / 1e9
+    peak = 1.0 / t_pair(dom["B"], nS) / 1e9
     traffic = load_traffic()
 
     res = {
@@ -319,18 +338,21 @@ def main():
                    "l2": "flushed between timed steps (256 MB write)",
                    "pairs_per_step": pairs_step, "records_per_step": n_rec},
         "roofline": {"bound": "alu" if 4.0 * n / p_int8 < 2.0 / p_int32 + 0.5 * nS / p_fp64 else "tensor",
-                     "kernel": ("b2search_kernel (B=2 closed form, CUDA cores)" if dom["B"] == 2
+                     "kernel": ("b2win_kernel (B=2 closed form, C windows, CUDA cores)" if dom["B"] == 2
                                 else f"tcsearch_kernel<B={dom['B']}> (tcgen05 kind::i8)"),
                      "achieved": achieved, "peak": peak, "unit": "Gpairs/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "peak_note": "SURVEY 8(d): 1/max(4n/P_int8, 2/P_int32 + 0.5|S|/P_fp64) pairs/s; "
                                   "P_int8 = 2 x measured bf16 burst, P_int32 = 148x128xf_max, "
-                                  "P_fp64 = 148x64xf_max (DESIGN.md 7)"},
+                                  "P_fp64 = 148x64xf_max; achieved counts the pairs the kernel "
+                                  "evaluated (DESIGN.md 7)"},
         "levels": [{"B": s["B"], "n_candidates": s["n_candidates"], "n_kept": s["n_kept"],
                     "n_ranges": s["n_ranges"], "pairs": s["pairs"],
                     "exact_evals": s["exact_evals"], "pairs_scanned": s["pairs_scanned"],
                     "ms_pool": s["ms_pool"] / args.steps, "ms_search": s["ms_search"] / args.steps,
-                    "ms_finalize": s["ms_finalize"] / args.steps} for s in level_acc],
+                    "ms_finalize": s["ms_finalize"] / args.steps, "roof_frac": s["roof_frac"]}
+                   for s in level_acc],
+        "quality": quality,
         "gpu_launches": int(launches),
         "clocks": clk,
     }

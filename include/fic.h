@@ -138,6 +138,29 @@ fic_status fic_encode_host(fic_ctx *ctx, const uint8_t *h_img, int32_t N, int32_
 fic_status fic_merge_shards(fic_ctx *ctx, const fic_record *in, const int64_t *h_counts,
                             int32_t n_shards, int64_t stride, fic_record *out);
 
+/* ------------------------------------------------------------------------ decoding, quality */
+
+/* PIFS decoding of a code (the paper encodes only; "an affine transformation that maps
+ * the selected domain block", readings R23-R25 in DESIGN.md): starting from `init` (device
+ * [N*N], or NULL for the constant image 128), `iterations` Jacobi passes, each setting every
+ * pixel of every record's B x B range to clamp(rint(s * d + o^), 0, 255), where d is the
+ * record's isometry T_iso applied to the 2 x 2-averaged (D'/4, exact) 2B x 2B block at (dx, dy)
+ * of the previous pass, s = the record level's s list [s_idx] and o^ = (o_code - 127.5) * 510/256
+ * (binary64, s*d then +o^, no contraction).  Pixels no record covers keep their value.
+ * rec: device fic_record [n_rec] (e.g. fic_encode's output; any order; ranges must not overlap);
+ * h_s / h_n_s: the per-level s lists as passed to fic_encode (level l has B = B_max >> l);
+ * out: device [N*N] (may not alias init).  Synchronous.
+ * Errors: ARG (null, iterations < 0, a record out of bounds or naming an unknown level / s index /
+ * isometry), CUDA. */
+fic_status fic_decode(fic_ctx *ctx, const fic_record *rec, int64_t n_rec, int32_t N, int32_t B_max,
+                      int32_t n_levels, const double *h_s, const int32_t *h_n_s, int32_t iterations,
+                      const uint8_t *init, uint8_t *out);
+
+/* PSNR of two device images of n pixels ("PSNR", reading R26):
+ * 10 log10(255^2 / MSE) with MSE = (exact integer sum of squared differences) / n, +inf when
+ * identical.  *h_psnr receives the value.  Synchronous.  Errors: ARG, CUDA. */
+fic_status fic_psnr(fic_ctx *ctx, const uint8_t *a, const uint8_t *b, int64_t n, double *h_psnr);
+
 /* Host-only: the entropy fixed-point table lut[c] = round-half-even(c log2(c) 2^32),
  * c = 0..mmax (h_lut host int64 [mmax+1]).  No device work. */
 fic_status fic_entropy_lut(int64_t *h_lut, int32_t mmax);

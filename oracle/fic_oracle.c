@@ -381,6 +381,78 @@ int fico_encode(const uint8_t *img, int32_t N, int32_t B_max, int32_t B_min, int
     return total > capacity ? FICO_ERR_CAPACITY : FICO_OK;
 }
 
+/* ---------------------------------------------------------------- decoding (PIFS) ---------- */
+/* The paper encodes only; decoding is the standard PIFS iteration implied by P:28-30 ("an
+ * affine transformation that maps the selected domain block").  Readings [R23-R26]:
+ *   o dequantiser  o^ = (code - 127.5) * 510/256, the centre of the [R11] midrise cell (exact);
+ *   one pass       out(R) = clamp(rint(s * d + o^), 0, 255) per pixel of each leaf R, with
+ *                  d = T_k(D'/4) of the 2B x 2B block at (dx, dy) of the PREVIOUS iterate
+ *                  (Jacobi, binary64, s * d rounded, then + o^ rounded, rint half-even);
+ *   start          the constant image 128 (or a given image); a fixed iteration count;
+ *   PSNR           10 log10(255^2 / MSE), MSE = (exact integer sum of squared differences)/n,
+ *                  +inf for identical images ("PSNR"). */
+double fico_o_value(int32_t code) { return ((double)code - 127.5) * 1.9921875; }
+
+static int32_t fico_level_of(int32_t B_max, int32_t B) {
+    int32_t l = 0;
+    while ((B_max >> l) > B) ++l;
+    return (B_max >> l) == B ? l : -1;
+}
+
+int fico_decode(const fico_record *rec, int64_t n_rec, int32_t N, const double *s_flat,
+                const int32_t *n_s, int32_t B_max, int32_t n_levels, int32_t iterations,
+                const uint8_t *init, uint8_t *out) {
+    if (!rec || !s_flat || !n_s || !out || N < 1 || n_levels < 1 || iterations < 0) return FICO_ERR_ARG;
+    int64_t off[16];
+    off[0] = 0;
+    for (int32_t l = 0; l < n_levels && l < 15; ++l) off[l + 1] = off[l] + n_s[l];
+    for (int64_t q = 0; q < n_rec; ++q) {  /* validate: in bounds, known level and s index */
+        const fico_record *r = &rec[q];
+        const int32_t l = fico_level_of(B_max, r->B);
+        if (l < 0 || l >= n_levels || r->s_idx >= n_s[l] || r->iso > 7) return FICO_ERR_ARG;
+        if (r->rx < 0 || r->ry < 0 || r->rx + r->B > N || r->ry + r->B > N) return FICO_ERR_ARG;
+        if (r->dx < 0 || r->dy < 0 || r->dx + 2 * r->B > N || r->dy + 2 * r->B > N) return FICO_ERR_ARG;
+    }
+    const int64_t np = (int64_t)N * N;
+    uint8_t *prev = (uint8_t *)malloc((size_t)np);
+    if (!prev) return FICO_ERR_NOMEM;
+    if (init) memcpy(out, init, (size_t)np);
+    else memset(out, 128, (size_t)np);
+    for (int32_t it = 0; it < iterations; ++it) {
+        memcpy(prev, out, (size_t)np);
+        for (int64_t q = 0; q < n_rec; ++q) {
+            const fico_record *r = &rec[q];
+            const int32_t B = r->B, l = fico_level_of(B_max, B);
+            const double s = s_flat[off[l] + r->s_idx], o = fico_o_value(r->o_code);
+            int32_t Dp[32 * 32];
+            fico_decimate(prev, N, r->dx, r->dy, B, Dp);
+            for (int32_t i = 0; i < B; ++i)
+                for (int32_t j = 0; j < B; ++j) {
+                    int32_t si, sj;
+                    fico_isometry_src(B, r->iso, i, j, &si, &sj);
+                    const double d = (double)Dp[si * B + sj] / 4.0;
+                    double v = rint(s * d + o);
+                    if (v < 0.0) v = 0.0;
+                    if (v > 255.0) v = 255.0;
+                    out[(int64_t)(r->ry + i) * N + r->rx + j] = (uint8_t)v;
+                }
+        }
+    }
+    free(prev);
+    return FICO_OK;
+}
+
+double fico_psnr(const uint8_t *a, const uint8_t *b, int64_t n) {
+    int64_t sse = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        const int64_t d = (int64_t)a[i] - (int64_t)b[i];
+        sse += d * d;
+    }
+    if (sse == 0) return INFINITY;
+    const double mse = (double)sse / (double)n;
+    return 10.0 * log10(65025.0 / mse);
+}
+
 int fico_num_threads(void) {
 #ifdef _OPENMP
     return omp_get_max_threads();

@@ -55,6 +55,11 @@ def lib():
             L.fico_encode.argtypes = [P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, P, P, P, P,
                                       C.c_int32, C.c_int32, P, C.c_int64, P]
             L.fico_num_threads.restype = C.c_int
+            L.fico_o_value.argtypes = [C.c_int32]
+            L.fico_o_value.restype = C.c_double
+            L.fico_decode.argtypes = [P, C.c_int64, C.c_int32, P, P, C.c_int32, C.c_int32, C.c_int32, P, P]
+            L.fico_psnr.argtypes = [P, P, C.c_int64]
+            L.fico_psnr.restype = C.c_double
             _lib = L
     return _lib
 
@@ -170,3 +175,30 @@ def encode_cfg(cfg, img=None, shard=0, n_shards=1):
         img = image_for(cfg)
     return encode(img, cfg["B_max"], cfg["B_min"], cfg["L"], cfg["tau"], cfg["s"],
                   cfg["rms_tol"], shard, n_shards)
+
+
+def o_value(code: int) -> float:
+    """Dequantised offset of an o code (centre of the [R11] cell), reading R23."""
+    return float(lib().fico_o_value(int(code)))
+
+
+def decode(records, N: int, s_sets, B_max: int, iterations: int = 12, init=None):
+    """PIFS decode (readings R23-R26): Jacobi iterations from the constant 128 image (or init)."""
+    rec = np.ascontiguousarray(records, dtype=RECORD_DTYPE)
+    n_s = np.array([len(x) for x in s_sets], np.int32)
+    s_flat = np.ascontiguousarray(np.concatenate([np.asarray(x, np.float64) for x in s_sets]))
+    out = np.zeros((N, N), np.uint8)
+    ini = None if init is None else _img(init)
+    st = lib().fico_decode(_p(rec), rec.shape[0], N, _p(s_flat), _p(n_s), B_max, len(s_sets), iterations,
+                           None if ini is None else _p(ini), _p(out))
+    if st:
+        raise RuntimeError(f"fico_decode status {st}")
+    return out
+
+
+def psnr(a, b) -> float:
+    a = np.ascontiguousarray(a, dtype=np.uint8)
+    b = np.ascontiguousarray(b, dtype=np.uint8)
+    if a.shape != b.shape:
+        raise ValueError("shape mismatch")
+    return float(lib().fico_psnr(_p(a), _p(b), a.size))

@@ -41,7 +41,7 @@ struct fic_ctx {
     cudaEvent_t main_ready = nullptr;
     int b2_window = 1;    // env FIC_B2_WINDOW=0: B = 2 full scan instead of the C windows
     int search_mode = 0;  // env FIC_SEARCH: auto (default: B=2 closed form, else tcgen05) | fourier | direct | tc
-    Buf b_rc, b_meta, b_u, b_gthr, b_rop;  // libfic kernels enqueued (for fic_level_stats.kernel_launches)  // pool start, search start, search end, finalize end, pool end
+    Buf b_rc, b_meta, b_u, b_gthr, b_rop, b_dec;  // libfic kernels enqueued (for fic_level_stats.kernel_launches)  // pool start, search start, search end, finalize end, pool end
 };
 
 namespace {
@@ -260,6 +260,9 @@ fic_status level_enqueue(fic_ctx *ctx, const Pool &P, const uint8_t *img, const 
     // dynamic kernels (tcgen05, B=2) choose their split count on the device, up to ns_cap
     const bool dyn = (P.mode == 0 || P.mode == 3);
     sp.b2_window = ctx->b2_window;
+    sp.L = P.L;
+    sp.Acnt = P.A;
+    sp.kept = P.kept;
     sp.ns_cap = dyn ? (int32_t)std::min<int64_t>(4 * (int64_t)sp.nsplit, std::max<int64_t>(1, tiles)) : sp.nsplit;
     sp.d_ns = ptr<unsigned long long>(ctx->b_counts) + 56 + level_slot;
     if (!dyn) CK(fic::launch_set_u64(sp.d_ns, (unsigned long long)sp.nsplit, st));
@@ -337,6 +340,52 @@ fic_status ctx_check(fic_ctx *ctx) {
 // =============================================================================== C ABI
 extern "C" {
 
+// ------------------------------------------------------------------------- decoding, PSNR
+fic_status fic_decode(fic_ctx *ctx, const fic_record *rec, int64_t n_rec, int32_t N, int32_t B_max,
+                      int32_t n_levels, const double *h_s, const int32_t *h_n_s, int32_t iterations,
+                      const uint8_t *init, uint8_t *out) {
+    CKS(ctx_check(ctx));
+    if ((!rec && n_rec) || n_rec < 0 || !h_s || !h_n_s || !out || iterations < 0)
+        return fail(ctx, FIC_ERR_ARG, "null or negative argument");
+    if (N < 1 || !pow2(B_max) || n_levels < 1 || n_levels > fic::kMaxLevels || (B_max >> (n_levels - 1)) < 1)
+        return fail(ctx, FIC_ERR_ARG, "bad N, B_max or level count");
+    fic::DecSList sl;
+    memset(&sl, 0, sizeof sl);
+    int32_t off = 0;
+    for (int l = 0; l < n_levels; ++l) {
+        CKS(check_s(ctx, h_s + off, h_n_s[l]));
+        sl.off[l] = off;
+        sl.n_s[l] = h_n_s[l];
+        for (int j = 0; j < h_n_s[l]; ++j) sl.s[off + j] = h_s[off + j];
+        off += h_n_s[l];
+    }
+    cudaStream_t st = ctx->stream;
+    CK(grow(ctx, ctx->b_dec, fic::decode_scratch_bytes(N, n_rec)));
+    unsigned long long *d_counts = ptr<unsigned long long>(ctx->b_counts);
+    int32_t *d_bad = reinterpret_cast<int32_t *>(d_counts + 62);
+    CK(cudaMemsetAsync(d_bad, 0, sizeof(int32_t), st));
+    CK(fic::launch_decode(rec, n_rec, N, B_max, n_levels, sl, iterations, init, out, ctx->b_dec.p, d_bad, st));
+    int32_t bad = 0;
+    CK(cudaMemcpyAsync(&bad, d_bad, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (bad) return fail(ctx, FIC_ERR_ARG, "a record is out of bounds or names an unknown level / s index");
+    return FIC_OK;
+}
+
+fic_status fic_psnr(fic_ctx *ctx, const uint8_t *a, const uint8_t *b, int64_t n, double *h_psnr) {
+    CKS(ctx_check(ctx));
+    if (!a || !b || !h_psnr || n < 1) return fail(ctx, FIC_ERR_ARG, "null argument or empty image");
+    cudaStream_t st = ctx->stream;
+    unsigned long long *d_sse = ptr<unsigned long long>(ctx->b_counts) + 63;
+    CK(fic::launch_sse(a, b, n, d_sse, st));
+    unsigned long long sse = 0;
+    CK(cudaMemcpyAsync(&sse, d_sse, sizeof sse, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    // reading R26: 10 log10(255^2 / MSE), MSE = SSE / n; +inf for identical images
+    *h_psnr = sse == 0 ? INFINITY : 10.0 * std::log10(65025.0 / ((double)sse / (double)n));
+    return FIC_OK;
+}
+
 const char *fic_version(void) { return "fic-b200 0.1 (sm_100a; fp32-exact CUDA-core search)"; }
 
 fic_status fic_entropy_lut(int64_t *h_lut, int32_t mmax) {
@@ -411,7 +460,7 @@ fic_status fic_ctx_destroy(fic_ctx *ctx) {
     for (auto &P : ctx->levels) free_pool(P);
     Buf *bufs[] = {&ctx->b_blocksum, &ctx->b_counts, &ctx->b_rng[0], &ctx->b_rng[1], &ctx->b_rec,
                    &ctx->b_acc, &ctx->b_child, &ctx->b_part, &ctx->b_t2f, &ctx->b_img, &ctx->b_out,
-                   &ctx->b_scounts, &ctx->b_rc, &ctx->b_meta, &ctx->b_u, &ctx->b_gthr, &ctx->b_rop};
+                   &ctx->b_scounts, &ctx->b_rc, &ctx->b_meta, &ctx->b_u, &ctx->b_gthr, &ctx->b_rop, &ctx->b_dec};
     for (Buf *b : bufs) free_buf(*b);
     if (ctx->d_delta) cudaFree(ctx->d_delta);
     if (ctx->h_counts) cudaFreeHost(ctx->h_counts);

@@ -90,6 +90,8 @@ struct SearchParams {
     unsigned long long *d_ns;    // splits actually used (written by the search kernel)
     int32_t ns_cap;              // partial stride (max splits)
     int32_t b2_window;           // B = 2: Cauchy-Schwarz C windows (env FIC_B2_WINDOW=0 disables)
+    int32_t L, Acnt;             // domain step and candidates per axis (threshold seeding)
+    const int32_t *kept;         // kept-domain candidate indices
 };
 
 struct FinalizeParams {
@@ -186,6 +188,18 @@ cudaError_t launch_b2_search(const SearchParams &sp, const B2Pool &bp, float *T,
                              cudaStream_t st);
 cudaError_t launch_fourier_u(const int64_t *C, const unsigned long long *d_nk, int64_t n_slots, const SList &sl,
                              int32_t nsp, float *U, cudaStream_t st);
+
+// decoding and PSNR (fic_decode.cu)
+struct DecSList {
+    double s[kMaxLevels * kMaxS];
+    int32_t off[kMaxLevels], n_s[kMaxLevels];
+};
+size_t decode_scratch_bytes(int32_t N, int64_t n_rec);
+// passes alternate between scratch and out; *d_bad = 1 on an invalid record (checked by the caller)
+cudaError_t launch_decode(const fic_record *rec, int64_t n_rec, int32_t N, int32_t B_max, int32_t n_levels,
+                          const DecSList &sl, int32_t iterations, const uint8_t *init, uint8_t *out,
+                          void *scratch, int32_t *d_bad, cudaStream_t st);
+cudaError_t launch_sse(const uint8_t *a, const uint8_t *b, int64_t n, unsigned long long *d_sse, cudaStream_t st);
 
 // tcgen05 search (fic_tc.cu), B in {2, 4, 8, 16}
 int tc_supported(int B);

@@ -30,7 +30,7 @@ EXPORTS = (
     "fic_ctx_create", "fic_ctx_set_stream", "fic_ctx_destroy", "fic_last_error",
     "fic_ctx_set_timing", "fic_get_stats", "fic_build_domain_pool", "fic_pool_info",
     "fic_pool_destroy", "fic_encode_level", "fic_encode", "fic_encode_host", "fic_merge_shards",
-    "fic_entropy_lut", "fic_version",
+    "fic_entropy_lut", "fic_version", "fic_decode", "fic_psnr",
 )
 
 
@@ -74,6 +74,8 @@ def load(path: str = SO_PATH):
         "fic_encode_host": ([P, P, i32, i32, i32, i32, P, P, P, P, i32, i32, P, i64, P], C.c_int),
         "fic_merge_shards": ([P, P, P, i32, i64, P], C.c_int),
         "fic_entropy_lut": ([P, i32], C.c_int),
+        "fic_decode": ([P, P, i64, i32, i32, i32, P, P, i32, P, P], C.c_int),
+        "fic_psnr": ([P, P, P, i64, P], C.c_int),
         "fic_version": ([], C.c_char_p),
     }
     for name, (args, res) in sig.items():
@@ -275,6 +277,26 @@ class Context:
         self._check(self.lib.fic_merge_shards(self.handle, _dptr(recs), _ptr(cnt), cnt.size,
                                               stride, _dptr(out)), "fic_merge_shards")
         return out[: int(cnt.sum())]
+
+    def decode(self, recs, N: int, B_max: int, s_sets, iterations: int = 12, init=None):
+        """PIFS decode (fic_decode): CUDA uint8 [n, 40] records -> CUDA uint8 [N, N] image."""
+        import torch
+        n_s = np.array([len(x) for x in s_sets], np.int32)
+        s_flat = np.ascontiguousarray(np.concatenate([np.asarray(x, np.float64) for x in s_sets]))
+        dev = recs.device if recs.is_cuda else torch.device("cuda")
+        out = torch.empty((N, N), dtype=torch.uint8, device=dev)
+        n = recs.shape[0]
+        self._check(self.lib.fic_decode(self.handle, _dptr(recs) if n else None, n, N, B_max, len(s_sets),
+                                        _ptr(s_flat), _ptr(n_s), int(iterations),
+                                        _dptr(init) if init is not None else None, _dptr(out)),
+                    "fic_decode")
+        return out
+
+    def psnr(self, a, b) -> float:
+        """PSNR of two CUDA uint8 images (fic_psnr)."""
+        v = C.c_double()
+        self._check(self.lib.fic_psnr(self.handle, _dptr(a), _dptr(b), a.numel(), C.byref(v)), "fic_psnr")
+        return v.value
 
 
 def records_to_numpy(t) -> np.ndarray:

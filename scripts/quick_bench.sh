@@ -7,5 +7,5 @@ import json
 d = json.loads(open("gpurun_out/qb.log").read().strip().splitlines()[-1])
 print("ms/encode %.3f  frac %.3f" % (d["ms_per_step"], d["roofline"]["frac"]))
 for l in d["levels"]:
-    print("B=%2d pool %.3f search %.3f exact %d scanned %.4f" % (l["B"], l["ms_pool"], l["ms_search"], l["exact_evals"], l["pairs_scanned"] * 8.0 / max(l["pairs"], 1)))
+    print("B=%2d pool %.3f search %.3f exact %d scanned %.4f frac %.3f" % (l["B"], l["ms_pool"], l["ms_search"], l["exact_evals"], l["pairs_scanned"] * 8.0 / max(l["pairs"], 1), l["roof_frac"] or 0))
 PY
