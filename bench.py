@@ -43,7 +43,9 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["fic", "reference"], default="fic")
     ap.add_argument("--config", default="C3")
-    ap.add_argument("--s-mode", default="predefined", choices=["predefined", "grid"])
+    ap.add_argument("--s-mode", default="predefined", choices=["predefined", "grid", "sampled10"])
+    ap.add_argument("--topk", type=int, default=0,
+                    help="pool size K per level (the paper's Tables 1-2 axis) instead of the entropy tau")
     ap.add_argument("--t", type=float, default=8.0)
     ap.add_argument("--cpu-shards", type=int, default=1,
                     help="cpu_baseline sample = 1/cpu-shards of the top-level blocks (1 = whole C3)")
@@ -149,7 +151,7 @@ def run_reference(args, cfg_name):
     if rank != 0:
         return 0
     from fic_inputs import config, image_for
-    cfg = config(cfg_name, s_mode=args.s_mode, t=args.t)
+    cfg = config(cfg_name, s_mode=args.s_mode, t=args.t, topk=args.topk or None)
     img = image_for(cfg)
     S = args.ref_shards
     for w in range(args.warmup):
@@ -197,7 +199,7 @@ def main():
     dev = torch.device("cuda", local if world > 1 else 0)
     torch.cuda.set_device(dev)
 
-    cfg = config(cfg_name, s_mode=args.s_mode, t=args.t, seed=rank)
+    cfg = config(cfg_name, s_mode=args.s_mode, t=args.t, seed=rank, topk=args.topk or None)
     img_np = image_for(cfg)
     img = torch.from_numpy(img_np).to(dev)
     stream = torch.cuda.current_stream(dev)
@@ -334,6 +336,7 @@ def main():
         "data": "synthetic",
         "config": {"workload": cfg_name, "N": cfg["N"], "levels": f"{cfg['B_max']}->{cfg['B_min']}",
                    "L": cfg["L"], "s_mode": args.s_mode, "rms_tol": args.t,
+                   "pool": (f"top-{args.topk}" if args.topk else "entropy tau"),
                    "entropy_tau": cfg["tau"], "images": "seed = rank",
                    "l2": "flushed between timed steps (256 MB write)",
                    "pairs_per_step": pairs_step, "records_per_step": n_rec},

@@ -17,6 +17,9 @@ from .synth import make_image
 PREDEFINED_S = {16: (0.1,), 8: (0.2, 0.4), 4: (0.3, 0.8), 2: (0.5, 0.9)}
 # PAPER.md §2 line 38 "pre-sampled set of [0,1]"; BASELINE.json: 16-value uniform grid
 GRID_S = tuple(j / 15.0 for j in range(16))
+# SPEC.md sampled10 (NEXT-4): the paper's 10-member baseline set "sampled from [0,1]",
+# read as ten uniform mid-point samples
+SAMPLED10_S = tuple((2 * j + 1) / 20.0 for j in range(10))
 
 _TAU_PATH = os.path.join(os.path.dirname(__file__), "tau.json")
 
@@ -47,12 +50,14 @@ def s_sets(B_max: int, B_min: int, mode: str):
             res.append(tuple(PREDEFINED_S.get(B, PREDEFINED_S[min(PREDEFINED_S, key=lambda b: abs(b - B))])))
         elif mode == "grid":
             res.append(GRID_S)
+        elif mode == "sampled10":
+            res.append(SAMPLED10_S)
         else:
             raise ValueError(mode)
     return res
 
 
-def config(name: str, *, s_mode: str = "predefined", t: float = 8.0, seed: int = 0):
+def config(name: str, *, s_mode: str = "predefined", t: float = 8.0, seed: int = 0, topk=None):
     """Return a dict describing one run: image + encoder parameters.
 
     Keys: name, N, seed, texture, B_max, B_min, L, tau (list per level), s (list of tuples per
@@ -84,6 +89,8 @@ def config(name: str, *, s_mode: str = "predefined", t: float = 8.0, seed: int =
     c["s_mode"] = s_mode
     c["s"] = s_sets(c["B_max"], c["B_min"], s_mode)
     c["rms_tol"] = [float(t)] * nlev
+    if topk is not None:  # the paper's "pool size" per level (Tables 1-2) instead of tau
+        c["topk"] = [int(k) for k in (topk if hasattr(topk, "__len__") else [topk] * nlev)]
     return c
 
 

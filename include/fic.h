@@ -92,6 +92,13 @@ fic_status fic_get_stats(const fic_ctx *ctx, fic_level_stats *h_out, int32_t max
 fic_status fic_build_domain_pool(fic_ctx *ctx, const uint8_t *img, int32_t N, int32_t B,
                                  int32_t L, double tau_nats, fic_pool **out);
 
+/* Same with the paper's "pool size" selection (Tables 1-2; reading R27) instead of a
+ * threshold: the K candidates with the largest entropy keys, ties to the lower row-major index;
+ * the kept list stays in ascending candidate order.  K >= n_candidates keeps all.
+ * Errors: ARG (K < 1 or as above), SHAPE, CUDA, NOMEM.  Synchronises the ctx stream. */
+fic_status fic_build_domain_pool_topk(fic_ctx *ctx, const uint8_t *img, int32_t N, int32_t B,
+                                      int32_t L, int64_t K, fic_pool **out);
+
 /* Host view of a pool.  keep_mask [n_candidates] u8, kept [n_kept] int32 (ascending candidate
  * indices), keys [n_candidates] int64 entropy keys (m * H_bits * 2^32 fixed point) -- all
  * device pointers owned by the pool.  Any output pointer may be NULL. */
@@ -123,6 +130,14 @@ fic_status fic_encode(fic_ctx *ctx, const uint8_t *img, int32_t N, int32_t B_max
                       int32_t L, const double *h_tau, const double *h_s, const int32_t *h_n_s,
                       const double *h_rms_tol, int32_t shard, int32_t n_shards, fic_record *out,
                       int64_t capacity, int64_t *h_n_out);
+
+/* fic_encode with per-level pool sizes h_K [levels] (top-K selection, as
+ * fic_build_domain_pool_topk) in place of the entropy thresholds.  Errors: as fic_encode, and
+ * ARG if some K < 1. */
+fic_status fic_encode_topk(fic_ctx *ctx, const uint8_t *img, int32_t N, int32_t B_max, int32_t B_min,
+                           int32_t L, const int64_t *h_K, const double *h_s, const int32_t *h_n_s,
+                           const double *h_rms_tol, int32_t shard, int32_t n_shards, fic_record *out,
+                           int64_t capacity, int64_t *h_n_out);
 
 /* Same as fic_encode with HOST buffers: h_img [N*N] is copied to the device, h_out [capacity]
  * receives the records (device->host copy inside the call).  Synchronous. */

@@ -17,5 +17,5 @@ different images).
 from .oracle import (  # noqa: F401
     build, lib, lut, threshold, axis_candidates, entropy_keys, kept_list, isometry,
     decimate, o_code, encode_level, encode, encode_cfg, RECORD_DTYPE, num_threads,
-    o_value, decode, psnr,
+    o_value, decode, psnr, kept_list_topk,
 )

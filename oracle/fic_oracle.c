@@ -306,15 +306,49 @@ int64_t fico_kept_list(const uint8_t *img, int32_t N, int32_t B, int32_t L, doub
     return n;
 }
 
+/* Top-K pool selection (the paper's "pool size", Tables 1-2; reading R27): the K
+ * candidates with the largest entropy keys, ties to the lower row-major index; the kept list is
+ * still returned in ascending (row-major) candidate order [R18].  K >= n_c keeps every candidate.
+ * The ranking is a plain sort (qsort on (key desc, index asc)).  Returns the count. */
+typedef struct { int64_t key; int64_t idx; } fico_kc;
+static int fico_kc_cmp(const void *a, const void *b) {
+    const fico_kc *x = (const fico_kc *)a, *y = (const fico_kc *)b;
+    if (x->key != y->key) return x->key > y->key ? -1 : 1;
+    return x->idx < y->idx ? -1 : (x->idx > y->idx);
+}
+static int fico_i32_cmp(const void *a, const void *b) {
+    const int32_t x = *(const int32_t *)a, y = *(const int32_t *)b;
+    return (x > y) - (x < y);
+}
+int64_t fico_kept_list_topk(const uint8_t *img, int32_t N, int32_t B, int32_t L, int64_t K,
+                            int32_t *kept_out /* capacity n_c */) {
+    int64_t A = fico_axis_candidates(N, B, L);
+    if (A <= 0) return -FICO_ERR_SHAPE;
+    if (K < 1) return -FICO_ERR_ARG;
+    const int64_t nc = A * A;
+    int64_t *keys = (int64_t *)malloc(sizeof(int64_t) * (size_t)nc);
+    fico_kc *kc = (fico_kc *)malloc(sizeof(fico_kc) * (size_t)nc);
+    if (!keys || !kc) { free(keys); free(kc); return -FICO_ERR_NOMEM; }
+    fico_entropy_keys(img, N, B, L, -1.0, keys, NULL, NULL);
+    for (int64_t c = 0; c < nc; ++c) { kc[c].key = keys[c]; kc[c].idx = c; }
+    qsort(kc, (size_t)nc, sizeof(fico_kc), fico_kc_cmp);
+    const int64_t n = K < nc ? K : nc;
+    for (int64_t i = 0; i < n; ++i) kept_out[i] = (int32_t)kc[i].idx;
+    qsort(kept_out, (size_t)n, sizeof(int32_t), fico_i32_cmp);
+    free(keys);
+    free(kc);
+    return n;
+}
+
 /* Full quadtree encode: level B_max ranges are all (uB, vB) row-major; the 4 children
  * (TL, TR, BL, BR) of every rejected range form the next level, re-sorted row-major [R16].
  * Records of accepted leaves, level by level (B descending), each level row-major (ry, rx).
  * Shard (shard, n_shards): keep only top-level blocks t with t % n_shards == shard (t = row-major
  * index) and their descendants; n_shards = 1 is the whole image. */
-int fico_encode(const uint8_t *img, int32_t N, int32_t B_max, int32_t B_min, int32_t L,
-                const double *tau, const double *s_flat, const int32_t *n_s,
-                const double *rms_tol, int32_t shard, int32_t n_shards, fico_record *out,
-                int64_t capacity, int64_t *n_out) {
+int fico_encode_sel(const uint8_t *img, int32_t N, int32_t B_max, int32_t B_min, int32_t L,
+                    const double *tau, const int64_t *topk, const double *s_flat, const int32_t *n_s,
+                    const double *rms_tol, int32_t shard, int32_t n_shards, fico_record *out,
+                    int64_t capacity, int64_t *n_out) {
     *n_out = 0;
     if (B_min < 2 || B_max > 32 || B_min > B_max || (B_max & (B_max - 1)) || (B_min & (B_min - 1)))
         return FICO_ERR_ARG;
@@ -338,7 +372,8 @@ int fico_encode(const uint8_t *img, int32_t N, int32_t B_max, int32_t B_min, int
         if (st) break;
         int64_t A = fico_axis_candidates(N, B, L);
         int32_t *kept = (int32_t *)malloc(sizeof(int32_t) * (size_t)(A * A));
-        int64_t n_k = fico_kept_list(img, N, B, L, tau[level], kept);
+        int64_t n_k = topk ? fico_kept_list_topk(img, N, B, L, topk[level], kept)
+                           : fico_kept_list(img, N, B, L, tau[level], kept);
         if (n_k < 1) { free(kept); st = FICO_ERR_EMPTY_POOL; break; }
         fico_record *rec = (fico_record *)malloc(sizeof(fico_record) * (size_t)(n_r ? n_r : 1));
         st = fico_encode_level(img, N, B, L, kept, n_k, ranges, n_r, s, n_s[level], rms_tol[level],
@@ -451,6 +486,15 @@ double fico_psnr(const uint8_t *a, const uint8_t *b, int64_t n) {
     if (sse == 0) return INFINITY;
     const double mse = (double)sse / (double)n;
     return 10.0 * log10(65025.0 / mse);
+}
+
+/* Pool selection per level: entropy threshold tau (keep iff H > tau) [R4]. */
+int fico_encode(const uint8_t *img, int32_t N, int32_t B_max, int32_t B_min, int32_t L,
+                const double *tau, const double *s_flat, const int32_t *n_s,
+                const double *rms_tol, int32_t shard, int32_t n_shards, fico_record *out,
+                int64_t capacity, int64_t *n_out) {
+    return fico_encode_sel(img, N, B_max, B_min, L, tau, NULL, s_flat, n_s, rms_tol, shard, n_shards,
+                           out, capacity, n_out);
 }
 
 int fico_num_threads(void) {

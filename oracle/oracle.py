@@ -55,6 +55,10 @@ def lib():
             L.fico_encode.argtypes = [P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, P, P, P, P,
                                       C.c_int32, C.c_int32, P, C.c_int64, P]
             L.fico_num_threads.restype = C.c_int
+            L.fico_kept_list_topk.argtypes = [P, C.c_int32, C.c_int32, C.c_int32, C.c_int64, P]
+            L.fico_kept_list_topk.restype = C.c_int64
+            L.fico_encode_sel.argtypes = [P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, P, P, P, P, P,
+                                          C.c_int32, C.c_int32, P, C.c_int64, P]
             L.fico_o_value.argtypes = [C.c_int32]
             L.fico_o_value.restype = C.c_double
             L.fico_decode.argtypes = [P, C.c_int64, C.c_int32, P, P, C.c_int32, C.c_int32, C.c_int32, P, P]
@@ -118,6 +122,17 @@ def kept_list(img, B: int, L: int, tau: float) -> np.ndarray:
     return out[:n].copy()
 
 
+def kept_list_topk(img, B: int, L: int, K: int) -> np.ndarray:
+    """Top-K selection (reading R27): K largest entropy keys, ties to the lower index; row-major."""
+    a = _img(img)
+    A = axis_candidates(a.shape[0], B, L)
+    out = np.zeros(max(A * A, 1), np.int32)
+    n = lib().fico_kept_list_topk(_p(a), a.shape[0], B, L, int(K), _p(out))
+    if n < 0:
+        raise RuntimeError(f"fico_kept_list_topk status {-n}")
+    return out[:n].copy()
+
+
 def isometry(X: np.ndarray, k: int) -> np.ndarray:
     X = np.ascontiguousarray(X, dtype=np.int32)
     out = np.zeros_like(X)
@@ -151,10 +166,12 @@ def encode_level(img, B: int, L: int, kept, ranges, s, rms_tol: float, is_min: b
     return out
 
 
-def encode(img, B_max, B_min, L, tau, s_sets, rms_tol, shard=0, n_shards=1):
-    """Full quadtree encode -> records of accepted leaves (B desc, then (ry, rx))."""
+def encode(img, B_max, B_min, L, tau, s_sets, rms_tol, shard=0, n_shards=1, topk=None):
+    """Full quadtree encode -> records of accepted leaves (B desc, then (ry, rx)).
+    topk: per-level pool sizes (reading R27) instead of the entropy thresholds tau."""
     a = _img(img)
     tau = np.ascontiguousarray(tau, dtype=np.float64)
+    tk = None if topk is None else np.ascontiguousarray(topk, dtype=np.int64)
     n_s = np.array([len(x) for x in s_sets], np.int32)
     s_flat = np.ascontiguousarray(np.concatenate([np.asarray(x, np.float64) for x in s_sets]))
     tol = np.ascontiguousarray(rms_tol, dtype=np.float64)
@@ -162,8 +179,8 @@ def encode(img, B_max, B_min, L, tau, s_sets, rms_tol, shard=0, n_shards=1):
     cap = max(1, (N // B_min) ** 2)
     out = np.zeros(cap, RECORD_DTYPE)
     n_out = np.zeros(1, np.int64)
-    st = lib().fico_encode(_p(a), N, B_max, B_min, L, _p(tau), _p(s_flat), _p(n_s), _p(tol),
-                           shard, n_shards, _p(out), cap, _p(n_out))
+    st = lib().fico_encode_sel(_p(a), N, B_max, B_min, L, _p(tau), None if tk is None else _p(tk),
+                               _p(s_flat), _p(n_s), _p(tol), shard, n_shards, _p(out), cap, _p(n_out))
     if st:
         raise RuntimeError(f"fico_encode status {st}")
     return out[: int(n_out[0])].copy()
@@ -174,7 +191,7 @@ def encode_cfg(cfg, img=None, shard=0, n_shards=1):
     if img is None:
         img = image_for(cfg)
     return encode(img, cfg["B_max"], cfg["B_min"], cfg["L"], cfg["tau"], cfg["s"],
-                  cfg["rms_tol"], shard, n_shards)
+                  cfg["rms_tol"], shard, n_shards, cfg.get("topk"))
 
 
 def o_value(code: int) -> float:

@@ -99,7 +99,7 @@ void free_buf(Buf &b) {
 void free_pool(Pool &P) {
     free_buf(P.b_keys); free_buf(P.b_keep); free_buf(P.b_kept); free_buf(P.b_Dt);
     free_buf(P.b_SDf); free_buf(P.b_SD); free_buf(P.b_C); free_buf(P.b_misc); free_buf(P.b_Dc);
-    free_buf(P.b_Dtc); free_buf(P.b_F2); free_buf(P.b_blocksum);
+    free_buf(P.b_Dtc); free_buf(P.b_F2); free_buf(P.b_blocksum); free_buf(P.b_topk);
 }
 
 bool pow2(int32_t v) { return v > 0 && (v & (v - 1)) == 0; }
@@ -127,7 +127,7 @@ int64_t entropy_threshold(double tau, int32_t m) {
 
 // ------------------------------------------------------------------------- pool building
 fic_status pool_enqueue(fic_ctx *ctx, Pool &P, const uint8_t *img, int32_t N, int32_t B,
-                        int32_t L, double tau, cudaStream_t st) {
+                        int32_t L, double tau, int64_t topk, cudaStream_t st) {
     P.device = ctx->device;
     P.N = N; P.B = B; P.L = L; P.n = B * B;
     P.A = (N - 2 * B) / L + 1;
@@ -164,6 +164,11 @@ fic_status pool_enqueue(fic_ctx *ctx, Pool &P, const uint8_t *img, int32_t N, in
     const int64_t T = use_tau ? entropy_threshold(tau, m) : 0;
     CK(fic::launch_entropy_keys(img, N, B, L, P.A, ctx->d_delta, ctx->lut[m], T, use_tau, P.keys,
                                 P.keep, st));
+    if (topk > 0) {  // pool size K instead of the threshold (reading R27)
+        CK(grow(ctx, P.b_topk, fic::topk_scratch_bytes(P.n_c)));
+        CK(fic::launch_topk_select(P.keys, P.n_c, topk, P.b_topk.p, P.keep, st));
+        ctx->launches += 2;
+    }
     CK(fic::launch_select_index(P.keep, P.n_c, ptr<int64_t>(P.b_blocksum), P.kept, &P.d_misc[0], st));
     if (P.mode == 2)
         CK(fic::launch_pool_gather(img, N, B, L, P.A, P.kept, &P.d_misc[0], tiles_max, P.Dt, st));
@@ -489,15 +494,15 @@ fic_status fic_get_stats(const fic_ctx *ctx, fic_level_stats *h_out, int32_t max
     return FIC_OK;
 }
 
-fic_status fic_build_domain_pool(fic_ctx *ctx, const uint8_t *img, int32_t N, int32_t B, int32_t L,
-                                 double tau_nats, fic_pool **out) {
+static fic_status build_pool(fic_ctx *ctx, const uint8_t *img, int32_t N, int32_t B, int32_t L, double tau_nats,
+                             int64_t topk, fic_pool **out) {
     CKS(ctx_check(ctx));
     if (!img || !out) return fail(ctx, FIC_ERR_ARG, "null argument");
     *out = nullptr;
     CKS(check_level(ctx, N, B, L));
     fic_pool *pool = new (std::nothrow) fic_pool();
     if (!pool) return fail(ctx, FIC_ERR_NOMEM, "host allocation failed");
-    fic_status st = pool_enqueue(ctx, pool->P, img, N, B, L, tau_nats, ctx->stream);
+    fic_status st = pool_enqueue(ctx, pool->P, img, N, B, L, tau_nats, topk, ctx->stream);
     if (st == FIC_OK) {
         cudaError_t e = cudaMemcpyAsync(ctx->h_counts, pool->P.d_misc, 3 * sizeof(unsigned long long),
                                         cudaMemcpyDeviceToHost, ctx->stream);
@@ -513,6 +518,20 @@ fic_status fic_build_domain_pool(fic_ctx *ctx, const uint8_t *img, int32_t N, in
     *out = pool;
     if (pool->P.n_k == 0) return fail(ctx, FIC_ERR_EMPTY_POOL, "no domain block passed the entropy filter");
     return FIC_OK;
+}
+
+fic_status fic_build_domain_pool(fic_ctx *ctx, const uint8_t *img, int32_t N, int32_t B, int32_t L,
+                                 double tau_nats, fic_pool **out) {
+    return build_pool(ctx, img, N, B, L, tau_nats, 0, out);
+}
+
+fic_status fic_build_domain_pool_topk(fic_ctx *ctx, const uint8_t *img, int32_t N, int32_t B, int32_t L,
+                                      int64_t K, fic_pool **out) {
+    if (K < 1) {
+        if (out) *out = nullptr;
+        return ctx ? fail(ctx, FIC_ERR_ARG, "pool size K must be >= 1") : FIC_ERR_ARG;
+    }
+    return build_pool(ctx, img, N, B, L, -1.0, K, out);
 }
 
 fic_status fic_pool_info(const fic_pool *pool, int64_t *h_n_candidates, int64_t *h_n_kept,
@@ -570,13 +589,13 @@ fic_status fic_encode_level(fic_ctx *ctx, const uint8_t *img, int32_t N, const f
 //   [0] running output total  [1] level accepted count  [2] next-level range count (scratch)
 //   [8 + l] exact evaluations of level l   [16 + l] accepted at level l   [24..] error flag (int)
 //   [32 + l] range count of level l
-fic_status fic_encode(fic_ctx *ctx, const uint8_t *img, int32_t N, int32_t B_max, int32_t B_min,
-                      int32_t L, const double *h_tau, const double *h_s, const int32_t *h_n_s,
-                      const double *h_rms_tol, int32_t shard, int32_t n_shards, fic_record *out,
-                      int64_t capacity, int64_t *h_n_out) {
+static fic_status encode_impl(fic_ctx *ctx, const uint8_t *img, int32_t N, int32_t B_max, int32_t B_min,
+                              int32_t L, const double *h_tau, const int64_t *h_topk, const double *h_s,
+                              const int32_t *h_n_s, const double *h_rms_tol, int32_t shard, int32_t n_shards,
+                              fic_record *out, int64_t capacity, int64_t *h_n_out) {
     CKS(ctx_check(ctx));
     if (h_n_out) *h_n_out = 0;
-    if (!img || !h_tau || !h_s || !h_n_s || !h_rms_tol || !h_n_out || (!out && capacity > 0) ||
+    if (!img || !(h_tau || h_topk) || !h_s || !h_n_s || !h_rms_tol || !h_n_out || (!out && capacity > 0) ||
         capacity < 0)
         return fail(ctx, FIC_ERR_ARG, "null argument");
     if (!pow2(B_max) || !pow2(B_min) || B_min < 2 || B_min > B_max)
@@ -614,7 +633,8 @@ fic_status fic_encode(fic_ctx *ctx, const uint8_t *img, int32_t N, int32_t B_max
         cudaStream_t ps = (l == 0 || !ctx->overlap_pools) ? st : ctx->side;
         ctx->launches = 0;
         if (ctx->timing) CK(cudaEventRecord(ctx->ev[l][0], ps));
-        CKS(pool_enqueue(ctx, ctx->levels[l], img, N, B_max >> l, L, h_tau[l], ps));
+        CKS(pool_enqueue(ctx, ctx->levels[l], img, N, B_max >> l, L, h_topk ? -1.0 : h_tau[l],
+                         h_topk ? h_topk[l] : 0, ps));
         if (ctx->timing) CK(cudaEventRecord(ctx->ev[l][4], ps));
         if (l > 0) CK(cudaEventRecord(ctx->pool_ready[l], ps));
         ctx->stats[l].kernel_launches = ctx->launches;
@@ -704,6 +724,30 @@ fic_status fic_encode(fic_ctx *ctx, const uint8_t *img, int32_t N, int32_t B_max
     *h_n_out = total;
     if (total > capacity) return fail(ctx, FIC_ERR_CAPACITY, "output capacity too small");
     return FIC_OK;
+}
+
+fic_status fic_encode(fic_ctx *ctx, const uint8_t *img, int32_t N, int32_t B_max, int32_t B_min, int32_t L,
+                      const double *h_tau, const double *h_s, const int32_t *h_n_s, const double *h_rms_tol,
+                      int32_t shard, int32_t n_shards, fic_record *out, int64_t capacity, int64_t *h_n_out) {
+    return encode_impl(ctx, img, N, B_max, B_min, L, h_tau, nullptr, h_s, h_n_s, h_rms_tol, shard, n_shards, out,
+                       capacity, h_n_out);
+}
+
+fic_status fic_encode_topk(fic_ctx *ctx, const uint8_t *img, int32_t N, int32_t B_max, int32_t B_min, int32_t L,
+                           const int64_t *h_K, const double *h_s, const int32_t *h_n_s, const double *h_rms_tol,
+                           int32_t shard, int32_t n_shards, fic_record *out, int64_t capacity,
+                           int64_t *h_n_out) {
+    if (h_K) {
+        int nl = 0;
+        for (int32_t B = B_max; B >= B_min && B > 0 && nl < 64; B /= 2) ++nl;
+        for (int l = 0; l < nl; ++l)
+            if (h_K[l] < 1) {
+                if (h_n_out) *h_n_out = 0;
+                return ctx ? fail(ctx, FIC_ERR_ARG, "pool size K must be >= 1") : FIC_ERR_ARG;
+            }
+    }
+    return encode_impl(ctx, img, N, B_max, B_min, L, nullptr, h_K, h_s, h_n_s, h_rms_tol, shard, n_shards, out,
+                       capacity, h_n_out);
 }
 
 fic_status fic_encode_host(fic_ctx *ctx, const uint8_t *h_img, int32_t N, int32_t B_max,

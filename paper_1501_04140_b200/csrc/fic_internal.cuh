@@ -51,7 +51,7 @@ struct Pool {
     int64_t *C = nullptr;
     unsigned long long *d_misc = nullptr;  // [0] = n_kept, [1] = Cmax, [2] = max |dh|_2 (float bits)
     double dnmax = 0.0;
-    Buf b_keys, b_keep, b_kept, b_Dt, b_SDf, b_SD, b_C, b_misc, b_Dc, b_Dtc, b_F2, b_blocksum;
+    Buf b_keys, b_keep, b_kept, b_Dt, b_SDf, b_SD, b_C, b_misc, b_Dc, b_Dtc, b_F2, b_blocksum, b_topk;
     int device = 0;
 };
 
@@ -140,6 +140,10 @@ __device__ __forceinline__ bool cta_work(int n_r, int rpc, int n_tiles, int min_
 cudaError_t launch_entropy_keys(const uint8_t *img, int32_t N, int32_t B, int32_t L, int32_t A,
                                 const int64_t *d_delta, int64_t lut_m, int64_t T, int use_tau,
                                 int64_t *keys, uint8_t *keep, cudaStream_t st);
+// top-K pool selection (reading R27): keep[c] = 1 for the K largest keys (ties: lower index)
+size_t topk_scratch_bytes(int64_t n_c);
+cudaError_t launch_topk_select(const int64_t *keys, int64_t n_c, int64_t K, void *scratch, uint8_t *keep,
+                               cudaStream_t st);
 // order-preserving compaction of u8 flags: writes indices and *d_total
 cudaError_t launch_select_index(const uint8_t *flags, int64_t n, int64_t *blocksum, int32_t *out,
                                 unsigned long long *d_total, cudaStream_t st);

@@ -9,6 +9,8 @@
 #include <cfloat>
 #include <cstdio>
 
+#include <cub/device/device_radix_sort.cuh>
+
 #include "fic_internal.cuh"
 
 namespace fic {
@@ -401,6 +403,59 @@ cudaError_t launch_merge_shards(const fic_record *in, const int64_t *d_counts, i
     if (max_count == 0) return cudaSuccess;
     dim3 grid((unsigned)((max_count + 255) / 256), (unsigned)n_shards);
     merge_shards_kernel<<<grid, 256, 0, st>>>(in, d_counts, n_shards, stride, out);
+    return cudaGetLastError();
+}
+
+// ----------------------------------------------------------------------------- top-K selection
+// The paper's "pool size" (Tables 1-2, Fig. 4; reading R27): keep the K candidates
+// with the largest entropy keys, ties to the lower row-major index.  A stable descending radix
+// sort of (key, index) pairs (CUB; equal keys keep ascending index order) ranks them; the first
+// K indices are flagged and the usual order-preserving compaction builds the row-major kept list.
+__global__ void iota_kernel(int32_t *__restrict__ v, int64_t n) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) v[i] = (int32_t)i;
+}
+__global__ void topk_flag_kernel(const int32_t *__restrict__ order, int64_t n, int64_t K, uint8_t *__restrict__ keep) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) keep[order[i]] = (uint8_t)(i < K);
+}
+
+struct TopkLayout {
+    size_t kout, vin, vout, tmp, tmp_bytes, total;
+};
+static TopkLayout topk_layout(int64_t n) {
+    auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+    TopkLayout L;
+    size_t o = 0;
+    L.kout = o; o += al(sizeof(int64_t) * n);
+    L.vin = o; o += al(sizeof(int32_t) * n);
+    L.vout = o; o += al(sizeof(int32_t) * n);
+    L.tmp_bytes = 0;
+    cub::DeviceRadixSort::SortPairsDescending(nullptr, L.tmp_bytes, (const int64_t *)nullptr, (int64_t *)nullptr,
+                                              (const int32_t *)nullptr, (int32_t *)nullptr, (int)n, 0, 50);
+    L.tmp = o; o += al(L.tmp_bytes);
+    L.total = o;
+    return L;
+}
+
+size_t topk_scratch_bytes(int64_t n_c) { return topk_layout(n_c).total; }
+
+cudaError_t launch_topk_select(const int64_t *keys, int64_t n_c, int64_t K, void *scratch, uint8_t *keep,
+                               cudaStream_t st) {
+    if (n_c == 0) return cudaSuccess;
+    const TopkLayout Ly = topk_layout(n_c);
+    char *b = static_cast<char *>(scratch);
+    int64_t *kout = reinterpret_cast<int64_t *>(b + Ly.kout);
+    int32_t *vin = reinterpret_cast<int32_t *>(b + Ly.vin), *vout = reinterpret_cast<int32_t *>(b + Ly.vout);
+    const unsigned g = (unsigned)((n_c + 255) / 256);
+    iota_kernel<<<g, 256, 0, st>>>(vin, n_c);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    size_t tb = Ly.tmp_bytes;
+    // keys = lut[m] - sum lut[h] >= 0 and < 2^50 for m <= 4096 (lut[4096] < 2^48)
+    e = cub::DeviceRadixSort::SortPairsDescending(b + Ly.tmp, tb, keys, kout, vin, vout, (int)n_c, 0, 50, st);
+    if (e != cudaSuccess) return e;
+    topk_flag_kernel<<<g, 256, 0, st>>>(vout, n_c, K, keep);
     return cudaGetLastError();
 }
 

@@ -30,7 +30,8 @@ EXPORTS = (
     "fic_ctx_create", "fic_ctx_set_stream", "fic_ctx_destroy", "fic_last_error",
     "fic_ctx_set_timing", "fic_get_stats", "fic_build_domain_pool", "fic_pool_info",
     "fic_pool_destroy", "fic_encode_level", "fic_encode", "fic_encode_host", "fic_merge_shards",
-    "fic_entropy_lut", "fic_version", "fic_decode", "fic_psnr",
+    "fic_entropy_lut", "fic_version", "fic_decode", "fic_psnr", "fic_build_domain_pool_topk",
+    "fic_encode_topk",
 )
 
 
@@ -75,6 +76,8 @@ def load(path: str = SO_PATH):
         "fic_merge_shards": ([P, P, P, i32, i64, P], C.c_int),
         "fic_entropy_lut": ([P, i32], C.c_int),
         "fic_decode": ([P, P, i64, i32, i32, i32, P, P, i32, P, P], C.c_int),
+        "fic_build_domain_pool_topk": ([P, P, i32, i32, i32, i64, P], C.c_int),
+        "fic_encode_topk": ([P, P, i32, i32, i32, i32, P, P, P, P, i32, i32, P, i64, P], C.c_int),
         "fic_psnr": ([P, P, P, i64, P], C.c_int),
         "fic_version": ([], C.c_char_p),
     }
@@ -204,10 +207,15 @@ class Context:
             pass
 
     # -- API
-    def build_domain_pool(self, img, B: int, L: int, tau: float) -> Pool:
+    def build_domain_pool(self, img, B: int, L: int, tau: float = -1.0, topk: int | None = None) -> Pool:
+        """Entropy-threshold pool (keep iff H > tau), or the K highest-entropy blocks (topk)."""
         h = C.c_void_p()
-        st = self.lib.fic_build_domain_pool(self.handle, _dptr(img), img.shape[0], B, L,
-                                            float(tau), C.byref(h))
+        if topk is not None:
+            st = self.lib.fic_build_domain_pool_topk(self.handle, _dptr(img), img.shape[0], B, L,
+                                                     int(topk), C.byref(h))
+        else:
+            st = self.lib.fic_build_domain_pool(self.handle, _dptr(img), img.shape[0], B, L,
+                                                float(tau), C.byref(h))
         pool = Pool(self, h, B, L, img.shape[0]) if h.value else None
         self._check(st, "fic_build_domain_pool")  # FIC_ERR_EMPTY_POOL raises; pool is freed by GC
         return pool
@@ -234,8 +242,9 @@ class Context:
         return tau, n_s, s_flat, tol
 
     def encode(self, img, B_max: int, B_min: int, L: int, tau, s_sets, rms_tol, shard: int = 0,
-               n_shards: int = 1, out=None):
-        """Full quadtree encode of a CUDA uint8 [N, N] image -> CUDA uint8 [n, 40] records."""
+               n_shards: int = 1, out=None, topk=None):
+        """Full quadtree encode of a CUDA uint8 [N, N] image -> CUDA uint8 [n, 40] records.
+        topk: per-level pool sizes (fic_encode_topk) instead of the entropy thresholds tau."""
         import torch
         N = img.shape[0]
         tau, n_s, s_flat, tol = self._cfg_arrays(tau, s_sets, rms_tol)
@@ -243,9 +252,15 @@ class Context:
         if out is None or out.shape[0] < cap:
             out = torch.empty((cap, RECORD_BYTES), dtype=torch.uint8, device=img.device)
         n_out = C.c_int64()
-        self._check(self.lib.fic_encode(self.handle, _dptr(img), N, B_max, B_min, L, _ptr(tau),
-                                        _ptr(s_flat), _ptr(n_s), _ptr(tol), shard, n_shards,
-                                        _dptr(out), out.shape[0], C.byref(n_out)), "fic_encode")
+        if topk is not None:
+            K = np.ascontiguousarray(topk, dtype=np.int64)
+            self._check(self.lib.fic_encode_topk(self.handle, _dptr(img), N, B_max, B_min, L, _ptr(K),
+                                                 _ptr(s_flat), _ptr(n_s), _ptr(tol), shard, n_shards,
+                                                 _dptr(out), out.shape[0], C.byref(n_out)), "fic_encode_topk")
+        else:
+            self._check(self.lib.fic_encode(self.handle, _dptr(img), N, B_max, B_min, L, _ptr(tau),
+                                            _ptr(s_flat), _ptr(n_s), _ptr(tol), shard, n_shards,
+                                            _dptr(out), out.shape[0], C.byref(n_out)), "fic_encode")
         return out[: n_out.value]
 
     def encode_host(self, img: np.ndarray, B_max: int, B_min: int, L: int, tau, s_sets, rms_tol,
@@ -265,6 +280,7 @@ class Context:
         return out[: n_out.value]
 
     def encode_cfg(self, cfg, img, **kw):
+        kw.setdefault("topk", cfg.get("topk"))
         return self.encode(img, cfg["B_max"], cfg["B_min"], cfg["L"], cfg["tau"], cfg["s"],
                            cfg["rms_tol"], **kw)
 

@@ -222,6 +222,12 @@ def test_errors(fic):
 
 
 # ------------------------------------------------------------------ full-size, sampled checks
+def kept_for(img, cfg, li, B):
+    if cfg.get("topk"):
+        return oracle.kept_list_topk(img, B, cfg["L"], cfg["topk"][li])
+    return oracle.kept_list(img, B, cfg["L"], cfg["tau"][li])
+
+
 def sampled_level_check(fic, img, cfg, got, per_level=24, seed=0, parents=8):
     """Sampled records of a GPU encode re-derived one by one by the oracle at their level, plus
     sampled parents re-derived as rejected; leaves tile the image."""
@@ -235,7 +241,7 @@ def sampled_level_check(fic, img, cfg, got, per_level=24, seed=0, parents=8):
         sel = got[got["B"] == B]
         if len(sel) == 0:
             continue
-        kept = oracle.kept_list(img, B, cfg["L"], cfg["tau"][li])
+        kept = kept_for(img, cfg, li, B)
         idx = sample_indices(len(sel), per_level, seed + li)
         ranges = np.stack([sel["rx"][idx], sel["ry"][idx]], 1).astype(np.int32)
         ref = oracle.encode_level(img, B, cfg["L"], kept, ranges, cfg["s"][li], cfg["rms_tol"][li],
@@ -243,7 +249,7 @@ def sampled_level_check(fic, img, cfg, got, per_level=24, seed=0, parents=8):
         assert_same(sel[idx], ref, f"sampled level B={B}")
         if li > 0 and parents:
             P = 2 * B
-            pk = oracle.kept_list(img, P, cfg["L"], cfg["tau"][li - 1])
+            pk = kept_for(img, cfg, li - 1, P)
             pi = sample_indices(len(sel), parents, seed + 100 + li)
             par = np.unique(np.stack([(sel["rx"][pi] // P) * P, (sel["ry"][pi] // P) * P], 1), axis=0)
             pref = oracle.encode_level(img, P, cfg["L"], pk, par.astype(np.int32), cfg["s"][li - 1],
@@ -345,3 +351,46 @@ def test_b32_and_bad_args(fic):
     assert ei.value.status == 1
     with pytest.raises(p.FicError):
         ctx.encode(img, 16, 2, 2, [-1] * 4, [(0.5,)] * 4, [8.0] * 4, shard=3, n_shards=2)
+
+
+# ------------------------------------------------------------------ top-K pools (NEXT-1, R27)
+@pytest.mark.parametrize("N,B,L,K", [(64, 4, 2, 100), (96, 8, 3, 37), (128, 2, 2, 1000), (64, 16, 4, 5),
+                                     (80, 4, 1, 10 ** 6)])
+def test_topk_pool_parity(fic, N, B, L, K):
+    p, ctx, torch = fic
+    img = make_image(N, N + K % 97)
+    pool = ctx.build_domain_pool(dev(torch, img), B, L, topk=K)
+    info = pool.info()
+    want = oracle.kept_list_topk(img, B, L, K)
+    assert np.array_equal(info["kept"].cpu().numpy(), want)
+    keep = np.zeros(info["n_candidates"], np.uint8)
+    keep[want] = 1
+    assert np.array_equal(info["keep"].cpu().numpy(), keep)
+
+
+def test_topk_ties_and_errors(fic):
+    p, ctx, torch = fic
+    img = constant_image(64, 77)  # every entropy key is 0: the K lowest indices
+    pool = ctx.build_domain_pool(dev(torch, img), 4, 2, topk=9)
+    assert np.array_equal(pool.info()["kept"].cpu().numpy(), np.arange(9))
+    with pytest.raises(p.FicError) as ei:
+        ctx.build_domain_pool(dev(torch, img), 4, 2, topk=0)
+    assert ei.value.status == 1
+
+
+@pytest.mark.parametrize("name,K,smode", [("C2", [256, 256, 256, 256], "predefined"),
+                                          ("C2", [32, 64, 256, 512], "grid"),
+                                          ("C2", [64, 64, 64, 64], "sampled10")])
+def test_encode_topk_parity(fic, name, K, smode):
+    p, ctx, torch = fic
+    cfg = config(name, s_mode=smode, topk=K)
+    img = image_for(cfg)
+    got = p.records_to_numpy(ctx.encode_cfg(cfg, dev(torch, img)))
+    assert_same(got, oracle.encode_cfg(cfg, img), f"{name} top-{K} {smode}")
+
+
+def test_c3_topk_sampled(fic):
+    p, ctx, torch = fic
+    cfg = config("C3", topk=256)  # the paper's Table 1-2 pool size 256 at the paper's image size
+    img, got = encode_both(fic, cfg)
+    sampled_level_check(fic, img, cfg, got, per_level=40, parents=4)
