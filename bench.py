@@ -43,7 +43,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["fic", "reference"], default="fic")
     ap.add_argument("--config", default="C3")
-    ap.add_argument("--s-mode", default="predefined", choices=["predefined", "grid", "sampled10"])
+    ap.add_argument("--s-mode", default="predefined", choices=["predefined", "grid", "sampled10", "closed5"])
     ap.add_argument("--topk", type=int, default=0,
                     help="pool size K per level (the paper's Tables 1-2 axis) instead of the entropy tau")
     ap.add_argument("--t", type=float, default=8.0)

@@ -20,6 +20,10 @@ GRID_S = tuple(j / 15.0 for j in range(16))
 # SPEC.md sampled10 (NEXT-4): the paper's 10-member baseline set "sampled from [0,1]",
 # read as ten uniform mid-point samples
 SAMPLED10_S = tuple((2 * j + 1) / 20.0 for j in range(10))
+# NEXT-2: Eq. 2 closed-form s, clamped to [0, 1] (R12) and stored in 5 bits:
+# e(s) is a parabola in s, so the nearest of the 32 levels j/31 to s* minimises e over them --
+# the mode is the exhaustive search over these levels (reading R28)
+CLOSED5_S = tuple(j / 31.0 for j in range(32))
 
 _TAU_PATH = os.path.join(os.path.dirname(__file__), "tau.json")
 
@@ -52,6 +56,8 @@ def s_sets(B_max: int, B_min: int, mode: str):
             res.append(GRID_S)
         elif mode == "sampled10":
             res.append(SAMPLED10_S)
+        elif mode == "closed5":
+            res.append(CLOSED5_S)
         else:
             raise ValueError(mode)
     return res

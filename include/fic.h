@@ -110,7 +110,7 @@ fic_status fic_pool_destroy(fic_pool *pool);
 
 /* Match every range of `ranges` (device int32 [n_r][2] = (rx, ry), each a multiple of the
  * pool's B) against every kept domain x 8 isometries x every s of h_s (host double [n_s],
- * each in [0,1]; 1 <= n_s <= 16), scoring Eq. 1 with o from Eq. 3, and write the
+ * each in [0,1]; 1 <= n_s <= 32), scoring Eq. 1 with o from Eq. 3, and write the
  * lexicographically first minimiser (E; dom, iso, s_idx) of each range to out[r] (device
  * fic_record [n_r]).  accepted = is_min_level || E <= rms_tol^2 * B^2.
  * Stream-asynchronous.  Errors: ARG, SHAPE, EMPTY_POOL, CUDA. */

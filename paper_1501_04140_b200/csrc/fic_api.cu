@@ -209,7 +209,7 @@ fic_status check_level(fic_ctx *ctx, int32_t N, int32_t B, int32_t L) {
 
 fic_status check_s(fic_ctx *ctx, const double *h_s, int32_t n_s) {
     if (!h_s || n_s < 1 || n_s > fic::kMaxS)
-        return fail(ctx, FIC_ERR_ARG, "need 1 <= n_s <= 16 contrast values");
+        return fail(ctx, FIC_ERR_ARG, "need 1 <= n_s <= 32 contrast values");
     for (int j = 0; j < n_s; ++j)
         if (!(h_s[j] >= 0.0 && h_s[j] <= 1.0))
             return fail(ctx, FIC_ERR_ARG, "contrast values s must lie in [0,1]");
@@ -279,7 +279,10 @@ fic_status level_enqueue(fic_ctx *ctx, const Pool &P, const uint8_t *img, const 
     fic::SList sl;
     memcpy(sl.s, sp.spos, sizeof sl.s);
     if (P.mode == 2 || P.mode == 0) {
-        CK(fic::launch_t2f(P.C, &P.d_misc[0], slots, sl, sp.nsp, ptr<float>(ctx->b_t2f), st));
+        if (P.mode == 2 && sp.nsp > 16)
+            return fail(ctx, FIC_ERR_ARG, "FIC_SEARCH=direct supports at most 16 contrast values > 0");
+        CK(fic::launch_t2f(P.C, &P.d_misc[0], slots, sl, sp.nsp, ptr<float>(ctx->b_t2f),
+                           (P.mode == 0 && sp.nsp > 2) ? 1 : 0, st));
         if (sp.nsp > 0 && slots > 0) ctx->launches += 1;
         if (ctx->timing) CK(cudaEventRecord(ctx->ev[level_slot][1], st));
         if (sp.nsp > 0) {
@@ -305,6 +308,7 @@ fic_status level_enqueue(fic_ctx *ctx, const Pool &P, const uint8_t *img, const 
         CK(grow(ctx, ctx->b_meta, fic::fourier_meta_bytes() * (size_t)n_r_max));
         CK(grow(ctx, ctx->b_u, sizeof(float) * (size_t)slots * (sp.nsp ? sp.nsp : 1)));
         if (ctx->timing) CK(cudaEventRecord(ctx->ev[level_slot][1], st));
+        if (sp.nsp > 16) return fail(ctx, FIC_ERR_ARG, "FIC_SEARCH=fourier supports at most 16 contrast values > 0");
         CK(fic::launch_fourier_level(P.B, sp, P.Dc, ptr<float>(ctx->b_rc), r_stride, ctx->b_meta.p,
                                      ptr<float>(ctx->b_u), st));
         ctx->launches += 1 + (sp.nsp > 0 ? 2 : 0);

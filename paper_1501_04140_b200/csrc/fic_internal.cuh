@@ -17,7 +17,7 @@
 namespace fic {
 
 constexpr int kTileD = 128;  // domains per pool tile
-constexpr int kMaxS = 16;    // s values per level
+constexpr int kMaxS = 32;    // s values per level (5-bit closed-form levels)
 constexpr int kMaxLevels = 8;
 // Partial.kj flag: s index final, isometry k* not yet evaluated (finalize computes it for the
 // winning domain; the B = 2 search defers it because the same domain never competes twice)
@@ -170,7 +170,7 @@ struct SList {
     double s[kMaxS];
 };
 cudaError_t launch_t2f(const int64_t *C, const unsigned long long *d_nk, int64_t n_slots, const SList &spos,
-                       int32_t nsp, float *t2f, cudaStream_t st);
+                       int32_t nsp, float *t2f, int32_t univ, cudaStream_t st);
 cudaError_t launch_search(int32_t B, int32_t nsp, const SearchParams &p, cudaStream_t st);
 cudaError_t launch_finalize(const FinalizeParams &p, cudaStream_t st);
 cudaError_t launch_merge_shards(const fic_record *in, const int64_t *d_counts, int32_t n_shards,

@@ -346,12 +346,17 @@ cudaError_t launch_pool_moments(const uint8_t *img, int32_t N, int32_t B, int32_
 }
 
 // t2f[j][d] = fp32 of (s_j s_j)(C/16) for s_j > 0; +inf for pad slots (never admitted).
+// univ (large s sets, the s-independent filter): t2f[0][d] = RN(1/C) (0 if C = 0), NaN on pads.
 __global__ void t2f_kernel(const int64_t *__restrict__ C, const unsigned long long *__restrict__ d_nk,
-                           int64_t n_slots, const SList spos, int32_t nsp, float *__restrict__ t2f) {
+                           int64_t n_slots, const SList spos, int32_t nsp, float *__restrict__ t2f, int32_t univ) {
     const int64_t d = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (d >= n_slots) return;
     const int64_t n_k = (int64_t)*d_nk;
     if (d >= ((n_k + kTileD - 1) / kTileD) * kTileD) return;
+    if (univ) {
+        t2f[d] = d < n_k ? (C[d] > 0 ? __double2float_rn(1.0 / (double)C[d]) : 0.f) : __int_as_float(0x7fc00000);
+        return;
+    }
     const double c16 = __dmul_rn(0.0625, (double)C[d]);
     for (int j = 0; j < nsp; ++j) {
         const double s = spos.s[j];
@@ -360,9 +365,9 @@ __global__ void t2f_kernel(const int64_t *__restrict__ C, const unsigned long lo
 }
 
 cudaError_t launch_t2f(const int64_t *C, const unsigned long long *d_nk, int64_t n_slots, const SList &spos,
-                       int32_t nsp, float *t2f, cudaStream_t st) {
+                       int32_t nsp, float *t2f, int32_t univ, cudaStream_t st) {
     if (n_slots == 0 || nsp == 0) return cudaSuccess;
-    t2f_kernel<<<(unsigned)((n_slots + 255) / 256), 256, 0, st>>>(C, d_nk, n_slots, spos, nsp, t2f);
+    t2f_kernel<<<(unsigned)((n_slots + 255) / 256), 256, 0, st>>>(C, d_nk, n_slots, spos, nsp, t2f, univ);
     return cudaGetLastError();
 }
 

@@ -282,7 +282,7 @@ template <int B>
 __global__ void tc_range_meta_kernel(const uint8_t *__restrict__ img, int32_t N, const int2 *__restrict__ ranges,
                                      const unsigned long long *__restrict__ d_nr, int32_t n_pad, double smax,
                                      const unsigned long long *__restrict__ d_misc,
-                                     TCRangeG *__restrict__ meta) {
+                                     TCRangeG *__restrict__ meta, int32_t univ) {
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= n_pad) return;
     const int n_r = (int)*d_nr;
@@ -315,6 +315,8 @@ __global__ void tc_range_meta_kernel(const uint8_t *__restrict__ img, int32_t N,
     // <= 64 at B = 8 (floor of Bq / 2 and Bq / 64): hs * 64 covers both
     R.margin = 8.0 * u * (hs * bq + t2m) + 1e-12 * (R.A + hs * bq + t2m) + (B == 4 || B == 8 ? hs * 64.0 : 0.0) +
                1e-30;
+    // s-independent filter (NSP = 0): Bq rounded once, squared, times RN(1/C): <= 4.04u Bq^2/C <= 4.04u A
+    if (univ) R.margin = 4.1 * u * R.A + 1e-12 * R.A + 1e-30;
     meta[r] = R;
 }
 
@@ -346,6 +348,11 @@ struct TCParams {
 
 using TCRange = TCRangeG;
 
+// NSP = number of s > 0 filtered one by one (1 or 2, the predefined sets); NSP = 0: any larger
+// set (grid, sampled10, 5-bit closed form) through the s-independent lower bound
+//     min_s e_s >= A - Bq^2 / C        (the unconstrained minimum of the parabola, Eq. 2)
+// evaluated as g = -(Bq Bq) u, u = RN(1/C) per domain (t2f row 0), with Bq converted exactly
+// (int -> float RN) -- margin 4.1u A (tc_range_meta_kernel).
 template <int B, int NSP>
 __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __grid_constant__ TCParams P) {
     using Cf = TCfg<B>;
@@ -454,9 +461,10 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
         const int eg = (warp - 2) >> 2;   // epilogue warpgroup
         const int lq = warp & 3;          // TMEM lane quarter accessible by this warp
         const int m = lq * 32 + lane;     // domain lane within the tile
-        float nhs[NSP];
+        constexpr int NT = NSP ? NSP : 1;  // t2 values per domain (u = 1/C for NSP = 0)
+        float nhs[NT];
 #pragma unroll
-        for (int jj = 0; jj < NSP; ++jj) nhs[jj] = sHsn[jj];
+        for (int jj = 0; jj < NT; ++jj) nhs[jj] = sHsn[jj];
         for (int q = 0; q < HALF; ++q) {
             Partial pb;
             if (P.has_zero) { pb.e = sR[eg * HALF + q].A; pb.d = 0; pb.kj = P.j_zero; }
@@ -470,27 +478,28 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
         int qn = 0;
         const int qbase = (threadIdx.x - 64) * 4;
         int32_t sd_n = 0;
-        float t2_n[NSP];
+        float t2_n[NT];
         {
             const int d = t0 * kTileD + m;
             if (ntl > 0) {
                 sd_n = P.SD[d];
 #pragma unroll
-                for (int jj = 0; jj < NSP; ++jj) t2_n[jj] = jj < P.nsp ? P.t2f[(int64_t)jj * P.n_slots + d] : INFINITY;
+                for (int jj = 0; jj < NT; ++jj)
+                    t2_n[jj] = (NSP == 0 || jj < P.nsp) ? P.t2f[(int64_t)jj * P.n_slots + d] : INFINITY;
             }
         }
         for (int tl = 0; tl < ntl; ++tl) {
             const int buf = tl & 1;
             const int d = (t0 + tl) * kTileD + m;
             const int32_t sd = sd_n;
-            float t2[NSP];
+            float t2[NT];
 #pragma unroll
-            for (int jj = 0; jj < NSP; ++jj) t2[jj] = t2_n[jj];
+            for (int jj = 0; jj < NT; ++jj) t2[jj] = t2_n[jj];
             if (tl + 1 < ntl) {  // prefetch the next tile's per-domain data
                 sd_n = P.SD[d + kTileD];
 #pragma unroll
-                for (int jj = 0; jj < NSP; ++jj)
-                    t2_n[jj] = jj < P.nsp ? P.t2f[(int64_t)jj * P.n_slots + d + kTileD] : INFINITY;
+                for (int jj = 0; jj < NT; ++jj)
+                    t2_n[jj] = (NSP == 0 || jj < P.nsp) ? P.t2f[(int64_t)jj * P.n_slots + d + kTileD] : INFINITY;
             }
             tmbar_wait(&tfull[buf], (uint32_t)((tl >> 1) & 1));
             tc_fence_after();
@@ -517,7 +526,10 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
                     mxs[q4] = mx;
                     const int rsr = rSR[q];
                     float bq;
-                    if constexpr (B == 2) {
+                    if constexpr (NSP == 0) {
+                        // exact Bq (int64 at B = 16), one RN conversion
+                        bq = (float)((long long)n * mx - (long long)rsr * sd);
+                    } else if constexpr (B == 2) {
                         // |Bq| <= sqrt(A C) < 2^22: exact int -> float by the 1.5 * 2^23 magic
                         bq = __int_as_float(n * mx - rsr * sd + 0x4B400000) - 12582912.0f;
                     } else if constexpr (B == 4) {
@@ -529,9 +541,14 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
                     } else {
                         bq = fmaf((float)n, (float)mx, -((float)rsr * (float)sd));
                     }
-                    float g0 = fmaf(nhs[0], bq, t2[0]);
+                    float g0;
+                    if constexpr (NSP == 0) {
+                        g0 = -(bq * bq) * t2[0];  // >= -(Bq^2 / C)(1 + 4.04u): continuous minimum
+                    } else {
+                        g0 = fmaf(nhs[0], bq, t2[0]);
 #pragma unroll
-                    for (int jj = 1; jj < NSP; ++jj) g0 = fminf(g0, fmaf(nhs[jj], bq, t2[jj]));
+                        for (int jj = 1; jj < NSP; ++jj) g0 = fminf(g0, fmaf(nhs[jj], bq, t2[jj]));
+                    }
                     pm |= (g0 <= sThr[eg * HALF + q]) ? (1u << q4) : 0u;
                 }
                 if (pm) {  // queue (q, k*, max SRD) of the passing ranges for the exact path
@@ -656,7 +673,7 @@ template <int B>
 static cudaError_t launch_tc_b(const TCParams &p, cudaStream_t st) {
     if (p.nsp <= 1) return launch_tc_t<B, 1>(p, st);
     if (p.nsp <= 2) return launch_tc_t<B, 2>(p, st);
-    return launch_tc_t<B, 16>(p, st);
+    return launch_tc_t<B, 0>(p, st);
 }
 
 int tc_ranges_per_cta(int B) { return B == 16 ? 16 : 32; }
@@ -684,7 +701,8 @@ static cudaError_t tc_range_prep(const SearchParams &sp, uint8_t *scratch, TCPar
     if (e != cudaSuccess) return e;
     const int n_pad = (int)(groups * Cf::NR);
     tc_range_meta_kernel<B><<<(unsigned)((n_pad + 127) / 128), 128, 0, st>>>(sp.img, sp.N, sp.ranges, sp.d_nr,
-                                                                              n_pad, sp.smax, sp.d_misc, meta);
+                                                                              n_pad, sp.smax, sp.d_misc, meta,
+                                                                              sp.nsp > 2 ? 1 : 0);
     p.Bop = Bop;
     p.rmeta = meta;
     return cudaGetLastError();

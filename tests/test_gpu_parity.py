@@ -11,7 +11,7 @@ import pytest
 
 import oracle
 from fic_inputs import (config, image_for, make_image, random_image, ramp_image, constant_image,
-                        sample_indices, PREDEFINED_S, GRID_S)
+                        sample_indices, PREDEFINED_S, GRID_S, SAMPLED10_S, CLOSED5_S)
 
 pytestmark = pytest.mark.gpu
 
@@ -85,10 +85,10 @@ def level_case(fic, img, B, L, tau, s, tol=8.0, is_min=True, ranges=None):
 
 
 @pytest.mark.parametrize("B", [2, 4, 8, 16])
-@pytest.mark.parametrize("smode", ["predefined", "grid"])
+@pytest.mark.parametrize("smode", ["predefined", "grid", "sampled10", "closed5"])
 def test_level_parity_synthetic(fic, B, smode):
     img = make_image(96, 100 + B)
-    s = PREDEFINED_S[B] if smode == "predefined" else GRID_S
+    s = {"predefined": PREDEFINED_S[B], "grid": GRID_S, "sampled10": SAMPLED10_S, "closed5": CLOSED5_S}[smode]
     level_case(fic, img, B, 2, -1.0, s, tol=6.0, is_min=False)
 
 
@@ -258,7 +258,7 @@ def sampled_level_check(fic, img, cfg, got, per_level=24, seed=0, parents=8):
 
 
 @pytest.mark.parametrize("smode,t", [("predefined", 4.0), ("predefined", 8.0), ("predefined", 12.0),
-                                     ("grid", 8.0)])
+                                     ("grid", 8.0), ("closed5", 8.0)])
 def test_c3_sampled(fic, smode, t):
     cfg = config("C3", s_mode=smode, t=t)
     img, got = encode_both(fic, cfg)
@@ -346,8 +346,8 @@ def test_b32_and_bad_args(fic):
     with pytest.raises(p.FicError) as ei:  # B_max = 32 not supported on the GPU path
         ctx.encode(img, 32, 2, 2, [-1] * 5, [(0.5,)] * 5, [8.0] * 5)
     assert ei.value.status == 1
-    with pytest.raises(p.FicError) as ei:  # more than 16 contrast values
-        ctx.encode(img, 16, 2, 2, [-1] * 4, [tuple(np.linspace(0, 1, 17))] * 4, [8.0] * 4)
+    with pytest.raises(p.FicError) as ei:  # more than 32 contrast values
+        ctx.encode(img, 16, 2, 2, [-1] * 4, [tuple(np.linspace(0, 1, 33))] * 4, [8.0] * 4)
     assert ei.value.status == 1
     with pytest.raises(p.FicError):
         ctx.encode(img, 16, 2, 2, [-1] * 4, [(0.5,)] * 4, [8.0] * 4, shard=3, n_shards=2)
@@ -394,3 +394,18 @@ def test_c3_topk_sampled(fic):
     cfg = config("C3", topk=256)  # the paper's Table 1-2 pool size 256 at the paper's image size
     img, got = encode_both(fic, cfg)
     sampled_level_check(fic, img, cfg, got, per_level=40, parents=4)
+
+
+@pytest.mark.parametrize("smode", ["closed5", "sampled10"])
+def test_c2_full_parity_large_s_sets(fic, smode):
+    cfg = config("C2", s_mode=smode)
+    img, got = encode_both(fic, cfg)
+    assert_same(got, oracle.encode_cfg(cfg, img), f"C2 {smode}")
+
+
+def test_more_than_32_s_values_rejected(fic):
+    p, ctx, torch = fic
+    img = dev(torch, make_image(64, 5))
+    with pytest.raises(p.FicError) as ei:
+        ctx.encode(img, 16, 2, 2, [-1] * 4, [tuple(np.linspace(0, 1, 33))] * 4, [8.0] * 4)
+    assert ei.value.status == 1
