@@ -115,13 +115,17 @@ def load_peaks():
         return {}
 
 
-def load_traffic():
-    """dram bytes per launch of the dominant kernel from the committed ncu summary (or None)."""
+def load_traffic(kernel_substr: str):
+    """dram read + write bytes per launch of the dominant kernel from the committed ncu summary
+    (profiles/ncu_summary.json, one `ncu --set full` capture per kernel), or None."""
     try:
         d = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
-        return d.get("search_dram_bytes_per_launch")
+        for k in d.get("kernels", []):
+            if kernel_substr in k["kernel"] and k.get("dram_bytes") is not None:
+                return k["dram_bytes"]
     except Exception:
-        return None
+        pass
+    return None
 
 
 # ----------------------------------------------------------------------------- oracle sample
@@ -327,7 +331,7 @@ def main():
     ms_launch = dom["ms_search"] / args.steps
     achieved = dom["pairs_scanned"] * 8 / (ms_launch / 1e3) / 1e9
     peak = 1.0 / t_pair(dom["B"], nS) / 1e9
-    traffic = load_traffic()
+    traffic = load_traffic("b2win_kernel" if dom["B"] == 2 else f"tcsearch_kernel<{dom['B']},")
 
     res = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
