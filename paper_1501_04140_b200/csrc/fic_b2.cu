@@ -181,7 +181,6 @@ struct B2Params {
     unsigned long long *d_ns;       // splits of the partials finalize merges (= 1 here)
     unsigned long long *scan_count; // (range, domain) pairs evaluated by the fp32 filter
     int32_t ns_cap;
-    int32_t univ;                   // > 2 s values: s-independent filter g = -(bq bq) RN(1/(4C))
 };
 
 constexpr int kB2Threads = 256;
@@ -191,10 +190,8 @@ constexpr int kB2Unroll = 4;
 
 // filter margin of one range (e units): |Bq| <= sqrt(A C); fp32 -hs and t2 roundings and one
 // FFMA -> 4u (hs |Bq| + t2)
-__device__ __forceinline__ double b2_margin(double A, double smax, double cmax, int univ = 0) {
+__device__ __forceinline__ double b2_margin(double A, double smax, double cmax) {
     const double u = 5.9604644775390625e-08;
-    // s-independent filter: bq exact, bq*bq, RN(1/(4C)) and the product rounded: 3.01u Bq^2/C <= 3.01u A
-    if (univ) return 3.1 * u * A + 1e-12 * A + 1e-30;
     const double hs = 0.5 * smax, t2m = smax * smax * cmax * 0.0625;
     return 4.0 * u * (hs * sqrt(A * cmax) * 1.01 + t2m) + 1e-12 * (A + t2m) + 1e-30;
 }
@@ -216,11 +213,12 @@ __device__ __forceinline__ B2Range b2_range(int a, int b, int c, int d) {
     return R;
 }
 
-// NP = pairs of s values filtered one by one; NP = 0: the s-independent bound of large sets
-// (grid, sampled10, 5-bit closed form), g = -(bq bq) u4 with u4 = RN(1/(4C)) >= min_s (e_s - A)
+// NP = pairs of s values (1, 8 or 16), each filtered one by one.  (The s-independent bound of
+// tcsearch_kernel<B, 0> would not give the pass-2 threshold below: that needs |g - (e - A)| <=
+// margin, which only the per-s filter has.)
 template <int NP>
 __global__ void __launch_bounds__(kB2Threads, 3) b2scan_kernel(const __grid_constant__ B2Params P) {
-    constexpr int RPT = kB2RPT, NB = kB2NB, TW = NP ? 2 * NP : 1;
+    constexpr int RPT = kB2RPT, NB = kB2NB, TW = 2 * NP;
     constexpr int TPS = NP == 1 ? 2 : 1;  // tiles per stage
     constexpr int SDOM = TPS * kTileD;    // domains per stage
     constexpr int NWARP = kB2Threads / 32;
@@ -277,7 +275,7 @@ __global__ void __launch_bounds__(kB2Threads, 3) b2scan_kernel(const __grid_cons
         else { X[q / 2].x = R.x2; SX[q / 2].x = R.sx; DX[q / 2].x = R.dx; }
         gm[q] = INFINITY;
     }
-    float2 nh[NP ? NP : 1];  // -(s_j / 4) (times 2 max Bq); zero on pads (t2 = +inf there)
+    float2 nh[NP];  // -(s_j / 4) (times 2 max Bq); zero on pads (t2 = +inf there)
 #pragma unroll
     for (int jp = 0; jp < NP; ++jp) {
         nh[jp].x = 2 * jp < P.nsp ? P.nhs[2 * jp] : 0.f;
@@ -293,20 +291,14 @@ __global__ void __launch_bounds__(kB2Threads, 3) b2scan_kernel(const __grid_cons
 #pragma unroll kB2Unroll
         for (int dl = 0; dl < nd; ++dl) {
             const float4 f = Fb[dl];
-            float2 t2[NP ? NP : 1];
+            float2 t2[NP];
 #pragma unroll
             for (int jp = 0; jp < NP; ++jp) t2[jp] = reinterpret_cast<const float2 *>(Tb + dl * TW)[jp];
-            const float nu4 = NP ? 0.f : -Tb[dl];
 #pragma unroll
             for (int p = 0; p < RPT / 2; ++p) {
                 float2 Q = __fmul2_rn(DX[p], b2_bc(f.z));
                 Q = __ffma2_rn(X[p], b2_bc(f.x), Q);
                 const float2 bq = __ffma2_rn(SX[p], b2_bc(f.y), make_float2(fabsf(Q.x), fabsf(Q.y)));
-                if constexpr (NP == 0) {
-                    const float2 g = __fmul2_rn(__fmul2_rn(bq, bq), b2_bc(nu4));
-                    gm[2 * p] = fminf(gm[2 * p], g.x);
-                    gm[2 * p + 1] = fminf(gm[2 * p + 1], g.y);
-                }
 #pragma unroll
                 for (int jp = 0; jp < NP; ++jp) {
                     const float2 g0 = __ffma2_rn(nh[jp], b2_bc(bq.x), t2[jp]);
@@ -400,7 +392,7 @@ __global__ void __launch_bounds__(256) b2exact_kernel(const __grid_constant__ B2
     const uint8_t *p0 = P.img + (size_t)rr.y * P.N + rr.x;
     const B2Range R = b2_range(p0[0], p0[1], p0[P.N + 1], p0[P.N]);
     const double A = (double)R.A;
-    const double margin = b2_margin(A, P.smax, cmax, P.univ);
+    const double margin = b2_margin(A, P.smax, cmax);
     float gmn = INFINITY;
     for (int i = lane; i < ns; i += 32) gmn = fminf(gmn, P.gmin[(size_t)r * P.ns_cap + i]);
 #pragma unroll
@@ -423,9 +415,7 @@ __global__ void __launch_bounds__(256) b2exact_kernel(const __grid_constant__ B2
             const float4 f = P.F[pos];
             const float bq = fmaf(R.sx, f.y, fabsf(fmaf(R.x2, f.x, R.dx * f.z)));
             float g = INFINITY;
-            if (P.univ) g = (bq * bq) * (-P.T[pos]);
-            else
-                for (int jj = 0; jj < P.nsp; ++jj) g = fminf(g, fmaf(P.nhs[jj], bq, P.T[pos * P.tw + jj]));
+            for (int jj = 0; jj < P.nsp; ++jj) g = fminf(g, fmaf(P.nhs[jj], bq, P.T[pos * P.tw + jj]));
             if (g <= thr) {
                 ++n_exact;
                 const int32_t d = P.ds[pos];
@@ -534,7 +524,7 @@ __global__ void __launch_bounds__(256) b2win_kernel(const __grid_constant__ B2Pa
     const uint8_t *p0 = P.img + (size_t)rr.y * P.N + rr.x;
     const B2Range R = b2_range(p0[0], p0[1], p0[P.N + 1], p0[P.N]);
     const double A = (double)R.A;
-    const double margin = b2_margin(A, P.smax, cmax, P.univ);
+    const double margin = b2_margin(A, P.smax, cmax);
     const float nh0 = P.nhs[0], nh1 = P.nsp > 1 ? P.nhs[1] : 0.f;
     const float2 *T2 = reinterpret_cast<const float2 *>(P.T);  // tw == 2 (pad j: +inf)
     auto gval = [&](int pos, float &bq, float &cf) {
@@ -658,10 +648,6 @@ __global__ void b2_t2_kernel(const float4 *__restrict__ F, const unsigned long l
     const int64_t n_k = (int64_t)*d_nk;
     if (d >= ((n_k + kTileD - 1) / kTileD) * kTileD) return;
     const double c16 = __dmul_rn(0.0625, (double)F[d].w);  // C (exact in fp32, < 2^23)
-    if (tw == 1) {  // s-independent filter: RN(1/(4C)), 0 for C = 0, NaN on pads (never admitted)
-        T[d] = d < n_k ? (F[d].w > 0.f ? __double2float_rn(0.25 / (double)F[d].w) : 0.f) : __int_as_float(0x7fc00000);
-        return;
-    }
     for (int j = 0; j < tw; ++j) {
         const double s = j < nsp ? spos.s[j] : 0.0;
         T[d * tw + j] = (d < n_k && j < nsp) ? __double2float_rn(__dmul_rn(__dmul_rn(s, s), c16)) : INFINITY;
@@ -671,8 +657,7 @@ __global__ void b2_t2_kernel(const float4 *__restrict__ F, const unsigned long l
 template <int NP>
 static size_t b2_smem() {
     constexpr int TPS = NP == 1 ? 2 : 1;
-    constexpr int TW = NP ? 2 * NP : 1;
-    return (size_t)kB2NB * TPS * kTileD * (16 + 4 * TW) + kB2NB * 12 + 64;
+    return (size_t)kB2NB * TPS * kTileD * (16 + 8 * NP) + kB2NB * 12 + 64;
 }
 
 template <int NP>
@@ -733,9 +718,6 @@ cudaError_t launch_b2_search(const SearchParams &sp, const B2Pool &bp, float *T,
     p.has_zero = sp.has_zero; p.j_zero = sp.j_zero;
     p.smax = sp.smax;
     p.part = sp.part; p.exact_count = sp.exact_count; p.scan_count = scan_count;
-    // per-s filter at every set size: the two-pass thresholds need g within a margin of e - A
-    // (an s-independent lower bound would not give pass 1 a valid threshold)
-    p.univ = 0;
     p.d_nscan = reinterpret_cast<unsigned long long *>(scratch);
     p.gmin = reinterpret_cast<float *>(static_cast<char *>(scratch) + 64);
     if (sp.b2_window && !sp.has_zero && sp.nsp <= 2) {  // predefined s: Cauchy-Schwarz windows

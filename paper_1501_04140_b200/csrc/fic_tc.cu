@@ -477,16 +477,17 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
         for (int q = 0; q < HALF; ++q) rSR[q] = sR[eg * HALF + q].SR;
         int qn = 0;
         const int qbase = (threadIdx.x - 64) * 4;
+        // per-domain data of this lane, walked tile by tile (pointers advanced, not recomputed);
+        // NSP > 0 is chosen only when the level has exactly NSP values s > 0, so every row exists
+        const int32_t *sdp = P.SD + (int64_t)t0 * kTileD + m;
+        const float *t2p = P.t2f + (int64_t)t0 * kTileD + m;
+        const int64_t t2row = P.n_slots;
         int32_t sd_n = 0;
         float t2_n[NT];
-        {
-            const int d = t0 * kTileD + m;
-            if (ntl > 0) {
-                sd_n = P.SD[d];
+        if (ntl > 0) {
+            sd_n = __ldg(sdp);
 #pragma unroll
-                for (int jj = 0; jj < NT; ++jj)
-                    t2_n[jj] = (NSP == 0 || jj < P.nsp) ? P.t2f[(int64_t)jj * P.n_slots + d] : INFINITY;
-            }
+            for (int jj = 0; jj < NT; ++jj) t2_n[jj] = __ldg(t2p + jj * t2row);
         }
         for (int tl = 0; tl < ntl; ++tl) {
             const int buf = tl & 1;
@@ -495,11 +496,12 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
             float t2[NT];
 #pragma unroll
             for (int jj = 0; jj < NT; ++jj) t2[jj] = t2_n[jj];
+            sdp += kTileD;
+            t2p += kTileD;
             if (tl + 1 < ntl) {  // prefetch the next tile's per-domain data
-                sd_n = P.SD[d + kTileD];
+                sd_n = __ldg(sdp);
 #pragma unroll
-                for (int jj = 0; jj < NT; ++jj)
-                    t2_n[jj] = (NSP == 0 || jj < P.nsp) ? P.t2f[(int64_t)jj * P.n_slots + d + kTileD] : INFINITY;
+                for (int jj = 0; jj < NT; ++jj) t2_n[jj] = __ldg(t2p + jj * t2row);
             }
             tmbar_wait(&tfull[buf], (uint32_t)((tl >> 1) & 1));
             tc_fence_after();
