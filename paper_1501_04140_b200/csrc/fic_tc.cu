@@ -38,7 +38,8 @@ struct TCfg {
     static constexpr int KCH = KP < 256 ? KP : (B == 16 ? 128 : 256);  // K bytes per pipeline stage
     static constexpr int CH = KP / KCH;                    // stages per domain tile
     static constexpr int STAGE_BYTES = kTileD * KCH;       // A bytes per stage
-    static constexpr int STAGES = (B >= 8) ? 2 : 4;
+    // B = 16 waits on the A-operand feed: a third 16 KB stage still fits (232,032 of 232,448 B)
+    static constexpr int STAGES = B == 16 ? 3 : (B == 8 ? 2 : 4);
     static constexpr int B_BYTES = N * KP;                 // resident range operand
     static constexpr int EWG = 4;                          // epilogue warpgroups
     static constexpr int THREADS = 64 + 128 * EWG;
@@ -312,9 +313,9 @@ __global__ void tc_range_meta_kernel(const uint8_t *__restrict__ img, int32_t N,
     const double bq = sqrt(R.A * cmax) * 1.01 + (B > 8 ? (double)n * 1020.0 * (double)sr : 0.0);
     const double t2m = smax * smax * cmax * 0.0625;
     // + the int -> float conversion of Bq in the epilogue: exact at B = 2, |error| <= 2 at B = 4,
-    // <= 64 at B = 8 (floor of Bq / 2 and Bq / 64): hs * 64 covers both
-    R.margin = 8.0 * u * (hs * bq + t2m) + 1e-12 * (R.A + hs * bq + t2m) + (B == 4 || B == 8 ? hs * 64.0 : 0.0) +
-               1e-30;
+    // <= 64 at B = 8 (floor of Bq / 2 and Bq / 64)
+    R.margin = 8.0 * u * (hs * bq + t2m) + 1e-12 * (R.A + hs * bq + t2m) +
+               (B == 4 ? hs * 2.0 : (B == 8 ? hs * 64.0 : 0.0)) + 1e-30;
     // s-independent filter (NSP = 0): Bq rounded once, squared, times RN(1/C): <= 4.04u Bq^2/C <= 4.04u A
     if (univ) R.margin = 4.1 * u * R.A + 1e-12 * R.A + 1e-30;
     meta[r] = R;
@@ -417,18 +418,26 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
     const uint32_t tmem = *sTmem;
 
     if (warp == 0) {
-        // ================= producer: one bulk copy per (tile, chunk) stage
+        // ================= producer: each (tile, chunk) stage as kCopyLanes bulk copies issued by
+        // different lanes -- copies from one thread are serviced one after another (~550 cycles
+        // each up to 32 KB, scripts/micro/bulk_rate.cu), copies from several threads overlap
+        constexpr int kCopyLanes = 4;
+        constexpr uint32_t PART = Cf::STAGE_BYTES / kCopyLanes;
+        static_assert(Cf::STAGE_BYTES % (16 * kCopyLanes) == 0, "bulk copies need 16-byte multiples");
         if (lane == 0) {
             // the resident range operand of this CTA's NR ranges (prepared by tc_range_operand_kernel)
             tmbar_expect_tx(bbar, Cf::B_BYTES);
             tbulk_g2s(sB, P.Bop + (size_t)group * Cf::B_BYTES, Cf::B_BYTES, bbar);
+        }
+        if (lane < kCopyLanes) {
             for (int i = 0; i < nsteps; ++i) {
                 const int s = i % STAGES;
                 if (i >= STAGES) tmbar_wait(&empty[s], (uint32_t)(((i / STAGES) + 1) & 1));
                 const int tile = t0 + i / CH, ch = i % CH;
-                tmbar_expect_tx(&full[s], Cf::STAGE_BYTES);
-                tbulk_g2s(sA + s * Cf::STAGE_BYTES, P.Dtc + ((size_t)tile * CH + ch) * Cf::STAGE_BYTES,
-                          Cf::STAGE_BYTES, &full[s]);
+                if (lane == 0) tmbar_expect_tx(&full[s], Cf::STAGE_BYTES);
+                __syncwarp((1u << kCopyLanes) - 1);  // expect_tx before any of the stage's copies lands
+                tbulk_g2s(sA + s * Cf::STAGE_BYTES + lane * PART,
+                          P.Dtc + ((size_t)tile * CH + ch) * Cf::STAGE_BYTES + lane * PART, PART, &full[s]);
             }
         }
     } else if (warp == 1) {
@@ -464,7 +473,10 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
         constexpr int NT = NSP ? NSP : 1;  // t2 values per domain (u = 1/C for NSP = 0)
         float nhs[NT];
 #pragma unroll
-        for (int jj = 0; jj < NT; ++jj) nhs[jj] = sHsn[jj];
+        // the B = 4 / 8 conversions below yield Bq / 2 and Bq / 64: fold the power of two into -s/2
+        // (exact), so g = fma(nhs, bq, t2) keeps its rounding without the multiply
+        constexpr float kBqScale = B == 4 ? 2.0f : (B == 8 ? 64.0f : 1.0f);
+        for (int jj = 0; jj < NT; ++jj) nhs[jj] = sHsn[jj] * kBqScale;
         for (int q = 0; q < HALF; ++q) {
             Partial pb;
             if (P.has_zero) { pb.e = sR[eg * HALF + q].A; pb.d = 0; pb.kj = P.j_zero; }
@@ -536,10 +548,10 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
                         bq = __int_as_float(n * mx - rsr * sd + 0x4B400000) - 12582912.0f;
                     } else if constexpr (B == 4) {
                         // |Bq| <= n^2 127.5 510 < 2^24: magic on Bq / 2, error <= 1 (margin)
-                        bq = (__int_as_float(((n * mx - rsr * sd) >> 1) + 0x4B400000) - 12582912.0f) * 2.0f;
+                        bq = __int_as_float(((n * mx - rsr * sd) >> 1) + 0x4B400000) - 12582912.0f;  // (x 2 in nhs)
                     } else if constexpr (B == 8) {
                         // |Bq| < 2^28: magic on Bq / 64, error <= 64 (margin)
-                        bq = (__int_as_float(((n * mx - rsr * sd) >> 6) + 0x4B400000) - 12582912.0f) * 64.0f;
+                        bq = __int_as_float(((n * mx - rsr * sd) >> 6) + 0x4B400000) - 12582912.0f;  // (x 64 in nhs)
                     } else {
                         bq = fmaf((float)n, (float)mx, -((float)rsr * (float)sd));
                     }
