@@ -33,7 +33,9 @@ template <int B>
 struct TCfg {
     static constexpr int n = B * B;
     static constexpr int KP = ((4 * n + 31) / 32) * 32;    // K bytes (padded)
-    static constexpr int NR = (B == 16) ? 16 : 32;         // ranges per CTA
+    // ranges per CTA: 8 per epilogue warp per tile; B = 4 uses 3 epilogue warpgroups (14 warps,
+    // at most 4 per SM sub-partition, so 128 registers per thread instead of 96 with 18 warps)
+    static constexpr int NR = (B == 16) ? 16 : (B == 4 ? 24 : 32);
     static constexpr int N = 8 * NR;                       // MMA N (columns per accumulator)
     static constexpr int KCH = KP < 256 ? KP : (B == 16 ? 128 : 256);  // K bytes per pipeline stage
     static constexpr int CH = KP / KCH;                    // stages per domain tile
@@ -41,7 +43,7 @@ struct TCfg {
     // B = 16 waits on the A-operand feed: a third 16 KB stage still fits (232,032 of 232,448 B)
     static constexpr int STAGES = B == 16 ? 3 : (B == 8 ? 2 : 4);
     static constexpr int B_BYTES = N * KP;                 // resident range operand
-    static constexpr int EWG = 4;                          // epilogue warpgroups
+    static constexpr int EWG = B == 4 ? 3 : 4;            // epilogue warpgroups
     static constexpr int THREADS = 64 + 128 * EWG;
 };
 
@@ -690,7 +692,7 @@ static cudaError_t launch_tc_b(const TCParams &p, cudaStream_t st) {
     return launch_tc_t<B, 0>(p, st);
 }
 
-int tc_ranges_per_cta(int B) { return B == 16 ? 16 : 32; }
+int tc_ranges_per_cta(int B) { return B == 16 ? 16 : (B == 4 ? 24 : 32); }
 
 size_t tc_range_bytes(int B, int64_t n_r) {
     switch (B) {
