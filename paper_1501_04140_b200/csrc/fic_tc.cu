@@ -32,17 +32,25 @@ namespace fic {
 template <int B>
 struct TCfg {
     static constexpr int n = B * B;
-    static constexpr int KP = ((4 * n + 31) / 32) * 32;    // K bytes (padded)
+    // B = 16 (QR): the A operand holds the decimated D' split as q = D' >> 2 and r = D' & 3
+    // (two n-byte planes) and two MMAs per tile give S_q = sum R q and S_r = sum R r in two
+    // accumulators, SRD = 4 S_q + S_r: half the MMA work, half the A bytes and a quarter of the
+    // resident range operand of the 4-polyphase-plane form used at B <= 8 (where the epilogue,
+    // not the MMA or the feed, is the bottleneck and a second accumulator would only add work)
+    static constexpr bool QR = (B == 16);
+    static constexpr int KP = QR ? 2 * n : ((4 * n + 31) / 32) * 32;  // A K bytes per domain (padded)
+    static constexpr int KB = QR ? n : KP;                 // B operand K bytes per (range, k) row
     // ranges per CTA: 8 per epilogue warp per tile; B = 4 uses 3 epilogue warpgroups (14 warps,
     // at most 4 per SM sub-partition, so 128 registers per thread instead of 96 with 18 warps)
     static constexpr int NR = (B == 16) ? 16 : (B == 4 ? 24 : 32);
     static constexpr int N = 8 * NR;                       // MMA N (columns per accumulator)
-    static constexpr int KCH = KP < 256 ? KP : (B == 16 ? 128 : 256);  // K bytes per pipeline stage
+    static constexpr int KCH = QR ? 128 : (KP < 256 ? KP : 256);  // K bytes per pipeline stage
     static constexpr int CH = KP / KCH;                    // stages per domain tile
     static constexpr int STAGE_BYTES = kTileD * KCH;       // A bytes per stage
-    // B = 16 waits on the A-operand feed: a third 16 KB stage still fits (232,032 of 232,448 B)
-    static constexpr int STAGES = B == 16 ? 3 : (B == 8 ? 2 : 4);
-    static constexpr int B_BYTES = N * KP;                 // resident range operand
+    // B = 16 is fed by bulk copies (latency x bytes in flight): 8 x 16 KB stages
+    static constexpr int STAGES = QR ? 8 : (B == 8 ? 2 : 4);
+    static constexpr int B_BYTES = N * KB;                 // resident range operand
+    static constexpr int ACC = QR ? 2 * N : N;             // TMEM columns per accumulator buffer
     static constexpr int EWG = B == 4 ? 3 : 4;            // epilogue warpgroups
     static constexpr int THREADS = 64 + 128 * EWG;
 };
@@ -173,27 +181,48 @@ __global__ void __launch_bounds__(256) pool_tc_kernel(const uint8_t *__restrict_
     const int rem = (int)(e - tile * kTileD * G16);
     const int m = rem / G16, g = rem % G16;
     const int64_t d = tile * kTileD + m;
-    uint32_t w[4] = {0, 0, 0, 0};
-    if (d < n_k) {
-        const int32_t c = kept[d];
-        const int64_t x = (int64_t)(c % A) * L, y = (int64_t)(c / A) * L;
+    auto store16 = [&](int kb0, const uint32_t (&w)[4]) {  // chunk layout: [tile][chunk][128 x KCH]
+        const int ch = kb0 / Cf::KCH, kc = kb0 % Cf::KCH;
+        uint8_t *dst = Dtc + ((size_t)tile * Cf::CH + ch) * Cf::STAGE_BYTES + cm_off(m, kc, Cf::KCH);
+        *reinterpret_cast<uint4 *>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
+    };
+    if constexpr (Cf::QR) {
+        // one thread per 16 pixels writes both planes: q = D' >> 2 at K byte p, r = D' & 3 at n + p
+        if (g >= Cf::n / 16) return;
+        uint32_t wq[4] = {0, 0, 0, 0}, wr[4] = {0, 0, 0, 0};
+        if (d < n_k) {
+            const int32_t c = kept[d];
+            const int64_t x = (int64_t)(c % A) * L, y = (int64_t)(c / A) * L;
 #pragma unroll
-        for (int q = 0; q < 16; ++q) {
-            const int kb = g * 16 + q;
-            uint32_t v = 0;
-            if (kb < 4 * Cf::n) {
-                const int plane = kb / Cf::n, p = kb % Cf::n;
-                const int i = p / B, j = p % B;
-                v = img[(y + 2 * i + (plane >> 1)) * N + x + 2 * j + (plane & 1)];
+            for (int q = 0; q < 16; ++q) {
+                const int p = g * 16 + q, i = p / B, j = p % B;
+                const uint8_t *px = img + (y + 2 * i) * N + x + 2 * j;
+                const uint32_t dp = (uint32_t)px[0] + px[1] + px[N] + px[N + 1];
+                wq[q >> 2] |= (dp >> 2) << (8 * (q & 3));
+                wr[q >> 2] |= (dp & 3u) << (8 * (q & 3));
             }
-            w[q >> 2] |= v << (8 * (q & 3));
         }
+        store16(g * 16, wq);
+        store16(Cf::n + g * 16, wr);
+    } else {
+        uint32_t w[4] = {0, 0, 0, 0};
+        if (d < n_k) {
+            const int32_t c = kept[d];
+            const int64_t x = (int64_t)(c % A) * L, y = (int64_t)(c / A) * L;
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+                const int kb = g * 16 + q;
+                uint32_t v = 0;
+                if (kb < 4 * Cf::n) {
+                    const int plane = kb / Cf::n, p = kb % Cf::n;
+                    const int i = p / B, j = p % B;
+                    v = img[(y + 2 * i + (plane >> 1)) * N + x + 2 * j + (plane & 1)];
+                }
+                w[q >> 2] |= v << (8 * (q & 3));
+            }
+        }
+        store16(g * 16, w);
     }
-    // chunk layout: [tile][chunk][128 x KCH]
-    const int kb0 = g * 16;
-    const int ch = kb0 / Cf::KCH, kc = kb0 % Cf::KCH;
-    uint8_t *dst = Dtc + ((size_t)tile * Cf::CH + ch) * Cf::STAGE_BYTES + cm_off(m, kc, Cf::KCH);
-    *reinterpret_cast<uint4 *>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
 }
 
 int tc_supported(int B) { return B == 2 || B == 4 || B == 8 || B == 16; }
@@ -243,8 +272,8 @@ __global__ void __launch_bounds__(256) tc_range_operand_kernel(const uint8_t *__
     const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // one 16-byte group
     if (e >= total16) return;
     const int64_t n_r = (int64_t)*d_nr;
-    if (e / ((int64_t)Cf::N * (Cf::KP / 16)) > (n_r + Cf::NR - 1) / Cf::NR) return;  // past the last group
-    constexpr int G16 = Cf::KP / 16;
+    if (e / ((int64_t)Cf::N * (Cf::KB / 16)) > (n_r + Cf::NR - 1) / Cf::NR) return;  // past the last group
+    constexpr int G16 = Cf::KB / 16;
     const int64_t row_g = e / G16;  // global row = group * N + row
     const int g = (int)(e % G16);
     const int64_t grp = row_g / Cf::N;
@@ -261,7 +290,7 @@ __global__ void __launch_bounds__(256) tc_range_operand_kernel(const uint8_t *__
         for (int q = 0; q < 16; ++q) {
             const int kb = g * 16 + q;
             uint32_t v = 0;
-            if (kb < 4 * Cf::n) {
+            if (kb < (Cf::QR ? Cf::n : 4 * Cf::n)) {  // 4 polyphase copies, or once (QR)
                 const int p = kb % Cf::n;
                 int si, sj;
                 tiso_src(B, kinv, p / B, p % B, si, sj);
@@ -270,7 +299,7 @@ __global__ void __launch_bounds__(256) tc_range_operand_kernel(const uint8_t *__
             w[q >> 2] |= v << (8 * (q & 3));
         }
     }
-    uint8_t *dst = Bop + (size_t)grp * Cf::B_BYTES + cm_off(row, g * 16, Cf::KP);
+    uint8_t *dst = Bop + (size_t)grp * Cf::B_BYTES + cm_off(row, g * 16, Cf::KB);
     *reinterpret_cast<uint4 *>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
 }
 
@@ -454,13 +483,18 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
             if (ch == 0 && tl >= 2) tmbar_wait(&tempty[buf], (uint32_t)(((tl >> 1) + 1) & 1));
             tc_fence_after();
             if (lane == 0) {
+                // QR: the first half of the stages (q plane) accumulates S_q at column 0 of the
+                // buffer, the second half (r plane) S_r at column N; both against the same B rows
+                constexpr int CHA = Cf::QR ? CH / 2 : CH;  // stages per accumulator
+                const int cha = ch % CHA;
+                const uint32_t dcol = buf * Cf::ACC + ((Cf::QR && ch >= CHA) ? NN : 0);
                 const uint32_t a0 = su32(sA + s * Cf::STAGE_BYTES);
-                const uint32_t b0 = su32(sB) + ch * (KCH / 16) * 128;
+                const uint32_t b0 = su32(sB) + cha * (KCH / 16) * 128;
 #pragma unroll
                 for (int kk = 0; kk < KCH / 32; ++kk) {
                     const uint64_t ad = smem_desc(a0 + kk * 256, 128, (KCH / 16) * 128);
-                    const uint64_t bd = smem_desc(b0 + kk * 256, 128, (KP / 16) * 128);
-                    tc_mma_i8(tmem + buf * NN, ad, bd, idesc, (ch > 0 || kk > 0) ? 1u : 0u);
+                    const uint64_t bd = smem_desc(b0 + kk * 256, 128, (Cf::KB / 16) * 128);
+                    tc_mma_i8(tmem + dcol, ad, bd, idesc, (cha > 0 || kk > 0) ? 1u : 0u);
                 }
                 tc_commit(&empty[s]);
                 if (ch == CH - 1) tc_commit(&tfull[buf]);
@@ -519,12 +553,20 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
             }
             tmbar_wait(&tfull[buf], (uint32_t)((tl >> 1) & 1));
             tc_fence_after();
-            const uint32_t tbase = tmem + ((uint32_t)(lq * 32) << 16) + buf * NN + eg * HALF * 8;
+            const uint32_t tbase = tmem + ((uint32_t)(lq * 32) << 16) + buf * Cf::ACC + eg * HALF * 8;
             // four ranges (32 columns) per tcgen05.ld, the next group in flight while one is scored
             constexpr int G = HALF / 4;
             uint32_t vv[64];
             tc_ld32<0>(tbase, vv);
-            tc_wait_ld();
+            if constexpr (Cf::QR) {  // SRD_k = 4 S_q + S_r (exact: < 2^31)
+                static_assert(!Cf::QR || G == 1, "QR keeps one 4-range group per warp and tile");
+                tc_ld32<32>(tbase + NN, vv);
+                tc_wait_ld();
+#pragma unroll
+                for (int i = 0; i < 32; ++i) vv[i] = 4u * vv[i] + vv[32 + i];
+            } else {
+                tc_wait_ld();
+            }
 #pragma unroll
             for (int g = 0; g < G; ++g) {
                 if (g + 1 < G) {
@@ -710,7 +752,7 @@ static cudaError_t tc_range_prep(const SearchParams &sp, uint8_t *scratch, TCPar
     const int64_t groups = (sp.n_r + Cf::NR - 1) / Cf::NR;
     uint8_t *Bop = scratch;
     TCRangeG *meta = reinterpret_cast<TCRangeG *>(scratch + (size_t)groups * Cf::B_BYTES);
-    const int64_t total16 = groups * Cf::N * (Cf::KP / 16);
+    const int64_t total16 = groups * Cf::N * (Cf::KB / 16);
     tc_range_operand_kernel<B><<<(unsigned)((total16 + 255) / 256), 256, 0, st>>>(sp.img, sp.N, sp.ranges,
                                                                                   sp.d_nr, total16, Bop);
     cudaError_t e = cudaGetLastError();
