@@ -57,10 +57,87 @@ __global__ void __launch_bounds__(256) entropy_keys_kernel(
     }
 }
 
+// Sliding-window form for large blocks (2B > 2L): one warp per run of kSlideSeg consecutive
+// candidates of one candidate row.  The first histogram is built by m insertions; each step to
+// the next candidate (L columns to the right) removes the L leaving columns and inserts the L
+// entering ones (2 L side updates instead of m).  Removing a pixel from a bin holding `old`
+// adds LUT[old-1] - LUT[old] = -delta[old-1]; per bin the contributions telescope to
+// LUT[final] - LUT[initial] in any order (a removed pixel is always present, so no count goes
+// negative), so every key is the same exact integer as the direct build.
+constexpr int kSlideSeg = 16;
+__global__ void __launch_bounds__(256) entropy_slide_kernel(
+    const uint8_t *__restrict__ img, int32_t N, int32_t side, int32_t L, int32_t A,
+    const int64_t *__restrict__ g_delta, int64_t lut_m, int64_t T, int use_tau,
+    int64_t *__restrict__ keys, uint8_t *__restrict__ keep) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    const int m = side * side;
+    int64_t *delta = reinterpret_cast<int64_t *>(sm);
+    int32_t *hist_all = reinterpret_cast<int32_t *>(sm + sizeof(int64_t) * m);
+    for (int i = threadIdx.x; i < m; i += blockDim.x) delta[i] = g_delta[i];
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    int32_t *hist = hist_all + warp * 256;
+    const int segs = (A + kSlideSeg - 1) / kSlideSeg;
+    const int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+    if (w >= (int64_t)A * segs) return;
+    const int b = (int)(w / segs), a0 = (int)(w % segs) * kSlideSeg, a1 = min(A, a0 + kSlideSeg);
+    const int64_t y = (int64_t)b * L;
+    for (int v = lane; v < 256; v += 32) hist[v] = 0;
+    __syncwarp();
+    int64_t acc = 0;
+    {
+        const int64_t x = (int64_t)a0 * L;
+        for (int idx = lane; idx < m; idx += 32) {
+            const int i = idx / side, j = idx - i * side;
+            const int old = atomicAdd(&hist[img[(y + i) * (int64_t)N + x + j]], 1);
+            acc += delta[old];
+        }
+    }
+    const int nu = L * side;  // pixels leaving (and entering) per step
+    for (int a = a0;; ++a) {
+        int64_t tot = acc;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+        if (lane == 0) {
+            const int64_t key = lut_m - tot;
+            const int64_t c = (int64_t)b * A + a;
+            keys[c] = key;
+            keep[c] = (uint8_t)(!use_tau || key > T);
+        }
+        if (a + 1 >= a1) break;
+        __syncwarp();
+        const int64_t x = (int64_t)a * L;
+        for (int u = lane; u < 2 * nu; u += 32) {
+            const int uu = u < nu ? u : u - nu;
+            const int i = uu / L, j = uu - i * L;
+            if (u < nu) {  // leaving column x + j
+                const int old = atomicSub(&hist[img[(y + i) * (int64_t)N + x + j]], 1);
+                acc -= delta[old - 1];
+            } else {       // entering column x + side + j
+                const int old = atomicAdd(&hist[img[(y + i) * (int64_t)N + x + side + j]], 1);
+                acc += delta[old];
+            }
+        }
+        __syncwarp();
+    }
+}
+
 cudaError_t launch_entropy_keys(const uint8_t *img, int32_t N, int32_t B, int32_t L, int32_t A,
                                 const int64_t *d_delta, int64_t lut_m, int64_t T, int use_tau,
                                 int64_t *keys, uint8_t *keep, cudaStream_t st) {
     const int side = 2 * B, m = side * side;
+    if (B >= 8 && L < side / 2) {  // sliding windows pay off (>= 4x fewer histogram updates)
+        const size_t smem = sizeof(int64_t) * m + 8 * 256 * sizeof(int32_t);
+        static bool attr2 = false;
+        if (!attr2) {
+            cudaFuncSetAttribute(entropy_slide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+            attr2 = true;
+        }
+        const int64_t warps = (int64_t)A * ((A + kSlideSeg - 1) / kSlideSeg);
+        entropy_slide_kernel<<<(unsigned)((warps + 7) / 8), 256, smem, st>>>(img, N, side, L, A, d_delta, lut_m, T,
+                                                                             use_tau, keys, keep);
+        return cudaGetLastError();
+    }
     const size_t smem = sizeof(int64_t) * m + 8 * 256 * sizeof(int32_t);
     static bool attr = false;
     if (!attr) {
