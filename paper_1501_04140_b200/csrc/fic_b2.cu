@@ -566,14 +566,29 @@ __global__ void __launch_bounds__(256) b2win_kernel(const __grid_constant__ B2Pa
         if (lane == 1 && q1 < q2) cn = __ldg(P.Cs + q1);
         if (lane == 2 && q1 < q2) cn = __ldg(P.Cs + q2 - 1);
         if (lane == 3 && q3 < n_k) cn = __ldg(P.Cs + q3);
-        float g = INFINITY, bq, cf;
+        // all of this lane's loads of the round first (up to 8 domains, L2-latency bound), then
+        // the arithmetic; absent slots read position 0 and are masked to +inf
+        float4 fv[8];
+        float2 tv[8];
+        bool ok8[8];
+        const int nf[4] = {n0, n1, n2, n3}, bf[4] = {b0, b1, b2, b3};
 #pragma unroll
         for (int k = 0; k < 2; ++k) {
-            const int o = lane + 32 * k;
-            if (o < n0) g = fminf(g, gval(b0 + o, bq, cf));
-            if (o < n1) g = fminf(g, gval(b1 + o, bq, cf));
-            if (o < n2) g = fminf(g, gval(b2 + o, bq, cf));
-            if (o < n3) g = fminf(g, gval(b3 + o, bq, cf));
+#pragma unroll
+            for (int f = 0; f < 4; ++f) {
+                const int o = lane + 32 * k;
+                ok8[k * 4 + f] = o < nf[f];
+                const int pos = ok8[k * 4 + f] ? bf[f] + o : 0;
+                fv[k * 4 + f] = __ldg(P.F + pos);
+                tv[k * 4 + f] = __ldg(T2 + pos);
+            }
+        }
+        float g = INFINITY;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const float bq = fmaf(R.sx, fv[i].y, fabsf(fmaf(R.x2, fv[i].x, R.dx * fv[i].z)));
+            const float gi = fminf(fmaf(nh0, bq, tv[i].x), fmaf(nh1, bq, tv[i].y));
+            g = fminf(g, ok8[i] ? gi : INFINITY);
         }
         gmin = fminf(gmin, b2_fdec(__reduce_min_sync(0xffffffffu, b2_fkey(g))));
         const float ub = gmin < INFINITY ? __double2float_ru(__dadd_ru(__dadd_ru(A, (double)gmin), margin)) : INFINITY;
@@ -605,18 +620,30 @@ __global__ void __launch_bounds__(256) b2win_kernel(const __grid_constant__ B2Pa
     for (int w = 0; w < nrun; ++w) {
         const int a0 = w == 0 ? q0 : q2;
         const int a1 = (w == 0 && nrun == 2) ? q1 : q3;
-#pragma unroll 4
-        for (int pos = a0 + lane; pos < a1; pos += 32) {
-            float bq, cf;
-            if (gval(pos, bq, cf) <= thr) {
-                ++n_exact;
-                int j0;
-                const double e0 = b2_canon(P, A, bq, cf, j0);
-                const int32_t d = __ldg(P.ds + pos);
-                const int32_t kj = P.jpos[j0] | kPendIso;
-                if (b2_less(e0, d, kj, be, bd, bkj)) {
-                    be = e0; bd = d; bkj = kj;
-                    thr = fminf(thr, fminf(__double2float_ru(__dadd_rn(__dsub_rn(e0, A), margin)), FLT_MAX));
+        // four domains per lane per pass: the loads first, then the filter (rare exact path)
+        for (int pos0 = a0 + lane; pos0 < a1; pos0 += 128) {
+            float4 fv[4];
+            float2 tv[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int pos = min(pos0 + 32 * i, a1 - 1);
+                fv[i] = __ldg(P.F + pos);
+                tv[i] = __ldg(T2 + pos);
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int pos = pos0 + 32 * i;
+                const float bq = fmaf(R.sx, fv[i].y, fabsf(fmaf(R.x2, fv[i].x, R.dx * fv[i].z)));
+                if (pos < a1 && fminf(fmaf(nh0, bq, tv[i].x), fmaf(nh1, bq, tv[i].y)) <= thr) {
+                    ++n_exact;
+                    int j0;
+                    const double e0 = b2_canon(P, A, bq, fv[i].w, j0);
+                    const int32_t d = __ldg(P.ds + pos);
+                    const int32_t kj = P.jpos[j0] | kPendIso;
+                    if (b2_less(e0, d, kj, be, bd, bkj)) {
+                        be = e0; bd = d; bkj = kj;
+                        thr = fminf(thr, fminf(__double2float_ru(__dadd_rn(__dsub_rn(e0, A), margin)), FLT_MAX));
+                    }
                 }
             }
         }
