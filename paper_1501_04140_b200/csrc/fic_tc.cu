@@ -51,6 +51,7 @@ struct TCfg {
     static constexpr int STAGES = QR ? 8 : (B == 8 ? 2 : 4);
     static constexpr int B_BYTES = N * KB;                 // resident range operand
     static constexpr int ACC = QR ? 2 * N : N;             // TMEM columns per accumulator buffer
+    static constexpr int NBUF = 512 / ACC >= 4 ? 4 : 2;    // TMEM accumulator buffers (MMA <-> epilogue)
     static constexpr int EWG = B == 4 ? 3 : 4;            // epilogue warpgroups
     static constexpr int THREADS = 64 + 128 * EWG;
 };
@@ -398,9 +399,10 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
     float *sThr = reinterpret_cast<float *>(sR + NR);          // [NR] RU(best - A + margin), CAS-min
     float *sHsn = reinterpret_cast<float *>(sThr + NR);        // [NSP]
     Partial *sRed = reinterpret_cast<Partial *>(sHsn + 16);    // [NR][4]
-    uint64_t *bar = reinterpret_cast<uint64_t *>(sRed + NR * 4);  // full[S], empty[S], tfull[2], tempty[2], bop
-    uint64_t *full = bar, *empty = bar + STAGES, *tfull = bar + 2 * STAGES, *tempty = tfull + 2;
-    uint64_t *bbar = tempty + 2;
+    constexpr int NBUF = Cf::NBUF;
+    uint64_t *bar = reinterpret_cast<uint64_t *>(sRed + NR * 4);  // full[S], empty[S], tfull[NB], tempty[NB], bop
+    uint64_t *full = bar, *empty = bar + STAGES, *tfull = bar + 2 * STAGES, *tempty = tfull + NBUF;
+    uint64_t *bbar = tempty + NBUF;
     uint32_t *sTmem = reinterpret_cast<uint32_t *>(bbar + 2);
     Partial *sBest = reinterpret_cast<Partial *>(sTmem + 4);  // [NR][128] per (range, domain lane)
     int2 *sQ = reinterpret_cast<int2 *>(sBest + NR * kTileD);  // [epilogue threads][4] exact queue
@@ -423,7 +425,7 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
             tmbar_init(&full[s], 1);
             tmbar_init(&empty[s], 1);
         }
-        for (int b = 0; b < 2; ++b) {
+        for (int b = 0; b < NBUF; ++b) {
             tmbar_init(&tfull[b], 1);
             tmbar_init(&tempty[b], 4 * Cf::EWG);
         }
@@ -478,9 +480,9 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
         for (int i = 0; i < nsteps; ++i) {
             const int s = i % STAGES;
             const int tl = i / CH, ch = i % CH;
-            const int buf = tl & 1;
+            const int buf = tl % NBUF;
             tmbar_wait(&full[s], (uint32_t)((i / STAGES) & 1));
-            if (ch == 0 && tl >= 2) tmbar_wait(&tempty[buf], (uint32_t)(((tl >> 1) + 1) & 1));
+            if (ch == 0 && tl >= NBUF) tmbar_wait(&tempty[buf], (uint32_t)(((tl / NBUF) + 1) & 1));
             tc_fence_after();
             if (lane == 0) {
                 // QR: the first half of the stages (q plane) accumulates S_q at column 0 of the
@@ -538,7 +540,7 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
             for (int jj = 0; jj < NT; ++jj) t2_n[jj] = __ldg(t2p + jj * t2row);
         }
         for (int tl = 0; tl < ntl; ++tl) {
-            const int buf = tl & 1;
+            const int buf = tl % NBUF;
             const int d = (t0 + tl) * kTileD + m;
             const int32_t sd = sd_n;
             float t2[NT];
@@ -551,7 +553,7 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
 #pragma unroll
                 for (int jj = 0; jj < NT; ++jj) t2_n[jj] = __ldg(t2p + jj * t2row);
             }
-            tmbar_wait(&tfull[buf], (uint32_t)((tl >> 1) & 1));
+            tmbar_wait(&tfull[buf], (uint32_t)((tl / NBUF) & 1));
             tc_fence_after();
             const uint32_t tbase = tmem + ((uint32_t)(lq * 32) << 16) + buf * Cf::ACC + eg * HALF * 8;
             // four ranges (32 columns) per tcgen05.ld, the next group in flight while one is scored
@@ -707,7 +709,7 @@ template <int B, int NSP>
 static size_t tc_smem_bytes() {
     using Cf = TCfg<B>;
     return (size_t)Cf::STAGES * Cf::STAGE_BYTES + Cf::B_BYTES + sizeof(TCRange) * Cf::NR + 4 * Cf::NR +
-           4 * 16 + sizeof(Partial) * Cf::NR * 4 + 8 * (2 * Cf::STAGES + 6) + 16 +
+           4 * 16 + sizeof(Partial) * Cf::NR * 4 + 8 * (2 * Cf::STAGES + 2 * Cf::NBUF + 2) + 16 +
            sizeof(Partial) * Cf::NR * kTileD + sizeof(int2) * 128 * Cf::EWG * 4 + 1024;
 }
 
