@@ -173,15 +173,18 @@ fic_status pool_enqueue(fic_ctx *ctx, Pool &P, const uint8_t *img, int32_t N, in
     if (P.mode == 2)
         CK(fic::launch_pool_gather(img, N, B, L, P.A, P.kept, &P.d_misc[0], tiles_max, P.Dt, st));
     else if (P.mode == 0)
-        CK(fic::launch_pool_tc(img, N, B, L, P.A, P.kept, &P.d_misc[0], tiles_max, P.Dtc, st));
+        CK(fic::launch_pool_tc(img, N, B, L, P.A, P.kept, &P.d_misc[0], tiles_max, P.Dtc, P.SD, P.SDf, P.C,
+                               &P.d_misc[1], st));
     else if (P.mode == 3)
         CK(fic::launch_b2_pool(img, N, L, P.A, P.kept, &P.d_misc[0], slots, P.b_F2.p, &P.b2, st));
     else
         CK(fic::launch_pool_coeff(img, N, B, L, P.A, P.kept, &P.d_misc[0], slots, P.Dc,
                                   reinterpret_cast<unsigned int *>(&P.d_misc[2]), st));
-    CK(fic::launch_pool_moments(img, N, B, L, P.A, P.kept, &P.d_misc[0], slots, P.SD, P.SDf, P.C,
-                                &P.d_misc[1], st));
-    ctx->launches += 6 + (P.mode == 3 ? 1 : 0);  // entropy, select x3, gather, moments (+ sorted gather)
+    const bool fused = P.mode == 0 && fic::tc_pool_has_moments(B);
+    if (!fused)
+        CK(fic::launch_pool_moments(img, N, B, L, P.A, P.kept, &P.d_misc[0], slots, P.SD, P.SDf, P.C,
+                                    &P.d_misc[1], st));
+    ctx->launches += 6 + (P.mode == 3 ? 1 : 0) - (fused ? 1 : 0);  // entropy, select x3, gather, moments
     return FIC_OK;
 }
 

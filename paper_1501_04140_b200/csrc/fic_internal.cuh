@@ -209,9 +209,12 @@ cudaError_t launch_sse(const uint8_t *a, const uint8_t *b, int64_t n, unsigned l
 int tc_supported(int B);
 size_t tc_pool_bytes(int B, int64_t n_tiles);
 int tc_nsplit_hint(int32_t B, int64_t n_r, int64_t n_tiles, int num_sms);
+// also writes SD, SDf, C and Cmax when tc_pool_has_moments(B) (pool_moments_kernel is skipped)
+int tc_pool_has_moments(int B);
 cudaError_t launch_pool_tc(const uint8_t *img, int32_t N, int32_t B, int32_t L, int32_t A,
                            const int32_t *kept, const unsigned long long *d_nk, int64_t n_tiles_max,
-                           uint8_t *Dtc, cudaStream_t st);
+                           uint8_t *Dtc, int32_t *SD, float *SDf, int64_t *C, unsigned long long *d_cmax,
+                           cudaStream_t st);
 size_t tc_range_bytes(int B, int64_t n_r);  // scratch for the prepared range operand + metadata
 cudaError_t launch_tc_search(int32_t B, const SearchParams &sp, const uint8_t *Dtc, int64_t n_slots,
                              uint8_t *scratch, cudaStream_t st);

@@ -170,13 +170,16 @@ template <int B>
 __global__ void __launch_bounds__(256) pool_tc_kernel(const uint8_t *__restrict__ img, int32_t N, int32_t L,
                                                       int32_t A, const int32_t *__restrict__ kept,
                                                       const unsigned long long *__restrict__ d_nk,
-                                                      int64_t total16, uint8_t *__restrict__ Dtc) {
+                                                      int64_t total16, uint8_t *__restrict__ Dtc,
+                                                      int32_t *__restrict__ SD, float *__restrict__ SDf,
+                                                      int64_t *__restrict__ Cm, unsigned long long *d_cmax) {
     using Cf = TCfg<B>;
     const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // one 16-byte group
     if (e >= total16) return;
     const int64_t n_k = (int64_t)*d_nk;
     const int64_t ntiles = (n_k + kTileD - 1) / kTileD;
-    constexpr int G16 = Cf::KP / 16;  // 16-byte groups per row
+    // QR: n/16 threads per domain (16 pixels each, both planes); else one per 16-byte K group
+    constexpr int G16 = Cf::QR ? Cf::n / 16 : Cf::KP / 16;
     const int64_t tile = e / ((int64_t)kTileD * G16);
     if (tile >= ntiles) return;
     const int rem = (int)(e - tile * kTileD * G16);
@@ -188,9 +191,13 @@ __global__ void __launch_bounds__(256) pool_tc_kernel(const uint8_t *__restrict_
         *reinterpret_cast<uint4 *>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
     };
     if constexpr (Cf::QR) {
-        // one thread per 16 pixels writes both planes: q = D' >> 2 at K byte p, r = D' & 3 at n + p
-        if (g >= Cf::n / 16) return;
+        // one thread per 16 pixels writes both planes (q = D' >> 2 at K byte p, r = D' & 3 at
+        // n + p) and the domain moments SD, SDD -> C = n SDD - SD^2 (reduced over the n/16 = 16
+        // threads of the domain, a half warp), which replaces pool_moments_kernel at this level
+        static_assert(Cf::n / 16 == 16, "QR moments assume 16 threads per domain");
         uint32_t wq[4] = {0, 0, 0, 0}, wr[4] = {0, 0, 0, 0};
+        int sd = 0;
+        long long sdd = 0;
         if (d < n_k) {
             const int32_t c = kept[d];
             const int64_t x = (int64_t)(c % A) * L, y = (int64_t)(c / A) * L;
@@ -201,10 +208,24 @@ __global__ void __launch_bounds__(256) pool_tc_kernel(const uint8_t *__restrict_
                 const uint32_t dp = (uint32_t)px[0] + px[1] + px[N] + px[N + 1];
                 wq[q >> 2] |= (dp >> 2) << (8 * (q & 3));
                 wr[q >> 2] |= (dp & 3u) << (8 * (q & 3));
+                sd += (int)dp;
+                sdd += (long long)dp * dp;
             }
         }
         store16(g * 16, wq);
         store16(Cf::n + g * 16, wr);
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) {
+            sd += __shfl_xor_sync(0xffffffffu, sd, o);
+            sdd += __shfl_xor_sync(0xffffffffu, sdd, o);
+        }
+        if (g == 0) {
+            const long long cc = (long long)Cf::n * sdd - (long long)sd * sd;
+            SD[d] = sd;
+            SDf[d] = (float)sd;
+            Cm[d] = cc;
+            if (d < n_k) atomicMax(d_cmax, (unsigned long long)cc);
+        }
     } else {
         uint32_t w[4] = {0, 0, 0, 0};
         if (d < n_k) {
@@ -238,25 +259,28 @@ size_t tc_pool_bytes(int B, int64_t n_tiles) {
     }
 }
 
+int tc_pool_has_moments(int B) { return TCfg<16>::QR && B == 16; }
+
 cudaError_t launch_pool_tc(const uint8_t *img, int32_t N, int32_t B, int32_t L, int32_t A,
                            const int32_t *kept, const unsigned long long *d_nk, int64_t n_tiles_max,
-                           uint8_t *Dtc, cudaStream_t st) {
-    int kp = 0;
+                           uint8_t *Dtc, int32_t *SD, float *SDf, int64_t *C, unsigned long long *d_cmax,
+                           cudaStream_t st) {
+    int g16 = 0;
     switch (B) {
-    case 2: kp = TCfg<2>::KP; break;
-    case 4: kp = TCfg<4>::KP; break;
-    case 8: kp = TCfg<8>::KP; break;
-    case 16: kp = TCfg<16>::KP; break;
+    case 2: g16 = TCfg<2>::KP / 16; break;
+    case 4: g16 = TCfg<4>::KP / 16; break;
+    case 8: g16 = TCfg<8>::KP / 16; break;
+    case 16: g16 = TCfg<16>::QR ? TCfg<16>::n / 16 : TCfg<16>::KP / 16; break;
     default: return cudaErrorInvalidValue;
     }
-    const int64_t total16 = n_tiles_max * kTileD * (kp / 16);
+    const int64_t total16 = n_tiles_max * kTileD * g16;
     if (total16 == 0) return cudaSuccess;
     const unsigned blocks = (unsigned)((total16 + 255) / 256);
     switch (B) {
-    case 2: pool_tc_kernel<2><<<blocks, 256, 0, st>>>(img, N, L, A, kept, d_nk, total16, Dtc); break;
-    case 4: pool_tc_kernel<4><<<blocks, 256, 0, st>>>(img, N, L, A, kept, d_nk, total16, Dtc); break;
-    case 8: pool_tc_kernel<8><<<blocks, 256, 0, st>>>(img, N, L, A, kept, d_nk, total16, Dtc); break;
-    case 16: pool_tc_kernel<16><<<blocks, 256, 0, st>>>(img, N, L, A, kept, d_nk, total16, Dtc); break;
+    case 2: pool_tc_kernel<2><<<blocks, 256, 0, st>>>(img, N, L, A, kept, d_nk, total16, Dtc, SD, SDf, C, d_cmax); break;
+    case 4: pool_tc_kernel<4><<<blocks, 256, 0, st>>>(img, N, L, A, kept, d_nk, total16, Dtc, SD, SDf, C, d_cmax); break;
+    case 8: pool_tc_kernel<8><<<blocks, 256, 0, st>>>(img, N, L, A, kept, d_nk, total16, Dtc, SD, SDf, C, d_cmax); break;
+    case 16: pool_tc_kernel<16><<<blocks, 256, 0, st>>>(img, N, L, A, kept, d_nk, total16, Dtc, SD, SDf, C, d_cmax); break;
     }
     return cudaGetLastError();
 }
