@@ -36,7 +36,7 @@ typedef enum {
     FIC_ERR_EMPTY_POOL = 3, /* no domain block survives the entropy filter                     */
     FIC_ERR_CAPACITY = 4,   /* output buffer too small; *h_n_out holds the required count       */
     FIC_ERR_CUDA = 5,       /* CUDA runtime error (message in fic_last_error)                  */
-    FIC_ERR_NCCL = 6,       /* reserved for the native collective path                         */
+    FIC_ERR_NCCL = 6,       /* NCCL failure (fic_ctx_create_nccl / fic_encode_nccl)            */
     FIC_ERR_NOMEM = 7       /* device or host allocation failed                                */
 } fic_status;
 
@@ -146,6 +146,28 @@ fic_status fic_encode_host(fic_ctx *ctx, const uint8_t *h_img, int32_t N, int32_
                            const int32_t *h_n_s, const double *h_rms_tol, int32_t shard,
                            int32_t n_shards, fic_record *h_out, int64_t capacity,
                            int64_t *h_n_out);
+
+/* ------------------------------------------------------------------------------ multi-GPU */
+
+/* Host-only: a new NCCL unique id (128 bytes) for fic_ctx_create_nccl; create it on one rank and
+ * hand the same bytes to every rank (any out-of-band channel, e.g. torch.distributed).
+ * Errors: ARG, NCCL. */
+fic_status fic_nccl_unique_id(uint8_t *h_id128);
+
+/* fic_ctx_create plus an NCCL communicator of nranks ranks, this process being `rank` (one GPU
+ * per rank; h_id128 from fic_nccl_unique_id).  fic_ctx_destroy releases the communicator.
+ * Errors: ARG, CUDA, NCCL. */
+fic_status fic_ctx_create_nccl(int32_t device, void *cuda_stream, const uint8_t *h_id128, int32_t nranks,
+                               int32_t rank, fic_ctx **out);
+
+/* Sharded fic_encode over the context's communicator: rank r encodes the top-level
+ * blocks t % nranks == r (no exchange on the data path), then an ncclAllGather of the record
+ * counts and one of the records, and the canonical merge; every rank receives the full code
+ * (identical to a one-GPU fic_encode) in `out` (device, capacity records; *h_n_out = count, also
+ * on CAPACITY).  Synchronous.  Errors: as fic_encode; ARG without a communicator; NCCL. */
+fic_status fic_encode_nccl(fic_ctx *ctx, const uint8_t *img, int32_t N, int32_t B_max, int32_t B_min,
+                           int32_t L, const double *h_tau, const double *h_s, const int32_t *h_n_s,
+                           const double *h_rms_tol, fic_record *out, int64_t capacity, int64_t *h_n_out);
 
 /* Merge per-shard record lists (each sorted by B desc, ry, rx) into one canonical list.
  * in: device fic_record [n_shards][stride]; h_counts: host int64 [n_shards]; out: device

@@ -10,7 +10,7 @@ ctypes binding (fic.py) and the multi-GPU sharding driver (dist.py).  It never i
 """
 from .fic import (  # noqa: F401
     Context, Pool, FicError, RECORD_DTYPE, RECORD_BYTES, EXPORTS, records_to_numpy, load,
-    entropy_lut, version, SO_PATH,
+    entropy_lut, version, SO_PATH, nccl_unique_id,
 )
 
 __version__ = "0.1.0"

@@ -38,7 +38,9 @@ def needs_build() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not needs_build():
         return SO
-    cmd = [NVCC, *NVCC_FLAGS, "-I", INCLUDE, "-I", CSRC, "-o", SO + ".tmp", *sources(), "-lquadmath"]
+    # NCCL (fic_ctx_create_nccl / fic_encode_nccl): the system headers and libnccl.so.2; at run
+    # time the soname resolves to the NCCL torch has already loaded, if any
+    cmd = [NVCC, *NVCC_FLAGS, "-I", INCLUDE, "-I", CSRC, "-o", SO + ".tmp", *sources(), "-lquadmath", "-lnccl"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     log = os.path.join(HERE, "build.log")
     with open(log, "w") as f:

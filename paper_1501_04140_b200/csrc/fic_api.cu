@@ -11,6 +11,8 @@
 #include <string>
 #include <vector>
 
+#include <nccl.h>
+
 #include "fic_internal.cuh"
 
 using fic::Buf;
@@ -41,7 +43,9 @@ struct fic_ctx {
     cudaEvent_t main_ready = nullptr;
     int b2_window = 1;    // env FIC_B2_WINDOW=0: B = 2 full scan instead of the C windows
     int search_mode = 0;  // env FIC_SEARCH: auto (default: B=2 closed form, else tcgen05) | fourier | direct | tc
-    Buf b_rc, b_meta, b_u, b_gthr, b_rop, b_dec;  // libfic kernels enqueued (for fic_level_stats.kernel_launches)  // pool start, search start, search end, finalize end, pool end
+    Buf b_rc, b_meta, b_u, b_gthr, b_rop, b_dec, b_nccl;
+    ncclComm_t comm = nullptr;  // fic_ctx_create_nccl: one rank per GPU
+    int32_t nranks = 1, rank = 0;  // libfic kernels enqueued (for fic_level_stats.kernel_launches)  // pool start, search start, search end, finalize end, pool end
 };
 
 namespace {
@@ -398,6 +402,90 @@ fic_status fic_psnr(fic_ctx *ctx, const uint8_t *a, const uint8_t *b, int64_t n,
     return FIC_OK;
 }
 
+// ------------------------------------------------------------------------- NCCL (multi-GPU)
+fic_status fic_nccl_unique_id(uint8_t *h_id128) {
+    if (!h_id128) return FIC_ERR_ARG;
+    static_assert(sizeof(ncclUniqueId) == 128, "NCCL unique id is 128 bytes");
+    ncclUniqueId id;
+    if (ncclGetUniqueId(&id) != ncclSuccess) return FIC_ERR_NCCL;
+    memcpy(h_id128, &id, sizeof id);
+    return FIC_OK;
+}
+
+fic_status fic_ctx_create_nccl(int32_t device, void *cuda_stream, const uint8_t *h_id128, int32_t nranks,
+                               int32_t rank, fic_ctx **out) {
+    if (!out || !h_id128 || nranks < 1 || rank < 0 || rank >= nranks) return FIC_ERR_ARG;
+    fic_status st = fic_ctx_create(device, cuda_stream, out);
+    if (st != FIC_OK) return st;
+    fic_ctx *ctx = *out;
+    ncclUniqueId id;
+    memcpy(&id, h_id128, sizeof id);
+    const ncclResult_t r = ncclCommInitRank(&ctx->comm, nranks, id, rank);
+    if (r != ncclSuccess) {
+        ctx->comm = nullptr;
+        fic_ctx_destroy(ctx);
+        *out = nullptr;
+        return FIC_ERR_NCCL;
+    }
+    ctx->nranks = nranks;
+    ctx->rank = rank;
+    return FIC_OK;
+}
+
+#define CKN(x)                                                                              \
+    do {                                                                                    \
+        const ncclResult_t r_ = (x);                                                        \
+        if (r_ != ncclSuccess) return fail(ctx, FIC_ERR_NCCL, std::string("NCCL: ") + ncclGetErrorString(r_)); \
+    } while (0)
+
+// Rank r encodes the top-level blocks t % nranks == r (no exchange on the data path), then one
+// all-gather of the counts and one of the records (padded to the largest shard) over the
+// communicator, and the canonical merge (B desc, ry, rx) on every rank.
+fic_status fic_encode_nccl(fic_ctx *ctx, const uint8_t *img, int32_t N, int32_t B_max, int32_t B_min, int32_t L,
+                           const double *h_tau, const double *h_s, const int32_t *h_n_s, const double *h_rms_tol,
+                           fic_record *out, int64_t capacity, int64_t *h_n_out) {
+    CKS(ctx_check(ctx));
+    if (h_n_out) *h_n_out = 0;
+    if (!ctx->comm) return fail(ctx, FIC_ERR_ARG, "context has no NCCL communicator (fic_ctx_create_nccl)");
+    if (!h_n_out || (!out && capacity > 0) || capacity < 0) return fail(ctx, FIC_ERR_ARG, "null argument");
+    if (B_min < 1 || N < 1) return fail(ctx, FIC_ERR_ARG, "bad sizes");
+    const int W = ctx->nranks;
+    const int64_t cap_local = (int64_t)(N / B_min) * (N / B_min);
+    // layout of b_nccl: local records [cap_local] | gathered [W][cap_local] | counts [W] | my count
+    const size_t rec_bytes = sizeof(fic_record) * (size_t)cap_local;
+    CK(grow(ctx, ctx->b_nccl, rec_bytes * (size_t)(W + 1) + sizeof(int64_t) * (size_t)(W + 1)));
+    char *base = static_cast<char *>(ctx->b_nccl.p);
+    fic_record *local = reinterpret_cast<fic_record *>(base);
+    fic_record *gathered = reinterpret_cast<fic_record *>(base + rec_bytes);
+    int64_t *d_counts = reinterpret_cast<int64_t *>(base + rec_bytes * (size_t)(W + 1));
+    int64_t *d_mine = d_counts + W;
+    int64_t n_local = 0;
+    CKS(fic_encode(ctx, img, N, B_max, B_min, L, h_tau, h_s, h_n_s, h_rms_tol, ctx->rank, W, local, cap_local,
+                   &n_local));
+    cudaStream_t st = ctx->stream;
+    CK(cudaMemcpyAsync(d_mine, &n_local, sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    CKN(ncclAllGather(d_mine, d_counts, 1, ncclInt64, ctx->comm, st));
+    std::vector<int64_t> counts(W);
+    CK(cudaMemcpyAsync(counts.data(), d_counts, sizeof(int64_t) * W, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    int64_t stride = 1, total = 0;
+    for (int i = 0; i < W; ++i) {
+        stride = std::max(stride, counts[i]);
+        total += counts[i];
+    }
+    // every rank sends `stride` records (entries past its count are not read by the merge)
+    CKN(ncclAllGather(local, gathered, sizeof(fic_record) * (size_t)stride, ncclUint8, ctx->comm, st));
+    *h_n_out = total;
+    if (total > capacity) {
+        CK(cudaStreamSynchronize(st));
+        return fail(ctx, FIC_ERR_CAPACITY, "output capacity too small");
+    }
+    // gathered is [W][stride] contiguous: merge with stride `stride`
+    CK(fic::launch_merge_shards(gathered, d_counts, W, stride, stride, out, st));
+    CK(cudaStreamSynchronize(st));
+    return FIC_OK;
+}
+
 const char *fic_version(void) { return "fic-b200 0.1 (sm_100a; fp32-exact CUDA-core search)"; }
 
 fic_status fic_entropy_lut(int64_t *h_lut, int32_t mmax) {
@@ -472,7 +560,8 @@ fic_status fic_ctx_destroy(fic_ctx *ctx) {
     for (auto &P : ctx->levels) free_pool(P);
     Buf *bufs[] = {&ctx->b_blocksum, &ctx->b_counts, &ctx->b_rng[0], &ctx->b_rng[1], &ctx->b_rec,
                    &ctx->b_acc, &ctx->b_child, &ctx->b_part, &ctx->b_t2f, &ctx->b_img, &ctx->b_out,
-                   &ctx->b_scounts, &ctx->b_rc, &ctx->b_meta, &ctx->b_u, &ctx->b_gthr, &ctx->b_rop, &ctx->b_dec};
+                   &ctx->b_scounts, &ctx->b_rc, &ctx->b_meta, &ctx->b_u, &ctx->b_gthr, &ctx->b_rop, &ctx->b_dec, &ctx->b_nccl};
+    if (ctx->comm) ncclCommDestroy(ctx->comm);
     for (Buf *b : bufs) free_buf(*b);
     if (ctx->d_delta) cudaFree(ctx->d_delta);
     if (ctx->h_counts) cudaFreeHost(ctx->h_counts);

@@ -38,3 +38,18 @@ def sharded_encode(ctx: Context, img, cfg, group=None):
     local = ctx.encode_cfg(cfg, img, shard=rank, n_shards=world)
     allrec, counts, stride = gather_records(local, group)
     return ctx.merge_shards(allrec, counts, stride)
+
+
+def native_context(device: int, group=None, **kw) -> Context:
+    """A Context with the library's own NCCL communicator over the ranks of `group`: rank 0 makes
+    the unique id, torch.distributed hands it to the others (plumbing only)."""
+    from .fic import nccl_unique_id
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    obj = [nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0, group=group)
+    return Context(device, nccl=(obj[0], world, rank), **kw)
+
+
+def native_sharded_encode(ctx: Context, img, cfg):
+    """fic_encode_nccl: shard, NCCL all-gather and merge inside the library."""
+    return ctx.encode_nccl(img, cfg["B_max"], cfg["B_min"], cfg["L"], cfg["tau"], cfg["s"], cfg["rms_tol"])

@@ -31,7 +31,7 @@ EXPORTS = (
     "fic_ctx_set_timing", "fic_get_stats", "fic_build_domain_pool", "fic_pool_info",
     "fic_pool_destroy", "fic_encode_level", "fic_encode", "fic_encode_host", "fic_merge_shards",
     "fic_entropy_lut", "fic_version", "fic_decode", "fic_psnr", "fic_build_domain_pool_topk",
-    "fic_encode_topk",
+    "fic_encode_topk", "fic_nccl_unique_id", "fic_ctx_create_nccl", "fic_encode_nccl",
 )
 
 
@@ -78,6 +78,9 @@ def load(path: str = SO_PATH):
         "fic_decode": ([P, P, i64, i32, i32, i32, P, P, i32, P, P], C.c_int),
         "fic_build_domain_pool_topk": ([P, P, i32, i32, i32, i64, P], C.c_int),
         "fic_encode_topk": ([P, P, i32, i32, i32, i32, P, P, P, P, i32, i32, P, i64, P], C.c_int),
+        "fic_nccl_unique_id": ([P], C.c_int),
+        "fic_ctx_create_nccl": ([i32, P, P, i32, i32, P], C.c_int),
+        "fic_encode_nccl": ([P, P, i32, i32, i32, i32, P, P, P, P, P, i64, P], C.c_int),
         "fic_psnr": ([P, P, P, i64, P], C.c_int),
         "fic_version": ([], C.c_char_p),
     }
@@ -159,7 +162,9 @@ class Pool:
 class Context:
     """A libfic context bound to one CUDA device and the current torch stream."""
 
-    def __init__(self, device: int = 0, stream=None, timing: bool = False):
+    def __init__(self, device: int = 0, stream=None, timing: bool = False, nccl=None):
+        """nccl = (unique_id bytes, nranks, rank): also create the context's NCCL communicator
+        (fic_ctx_create_nccl; the id from nccl_unique_id() on one rank, shared with all)."""
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("libfic needs a CUDA device (no CPU fallback)")
@@ -169,9 +174,15 @@ class Context:
             stream = torch.cuda.current_stream(device)
         self.stream = stream
         h = C.c_void_p()
-        st = self.lib.fic_ctx_create(device, C.c_void_p(stream.cuda_stream), C.byref(h))
+        if nccl is None:
+            st = self.lib.fic_ctx_create(device, C.c_void_p(stream.cuda_stream), C.byref(h))
+        else:
+            uid, nranks, rank = nccl
+            buf = (C.c_uint8 * 128).from_buffer_copy(bytes(uid))
+            st = self.lib.fic_ctx_create_nccl(device, C.c_void_p(stream.cuda_stream), buf, int(nranks),
+                                              int(rank), C.byref(h))
         if st:
-            raise FicError(st, "fic_ctx_create")
+            raise FicError(st, "fic_ctx_create" if nccl is None else "fic_ctx_create_nccl")
         self.handle = h
         self.set_timing(timing)
 
@@ -294,6 +305,21 @@ class Context:
                                               stride, _dptr(out)), "fic_merge_shards")
         return out[: int(cnt.sum())]
 
+    def encode_nccl(self, img, B_max: int, B_min: int, L: int, tau, s_sets, rms_tol, out=None):
+        """Sharded encode over the context's NCCL communicator (fic_encode_nccl): every rank gets
+        the full canonical code (CUDA uint8 [n, 40])."""
+        import torch
+        N = img.shape[0]
+        tau, n_s, s_flat, tol = self._cfg_arrays(tau, s_sets, rms_tol)
+        cap = (N // B_min) ** 2
+        if out is None or out.shape[0] < cap:
+            out = torch.empty((cap, RECORD_BYTES), dtype=torch.uint8, device=img.device)
+        n_out = C.c_int64()
+        self._check(self.lib.fic_encode_nccl(self.handle, _dptr(img), N, B_max, B_min, L, _ptr(tau), _ptr(s_flat),
+                                             _ptr(n_s), _ptr(tol), _dptr(out), out.shape[0], C.byref(n_out)),
+                    "fic_encode_nccl")
+        return out[: n_out.value]
+
     def decode(self, recs, N: int, B_max: int, s_sets, iterations: int = 12, init=None):
         """PIFS decode (fic_decode): CUDA uint8 [n, 40] records -> CUDA uint8 [N, N] image."""
         import torch
@@ -313,6 +339,15 @@ class Context:
         v = C.c_double()
         self._check(self.lib.fic_psnr(self.handle, _dptr(a), _dptr(b), a.numel(), C.byref(v)), "fic_psnr")
         return v.value
+
+
+def nccl_unique_id() -> bytes:
+    """A fresh NCCL unique id (128 bytes) for Context(nccl=(id, nranks, rank))."""
+    buf = (C.c_uint8 * 128)()
+    st = load().fic_nccl_unique_id(buf)
+    if st:
+        raise FicError(st, "fic_nccl_unique_id")
+    return bytes(buf)
 
 
 def records_to_numpy(t) -> np.ndarray:

@@ -409,3 +409,33 @@ def test_more_than_32_s_values_rejected(fic):
     with pytest.raises(p.FicError) as ei:
         ctx.encode(img, 16, 2, 2, [-1] * 4, [tuple(np.linspace(0, 1, 33))] * 4, [8.0] * 4)
     assert ei.value.status == 1
+
+
+# ------------------------------------------------------------------ native NCCL path (8(e))
+def test_native_nccl_single_rank(fic):
+    """fic_ctx_create_nccl / fic_encode_nccl on a one-rank communicator (the box has one GPU):
+    the shard / all-gather / merge path returns the one-GPU code byte for byte.  The multi-rank
+    protocol (t % W shards, gather, canonical merge) is covered by the gloo tests and by
+    test_shards_merge_equals_single."""
+    p, ctx, torch = fic
+    cfg = config("C2", seed=4)
+    img = dev(torch, image_for(cfg))
+    ref = ctx.encode_cfg(cfg, img)
+    nctx = p.Context(0, nccl=(p.nccl_unique_id(), 1, 0))
+    try:
+        got = nctx.encode_nccl(img, cfg["B_max"], cfg["B_min"], cfg["L"], cfg["tau"], cfg["s"], cfg["rms_tol"])
+        assert got.cpu().numpy().tobytes() == ref.cpu().numpy().tobytes()
+        import ctypes as C
+        from paper_1501_04140_b200.fic import _dptr, _ptr
+        small = torch.empty((5, 40), dtype=torch.uint8, device="cuda")
+        tau, n_s, s_flat, tol = nctx._cfg_arrays(cfg["tau"], cfg["s"], cfg["rms_tol"])
+        n_out = C.c_int64()
+        st = nctx.lib.fic_encode_nccl(nctx.handle, _dptr(img), cfg["N"], cfg["B_max"], cfg["B_min"], cfg["L"],
+                                      _ptr(tau), _ptr(s_flat), _ptr(n_s), _ptr(tol), _dptr(small), 5,
+                                      C.byref(n_out))
+        assert st == 4 and n_out.value == ref.shape[0]  # capacity error reports the full count
+    finally:
+        nctx.close()
+    with pytest.raises(p.FicError) as ei:  # no communicator on a plain context
+        ctx.encode_nccl(img, cfg["B_max"], cfg["B_min"], cfg["L"], cfg["tau"], cfg["s"], cfg["rms_tol"])
+    assert ei.value.status == 1
