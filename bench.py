@@ -128,6 +128,24 @@ def load_traffic(kernel_substr: str):
     return None
 
 
+def code_size(cfg, stats):
+    """Size of the code in SPEC's FIC1 layout (15-byte header + 1 byte per level; one
+    split bit per visited range above B_min; per leaf 2 x ceil(log2 A) position bits (A candidate
+    positions per axis, in units of L), 3 isometry bits, ceil(log2 |S_B|) s bits, 8 o bits) and
+    the compression ratio N^2 / bytes (the paper's "Com. rat", Tables 1-2).  Computed from the
+    per-level counts, not by writing the stream."""
+    import math
+    bits = 0
+    for lv, sB in zip(stats, cfg["s"]):
+        A = int(round(math.sqrt(lv["n_candidates"])))
+        leaf = 2 * max(1, math.ceil(math.log2(max(A, 2)))) + 3 + (math.ceil(math.log2(len(sB))) if len(sB) > 1 else 0) + 8
+        bits += lv["n_accepted"] * leaf
+        if lv["B"] > cfg["B_min"]:
+            bits += lv["n_ranges"]
+    nbytes = 15 + len(stats) + (bits + 7) // 8
+    return {"code_bytes_fic1": nbytes, "compression_ratio": cfg["N"] * cfg["N"] / nbytes}
+
+
 # ----------------------------------------------------------------------------- oracle sample
 def oracle_sample(cfg, img, shards: int, shard: int = 0):
     """Time the oracle on every `shards`-th top-level block (+ subtree); returns (pairs, s, threads)."""
@@ -260,6 +278,7 @@ def main():
     d1.synchronize()
     quality = {"psnr_db": ctx.psnr(decoded, img), "decode_iterations": 12,
                "decode_ms": d0.elapsed_time(d1), "note": "sanity report on the synthetic image"}
+    quality.update(code_size(cfg, ctx.stats()))
     total_ms = sum(times)
     pairs_step = sum(s["pairs"] for s in level_acc)
     t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
