@@ -512,8 +512,14 @@ __device__ __forceinline__ double b2_canon(const B2Params &P, double A, float bq
 
 constexpr int kWinStep = 64;  // domains per frontier per round
 
+constexpr int kStash = 64;  // phase-1 candidates kept per warp (overflow: full phase-2 sweep)
+
 __global__ void __launch_bounds__(256) b2win_kernel(const __grid_constant__ B2Params P) {
-    const int lane = threadIdx.x & 31;
+    __shared__ int sStash[8][kStash];
+    __shared__ int sNst[8];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    if (lane == 0) sNst[wib] = 0;
+    __syncwarp();
     const int r = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
     if (blockIdx.x == 0 && threadIdx.x == 0) *P.d_ns = 1ull;
     const int n_r = (int)*P.d_nr;
@@ -583,14 +589,27 @@ __global__ void __launch_bounds__(256) b2win_kernel(const __grid_constant__ B2Pa
                 tv[k * 4 + f] = __ldg(T2 + pos);
             }
         }
-        float g = INFINITY;
+        float g = INFINITY, gv[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
             const float bq = fmaf(R.sx, fv[i].y, fabsf(fmaf(R.x2, fv[i].x, R.dx * fv[i].z)));
-            const float gi = fminf(fmaf(nh0, bq, tv[i].x), fmaf(nh1, bq, tv[i].y));
-            g = fminf(g, ok8[i] ? gi : INFINITY);
+            gv[i] = ok8[i] ? fminf(fmaf(nh0, bq, tv[i].x), fmaf(nh1, bq, tv[i].y)) : INFINITY;
+            g = fminf(g, gv[i]);
         }
         gmin = fminf(gmin, b2_fdec(__reduce_min_sync(0xffffffffu, b2_fkey(g))));
+        {
+            // stash every domain with g <= RU(gmin + 2 margin) (gmin including this round): the
+            // final threshold RU(gmin_final + 2 margin) is never larger, so the stash holds every
+            // pair phase 2 has to score
+            const float ts = fminf(__double2float_ru(__dadd_rn((double)gmin, 2.0 * margin)), FLT_MAX);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                if (gv[i] <= ts) {
+                    const int slot = atomicAdd(&sNst[wib], 1);
+                    if (slot < kStash) sStash[wib][slot] = bf[i & 3] + lane + 32 * (i >> 2);
+                }
+            }
+        }
         const float ub = gmin < INFINITY ? __double2float_ru(__dadd_ru(__dadd_ru(A, (double)gmin), margin)) : INFINITY;
         const float u = sqrtf(fmaxf(ub, 0.f)) * 1.0001f + 1e-3f * (1.f + sqAf);
         const float la = ka * (sqAf - u), lb = kb * (sqAf - u);
@@ -611,12 +630,29 @@ __global__ void __launch_bounds__(256) b2win_kernel(const __grid_constant__ B2Pa
         al3 = (m >> 3) & 1u;
     }
     // phase 2: every pair of the visited runs with g <= thr takes the canonical binary64 path
-    // (thr = RU(gmin + 2 margin) >= best - A + margin; unvisited domains have lb > ub >= best)
+    // (thr = RU(gmin + 2 margin) >= best - A + margin; unvisited domains have lb > ub >= best):
+    // the stashed candidates, or a sweep of the visited runs if the stash overflowed
     float thr = gmin < INFINITY ? fminf(__double2float_ru(__dadd_rn((double)gmin, 2.0 * margin)), FLT_MAX) : -FLT_MAX;
     double be = INFINITY;
     int32_t bd = INT_MAX, bkj = INT_MAX;
     unsigned n_exact = 0;
-    const int nrun = q1 < q2 ? 2 : 1;  // visited: [q0, q1) and [q2, q3), one run once q1 == q2
+    __syncwarp();
+    const int nst = sNst[wib];
+    if (nst <= kStash) {
+        for (int i = lane; i < nst; i += 32) {
+            const int pos = sStash[wib][i];
+            float bq, cf;
+            if (gval(pos, bq, cf) <= thr) {
+                ++n_exact;
+                int j0;
+                const double e0 = b2_canon(P, A, bq, cf, j0);
+                const int32_t d = __ldg(P.ds + pos);
+                const int32_t kj = P.jpos[j0] | kPendIso;
+                if (b2_less(e0, d, kj, be, bd, bkj)) { be = e0; bd = d; bkj = kj; }
+            }
+        }
+    }
+    const int nrun = nst <= kStash ? 0 : (q1 < q2 ? 2 : 1);  // visited: [q0, q1), [q2, q3) (one run once q1 == q2)
     for (int w = 0; w < nrun; ++w) {
         const int a0 = w == 0 ? q0 : q2;
         const int a1 = (w == 0 && nrun == 2) ? q1 : q3;
