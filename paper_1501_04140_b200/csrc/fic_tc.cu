@@ -20,6 +20,7 @@
 // elected thread), warps 2..9 = epilogue (two warpgroups, each half of the ranges; warp w reads
 // TMEM lanes 32 (w % 4) ..).  Pipelines: A stages full/empty (producer <-> MMA), TMEM buffers
 // full/empty (MMA <-> epilogue), two accumulator buffers of N columns.
+#include <algorithm>
 #include <cfloat>
 #include <climits>
 #include <cstring>
@@ -833,6 +834,19 @@ int tc_nsplit_hint(int32_t B, int64_t n_r, int64_t n_tiles, int num_sms) {
     const int64_t max_ns = (n_tiles + 3) / 4;  // at least ~4 tiles per split
     if (ns > max_ns) ns = max_ns;
     if (ns < 1) ns = 1;
+    // B = 16 (one CTA per SM, few range groups): prefer a split count whose last wave is nearly
+    // full (up to 3x more splits).  At B <= 8 every extra split adds a first tile in which every
+    // pair passes the filter, which costs more than the tail it saves.
+    if (B == 16) {
+        auto eff = [&](int64_t k) {
+            const int64_t c = gx * k, w = (c + num_sms - 1) / num_sms;
+            return (double)c / (double)(w * num_sms);
+        };
+        int64_t best = ns;
+        for (int64_t k = ns; k <= std::min<int64_t>(3 * ns, max_ns); ++k)
+            if (eff(k) > eff(best) + 0.05) best = k;
+        ns = best;
+    }
     if (ns > 65535) ns = 65535;
     return (int)ns;
 }
