@@ -248,10 +248,12 @@ __global__ void __launch_bounds__(kSelThreads) select_scatter_kernel(const uint8
 }
 
 struct EmitIndex {
+    static constexpr bool kSmallOk = true;
     int32_t *out;
     __device__ void operator()(int64_t i, int64_t pos) const { out[pos] = (int32_t)i; }
 };
 struct EmitGrid {
+    static constexpr bool kSmallOk = true;
     int2 *out;
     int64_t G;
     int32_t B;
@@ -268,6 +270,7 @@ __device__ __forceinline__ void copy_record(fic_record *dst, const fic_record *s
 }
 
 struct EmitRecord {
+    static constexpr bool kSmallOk = false;
     const fic_record *in;
     fic_record *out;
     const unsigned long long *base;
@@ -278,11 +281,80 @@ struct EmitRecord {
     }
 };
 
+// Small inputs (n <= 1024 x 64, every level of a 512^2 encode): the same order-preserving
+// compaction in one CTA and one launch (contiguous chunk per thread, block scan, scatter).
+constexpr int kSmallPer = 64;
+template <class Emit>
+__global__ void __launch_bounds__(1024) select_small_kernel(const uint8_t *__restrict__ flags, int64_t n, Emit emit,
+                                                            unsigned long long *d_total) {
+    __shared__ int wsum[32];
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const int64_t b0 = (int64_t)t * kSmallPer;  // this thread's 64 flags, kept in registers
+    uint32_t w[kSmallPer / 4];
+    if (b0 + kSmallPer <= n && ((reinterpret_cast<uintptr_t>(flags) & 15) == 0)) {
+#pragma unroll
+        for (int q = 0; q < kSmallPer / 16; ++q) {
+            const uint4 v = *reinterpret_cast<const uint4 *>(flags + b0 + 16 * q);
+            w[4 * q] = v.x; w[4 * q + 1] = v.y; w[4 * q + 2] = v.z; w[4 * q + 3] = v.w;
+        }
+    } else {
+#pragma unroll
+        for (int q = 0; q < kSmallPer / 4; ++q) {
+            uint32_t x = 0;
+            for (int b = 0; b < 4; ++b) {
+                const int64_t i = b0 + 4 * q + b;
+                if (i < n) x |= (uint32_t)(flags[i] & 1) << (8 * b);
+            }
+            w[q] = x;
+        }
+    }
+    int cnt = 0;
+#pragma unroll
+    for (int q = 0; q < kSmallPer / 4; ++q) {
+        w[q] &= 0x01010101u;  // flags are 0/1 bytes
+        cnt += __popc(w[q]);
+    }
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+    }
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        const int ws = wsum[lane];
+        int wi = ws;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, wi, o);
+            if (lane >= o) wi += v;
+        }
+        wsum[lane] = wi - ws;  // exclusive warp offsets
+        if (lane == 31) *d_total = (unsigned long long)wi;
+    }
+    __syncthreads();
+    int64_t pos = wsum[warp] + incl - cnt;
+#pragma unroll
+    for (int q = 0; q < kSmallPer / 4; ++q) {
+        uint32_t x = w[q];
+        while (x) {
+            const int bit = __ffs(x) - 1;  // lowest set flag byte first: index order
+            emit(b0 + 4 * q + (bit >> 3), pos++);
+            x &= x - 1;
+        }
+    }
+}
+
 template <class Emit>
 static cudaError_t select_run(const uint8_t *flags, int64_t n, int64_t *blocksum, Emit emit,
                               unsigned long long *d_total, cudaStream_t st) {
     const int64_t nb = (n + kSelBlock - 1) / kSelBlock;
     if (nb == 0) return cudaMemsetAsync(d_total, 0, sizeof(unsigned long long), st);
+    if (Emit::kSmallOk && n <= 1024 * kSmallPer) {  // not for 40-byte records (one SM would copy them all)
+        select_small_kernel<Emit><<<1, 1024, 0, st>>>(flags, n, emit, d_total);
+        return cudaGetLastError();
+    }
     select_count_kernel<<<(unsigned)nb, kSelThreads, 0, st>>>(flags, n, blocksum);
     select_scan_kernel<<<1, 1024, 0, st>>>(blocksum, nb, d_total);
     select_scatter_kernel<<<(unsigned)nb, kSelThreads, 0, st>>>(flags, n, blocksum, emit);
