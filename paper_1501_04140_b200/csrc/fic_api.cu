@@ -40,6 +40,8 @@ struct fic_ctx {
     cudaStream_t side = nullptr;                 // pool builds of levels >= 1 overlap the searches
     int overlap_pools = 0;                       // env FIC_OVERLAP_POOLS=1
     cudaEvent_t pool_ready[fic::kMaxLevels] = {};
+    cudaEvent_t level_done[fic::kMaxLevels] = {};  // finalize of level l done (records ready)
+    Buf b_blocksum2;  // compaction scratch of the side-stream record gathering
     cudaEvent_t main_ready = nullptr;
     int b2_window = 1;    // env FIC_B2_WINDOW=0: B = 2 full scan instead of the C windows
     int search_mode = 0;  // env FIC_SEARCH: auto (default: B=2 closed form, else tcgen05) | fourier | direct | tc
@@ -532,6 +534,8 @@ fic_status fic_ctx_create(int32_t device, void *cuda_stream, fic_ctx **out) {
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking);
     for (int l = 0; l < fic::kMaxLevels && e == cudaSuccess; ++l)
         e = cudaEventCreateWithFlags(&ctx->pool_ready[l], cudaEventDisableTiming);
+    for (int l = 0; l < fic::kMaxLevels && e == cudaSuccess; ++l)
+        e = cudaEventCreateWithFlags(&ctx->level_done[l], cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->main_ready, cudaEventDisableTiming);
     if (e != cudaSuccess) {
         fic_ctx_destroy(ctx);
@@ -570,6 +574,9 @@ fic_status fic_ctx_destroy(fic_ctx *ctx) {
             if (e) cudaEventDestroy(e);
     for (auto &e : ctx->pool_ready)
         if (e) cudaEventDestroy(e);
+    for (auto &e : ctx->level_done)
+        if (e) cudaEventDestroy(e);
+    free_buf(ctx->b_blocksum2);
     if (ctx->main_ready) cudaEventDestroy(ctx->main_ready);
     if (ctx->side) {
         cudaStreamSynchronize(ctx->side);
@@ -718,9 +725,23 @@ static fic_status encode_impl(fic_ctx *ctx, const uint8_t *img, int32_t N, int32
     CK(grow(ctx, ctx->b_child, (size_t)(Gmin * Gmin) + 16));
     CK(grow(ctx, ctx->b_rng[0], sizeof(int2) * (size_t)(Gmin * Gmin)));
     CK(grow(ctx, ctx->b_rng[1], sizeof(int2) * (size_t)(Gmin * Gmin)));
-    CK(grow(ctx, ctx->b_rec, sizeof(fic_record) * (size_t)(Gmin * Gmin)));
-    CK(grow(ctx, ctx->b_acc, (size_t)(Gmin * Gmin) + 16));
+    // range-count upper bounds of every level, and per-level slices of the record / accepted
+    // buffers: the records of level l are gathered into `out` on the side stream while the main
+    // stream already searches level l + 1, so levels must not share these buffers
+    std::vector<int64_t> nr_bound(nl + 1, 0), rec_off(nl + 1, 0);
+    {
+        int64_t nb = G * G > shard ? (G * G - shard + n_shards - 1) / n_shards : 0;
+        for (int l = 0; l < nl; ++l) {
+            nr_bound[l] = nb;
+            rec_off[l + 1] = rec_off[l] + nb + 16;
+            const int64_t Gc = N / std::max<int32_t>((B_max >> l) / 2, 1);
+            nb = std::min<int64_t>(4 * nb, Gc * Gc);
+        }
+    }
+    CK(grow(ctx, ctx->b_rec, sizeof(fic_record) * (size_t)rec_off[nl]));
+    CK(grow(ctx, ctx->b_acc, (size_t)rec_off[nl] + 16));
     CK(grow(ctx, ctx->b_blocksum, sizeof(int64_t) * fic::select_blocksum_len(Gmin * Gmin)));
+    CK(grow(ctx, ctx->b_blocksum2, sizeof(int64_t) * fic::select_blocksum_len(Gmin * Gmin)));
     // 1. pools: level 0 on the main stream; levels >= 1 on the side stream, overlapping the
     //    level-0 search (pools depend only on the image)
     CK(cudaEventRecord(ctx->main_ready, st));  // the image is ready (caller's stream order)
@@ -755,13 +776,17 @@ static fic_status encode_impl(fic_ctx *ctx, const uint8_t *img, int32_t N, int32
         bound[l] = n_r_max;
         if (l > 0) CK(cudaStreamWaitEvent(st, ctx->pool_ready[l], 0));
         if (!last) CK(cudaMemsetAsync(child, 0, (size_t)(Gc * Gc), st));
+        fic_record *rec_l = ptr<fic_record>(ctx->b_rec) + rec_off[l];
+        uint8_t *acc_l = ptr<uint8_t>(ctx->b_acc) + rec_off[l];
         CKS(level_enqueue(ctx, P, img, ptr<int2>(ctx->b_rng[cur]), d_counts + 32 + l, n_r_max, h_s + s_off[l],
-                          h_n_s[l], h_rms_tol[l], last, ptr<fic_record>(ctx->b_rec), ptr<uint8_t>(ctx->b_acc),
-                          last ? nullptr : child, l, d_err));
-        CK(fic::launch_select_records(ptr<uint8_t>(ctx->b_acc), n_r_max, ptr<int64_t>(ctx->b_blocksum),
-                                      ptr<fic_record>(ctx->b_rec), out, d_counts + 0, capacity, d_counts + 16 + l,
-                                      st));
-        CK(fic::launch_accumulate(d_counts + 0, d_counts + 16 + l, st));
+                          h_n_s[l], h_rms_tol[l], last, rec_l, acc_l, last ? nullptr : child, l, d_err));
+        // the accepted records of this level go to `out` on the side stream (in level order, after
+        // the pools there), off the critical path of the next level's search
+        CK(cudaEventRecord(ctx->level_done[l], st));
+        CK(cudaStreamWaitEvent(ctx->side, ctx->level_done[l], 0));
+        CK(fic::launch_select_records(acc_l, n_r_max, ptr<int64_t>(ctx->b_blocksum2), rec_l, out, d_counts + 0,
+                                      capacity, d_counts + 16 + l, ctx->side));
+        CK(fic::launch_accumulate(d_counts + 0, d_counts + 16 + l, ctx->side));
         ctx->launches += 4;
         if (!last) {
             CK(fic::launch_select_grid(child, Gc, B / 2, ptr<int64_t>(ctx->b_blocksum),
@@ -773,9 +798,11 @@ static fic_status encode_impl(fic_ctx *ctx, const uint8_t *img, int32_t N, int32
         ctx->launches = 0;
         cur ^= 1;
     }
-    // 4. join the side stream (pools of levels the quadtree never reached), then one device -> host
-    //    read of every counter and one synchronisation
+    // 4. join the side stream (record gathering, pools of levels the quadtree never reached),
+    //    then one device -> host read of every counter and one synchronisation
     for (int l = 1; l < nl; ++l) CK(cudaStreamWaitEvent(st, ctx->pool_ready[l], 0));
+    CK(cudaEventRecord(ctx->main_ready, ctx->side));
+    CK(cudaStreamWaitEvent(st, ctx->main_ready, 0));
     CK(cudaMemcpyAsync(ctx->h_counts, d_counts, 64 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     const unsigned long long *h = ctx->h_counts;
