@@ -295,6 +295,18 @@ __global__ void __launch_bounds__(256) tc_range_operand_kernel(const uint8_t *__
                                                                const unsigned long long *__restrict__ d_nr,
                                                                int64_t total16, uint8_t *__restrict__ Bop) {
     using Cf = TCfg<B>;
+    // source pixel of byte p of row k: Rperm_k(p) = R(f_k^{-1}(p)); under this numbering
+    // f_k^{-1} = f_{k'} with k' = [0,3,2,1,4,5,6,7][k] (rotations by 90/270 swap, the rest are
+    // involutions) -- tabulated once per block
+    __shared__ uint8_t src[8][Cf::n];
+    for (int t = threadIdx.x; t < 8 * Cf::n; t += blockDim.x) {
+        const int kk = t / Cf::n, p = t % Cf::n;
+        const int kinv = (kk == 1) ? 3 : (kk == 3 ? 1 : kk);
+        int si, sj;
+        tiso_src(B, kinv, p / B, p % B, si, sj);
+        src[kk][p] = (uint8_t)(si * B + sj);
+    }
+    __syncthreads();
     const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // one 16-byte group
     if (e >= total16) return;
     const int64_t n_r = (int64_t)*d_nr;
@@ -309,18 +321,14 @@ __global__ void __launch_bounds__(256) tc_range_operand_kernel(const uint8_t *__
     uint32_t w[4] = {0, 0, 0, 0};
     if (r < n_r) {
         const int2 rr = ranges[r];
-        // Rperm_k(p) = R(f_k^{-1}(p)); under this numbering f_k^{-1} = f_{k'} with
-        // k' = [0,3,2,1,4,5,6,7][k] (rotations by 90/270 swap, the rest are involutions)
-        const int kinv = (k == 1) ? 3 : (k == 3 ? 1 : k);
+        const uint8_t *rb = img + (size_t)rr.y * N + rr.x;
 #pragma unroll
         for (int q = 0; q < 16; ++q) {
             const int kb = g * 16 + q;
             uint32_t v = 0;
             if (kb < (Cf::QR ? Cf::n : 4 * Cf::n)) {  // 4 polyphase copies, or once (QR)
-                const int p = kb % Cf::n;
-                int si, sj;
-                tiso_src(B, kinv, p / B, p % B, si, sj);
-                v = img[(size_t)(rr.y + si) * N + rr.x + sj];
+                const int sp = src[k][kb % Cf::n];
+                v = rb[(size_t)(sp / B) * N + sp % B];
             }
             w[q >> 2] |= v << (8 * (q & 3));
         }
@@ -341,7 +349,10 @@ __global__ void tc_range_meta_kernel(const uint8_t *__restrict__ img, int32_t N,
                                      const unsigned long long *__restrict__ d_nr, int32_t n_pad, double smax,
                                      const unsigned long long *__restrict__ d_misc,
                                      TCRangeG *__restrict__ meta, int32_t univ) {
-    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    // B >= 8: a warp per range (lanes over the pixels), else a thread per range
+    constexpr int TPR = B >= 8 ? 32 : 1;
+    const int gt = blockIdx.x * blockDim.x + threadIdx.x;
+    const int r = gt / TPR, sub = gt % TPR;
     if (r >= n_pad) return;
     const int n_r = (int)*d_nr;
     const double cmax = (double)d_misc[1];
@@ -351,15 +362,19 @@ __global__ void tc_range_meta_kernel(const uint8_t *__restrict__ img, int32_t N,
     R.valid = r < n_r;
     if (R.valid) {
         const int2 rr = ranges[r];
-        for (int i = 0; i < B; ++i) {
-            const uint8_t *row = img + (size_t)(rr.y + i) * N + rr.x;
-#pragma unroll
-            for (int j = 0; j < B; ++j) {
-                const int v = row[j];
-                sr += v;
-                srr += v * v;
-            }
+        for (int p = sub; p < n; p += TPR) {
+            const int v = img[(size_t)(rr.y + p / B) * N + rr.x + p % B];
+            sr += v;
+            srr += v * v;
         }
+    }
+    if constexpr (TPR > 1) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            sr += __shfl_xor_sync(0xffffffffu, sr, o);
+            srr += __shfl_xor_sync(0xffffffffu, srr, o);
+        }
+        if (sub != 0) return;
     }
     R.A = (double)((long long)n * srr - sr * sr);
     R.SR = (int32_t)sr;
@@ -785,7 +800,8 @@ static cudaError_t tc_range_prep(const SearchParams &sp, uint8_t *scratch, TCPar
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     const int n_pad = (int)(groups * Cf::NR);
-    tc_range_meta_kernel<B><<<(unsigned)((n_pad + 127) / 128), 128, 0, st>>>(sp.img, sp.N, sp.ranges, sp.d_nr,
+    const int64_t meta_threads = (int64_t)n_pad * (B >= 8 ? 32 : 1);
+    tc_range_meta_kernel<B><<<(unsigned)((meta_threads + 127) / 128), 128, 0, st>>>(sp.img, sp.N, sp.ranges, sp.d_nr,
                                                                               n_pad, sp.smax, sp.d_misc, meta,
                                                                               sp.nsp > 2 ? 1 : 0);
     p.Bop = Bop;
