@@ -579,6 +579,79 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
 #pragma unroll
             for (int jj = 0; jj < NT; ++jj) t2_n[jj] = __ldg(t2p + jj * t2row);
         }
+        // fp32 filter score of one (range, domain) pair from the max over isometries of SRD_k
+        auto score = [&](int mx, int rsr, int32_t sd, const float *t2) -> float {
+            float bq;
+            if constexpr (NSP == 0) {
+                // exact Bq (int64 at B = 16), one RN conversion
+                bq = (float)((long long)n * mx - (long long)rsr * sd);
+            } else if constexpr (B == 2) {
+                // |Bq| <= sqrt(A C) < 2^22: exact int -> float by the 1.5 * 2^23 magic
+                bq = __int_as_float(n * mx - rsr * sd + 0x4B400000) - 12582912.0f;
+            } else if constexpr (B == 4) {
+                // |Bq| <= n^2 127.5 510 < 2^24: magic on Bq / 2, error <= 1 (margin)
+                bq = __int_as_float(((n * mx - rsr * sd) >> 1) + 0x4B400000) - 12582912.0f;  // (x 2 in nhs)
+            } else if constexpr (B == 8) {
+                // |Bq| < 2^28: magic on Bq / 64, error <= 64 (margin)
+                bq = __int_as_float(((n * mx - rsr * sd) >> 6) + 0x4B400000) - 12582912.0f;  // (x 64 in nhs)
+            } else {
+                bq = fmaf((float)n, (float)mx, -((float)rsr * (float)sd));
+            }
+            float g0;
+            if constexpr (NSP == 0) {
+                g0 = -(bq * bq) * t2[0];  // >= -(Bq^2 / C)(1 + 4.04u): continuous minimum
+            } else {
+                g0 = fmaf(nhs[0], bq, t2[0]);
+#pragma unroll
+                for (int jj = 1; jj < NSP; ++jj) g0 = fminf(g0, fmaf(nhs[jj], bq, t2[jj]));
+            }
+            return g0;
+        };
+        if constexpr (NSP > 0) {
+            // ---- seed the thresholds from the first tile: with NSP > 0, g approximates
+            // min_{s > 0} e_s - A within the margin, so every range's best is <= A + min_m g + margin
+            // and RU(min_m g + 2 margin) is a valid threshold -- the first tile no longer sends every
+            // pair better than s = 0 to the exact path
+            if (ntl > 0) {
+                tmbar_wait(&tfull[0], 0u);
+                tc_fence_after();
+                const uint32_t tb0 = tmem + ((uint32_t)(lq * 32) << 16) + eg * HALF * 8;
+#pragma unroll 1
+                for (int g = 0; g < HALF / 4; ++g) {
+                    uint32_t sv[64];
+                    tc_ld32<0>(tb0 + g * 32, sv);
+                    if constexpr (Cf::QR) {
+                        tc_ld32<32>(tb0 + NN, sv);
+                        tc_wait_ld();
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) sv[i] = 4u * sv[i] + sv[32 + i];
+                    } else {
+                        tc_wait_ld();
+                    }
+#pragma unroll
+                    for (int q4 = 0; q4 < 4; ++q4) {
+                        const int q = g * 4 + q4;
+                        const uint32_t *v = sv + q4 * 8;
+                        const int mx = max(__vimax3_s32((int)v[0], (int)v[1], (int)v[2]),
+                                           __vimax3_s32((int)v[3], (int)v[4], __vimax3_s32((int)v[5], (int)v[6], (int)v[7])));
+                        float gm = score(mx, rSR[q], sd_n, t2_n);
+#pragma unroll
+                        for (int o = 16; o > 0; o >>= 1) gm = fminf(gm, __shfl_xor_sync(0xffffffffu, gm, o));
+                        if (lane == 0) {
+                            const float t = fminf(__fadd_ru(gm, __double2float_ru(2.0 * sR[eg * HALF + q].margin)), FLT_MAX);
+                            int *ti = reinterpret_cast<int *>(&sThr[eg * HALF + q]);
+                            int old = *ti;
+                            while (t < __int_as_float(old)) {  // (NaN / +inf pads never lower it)
+                                const int prev = atomicCAS(ti, old, __float_as_int(t));
+                                if (prev == old) break;
+                                old = prev;
+                            }
+                        }
+                    }
+                }
+                asm volatile("bar.sync %0, 128;" ::"r"(1 + eg) : "memory");  // the warpgroup's seeds
+            }
+        }
         for (int tl = 0; tl < ntl; ++tl) {
             const int buf = tl % NBUF;
             const int d = (t0 + tl) * kTileD + m;
@@ -624,31 +697,7 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
                     const int mx = max(__vimax3_s32((int)v[0], (int)v[1], (int)v[2]),
                                        __vimax3_s32((int)v[3], (int)v[4], __vimax3_s32((int)v[5], (int)v[6], (int)v[7])));
                     mxs[q4] = mx;
-                    const int rsr = rSR[q];
-                    float bq;
-                    if constexpr (NSP == 0) {
-                        // exact Bq (int64 at B = 16), one RN conversion
-                        bq = (float)((long long)n * mx - (long long)rsr * sd);
-                    } else if constexpr (B == 2) {
-                        // |Bq| <= sqrt(A C) < 2^22: exact int -> float by the 1.5 * 2^23 magic
-                        bq = __int_as_float(n * mx - rsr * sd + 0x4B400000) - 12582912.0f;
-                    } else if constexpr (B == 4) {
-                        // |Bq| <= n^2 127.5 510 < 2^24: magic on Bq / 2, error <= 1 (margin)
-                        bq = __int_as_float(((n * mx - rsr * sd) >> 1) + 0x4B400000) - 12582912.0f;  // (x 2 in nhs)
-                    } else if constexpr (B == 8) {
-                        // |Bq| < 2^28: magic on Bq / 64, error <= 64 (margin)
-                        bq = __int_as_float(((n * mx - rsr * sd) >> 6) + 0x4B400000) - 12582912.0f;  // (x 64 in nhs)
-                    } else {
-                        bq = fmaf((float)n, (float)mx, -((float)rsr * (float)sd));
-                    }
-                    float g0;
-                    if constexpr (NSP == 0) {
-                        g0 = -(bq * bq) * t2[0];  // >= -(Bq^2 / C)(1 + 4.04u): continuous minimum
-                    } else {
-                        g0 = fmaf(nhs[0], bq, t2[0]);
-#pragma unroll
-                        for (int jj = 1; jj < NSP; ++jj) g0 = fminf(g0, fmaf(nhs[jj], bq, t2[jj]));
-                    }
+                    const float g0 = score(mx, rSR[q], sd, t2);
                     pm |= (g0 <= sThr[eg * HALF + q]) ? (1u << q4) : 0u;
                 }
                 if (pm) {  // queue (q, k*, max SRD) of the passing ranges for the exact path
