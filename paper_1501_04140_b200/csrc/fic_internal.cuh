@@ -118,6 +118,23 @@ struct FinalizeParams {
 
 // Dynamic mapping of a CTA to (range group, domain split) from the actual counts: the grid is
 // sized from host upper bounds; ns = min(ns_cap, ctas / groups, tiles / min_tiles) splits.
+// Max of v over the block, one global atomicMax per block (same-address atomics from every
+// thread serialise in L2). Every thread of the block must call it (no early returns before).
+__device__ __forceinline__ void block_max_atomic(unsigned long long v, unsigned long long *dst) {
+    __shared__ unsigned long long s_max[32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long w = __shfl_xor_sync(0xffffffffu, v, o);
+        v = w > v ? w : v;
+    }
+    if ((threadIdx.x & 31) == 0) s_max[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) v = s_max[w] > v ? s_max[w] : v;
+        if (v) atomicMax(dst, v);
+    }
+}
+
 __device__ __forceinline__ bool cta_work(int n_r, int rpc, int n_tiles, int min_tiles, int ns_cap, int &group,
                                          int &split, int &ns) {
     const int groups = (n_r + rpc - 1) / rpc;

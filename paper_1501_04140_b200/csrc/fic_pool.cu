@@ -452,13 +452,12 @@ __global__ void __launch_bounds__(256) pool_moments_kernel(const uint8_t *__rest
                                                            unsigned long long *d_cmax) {
     const int64_t d = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
-    if (d >= n_slots) return;
     const int64_t n_k = (int64_t)*d_nk;
     const int64_t ntiles = (n_k + kTileD - 1) / kTileD;
-    if (d >= ntiles * kTileD) return;
+    const bool live = d < n_slots && d < ntiles * kTileD;  // (no early return: block_max_atomic)
     const int n = B * B;
     int64_t sd = 0, sdd = 0;
-    if (d < n_k) {
+    if (live && d < n_k) {
         const int32_t c = kept[d];
         const int64_t x = (int64_t)(c % A) * L, y = (int64_t)(c / A) * L;
         for (int p = lane; p < n; p += 32) {
@@ -474,13 +473,13 @@ __global__ void __launch_bounds__(256) pool_moments_kernel(const uint8_t *__rest
         sd += __shfl_xor_sync(0xffffffffu, sd, o);
         sdd += __shfl_xor_sync(0xffffffffu, sdd, o);
     }
-    if (lane == 0) {
-        const int64_t cc = (int64_t)n * sdd - sd * sd;
+    const int64_t cc = (int64_t)n * sdd - sd * sd;
+    if (lane == 0 && live) {
         SD[d] = (int32_t)sd;
         SDf[d] = (float)sd;
         C[d] = cc;
-        if (d < n_k) atomicMax(d_cmax, (unsigned long long)cc);
     }
+    block_max_atomic(live && d < n_k ? (unsigned long long)cc : 0ull, d_cmax);
 }
 
 cudaError_t launch_pool_moments(const uint8_t *img, int32_t N, int32_t B, int32_t L, int32_t A,

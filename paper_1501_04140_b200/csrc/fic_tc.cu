@@ -176,13 +176,14 @@ __global__ void __launch_bounds__(256) pool_tc_kernel(const uint8_t *__restrict_
                                                       int64_t *__restrict__ Cm, unsigned long long *d_cmax) {
     using Cf = TCfg<B>;
     const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // one 16-byte group
-    if (e >= total16) return;
     const int64_t n_k = (int64_t)*d_nk;
     const int64_t ntiles = (n_k + kTileD - 1) / kTileD;
     // QR: n/16 threads per domain (16 pixels each, both planes); else one per 16-byte K group
     constexpr int G16 = Cf::QR ? Cf::n / 16 : Cf::KP / 16;
     const int64_t tile = e / ((int64_t)kTileD * G16);
-    if (tile >= ntiles) return;
+    // (QR: no early return -- the block reduces Cmax with one atomic)
+    if (!Cf::QR && (e >= total16 || tile >= ntiles)) return;
+    const bool live = e < total16 && tile < ntiles;
     const int rem = (int)(e - tile * kTileD * G16);
     const int m = rem / G16, g = rem % G16;
     const int64_t d = tile * kTileD + m;
@@ -199,34 +200,58 @@ __global__ void __launch_bounds__(256) pool_tc_kernel(const uint8_t *__restrict_
         uint32_t wq[4] = {0, 0, 0, 0}, wr[4] = {0, 0, 0, 0};
         int sd = 0;
         long long sdd = 0;
-        if (d < n_k) {
+        if (live && d < n_k) {
+            // thread g = decimated row g: source rows y + 2g, y + 2g + 1, bytes x .. x + 31, read as
+            // aligned 32-bit words (byte shift x % 4; with N % 4 == 0 the 9th word, read only for a
+            // nonzero shift, ends at or before the row's last byte) and summed two pixels per 16-bit lane
             const int32_t c = kept[d];
             const int64_t x = (int64_t)(c % A) * L, y = (int64_t)(c / A) * L;
+            const uint8_t *r0 = img + (y + 2 * g) * N + x;
+            const uint32_t *w0 = reinterpret_cast<const uint32_t *>(reinterpret_cast<uintptr_t>(r0) & ~(uintptr_t)3);
+            const uint32_t *w1 = w0 + N / 4;
+            const uint32_t sh = (uint32_t)(reinterpret_cast<uintptr_t>(r0) & 3) * 8;
+            uint32_t u0[9], u1[9];
 #pragma unroll
-            for (int q = 0; q < 16; ++q) {
-                const int p = g * 16 + q, i = p / B, j = p % B;
-                const uint8_t *px = img + (y + 2 * i) * N + x + 2 * j;
-                const uint32_t dp = (uint32_t)px[0] + px[1] + px[N] + px[N + 1];
-                wq[q >> 2] |= (dp >> 2) << (8 * (q & 3));
-                wr[q >> 2] |= (dp & 3u) << (8 * (q & 3));
-                sd += (int)dp;
-                sdd += (long long)dp * dp;
+            for (int k = 0; k < 8; ++k) { u0[k] = __ldg(w0 + k); u1[k] = __ldg(w1 + k); }
+            u0[8] = sh ? __ldg(w0 + 8) : 0u;
+            u1[8] = sh ? __ldg(w1 + 8) : 0u;
+#pragma unroll
+            for (int k = 0; k < 8; k += 2) {
+                uint32_t sq[2], sr2[2];
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const uint32_t v0 = __funnelshift_r(u0[k + h], u0[k + h + 1], sh);
+                    const uint32_t v1 = __funnelshift_r(u1[k + h], u1[k + h + 1], sh);
+                    // 16-bit lanes: D'_{2(k+h)}, D'_{2(k+h)+1} (<= 1020)
+                    const uint32_t dd = (v0 & 0x00FF00FFu) + ((v0 >> 8) & 0x00FF00FFu) +
+                                        (v1 & 0x00FF00FFu) + ((v1 >> 8) & 0x00FF00FFu);
+                    const int da = (int)(dd & 0xFFFFu), db = (int)(dd >> 16);
+                    sd += da + db;
+                    sdd += (long long)(da * da + db * db);
+                    sq[h] = (dd >> 2) & 0x00FF00FFu;
+                    sr2[h] = dd & 0x00030003u;
+                }
+                // bytes in K order: [lo(h0), hi(h0), lo(h1), hi(h1)]
+                wq[k >> 1] = __byte_perm(sq[0], sq[1], 0x6420);
+                wr[k >> 1] = __byte_perm(sr2[0], sr2[1], 0x6420);
             }
         }
-        store16(g * 16, wq);
-        store16(Cf::n + g * 16, wr);
+        if (live) {
+            store16(g * 16, wq);
+            store16(Cf::n + g * 16, wr);
+        }
 #pragma unroll
         for (int o = 8; o > 0; o >>= 1) {
             sd += __shfl_xor_sync(0xffffffffu, sd, o);
             sdd += __shfl_xor_sync(0xffffffffu, sdd, o);
         }
-        if (g == 0) {
-            const long long cc = (long long)Cf::n * sdd - (long long)sd * sd;
+        const long long cc = (long long)Cf::n * sdd - (long long)sd * sd;
+        if (g == 0 && live) {
             SD[d] = sd;
             SDf[d] = (float)sd;
             Cm[d] = cc;
-            if (d < n_k) atomicMax(d_cmax, (unsigned long long)cc);
         }
+        block_max_atomic(g == 0 && live && d < n_k ? (unsigned long long)cc : 0ull, d_cmax);
     } else {
         uint32_t w[4] = {0, 0, 0, 0};
         if (d < n_k) {
