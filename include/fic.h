@@ -63,7 +63,9 @@ fic_status fic_ctx_destroy(fic_ctx *ctx);
 const char *fic_last_error(const fic_ctx *ctx);
 
 /* Per-level counters and device times of the last fic_encode / fic_encode_level on ctx.
- * Times are CUDA-event durations on the ctx stream (ms); enable with fic_ctx_set_timing. */
+ * Times are CUDA-event durations on the ctx stream (ms); enable with fic_ctx_set_timing:
+ * 1 = ms_search only (two events per level around the search launches), 2 = also ms_pool and
+ * ms_finalize (five events per level; the extra events cost device time), 0 = off. */
 typedef struct {
     int32_t B;
     int64_t n_candidates, n_kept, n_ranges, n_accepted;

@@ -342,7 +342,7 @@ fic_status level_enqueue(fic_ctx *ctx, const Pool &P, const uint8_t *img, const 
     if (acc) CK(cudaMemsetAsync(acc, 0, (size_t)n_r_max, st));
     CK(fic::launch_finalize(fp, st));
     ctx->launches += 1;
-    if (ctx->timing) CK(cudaEventRecord(ctx->ev[level_slot][3], st));
+    if (ctx->timing >= 2) CK(cudaEventRecord(ctx->ev[level_slot][3], st));
     return FIC_OK;
 }
 
@@ -553,7 +553,7 @@ fic_status fic_ctx_set_stream(fic_ctx *ctx, void *cuda_stream) {
 
 fic_status fic_ctx_set_timing(fic_ctx *ctx, int32_t enable) {
     if (!ctx) return FIC_ERR_ARG;
-    ctx->timing = enable != 0;
+    ctx->timing = enable < 0 ? 0 : (enable > 2 ? 2 : enable);
     return FIC_OK;
 }
 
@@ -749,10 +749,10 @@ static fic_status encode_impl(fic_ctx *ctx, const uint8_t *img, int32_t N, int32
     for (int l = 0; l < nl; ++l) {
         cudaStream_t ps = (l == 0 || !ctx->overlap_pools) ? st : ctx->side;
         ctx->launches = 0;
-        if (ctx->timing) CK(cudaEventRecord(ctx->ev[l][0], ps));
+        if (ctx->timing >= 2) CK(cudaEventRecord(ctx->ev[l][0], ps));
         CKS(pool_enqueue(ctx, ctx->levels[l], img, N, B_max >> l, L, h_topk ? -1.0 : h_tau[l],
                          h_topk ? h_topk[l] : 0, ps));
-        if (ctx->timing) CK(cudaEventRecord(ctx->ev[l][4], ps));
+        if (ctx->timing >= 2) CK(cudaEventRecord(ctx->ev[l][4], ps));
         if (l > 0) CK(cudaEventRecord(ctx->pool_ready[l], ps));
         ctx->stats[l].kernel_launches = ctx->launches;
     }
@@ -804,6 +804,9 @@ static fic_status encode_impl(fic_ctx *ctx, const uint8_t *img, int32_t N, int32
     CK(cudaEventRecord(ctx->main_ready, ctx->side));
     CK(cudaStreamWaitEvent(st, ctx->main_ready, 0));
     CK(cudaMemcpyAsync(ctx->h_counts, d_counts, 64 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    for (int l = 0; l < nl; ++l)  // pool counters (n_kept) of the levels
+        CK(cudaMemcpyAsync(ctx->h_counts + 48 + l, ctx->levels[l].d_misc, sizeof(unsigned long long),
+                           cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     const unsigned long long *h = ctx->h_counts;
     if (*reinterpret_cast<const int32_t *>(h + 24) == FIC_ERR_EMPTY_POOL)
@@ -818,12 +821,6 @@ static fic_status encode_impl(fic_ctx *ctx, const uint8_t *img, int32_t N, int32
         ls.exact_evals = (int64_t)h[8 + l];
         ls.n_kept = -1;  // filled below from the pool counters
     }
-    // pool counters (n_kept) of the levels
-    for (int l = 0; l < nl; ++l) {
-        CK(cudaMemcpyAsync(ctx->h_counts + 48 + l, ctx->levels[l].d_misc, sizeof(unsigned long long),
-                           cudaMemcpyDeviceToHost, st));
-    }
-    CK(cudaStreamSynchronize(st));
     for (int l = 0; l < nl; ++l) {
         fic_level_stats &ls = ctx->stats[l];
         ls.n_kept = (int64_t)ctx->h_counts[48 + l];
@@ -837,9 +834,11 @@ static fic_status encode_impl(fic_ctx *ctx, const uint8_t *img, int32_t N, int32
             fic_level_stats &ls = ctx->stats[l];
             if (bound[l] == 0) continue;
             float a = 0, b = 0, c = 0;
-            cudaEventElapsedTime(&a, ctx->ev[l][0], ctx->ev[l][4]);
             cudaEventElapsedTime(&b, ctx->ev[l][1], ctx->ev[l][2]);
-            cudaEventElapsedTime(&c, ctx->ev[l][2], ctx->ev[l][3]);
+            if (ctx->timing >= 2) {
+                cudaEventElapsedTime(&a, ctx->ev[l][0], ctx->ev[l][4]);
+                cudaEventElapsedTime(&c, ctx->ev[l][2], ctx->ev[l][3]);
+            }
             ls.ms_pool = a; ls.ms_search = b; ls.ms_finalize = c;
         }
     }

@@ -197,8 +197,9 @@ class Context:
         self._check(self.lib.fic_ctx_set_stream(self.handle, C.c_void_p(stream.cuda_stream)),
                     "fic_ctx_set_stream")
 
-    def set_timing(self, on: bool):
-        self._check(self.lib.fic_ctx_set_timing(self.handle, int(bool(on))), "fic_ctx_set_timing")
+    def set_timing(self, on):
+        """0/False off, 1/True search times only, 2 also pool and finalize times."""
+        self._check(self.lib.fic_ctx_set_timing(self.handle, int(on)), "fic_ctx_set_timing")
 
     def stats(self):
         arr = (LevelStats * 16)()
