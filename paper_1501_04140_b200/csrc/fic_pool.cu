@@ -6,6 +6,7 @@
 //   select_*             row-major compaction (kept list, next-level ranges, accepted records)
 //   pool_gather_kernel   P:30 "decimated domain block": D'(i,j) = 2x2 sum  [R1]
 //   pool_moments_kernel  SD = sum D', SDD = sum D'^2, C = n SDD - SD^2 (int64, exact)
+#include <atomic>
 #include <cfloat>
 #include <cstdio>
 
@@ -248,17 +249,18 @@ __global__ void __launch_bounds__(kSelThreads) select_scatter_kernel(const uint8
 }
 
 struct EmitIndex {
-    static constexpr bool kSmallOk = true;
+    static constexpr bool kChainOk = true;
     int32_t *out;
     __device__ void operator()(int64_t i, int64_t pos) const { out[pos] = (int32_t)i; }
 };
 struct EmitGrid {
-    static constexpr bool kSmallOk = true;
+    static constexpr bool kChainOk = true;
     int2 *out;
     int64_t G;
     int32_t B;
-    __device__ void operator()(int64_t i, int64_t pos) const {
-        out[pos] = make_int2((int)(i % G) * B, (int)(i / G) * B);
+    __device__ void operator()(int64_t i, int64_t pos) const {  // (G * G < 2^31: 32-bit division)
+        const int ii = (int)i, g = (int)G;
+        out[pos] = make_int2((ii % g) * B, (ii / g) * B);
     }
 };
 // records are moved as five 8-byte words so padding bytes (zero) are preserved
@@ -270,7 +272,7 @@ __device__ __forceinline__ void copy_record(fic_record *dst, const fic_record *s
 }
 
 struct EmitRecord {
-    static constexpr bool kSmallOk = false;
+    static constexpr bool kChainOk = false;
     const fic_record *in;
     fic_record *out;
     const unsigned long long *base;
@@ -281,25 +283,27 @@ struct EmitRecord {
     }
 };
 
-// Small inputs (n <= 1024 x 64, every level of a 512^2 encode): the same order-preserving
-// compaction in one CTA and one launch (contiguous chunk per thread, block scan, scatter).
-constexpr int kSmallPer = 64;
+// Single-pass order-preserving compaction (index / grid emits): 4096 flags per CTA, block scan,
+// then a decoupled look-back over the predecessors' published (aggregate | inclusive prefix)
+// words, then the scatter -- one launch, every SM.  A word is tag << 34 | status << 32 | count;
+// the per-call tag makes the words of earlier calls (same scratch buffer) invisible, so the
+// buffer is never cleared.  Predecessors have lower block indices, which are dispatched first.
+constexpr int kChainItems = 16, kChainThreads = 256, kChainBlock = kChainItems * kChainThreads;
 template <class Emit>
-__global__ void __launch_bounds__(1024) select_small_kernel(const uint8_t *__restrict__ flags, int64_t n, Emit emit,
-                                                            unsigned long long *d_total) {
-    __shared__ int wsum[32];
+__global__ void __launch_bounds__(kChainThreads) select_chain_kernel(const uint8_t *__restrict__ flags, int64_t n,
+                                                                     Emit emit, unsigned long long *state,
+                                                                     uint32_t tag, unsigned long long *d_total) {
+    __shared__ int wsum[kChainThreads / 32];
+    __shared__ long long s_excl;
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-    const int64_t b0 = (int64_t)t * kSmallPer;  // this thread's 64 flags, kept in registers
-    uint32_t w[kSmallPer / 4];
-    if (b0 + kSmallPer <= n && ((reinterpret_cast<uintptr_t>(flags) & 15) == 0)) {
-#pragma unroll
-        for (int q = 0; q < kSmallPer / 16; ++q) {
-            const uint4 v = *reinterpret_cast<const uint4 *>(flags + b0 + 16 * q);
-            w[4 * q] = v.x; w[4 * q + 1] = v.y; w[4 * q + 2] = v.z; w[4 * q + 3] = v.w;
-        }
+    const int64_t b0 = (int64_t)blockIdx.x * kChainBlock + (int64_t)t * kChainItems;
+    uint32_t w[kChainItems / 4];
+    if (b0 + kChainItems <= n && ((reinterpret_cast<uintptr_t>(flags) & 15) == 0)) {
+        const uint4 v = *reinterpret_cast<const uint4 *>(flags + b0);
+        w[0] = v.x; w[1] = v.y; w[2] = v.z; w[3] = v.w;
     } else {
 #pragma unroll
-        for (int q = 0; q < kSmallPer / 4; ++q) {
+        for (int q = 0; q < kChainItems / 4; ++q) {
             uint32_t x = 0;
             for (int b = 0; b < 4; ++b) {
                 const int64_t i = b0 + 4 * q + b;
@@ -310,7 +314,7 @@ __global__ void __launch_bounds__(1024) select_small_kernel(const uint8_t *__res
     }
     int cnt = 0;
 #pragma unroll
-    for (int q = 0; q < kSmallPer / 4; ++q) {
+    for (int q = 0; q < kChainItems / 4; ++q) {
         w[q] &= 0x01010101u;  // flags are 0/1 bytes
         cnt += __popc(w[q]);
     }
@@ -322,21 +326,38 @@ __global__ void __launch_bounds__(1024) select_small_kernel(const uint8_t *__res
     }
     if (lane == 31) wsum[warp] = incl;
     __syncthreads();
-    if (warp == 0) {
-        const int ws = wsum[lane];
-        int wi = ws;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int v = __shfl_up_sync(0xffffffffu, wi, o);
-            if (lane >= o) wi += v;
+    if (t == 0) {
+        long long tot = 0;
+        for (int i = 0; i < kChainThreads / 32; ++i) {
+            const int ws = wsum[i];
+            wsum[i] = (int)tot;
+            tot += ws;
         }
-        wsum[lane] = wi - ws;  // exclusive warp offsets
-        if (lane == 31) *d_total = (unsigned long long)wi;
+        const unsigned long long T = (unsigned long long)tag << 34;
+        volatile unsigned long long *vs = state;
+        long long excl = 0;
+        if (blockIdx.x == 0) {
+            vs[0] = T | (2ull << 32) | (unsigned long long)tot;
+        } else {
+            vs[blockIdx.x] = T | (1ull << 32) | (unsigned long long)tot;  // aggregate
+            __threadfence();
+            for (int j = (int)blockIdx.x - 1;;) {
+                const unsigned long long v = vs[j];
+                if ((v >> 34) != tag) continue;  // predecessor not published yet
+                excl += (long long)(v & 0xffffffffull);
+                if (((v >> 32) & 3ull) == 2ull) break;  // inclusive prefix: done
+                --j;
+            }
+            __threadfence();
+            vs[blockIdx.x] = T | (2ull << 32) | (unsigned long long)(excl + tot);
+        }
+        s_excl = excl;
+        if (blockIdx.x == gridDim.x - 1) *d_total = (unsigned long long)(excl + tot);
     }
     __syncthreads();
-    int64_t pos = wsum[warp] + incl - cnt;
+    int64_t pos = s_excl + wsum[warp] + incl - cnt;
 #pragma unroll
-    for (int q = 0; q < kSmallPer / 4; ++q) {
+    for (int q = 0; q < kChainItems / 4; ++q) {
         uint32_t x = w[q];
         while (x) {
             const int bit = __ffs(x) - 1;  // lowest set flag byte first: index order
@@ -346,13 +367,23 @@ __global__ void __launch_bounds__(1024) select_small_kernel(const uint8_t *__res
     }
 }
 
+static uint32_t next_chain_tag() {
+    static std::atomic<uint32_t> ctr{0};
+    uint32_t t;
+    do t = (ctr.fetch_add(1) + 1) & 0x3fffffffu; while (t == 0);
+    return t;
+}
+
 template <class Emit>
 static cudaError_t select_run(const uint8_t *flags, int64_t n, int64_t *blocksum, Emit emit,
                               unsigned long long *d_total, cudaStream_t st) {
     const int64_t nb = (n + kSelBlock - 1) / kSelBlock;
     if (nb == 0) return cudaMemsetAsync(d_total, 0, sizeof(unsigned long long), st);
-    if (Emit::kSmallOk && n <= 1024 * kSmallPer) {  // not for 40-byte records (one SM would copy them all)
-        select_small_kernel<Emit><<<1, 1024, 0, st>>>(flags, n, emit, d_total);
+    if (Emit::kChainOk) {  // (40-byte records keep the three-pass form: side stream, wide copies)
+        const int64_t nc = (n + kChainBlock - 1) / kChainBlock;
+        static_assert(kChainBlock == kSelBlock, "blocksum scratch holds one word per chain block");
+        select_chain_kernel<Emit><<<(unsigned)nc, kChainThreads, 0, st>>>(
+            flags, n, emit, reinterpret_cast<unsigned long long *>(blocksum), next_chain_tag(), d_total);
         return cudaGetLastError();
     }
     select_count_kernel<<<(unsigned)nb, kSelThreads, 0, st>>>(flags, n, blocksum);
