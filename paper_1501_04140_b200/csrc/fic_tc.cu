@@ -51,6 +51,9 @@ struct TCfg {
     // B = 16 is fed by bulk copies (latency x bytes in flight): 8 x 16 KB stages
     static constexpr int STAGES = QR ? 8 : (B == 8 ? 2 : 4);
     static constexpr int B_BYTES = N * KB;                 // resident range operand
+    // range-operand buffers: 2 where shared memory allows, so the next segment's operand loads
+    // while the current segment's MMAs still read the other one
+    static constexpr int BBUF = B == 4 ? 2 : 1;
     static constexpr int ACC = QR ? 2 * N : N;             // TMEM columns per accumulator buffer
     static constexpr int NBUF = 512 / ACC >= 4 ? 4 : 2;    // TMEM accumulator buffers (MMA <-> epilogue)
     static constexpr int EWG = B == 4 ? 3 : 4;            // epilogue warpgroups
@@ -460,29 +463,36 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t *sA = smem;                                        // [STAGES][128 x KCH]
     uint8_t *sB = sA + STAGES * Cf::STAGE_BYTES;               // [N x KP]
-    TCRange *sR = reinterpret_cast<TCRange *>(sB + Cf::B_BYTES);   // [NR]
+    TCRange *sR = reinterpret_cast<TCRange *>(sB + Cf::BBUF * Cf::B_BYTES);   // [NR]
     float *sThr = reinterpret_cast<float *>(sR + NR);          // [NR] RU(best - A + margin), CAS-min
     float *sHsn = reinterpret_cast<float *>(sThr + NR);        // [NSP]
     Partial *sRed = reinterpret_cast<Partial *>(sHsn + 16);    // [NR][4]
     constexpr int NBUF = Cf::NBUF;
     uint64_t *bar = reinterpret_cast<uint64_t *>(sRed + NR * 4);  // full[S], empty[S], tfull[NB], tempty[NB], bop
     uint64_t *full = bar, *empty = bar + STAGES, *tfull = bar + 2 * STAGES, *tempty = tfull + NBUF;
-    uint64_t *bbar = tempty + NBUF;
-    uint32_t *sTmem = reinterpret_cast<uint32_t *>(bbar + 2);
+    uint64_t *bbar = tempty + NBUF;  // [BBUF] range operand loaded, [BBUF] range operand free
+    uint32_t *sTmem = reinterpret_cast<uint32_t *>(bbar + 4);
     Partial *sBest = reinterpret_cast<Partial *>(sTmem + 4);  // [NR][128] per (range, domain lane)
     int2 *sQ = reinterpret_cast<int2 *>(sBest + NR * kTileD);  // [epilogue threads][4] exact queue
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int n_r = (int)*P.d_nr;
-    const int n_tiles = (int)((P.d_misc[0] + kTileD - 1) / kTileD);
-    int group, split, ns;  // uniform per CTA: decided before any barrier
-    if (!cta_work(n_r, NR, n_tiles, 4, P.ns_cap, group, split, ns)) return;
-    if (group == 0 && split == 0 && threadIdx.x == 0) *P.d_ns = (unsigned long long)ns;
-    const int r0 = group * NR;
-    const int t0 = (int)(((int64_t)split * n_tiles) / ns);
-    const int t1 = (int)(((int64_t)(split + 1) * n_tiles) / ns);
-    const int ntl = max(0, t1 - t0);
-    const int nsteps = ntl * CH;
+    const int T = (int)((P.d_misc[0] + kTileD - 1) / kTileD);  // domain tiles
+    const int groups = (n_r + NR - 1) / NR;
+    const int64_t total = (int64_t)groups * T;
+    // persistent CTAs (one per SM): CTA c owns the flattened (group, tile) range [c W, (c+1) W),
+    // so every SM gets the same number of tiles whatever the group count; a group cut by CTA
+    // boundaries leaves one partial per CTA (slot c - c_first(g) < ns_cap).  Decided before any
+    // barrier, uniformly per CTA.
+    int64_t Gc = gridDim.x;
+    Gc = min(Gc, (int64_t)groups * (P.ns_cap - 1));  // ceil(T / W) + 1 <= ns_cap slots per group
+    Gc = min(Gc, max((int64_t)1, total / 4));         // >= ~4 tiles per CTA
+    if (total == 0 || (int64_t)blockIdx.x >= Gc) return;
+    const int64_t W = (total + Gc - 1) / Gc;
+    const int64_t f0 = (int64_t)blockIdx.x * W, f1 = min(total, f0 + W);
+    if (f0 >= f1) return;
+    const int nseg_max = (int)((T + W - 1) / W) + 1;
+    if (blockIdx.x == 0 && threadIdx.x == 0) *P.d_ns = (unsigned long long)min(nseg_max, P.ns_cap);
 
     // ---- setup: barriers, TMEM, per-range constants, the resident range operand
     if (threadIdx.x == 0) {
@@ -494,7 +504,7 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
             tmbar_init(&tfull[b], 1);
             tmbar_init(&tempty[b], 4 * Cf::EWG);
         }
-        tmbar_init(bbar, 1);
+        for (int b = 0; b < 2 * Cf::BBUF; ++b) tmbar_init(&bbar[b], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
@@ -502,12 +512,6 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(sTmem)),
                      "r"(kTmemCols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-    }
-    if (threadIdx.x < NR) {
-        const TCRange R = P.rmeta[r0 + threadIdx.x];
-        sR[threadIdx.x] = R;
-        const float th = P.has_zero ? fminf(__double2float_ru(R.margin), FLT_MAX) : FLT_MAX;
-        sThr[threadIdx.x] = R.valid ? th : -FLT_MAX;
     }
     if (threadIdx.x < 16) sHsn[threadIdx.x] = threadIdx.x < P.nsp ? -__double2float_rn(0.5 * P.spos[threadIdx.x]) : 0.f;
     tc_fence_before();
@@ -522,57 +526,77 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
         constexpr int kCopyLanes = 4;
         constexpr uint32_t PART = Cf::STAGE_BYTES / kCopyLanes;
         static_assert(Cf::STAGE_BYTES % (16 * kCopyLanes) == 0, "bulk copies need 16-byte multiples");
-        if (lane == 0) {
-            // the resident range operand of this CTA's NR ranges (prepared by tc_range_operand_kernel)
-            tmbar_expect_tx(bbar, Cf::B_BYTES);
-            tbulk_g2s(sB, P.Bop + (size_t)group * Cf::B_BYTES, Cf::B_BYTES, bbar);
-        }
         if (lane < kCopyLanes) {
-            for (int i = 0; i < nsteps; ++i) {
-                const int s = i % STAGES;
-                if (i >= STAGES) tmbar_wait(&empty[s], (uint32_t)(((i / STAGES) + 1) & 1));
-                const int tile = t0 + i / CH, ch = i % CH;
-                if (lane == 0) tmbar_expect_tx(&full[s], Cf::STAGE_BYTES);
-                __syncwarp((1u << kCopyLanes) - 1);  // expect_tx before any of the stage's copies lands
-                tbulk_g2s(sA + s * Cf::STAGE_BYTES + lane * PART,
-                          P.Dtc + ((size_t)tile * CH + ch) * Cf::STAGE_BYTES + lane * PART, PART, &full[s]);
+            int i = 0;
+            for (int64_t f = f0; f < f1; ++f) {  // tile by tile across the CTA's segments
+                const int tile = (int)(f % T);
+                for (int ch = 0; ch < CH; ++ch, ++i) {
+                    const int s = i % STAGES;
+                    if (i >= STAGES) tmbar_wait(&empty[s], (uint32_t)(((i / STAGES) + 1) & 1));
+                    if (lane == 0) tmbar_expect_tx(&full[s], Cf::STAGE_BYTES);
+                    __syncwarp((1u << kCopyLanes) - 1);  // expect_tx before any of the stage's copies lands
+                    tbulk_g2s(sA + s * Cf::STAGE_BYTES + lane * PART,
+                              P.Dtc + ((size_t)tile * CH + ch) * Cf::STAGE_BYTES + lane * PART, PART, &full[s]);
+                }
+            }
+        } else if (lane == kCopyLanes) {
+            // the resident range operand of each segment's group (tc_range_operand_kernel), once
+            // the previous segment's MMAs released it
+            int k = 0;
+            for (int64_t f = f0; f < f1; ++k) {
+                const int g = (int)(f / T), kb = k % Cf::BBUF;
+                if (k >= Cf::BBUF) tmbar_wait(&bbar[Cf::BBUF + kb], (uint32_t)(((k / Cf::BBUF) - 1) & 1));
+                tmbar_expect_tx(&bbar[kb], Cf::B_BYTES);
+                tbulk_g2s(sB + kb * Cf::B_BYTES, P.Bop + (size_t)g * Cf::B_BYTES, Cf::B_BYTES, &bbar[kb]);
+                f = min(f1, (int64_t)(g + 1) * T);
             }
         }
     } else if (warp == 1) {
         // ================= MMA issuer
         constexpr uint32_t idesc = idesc_i8(NN);
-        if (nsteps > 0) tmbar_wait(bbar, 0);
-        for (int i = 0; i < nsteps; ++i) {
-            const int s = i % STAGES;
-            const int tl = i / CH, ch = i % CH;
-            const int buf = tl % NBUF;
-            tmbar_wait(&full[s], (uint32_t)((i / STAGES) & 1));
-            if (ch == 0 && tl >= NBUF) tmbar_wait(&tempty[buf], (uint32_t)(((tl / NBUF) + 1) & 1));
-            tc_fence_after();
-            if (lane == 0) {
-                // QR: the first half of the stages (q plane) accumulates S_q at column 0 of the
-                // buffer, the second half (r plane) S_r at column N; both against the same B rows
-                constexpr int CHA = Cf::QR ? CH / 2 : CH;  // stages per accumulator
-                const int cha = ch % CHA;
-                const uint32_t dcol = buf * Cf::ACC + ((Cf::QR && ch >= CHA) ? NN : 0);
-                const uint32_t a0 = su32(sA + s * Cf::STAGE_BYTES);
-                const uint32_t b0 = su32(sB) + cha * (KCH / 16) * 128;
+        int i = 0, tl = 0, k = 0;
+        for (int64_t f = f0; f < f1; ++k) {
+            const int64_t fe = min(f1, (int64_t)(f / T + 1) * T);  // end of this segment
+            const int kb = k % Cf::BBUF;
+            tmbar_wait(&bbar[kb], (uint32_t)((k / Cf::BBUF) & 1));
+            const uint32_t bbase = su32(sB + kb * Cf::B_BYTES);
+            for (; f < fe; ++f, ++tl) {
+                const int buf = tl % NBUF;
+                for (int ch = 0; ch < CH; ++ch, ++i) {
+                    const int s = i % STAGES;
+                    tmbar_wait(&full[s], (uint32_t)((i / STAGES) & 1));
+                    if (ch == 0 && tl >= NBUF) tmbar_wait(&tempty[buf], (uint32_t)(((tl / NBUF) + 1) & 1));
+                    tc_fence_after();
+                    if (lane == 0) {
+                        // QR: the first half of the stages (q plane) accumulates S_q at column 0 of
+                        // the buffer, the second half (r plane) S_r at column N; same B rows
+                        constexpr int CHA = Cf::QR ? CH / 2 : CH;  // stages per accumulator
+                        const int cha = ch % CHA;
+                        const uint32_t dcol = buf * Cf::ACC + ((Cf::QR && ch >= CHA) ? NN : 0);
+                        const uint32_t a0 = su32(sA + s * Cf::STAGE_BYTES);
+                        const uint32_t b0 = bbase + cha * (KCH / 16) * 128;
 #pragma unroll
-                for (int kk = 0; kk < KCH / 32; ++kk) {
-                    const uint64_t ad = smem_desc(a0 + kk * 256, 128, (KCH / 16) * 128);
-                    const uint64_t bd = smem_desc(b0 + kk * 256, 128, (Cf::KB / 16) * 128);
-                    tc_mma_i8(tmem + dcol, ad, bd, idesc, (cha > 0 || kk > 0) ? 1u : 0u);
+                        for (int kk = 0; kk < KCH / 32; ++kk) {
+                            const uint64_t ad = smem_desc(a0 + kk * 256, 128, (KCH / 16) * 128);
+                            const uint64_t bd = smem_desc(b0 + kk * 256, 128, (Cf::KB / 16) * 128);
+                            tc_mma_i8(tmem + dcol, ad, bd, idesc, (cha > 0 || kk > 0) ? 1u : 0u);
+                        }
+                        tc_commit(&empty[s]);
+                        if (ch == CH - 1) tc_commit(&tfull[buf]);
+                    }
+                    __syncwarp();
                 }
-                tc_commit(&empty[s]);
-                if (ch == CH - 1) tc_commit(&tfull[buf]);
             }
+            if (lane == 0) tc_commit(&bbar[Cf::BBUF + kb]);  // operand free once these MMAs complete
             __syncwarp();
         }
     } else {
-        // ================= epilogue: lane = domain (TMEM lane), warpgroup = half of the ranges
+        // ================= epilogue: lane = domain (TMEM lane), warpgroup = a quarter (third) of
+        // the ranges; segment by segment (one range group each), tiles counted across segments
         const int eg = (warp - 2) >> 2;   // epilogue warpgroup
         const int lq = warp & 3;          // TMEM lane quarter accessible by this warp
         const int m = lq * 32 + lane;     // domain lane within the tile
+        const int et = threadIdx.x - 64;  // epilogue thread
         constexpr int NT = NSP ? NSP : 1;  // t2 values per domain (u = 1/C for NSP = 0)
         float nhs[NT];
 #pragma unroll
@@ -580,30 +604,11 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
         // (exact), so g = fma(nhs, bq, t2) keeps its rounding without the multiply
         constexpr float kBqScale = B == 4 ? 2.0f : (B == 8 ? 64.0f : 1.0f);
         for (int jj = 0; jj < NT; ++jj) nhs[jj] = sHsn[jj] * kBqScale;
-        for (int q = 0; q < HALF; ++q) {
-            Partial pb;
-            if (P.has_zero) { pb.e = sR[eg * HALF + q].A; pb.d = 0; pb.kj = P.j_zero; }
-            else { pb.e = INFINITY; pb.d = INT_MAX; pb.kj = INT_MAX; }
-            sBest[(eg * HALF + q) * kTileD + m] = pb;
-        }
+        auto epi_sync = [&]() { asm volatile("bar.sync 6, %0;" ::"r"(128 * Cf::EWG) : "memory"); };
         unsigned n_exact = 0;
-        int rSR[HALF];
-#pragma unroll
-        for (int q = 0; q < HALF; ++q) rSR[q] = sR[eg * HALF + q].SR;
         int qn = 0;
-        const int qbase = (threadIdx.x - 64) * 4;
-        // per-domain data of this lane, walked tile by tile (pointers advanced, not recomputed);
-        // NSP > 0 is chosen only when the level has exactly NSP values s > 0, so every row exists
-        const int32_t *sdp = P.SD + (int64_t)t0 * kTileD + m;
-        const float *t2p = P.t2f + (int64_t)t0 * kTileD + m;
+        const int qbase = et * 4;
         const int64_t t2row = P.n_slots;
-        int32_t sd_n = 0;
-        float t2_n[NT];
-        if (ntl > 0) {
-            sd_n = __ldg(sdp);
-#pragma unroll
-            for (int jj = 0; jj < NT; ++jj) t2_n[jj] = __ldg(t2p + jj * t2row);
-        }
         // fp32 filter score of one (range, domain) pair from the max over isometries of SRD_k
         auto score = [&](int mx, int rsr, int32_t sd, const float *t2) -> float {
             float bq;
@@ -632,15 +637,49 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
             }
             return g0;
         };
-        if constexpr (NSP > 0) {
-            // ---- seed the thresholds from the first tile: with NSP > 0, g approximates
-            // min_{s > 0} e_s - A within the margin, so every range's best is <= A + min_m g + margin
-            // and RU(min_m g + 2 margin) is a valid threshold -- the first tile no longer sends every
-            // pair better than s = 0 to the exact path
-            if (ntl > 0) {
-                tmbar_wait(&tfull[0], 0u);
+        int tl = 0;  // tiles consumed by this CTA (TMEM buffer ring position)
+        for (int64_t f = f0; f < f1;) {
+            const int grp = (int)(f / T);
+            const int ta = (int)(f % T);
+            const int64_t fe = min(f1, (int64_t)(grp + 1) * T);
+            const int ntl = (int)(fe - f);
+            const int r0 = grp * NR;
+            // ---- segment setup: this group's range constants and thresholds (the previous
+            // segment's readers of sR / sThr / sRed have passed the barrier)
+            epi_sync();
+            if (et < NR) {
+                const TCRange R = P.rmeta[r0 + et];
+                sR[et] = R;
+                const float th = P.has_zero ? fminf(__double2float_ru(R.margin), FLT_MAX) : FLT_MAX;
+                sThr[et] = R.valid ? th : -FLT_MAX;
+            }
+            epi_sync();
+            for (int q = 0; q < HALF; ++q) {
+                Partial pb;
+                if (P.has_zero) { pb.e = sR[eg * HALF + q].A; pb.d = 0; pb.kj = P.j_zero; }
+                else { pb.e = INFINITY; pb.d = INT_MAX; pb.kj = INT_MAX; }
+                sBest[(eg * HALF + q) * kTileD + m] = pb;
+            }
+            int rSR[HALF];
+#pragma unroll
+            for (int q = 0; q < HALF; ++q) rSR[q] = sR[eg * HALF + q].SR;
+            // per-domain data of this lane, walked tile by tile (pointers advanced, not recomputed);
+            // NSP > 0 is chosen only when the level has exactly NSP values s > 0, so every row exists
+            const int32_t *sdp = P.SD + (int64_t)ta * kTileD + m;
+            const float *t2p = P.t2f + (int64_t)ta * kTileD + m;
+            int32_t sd_n = __ldg(sdp);
+            float t2_n[NT];
+#pragma unroll
+            for (int jj = 0; jj < NT; ++jj) t2_n[jj] = __ldg(t2p + jj * t2row);
+            if constexpr (NSP > 0) {
+                // ---- seed the thresholds from the segment's first tile: with NSP > 0, g approximates
+                // min_{s > 0} e_s - A within the margin, so every range's best is <= A + min_m g +
+                // margin and RU(min_m g + 2 margin) is a valid threshold -- the first tile no longer
+                // sends every pair better than s = 0 to the exact path
+                const int buf0 = tl % NBUF;
+                tmbar_wait(&tfull[buf0], (uint32_t)((tl / NBUF) & 1));
                 tc_fence_after();
-                const uint32_t tb0 = tmem + ((uint32_t)(lq * 32) << 16) + eg * HALF * 8;
+                const uint32_t tb0 = tmem + ((uint32_t)(lq * 32) << 16) + buf0 * Cf::ACC + eg * HALF * 8;
 #pragma unroll 1
                 for (int g = 0; g < HALF / 4; ++g) {
                     uint32_t sv[64];
@@ -676,127 +715,158 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
                 }
                 asm volatile("bar.sync %0, 128;" ::"r"(1 + eg) : "memory");  // the warpgroup's seeds
             }
-        }
-        for (int tl = 0; tl < ntl; ++tl) {
-            const int buf = tl % NBUF;
-            const int d = (t0 + tl) * kTileD + m;
-            const int32_t sd = sd_n;
-            float t2[NT];
+            for (int tt = 0; tt < ntl; ++tt, ++tl) {
+                const int buf = tl % NBUF;
+                const int d = (ta + tt) * kTileD + m;
+                const int32_t sd = sd_n;
+                float t2[NT];
 #pragma unroll
-            for (int jj = 0; jj < NT; ++jj) t2[jj] = t2_n[jj];
-            sdp += kTileD;
-            t2p += kTileD;
-            if (tl + 1 < ntl) {  // prefetch the next tile's per-domain data
-                sd_n = __ldg(sdp);
+                for (int jj = 0; jj < NT; ++jj) t2[jj] = t2_n[jj];
+                sdp += kTileD;
+                t2p += kTileD;
+                if (tt + 1 < ntl) {  // prefetch the next tile's per-domain data
+                    sd_n = __ldg(sdp);
 #pragma unroll
-                for (int jj = 0; jj < NT; ++jj) t2_n[jj] = __ldg(t2p + jj * t2row);
-            }
-            tmbar_wait(&tfull[buf], (uint32_t)((tl / NBUF) & 1));
-            tc_fence_after();
-            const uint32_t tbase = tmem + ((uint32_t)(lq * 32) << 16) + buf * Cf::ACC + eg * HALF * 8;
-            // four ranges (32 columns) per tcgen05.ld, the next group in flight while one is scored
-            constexpr int G = HALF / 4;
-            uint32_t vv[64];
-            tc_ld32<0>(tbase, vv);
-            if constexpr (Cf::QR) {  // SRD_k = 4 S_q + S_r (exact: < 2^31)
-                static_assert(!Cf::QR || G == 1, "QR keeps one 4-range group per warp and tile");
-                tc_ld32<32>(tbase + NN, vv);
-                tc_wait_ld();
-#pragma unroll
-                for (int i = 0; i < 32; ++i) vv[i] = 4u * vv[i] + vv[32 + i];
-            } else {
-                tc_wait_ld();
-            }
-#pragma unroll
-            for (int g = 0; g < G; ++g) {
-                if (g + 1 < G) {
-                    if ((g & 1) == 0) tc_ld32<32>(tbase + (g + 1) * 32, vv);
-                    else tc_ld32<0>(tbase + (g + 1) * 32, vv);
+                    for (int jj = 0; jj < NT; ++jj) t2_n[jj] = __ldg(t2p + jj * t2row);
                 }
-                unsigned pm = 0;
-                int mxs[4];
+                tmbar_wait(&tfull[buf], (uint32_t)((tl / NBUF) & 1));
+                tc_fence_after();
+                const uint32_t tbase = tmem + ((uint32_t)(lq * 32) << 16) + buf * Cf::ACC + eg * HALF * 8;
+                // four ranges (32 columns) per tcgen05.ld, the next group in flight while one is scored
+                constexpr int G = HALF / 4;
+                uint32_t vv[64];
+                tc_ld32<0>(tbase, vv);
+                if constexpr (Cf::QR) {  // SRD_k = 4 S_q + S_r (exact: < 2^31)
+                    static_assert(!Cf::QR || G == 1, "QR keeps one 4-range group per warp and tile");
+                    tc_ld32<32>(tbase + NN, vv);
+                    tc_wait_ld();
 #pragma unroll
-                for (int q4 = 0; q4 < 4; ++q4) {  // branch-free filter of four ranges
-                    const int q = g * 4 + q4;
-                    const uint32_t *v = vv + (g & 1) * 32 + q4 * 8;
-                    const int mx = max(__vimax3_s32((int)v[0], (int)v[1], (int)v[2]),
-                                       __vimax3_s32((int)v[3], (int)v[4], __vimax3_s32((int)v[5], (int)v[6], (int)v[7])));
-                    mxs[q4] = mx;
-                    const float g0 = score(mx, rSR[q], sd, t2);
-                    pm |= (g0 <= sThr[eg * HALF + q]) ? (1u << q4) : 0u;
+                    for (int i = 0; i < 32; ++i) vv[i] = 4u * vv[i] + vv[32 + i];
+                } else {
+                    tc_wait_ld();
                 }
-                if (pm) {  // queue (q, k*, max SRD) of the passing ranges for the exact path
 #pragma unroll
-                    for (int q4 = 0; q4 < 4; ++q4) {
-                        if (pm >> q4 & 1) {
-                            const uint32_t *v = vv + (g & 1) * 32 + q4 * 8;
-                            int ks = 7;
+                for (int g = 0; g < G; ++g) {
+                    if (g + 1 < G) {
+                        if ((g & 1) == 0) tc_ld32<32>(tbase + (g + 1) * 32, vv);
+                        else tc_ld32<0>(tbase + (g + 1) * 32, vv);
+                    }
+                    unsigned pm = 0;
+                    int mxs[4];
 #pragma unroll
-                            for (int k = 6; k >= 0; --k)
-                                if ((int)v[k] == mxs[q4]) ks = k;  // lowest index attaining the max
-                            sQ[qbase + qn] = make_int2((g * 4 + q4) | (ks << 8), mxs[q4]);
-                            ++qn;
+                    for (int q4 = 0; q4 < 4; ++q4) {  // branch-free filter of four ranges
+                        const int q = g * 4 + q4;
+                        const uint32_t *v = vv + (g & 1) * 32 + q4 * 8;
+                        const int mx = max(__vimax3_s32((int)v[0], (int)v[1], (int)v[2]),
+                                           __vimax3_s32((int)v[3], (int)v[4], __vimax3_s32((int)v[5], (int)v[6], (int)v[7])));
+                        mxs[q4] = mx;
+                        const float g0 = score(mx, rSR[q], sd, t2);
+                        pm |= (g0 <= sThr[eg * HALF + q]) ? (1u << q4) : 0u;
+                    }
+                    if (pm) {  // queue (q, k*, max SRD) of the passing ranges for the exact path
+#pragma unroll
+                        for (int q4 = 0; q4 < 4; ++q4) {
+                            if (pm >> q4 & 1) {
+                                const uint32_t *v = vv + (g & 1) * 32 + q4 * 8;
+                                int ks = 7;
+#pragma unroll
+                                for (int k = 6; k >= 0; --k)
+                                    if ((int)v[k] == mxs[q4]) ks = k;  // lowest index attaining the max
+                                sQ[qbase + qn] = make_int2((g * 4 + q4) | (ks << 8), mxs[q4]);
+                                ++qn;
+                            }
+                        }
+                    }
+                    // ---- exact path (rare, one rolled copy): canonical binary64 score for every s > 0,
+                    // lexicographic first-min update of this lane's best, CAS-min of the shared threshold
+                    for (int i = 0; i < qn; ++i) {
+                        const int2 ent = sQ[qbase + i];
+                        const int q = ent.x & 255, ks = ent.x >> 8, mx = ent.y;
+                        const TCRange &R = sR[eg * HALF + q];
+                        Partial *bp = &sBest[(eg * HALF + q) * kTileD + m];
+                        const double Bq = __dsub_rn(__dmul_rn((double)n, (double)mx),
+                                                    __dmul_rn((double)R.SR, (double)sd));
+                        const double c16 = __dmul_rn(0.0625, (double)P.C[d]);
+                        double e0 = bp->e;
+                        int32_t d0 = bp->d, kj0 = bp->kj;
+                        for (int jj = 0; jj < P.nsp; ++jj) {
+                            const double sj = P.spos[jj];
+                            const double e = __dadd_rn(__dsub_rn(R.A, __dmul_rn(__dmul_rn(0.5, sj), Bq)),
+                                                       __dmul_rn(__dmul_rn(sj, sj), c16));
+                            const int32_t kj = (ks << 8) | P.jpos[jj];
+                            if (e < e0 || (e == e0 && (d < d0 || (d == d0 && kj < kj0)))) { e0 = e; d0 = d; kj0 = kj; }
+                        }
+                        bp->e = e0;
+                        bp->d = d0;
+                        bp->kj = kj0;
+                        const float t = fminf(__double2float_ru(__dadd_rn(__dsub_rn(e0, R.A), R.margin)), FLT_MAX);
+                        int *ti = reinterpret_cast<int *>(&sThr[eg * HALF + q]);
+                        int old = *ti;
+                        while (t < __int_as_float(old)) {
+                            const int prev = atomicCAS(ti, old, __float_as_int(t));
+                            if (prev == old) break;
+                            old = prev;
+                        }
+                    }
+                    n_exact += qn;
+                    qn = 0;
+                    __syncwarp();  // reconverge after the (rare, divergent) exact path
+                    if (g + 1 < G) tc_wait_ld();
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) tmbar_arrive(&tempty[buf]);
+            }
+            // ---- reduce each range's best over the 128 domain lanes (lexicographic); the HALF
+            // shuffle chains interleaved (independent ranges)
+            {
+                double e0[HALF];
+                int32_t d0[HALF], kj0[HALF];
+#pragma unroll
+                for (int q = 0; q < HALF; ++q) {
+                    const Partial mine = sBest[(eg * HALF + q) * kTileD + m];
+                    e0[q] = mine.e; d0[q] = mine.d; kj0[q] = mine.kj;
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+                    for (int q = 0; q < HALF; ++q) {
+                        const double oe = __shfl_xor_sync(0xffffffffu, e0[q], o);
+                        const int od = __shfl_xor_sync(0xffffffffu, d0[q], o);
+                        const int okj = __shfl_xor_sync(0xffffffffu, kj0[q], o);
+                        if (oe < e0[q] || (oe == e0[q] && (od < d0[q] || (od == d0[q] && okj < kj0[q])))) {
+                            e0[q] = oe; d0[q] = od; kj0[q] = okj;
                         }
                     }
                 }
-                // ---- exact path (rare, one rolled copy): canonical binary64 score for every s > 0,
-                // lexicographic first-min update of this lane's best, CAS-min of the shared threshold
-                for (int i = 0; i < qn; ++i) {
-                    const int2 ent = sQ[qbase + i];
-                    const int q = ent.x & 255, ks = ent.x >> 8, mx = ent.y;
-                    const TCRange &R = sR[eg * HALF + q];
-                    Partial *bp = &sBest[(eg * HALF + q) * kTileD + m];
-                    const double Bq = __dsub_rn(__dmul_rn((double)n, (double)mx),
-                                                __dmul_rn((double)R.SR, (double)sd));
-                    const double c16 = __dmul_rn(0.0625, (double)P.C[d]);
-                    double e0 = bp->e;
-                    int32_t d0 = bp->d, kj0 = bp->kj;
-                    for (int jj = 0; jj < P.nsp; ++jj) {
-                        const double sj = P.spos[jj];
-                        const double e = __dadd_rn(__dsub_rn(R.A, __dmul_rn(__dmul_rn(0.5, sj), Bq)),
-                                                   __dmul_rn(__dmul_rn(sj, sj), c16));
-                        const int32_t kj = (ks << 8) | P.jpos[jj];
-                        if (e < e0 || (e == e0 && (d < d0 || (d == d0 && kj < kj0)))) { e0 = e; d0 = d; kj0 = kj; }
-                    }
-                    bp->e = e0;
-                    bp->d = d0;
-                    bp->kj = kj0;
-                    const float t = fminf(__double2float_ru(__dadd_rn(__dsub_rn(e0, R.A), R.margin)), FLT_MAX);
-                    int *ti = reinterpret_cast<int *>(&sThr[eg * HALF + q]);
-                    int old = *ti;
-                    while (t < __int_as_float(old)) {
-                        const int prev = atomicCAS(ti, old, __float_as_int(t));
-                        if (prev == old) break;
-                        old = prev;
+                if (lane == 0) {
+#pragma unroll
+                    for (int q = 0; q < HALF; ++q) {
+                        Partial pb;
+                        pb.e = e0[q]; pb.d = d0[q]; pb.kj = kj0[q];
+                        sRed[(eg * HALF + q) * 4 + lq] = pb;
                     }
                 }
-                n_exact += qn;
-                qn = 0;
-                __syncwarp();  // reconverge after the (rare, divergent) exact path
-                if (g + 1 < G) tc_wait_ld();
             }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) tmbar_arrive(&tempty[buf]);
-        }
-        // ---- reduce each range's best over the 128 domain lanes (lexicographic)
-#pragma unroll 1
-        for (int q = 0; q < HALF; ++q) {
-            const Partial mine = sBest[(eg * HALF + q) * kTileD + m];
-            double e0 = mine.e;
-            int32_t d0 = mine.d, kj0 = mine.kj;
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                const double oe = __shfl_xor_sync(0xffffffffu, e0, o);
-                const int od = __shfl_xor_sync(0xffffffffu, d0, o);
-                const int okj = __shfl_xor_sync(0xffffffffu, kj0, o);
-                if (oe < e0 || (oe == e0 && (od < d0 || (od == d0 && okj < kj0)))) { e0 = oe; d0 = od; kj0 = okj; }
+            epi_sync();
+            if (et < NR) {  // the segment's partial of each range; the group's last segment also
+                const int r = r0 + et;  // fills the unused slots
+                Partial b = sRed[et * 4];
+                for (int w = 1; w < 4; ++w) {
+                    const Partial c = sRed[et * 4 + w];
+                    if (c.e < b.e || (c.e == b.e && (c.d < b.d || (c.d == b.d && c.kj < b.kj)))) b = c;
+                }
+                if (r < n_r) {
+                    const int slot = (int)(blockIdx.x - ((int64_t)grp * T) / W);
+                    P.part[(size_t)r * P.ns_cap + slot] = b;
+                    if (fe == (int64_t)(grp + 1) * T) {
+                        Partial none;
+                        none.e = INFINITY; none.d = INT_MAX; none.kj = INT_MAX;
+                        for (int s2 = slot + 1; s2 < nseg_max && s2 < P.ns_cap; ++s2) P.part[(size_t)r * P.ns_cap + s2] = none;
+                    }
+                }
             }
-            if (lane == 0) {
-                Partial pb;
-                pb.e = e0; pb.d = d0; pb.kj = kj0;
-                sRed[(eg * HALF + q) * 4 + lq] = pb;
-            }
+            f = fe;
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) n_exact += __shfl_xor_sync(0xffffffffu, n_exact, o);
@@ -804,15 +874,6 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
     }
     tc_fence_before();
     __syncthreads();
-    if (threadIdx.x < NR) {
-        const int r = r0 + threadIdx.x;
-        Partial b = sRed[threadIdx.x * 4];
-        for (int w = 1; w < 4; ++w) {
-            const Partial c = sRed[threadIdx.x * 4 + w];
-            if (c.e < b.e || (c.e == b.e && (c.d < b.d || (c.d == b.d && c.kj < b.kj)))) b = c;
-        }
-        if (r < n_r) P.part[(size_t)r * P.ns_cap + split] = b;
-    }
     if (warp == 0) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
@@ -822,8 +883,8 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
 template <int B, int NSP>
 static size_t tc_smem_bytes() {
     using Cf = TCfg<B>;
-    return (size_t)Cf::STAGES * Cf::STAGE_BYTES + Cf::B_BYTES + sizeof(TCRange) * Cf::NR + 4 * Cf::NR +
-           4 * 16 + sizeof(Partial) * Cf::NR * 4 + 8 * (2 * Cf::STAGES + 2 * Cf::NBUF + 2) + 16 +
+    return (size_t)Cf::STAGES * Cf::STAGE_BYTES + Cf::BBUF * Cf::B_BYTES + sizeof(TCRange) * Cf::NR + 4 * Cf::NR +
+           4 * 16 + sizeof(Partial) * Cf::NR * 4 + 8 * (2 * Cf::STAGES + 2 * Cf::NBUF + 4) + 16 +
            sizeof(Partial) * Cf::NR * kTileD + sizeof(int2) * 128 * Cf::EWG * 4 + 1024;
 }
 
@@ -838,8 +899,15 @@ static cudaError_t launch_tc_t(const TCParams &p, cudaStream_t st) {
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    dim3 grid((unsigned)((p.n_r + Cf::NR - 1) / Cf::NR), (unsigned)p.nsplit);
-    tcsearch_kernel<B, NSP><<<grid, Cf::THREADS, smem, st>>>(p);
+    // persistent: one CTA per SM (the kernel partitions the (group, tile) space itself)
+    static int num_sms = 0;
+    if (!num_sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+        if (num_sms <= 0) num_sms = 148;
+    }
+    tcsearch_kernel<B, NSP><<<(unsigned)num_sms, Cf::THREADS, smem, st>>>(p);
     return cudaGetLastError();
 }
 
