@@ -521,9 +521,11 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
 
     if (warp == 0) {
         // ================= producer: each (tile, chunk) stage as kCopyLanes bulk copies issued by
-        // different lanes -- copies from one thread are serviced one after another (~550 cycles
-        // each up to 32 KB, scripts/micro/bulk_rate.cu), copies from several threads overlap
-        constexpr int kCopyLanes = 4;
+        // different lanes.  In isolation copies from several threads overlap
+        // (scripts/micro/bulk_rate.cu), but inside the persistent kernel, with every SM streaming
+        // the pool from L2, one copy per stage is fastest (C3: 1.90 ms vs 1.93 with 2 lanes, 1.94
+        // with 4, 2.06 with 8)
+        constexpr int kCopyLanes = 1;
         constexpr uint32_t PART = Cf::STAGE_BYTES / kCopyLanes;
         static_assert(Cf::STAGE_BYTES % (16 * kCopyLanes) == 0, "bulk copies need 16-byte multiples");
         if (lane < kCopyLanes) {
