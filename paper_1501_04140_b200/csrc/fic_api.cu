@@ -38,6 +38,8 @@ struct fic_ctx {
     cudaEvent_t ev[fic::kMaxLevels][5] = {};
     int64_t launches = 0;
     cudaStream_t side = nullptr;                 // pool builds of levels >= 1 overlap the searches
+    cudaStream_t crit = nullptr;                 // the encode's critical path (highest priority)
+    cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
     int overlap_pools = 0;                       // env FIC_OVERLAP_POOLS=1
     cudaEvent_t pool_ready[fic::kMaxLevels] = {};
     cudaEvent_t level_done[fic::kMaxLevels] = {};  // finalize of level l done (records ready)
@@ -531,7 +533,15 @@ fic_status fic_ctx_create(int32_t device, void *cuda_stream, fic_ctx **out) {
     }
     for (int l = 0; l < fic::kMaxLevels && e == cudaSuccess; ++l)
         for (int q = 0; q < 5 && e == cudaSuccess; ++q) e = cudaEventCreate(&ctx->ev[l][q]);
-    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking);
+    // the quadtree's critical path runs on a highest-priority stream, the overlapped pool builds
+    // and record gathering on a lowest-priority one: when both have blocks waiting, the critical
+    // path's small kernels are scheduled first
+    int prio_lo = 0, prio_hi = 0;
+    if (e == cudaSuccess) e = cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+    if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&ctx->side, cudaStreamNonBlocking, prio_lo);
+    if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&ctx->crit, cudaStreamNonBlocking, prio_hi);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->fork_ev, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->join_ev, cudaEventDisableTiming);
     for (int l = 0; l < fic::kMaxLevels && e == cudaSuccess; ++l)
         e = cudaEventCreateWithFlags(&ctx->pool_ready[l], cudaEventDisableTiming);
     for (int l = 0; l < fic::kMaxLevels && e == cudaSuccess; ++l)
@@ -582,6 +592,12 @@ fic_status fic_ctx_destroy(fic_ctx *ctx) {
         cudaStreamSynchronize(ctx->side);
         cudaStreamDestroy(ctx->side);
     }
+    if (ctx->crit) {
+        cudaStreamSynchronize(ctx->crit);
+        cudaStreamDestroy(ctx->crit);
+    }
+    if (ctx->fork_ev) cudaEventDestroy(ctx->fork_ev);
+    if (ctx->join_ev) cudaEventDestroy(ctx->join_ev);
     delete ctx;
     return FIC_OK;
 }
@@ -692,11 +708,34 @@ fic_status fic_encode_level(fic_ctx *ctx, const uint8_t *img, int32_t N, const f
 //   [0] running output total  [1] level accepted count  [2] next-level range count (scratch)
 //   [8 + l] exact evaluations of level l   [16 + l] accepted at level l   [24..] error flag (int)
 //   [32 + l] range count of level l
+static fic_status encode_body(fic_ctx *ctx, const uint8_t *img, int32_t N, int32_t B_max, int32_t B_min,
+                              int32_t L, const double *h_tau, const int64_t *h_topk, const double *h_s,
+                              const int32_t *h_n_s, const double *h_rms_tol, int32_t shard, int32_t n_shards,
+                              fic_record *out, int64_t capacity, int64_t *h_n_out);
+
+// The encode runs on ctx->crit, forked from the caller's stream (the image is ready in its order)
+// and joined back into it; ctx->stream is pointed at ctx->crit for the duration of the call.
 static fic_status encode_impl(fic_ctx *ctx, const uint8_t *img, int32_t N, int32_t B_max, int32_t B_min,
                               int32_t L, const double *h_tau, const int64_t *h_topk, const double *h_s,
                               const int32_t *h_n_s, const double *h_rms_tol, int32_t shard, int32_t n_shards,
                               fic_record *out, int64_t capacity, int64_t *h_n_out) {
     CKS(ctx_check(ctx));
+    cudaStream_t user = ctx->stream;
+    CK(cudaEventRecord(ctx->fork_ev, user));
+    CK(cudaStreamWaitEvent(ctx->crit, ctx->fork_ev, 0));
+    ctx->stream = ctx->crit;
+    const fic_status r = encode_body(ctx, img, N, B_max, B_min, L, h_tau, h_topk, h_s, h_n_s, h_rms_tol, shard,
+                                     n_shards, out, capacity, h_n_out);
+    ctx->stream = user;
+    cudaEventRecord(ctx->join_ev, ctx->crit);
+    cudaStreamWaitEvent(user, ctx->join_ev, 0);
+    return r;
+}
+
+static fic_status encode_body(fic_ctx *ctx, const uint8_t *img, int32_t N, int32_t B_max, int32_t B_min,
+                              int32_t L, const double *h_tau, const int64_t *h_topk, const double *h_s,
+                              const int32_t *h_n_s, const double *h_rms_tol, int32_t shard, int32_t n_shards,
+                              fic_record *out, int64_t capacity, int64_t *h_n_out) {
     if (h_n_out) *h_n_out = 0;
     if (!img || !(h_tau || h_topk) || !h_s || !h_n_s || !h_rms_tol || !h_n_out || (!out && capacity > 0) ||
         capacity < 0)
@@ -840,6 +879,12 @@ static fic_status encode_impl(fic_ctx *ctx, const uint8_t *img, int32_t N, int32
                 cudaEventElapsedTime(&c, ctx->ev[l][2], ctx->ev[l][3]);
             }
             ls.ms_pool = a; ls.ms_search = b; ls.ms_finalize = c;
+            if (ctx->timing >= 2 && getenv("FIC_TRACE")) {
+                float g = 0, p0 = 0;
+                if (l > 0) cudaEventElapsedTime(&g, ctx->ev[l - 1][3], ctx->ev[l][1]);
+                cudaEventElapsedTime(&p0, ctx->ev[0][0], ctx->ev[l][1]);
+                fprintf(stderr, "[trace] level %d: search starts at %.3f ms, gap after previous finalize %.3f ms, search %.3f, finalize %.3f\n", l, p0, g, b, c);
+            }
         }
     }
     const int64_t total = (int64_t)ctx->h_counts[0];
