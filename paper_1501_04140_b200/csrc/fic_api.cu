@@ -4,6 +4,7 @@
 #include <quadmath.h>
 
 #include <cmath>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -39,6 +40,7 @@ struct fic_ctx {
     int64_t launches = 0;
     cudaStream_t side = nullptr;                 // pool builds of levels >= 1 overlap the searches
     cudaStream_t crit = nullptr;                 // the encode's critical path (highest priority)
+    bool child_clean = false;                    // b_child is all zero (see encode_body)
     cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
     int overlap_pools = 0;                       // env FIC_OVERLAP_POOLS=1
     cudaEvent_t pool_ready[fic::kMaxLevels] = {};
@@ -107,7 +109,7 @@ void free_buf(Buf &b) {
 void free_pool(Pool &P) {
     free_buf(P.b_keys); free_buf(P.b_keep); free_buf(P.b_kept); free_buf(P.b_Dt);
     free_buf(P.b_SDf); free_buf(P.b_SD); free_buf(P.b_C); free_buf(P.b_misc); free_buf(P.b_Dc);
-    free_buf(P.b_Dtc); free_buf(P.b_F2); free_buf(P.b_blocksum); free_buf(P.b_topk);
+    free_buf(P.b_Dtc); free_buf(P.b_F2); free_buf(P.b_blocksum); free_buf(P.b_topk); free_buf(P.b_t2f);
 }
 
 bool pow2(int32_t v) { return v > 0 && (v & (v - 1)) == 0; }
@@ -230,6 +232,26 @@ fic_status check_s(fic_ctx *ctx, const double *h_s, int32_t n_s) {
 // --------------------------------------------------------------------------- one level
 // ranges: device int2 [n_r]; the range count is *d_nr (device), n_r_max a host upper bound that
 // sizes grids and buffers.  Writes rec [n_r], acc [n_r_max] (0 past n_r) and child marks.
+// The level's fp32 filter table (t2f_kernel) from the pool's C and the level's s set, enqueued on
+// the pool's stream right after the pool (off the quadtree's critical path); tcgen05 / direct only.
+fic_status t2f_enqueue(fic_ctx *ctx, Pool &P, const double *h_s, int32_t n_s, cudaStream_t st) {
+    P.t2f_ready = 0;
+    if (P.mode != 0 && P.mode != 2) return FIC_OK;
+    fic::SList sl;
+    memset(&sl, 0, sizeof sl);
+    int nsp = 0;
+    for (int j = 0; j < n_s; ++j)
+        if (h_s[j] != 0.0) sl.s[nsp++] = h_s[j];
+    if (P.mode == 2 && nsp > 16) return FIC_OK;  // level_enqueue reports the error
+    const int64_t slots = P.n_tiles_max * fic::kTileD;
+    CK(grow(ctx, P.b_t2f, sizeof(float) * (size_t)slots * (nsp ? nsp : 1)));
+    CK(fic::launch_t2f(P.C, &P.d_misc[0], slots, sl, nsp, reinterpret_cast<float *>(P.b_t2f.p),
+                       (P.mode == 0 && nsp > 2) ? 1 : 0, st));
+    if (nsp > 0 && slots > 0) ctx->launches += 1;
+    P.t2f_ready = 1;
+    return FIC_OK;
+}
+
 fic_status level_enqueue(fic_ctx *ctx, const Pool &P, const uint8_t *img, const int2 *ranges,
                          const unsigned long long *d_nr, int64_t n_r_max, const double *h_s, int32_t n_s,
                          double rms_tol, int is_min, fic_record *rec, uint8_t *acc, uint8_t *child,
@@ -282,9 +304,10 @@ fic_status level_enqueue(fic_ctx *ctx, const Pool &P, const uint8_t *img, const 
     sp.ns_cap = dyn ? (int32_t)std::min<int64_t>(4 * (int64_t)sp.nsplit, std::max<int64_t>(1, tiles)) : sp.nsplit;
     sp.d_ns = ptr<unsigned long long>(ctx->b_counts) + 56 + level_slot;
     if (!dyn) CK(fic::launch_set_u64(sp.d_ns, (unsigned long long)sp.nsplit, st));
-    CK(grow(ctx, ctx->b_t2f, sizeof(float) * (size_t)slots * (sp.nsp ? sp.nsp : 1)));
+    const bool t2f_pre = P.t2f_ready && (P.mode == 0 || P.mode == 2);  // enqueued with the pool
+    if (!t2f_pre) CK(grow(ctx, ctx->b_t2f, sizeof(float) * (size_t)slots * (sp.nsp ? sp.nsp : 1)));
     CK(grow(ctx, ctx->b_part, sizeof(fic::Partial) * (size_t)n_r_max * sp.ns_cap));
-    sp.t2f = ptr<float>(ctx->b_t2f);
+    sp.t2f = t2f_pre ? reinterpret_cast<float *>(P.b_t2f.p) : ptr<float>(ctx->b_t2f);
     sp.part = ptr<fic::Partial>(ctx->b_part);
     sp.exact_count = ptr<unsigned long long>(ctx->b_counts) + 8 + level_slot;
     fic::SList sl;
@@ -292,9 +315,11 @@ fic_status level_enqueue(fic_ctx *ctx, const Pool &P, const uint8_t *img, const 
     if (P.mode == 2 || P.mode == 0) {
         if (P.mode == 2 && sp.nsp > 16)
             return fail(ctx, FIC_ERR_ARG, "FIC_SEARCH=direct supports at most 16 contrast values > 0");
-        CK(fic::launch_t2f(P.C, &P.d_misc[0], slots, sl, sp.nsp, ptr<float>(ctx->b_t2f),
-                           (P.mode == 0 && sp.nsp > 2) ? 1 : 0, st));
-        if (sp.nsp > 0 && slots > 0) ctx->launches += 1;
+        if (!t2f_pre) {
+            CK(fic::launch_t2f(P.C, &P.d_misc[0], slots, sl, sp.nsp, ptr<float>(ctx->b_t2f),
+                               (P.mode == 0 && sp.nsp > 2) ? 1 : 0, st));
+            if (sp.nsp > 0 && slots > 0) ctx->launches += 1;
+        }
         if (ctx->timing) CK(cudaEventRecord(ctx->ev[level_slot][1], st));
         if (sp.nsp > 0) {
             if (P.mode == 2) CK(fic::launch_search(P.B, sp.nsp, sp, st));
@@ -761,7 +786,15 @@ static fic_status encode_body(fic_ctx *ctx, const uint8_t *img, int32_t N, int32
 
     const int64_t G = N / B_max;
     const int64_t Gmin = N / B_min;
-    CK(grow(ctx, ctx->b_child, (size_t)(Gmin * Gmin) + 16));
+    // the child bitmap is all zero between encodes: finalize marks it, select_grid clears what it
+    // consumes; a fresh buffer or an encode that stopped half way is cleared here once
+    {
+        void *before = ctx->b_child.p;
+        CK(grow(ctx, ctx->b_child, (size_t)(Gmin * Gmin) + 16));
+        if (ctx->b_child.p != before || !ctx->child_clean)
+            CK(cudaMemsetAsync(ctx->b_child.p, 0, ctx->b_child.cap, st));
+        ctx->child_clean = false;
+    }
     CK(grow(ctx, ctx->b_rng[0], sizeof(int2) * (size_t)(Gmin * Gmin)));
     CK(grow(ctx, ctx->b_rng[1], sizeof(int2) * (size_t)(Gmin * Gmin)));
     // range-count upper bounds of every level, and per-level slices of the record / accepted
@@ -791,6 +824,7 @@ static fic_status encode_body(fic_ctx *ctx, const uint8_t *img, int32_t N, int32
         if (ctx->timing >= 2) CK(cudaEventRecord(ctx->ev[l][0], ps));
         CKS(pool_enqueue(ctx, ctx->levels[l], img, N, B_max >> l, L, h_topk ? -1.0 : h_tau[l],
                          h_topk ? h_topk[l] : 0, ps));
+        CKS(t2f_enqueue(ctx, ctx->levels[l], h_s + s_off[l], h_n_s[l], ps));
         if (ctx->timing >= 2) CK(cudaEventRecord(ctx->ev[l][4], ps));
         if (l > 0) CK(cudaEventRecord(ctx->pool_ready[l], ps));
         ctx->stats[l].kernel_launches = ctx->launches;
@@ -814,11 +848,11 @@ static fic_status encode_body(fic_ctx *ctx, const uint8_t *img, int32_t N, int32
         const int64_t Gc = N / (B / 2 > 0 ? B / 2 : 1);
         bound[l] = n_r_max;
         if (l > 0) CK(cudaStreamWaitEvent(st, ctx->pool_ready[l], 0));
-        if (!last) CK(cudaMemsetAsync(child, 0, (size_t)(Gc * Gc), st));
         fic_record *rec_l = ptr<fic_record>(ctx->b_rec) + rec_off[l];
         uint8_t *acc_l = ptr<uint8_t>(ctx->b_acc) + rec_off[l];
         CKS(level_enqueue(ctx, P, img, ptr<int2>(ctx->b_rng[cur]), d_counts + 32 + l, n_r_max, h_s + s_off[l],
                           h_n_s[l], h_rms_tol[l], last, rec_l, acc_l, last ? nullptr : child, l, d_err));
+        ctx->levels[l].t2f_ready = 0;
         // the accepted records of this level go to `out` on the side stream (in level order, after
         // the pools there), off the critical path of the next level's search
         CK(cudaEventRecord(ctx->level_done[l], st));
@@ -842,11 +876,25 @@ static fic_status encode_body(fic_ctx *ctx, const uint8_t *img, int32_t N, int32
     for (int l = 1; l < nl; ++l) CK(cudaStreamWaitEvent(st, ctx->pool_ready[l], 0));
     CK(cudaEventRecord(ctx->main_ready, ctx->side));
     CK(cudaStreamWaitEvent(st, ctx->main_ready, 0));
+    const bool trace = ctx->timing >= 2 && getenv("FIC_TRACE");
+    if (trace) CK(cudaEventRecord(ctx->ev[fic::kMaxLevels - 1][0], st));
+    {  // the pool counters (n_kept) of the levels next to the others, then one copy
+        fic::U64Ptrs src;
+        for (int l = 0; l < nl; ++l) src.p[l] = ctx->levels[l].d_misc;
+        CK(fic::launch_gather_u64(d_counts + 48, src, nl, st));
+    }
     CK(cudaMemcpyAsync(ctx->h_counts, d_counts, 64 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
-    for (int l = 0; l < nl; ++l)  // pool counters (n_kept) of the levels
-        CK(cudaMemcpyAsync(ctx->h_counts + 48 + l, ctx->levels[l].d_misc, sizeof(unsigned long long),
-                           cudaMemcpyDeviceToHost, st));
+    if (trace) CK(cudaEventRecord(ctx->ev[fic::kMaxLevels - 1][1], st));
+    const auto hs0 = std::chrono::steady_clock::now();
     CK(cudaStreamSynchronize(st));
+    const auto hs1 = std::chrono::steady_clock::now();
+    if (trace) fprintf(stderr, "[trace] host waited %.3f ms in the sync\n", std::chrono::duration<double, std::milli>(hs1 - hs0).count());
+    if (trace) {
+        float a = 0, b = 0;
+        cudaEventElapsedTime(&a, ctx->ev[0][0], ctx->ev[fic::kMaxLevels - 1][0]);
+        cudaEventElapsedTime(&b, ctx->ev[0][0], ctx->ev[fic::kMaxLevels - 1][1]);
+        fprintf(stderr, "[trace] joined at %.3f ms, counters copied at %.3f ms\n", a, b);
+    }
     const unsigned long long *h = ctx->h_counts;
     if (*reinterpret_cast<const int32_t *>(h + 24) == FIC_ERR_EMPTY_POOL)
         return fail(ctx, FIC_ERR_EMPTY_POOL, "empty domain pool at a level that has ranges");
@@ -887,6 +935,8 @@ static fic_status encode_body(fic_ctx *ctx, const uint8_t *img, int32_t N, int32
             }
         }
     }
+    for (int l = 0; l < nl; ++l) ctx->levels[l].t2f_ready = 0;
+    ctx->child_clean = true;  // every bitmap byte finalize marked was consumed by select_grid
     const int64_t total = (int64_t)ctx->h_counts[0];
     *h_n_out = total;
     if (total > capacity) return fail(ctx, FIC_ERR_CAPACITY, "output capacity too small");

@@ -52,6 +52,8 @@ struct Pool {
     unsigned long long *d_misc = nullptr;  // [0] = n_kept, [1] = Cmax, [2] = max |dh|_2 (float bits)
     double dnmax = 0.0;
     Buf b_keys, b_keep, b_kept, b_Dt, b_SDf, b_SD, b_C, b_misc, b_Dc, b_Dtc, b_F2, b_blocksum, b_topk;
+    Buf b_t2f;           // fp32 filter table of this level, enqueued with the pool (fic_encode)
+    int t2f_ready = 0;   // b_t2f holds the table for the level's s set (reset after the level)
     int device = 0;
 };
 
@@ -173,6 +175,11 @@ cudaError_t launch_select_records(const uint8_t *flags, int64_t n, int64_t *bloc
 cudaError_t launch_set_u64(unsigned long long *d, unsigned long long v, cudaStream_t st);
 // *d_acc += *d_add (single thread)
 cudaError_t launch_accumulate(unsigned long long *d_acc, const unsigned long long *d_add, cudaStream_t st);
+// dst[i] = *src[i] for i < n <= 8 (one launch instead of n device -> host copies)
+struct U64Ptrs {
+    const unsigned long long *p[8];
+};
+cudaError_t launch_gather_u64(unsigned long long *dst, const U64Ptrs &src, int n, cudaStream_t st);
 size_t select_blocksum_len(int64_t n);
 cudaError_t launch_top_flags(uint8_t *flags, int64_t G, int32_t shard, int32_t n_shards,
                              cudaStream_t st);

@@ -156,105 +156,17 @@ cudaError_t launch_entropy_keys(const uint8_t *img, int32_t N, int32_t B, int32_
 }
 
 // ------------------------------------------------------------------------- order-preserving select
-// Three passes: per-block counts -> single-block exclusive scan -> per-block scatter.
-constexpr int kSelThreads = 256, kSelItems = 16, kSelBlock = kSelThreads * kSelItems;
+constexpr int kSelBlock = 4096;  // flags per CTA (select_chain_kernel); one scratch word each
 
 size_t select_blocksum_len(int64_t n) { return (size_t)((n + kSelBlock - 1) / kSelBlock) + 1; }
 
-__device__ __forceinline__ int thread_flag_count(const uint8_t *flags, int64_t n, int64_t base) {
-    int cnt = 0;
-    if (base + kSelItems <= n && ((reinterpret_cast<uintptr_t>(flags + base) & 15) == 0)) {
-        const uint4 v = *reinterpret_cast<const uint4 *>(flags + base);
-        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-        for (int q = 0; q < 4; ++q) cnt += __popc(w[q] & 0x01010101u);  // flags are 0/1 bytes
-    } else {
-        for (int q = 0; q < kSelItems; ++q)
-            if (base + q < n) cnt += flags[base + q] & 1;
-    }
-    return cnt;
-}
-
-__global__ void __launch_bounds__(kSelThreads) select_count_kernel(const uint8_t *__restrict__ flags,
-                                                                   int64_t n, int64_t *blocksum) {
-    __shared__ int wsum[kSelThreads / 32];
-    const int64_t base = (int64_t)blockIdx.x * kSelBlock + (int64_t)threadIdx.x * kSelItems;
-    int cnt = base < n ? thread_flag_count(flags, n, base) : 0;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-    if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = cnt;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        int t = 0;
-        for (int w = 0; w < kSelThreads / 32; ++w) t += wsum[w];
-        blocksum[blockIdx.x] = t;
-    }
-}
-
-// exclusive scan of blocksum[0..nb) in place, total -> *d_total (single block of 1024 threads)
-__global__ void __launch_bounds__(1024) select_scan_kernel(int64_t *blocksum, int64_t nb,
-                                                           unsigned long long *d_total) {
-    __shared__ int64_t part[1024];
-    const int t = threadIdx.x;
-    const int64_t per = (nb + 1023) / 1024;
-    const int64_t b0 = t * per, b1 = min(nb, b0 + per);
-    int64_t s = 0;
-    for (int64_t b = b0; b < b1; ++b) s += blocksum[b];
-    part[t] = s;
-    __syncthreads();
-    for (int o = 1; o < 1024; o <<= 1) {
-        int64_t v = t >= o ? part[t - o] : 0;
-        __syncthreads();
-        part[t] += v;
-        __syncthreads();
-    }
-    int64_t run = t ? part[t - 1] : 0;
-    for (int64_t b = b0; b < b1; ++b) {
-        const int64_t v = blocksum[b];
-        blocksum[b] = run;
-        run += v;
-    }
-    if (t == 1023) *d_total = (unsigned long long)part[1023];
-}
-
-template <class Emit>
-__global__ void __launch_bounds__(kSelThreads) select_scatter_kernel(const uint8_t *__restrict__ flags,
-                                                                     int64_t n,
-                                                                     const int64_t *__restrict__ blockoff,
-                                                                     Emit emit) {
-    __shared__ int wsum[kSelThreads / 32];
-    const int64_t base = (int64_t)blockIdx.x * kSelBlock + (int64_t)threadIdx.x * kSelItems;
-    uint8_t f[kSelItems];
-#pragma unroll
-    for (int q = 0; q < kSelItems; ++q) f[q] = (base + q < n) ? (flags[base + q] & 1) : 0;
-    int cnt = 0;
-#pragma unroll
-    for (int q = 0; q < kSelItems; ++q) cnt += f[q];
-    // block exclusive scan of cnt
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    int incl = cnt;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const int v = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += v;
-    }
-    if (lane == 31) wsum[warp] = incl;
-    __syncthreads();
-    int woff = 0;
-    for (int w = 0; w < warp; ++w) woff += wsum[w];
-    int64_t pos = blockoff[blockIdx.x] + woff + incl - cnt;
-#pragma unroll
-    for (int q = 0; q < kSelItems; ++q)
-        if (f[q]) emit(base + q, pos++);
-}
-
 struct EmitIndex {
-    static constexpr bool kChainOk = true;
+    static constexpr bool kClear = false;
     int32_t *out;
     __device__ void operator()(int64_t i, int64_t pos) const { out[pos] = (int32_t)i; }
 };
-struct EmitGrid {
-    static constexpr bool kChainOk = true;
+struct EmitGrid {  // the child bitmap is cleared as it is consumed (ready for the next level)
+    static constexpr bool kClear = true;
     int2 *out;
     int64_t G;
     int32_t B;
@@ -272,7 +184,7 @@ __device__ __forceinline__ void copy_record(fic_record *dst, const fic_record *s
 }
 
 struct EmitRecord {
-    static constexpr bool kChainOk = false;
+    static constexpr bool kClear = false;
     const fic_record *in;
     fic_record *out;
     const unsigned long long *base;
@@ -290,7 +202,7 @@ struct EmitRecord {
 // buffer is never cleared.  Predecessors have lower block indices, which are dispatched first.
 constexpr int kChainItems = 16, kChainThreads = 256, kChainBlock = kChainItems * kChainThreads;
 template <class Emit>
-__global__ void __launch_bounds__(kChainThreads) select_chain_kernel(const uint8_t *__restrict__ flags, int64_t n,
+__global__ void __launch_bounds__(kChainThreads) select_chain_kernel(const uint8_t *flags, int64_t n,
                                                                      Emit emit, unsigned long long *state,
                                                                      uint32_t tag, unsigned long long *d_total) {
     __shared__ int wsum[kChainThreads / 32];
@@ -301,13 +213,17 @@ __global__ void __launch_bounds__(kChainThreads) select_chain_kernel(const uint8
     if (b0 + kChainItems <= n && ((reinterpret_cast<uintptr_t>(flags) & 15) == 0)) {
         const uint4 v = *reinterpret_cast<const uint4 *>(flags + b0);
         w[0] = v.x; w[1] = v.y; w[2] = v.z; w[3] = v.w;
+        if constexpr (Emit::kClear) *reinterpret_cast<uint4 *>(const_cast<uint8_t *>(flags) + b0) = make_uint4(0, 0, 0, 0);
     } else {
 #pragma unroll
         for (int q = 0; q < kChainItems / 4; ++q) {
             uint32_t x = 0;
             for (int b = 0; b < 4; ++b) {
                 const int64_t i = b0 + 4 * q + b;
-                if (i < n) x |= (uint32_t)(flags[i] & 1) << (8 * b);
+                if (i < n) {
+                    x |= (uint32_t)(flags[i] & 1) << (8 * b);
+                    if constexpr (Emit::kClear) const_cast<uint8_t *>(flags)[i] = 0;
+                }
             }
             w[q] = x;
         }
@@ -379,16 +295,9 @@ static cudaError_t select_run(const uint8_t *flags, int64_t n, int64_t *blocksum
                               unsigned long long *d_total, cudaStream_t st) {
     const int64_t nb = (n + kSelBlock - 1) / kSelBlock;
     if (nb == 0) return cudaMemsetAsync(d_total, 0, sizeof(unsigned long long), st);
-    if (Emit::kChainOk) {  // (40-byte records keep the three-pass form: side stream, wide copies)
-        const int64_t nc = (n + kChainBlock - 1) / kChainBlock;
-        static_assert(kChainBlock == kSelBlock, "blocksum scratch holds one word per chain block");
-        select_chain_kernel<Emit><<<(unsigned)nc, kChainThreads, 0, st>>>(
-            flags, n, emit, reinterpret_cast<unsigned long long *>(blocksum), next_chain_tag(), d_total);
-        return cudaGetLastError();
-    }
-    select_count_kernel<<<(unsigned)nb, kSelThreads, 0, st>>>(flags, n, blocksum);
-    select_scan_kernel<<<1, 1024, 0, st>>>(blocksum, nb, d_total);
-    select_scatter_kernel<<<(unsigned)nb, kSelThreads, 0, st>>>(flags, n, blocksum, emit);
+    static_assert(kChainBlock == kSelBlock, "blocksum scratch holds one word per chain block");
+    select_chain_kernel<Emit><<<(unsigned)nb, kChainThreads, 0, st>>>(
+        flags, n, emit, reinterpret_cast<unsigned long long *>(blocksum), next_chain_tag(), d_total);
     return cudaGetLastError();
 }
 
@@ -414,6 +323,16 @@ cudaError_t launch_set_u64(unsigned long long *d, unsigned long long v, cudaStre
 }
 
 __global__ void accumulate_kernel(unsigned long long *acc, const unsigned long long *add) { *acc += *add; }
+
+__global__ void gather_u64_kernel(unsigned long long *dst, const U64Ptrs src, int n) {
+    if ((int)threadIdx.x < n) dst[threadIdx.x] = *src.p[threadIdx.x];
+}
+
+cudaError_t launch_gather_u64(unsigned long long *dst, const U64Ptrs &src, int n, cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    gather_u64_kernel<<<1, 32, 0, st>>>(dst, src, n);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_accumulate(unsigned long long *d_acc, const unsigned long long *d_add, cudaStream_t st) {
     accumulate_kernel<<<1, 1, 0, st>>>(d_acc, d_add);
