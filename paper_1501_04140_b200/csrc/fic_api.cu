@@ -255,7 +255,9 @@ fic_status t2f_enqueue(fic_ctx *ctx, Pool &P, const double *h_s, int32_t n_s, cu
 fic_status level_enqueue(fic_ctx *ctx, const Pool &P, const uint8_t *img, const int2 *ranges,
                          const unsigned long long *d_nr, int64_t n_r_max, const double *h_s, int32_t n_s,
                          double rms_tol, int is_min, fic_record *rec, uint8_t *acc, uint8_t *child,
-                         int level_slot, int32_t *d_err) {
+                         int level_slot, int32_t *d_err, fic_record *out_direct = nullptr,
+                         const unsigned long long *d_base = nullptr, int64_t capacity = 0,
+                         unsigned long long *d_level_count = nullptr, cudaEvent_t before_finalize = nullptr) {
     cudaStream_t st = ctx->stream;
     if (n_r_max == 0) return FIC_OK;
     fic::SearchParams sp;
@@ -366,7 +368,9 @@ fic_status level_enqueue(fic_ctx *ctx, const Pool &P, const uint8_t *img, const 
     fp.n_s = n_s; fp.has_zero = sp.has_zero; fp.j_zero = sp.j_zero;
     fp.rms_tol = rms_tol; fp.is_min = is_min;
     fp.rec = rec; fp.accepted = acc; fp.child = child;
-    if (acc) CK(cudaMemsetAsync(acc, 0, (size_t)n_r_max, st));
+    fp.out_direct = out_direct; fp.d_base = d_base; fp.capacity = capacity; fp.d_level_count = d_level_count;
+    if (acc && !out_direct) CK(cudaMemsetAsync(acc, 0, (size_t)n_r_max, st));
+    if (before_finalize) CK(cudaStreamWaitEvent(st, before_finalize, 0));
     CK(fic::launch_finalize(fp, st));
     ctx->launches += 1;
     if (ctx->timing >= 2) CK(cudaEventRecord(ctx->ev[level_slot][3], st));
@@ -850,17 +854,29 @@ static fic_status encode_body(fic_ctx *ctx, const uint8_t *img, int32_t N, int32
         if (l > 0) CK(cudaStreamWaitEvent(st, ctx->pool_ready[l], 0));
         fic_record *rec_l = ptr<fic_record>(ctx->b_rec) + rec_off[l];
         uint8_t *acc_l = ptr<uint8_t>(ctx->b_acc) + rec_off[l];
-        CKS(level_enqueue(ctx, P, img, ptr<int2>(ctx->b_rng[cur]), d_counts + 32 + l, n_r_max, h_s + s_off[l],
-                          h_n_s[l], h_rms_tol[l], last, rec_l, acc_l, last ? nullptr : child, l, d_err));
+        if (last) {
+            // every range of the last level is accepted: finalize writes the records straight
+            // into `out` after those the side stream gathered for the earlier levels
+            // (finalize waits for that gathering; the search overlaps it)
+            CK(cudaEventRecord(ctx->main_ready, ctx->side));
+            CKS(level_enqueue(ctx, P, img, ptr<int2>(ctx->b_rng[cur]), d_counts + 32 + l, n_r_max,
+                              h_s + s_off[l], h_n_s[l], h_rms_tol[l], 1, rec_l, acc_l, nullptr, l, d_err, out,
+                              d_counts + 0, capacity, d_counts + 16 + l, ctx->main_ready));
+            CK(fic::launch_accumulate(d_counts + 0, d_counts + 16 + l, st));
+            ctx->launches += 1;
+        } else {
+            CKS(level_enqueue(ctx, P, img, ptr<int2>(ctx->b_rng[cur]), d_counts + 32 + l, n_r_max,
+                              h_s + s_off[l], h_n_s[l], h_rms_tol[l], 0, rec_l, acc_l, child, l, d_err));
+            // the accepted records of this level go to `out` on the side stream (in level order,
+            // after the pools there), off the critical path of the next level's search
+            CK(cudaEventRecord(ctx->level_done[l], st));
+            CK(cudaStreamWaitEvent(ctx->side, ctx->level_done[l], 0));
+            CK(fic::launch_select_records(acc_l, n_r_max, ptr<int64_t>(ctx->b_blocksum2), rec_l, out,
+                                          d_counts + 0, capacity, d_counts + 16 + l, ctx->side));
+            CK(fic::launch_accumulate(d_counts + 0, d_counts + 16 + l, ctx->side));
+            ctx->launches += 2;
+        }
         ctx->levels[l].t2f_ready = 0;
-        // the accepted records of this level go to `out` on the side stream (in level order, after
-        // the pools there), off the critical path of the next level's search
-        CK(cudaEventRecord(ctx->level_done[l], st));
-        CK(cudaStreamWaitEvent(ctx->side, ctx->level_done[l], 0));
-        CK(fic::launch_select_records(acc_l, n_r_max, ptr<int64_t>(ctx->b_blocksum2), rec_l, out, d_counts + 0,
-                                      capacity, d_counts + 16 + l, ctx->side));
-        CK(fic::launch_accumulate(d_counts + 0, d_counts + 16 + l, ctx->side));
-        ctx->launches += 4;
         if (!last) {
             CK(fic::launch_select_grid(child, Gc, B / 2, ptr<int64_t>(ctx->b_blocksum),
                                        ptr<int2>(ctx->b_rng[cur ^ 1]), d_counts + 33 + l, st));

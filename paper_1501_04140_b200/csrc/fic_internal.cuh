@@ -116,6 +116,12 @@ struct FinalizeParams {
     fic_record *rec;
     uint8_t *accepted;
     uint8_t *child;  // child bitmap [(N/(B/2))^2] or null
+    // last quadtree level (every range accepted): records straight into the output at
+    // *d_base + r (< capacity), the level's count into *d_level_count; rec / accepted unused
+    fic_record *out_direct;
+    const unsigned long long *d_base;
+    int64_t capacity;
+    unsigned long long *d_level_count;
 };
 
 // Dynamic mapping of a CTA to (range group, domain split) from the actual counts: the grid is

@@ -538,10 +538,19 @@ __global__ void finalize_kernel(const __grid_constant__ FinalizeParams P) {
     uint64_t w[5] = {0, 0, 0, 0, 0};
     memcpy(w, &rec, 28);
     memcpy(&w[4], &rec.err, 8);
-    uint64_t *dst = reinterpret_cast<uint64_t *>(P.rec + r);
+    fic_record *slot = P.rec + r;
+    if (P.out_direct) {  // last level: every range is accepted, in range order
+        if (r == 0) *P.d_level_count = (unsigned long long)*P.d_nr;
+        const int64_t o = (int64_t)*P.d_base + r;
+        slot = o < P.capacity ? P.out_direct + o : nullptr;
+    } else {
+        P.accepted[r] = (uint8_t)acc;
+    }
+    if (slot) {
+        uint64_t *dst = reinterpret_cast<uint64_t *>(slot);
 #pragma unroll
-    for (int q = 0; q < 5; ++q) dst[q] = w[q];
-    P.accepted[r] = (uint8_t)acc;
+        for (int q = 0; q < 5; ++q) dst[q] = w[q];
+    }
     if (!acc && P.child) {
         const int h = B / 2;
         const int64_t Gc = P.N / h;
