@@ -445,6 +445,7 @@ struct TCParams {
     double smax, cmax;
     Partial *part;
     unsigned long long *exact_count;
+    int32_t lockstep;  // full rounds in lockstep (pool larger than ~L2/2), else all flattened
 };
 
 using TCRange = TCRangeG;
@@ -454,6 +455,38 @@ using TCRange = TCRangeG;
 //     min_s e_s >= A - Bq^2 / C        (the unconstrained minimum of the parabola, Eq. 2)
 // evaluated as g = -(Bq Bq) u, u = RN(1/C) per domain (t2f row 0), with Bq converted exactly
 // (int -> float RN) -- margin 4.1u A (tc_range_meta_kernel).
+// Work of one persistent CTA: a sequence of segments (one range group, a run of its domain
+// tiles).  Pools larger than about half of L2 (P.lockstep): full rounds first -- while at least
+// gridDim.x groups remain, CTA c takes group k gridDim.x + c over every tile, so all SMs stream
+// the pool in the same order and each tile comes from HBM about once per round (C4: 33 -> 29.6 ms).
+// The remaining groups (the tail; every group when the pool sits in L2, where spreading the SMs
+// over the pool beats 148 SMs requesting the same lines) are flattened into (group, tile) order
+// and cut into equal runs, one per CTA, so no SM idles in the last round; a group cut by CTA
+// boundaries leaves one partial per run (slot c - c_first < ns_cap).
+struct SegPlan {  // per CTA, in shared memory (kept out of the tile loops' registers)
+    int R, Gc, c, T, gbase, n_tail;
+    long long fbeg, f1, W;
+};
+// segment k of the CTA's plan: (group, first tile, tile count, partial slot, last of its group)
+__device__ __forceinline__ void plan_segment(const SegPlan *sp, int k, int &grp, int &ta, int &ntl, int &slot,
+                                             bool &lastseg) {
+    const volatile SegPlan *v = sp;
+    const int R = v->R, T = v->T;
+    if (k < R) {
+        grp = k * v->Gc + v->c; ta = 0; ntl = T; slot = 0; lastseg = true;
+        return;
+    }
+    const long long fbeg = v->fbeg, f1 = v->f1, W = v->W;
+    const long long g = fbeg / T + (k - R);
+    const long long s0 = k == R ? fbeg : g * T;
+    const long long fe = min(f1, (g + 1) * T);
+    grp = v->gbase + (int)g;
+    ta = (int)(s0 - g * T);
+    ntl = (int)(fe - s0);
+    slot = (int)(v->c - (g * T) / W);
+    lastseg = fe == (g + 1) * T;
+}
+
 template <int B, int NSP>
 __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __grid_constant__ TCParams P) {
     using Cf = TCfg<B>;
@@ -479,19 +512,32 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
     const int n_r = (int)*P.d_nr;
     const int T = (int)((P.d_misc[0] + kTileD - 1) / kTileD);  // domain tiles
     const int groups = (n_r + NR - 1) / NR;
-    const int64_t total = (int64_t)groups * T;
-    // persistent CTAs (one per SM): CTA c owns the flattened (group, tile) range [c W, (c+1) W),
-    // so every SM gets the same number of tiles whatever the group count; a group cut by CTA
-    // boundaries leaves one partial per CTA (slot c - c_first(g) < ns_cap).  Decided before any
-    // barrier, uniformly per CTA.
-    int64_t Gc = gridDim.x;
-    Gc = min(Gc, (int64_t)groups * (P.ns_cap - 1));  // ceil(T / W) + 1 <= ns_cap slots per group
-    Gc = min(Gc, max((int64_t)1, total / 4));         // >= ~4 tiles per CTA
-    if (total == 0 || (int64_t)blockIdx.x >= Gc) return;
-    const int64_t W = (total + Gc - 1) / Gc;
-    const int64_t f0 = (int64_t)blockIdx.x * W, f1 = min(total, f0 + W);
-    if (f0 >= f1) return;
-    const int nseg_max = (int)((T + W - 1) / W) + 1;
+    // persistent CTAs (one per SM), work decided before any barrier, uniformly per CTA (SegPlan)
+    __shared__ SegPlan plan;
+    int nseg_max = 1, nseg = 0;
+    {
+        const int R = P.lockstep ? groups / (int)gridDim.x : 0;
+        const int rem = groups - R * (int)gridDim.x;
+        const long long tail = (long long)rem * T;
+        long long Gt = gridDim.x;
+        Gt = min(Gt, (long long)rem * (P.ns_cap - 1));  // ceil(T / W) + 1 <= ns_cap slots per group
+        Gt = min(Gt, max(1LL, tail / 4));               // >= ~4 tiles per run
+        Gt = max(Gt, 1LL);
+        const long long W = (tail + Gt - 1) / Gt;
+        long long fbeg = 0, f1 = 0;
+        if (tail > 0 && (long long)blockIdx.x < Gt) {
+            fbeg = (long long)blockIdx.x * W;
+            f1 = min(tail, fbeg + W);
+        }
+        const int n_tail = f1 > fbeg ? (int)((f1 - 1) / T - fbeg / T + 1) : 0;
+        if (tail > 0) nseg_max = (int)((T + W - 1) / W) + 1;
+        nseg = T > 0 ? R + n_tail : 0;
+        if (threadIdx.x == 0) {
+            plan.R = R; plan.Gc = gridDim.x; plan.c = blockIdx.x; plan.T = T; plan.gbase = R * (int)gridDim.x;
+            plan.n_tail = n_tail; plan.fbeg = fbeg; plan.f1 = f1; plan.W = W;
+        }
+    }
+    if (nseg == 0) return;
     if (blockIdx.x == 0 && threadIdx.x == 0) *P.d_ns = (unsigned long long)min(nseg_max, P.ns_cap);
 
     // ---- setup: barriers, TMEM, per-range constants, the resident range operand
@@ -530,8 +576,11 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
         static_assert(Cf::STAGE_BYTES % (16 * kCopyLanes) == 0, "bulk copies need 16-byte multiples");
         if (lane < kCopyLanes) {
             int i = 0;
-            for (int64_t f = f0; f < f1; ++f) {  // tile by tile across the CTA's segments
-                const int tile = (int)(f % T);
+            for (int k = 0; k < nseg; ++k) {
+            int grp, ta, ntl, slot;
+            bool lastseg;
+            plan_segment(&plan, k, grp, ta, ntl, slot, lastseg);
+            for (int tile = ta; tile < ta + ntl; ++tile) {  // tile by tile across the CTA's segments
                 for (int ch = 0; ch < CH; ++ch, ++i) {
                     const int s = i % STAGES;
                     if (i >= STAGES) tmbar_wait(&empty[s], (uint32_t)(((i / STAGES) + 1) & 1));
@@ -541,28 +590,32 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
                               P.Dtc + ((size_t)tile * CH + ch) * Cf::STAGE_BYTES + lane * PART, PART, &full[s]);
                 }
             }
+            }
         } else if (lane == kCopyLanes) {
             // the resident range operand of each segment's group (tc_range_operand_kernel), once
             // the previous segment's MMAs released it
-            int k = 0;
-            for (int64_t f = f0; f < f1; ++k) {
-                const int g = (int)(f / T), kb = k % Cf::BBUF;
+            for (int k = 0; k < nseg; ++k) {
+                int grp, ta, ntl, slot;
+                bool lastseg;
+                plan_segment(&plan, k, grp, ta, ntl, slot, lastseg);
+                const int kb = k % Cf::BBUF;
                 if (k >= Cf::BBUF) tmbar_wait(&bbar[Cf::BBUF + kb], (uint32_t)(((k / Cf::BBUF) - 1) & 1));
                 tmbar_expect_tx(&bbar[kb], Cf::B_BYTES);
-                tbulk_g2s(sB + kb * Cf::B_BYTES, P.Bop + (size_t)g * Cf::B_BYTES, Cf::B_BYTES, &bbar[kb]);
-                f = min(f1, (int64_t)(g + 1) * T);
+                tbulk_g2s(sB + kb * Cf::B_BYTES, P.Bop + (size_t)grp * Cf::B_BYTES, Cf::B_BYTES, &bbar[kb]);
             }
         }
     } else if (warp == 1) {
         // ================= MMA issuer
         constexpr uint32_t idesc = idesc_i8(NN);
-        int i = 0, tl = 0, k = 0;
-        for (int64_t f = f0; f < f1; ++k) {
-            const int64_t fe = min(f1, (int64_t)(f / T + 1) * T);  // end of this segment
+        int i = 0, tl = 0;
+        for (int k = 0; k < nseg; ++k) {
+            int grp, ta, ntl, slot;
+            bool lastseg;
+            plan_segment(&plan, k, grp, ta, ntl, slot, lastseg);
             const int kb = k % Cf::BBUF;
             tmbar_wait(&bbar[kb], (uint32_t)((k / Cf::BBUF) & 1));
             const uint32_t bbase = su32(sB + kb * Cf::B_BYTES);
-            for (; f < fe; ++f, ++tl) {
+            for (int tt = 0; tt < ntl; ++tt, ++tl) {
                 const int buf = tl % NBUF;
                 for (int ch = 0; ch < CH; ++ch, ++i) {
                     const int s = i % STAGES;
@@ -640,11 +693,10 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
             return g0;
         };
         int tl = 0;  // tiles consumed by this CTA (TMEM buffer ring position)
-        for (int64_t f = f0; f < f1;) {
-            const int grp = (int)(f / T);
-            const int ta = (int)(f % T);
-            const int64_t fe = min(f1, (int64_t)(grp + 1) * T);
-            const int ntl = (int)(fe - f);
+        for (int k = 0; k < nseg; ++k) {
+            int grp, ta, ntl, slot;
+            bool lastseg;
+            plan_segment(&plan, k, grp, ta, ntl, slot, lastseg);
             const int r0 = grp * NR;
             // ---- segment setup: this group's range constants and thresholds (the previous
             // segment's readers of sR / sThr / sRed have passed the barrier)
@@ -859,16 +911,14 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
                     if (c.e < b.e || (c.e == b.e && (c.d < b.d || (c.d == b.d && c.kj < b.kj)))) b = c;
                 }
                 if (r < n_r) {
-                    const int slot = (int)(blockIdx.x - ((int64_t)grp * T) / W);
                     P.part[(size_t)r * P.ns_cap + slot] = b;
-                    if (fe == (int64_t)(grp + 1) * T) {
+                    if (lastseg) {
                         Partial none;
                         none.e = INFINITY; none.d = INT_MAX; none.kj = INT_MAX;
                         for (int s2 = slot + 1; s2 < nseg_max && s2 < P.ns_cap; ++s2) P.part[(size_t)r * P.ns_cap + s2] = none;
                     }
                 }
             }
-            f = fe;
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) n_exact += __shfl_xor_sync(0xffffffffu, n_exact, o);
@@ -977,6 +1027,7 @@ cudaError_t launch_tc_search(int32_t B, const SearchParams &sp, const uint8_t *D
     p.has_zero = sp.has_zero; p.j_zero = sp.j_zero;
     p.smax = sp.smax;
     p.part = sp.part; p.exact_count = sp.exact_count;
+    p.lockstep = tc_pool_bytes(B, (n_slots + kTileD - 1) / kTileD) > ((size_t)48 << 20) ? 1 : 0;
     switch (B) {
     case 2: return launch_tc_b<2>(p, st);
     case 4: return launch_tc_b<4>(p, st);

@@ -13,7 +13,7 @@ from typing import Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-SO_PATH = os.path.join(_HERE, "libfic.so")
+SO_PATH = os.environ.get("FIC_SO") or os.path.join(_HERE, "libfic.so")  # (FIC_SO: A/B builds)
 
 RECORD_DTYPE = np.dtype([
     ("rx", "<i4"), ("ry", "<i4"), ("B", "<i4"), ("dom", "<i4"), ("dx", "<i4"), ("dy", "<i4"),
