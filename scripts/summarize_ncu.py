@@ -89,7 +89,7 @@ def main():
                       f"{l['ms_pool']:.3f} | {l['ms_search']:.3f} |")
         md.append("")
     if a.launches:
-        md.append("## Launch list (`bench.py --steps 2 --warmup 1`, 4 encodes; cold-cache serialised: compare shares)\n")
+        md.append("## Launch list (`bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e`: 3 warm-up, 2 timed and 2 instrumented encodes; cold-cache serialised: compare shares)\n")
         md.append(launch_table(a.launches))
         md.append("")
     summary = {"round": a.round, "kernels": []}
