@@ -45,11 +45,11 @@ struct TCfg {
     // at most 4 per SM sub-partition, so 128 registers per thread instead of 96 with 18 warps)
     static constexpr int NR = (B == 16) ? 16 : (B == 4 ? 24 : 32);
     static constexpr int N = 8 * NR;                       // MMA N (columns per accumulator)
-    static constexpr int KCH = QR ? 128 : (KP < 256 ? KP : 256);  // K bytes per pipeline stage
+    static constexpr int KCH = QR ? 512 : (KP < 256 ? KP : 256);  // K bytes per pipeline stage
     static constexpr int CH = KP / KCH;                    // stages per domain tile
     static constexpr int STAGE_BYTES = kTileD * KCH;       // A bytes per stage
     // B = 16 is fed by bulk copies (latency x bytes in flight): 8 x 16 KB stages
-    static constexpr int STAGES = QR ? 8 : (B == 8 ? 2 : 4);
+    static constexpr int STAGES = QR ? 2 : (B == 8 ? 2 : 4);
     static constexpr int B_BYTES = N * KB;                 // resident range operand
     // range-operand buffers: 2 where shared memory allows, so the next segment's operand loads
     // while the current segment's MMAs still read the other one
@@ -623,18 +623,18 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
                     if (ch == 0 && tl >= NBUF) tmbar_wait(&tempty[buf], (uint32_t)(((tl / NBUF) + 1) & 1));
                     tc_fence_after();
                     if (lane == 0) {
-                        // QR: the first half of the stages (q plane) accumulates S_q at column 0 of
-                        // the buffer, the second half (r plane) S_r at column N; same B rows
-                        constexpr int CHA = Cf::QR ? CH / 2 : CH;  // stages per accumulator
-                        const int cha = ch % CHA;
-                        const uint32_t dcol = buf * Cf::ACC + ((Cf::QR && ch >= CHA) ? NN : 0);
+                        // K bytes kg of the tile: QR's q plane (kg < n) accumulates S_q at column 0
+                        // of the buffer, its r plane S_r at column N, both against the same B rows
                         const uint32_t a0 = su32(sA + s * Cf::STAGE_BYTES);
-                        const uint32_t b0 = bbase + cha * (KCH / 16) * 128;
 #pragma unroll
                         for (int kk = 0; kk < KCH / 32; ++kk) {
+                            const int kg = ch * KCH + kk * 32;
+                            const int plane = Cf::QR ? kg / n : 0;
+                            const int kp = Cf::QR ? kg - plane * n : kg;
+                            const uint32_t dcol = buf * Cf::ACC + plane * NN;
                             const uint64_t ad = smem_desc(a0 + kk * 256, 128, (KCH / 16) * 128);
-                            const uint64_t bd = smem_desc(b0 + kk * 256, 128, (Cf::KB / 16) * 128);
-                            tc_mma_i8(tmem + dcol, ad, bd, idesc, (cha > 0 || kk > 0) ? 1u : 0u);
+                            const uint64_t bd = smem_desc(bbase + kp * 8, 128, (Cf::KB / 16) * 128);
+                            tc_mma_i8(tmem + dcol, ad, bd, idesc, kp > 0 ? 1u : 0u);
                         }
                         tc_commit(&empty[s]);
                         if (ch == CH - 1) tc_commit(&tfull[buf]);
