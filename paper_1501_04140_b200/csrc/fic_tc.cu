@@ -789,22 +789,23 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
                 // four ranges (32 columns) per tcgen05.ld, the next group in flight while one is scored
                 constexpr int G = HALF / 4;
                 uint32_t vv[64];
+                // the tile's accumulators (<= 2 groups of 4 ranges, or QR's two planes) into
+                // registers, then the buffer goes straight back to the MMA warp: the next MMA into
+                // it overlaps this tile's scoring
+                static_assert(G <= 2 && (!Cf::QR || G == 1), "one tile's accumulators fit vv[64]");
                 tc_ld32<0>(tbase, vv);
+                if constexpr (Cf::QR) tc_ld32<32>(tbase + NN, vv);
+                else if constexpr (G == 2) tc_ld32<32>(tbase + 32, vv);
+                tc_wait_ld();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) tmbar_arrive(&tempty[buf]);
                 if constexpr (Cf::QR) {  // SRD_k = 4 S_q + S_r (exact: < 2^31)
-                    static_assert(!Cf::QR || G == 1, "QR keeps one 4-range group per warp and tile");
-                    tc_ld32<32>(tbase + NN, vv);
-                    tc_wait_ld();
 #pragma unroll
                     for (int i = 0; i < 32; ++i) vv[i] = 4u * vv[i] + vv[32 + i];
-                } else {
-                    tc_wait_ld();
                 }
 #pragma unroll
                 for (int g = 0; g < G; ++g) {
-                    if (g + 1 < G) {
-                        if ((g & 1) == 0) tc_ld32<32>(tbase + (g + 1) * 32, vv);
-                        else tc_ld32<0>(tbase + (g + 1) * 32, vv);
-                    }
                     unsigned pm = 0;
                     int mxs[4];
 #pragma unroll
@@ -865,11 +866,7 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
                     n_exact += qn;
                     qn = 0;
                     __syncwarp();  // reconverge after the (rare, divergent) exact path
-                    if (g + 1 < G) tc_wait_ld();
                 }
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) tmbar_arrive(&tempty[buf]);
             }
             // ---- reduce each range's best over the 128 domain lanes (lexicographic); the HALF
             // shuffle chains interleaved (independent ranges)
