@@ -514,7 +514,10 @@ constexpr int kWinStep = 64;  // domains per frontier per round
 
 constexpr int kStash = 64;  // phase-1 candidates kept per warp (overflow: full phase-2 sweep)
 
-__global__ void __launch_bounds__(256) b2win_kernel(const __grid_constant__ B2Params P) {
+// 6 CTAs (48 warps) per SM: the rounds are L2-latency bound, and more resident warps beat the
+// few spills of the 40-register budget (C3 B = 2: 74 regs 0.312 ms, 64 0.273, 48 0.260, 40 0.251,
+// 32 0.265)
+__global__ void __launch_bounds__(256, 6) b2win_kernel(const __grid_constant__ B2Params P) {
     __shared__ int sStash[8][kStash];
     __shared__ int sNst[8];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
