@@ -246,7 +246,7 @@ fic_status t2f_enqueue(fic_ctx *ctx, Pool &P, const double *h_s, int32_t n_s, cu
     const int64_t slots = P.n_tiles_max * fic::kTileD;
     CK(grow(ctx, P.b_t2f, sizeof(float) * (size_t)slots * (nsp ? nsp : 1)));
     CK(fic::launch_t2f(P.C, &P.d_misc[0], slots, sl, nsp, reinterpret_cast<float *>(P.b_t2f.p),
-                       (P.mode == 0 && nsp > 2) ? 1 : 0, st));
+                       (P.mode == 0 && nsp > 2) ? 1 : 0, P.mode == 0 ? fic::tc_t2_fold(P.B, nsp) : 0.f, st));
     if (nsp > 0 && slots > 0) ctx->launches += 1;
     P.t2f_ready = 1;
     return FIC_OK;
@@ -319,7 +319,8 @@ fic_status level_enqueue(fic_ctx *ctx, const Pool &P, const uint8_t *img, const 
             return fail(ctx, FIC_ERR_ARG, "FIC_SEARCH=direct supports at most 16 contrast values > 0");
         if (!t2f_pre) {
             CK(fic::launch_t2f(P.C, &P.d_misc[0], slots, sl, sp.nsp, ptr<float>(ctx->b_t2f),
-                               (P.mode == 0 && sp.nsp > 2) ? 1 : 0, st));
+                               (P.mode == 0 && sp.nsp > 2) ? 1 : 0,
+                               P.mode == 0 ? fic::tc_t2_fold(P.B, sp.nsp) : 0.f, st));
             if (sp.nsp > 0 && slots > 0) ctx->launches += 1;
         }
         if (ctx->timing) CK(cudaEventRecord(ctx->ev[level_slot][1], st));

@@ -161,6 +161,12 @@ __device__ __forceinline__ bool cta_work(int n_r, int rpc, int n_tiles, int min_
     return true;
 }
 
+// scale of -s/2 in the tcgen05 epilogue's magic-number filter (B <= 8, one or two s), which the
+// t2f table folds the magic constant into; 0 = plain table
+__host__ __device__ constexpr float tc_t2_fold(int B, int nsp) {
+    return (nsp >= 1 && nsp <= 2) ? (B == 2 ? 1.f : (B == 4 ? 2.f : (B == 8 ? 64.f : 0.f))) : 0.f;
+}
+
 // ---- launchers (return cudaError_t of the launch) ---------------------------------------------
 cudaError_t launch_entropy_keys(const uint8_t *img, int32_t N, int32_t B, int32_t L, int32_t A,
                                 const int64_t *d_delta, int64_t lut_m, int64_t T, int use_tau,
@@ -200,7 +206,7 @@ struct SList {
     double s[kMaxS];
 };
 cudaError_t launch_t2f(const int64_t *C, const unsigned long long *d_nk, int64_t n_slots, const SList &spos,
-                       int32_t nsp, float *t2f, int32_t univ, cudaStream_t st);
+                       int32_t nsp, float *t2f, int32_t univ, float fold, cudaStream_t st);
 cudaError_t launch_search(int32_t B, int32_t nsp, const SearchParams &p, cudaStream_t st);
 cudaError_t launch_finalize(const FinalizeParams &p, cudaStream_t st);
 cudaError_t launch_merge_shards(const fic_record *in, const int64_t *d_counts, int32_t n_shards,

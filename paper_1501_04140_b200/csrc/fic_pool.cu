@@ -445,8 +445,12 @@ cudaError_t launch_pool_moments(const uint8_t *img, int32_t N, int32_t B, int32_
 
 // t2f[j][d] = fp32 of (s_j s_j)(C/16) for s_j > 0; +inf for pad slots (never admitted).
 // univ (large s sets, the s-independent filter): t2f[0][d] = RN(1/C) (0 if C = 0), NaN on pads.
+// fold > 0 (tcgen05 filter at B <= 8, one or two s): the table holds RN(t2 - nhs_j * 1.5 * 2^23)
+// with nhs_j = -RN(s_j / 2) * fold, so the epilogue's g = fma(nhs, magic-converted Bq, t2') needs
+// no subtraction of the magic constant (the extra rounding is in the filter margin)
 __global__ void t2f_kernel(const int64_t *__restrict__ C, const unsigned long long *__restrict__ d_nk,
-                           int64_t n_slots, const SList spos, int32_t nsp, float *__restrict__ t2f, int32_t univ) {
+                           int64_t n_slots, const SList spos, int32_t nsp, float *__restrict__ t2f, int32_t univ,
+                           float fold) {
     const int64_t d = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (d >= n_slots) return;
     const int64_t n_k = (int64_t)*d_nk;
@@ -458,14 +462,19 @@ __global__ void t2f_kernel(const int64_t *__restrict__ C, const unsigned long lo
     const double c16 = __dmul_rn(0.0625, (double)C[d]);
     for (int j = 0; j < nsp; ++j) {
         const double s = spos.s[j];
-        t2f[j * n_slots + d] = d < n_k ? __double2float_rn(__dmul_rn(__dmul_rn(s, s), c16)) : INFINITY;
+        double t = __dmul_rn(__dmul_rn(s, s), c16);
+        if (fold > 0.f) {
+            const double nhs = -(double)__double2float_rn(0.5 * s) * (double)fold;  // as the epilogue
+            t = __dsub_rn(t, nhs * 12582912.0);                                     // (product exact)
+        }
+        t2f[j * n_slots + d] = d < n_k ? __double2float_rn(t) : INFINITY;
     }
 }
 
 cudaError_t launch_t2f(const int64_t *C, const unsigned long long *d_nk, int64_t n_slots, const SList &spos,
-                       int32_t nsp, float *t2f, int32_t univ, cudaStream_t st) {
+                       int32_t nsp, float *t2f, int32_t univ, float fold, cudaStream_t st) {
     if (n_slots == 0 || nsp == 0) return cudaSuccess;
-    t2f_kernel<<<(unsigned)((n_slots + 255) / 256), 256, 0, st>>>(C, d_nk, n_slots, spos, nsp, t2f, univ);
+    t2f_kernel<<<(unsigned)((n_slots + 255) / 256), 256, 0, st>>>(C, d_nk, n_slots, spos, nsp, t2f, univ, fold);
     return cudaGetLastError();
 }
 

@@ -416,6 +416,8 @@ __global__ void tc_range_meta_kernel(const uint8_t *__restrict__ img, int32_t N,
     // <= 64 at B = 8 (floor of Bq / 2 and Bq / 64)
     R.margin = 8.0 * u * (hs * bq + t2m) + 1e-12 * (R.A + hs * bq + t2m) +
                (B == 4 ? hs * 2.0 : (B == 8 ? hs * 64.0 : 0.0)) + 1e-30;
+    // folded magic constant (B <= 8): t2' = RN(t2 - nhs M) adds u |t2 - nhs M| <= u (t2m + hs k M)
+    if (B <= 8) R.margin += 2.0 * u * (t2m + hs * (B == 2 ? 1.0 : (B == 4 ? 2.0 : 64.0)) * 12582912.0);
     // s-independent filter (NSP = 0): Bq rounded once, squared, times RN(1/C): <= 4.04u Bq^2/C <= 4.04u A
     if (univ) R.margin = 4.1 * u * R.A + 1e-12 * R.A + 1e-30;
     meta[r] = R;
@@ -671,14 +673,15 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
                 // exact Bq (int64 at B = 16), one RN conversion
                 bq = (float)((long long)n * mx - (long long)rsr * sd);
             } else if constexpr (B == 2) {
-                // |Bq| <= sqrt(A C) < 2^22: exact int -> float by the 1.5 * 2^23 magic
-                bq = __int_as_float(n * mx - rsr * sd + 0x4B400000) - 12582912.0f;
+                // |Bq| <= sqrt(A C) < 2^22: exact int -> float by the 1.5 * 2^23 magic; the magic
+                // constant itself is folded into t2 (t2f_kernel, fold), so bq = M + Bq here
+                bq = __int_as_float(n * mx - rsr * sd + 0x4B400000);
             } else if constexpr (B == 4) {
-                // |Bq| <= n^2 127.5 510 < 2^24: magic on Bq / 2, error <= 1 (margin)
-                bq = __int_as_float(((n * mx - rsr * sd) >> 1) + 0x4B400000) - 12582912.0f;  // (x 2 in nhs)
+                // |Bq| <= n^2 127.5 510 < 2^24: magic on Bq / 2, error <= 1 (margin); M folded
+                bq = __int_as_float(((n * mx - rsr * sd) >> 1) + 0x4B400000);  // (x 2 in nhs)
             } else if constexpr (B == 8) {
-                // |Bq| < 2^28: magic on Bq / 64, error <= 64 (margin)
-                bq = __int_as_float(((n * mx - rsr * sd) >> 6) + 0x4B400000) - 12582912.0f;  // (x 64 in nhs)
+                // |Bq| < 2^28: magic on Bq / 64, error <= 64 (margin); M folded
+                bq = __int_as_float(((n * mx - rsr * sd) >> 6) + 0x4B400000);  // (x 64 in nhs)
             } else {
                 bq = fmaf((float)n, (float)mx, -((float)rsr * (float)sd));
             }
