@@ -552,12 +552,16 @@ __global__ void __launch_bounds__(256, 6) b2win_kernel(const __grid_constant__ B
     // sqrt C -- far above the fp32 rounding of these few operations, so never too narrow)
     const float sqAf = sqrtf((float)R.A);
     const float ka = (float)(4.0 / sa), kb = (float)(4.0 / sb);
+    // round-up fp32 copies for the per-round bounds (every rounding upward keeps ub >= best and
+    // the stash threshold >= the final one)
+    const float A_ru = __double2float_ru(A), marg_ru = __double2float_ru(margin);
+    const float marg2_ru = __double2float_ru(2.0 * margin);
     // frontiers: f0 [q0, c_a) grows down (s_a), f1 [c_a, q1) grows up (s_a), f2 [q2, c_b) grows
     // down (s_b), f3 [c_b, q3) grows up (s_b); f1 and f2 share [c_a, c_b) and stop when they meet
     int q0 = ca, q1 = ca, q2 = cb, q3 = cb;
     bool al0 = q0 > 0, al1 = q1 < q2, al2 = q1 < q2, al3 = q3 < n_k;
     float gmin = INFINITY;
-    unsigned long long scanned = 0;
+    unsigned scanned = 0;
     // phase 1: rounds over the four frontiers with the fp32 filter; the bound ub = A + gmin +
     // margin (>= best) narrows the windows after every round
     while (al0 || al1 || al2 || al3) {
@@ -568,7 +572,7 @@ __global__ void __launch_bounds__(256, 6) b2win_kernel(const __grid_constant__ B
         const int n3 = al3 ? min(kWinStep, n_k - q3) : 0;
         const int b0 = q0 - n0, b1 = q1, b2 = q2 - n2, b3 = q3;
         q0 -= n0; q1 += n1; q2 -= n2; q3 += n3;
-        scanned += (unsigned long long)(n0 + n1 + n2 + n3);
+        scanned += (unsigned)(n0 + n1 + n2 + n3);
         // next frontier C values (lanes 0..3), in flight with this round's features
         int cn = 0;
         if (lane == 0 && q0 > 0) cn = __ldg(P.Cs + q0 - 1);
@@ -604,16 +608,21 @@ __global__ void __launch_bounds__(256, 6) b2win_kernel(const __grid_constant__ B
             // stash every domain with g <= RU(gmin + 2 margin) (gmin including this round): the
             // final threshold RU(gmin_final + 2 margin) is never larger, so the stash holds every
             // pair phase 2 has to score
-            const float ts = fminf(__double2float_ru(__dadd_rn((double)gmin, 2.0 * margin)), FLT_MAX);
+            const float ts = fminf(__fadd_ru(gmin, marg2_ru), FLT_MAX);
+            unsigned pass = 0;
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                if (gv[i] <= ts) {
-                    const int slot = atomicAdd(&sNst[wib], 1);
-                    if (slot < kStash) sStash[wib][slot] = bf[i & 3] + lane + 32 * (i >> 2);
+            for (int i = 0; i < 8; ++i) pass |= gv[i] <= ts ? 1u << i : 0u;
+            if (__any_sync(0xffffffffu, pass)) {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    if (pass >> i & 1u) {
+                        const int slot = atomicAdd(&sNst[wib], 1);
+                        if (slot < kStash) sStash[wib][slot] = bf[i & 3] + lane + 32 * (i >> 2);
+                    }
                 }
             }
         }
-        const float ub = gmin < INFINITY ? __double2float_ru(__dadd_ru(__dadd_ru(A, (double)gmin), margin)) : INFINITY;
+        const float ub = gmin < INFINITY ? __fadd_ru(__fadd_ru(A_ru, gmin), marg_ru) : INFINITY;
         const float u = sqrtf(fmaxf(ub, 0.f)) * 1.0001f + 1e-3f * (1.f + sqAf);
         const float la = ka * (sqAf - u), lb = kb * (sqAf - u);
         const float cl = (lane == 0 ? la : lb);
@@ -702,7 +711,7 @@ __global__ void __launch_bounds__(256, 6) b2win_kernel(const __grid_constant__ B
         pb.kj = bkj;
         P.part[(size_t)r * P.ns_cap] = pb;
         if (n_exact && P.exact_count) atomicAdd(P.exact_count, (unsigned long long)n_exact);
-        if (P.scan_count) atomicAdd(P.scan_count, scanned);
+        if (P.scan_count) atomicAdd(P.scan_count, (unsigned long long)scanned);
     }
 }
 
