@@ -339,7 +339,9 @@ fic_status level_enqueue(fic_ctx *ctx, const Pool &P, const uint8_t *img, const 
         CK(grow(ctx, ctx->b_gthr, fic::b2_scratch_bytes(n_r_max, sp.ns_cap)));
         CK(fic::launch_b2_search(sp, P.b2, ptr<float>(ctx->b_u), P.kept, P.L, P.A, ctx->b_gthr.p,
                                  ptr<unsigned long long>(ctx->b_counts) + 40 + level_slot, st));
-        ctx->launches += sp.nsp > 0 && n_r_max > 0 ? 3 : 0;  // t2 table, pass 1 scan, pass 2 exact
+        // t2 table, pass 1 scan, pass 2 exact -- or the single window kernel
+        const bool win = sp.b2_window && !sp.has_zero && sp.nsp <= 2;
+        ctx->launches += sp.nsp > 0 && n_r_max > 0 ? (win ? 1 : 3) : 0;
     } else {
         const int nc = fic::fourier_record_stride(P.B);  // >= 8 nO + 1
         const int32_t r_stride = (int32_t)((n_r_max + 31) / 32 * 32);

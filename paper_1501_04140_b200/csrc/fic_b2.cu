@@ -533,15 +533,20 @@ __global__ void __launch_bounds__(256, 6) b2win_kernel(const __grid_constant__ B
     const uint8_t *p0 = P.img + (size_t)rr.y * P.N + rr.x;
     const B2Range R = b2_range(p0[0], p0[1], p0[P.N + 1], p0[P.N]);
     const double A = (double)R.A;
-    const double margin = b2_margin(A, P.smax, cmax);
-    const float nh0 = P.nhs[0], nh1 = P.nsp > 1 ? P.nhs[1] : 0.f;
-    const float2 *T2 = reinterpret_cast<const float2 *>(P.T);  // tw == 2 (pad j: +inf)
+    // t2_j = RN(RN(s_j^2 / 16) C) from the feature's C (exact in fp32, C < 2^24) instead of a
+    // table load: two roundings, 2u t2 more than the table's one -- added to the margin
+    const double margin = b2_margin(A, P.smax, cmax) + 2.0 * 5.9604644775390625e-08 * (P.smax * P.smax * cmax * 0.0625);
+    const float nh0 = P.nhs[0], nh1 = P.nsp > 1 ? P.nhs[1] : P.nhs[0];
+    const float k0 = __double2float_rn(P.spos[0] * P.spos[0] * 0.0625);
+    const float k1 = P.nsp > 1 ? __double2float_rn(P.spos[1] * P.spos[1] * 0.0625) : k0;
+    auto gof = [&](const float4 fv, float &bq) {
+        bq = fmaf(R.sx, fv.y, fabsf(fmaf(R.x2, fv.x, R.dx * fv.z)));
+        return fminf(fmaf(nh0, bq, k0 * fv.w), fmaf(nh1, bq, k1 * fv.w));
+    };
     auto gval = [&](int pos, float &bq, float &cf) {
         const float4 fv = __ldg(P.F + pos);
-        const float2 t2 = __ldg(T2 + pos);
-        bq = fmaf(R.sx, fv.y, fabsf(fmaf(R.x2, fv.x, R.dx * fv.z)));
         cf = fv.w;
-        return fminf(fmaf(nh0, bq, t2.x), fmaf(nh1, bq, t2.y));
+        return gof(fv, bq);
     };
     // s_a >= s_b, centres c_a <= c_b
     const int ia = (P.nsp > 1 && P.spos[1] > P.spos[0]) ? 1 : 0, ib = P.nsp > 1 ? 1 - ia : ia;
@@ -582,7 +587,6 @@ __global__ void __launch_bounds__(256, 6) b2win_kernel(const __grid_constant__ B
         // all of this lane's loads of the round first (up to 8 domains, L2-latency bound), then
         // the arithmetic; absent slots read position 0 and are masked to +inf
         float4 fv[8];
-        float2 tv[8];
         bool ok8[8];
         const int nf[4] = {n0, n1, n2, n3}, bf[4] = {b0, b1, b2, b3};
 #pragma unroll
@@ -593,14 +597,14 @@ __global__ void __launch_bounds__(256, 6) b2win_kernel(const __grid_constant__ B
                 ok8[k * 4 + f] = o < nf[f];
                 const int pos = ok8[k * 4 + f] ? bf[f] + o : 0;
                 fv[k * 4 + f] = __ldg(P.F + pos);
-                tv[k * 4 + f] = __ldg(T2 + pos);
             }
         }
         float g = INFINITY, gv[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-            const float bq = fmaf(R.sx, fv[i].y, fabsf(fmaf(R.x2, fv[i].x, R.dx * fv[i].z)));
-            gv[i] = ok8[i] ? fminf(fmaf(nh0, bq, tv[i].x), fmaf(nh1, bq, tv[i].y)) : INFINITY;
+            float bq;
+            const float gi = gof(fv[i], bq);
+            gv[i] = ok8[i] ? gi : INFINITY;
             g = fminf(g, gv[i]);
         }
         gmin = fminf(gmin, b2_fdec(__reduce_min_sync(0xffffffffu, b2_fkey(g))));
@@ -671,18 +675,17 @@ __global__ void __launch_bounds__(256, 6) b2win_kernel(const __grid_constant__ B
         // four domains per lane per pass: the loads first, then the filter (rare exact path)
         for (int pos0 = a0 + lane; pos0 < a1; pos0 += 128) {
             float4 fv[4];
-            float2 tv[4];
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
                 const int pos = min(pos0 + 32 * i, a1 - 1);
                 fv[i] = __ldg(P.F + pos);
-                tv[i] = __ldg(T2 + pos);
             }
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
                 const int pos = pos0 + 32 * i;
-                const float bq = fmaf(R.sx, fv[i].y, fabsf(fmaf(R.x2, fv[i].x, R.dx * fv[i].z)));
-                if (pos < a1 && fminf(fmaf(nh0, bq, tv[i].x), fmaf(nh1, bq, tv[i].y)) <= thr) {
+                float bq;
+                const float gi = gof(fv[i], bq);
+                if (pos < a1 && gi <= thr) {
                     ++n_exact;
                     int j0;
                     const double e0 = b2_canon(P, A, bq, fv[i].w, j0);
@@ -776,7 +779,8 @@ cudaError_t launch_b2_search(const SearchParams &sp, const B2Pool &bp, float *T,
     const int64_t slots = sp.slot_stride;
     SList sl;
     memcpy(sl.s, sp.spos, sizeof sl.s);
-    if (slots > 0) {
+    const bool win = sp.b2_window && !sp.has_zero && sp.nsp <= 2;  // predefined s: C windows
+    if (slots > 0 && !win) {  // (b2win forms t2 from the feature's C itself)
         b2_t2_kernel<<<(unsigned)((slots + 255) / 256), 256, 0, st>>>(bp.F, &sp.d_misc[0], slots, sl, sp.nsp, tw, T);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
@@ -795,7 +799,7 @@ cudaError_t launch_b2_search(const SearchParams &sp, const B2Pool &bp, float *T,
     p.part = sp.part; p.exact_count = sp.exact_count; p.scan_count = scan_count;
     p.d_nscan = reinterpret_cast<unsigned long long *>(scratch);
     p.gmin = reinterpret_cast<float *>(static_cast<char *>(scratch) + 64);
-    if (sp.b2_window && !sp.has_zero && sp.nsp <= 2) {  // predefined s: Cauchy-Schwarz windows
+    if (win) {  // predefined s: Cauchy-Schwarz windows
         b2win_kernel<<<(unsigned)((sp.n_r + 7) / 8), 256, 0, st>>>(p);
         return cudaGetLastError();
     }
