@@ -329,7 +329,7 @@ fic_status level_enqueue(fic_ctx *ctx, const Pool &P, const uint8_t *img, const 
             else {
                 CK(grow(ctx, ctx->b_rop, fic::tc_range_bytes(P.B, n_r_max)));
                 CK(fic::launch_tc_search(P.B, sp, P.Dtc, slots, ptr<uint8_t>(ctx->b_rop), st));
-                ctx->launches += 2;
+                ctx->launches += 1;  // range preparation (operand + moments, one launch)
             }
             ctx->launches += 1;
         }

@@ -515,10 +515,13 @@ __global__ void finalize_kernel(const __grid_constant__ FinalizeParams P) {
     }
     if (best.kj & kPendIso) best.kj = (kstar_dev(P, rr, best.d) << 8) | (best.kj & 255);
     const int d = best.d, k = best.kj >> 8, j = best.kj & 255;
-    const double E = __ddiv_rn(best.e, (double)n);
+    // n = B^2 is a power of two: the divisions by n and 4n are exact scalings (bit-identical
+    // to __ddiv_rn), done as multiplications
+    const double inv_n = 1.0 / (double)n;
+    const double E = best.e * inv_n;
     const double s = P.s[j];
-    const double Rbar = __ddiv_rn((double)sr, (double)n);
-    const double Dbar = __ddiv_rn((double)P.SD[d], (double)(4 * n));
+    const double Rbar = (double)sr * inv_n;
+    const double Dbar = (double)P.SD[d] * (0.25 * inv_n);
     const double o = __dsub_rn(Rbar, __dmul_rn(s, Dbar));
     const bool acc = P.is_min || E <= __dmul_rn(__dmul_rn(P.rms_tol, P.rms_tol), (double)n);
     const int32_t cand = P.kept[d];

@@ -318,10 +318,10 @@ cudaError_t launch_pool_tc(const uint8_t *img, int32_t N, int32_t B, int32_t L, 
 // Per group of NR ranges: rows (rl, k) = Rperm_k replicated over the 4 polyphase planes, K-major
 // core-matrix layout, B_BYTES contiguous bytes (one bulk copy per CTA); zero rows past n_r.
 template <int B>
-__global__ void __launch_bounds__(256) tc_range_operand_kernel(const uint8_t *__restrict__ img, int32_t N,
-                                                               const int2 *__restrict__ ranges,
-                                                               const unsigned long long *__restrict__ d_nr,
-                                                               int64_t total16, uint8_t *__restrict__ Bop) {
+__device__ __forceinline__ void tc_range_operand_body(const uint8_t *__restrict__ img, int32_t N,
+                                                      const int2 *__restrict__ ranges,
+                                                      const unsigned long long *__restrict__ d_nr,
+                                                      int64_t total16, uint8_t *__restrict__ Bop, int bx) {
     using Cf = TCfg<B>;
     // source pixel of byte p of row k: Rperm_k(p) = R(f_k^{-1}(p)); under this numbering
     // f_k^{-1} = f_{k'} with k' = [0,3,2,1,4,5,6,7][k] (rotations by 90/270 swap, the rest are
@@ -335,7 +335,7 @@ __global__ void __launch_bounds__(256) tc_range_operand_kernel(const uint8_t *__
         src[kk][p] = (uint8_t)(si * B + sj);
     }
     __syncthreads();
-    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // one 16-byte group
+    const int64_t e = (int64_t)bx * blockDim.x + threadIdx.x;  // one 16-byte group
     if (e >= total16) return;
     const int64_t n_r = (int64_t)*d_nr;
     if (e / ((int64_t)Cf::N * (Cf::KB / 16)) > (n_r + Cf::NR - 1) / Cf::NR) return;  // past the last group
@@ -373,13 +373,14 @@ struct TCRangeG {
 
 // Thread per range: SR, A = n SRR - SR^2 and the filter margin
 template <int B>
-__global__ void tc_range_meta_kernel(const uint8_t *__restrict__ img, int32_t N, const int2 *__restrict__ ranges,
-                                     const unsigned long long *__restrict__ d_nr, int32_t n_pad, double smax,
-                                     const unsigned long long *__restrict__ d_misc,
-                                     TCRangeG *__restrict__ meta, int32_t univ) {
+__device__ __forceinline__ void tc_range_meta_body(const uint8_t *__restrict__ img, int32_t N,
+                                                   const int2 *__restrict__ ranges,
+                                                   const unsigned long long *__restrict__ d_nr, int32_t n_pad,
+                                                   double smax, const unsigned long long *__restrict__ d_misc,
+                                                   TCRangeG *__restrict__ meta, int32_t univ, int bx) {
     // B >= 8: a warp per range (lanes over the pixels), else a thread per range
     constexpr int TPR = B >= 8 ? 32 : 1;
-    const int gt = blockIdx.x * blockDim.x + threadIdx.x;
+    const int gt = bx * blockDim.x + threadIdx.x;
     const int r = gt / TPR, sub = gt % TPR;
     if (r >= n_pad) return;
     const int n_r = (int)*d_nr;
@@ -421,6 +422,20 @@ __global__ void tc_range_meta_kernel(const uint8_t *__restrict__ img, int32_t N,
     // s-independent filter (NSP = 0): Bq rounded once, squared, times RN(1/C): <= 4.04u Bq^2/C <= 4.04u A
     if (univ) R.margin = 4.1 * u * R.A + 1e-12 * R.A + 1e-30;
     meta[r] = R;
+}
+
+// both range-preparation passes in one launch: blocks [0, nb_op) build the range operand,
+// the rest the per-range moments and margins
+template <int B>
+__global__ void __launch_bounds__(256) tc_range_prep_kernel(const uint8_t *__restrict__ img, int32_t N,
+                                                            const int2 *__restrict__ ranges,
+                                                            const unsigned long long *__restrict__ d_nr,
+                                                            int64_t total16, uint8_t *__restrict__ Bop, int nb_op,
+                                                            int32_t n_pad, double smax,
+                                                            const unsigned long long *__restrict__ d_misc,
+                                                            TCRangeG *__restrict__ meta, int32_t univ) {
+    if ((int)blockIdx.x < nb_op) tc_range_operand_body<B>(img, N, ranges, d_nr, total16, Bop, blockIdx.x);
+    else tc_range_meta_body<B>(img, N, ranges, d_nr, n_pad, smax, d_misc, meta, univ, blockIdx.x - nb_op);
 }
 
 // ------------------------------------------------------------------------------ search kernel
@@ -989,15 +1004,12 @@ static cudaError_t tc_range_prep(const SearchParams &sp, uint8_t *scratch, TCPar
     uint8_t *Bop = scratch;
     TCRangeG *meta = reinterpret_cast<TCRangeG *>(scratch + (size_t)groups * Cf::B_BYTES);
     const int64_t total16 = groups * Cf::N * (Cf::KB / 16);
-    tc_range_operand_kernel<B><<<(unsigned)((total16 + 255) / 256), 256, 0, st>>>(sp.img, sp.N, sp.ranges,
-                                                                                  sp.d_nr, total16, Bop);
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
     const int n_pad = (int)(groups * Cf::NR);
     const int64_t meta_threads = (int64_t)n_pad * (B >= 8 ? 32 : 1);
-    tc_range_meta_kernel<B><<<(unsigned)((meta_threads + 127) / 128), 128, 0, st>>>(sp.img, sp.N, sp.ranges, sp.d_nr,
-                                                                              n_pad, sp.smax, sp.d_misc, meta,
-                                                                              sp.nsp > 2 ? 1 : 0);
+    const int nb_op = (int)((total16 + 255) / 256), nb_meta = (int)((meta_threads + 255) / 256);
+    tc_range_prep_kernel<B><<<(unsigned)(nb_op + nb_meta), 256, 0, st>>>(sp.img, sp.N, sp.ranges, sp.d_nr, total16,
+                                                                        Bop, nb_op, n_pad, sp.smax, sp.d_misc, meta,
+                                                                        sp.nsp > 2 ? 1 : 0);
     p.Bop = Bop;
     p.rmeta = meta;
     return cudaGetLastError();
