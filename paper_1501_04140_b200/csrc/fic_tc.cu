@@ -703,6 +703,9 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
             float g0;
             if constexpr (NSP == 0) {
                 g0 = -(bq * bq) * t2[0];  // >= -(Bq^2 / C)(1 + 4.04u): continuous minimum
+            } else if constexpr (NSP == 2) {  // both s in one packed FFMA2 (the same two roundings)
+                const float2 g2 = __ffma2_rn(make_float2(nhs[0], nhs[1]), make_float2(bq, bq), make_float2(t2[0], t2[1]));
+                g0 = fminf(g2.x, g2.y);
             } else {
                 g0 = fmaf(nhs[0], bq, t2[0]);
 #pragma unroll
