@@ -25,6 +25,8 @@
 #include <climits>
 #include <cstring>
 
+#include <cstdlib>
+
 #include "fic_internal.cuh"
 
 namespace fic {
@@ -977,7 +979,9 @@ static cudaError_t launch_tc_t(const TCParams &p, cudaStream_t st) {
         cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
         if (num_sms <= 0) num_sms = 148;
     }
-    tcsearch_kernel<B, NSP><<<(unsigned)num_sms, Cf::THREADS, smem, st>>>(p);
+    int ctas = num_sms;
+    if (const char *e = getenv("FIC_TC_CTAS")) ctas = std::max(1, atoi(e));  // test hook: small grids
+    tcsearch_kernel<B, NSP><<<(unsigned)ctas, Cf::THREADS, smem, st>>>(p);
     return cudaGetLastError();
 }
 
@@ -1043,6 +1047,7 @@ cudaError_t launch_tc_search(int32_t B, const SearchParams &sp, const uint8_t *D
     p.smax = sp.smax;
     p.part = sp.part; p.exact_count = sp.exact_count;
     p.lockstep = tc_pool_bytes(B, (n_slots + kTileD - 1) / kTileD) > ((size_t)48 << 20) ? 1 : 0;
+    if (const char *e = getenv("FIC_TC_LOCKSTEP")) p.lockstep = atoi(e) != 0;  // test hook
     switch (B) {
     case 2: return launch_tc_b<2>(p, st);
     case 4: return launch_tc_b<4>(p, st);

@@ -439,3 +439,23 @@ def test_native_nccl_single_rank(fic):
     with pytest.raises(p.FicError) as ei:  # no communicator on a plain context
         ctx.encode_nccl(img, cfg["B_max"], cfg["B_min"], cfg["L"], cfg["tau"], cfg["s"], cfg["rms_tol"])
     assert ei.value.status == 1
+
+
+# ------------------------------------------------------------- persistent search plan (fic_tc.cu)
+_C2_ORACLE = {}
+
+
+@pytest.mark.parametrize("ctas,lockstep", [(16, 1), (7, 0), (3, 1), (148, 1)])
+def test_persistent_plan_parity(fic, monkeypatch, ctas, lockstep):
+    """The tcgen05 search runs as persistent CTAs whose work is full lockstep rounds of range
+    groups plus a flattened (group, tile) tail cut into equal runs (partials per run, unused slots
+    filled).  Small grids (FIC_TC_CTAS) and forced lockstep (FIC_TC_LOCKSTEP) put C2's levels
+    through several full rounds, tails split across CTAs and groups split into many slots; the
+    code must equal the oracle's bit for bit in every case."""
+    monkeypatch.setenv("FIC_TC_CTAS", str(ctas))
+    monkeypatch.setenv("FIC_TC_LOCKSTEP", str(lockstep))
+    cfg = config("C2")
+    img, got = encode_both(fic, cfg)
+    if "C2" not in _C2_ORACLE:
+        _C2_ORACLE["C2"] = oracle.encode_cfg(cfg, img)
+    assert_same(got, _C2_ORACLE["C2"], f"C2 ctas={ctas} lockstep={lockstep}")
