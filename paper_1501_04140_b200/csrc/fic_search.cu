@@ -432,6 +432,30 @@ __device__ __noinline__ int kstar_dev(const FinalizeParams &P, int2 rr, int32_t 
     const int B = P.B, b = B - 1;
     const int32_t c = P.kept[d];
     const int64_t x0 = (int64_t)(c % P.A) * P.L, y0 = (int64_t)(c / P.A) * P.L;
+    if (B == 2) {  // (the B = 2 closed form defers k*): 4 range and 16 domain pixels loaded once
+        const uint8_t *rp = P.img + (size_t)rr.y * P.N + rr.x;
+        const long long r00 = rp[0], r01 = rp[1], r10 = rp[P.N], r11 = rp[P.N + 1];
+        long long D[2][2];
+        for (int i = 0; i < 2; ++i)
+            for (int j = 0; j < 2; ++j) {
+                const uint8_t *q = P.img + (y0 + 2 * i) * P.N + x0 + 2 * j;
+                D[i][j] = (int)q[0] + (int)q[1] + (int)q[P.N] + (int)q[P.N + 1];
+            }
+        // SRD_k = sum_ij R(i,j) D(f_k(i,j)) with the isometry convention below (b = 1)
+        long long srd[8];
+        srd[0] = r00 * D[0][0] + r01 * D[0][1] + r10 * D[1][0] + r11 * D[1][1];
+        srd[1] = r00 * D[1][0] + r01 * D[0][0] + r10 * D[1][1] + r11 * D[0][1];
+        srd[2] = r00 * D[1][1] + r01 * D[1][0] + r10 * D[0][1] + r11 * D[0][0];
+        srd[3] = r00 * D[0][1] + r01 * D[1][1] + r10 * D[0][0] + r11 * D[1][0];
+        srd[4] = r00 * D[0][1] + r01 * D[0][0] + r10 * D[1][1] + r11 * D[1][0];
+        srd[5] = r00 * D[0][0] + r01 * D[1][0] + r10 * D[0][1] + r11 * D[1][1];
+        srd[6] = r00 * D[1][0] + r01 * D[1][1] + r10 * D[0][0] + r11 * D[0][1];
+        srd[7] = r00 * D[1][1] + r01 * D[0][1] + r10 * D[1][0] + r11 * D[0][0];
+        int ks = 0;
+        for (int k = 1; k < 8; ++k)
+            if (srd[k] > srd[ks]) ks = k;
+        return ks;
+    }
     auto Dp = [&](int i, int j) {  // decimated domain value D'(i, j)
         const uint8_t *q = P.img + (y0 + 2 * i) * P.N + x0 + 2 * j;
         return (int)q[0] + (int)q[1] + (int)q[P.N] + (int)q[P.N + 1];
