@@ -76,6 +76,19 @@ __device__ __forceinline__ void tmbar_expect_tx(uint64_t *bar, uint32_t bytes) {
 __device__ __forceinline__ void tmbar_arrive(uint64_t *bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(bar)) : "memory");
 }
+__device__ __forceinline__ void tmbar_wait_sa(uint32_t bar_sa, uint32_t parity) {  // shared address
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+            : "=r"(done)
+            : "r"(bar_sa), "r"(parity)
+            : "memory");
+    }
+}
+__device__ __forceinline__ void tmbar_arrive_sa(uint32_t bar_sa) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar_sa) : "memory");
+}
 __device__ __forceinline__ void tmbar_wait(uint64_t *bar, uint32_t parity) {
     uint32_t done = 0;
     while (!done) {
@@ -715,7 +728,8 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
             }
             return g0;
         };
-        int tl = 0;  // tiles consumed by this CTA (TMEM buffer ring position)
+        unsigned tl = 0;  // tiles consumed by this CTA (TMEM buffer ring position)
+        const uint32_t tfull_sa = su32(tfull), tempty_sa = su32(tempty);
         for (int k = 0; k < nseg; ++k) {
             int grp, ta, ntl, slot;
             bool lastseg;
@@ -753,8 +767,8 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
                 // min_{s > 0} e_s - A within the margin, so every range's best is <= A + min_m g +
                 // margin and RU(min_m g + 2 margin) is a valid threshold -- the first tile no longer
                 // sends every pair better than s = 0 to the exact path
-                const int buf0 = tl % NBUF;
-                tmbar_wait(&tfull[buf0], (uint32_t)((tl / NBUF) & 1));
+                const unsigned buf0 = tl % NBUF;
+                tmbar_wait_sa(tfull_sa + 8 * buf0, (tl / NBUF) & 1);
                 tc_fence_after();
                 const uint32_t tb0 = tmem + ((uint32_t)(lq * 32) << 16) + buf0 * Cf::ACC + eg * HALF * 8;
 #pragma unroll 1
@@ -793,7 +807,7 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
                 asm volatile("bar.sync %0, 128;" ::"r"(1 + eg) : "memory");  // the warpgroup's seeds
             }
             for (int tt = 0; tt < ntl; ++tt, ++tl) {
-                const int buf = tl % NBUF;
+                const unsigned buf = tl % NBUF;
                 const int d = (ta + tt) * kTileD + m;
                 const int32_t sd = sd_n;
                 float t2[NT];
@@ -806,7 +820,7 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
 #pragma unroll
                     for (int jj = 0; jj < NT; ++jj) t2_n[jj] = __ldg(t2p + jj * t2row);
                 }
-                tmbar_wait(&tfull[buf], (uint32_t)((tl / NBUF) & 1));
+                tmbar_wait_sa(tfull_sa + 8 * buf, (tl / NBUF) & 1);
                 tc_fence_after();
                 const uint32_t tbase = tmem + ((uint32_t)(lq * 32) << 16) + buf * Cf::ACC + eg * HALF * 8;
                 // four ranges (32 columns) per tcgen05.ld, the next group in flight while one is scored
@@ -822,7 +836,7 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
                 tc_wait_ld();
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) tmbar_arrive(&tempty[buf]);
+                if (lane == 0) tmbar_arrive_sa(tempty_sa + 8 * buf);
                 if constexpr (Cf::QR) {  // SRD_k = 4 S_q + S_r (exact: < 2^31)
 #pragma unroll
                     for (int i = 0; i < 32; ++i) vv[i] = 4u * vv[i] + vv[32 + i];
