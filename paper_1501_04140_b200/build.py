@@ -35,12 +35,23 @@ def needs_build() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
+def nccl_link() -> list:
+    import sysconfig
+    for base in {sysconfig.get_paths()["purelib"], sysconfig.get_paths()["platlib"]}:
+        d = os.path.join(base, "nvidia", "nccl", "lib")
+        if os.path.exists(os.path.join(d, "libnccl.so.2")):
+            return ["-L" + d, "-l:libnccl.so.2", "-Xlinker", "-rpath", "-Xlinker", d]
+    return ["-lnccl"]
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not needs_build():
         return SO
-    # NCCL (fic_ctx_create_nccl / fic_encode_nccl): the system headers and libnccl.so.2; at run
-    # time the soname resolves to the NCCL torch has already loaded, if any
-    cmd = [NVCC, *NVCC_FLAGS, "-I", INCLUDE, "-I", CSRC, "-o", SO + ".tmp", *sources(), "-lquadmath", "-lnccl"]
+    # NCCL (fic_ctx_create_nccl / fic_encode_nccl): the system headers; the library is the one
+    # torch bundles (nvidia/nccl/lib, rpath), so whichever of torch and libfic.so loads first,
+    # the process holds one libnccl.so.2 new enough for both (the system 2.27 one lacks symbols
+    # torch 2.11 needs); without the bundled copy, the system libnccl.so.2
+    cmd = [NVCC, *NVCC_FLAGS, "-I", INCLUDE, "-I", CSRC, "-o", SO + ".tmp", *sources(), "-lquadmath", *nccl_link()]
     res = subprocess.run(cmd, capture_output=True, text=True)
     log = os.path.join(HERE, "build.log")
     with open(log, "w") as f:

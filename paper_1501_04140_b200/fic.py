@@ -58,6 +58,9 @@ def load(path: str = SO_PATH):
         return _lib
     if not os.path.exists(path):
         raise ImportError(f"{path} not built: run python -m paper_1501_04140_b200.build")
+    # torch first: its CUDA libraries and NCCL are then the ones libfic.so binds to (one copy
+    # of each in the process, whatever the caller imports later)
+    import torch  # noqa: F401
     L = C.CDLL(path)
     P, i32, i64, dbl = C.c_void_p, C.c_int32, C.c_int64, C.c_double
     sig = {
