@@ -539,9 +539,12 @@ __global__ void __launch_bounds__(256, 6) b2win_kernel(const __grid_constant__ B
     const float nh0 = P.nhs[0], nh1 = P.nsp > 1 ? P.nhs[1] : P.nhs[0];
     const float k0 = __double2float_rn(P.spos[0] * P.spos[0] * 0.0625);
     const float k1 = P.nsp > 1 ? __double2float_rn(P.spos[1] * P.spos[1] * 0.0625) : k0;
-    auto gof = [&](const float4 fv, float &bq) {
+    const float2 nh01 = make_float2(nh0, nh1), k01 = make_float2(k0, k1);
+    auto gof = [&](const float4 fv, float &bq) {  // both s in packed FMUL2 / FFMA2 (same roundings)
         bq = fmaf(R.sx, fv.y, fabsf(fmaf(R.x2, fv.x, R.dx * fv.z)));
-        return fminf(fmaf(nh0, bq, k0 * fv.w), fmaf(nh1, bq, k1 * fv.w));
+        const float2 t2 = __fmul2_rn(k01, make_float2(fv.w, fv.w));
+        const float2 g2 = __ffma2_rn(nh01, make_float2(bq, bq), t2);
+        return fminf(g2.x, g2.y);
     };
     auto gval = [&](int pos, float &bq, float &cf) {
         const float4 fv = __ldg(P.F + pos);
