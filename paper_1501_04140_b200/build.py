@@ -47,6 +47,17 @@ def nccl_link() -> list:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not needs_build():
         return SO
+    # one compiler run at a time per tree (torchrun ranks all call build()): the first takes the
+    # lock and builds, the others find the library up to date once they get it
+    import fcntl
+    with open(SO + ".lock", "w") as lk:
+        fcntl.flock(lk, fcntl.LOCK_EX)
+        if not force and not needs_build():
+            return SO
+        return _build_locked(verbose)
+
+
+def _build_locked(verbose: bool) -> str:
     # NCCL (fic_ctx_create_nccl / fic_encode_nccl): the system headers; the library is the one
     # torch bundles (nvidia/nccl/lib, rpath), so whichever of torch and libfic.so loads first,
     # the process holds one libnccl.so.2 new enough for both (the system 2.27 one lacks symbols
