@@ -138,7 +138,7 @@ def code_size(cfg, stats):
     bits = 0
     for lv, sB in zip(stats, cfg["s"]):
         A = int(round(math.sqrt(lv["n_candidates"])))
-        leaf = 2 * max(1, math.ceil(math.log2(max(A, 2)))) + 3 + (math.ceil(math.log2(len(sB))) if len(sB) > 1 else 0) + 8
+        leaf = 2 * (math.ceil(math.log2(A)) if A > 1 else 0) + 3 + (math.ceil(math.log2(len(sB))) if len(sB) > 1 else 0) + 8
         bits += lv["n_accepted"] * leaf
         if lv["B"] > cfg["B_min"]:
             bits += lv["n_ranges"]

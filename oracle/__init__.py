@@ -7,6 +7,7 @@ neither imports the other; both read their inputs from fic_inputs/.
   fic_oracle.c  -- O1: plain C (int64 + binary64, -ffp-contract=off, OpenMP over ranges)
   exact.py      -- O2: literal Eq. (1)/(3)/(5) in exact rationals for tiny images
   oracle.py     -- ctypes wrapper + build() for O1
+  codeformat.py -- the FIC1 container: serialize / deserialize, plain bit lists
 
 Parity status per function: see DESIGN.md §"Oracle pins".  The decoder and PSNR (readings
 R23-R26) are pinned by closed forms (s = 0 codes, the scalar fixed-point recursion of a uniform
@@ -19,3 +20,4 @@ from .oracle import (  # noqa: F401
     decimate, o_code, encode_level, encode, encode_cfg, RECORD_DTYPE, num_threads,
     o_value, decode, psnr, kept_list_topk,
 )
+from . import codeformat  # noqa: F401
