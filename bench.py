@@ -294,7 +294,14 @@ def main():
     d1.synchronize()
     quality = {"psnr_db": ctx.psnr(decoded, img), "decode_iterations": 12,
                "decode_ms": d0.elapsed_time(d1), "note": "sanity report on the synthetic image"}
-    quality.update(code_size(cfg, ctx.stats()))
+    # the FIC1 stream of the last code (fic_serialize, NEXT-3) and its compression ratio; the
+    # size computed from the per-level counts must agree
+    h0 = time.perf_counter()
+    fic1 = ctx.serialize_cfg(cfg, rec)
+    ser_ms = (time.perf_counter() - h0) * 1e3
+    expect = code_size(cfg, ctx.stats())
+    quality.update({"code_bytes_fic1": len(fic1), "compression_ratio": cfg["N"] * cfg["N"] / len(fic1),
+                    "serialize_ms_host": ser_ms, "size_matches_counts": expect["code_bytes_fic1"] == len(fic1)})
     total_ms = sum(times)
     pairs_step = sum(s["pairs"] for s in level_acc)
     t = torch.tensor([total_ms], dtype=torch.float64, device=dev)

@@ -200,6 +200,21 @@ fic_status fic_decode(fic_ctx *ctx, const fic_record *rec, int64_t n_rec, int32_
  * identical.  *h_psnr receives the value.  Synchronous.  Errors: ARG, CUDA. */
 fic_status fic_psnr(fic_ctx *ctx, const uint8_t *a, const uint8_t *b, int64_t n, double *h_psnr);
 
+/* FIC1 container of a code (NEXT-3; SPEC S:352-413 -- the paper fixes no format, P:154 reports
+ * compression ratios): magic "FIC1", header (width u16, height u16, B_max u8, B_min u8,
+ * s_mode u8, s_max u16 x 10000, L u16, big-endian; one u8 per level = that level's s count), then
+ * the depth-first quadtree walk of the top-level blocks in row-major order, children row-major,
+ * one split bit per visited range above B_min, per leaf [dx / L, dy / L (ceil log2 A bits each,
+ * A = (N - 2B) / L + 1), isometry (3), s index (ceil log2 |S_B| bits), o code (8)], MSB first,
+ * zero-padded to a byte.
+ * rec: device fic_record [n_rec], one per leaf (fic_encode's output; any order; the leaves must
+ * tile the image); h_n_s: per-level s counts; s_mode: 0 predefined, 1 sampled10, 2 closed form
+ * (5 bits), 3 grid; out: device [capacity] bytes.  *h_nbytes = stream length (also when it does
+ * not fit).  Synchronous.  Errors: ARG, CAPACITY (stream longer than capacity), CUDA. */
+fic_status fic_serialize(fic_ctx *ctx, const fic_record *rec, int64_t n_rec, int32_t N, int32_t B_max,
+                         int32_t B_min, int32_t L, const int32_t *h_n_s, int32_t s_mode, double s_max,
+                         uint8_t *out, int64_t capacity, int64_t *h_nbytes);
+
 /* Host-only: the entropy fixed-point table lut[c] = round-half-even(c log2(c) 2^32),
  * c = 0..mmax (h_lut host int64 [mmax+1]).  No device work. */
 fic_status fic_entropy_lut(int64_t *h_lut, int32_t mmax);

@@ -46,6 +46,7 @@ struct fic_ctx {
     cudaEvent_t pool_ready[fic::kMaxLevels] = {};
     cudaEvent_t level_done[fic::kMaxLevels] = {};  // finalize of level l done (records ready)
     Buf b_blocksum2;  // compaction scratch of the side-stream record gathering
+    Buf b_code;       // FIC1 writer scratch (fic_serialize)
     cudaEvent_t main_ready = nullptr;
     int b2_window = 1;    // env FIC_B2_WINDOW=0: B = 2 full scan instead of the C windows
     int search_mode = 0;  // env FIC_SEARCH: auto (default: B=2 closed form, else tcgen05) | fourier | direct | tc
@@ -439,6 +440,56 @@ fic_status fic_psnr(fic_ctx *ctx, const uint8_t *a, const uint8_t *b, int64_t n,
 }
 
 // ------------------------------------------------------------------------- NCCL (multi-GPU)
+fic_status fic_serialize(fic_ctx *ctx, const fic_record *rec, int64_t n_rec, int32_t N, int32_t B_max,
+                         int32_t B_min, int32_t L, const int32_t *h_n_s, int32_t s_mode, double s_max,
+                         uint8_t *out, int64_t capacity, int64_t *h_nbytes) {
+    CKS(ctx_check(ctx));
+    if (h_nbytes) *h_nbytes = 0;
+    if (!h_n_s || !h_nbytes || (!rec && n_rec > 0) || n_rec < 0 || (!out && capacity > 0) || capacity < 0)
+        return fail(ctx, FIC_ERR_ARG, "null argument");
+    if (!pow2(B_max) || !pow2(B_min) || B_min < 2 || B_min > B_max || N < 1 || N % B_max || N > 65535 ||
+        B_max > 255 || L < 1 || L > 65535 || s_mode < 0 || s_mode > 255 || !(s_max >= 0.0 && s_max <= 6.5535))
+        return fail(ctx, FIC_ERR_ARG, "bad code parameters");
+    int nl = 0;
+    for (int32_t B = B_max; B >= B_min; B /= 2) ++nl;
+    if (nl > fic::kMaxLevels) return fail(ctx, FIC_ERR_ARG, "too many levels");
+    fic::CodeParams P;
+    memset(&P, 0, sizeof P);
+    P.N = N; P.B_max = B_max; P.B_min = B_min; P.L = L;
+    auto nbits = [](int64_t c) { int b = 0; while ((int64_t{1} << b) < c) ++b; return b; };
+    std::vector<uint8_t> head = {'F', 'I', 'C', '1', (uint8_t)(N >> 8), (uint8_t)N, (uint8_t)(N >> 8), (uint8_t)N,
+                                 (uint8_t)B_max, (uint8_t)B_min, (uint8_t)s_mode};
+    const int sm = (int)std::lround(s_max * 10000.0);
+    head.push_back((uint8_t)(sm >> 8)); head.push_back((uint8_t)sm);
+    head.push_back((uint8_t)(L >> 8)); head.push_back((uint8_t)L);
+    for (int l = 0; l < nl; ++l) {
+        const int32_t B = B_max >> l;
+        if (h_n_s[l] < 1 || h_n_s[l] > 255) return fail(ctx, FIC_ERR_ARG, "s count out of range");
+        head.push_back((uint8_t)h_n_s[l]);
+        P.sbits[l] = nbits(h_n_s[l]);
+        P.posbits[l] = N >= 2 * B ? nbits((N - 2 * B) / L + 1) : 0;
+    }
+    const int64_t hb = (int64_t)head.size();
+    cudaStream_t st = ctx->stream;
+    // body bound: per leaf <= log2(B_max / B_min) + 1 + 2 * 16 + 3 + 8 + 8 bits
+    const int64_t max_words = (n_rec * 64 + 31) / 32 + 2;
+    CK(grow(ctx, ctx->b_code, fic::code_scratch_bytes(n_rec) + sizeof(unsigned) * (size_t)max_words + 256));
+    unsigned *words = reinterpret_cast<unsigned *>(static_cast<char *>(ctx->b_code.p) + fic::code_scratch_bytes(n_rec));
+    unsigned long long *d_total = ptr<unsigned long long>(ctx->b_counts) + 63;
+    CK(cudaMemsetAsync(words, 0, sizeof(unsigned) * (size_t)max_words, st));
+    CK(fic::launch_code_body(rec, n_rec, P, ctx->b_code.p, words, d_total, st));
+    unsigned long long bits = 0;
+    CK(cudaMemcpyAsync(&bits, d_total, sizeof bits, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    const int64_t nbytes = hb + (int64_t)((bits + 7) / 8);
+    *h_nbytes = nbytes;
+    if (nbytes > capacity) return fail(ctx, FIC_ERR_CAPACITY, "output capacity too small for the stream");
+    CK(cudaMemcpyAsync(out, head.data(), (size_t)hb, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(out + hb, words, (size_t)(nbytes - hb), cudaMemcpyDeviceToDevice, st));
+    CK(cudaStreamSynchronize(st));
+    return FIC_OK;
+}
+
 fic_status fic_nccl_unique_id(uint8_t *h_id128) {
     if (!h_id128) return FIC_ERR_ARG;
     static_assert(sizeof(ncclUniqueId) == 128, "NCCL unique id is 128 bytes");
@@ -619,6 +670,7 @@ fic_status fic_ctx_destroy(fic_ctx *ctx) {
     for (auto &e : ctx->level_done)
         if (e) cudaEventDestroy(e);
     free_buf(ctx->b_blocksum2);
+    free_buf(ctx->b_code);
     if (ctx->main_ready) cudaEventDestroy(ctx->main_ready);
     if (ctx->side) {
         cudaStreamSynchronize(ctx->side);

@@ -167,6 +167,16 @@ __host__ __device__ constexpr float tc_t2_fold(int B, int nsp) {
     return (nsp >= 1 && nsp <= 2) ? (B == 2 ? 1.f : (B == 4 ? 2.f : (B == 8 ? 64.f : 0.f))) : 0.f;
 }
 
+// FIC1 body writer (fic_code.cu): per level (index 0 = B_max) the position and s-index widths
+struct CodeParams {
+    int32_t N, B_max, B_min, L;
+    int32_t posbits[kMaxLevels], sbits[kMaxLevels];
+};
+size_t code_scratch_bytes(int64_t n);
+// words: zeroed body buffer (>= ceil(bits / 32) words); *d_total = body length in bits
+cudaError_t launch_code_body(const fic_record *rec, int64_t n, const CodeParams &P, void *scratch,
+                             unsigned *words, unsigned long long *d_total, cudaStream_t st);
+
 // ---- launchers (return cudaError_t of the launch) ---------------------------------------------
 cudaError_t launch_entropy_keys(const uint8_t *img, int32_t N, int32_t B, int32_t L, int32_t A,
                                 const int64_t *d_delta, int64_t lut_m, int64_t T, int use_tau,

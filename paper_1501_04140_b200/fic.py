@@ -31,8 +31,10 @@ EXPORTS = (
     "fic_ctx_set_timing", "fic_get_stats", "fic_build_domain_pool", "fic_pool_info",
     "fic_pool_destroy", "fic_encode_level", "fic_encode", "fic_encode_host", "fic_merge_shards",
     "fic_entropy_lut", "fic_version", "fic_decode", "fic_psnr", "fic_build_domain_pool_topk",
-    "fic_encode_topk", "fic_nccl_unique_id", "fic_ctx_create_nccl", "fic_encode_nccl",
+    "fic_encode_topk", "fic_nccl_unique_id", "fic_ctx_create_nccl", "fic_encode_nccl", "fic_serialize",
 )
+
+S_MODE_CODES = {"predefined": 0, "sampled10": 1, "closed5": 2, "grid": 3}  # FIC1 header s_mode
 
 
 class FicError(RuntimeError):
@@ -85,6 +87,7 @@ def load(path: str = SO_PATH):
         "fic_ctx_create_nccl": ([i32, P, P, i32, i32, P], C.c_int),
         "fic_encode_nccl": ([P, P, i32, i32, i32, i32, P, P, P, P, P, i64, P], C.c_int),
         "fic_psnr": ([P, P, P, i64, P], C.c_int),
+        "fic_serialize": ([P, P, i64, i32, i32, i32, i32, P, i32, dbl, P, i64, P], C.c_int),
         "fic_version": ([], C.c_char_p),
     }
     for name, (args, res) in sig.items():
@@ -337,6 +340,24 @@ class Context:
                                         _dptr(init) if init is not None else None, _dptr(out)),
                     "fic_decode")
         return out
+
+    def serialize(self, recs, N: int, B_max: int, B_min: int, L: int, s_sets, s_mode: str = "predefined",
+                  s_max: float = 1.0) -> bytes:
+        """FIC1 stream of a code (fic_serialize): recs = CUDA uint8 [n, 40] records (one per leaf)."""
+        import torch
+        n_s = np.ascontiguousarray([len(s) for s in s_sets], dtype=np.int32)
+        n = recs.shape[0]
+        cap = 64 + len(s_sets) + n * 8
+        out = torch.empty(cap, dtype=torch.uint8, device=recs.device)
+        nb = C.c_int64()
+        self._check(self.lib.fic_serialize(self.handle, _dptr(recs), n, N, B_max, B_min, L, _ptr(n_s),
+                                           S_MODE_CODES[s_mode], float(s_max), _dptr(out), cap, C.byref(nb)),
+                    "fic_serialize")
+        return bytes(out[: nb.value].cpu().numpy().tobytes())
+
+    def serialize_cfg(self, cfg, recs) -> bytes:
+        return self.serialize(recs, cfg["N"], cfg["B_max"], cfg["B_min"], cfg["L"], cfg["s"],
+                              cfg.get("s_mode", "predefined"))
 
     def psnr(self, a, b) -> float:
         """PSNR of two CUDA uint8 images (fic_psnr)."""
