@@ -98,3 +98,22 @@ def test_decode_errors(fic):
     # the context stays usable
     got = ctx.decode(rec_dev(torch, code), 32, 8, s_sets, 2).cpu().numpy()
     assert np.array_equal(got, oracle.decode(code, 32, s_sets, 8, 2))
+
+
+@pytest.mark.parametrize("name", ["C2", "C3"])
+def test_decoder_convergence(fic, name):
+    """SPEC acceptance 5 on the GPU decoder (readings R23-R25): from the constant 128 image the
+    pass-to-pass change max |x_{i+1} - x_i| never grows after pass 2 and is at most one gray level
+    by pass 16 (the passes round to 8 bits, so the real-valued "< 1" becomes "<= 1": a rounding
+    limit cycle of one level can remain; the codes use s <= 0.9, a contraction up to rounding)."""
+    p, ctx, torch = fic
+    cfg = config(name)
+    recs = ctx.encode_cfg(cfg, torch.from_numpy(image_for(cfg)).cuda())
+    prev = ctx.decode(recs, cfg["N"], cfg["B_max"], cfg["s"], 0)
+    deltas = []
+    for it in range(1, 17):
+        cur = ctx.decode(recs, cfg["N"], cfg["B_max"], cfg["s"], 1, init=prev)
+        deltas.append(int((cur.int() - prev.int()).abs().max()))
+        prev = cur
+    assert deltas[-1] <= 1, deltas
+    assert all(b <= a for a, b in zip(deltas[1:], deltas[2:])), deltas
