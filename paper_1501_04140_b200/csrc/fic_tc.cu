@@ -691,6 +691,7 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
         // (exact), so g = fma(nhs, bq, t2) keeps its rounding without the multiply
         constexpr float kBqScale = B == 4 ? 2.0f : (B == 8 ? 64.0f : 1.0f);
         for (int jj = 0; jj < NT; ++jj) nhs[jj] = sHsn[jj] * kBqScale;
+        static_assert(Cf::EWG <= 5, "named barriers 1..EWG (seeding) and 6 (segments) must not collide");
         auto epi_sync = [&]() { asm volatile("bar.sync 6, %0;" ::"r"(128 * Cf::EWG) : "memory"); };
         unsigned n_exact = 0;
         int qn = 0;
