@@ -616,13 +616,10 @@ __global__ void __launch_bounds__(256, 6) b2win_kernel(const __grid_constant__ B
             // final threshold RU(gmin_final + 2 margin) is never larger, so the stash holds every
             // pair phase 2 has to score
             const float ts = fminf(__fadd_ru(gmin, marg2_ru), FLT_MAX);
-            unsigned pass = 0;
-#pragma unroll
-            for (int i = 0; i < 8; ++i) pass |= gv[i] <= ts ? 1u << i : 0u;
-            if (__any_sync(0xffffffffu, pass)) {
+            if (__any_sync(0xffffffffu, g <= ts)) {  // (g: this lane's minimum of the round)
 #pragma unroll
                 for (int i = 0; i < 8; ++i) {
-                    if (pass >> i & 1u) {
+                    if (gv[i] <= ts) {
                         const int slot = atomicAdd(&sNst[wib], 1);
                         if (slot < kStash) sStash[wib][slot] = bf[i & 3] + lane + 32 * (i >> 2);
                     }
