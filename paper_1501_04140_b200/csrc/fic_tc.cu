@@ -757,12 +757,18 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
             for (int q = 0; q < HALF; ++q) rSR[q] = sR[eg * HALF + q].SR;
             // per-domain data of this lane, walked tile by tile (pointers advanced, not recomputed);
             // NSP > 0 is chosen only when the level has exactly NSP values s > 0, so every row exists
+            // B >= 8: a 32-bit slot index (one IMAD.WIDE per load instead of 64-bit pointer
+            // arithmetic: B = 16 0.149 -> 0.146 ms, B = 8 0.284 -> 0.278); B = 4, at its 128-register
+            // ceiling, keeps the advanced pointers (the index form cost it 0.706 -> 0.726)
+            constexpr bool kIdx = B >= 8;
+            unsigned di = (unsigned)ta * kTileD + m;
+            const unsigned t2r = (unsigned)t2row;
             const int32_t *sdp = P.SD + (int64_t)ta * kTileD + m;
             const float *t2p = P.t2f + (int64_t)ta * kTileD + m;
-            int32_t sd_n = __ldg(sdp);
+            int32_t sd_n = kIdx ? __ldg(P.SD + di) : __ldg(sdp);
             float t2_n[NT];
 #pragma unroll
-            for (int jj = 0; jj < NT; ++jj) t2_n[jj] = __ldg(t2p + jj * t2row);
+            for (int jj = 0; jj < NT; ++jj) t2_n[jj] = kIdx ? __ldg(P.t2f + (di + jj * t2r)) : __ldg(t2p + jj * t2row);
             if constexpr (NSP > 0) {
                 // ---- seed the thresholds from the segment's first tile: with NSP > 0, g approximates
                 // min_{s > 0} e_s - A within the margin, so every range's best is <= A + min_m g +
@@ -814,12 +820,12 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
                 float t2[NT];
 #pragma unroll
                 for (int jj = 0; jj < NT; ++jj) t2[jj] = t2_n[jj];
-                sdp += kTileD;
-                t2p += kTileD;
+                if constexpr (kIdx) di += kTileD;
+                else { sdp += kTileD; t2p += kTileD; }
                 if (tt + 1 < ntl) {  // prefetch the next tile's per-domain data
-                    sd_n = __ldg(sdp);
+                    sd_n = kIdx ? __ldg(P.SD + di) : __ldg(sdp);
 #pragma unroll
-                    for (int jj = 0; jj < NT; ++jj) t2_n[jj] = __ldg(t2p + jj * t2row);
+                    for (int jj = 0; jj < NT; ++jj) t2_n[jj] = kIdx ? __ldg(P.t2f + (di + jj * t2r)) : __ldg(t2p + jj * t2row);
                 }
                 tmbar_wait_sa(tfull_sa + 8 * buf, (tl / NBUF) & 1);
                 tc_fence_after();
