@@ -531,7 +531,8 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
     TCRange *sR = reinterpret_cast<TCRange *>(sB + Cf::BBUF * Cf::B_BYTES);   // [NR]
     float *sThr = reinterpret_cast<float *>(sR + NR);          // [NR] RU(best - A + margin), CAS-min
     float *sHsn = reinterpret_cast<float *>(sThr + NR);        // [NSP]
-    Partial *sRed = reinterpret_cast<Partial *>(sHsn + 16);    // [NR][4]
+    int *sSR = reinterpret_cast<int *>(sHsn + 16);              // [NR] range sums (B = 8 reads them here)
+    Partial *sRed = reinterpret_cast<Partial *>(sSR + NR);      // [NR][4]
     constexpr int NBUF = Cf::NBUF;
     uint64_t *bar = reinterpret_cast<uint64_t *>(sRed + NR * 4);  // full[S], empty[S], tfull[NB], tempty[NB], bop
     uint64_t *full = bar, *empty = bar + STAGES, *tfull = bar + 2 * STAGES, *tempty = tfull + NBUF;
@@ -742,6 +743,7 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
             if (et < NR) {
                 const TCRange R = P.rmeta[r0 + et];
                 sR[et] = R;
+                sSR[et] = R.SR;
                 const float th = P.has_zero ? fminf(__double2float_ru(R.margin), FLT_MAX) : FLT_MAX;
                 sThr[et] = R.valid ? th : -FLT_MAX;
             }
@@ -859,7 +861,8 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
                         const int mx = max(__vimax3_s32((int)v[0], (int)v[1], (int)v[2]),
                                            __vimax3_s32((int)v[3], (int)v[4], __vimax3_s32((int)v[5], (int)v[6], (int)v[7])));
                         mxs[q4] = mx;
-                        const float g0 = score(mx, rSR[q], sd, t2);
+                        // (B = 8, at its 96-register ceiling: the range sums from shared memory)
+                        const float g0 = score(mx, B == 8 ? sSR[eg * HALF + q] : rSR[q], sd, t2);
                         pm |= (g0 <= sThr[eg * HALF + q]) ? (1u << q4) : 0u;
                     }
                     if (pm) {  // queue (q, k*, max SRD) of the passing ranges for the exact path
@@ -977,7 +980,7 @@ template <int B, int NSP>
 static size_t tc_smem_bytes() {
     using Cf = TCfg<B>;
     return (size_t)Cf::STAGES * Cf::STAGE_BYTES + Cf::BBUF * Cf::B_BYTES + sizeof(TCRange) * Cf::NR + 4 * Cf::NR +
-           4 * 16 + sizeof(Partial) * Cf::NR * 4 + 8 * (2 * Cf::STAGES + 2 * Cf::NBUF + 4) + 16 +
+           4 * 16 + 4 * Cf::NR + sizeof(Partial) * Cf::NR * 4 + 8 * (2 * Cf::STAGES + 2 * Cf::NBUF + 4) + 16 +
            sizeof(Partial) * Cf::NR * kTileD + sizeof(int2) * 128 * Cf::EWG * 4 + 1024;
 }
 
