@@ -19,6 +19,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -49,8 +50,9 @@ def parse():
     ap.add_argument("--t", type=float, default=8.0)
     ap.add_argument("--cpu-shards", type=int, default=1,
                     help="cpu_baseline sample = 1/cpu-shards of the top-level blocks (1 = whole C3)")
-    ap.add_argument("--ref-shards", type=int, default=4,
-                    help="--impl reference: each step encodes 1/ref-shards of the top-level blocks")
+    ap.add_argument("--ref-shards", type=int, default=0,
+                    help="--impl reference: each step encodes 1/ref-shards of the top-level blocks "
+                         "(0 = sized so that the whole run takes about 2.5 minutes)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     return ap.parse_args()
@@ -176,7 +178,13 @@ def run_reference(args, cfg_name):
     cfg = config(cfg_name, s_mode=args.s_mode, t=args.t, topk=args.topk or None)
     img = image_for(cfg)
     S = args.ref_shards
-    for w in range(args.warmup):
+    w0 = 0
+    if S <= 0:  # size the per-step sample from one timed probe (1/64 of the blocks, a warm-up step)
+        _, dt0, _ = oracle_sample(cfg, img, 64, 0)
+        full = max(dt0 * 64, 1e-3)
+        S = max(1, min(1024, int(math.ceil((args.steps + args.warmup) * full / 150.0))))
+        w0 = 1
+    for w in range(w0, args.warmup):
         oracle_sample(cfg, img, S, w % S)
     tot_pairs, tot_t, thr = 0, 0.0, 1
     for k in range(args.steps):
