@@ -16,16 +16,21 @@
 //   (e; dom, k, j) first-min update; the running best of each range is shared by the CTA's
 //   128 domain lanes through a shared-memory atomic threshold.
 //
-// Roles (10 warps): warp 0 = TMEM allocator + bulk-copy producer, warp 1 = MMA issuer (one
-// elected thread), warps 2..9 = epilogue (two warpgroups, each half of the ranges; warp w reads
-// TMEM lanes 32 (w % 4) ..).  Pipelines: A stages full/empty (producer <-> MMA), TMEM buffers
-// full/empty (MMA <-> epilogue), two accumulator buffers of N columns.
+// B = 16 uses the QR form instead (A = the decimated D' as q = D' >> 2 and r = D' & 3 planes,
+// two accumulators, SRD = 4 S_q + S_r).
+//
+// Persistent CTAs, one per SM (SegPlan: lockstep rounds of range groups for pools larger than
+// ~L2/2, then a flattened (group, tile) tail in equal runs).  Roles: warp 0 = TMEM allocator +
+// bulk-copy producer (lane 0 the A stages, lane 1 the per-segment range operand), warp 1 = MMA
+// issuer (one elected thread), then EWG epilogue warpgroups (3 at B = 4, else 4), each a share
+// of the ranges; warp w reads TMEM lanes 32 (w % 4) ...  Pipelines: A stages full/empty
+// (producer <-> MMA), two TMEM accumulator buffers full/empty (MMA <-> epilogue, released right
+// after the tile's loads), range operand loaded/free (producer <-> MMA).
 #include <algorithm>
 #include <cfloat>
 #include <climits>
-#include <cstring>
-
 #include <cstdlib>
+#include <cstring>
 
 #include "fic_internal.cuh"
 
