@@ -1086,27 +1086,17 @@ cudaError_t launch_tc_search(int32_t B, const SearchParams &sp, const uint8_t *D
     }
 }
 
+// Partial-slot sizing for the persistent search: the level's ns_cap (4 x this hint, at most the
+// tile count) bounds the runs a range group can be cut into (SegPlan), so the flattened tail
+// can spread a few groups over every SM; the actual slot count is decided on the device.
 int tc_nsplit_hint(int32_t B, int64_t n_r, int64_t n_tiles, int num_sms) {
     const int64_t nr = tc_ranges_per_cta(B);
     const int64_t gx = (n_r + nr - 1) / nr;
     if (gx <= 0 || n_tiles <= 0) return 1;
     int64_t ns = ((int64_t)num_sms * 2 + gx - 1) / gx;
-    const int64_t max_ns = (n_tiles + 3) / 4;  // at least ~4 tiles per split
+    const int64_t max_ns = (n_tiles + 3) / 4;  // at least ~4 tiles per run
     if (ns > max_ns) ns = max_ns;
     if (ns < 1) ns = 1;
-    // B = 16 (one CTA per SM, few range groups): prefer a split count whose last wave is nearly
-    // full (up to 3x more splits).  At B <= 8 every extra split adds a first tile in which every
-    // pair passes the filter, which costs more than the tail it saves.
-    if (B == 16) {
-        auto eff = [&](int64_t k) {
-            const int64_t c = gx * k, w = (c + num_sms - 1) / num_sms;
-            return (double)c / (double)(w * num_sms);
-        };
-        int64_t best = ns;
-        for (int64_t k = ns; k <= std::min<int64_t>(3 * ns, max_ns); ++k)
-            if (eff(k) > eff(best) + 0.05) best = k;
-        ns = best;
-    }
     if (ns > 65535) ns = 65535;
     return (int)ns;
 }
