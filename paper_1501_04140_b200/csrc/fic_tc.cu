@@ -706,7 +706,10 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
         // fp32 filter score of one (range, domain) pair from the max over isometries of SRD_k
         auto score = [&](int mx, int rsr, int32_t sd, const float *t2) -> float {
             float bq;
-            if constexpr (NSP == 0) {
+            if constexpr (NSP == 0 && B <= 8) {
+                // exact Bq in int32 (|n SRD|, |SR SD| <= 1.06e9 at B = 8), one RN conversion
+                bq = (float)(n * mx - rsr * sd);
+            } else if constexpr (NSP == 0) {
                 // exact Bq (int64 at B = 16), one RN conversion
                 bq = (float)((long long)n * mx - (long long)rsr * sd);
             } else if constexpr (B == 2) {
