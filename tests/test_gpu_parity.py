@@ -185,6 +185,20 @@ def test_determinism_and_host_api(fic):
     assert a == b
     h = ctx.encode_host(img, cfg["B_max"], cfg["B_min"], cfg["L"], cfg["tau"], cfg["s"], cfg["rms_tol"])
     assert h.tobytes() == a
+    # a pinned output buffer: the kernels write the records into it directly (no final copy)
+    cap = (cfg["N"] // cfg["B_min"]) ** 2
+    pinned = torch.empty(cap * p.RECORD_BYTES, dtype=torch.uint8, pin_memory=True)
+    hp = ctx.encode_host(img, cfg["B_max"], cfg["B_min"], cfg["L"], cfg["tau"], cfg["s"], cfg["rms_tol"],
+                         out=pinned.numpy().view(p.RECORD_DTYPE))
+    assert hp.tobytes() == a
+    c3 = config("C3")  # a multi-level code: records from the side stream and the last finalize
+    img3 = image_for(c3)
+    ref = ctx.encode_cfg(c3, dev(torch, img3)).cpu().numpy().tobytes()
+    cap3 = (c3["N"] // c3["B_min"]) ** 2
+    pinned3 = torch.zeros(cap3 * p.RECORD_BYTES, dtype=torch.uint8, pin_memory=True)
+    hp3 = ctx.encode_host(img3, c3["B_max"], c3["B_min"], c3["L"], c3["tau"], c3["s"], c3["rms_tol"],
+                          out=pinned3.numpy().view(p.RECORD_DTYPE))
+    assert hp3.tobytes() == ref
 
 
 def test_shards_merge_equals_single(fic):
