@@ -138,7 +138,8 @@ int64_t entropy_threshold(double tau, int32_t m) {
 
 // ------------------------------------------------------------------------- pool building
 fic_status pool_enqueue(fic_ctx *ctx, Pool &P, const uint8_t *img, int32_t N, int32_t B,
-                        int32_t L, double tau, int64_t topk, cudaStream_t st) {
+                        int32_t L, double tau, int64_t topk, cudaStream_t st,
+                        unsigned long long *d_kept_mirror = nullptr) {
     P.device = ctx->device;
     P.N = N; P.B = B; P.L = L; P.n = B * B;
     P.A = (N - 2 * B) / L + 1;
@@ -180,7 +181,8 @@ fic_status pool_enqueue(fic_ctx *ctx, Pool &P, const uint8_t *img, int32_t N, in
         CK(fic::launch_topk_select(P.keys, P.n_c, topk, P.b_topk.p, P.keep, st));
         ctx->launches += 2;
     }
-    CK(fic::launch_select_index(P.keep, P.n_c, ptr<int64_t>(P.b_blocksum), P.kept, &P.d_misc[0], st));
+    CK(fic::launch_select_index(P.keep, P.n_c, ptr<int64_t>(P.b_blocksum), P.kept, &P.d_misc[0], st,
+                                d_kept_mirror));
     if (P.mode == 2)
         CK(fic::launch_pool_gather(img, N, B, L, P.A, P.kept, &P.d_misc[0], tiles_max, P.Dt, st));
     else if (P.mode == 0)
@@ -881,8 +883,9 @@ static fic_status encode_body(fic_ctx *ctx, const uint8_t *img, int32_t N, int32
         cudaStream_t ps = (l == 0 || !ctx->overlap_pools) ? st : ctx->side;
         ctx->launches = 0;
         if (ctx->timing >= 2) CK(cudaEventRecord(ctx->ev[l][0], ps));
+        // (n_kept is also written next to the other counters: one device -> host copy at the end)
         CKS(pool_enqueue(ctx, ctx->levels[l], img, N, B_max >> l, L, h_topk ? -1.0 : h_tau[l],
-                         h_topk ? h_topk[l] : 0, ps));
+                         h_topk ? h_topk[l] : 0, ps, d_counts + 48 + l));
         CKS(t2f_enqueue(ctx, ctx->levels[l], h_s + s_off[l], h_n_s[l], ps));
         if (ctx->timing >= 2) CK(cudaEventRecord(ctx->ev[l][4], ps));
         if (l > 0) CK(cudaEventRecord(ctx->pool_ready[l], ps));
@@ -949,11 +952,6 @@ static fic_status encode_body(fic_ctx *ctx, const uint8_t *img, int32_t N, int32
     CK(cudaStreamWaitEvent(st, ctx->main_ready, 0));
     const bool trace = ctx->timing >= 2 && getenv("FIC_TRACE");
     if (trace) CK(cudaEventRecord(ctx->ev[fic::kMaxLevels - 1][0], st));
-    {  // the pool counters (n_kept) of the levels next to the others, then one copy
-        fic::U64Ptrs src;
-        for (int l = 0; l < nl; ++l) src.p[l] = ctx->levels[l].d_misc;
-        CK(fic::launch_gather_u64(d_counts + 48, src, nl, st));
-    }
     CK(cudaMemcpyAsync(ctx->h_counts, d_counts, 64 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
     if (trace) CK(cudaEventRecord(ctx->ev[fic::kMaxLevels - 1][1], st));
     const auto hs0 = std::chrono::steady_clock::now();

@@ -187,7 +187,8 @@ cudaError_t launch_topk_select(const int64_t *keys, int64_t n_c, int64_t K, void
                                cudaStream_t st);
 // order-preserving compaction of u8 flags: writes indices and *d_total
 cudaError_t launch_select_index(const uint8_t *flags, int64_t n, int64_t *blocksum, int32_t *out,
-                                unsigned long long *d_total, cudaStream_t st);
+                                unsigned long long *d_total, cudaStream_t st,
+                                unsigned long long *d_total2 = nullptr);
 cudaError_t launch_select_grid(const uint8_t *flags, int64_t G, int32_t B, int64_t *blocksum,
                                int2 *out, unsigned long long *d_total, cudaStream_t st);
 // appends the flagged records at out[*d_base ...] (only below capacity), *d_total = count
@@ -197,11 +198,7 @@ cudaError_t launch_select_records(const uint8_t *flags, int64_t n, int64_t *bloc
 cudaError_t launch_set_u64(unsigned long long *d, unsigned long long v, cudaStream_t st);
 // *d_acc += *d_add (single thread)
 cudaError_t launch_accumulate(unsigned long long *d_acc, const unsigned long long *d_add, cudaStream_t st);
-// dst[i] = *src[i] for i < n <= 8 (one launch instead of n device -> host copies)
-struct U64Ptrs {
-    const unsigned long long *p[8];
-};
-cudaError_t launch_gather_u64(unsigned long long *dst, const U64Ptrs &src, int n, cudaStream_t st);
+
 size_t select_blocksum_len(int64_t n);
 cudaError_t launch_top_flags(uint8_t *flags, int64_t G, int32_t shard, int32_t n_shards,
                              cudaStream_t st);

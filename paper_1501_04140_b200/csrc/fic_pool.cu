@@ -204,7 +204,8 @@ constexpr int kChainItems = 16, kChainThreads = 256, kChainBlock = kChainItems *
 template <class Emit>
 __global__ void __launch_bounds__(kChainThreads) select_chain_kernel(const uint8_t *flags, int64_t n,
                                                                      Emit emit, unsigned long long *state,
-                                                                     uint32_t tag, unsigned long long *d_total) {
+                                                                     uint32_t tag, unsigned long long *d_total,
+                                                                     unsigned long long *d_total2) {
     __shared__ int wsum[kChainThreads / 32];
     __shared__ long long s_excl;
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
@@ -268,7 +269,10 @@ __global__ void __launch_bounds__(kChainThreads) select_chain_kernel(const uint8
             vs[blockIdx.x] = T | (2ull << 32) | (unsigned long long)(excl + tot);
         }
         s_excl = excl;
-        if (blockIdx.x == gridDim.x - 1) *d_total = (unsigned long long)(excl + tot);
+        if (blockIdx.x == gridDim.x - 1) {
+            *d_total = (unsigned long long)(excl + tot);
+            if (d_total2) *d_total2 = (unsigned long long)(excl + tot);
+        }
     }
     __syncthreads();
     int64_t pos = s_excl + wsum[warp] + incl - cnt;
@@ -292,18 +296,24 @@ static uint32_t next_chain_tag() {
 
 template <class Emit>
 static cudaError_t select_run(const uint8_t *flags, int64_t n, int64_t *blocksum, Emit emit,
-                              unsigned long long *d_total, cudaStream_t st) {
+                              unsigned long long *d_total, cudaStream_t st, unsigned long long *d_total2 = nullptr) {
     const int64_t nb = (n + kSelBlock - 1) / kSelBlock;
-    if (nb == 0) return cudaMemsetAsync(d_total, 0, sizeof(unsigned long long), st);
+    if (nb == 0) {
+        if (d_total2) {
+            const cudaError_t e = cudaMemsetAsync(d_total2, 0, sizeof(unsigned long long), st);
+            if (e != cudaSuccess) return e;
+        }
+        return cudaMemsetAsync(d_total, 0, sizeof(unsigned long long), st);
+    }
     static_assert(kChainBlock == kSelBlock, "blocksum scratch holds one word per chain block");
     select_chain_kernel<Emit><<<(unsigned)nb, kChainThreads, 0, st>>>(
-        flags, n, emit, reinterpret_cast<unsigned long long *>(blocksum), next_chain_tag(), d_total);
+        flags, n, emit, reinterpret_cast<unsigned long long *>(blocksum), next_chain_tag(), d_total, d_total2);
     return cudaGetLastError();
 }
 
 cudaError_t launch_select_index(const uint8_t *flags, int64_t n, int64_t *blocksum, int32_t *out,
-                                unsigned long long *d_total, cudaStream_t st) {
-    return select_run(flags, n, blocksum, EmitIndex{out}, d_total, st);
+                                unsigned long long *d_total, cudaStream_t st, unsigned long long *d_total2) {
+    return select_run(flags, n, blocksum, EmitIndex{out}, d_total, st, d_total2);
 }
 cudaError_t launch_select_grid(const uint8_t *flags, int64_t G, int32_t B, int64_t *blocksum,
                                int2 *out, unsigned long long *d_total, cudaStream_t st) {
@@ -323,16 +333,6 @@ cudaError_t launch_set_u64(unsigned long long *d, unsigned long long v, cudaStre
 }
 
 __global__ void accumulate_kernel(unsigned long long *acc, const unsigned long long *add) { *acc += *add; }
-
-__global__ void gather_u64_kernel(unsigned long long *dst, const U64Ptrs src, int n) {
-    if ((int)threadIdx.x < n) dst[threadIdx.x] = *src.p[threadIdx.x];
-}
-
-cudaError_t launch_gather_u64(unsigned long long *dst, const U64Ptrs &src, int n, cudaStream_t st) {
-    if (n <= 0) return cudaSuccess;
-    gather_u64_kernel<<<1, 32, 0, st>>>(dst, src, n);
-    return cudaGetLastError();
-}
 
 cudaError_t launch_accumulate(unsigned long long *d_acc, const unsigned long long *d_add, cudaStream_t st) {
     accumulate_kernel<<<1, 1, 0, st>>>(d_acc, d_add);
