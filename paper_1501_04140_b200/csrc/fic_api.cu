@@ -903,6 +903,7 @@ static fic_status encode_body(fic_ctx *ctx, const uint8_t *img, int32_t N, int32
 
     // 3. the quadtree, one level at a time, sizes carried on the device
     int cur = 0;
+    int last_direct = -1;  // level whose records finalize wrote straight into `out`
     for (int l = 0; l < nl && n_r_max > 0; ++l) {
         const int32_t B = B_max >> l;
         const Pool &P = ctx->levels[l];
@@ -920,8 +921,7 @@ static fic_status encode_body(fic_ctx *ctx, const uint8_t *img, int32_t N, int32
             CKS(level_enqueue(ctx, P, img, ptr<int2>(ctx->b_rng[cur]), d_counts + 32 + l, n_r_max,
                               h_s + s_off[l], h_n_s[l], h_rms_tol[l], 1, rec_l, acc_l, nullptr, l, d_err, out,
                               d_counts + 0, capacity, d_counts + 16 + l, ctx->main_ready));
-            CK(fic::launch_accumulate(d_counts + 0, d_counts + 16 + l, st));
-            ctx->launches += 1;
+            last_direct = l;  // (the host adds this level's count to the total after the copy)
         } else {
             CKS(level_enqueue(ctx, P, img, ptr<int2>(ctx->b_rng[cur]), d_counts + 32 + l, n_r_max,
                               h_s + s_off[l], h_n_s[l], h_rms_tol[l], 0, rec_l, acc_l, child, l, d_err));
@@ -1006,7 +1006,7 @@ static fic_status encode_body(fic_ctx *ctx, const uint8_t *img, int32_t N, int32
     }
     for (int l = 0; l < nl; ++l) ctx->levels[l].t2f_ready = 0;
     ctx->child_clean = true;  // every bitmap byte finalize marked was consumed by select_grid
-    const int64_t total = (int64_t)ctx->h_counts[0];
+    const int64_t total = (int64_t)ctx->h_counts[0] + (last_direct >= 0 ? (int64_t)ctx->h_counts[16 + last_direct] : 0);
     *h_n_out = total;
     if (total > capacity) return fail(ctx, FIC_ERR_CAPACITY, "output capacity too small");
     return FIC_OK;
