@@ -70,3 +70,15 @@ def test_capacity_and_argument_errors(fic):
                                cfg["B_min"], cfg["L"], n_s.ctypes.data_as(C.c_void_p), 0, 1.0,
                                C.c_void_p(out.data_ptr()), 16, C.byref(nb))
     assert st == 1  # FIC_ERR_ARG (B_max not a power of two)
+
+
+def test_stream_of_concatenated_shards(fic):
+    """The writer orders leaves itself (depth-first key), so the shards' codes simply
+    concatenated -- without the canonical merge -- give the same stream as the one-GPU code."""
+    p, ctx, torch = fic
+    cfg = config("C2", seed=3)
+    img = torch.from_numpy(image_for(cfg)).cuda()
+    full = ctx.serialize_cfg(cfg, ctx.encode_cfg(cfg, img))
+    parts = [ctx.encode_cfg(cfg, img, shard=r, n_shards=3).clone() for r in range(3)]
+    cat = torch.cat(parts, 0)
+    assert ctx.serialize_cfg(cfg, cat) == full
