@@ -1,0 +1,65 @@
+"""Randomized end-to-end parity (GPU vs oracle) over shapes the named configs do not reach:
+image sizes that leave ragged domain tiles and few range groups, odd steps L, 1-4 levels, every
+s mode, random entropy thresholds and tolerances, and small persistent grids (FIC_TC_CTAS) so
+that the search plan splits groups across runs.  Every record field must match bit for bit."""
+import numpy as np
+import pytest
+
+import oracle
+from fic_inputs import make_image
+from fic_inputs.configs import PREDEFINED_S, GRID_S, SAMPLED10_S, CLOSED5_S
+
+pytestmark = pytest.mark.gpu
+
+FIELDS = ("rx", "ry", "B", "dom", "dx", "dy", "iso", "s_idx", "o_code", "accepted", "err")
+
+
+@pytest.fixture(scope="module")
+def fic():
+    import torch
+    from paper_1501_04140_b200 import build as b
+    b.build()
+    import paper_1501_04140_b200 as p
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    ctx = p.Context(0)
+    yield p, ctx, torch
+    ctx.close()
+
+
+def case(seed):
+    rng = np.random.default_rng(1000 + seed)
+    B_max = int(rng.choice([4, 8, 16]))
+    B_min = int(rng.choice([b for b in (2, 4, 8, 16) if b <= B_max]))
+    N = B_max * int(rng.integers(2, 6))
+    L = int(rng.integers(1, 4))
+    levels = []
+    B = B_max
+    while B >= B_min:
+        levels.append(B)
+        B //= 2
+    mode = ["predefined", "grid", "sampled10", "closed5"][seed % 4]
+    sets = {"grid": GRID_S, "sampled10": SAMPLED10_S, "closed5": CLOSED5_S}
+    s_sets = [tuple(PREDEFINED_S[B]) if mode == "predefined" else sets[mode] for B in levels]
+    tau = [float(rng.choice([-1.0, 0.5, 1.5])) for _ in levels]
+    tol = [float(rng.choice([2.0, 6.0, 12.0]))] * len(levels)
+    img = make_image(N, 77 + seed, texture=bool(seed % 2))
+    ctas = int(rng.choice([3, 7, 148]))
+    return img, B_max, B_min, L, tau, s_sets, tol, mode, ctas
+
+
+@pytest.mark.parametrize("seed", range(48))
+def test_random_config_parity(fic, monkeypatch, seed):
+    p, ctx, torch = fic
+    img, B_max, B_min, L, tau, s_sets, tol, mode, ctas = case(seed)
+    monkeypatch.setenv("FIC_TC_CTAS", str(ctas))
+    try:
+        ref = oracle.encode(img, B_max, B_min, L, tau, s_sets, tol)
+    except Exception as e:  # e.g. an empty pool at a level with ranges: the GPU must refuse too
+        with pytest.raises(p.FicError):
+            ctx.encode(torch.from_numpy(img).cuda(), B_max, B_min, L, tau, s_sets, tol)
+        return
+    got = p.records_to_numpy(ctx.encode(torch.from_numpy(img).cuda(), B_max, B_min, L, tau, s_sets, tol))
+    what = f"seed {seed}: N={img.shape[0]} B {B_max}->{B_min} L={L} {mode} tau={tau} tol={tol[0]} ctas={ctas}"
+    assert len(got) == len(ref), what
+    for f in FIELDS:
+        assert np.array_equal(got[f], ref[f]), f"{what}: field {f}"
