@@ -63,3 +63,34 @@ def test_random_config_parity(fic, monkeypatch, seed):
     assert len(got) == len(ref), what
     for f in FIELDS:
         assert np.array_equal(got[f], ref[f]), f"{what}: field {f}"
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_random_topk_and_shards(fic, seed):
+    """Random pool sizes (top-K, reading R27) and a random shard count: every shard's code and
+    the merged code against the oracle's."""
+    p, ctx, torch = fic
+    img, B_max, B_min, L, tau, s_sets, tol, mode, _ = case(100 + seed)
+    rng = np.random.default_rng(seed)
+    K = [int(rng.integers(1, 300)) for _ in s_sets]
+    W = int(rng.integers(1, 5))
+    dimg = torch.from_numpy(img).cuda()
+    parts = []
+    for r in range(W):
+        ref = oracle.encode(img, B_max, B_min, L, tau, s_sets, tol, shard=r, n_shards=W, topk=K)
+        got = ctx.encode(dimg, B_max, B_min, L, tau, s_sets, tol, shard=r, n_shards=W, topk=K)
+        g = p.records_to_numpy(got)
+        assert len(g) == len(ref), (seed, r)
+        for f in FIELDS:
+            assert np.array_equal(g[f], ref[f]), (seed, r, f)
+        parts.append(got.clone())
+    counts = [x.shape[0] for x in parts]
+    stride = max(max(counts), 1)
+    buf = torch.zeros((W * stride, 40), dtype=torch.uint8, device="cuda")
+    for r, x in enumerate(parts):
+        buf[r * stride: r * stride + x.shape[0]] = x
+    merged = p.records_to_numpy(ctx.merge_shards(buf, counts, stride))
+    full = oracle.encode(img, B_max, B_min, L, tau, s_sets, tol, topk=K)
+    assert len(merged) == len(full)
+    for f in FIELDS:
+        assert np.array_equal(merged[f], full[f]), (seed, "merged", f)
