@@ -49,8 +49,7 @@ struct fic_ctx {
     Buf b_code;       // FIC1 writer scratch (fic_serialize)
     cudaEvent_t main_ready = nullptr;
     int b2_window = 1;    // env FIC_B2_WINDOW=0: B = 2 full scan instead of the C windows
-    int search_mode = 0;  // env FIC_SEARCH: auto (default: B=2 closed form, else tcgen05) | fourier | direct | tc
-    Buf b_rc, b_meta, b_u, b_gthr, b_rop, b_dec, b_nccl;
+    Buf b_u, b_gthr, b_rop, b_dec, b_nccl;
     ncclComm_t comm = nullptr;  // fic_ctx_create_nccl: one rank per GPU
     int32_t nranks = 1, rank = 0;  // libfic kernels enqueued (for fic_level_stats.kernel_launches)  // pool start, search start, search end, finalize end, pool end
 };
@@ -108,8 +107,8 @@ void free_buf(Buf &b) {
     b.cap = 0;
 }
 void free_pool(Pool &P) {
-    free_buf(P.b_keys); free_buf(P.b_keep); free_buf(P.b_kept); free_buf(P.b_Dt);
-    free_buf(P.b_SDf); free_buf(P.b_SD); free_buf(P.b_C); free_buf(P.b_misc); free_buf(P.b_Dc);
+    free_buf(P.b_keys); free_buf(P.b_keep); free_buf(P.b_kept);
+    free_buf(P.b_SDf); free_buf(P.b_SD); free_buf(P.b_C); free_buf(P.b_misc);
     free_buf(P.b_Dtc); free_buf(P.b_F2); free_buf(P.b_blocksum); free_buf(P.b_topk); free_buf(P.b_t2f);
 }
 
@@ -149,12 +148,7 @@ fic_status pool_enqueue(fic_ctx *ctx, Pool &P, const uint8_t *img, int32_t N, in
     CK(grow(ctx, P.b_keys, sizeof(int64_t) * P.n_c));
     CK(grow(ctx, P.b_keep, P.n_c + 16));
     CK(grow(ctx, P.b_kept, sizeof(int32_t) * P.n_c));
-    P.mode = ctx->search_mode == 4 ? 0 : ctx->search_mode;
-    if (ctx->search_mode == 0 && B == 2) P.mode = 3;
-    if (P.mode == 0 && !fic::tc_supported(B)) P.mode = 2;
-    if (P.mode == 1 && fic::fourier_record_stride(B) == 0) P.mode = 2;
-    if (P.mode == 2) CK(grow(ctx, P.b_Dt, sizeof(float) * slots * P.n));
-    if (P.mode == 1) CK(grow(ctx, P.b_Dc, sizeof(float) * slots * fic::fourier_record_stride(B)));
+    P.mode = B == 2 ? 3 : 0;  // B = 2: closed form on CUDA cores (fic_b2.cu); else tcgen05 (fic_tc.cu)
     if (P.mode == 0) CK(grow(ctx, P.b_Dtc, fic::tc_pool_bytes(B, tiles_max)));
     if (P.mode == 3) CK(grow(ctx, P.b_F2, fic::b2_pool_bytes(slots)));
     CK(grow(ctx, P.b_SDf, sizeof(float) * slots));
@@ -165,8 +159,6 @@ fic_status pool_enqueue(fic_ctx *ctx, Pool &P, const uint8_t *img, int32_t N, in
     P.n_tiles_max = tiles_max;
     P.keys = ptr<int64_t>(P.b_keys); P.keep = ptr<uint8_t>(P.b_keep);
     P.kept = ptr<int32_t>(P.b_kept); P.SDf = ptr<float>(P.b_SDf);
-    P.Dt = P.mode == 2 ? ptr<float>(P.b_Dt) : nullptr;
-    P.Dc = P.mode == 1 ? ptr<float>(P.b_Dc) : nullptr;
     P.Dtc = P.mode == 0 ? ptr<uint8_t>(P.b_Dtc) : nullptr;
     P.SD = ptr<int32_t>(P.b_SD); P.C = ptr<int64_t>(P.b_C);
     P.d_misc = ptr<unsigned long long>(P.b_misc);
@@ -183,16 +175,11 @@ fic_status pool_enqueue(fic_ctx *ctx, Pool &P, const uint8_t *img, int32_t N, in
     }
     CK(fic::launch_select_index(P.keep, P.n_c, ptr<int64_t>(P.b_blocksum), P.kept, &P.d_misc[0], st,
                                 d_kept_mirror));
-    if (P.mode == 2)
-        CK(fic::launch_pool_gather(img, N, B, L, P.A, P.kept, &P.d_misc[0], tiles_max, P.Dt, st));
-    else if (P.mode == 0)
+    if (P.mode == 0)
         CK(fic::launch_pool_tc(img, N, B, L, P.A, P.kept, &P.d_misc[0], tiles_max, P.Dtc, P.SD, P.SDf, P.C,
                                &P.d_misc[1], st));
-    else if (P.mode == 3)
-        CK(fic::launch_b2_pool(img, N, L, P.A, P.kept, &P.d_misc[0], slots, P.b_F2.p, &P.b2, st));
     else
-        CK(fic::launch_pool_coeff(img, N, B, L, P.A, P.kept, &P.d_misc[0], slots, P.Dc,
-                                  reinterpret_cast<unsigned int *>(&P.d_misc[2]), st));
+        CK(fic::launch_b2_pool(img, N, L, P.A, P.kept, &P.d_misc[0], slots, P.b_F2.p, &P.b2, st));
     const bool fused = P.mode == 0 && fic::tc_pool_has_moments(B);
     if (!fused)
         CK(fic::launch_pool_moments(img, N, B, L, P.A, P.kept, &P.d_misc[0], slots, P.SD, P.SDf, P.C,
@@ -239,13 +226,12 @@ fic_status check_s(fic_ctx *ctx, const double *h_s, int32_t n_s) {
 // the pool's stream right after the pool (off the quadtree's critical path); tcgen05 / direct only.
 fic_status t2f_enqueue(fic_ctx *ctx, Pool &P, const double *h_s, int32_t n_s, cudaStream_t st) {
     P.t2f_ready = 0;
-    if (P.mode != 0 && P.mode != 2) return FIC_OK;
+    if (P.mode != 0) return FIC_OK;
     fic::SList sl;
     memset(&sl, 0, sizeof sl);
     int nsp = 0;
     for (int j = 0; j < n_s; ++j)
         if (h_s[j] != 0.0) sl.s[nsp++] = h_s[j];
-    if (P.mode == 2 && nsp > 16) return FIC_OK;  // level_enqueue reports the error
     const int64_t slots = P.n_tiles_max * fic::kTileD;
     CK(grow(ctx, P.b_t2f, sizeof(float) * (size_t)slots * (nsp ? nsp : 1)));
     CK(fic::launch_t2f(P.C, &P.d_misc[0], slots, sl, nsp, reinterpret_cast<float *>(P.b_t2f.p),
@@ -271,7 +257,7 @@ fic_status level_enqueue(fic_ctx *ctx, const Pool &P, const uint8_t *img, const 
     sp.n_r = (int32_t)n_r_max;
     sp.d_nr = d_nr;
     sp.d_misc = P.d_misc;
-    sp.Dt = P.Dt; sp.SDf = P.SDf; sp.SD = P.SD; sp.C = P.C;
+    sp.SDf = P.SDf; sp.SD = P.SD; sp.C = P.C;
     const int64_t tiles = P.n_tiles_max;
     sp.n_k = (int32_t)(tiles * fic::kTileD);
     sp.n_tiles = (int32_t)tiles;
@@ -290,18 +276,14 @@ fic_status level_enqueue(fic_ctx *ctx, const Pool &P, const uint8_t *img, const 
         }
         if (h_s[j] > sp.smax) sp.smax = h_s[j];
     }
-    if (P.mode == 2)
-        sp.nsplit = fic::search_nsplit_hint(P.B, n_r_max, tiles, ctx->num_sms);
-    else if (P.mode == 0)
+    if (P.mode == 0)
         sp.nsplit = fic::tc_nsplit_hint(P.B, n_r_max, tiles, ctx->num_sms);
-    else if (P.mode == 3)
-        sp.nsplit = fic::b2_nsplit_hint(n_r_max, tiles, ctx->num_sms);
     else
-        sp.nsplit = fic::fourier_nsplit_hint(P.B, sp.nsp, n_r_max, tiles, ctx->num_sms);
+        sp.nsplit = fic::b2_nsplit_hint(n_r_max, tiles, ctx->num_sms);
     if (sp.nsplit < 1) sp.nsplit = 1;
     sp.tiles_per_split = (int32_t)((tiles + sp.nsplit - 1) / sp.nsplit);
-    // dynamic kernels (tcgen05, B=2) choose their split count on the device, up to ns_cap
-    const bool dyn = (P.mode == 0 || P.mode == 3);
+    // both search kernels (tcgen05, B = 2) choose their split count on the device, up to ns_cap
+    const bool dyn = true;
     sp.b2_window = ctx->b2_window;
     sp.L = P.L;
     sp.Acnt = P.A;
@@ -309,7 +291,7 @@ fic_status level_enqueue(fic_ctx *ctx, const Pool &P, const uint8_t *img, const 
     sp.ns_cap = dyn ? (int32_t)std::min<int64_t>(4 * (int64_t)sp.nsplit, std::max<int64_t>(1, tiles)) : sp.nsplit;
     sp.d_ns = ptr<unsigned long long>(ctx->b_counts) + 56 + level_slot;
     if (!dyn) CK(fic::launch_set_u64(sp.d_ns, (unsigned long long)sp.nsplit, st));
-    const bool t2f_pre = P.t2f_ready && (P.mode == 0 || P.mode == 2);  // enqueued with the pool
+    const bool t2f_pre = P.t2f_ready && P.mode == 0;  // enqueued with the pool
     if (!t2f_pre) CK(grow(ctx, ctx->b_t2f, sizeof(float) * (size_t)slots * (sp.nsp ? sp.nsp : 1)));
     CK(grow(ctx, ctx->b_part, sizeof(fic::Partial) * (size_t)n_r_max * sp.ns_cap));
     sp.t2f = t2f_pre ? reinterpret_cast<float *>(P.b_t2f.p) : ptr<float>(ctx->b_t2f);
@@ -317,9 +299,7 @@ fic_status level_enqueue(fic_ctx *ctx, const Pool &P, const uint8_t *img, const 
     sp.exact_count = ptr<unsigned long long>(ctx->b_counts) + 8 + level_slot;
     fic::SList sl;
     memcpy(sl.s, sp.spos, sizeof sl.s);
-    if (P.mode == 2 || P.mode == 0) {
-        if (P.mode == 2 && sp.nsp > 16)
-            return fail(ctx, FIC_ERR_ARG, "FIC_SEARCH=direct supports at most 16 contrast values > 0");
+    if (P.mode == 0) {
         if (!t2f_pre) {
             CK(fic::launch_t2f(P.C, &P.d_misc[0], slots, sl, sp.nsp, ptr<float>(ctx->b_t2f),
                                (P.mode == 0 && sp.nsp > 2) ? 1 : 0,
@@ -328,15 +308,11 @@ fic_status level_enqueue(fic_ctx *ctx, const Pool &P, const uint8_t *img, const 
         }
         if (ctx->timing) CK(cudaEventRecord(ctx->ev[level_slot][1], st));
         if (sp.nsp > 0) {
-            if (P.mode == 2) CK(fic::launch_search(P.B, sp.nsp, sp, st));
-            else {
-                CK(grow(ctx, ctx->b_rop, fic::tc_range_bytes(P.B, n_r_max)));
-                CK(fic::launch_tc_search(P.B, sp, P.Dtc, slots, ptr<uint8_t>(ctx->b_rop), st));
-                ctx->launches += 1;  // range preparation (operand + moments, one launch)
-            }
-            ctx->launches += 1;
+            CK(grow(ctx, ctx->b_rop, fic::tc_range_bytes(P.B, n_r_max)));
+            CK(fic::launch_tc_search(P.B, sp, P.Dtc, slots, ptr<uint8_t>(ctx->b_rop), st));
+            ctx->launches += 2;  // range preparation (operand + moments, one launch) + search
         }
-    } else if (P.mode == 3) {
+    } else {
         CK(grow(ctx, ctx->b_u, sizeof(float) * (size_t)slots * fic::b2_t2_width(sp.nsp)));
         if (ctx->timing) CK(cudaEventRecord(ctx->ev[level_slot][1], st));
         CK(grow(ctx, ctx->b_gthr, fic::b2_scratch_bytes(n_r_max, sp.ns_cap)));
@@ -345,17 +321,6 @@ fic_status level_enqueue(fic_ctx *ctx, const Pool &P, const uint8_t *img, const 
         // t2 table, pass 1 scan, pass 2 exact -- or the single window kernel
         const bool win = sp.b2_window && !sp.has_zero && sp.nsp <= 2;
         ctx->launches += sp.nsp > 0 && n_r_max > 0 ? (win ? 1 : 3) : 0;
-    } else {
-        const int nc = fic::fourier_record_stride(P.B);  // >= 8 nO + 1
-        const int32_t r_stride = (int32_t)((n_r_max + 31) / 32 * 32);
-        CK(grow(ctx, ctx->b_rc, sizeof(float) * (size_t)nc * r_stride));
-        CK(grow(ctx, ctx->b_meta, fic::fourier_meta_bytes() * (size_t)n_r_max));
-        CK(grow(ctx, ctx->b_u, sizeof(float) * (size_t)slots * (sp.nsp ? sp.nsp : 1)));
-        if (ctx->timing) CK(cudaEventRecord(ctx->ev[level_slot][1], st));
-        if (sp.nsp > 16) return fail(ctx, FIC_ERR_ARG, "FIC_SEARCH=fourier supports at most 16 contrast values > 0");
-        CK(fic::launch_fourier_level(P.B, sp, P.Dc, ptr<float>(ctx->b_rc), r_stride, ctx->b_meta.p,
-                                     ptr<float>(ctx->b_u), st));
-        ctx->launches += 1 + (sp.nsp > 0 ? 2 : 0);
     }
     if (ctx->timing) CK(cudaEventRecord(ctx->ev[level_slot][2], st));
     fic::FinalizeParams fp;
@@ -372,6 +337,9 @@ fic_status level_enqueue(fic_ctx *ctx, const Pool &P, const uint8_t *img, const 
     fp.SD = P.SD; fp.kept = P.kept;
     for (int j = 0; j < n_s; ++j) fp.s[j] = h_s[j];
     fp.n_s = n_s; fp.has_zero = sp.has_zero; fp.j_zero = sp.j_zero;
+    fp.fix_kj = 0;
+    for (int j = 0; j < n_s; ++j)
+        if (h_s[j] > 0.0 && h_s[j] < fic::kSLicensed) fp.fix_kj = 1;
     fp.rms_tol = rms_tol; fp.is_min = is_min;
     fp.rec = rec; fp.accepted = acc; fp.child = child;
     fp.out_direct = out_direct; fp.d_base = d_base; fp.capacity = capacity; fp.d_level_count = d_level_count;
@@ -604,15 +572,9 @@ fic_status fic_ctx_create(int32_t device, void *cuda_stream, fic_ctx **out) {
         e = cudaMemcpy(ctx->d_delta, delta.data(), sizeof(int64_t) * 4096, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMallocHost(&ctx->h_counts, 64 * sizeof(unsigned long long));
     if (e == cudaSuccess) e = grow(nullptr, ctx->b_counts, 64 * sizeof(unsigned long long));
-    if (e == cudaSuccess) e = fic::fourier_init();
     {
-        const char *env = getenv("FIC_SEARCH");
-        ctx->search_mode = 0;
         const char *bw = getenv("FIC_B2_WINDOW");
         ctx->b2_window = bw && strcmp(bw, "0") == 0 ? 0 : 1;
-        if (env && strcmp(env, "fourier") == 0) ctx->search_mode = 1;
-        if (env && strcmp(env, "direct") == 0) ctx->search_mode = 2;
-        if (env && strcmp(env, "tc") == 0) ctx->search_mode = 4;
         const char *ov = getenv("FIC_OVERLAP_POOLS");
         ctx->overlap_pools = ov ? atoi(ov) != 0 : 1;
     }
@@ -659,7 +621,7 @@ fic_status fic_ctx_destroy(fic_ctx *ctx) {
     for (auto &P : ctx->levels) free_pool(P);
     Buf *bufs[] = {&ctx->b_blocksum, &ctx->b_counts, &ctx->b_rng[0], &ctx->b_rng[1], &ctx->b_rec,
                    &ctx->b_acc, &ctx->b_child, &ctx->b_part, &ctx->b_t2f, &ctx->b_img, &ctx->b_out,
-                   &ctx->b_scounts, &ctx->b_rc, &ctx->b_meta, &ctx->b_u, &ctx->b_gthr, &ctx->b_rop, &ctx->b_dec, &ctx->b_nccl};
+                   &ctx->b_scounts, &ctx->b_u, &ctx->b_gthr, &ctx->b_rop, &ctx->b_dec, &ctx->b_nccl};
     if (ctx->comm) ncclCommDestroy(ctx->comm);
     for (Buf *b : bufs) free_buf(*b);
     if (ctx->d_delta) cudaFree(ctx->d_delta);
@@ -967,6 +929,8 @@ static fic_status encode_body(fic_ctx *ctx, const uint8_t *img, int32_t N, int32
     const unsigned long long *h = ctx->h_counts;
     if (*reinterpret_cast<const int32_t *>(h + 24) == FIC_ERR_EMPTY_POOL)
         return fail(ctx, FIC_ERR_EMPTY_POOL, "empty domain pool at a level that has ranges");
+    if (*reinterpret_cast<const int32_t *>(h + 24) != 0)
+        return fail(ctx, FIC_ERR_CUDA, "internal consistency check failed in finalize");
     for (int l = 0; l < nl; ++l) {
         fic_level_stats &ls = ctx->stats[l];
         const Pool &P = ctx->levels[l];

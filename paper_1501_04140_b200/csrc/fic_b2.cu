@@ -10,8 +10,7 @@
 //   X2 = a - b + c - d,  xr2 = 2|a - c|,  xi2 = 2|b - d|      (range features)
 //   Y2 = w - x + y - z,  yr = |w - y|,    yi = |x - z|        (domain features)
 // with Bq_k = n SRD_k - SR SD (n = 4).  Every product and sum is an integer below 2^24, so the
-// fp32 evaluation is exact.  The score filter and the exact path are those of fic_fourier.cu:
-// an fp32 lower bound of every binary64 score with a rigorous margin; surviving pairs are
+// fp32 evaluation is exact.  The score filter and the exact path follow fic_tc.cu's: an fp32 lower bound of every binary64 score with a rigorous margin; surviving pairs are
 // re-scored exactly (all 8 SRD_k in integers, canonical binary64 Eq. 1/3, lexicographic
 // first-min).  Result identical to the oracle's exhaustive loop.
 #include <cfloat>

@@ -1,9 +1,8 @@
 // fic_internal.cuh -- internal declarations of libfic (B200 / sm_100a).  Not part of the ABI.
 //
-// Layout of one level's pool in HBM (DESIGN.md §"Data layout"):
-//   Dt  float [n_tiles][n][128]   decimated domain D' (2x2 sums, exact integers <= 1020), one
-//                                 128-domain tile is one contiguous n*512-byte slab so a stage of
-//                                 the search kernel is a single cp.async.bulk copy
+// Layout of one level's pool in HBM (DESIGN.md §5 "Data layout"):
+//   Dtc u8 [n_tiles][chunks][128 x KCH]  tcgen05 A operand (B >= 4), core-matrix layout
+//   F2 / Cs / ds                         B = 2 closed-form pool, sorted by C
 //   SDf float [n_tiles*128], SD int32, C int64   domain moments (C = n*SDD - SD^2)
 // Pad domains (index >= n_kept) carry t2f = +inf, so the search filter never admits them.
 #pragma once
@@ -19,6 +18,10 @@ namespace fic {
 constexpr int kTileD = 128;  // domains per pool tile
 constexpr int kMaxS = 32;    // s values per level (5-bit closed-form levels)
 constexpr int kMaxLevels = 8;
+// Smallest s > 0 for which the searches may take the isometry as the lowest argmax of SRD_k
+// (distinct SRD give distinct binary64 scores; DESIGN.md §6 "Exactness"): a level whose s list
+// holds some s in (0, kSLicensed) has finalize re-derive (k, j) from the definition.
+constexpr double kSLicensed = 9.5367431640625e-07;  // 2^-20
 // Partial.kj flag: s index final, isometry k* not yet evaluated (finalize computes it for the
 // winning domain; the B = 2 search defers it because the same domain never competes twice)
 constexpr int32_t kPendIso = 1 << 16;
@@ -42,16 +45,15 @@ struct Pool {
     int64_t *keys = nullptr;
     uint8_t *keep = nullptr;
     int32_t *kept = nullptr;
-    float *Dt = nullptr, *SDf = nullptr;
-    float *Dc = nullptr;    // D4-Fourier domain records [slots][NCS] (B <= 8), or null
+    float *SDf = nullptr;
     uint8_t *Dtc = nullptr; // tcgen05 A operand: [tiles][chunks][128 x KCH] core-matrix u8, or null
     B2Pool b2;              // B = 2 closed-form pool (sorted by C)
-    int mode = 0;           // 0: tcgen05 (Dtc), 1: D4-Fourier (Dc), 2: direct FFMA (Dt), 3: B=2 closed form (F2)
+    int mode = 0;           // 0: tcgen05 (Dtc, B >= 4), 3: B = 2 closed form (F2)
     int32_t *SD = nullptr;
     int64_t *C = nullptr;
     unsigned long long *d_misc = nullptr;  // [0] = n_kept, [1] = Cmax, [2] = max |dh|_2 (float bits)
     double dnmax = 0.0;
-    Buf b_keys, b_keep, b_kept, b_Dt, b_SDf, b_SD, b_C, b_misc, b_Dc, b_Dtc, b_F2, b_blocksum, b_topk;
+    Buf b_keys, b_keep, b_kept, b_SDf, b_SD, b_C, b_misc, b_Dtc, b_F2, b_blocksum, b_topk;
     Buf b_t2f;           // fp32 filter table of this level, enqueued with the pool (fic_encode)
     int t2f_ready = 0;   // b_t2f holds the table for the level's s set (reset after the level)
     int device = 0;
@@ -75,7 +77,6 @@ struct SearchParams {
     const unsigned long long *d_nr;    // actual range count
     const unsigned long long *d_misc;  // pool: [0] n_kept, [1] Cmax, [2] max |dh|
     int64_t slot_stride;               // n_tiles (upper bound) * 128: stride of t2f rows
-    const float *Dt;
     const float *SDf;
     const int32_t *SD;
     const int64_t *C;
@@ -109,6 +110,7 @@ struct FinalizeParams {
     const int32_t *SD;
     const int32_t *kept;
     int32_t n_k;
+    int32_t fix_kj;  // the level's s list holds some s in (0, kSLicensed)
     double s[kMaxS];
     int32_t n_s, has_zero, j_zero;
     double rms_tol;
@@ -202,9 +204,6 @@ cudaError_t launch_accumulate(unsigned long long *d_acc, const unsigned long lon
 size_t select_blocksum_len(int64_t n);
 cudaError_t launch_top_flags(uint8_t *flags, int64_t G, int32_t shard, int32_t n_shards,
                              cudaStream_t st);
-cudaError_t launch_pool_gather(const uint8_t *img, int32_t N, int32_t B, int32_t L, int32_t A,
-                               const int32_t *kept, const unsigned long long *d_nk,
-                               int64_t n_tiles_max, float *Dt, cudaStream_t st);
 cudaError_t launch_pool_moments(const uint8_t *img, int32_t N, int32_t B, int32_t L, int32_t A,
                                 const int32_t *kept, const unsigned long long *d_nk,
                                 int64_t n_slots, int32_t *SD, float *SDf, int64_t *C,
@@ -214,11 +213,9 @@ struct SList {
 };
 cudaError_t launch_t2f(const int64_t *C, const unsigned long long *d_nk, int64_t n_slots, const SList &spos,
                        int32_t nsp, float *t2f, int32_t univ, float fold, cudaStream_t st);
-cudaError_t launch_search(int32_t B, int32_t nsp, const SearchParams &p, cudaStream_t st);
 cudaError_t launch_finalize(const FinalizeParams &p, cudaStream_t st);
 cudaError_t launch_merge_shards(const fic_record *in, const int64_t *d_counts, int32_t n_shards,
                                 int64_t stride, int64_t max_count, fic_record *out, cudaStream_t st);
-int search_nsplit_hint(int32_t B, int64_t n_r, int64_t n_tiles, int num_sms);
 
 // B = 2 closed-form search (fic_b2.cu)
 size_t b2_pool_bytes(int64_t n_slots);
@@ -233,8 +230,6 @@ size_t b2_scratch_bytes(int64_t n_r, int32_t ns_cap);  // pass-1 minima + split 
 cudaError_t launch_b2_search(const SearchParams &sp, const B2Pool &bp, float *T, const int32_t *kept,
                              int32_t L, int32_t A, void *scratch, unsigned long long *scan_count,
                              cudaStream_t st);
-cudaError_t launch_fourier_u(const int64_t *C, const unsigned long long *d_nk, int64_t n_slots, const SList &sl,
-                             int32_t nsp, float *U, cudaStream_t st);
 
 // decoding and PSNR (fic_decode.cu)
 struct DecSList {
@@ -248,7 +243,7 @@ cudaError_t launch_decode(const fic_record *rec, int64_t n_rec, int32_t N, int32
                           void *scratch, int32_t *d_bad, cudaStream_t st);
 cudaError_t launch_sse(const uint8_t *a, const uint8_t *b, int64_t n, unsigned long long *d_sse, cudaStream_t st);
 
-// tcgen05 search (fic_tc.cu), B in {2, 4, 8, 16}
+// tcgen05 search (fic_tc.cu), B in {4, 8, 16, 32}
 int tc_supported(int B);
 size_t tc_pool_bytes(int B, int64_t n_tiles);
 int tc_nsplit_hint(int32_t B, int64_t n_r, int64_t n_tiles, int num_sms);
@@ -261,17 +256,5 @@ cudaError_t launch_pool_tc(const uint8_t *img, int32_t N, int32_t B, int32_t L, 
 size_t tc_range_bytes(int B, int64_t n_r);  // scratch for the prepared range operand + metadata
 cudaError_t launch_tc_search(int32_t B, const SearchParams &sp, const uint8_t *Dtc, int64_t n_slots,
                              uint8_t *scratch, cudaStream_t st);
-
-// D4 group-Fourier search (fic_fourier.cu), B in {2, 4, 8}
-cudaError_t fourier_init();
-int fourier_record_stride(int B);  // floats per domain record (0 if B unsupported)
-size_t fourier_meta_bytes();
-int fourier_rpt(int32_t B, int32_t nsp);
-int fourier_nsplit_hint(int32_t B, int32_t nsp, int64_t n_r, int64_t n_tiles, int num_sms);
-cudaError_t launch_pool_coeff(const uint8_t *img, int32_t N, int32_t B, int32_t L, int32_t A,
-                              const int32_t *kept, const unsigned long long *d_nk, int64_t n_slots,
-                              float *Dc, unsigned int *d_dnmax, cudaStream_t st);
-cudaError_t launch_fourier_level(int32_t B, const SearchParams &sp, const float *Dc, float *Rc,
-                                 int32_t r_stride, void *meta, float *U, cudaStream_t st);
 
 }  // namespace fic

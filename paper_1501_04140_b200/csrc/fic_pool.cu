@@ -4,7 +4,6 @@
 //   entropy_keys_kernel  P:44-56 Eq. (4)-(5) + Abstract P:14: entropy of each raw 2B x 2B candidate
 //                        as the exact fixed-point key  K = LUT[m] - sum_v LUT[h_v]  [R6]
 //   select_*             row-major compaction (kept list, next-level ranges, accepted records)
-//   pool_gather_kernel   P:30 "decimated domain block": D'(i,j) = 2x2 sum  [R1]
 //   pool_moments_kernel  SD = sum D', SDD = sum D'^2, C = n SDD - SD^2 (int64, exact)
 #include <atomic>
 #include <cfloat>
@@ -348,46 +347,6 @@ cudaError_t launch_top_flags(uint8_t *flags, int64_t G, int32_t shard, int32_t n
                              cudaStream_t st) {
     const int64_t n = G * G;
     top_flags_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(flags, n, shard, n_shards);
-    return cudaGetLastError();
-}
-
-// ------------------------------------------------------------------------------ pool gather
-
-// Thread per (tile, p, lane128): Dt[tile][p][dl] = D'_{tile*128+dl}(p).  Consecutive threads
-// write consecutive domains of the same pixel p (coalesced 512-byte rows of the tile slab).
-__global__ void __launch_bounds__(256) pool_gather_kernel(const uint8_t *__restrict__ img, int32_t N,
-                                                          int32_t B, int32_t L, int32_t A,
-                                                          const int32_t *__restrict__ kept,
-                                                          const unsigned long long *__restrict__ d_nk,
-                                                          int64_t total, float *__restrict__ Dt) {
-    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (e >= total) return;
-    const int n = B * B;
-    const int64_t n_k = (int64_t)*d_nk;
-    const int64_t tile = e / ((int64_t)n * kTileD);
-    const int64_t ntiles = (n_k + kTileD - 1) / kTileD;
-    if (tile >= ntiles) return;
-    const int rem = (int)(e - tile * (int64_t)n * kTileD);
-    const int p = rem / kTileD, dl = rem - p * kTileD;
-    const int64_t d = tile * kTileD + dl;
-    float v = 0.f;
-    if (d < n_k) {
-        const int32_t c = kept[d];
-        const int64_t x = (int64_t)(c % A) * L, y = (int64_t)(c / A) * L;
-        const int i = p / B, j = p - (p / B) * B;
-        const uint8_t *q = img + (y + 2 * i) * N + x + 2 * j;
-        v = (float)((int)q[0] + (int)q[1] + (int)q[N] + (int)q[N + 1]);
-    }
-    Dt[e] = v;
-}
-
-cudaError_t launch_pool_gather(const uint8_t *img, int32_t N, int32_t B, int32_t L, int32_t A,
-                               const int32_t *kept, const unsigned long long *d_nk,
-                               int64_t n_tiles_max, float *Dt, cudaStream_t st) {
-    const int64_t total = n_tiles_max * (int64_t)B * B * kTileD;
-    if (total == 0) return cudaSuccess;
-    pool_gather_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(img, N, B, L, A, kept,
-                                                                        d_nk, total, Dt);
     return cudaGetLastError();
 }
 

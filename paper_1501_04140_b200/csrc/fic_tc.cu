@@ -296,11 +296,10 @@ __global__ void __launch_bounds__(256) pool_tc_kernel(const uint8_t *__restrict_
     }
 }
 
-int tc_supported(int B) { return B == 2 || B == 4 || B == 8 || B == 16; }
+int tc_supported(int B) { return B == 4 || B == 8 || B == 16; }
 
 size_t tc_pool_bytes(int B, int64_t n_tiles) {
     switch (B) {
-    case 2: return (size_t)n_tiles * TCfg<2>::CH * TCfg<2>::STAGE_BYTES;
     case 4: return (size_t)n_tiles * TCfg<4>::CH * TCfg<4>::STAGE_BYTES;
     case 8: return (size_t)n_tiles * TCfg<8>::CH * TCfg<8>::STAGE_BYTES;
     case 16: return (size_t)n_tiles * TCfg<16>::CH * TCfg<16>::STAGE_BYTES;
@@ -316,7 +315,6 @@ cudaError_t launch_pool_tc(const uint8_t *img, int32_t N, int32_t B, int32_t L, 
                            cudaStream_t st) {
     int g16 = 0;
     switch (B) {
-    case 2: g16 = TCfg<2>::KP / 16; break;
     case 4: g16 = TCfg<4>::KP / 16; break;
     case 8: g16 = TCfg<8>::KP / 16; break;
     case 16: g16 = TCfg<16>::QR ? TCfg<16>::n / 16 : TCfg<16>::KP / 16; break;
@@ -326,7 +324,6 @@ cudaError_t launch_pool_tc(const uint8_t *img, int32_t N, int32_t B, int32_t L, 
     if (total16 == 0) return cudaSuccess;
     const unsigned blocks = (unsigned)((total16 + 255) / 256);
     switch (B) {
-    case 2: pool_tc_kernel<2><<<blocks, 256, 0, st>>>(img, N, L, A, kept, d_nk, total16, Dtc, SD, SDf, C, d_cmax); break;
     case 4: pool_tc_kernel<4><<<blocks, 256, 0, st>>>(img, N, L, A, kept, d_nk, total16, Dtc, SD, SDf, C, d_cmax); break;
     case 8: pool_tc_kernel<8><<<blocks, 256, 0, st>>>(img, N, L, A, kept, d_nk, total16, Dtc, SD, SDf, C, d_cmax); break;
     case 16: pool_tc_kernel<16><<<blocks, 256, 0, st>>>(img, N, L, A, kept, d_nk, total16, Dtc, SD, SDf, C, d_cmax); break;
@@ -1028,7 +1025,6 @@ int tc_ranges_per_cta(int B) { return B == 16 ? 16 : (B == 4 ? 24 : 32); }
 
 size_t tc_range_bytes(int B, int64_t n_r) {
     switch (B) {
-    case 2: return (size_t)((n_r + TCfg<2>::NR - 1) / TCfg<2>::NR) * (TCfg<2>::B_BYTES + TCfg<2>::NR * sizeof(TCRangeG));
     case 4: return (size_t)((n_r + TCfg<4>::NR - 1) / TCfg<4>::NR) * (TCfg<4>::B_BYTES + TCfg<4>::NR * sizeof(TCRangeG));
     case 8: return (size_t)((n_r + TCfg<8>::NR - 1) / TCfg<8>::NR) * (TCfg<8>::B_BYTES + TCfg<8>::NR * sizeof(TCRangeG));
     case 16: return (size_t)((n_r + TCfg<16>::NR - 1) / TCfg<16>::NR) * (TCfg<16>::B_BYTES + TCfg<16>::NR * sizeof(TCRangeG));
@@ -1061,7 +1057,6 @@ cudaError_t launch_tc_search(int32_t B, const SearchParams &sp, const uint8_t *D
     memset(&p, 0, sizeof p);
     cudaError_t e0 = cudaSuccess;
     switch (B) {
-    case 2: e0 = tc_range_prep<2>(sp, scratch, p, st); break;
     case 4: e0 = tc_range_prep<4>(sp, scratch, p, st); break;
     case 8: e0 = tc_range_prep<8>(sp, scratch, p, st); break;
     case 16: e0 = tc_range_prep<16>(sp, scratch, p, st); break;
@@ -1081,7 +1076,6 @@ cudaError_t launch_tc_search(int32_t B, const SearchParams &sp, const uint8_t *D
     p.lockstep = tc_pool_bytes(B, (n_slots + kTileD - 1) / kTileD) > ((size_t)48 << 20) ? 1 : 0;
     if (const char *e = getenv("FIC_TC_LOCKSTEP")) p.lockstep = atoi(e) != 0;  // test hook
     switch (B) {
-    case 2: return launch_tc_b<2>(p, st);
     case 4: return launch_tc_b<4>(p, st);
     case 8: return launch_tc_b<8>(p, st);
     case 16: return launch_tc_b<16>(p, st);
