@@ -166,10 +166,19 @@ fic_status fic_ctx_create_nccl(int32_t device, void *cuda_stream, const uint8_t 
  * blocks t % nranks == r (no exchange on the data path), then an ncclAllGather of the record
  * counts and one of the records, and the canonical merge; every rank receives the full code
  * (identical to a one-GPU fic_encode) in `out` (device, capacity records; *h_n_out = count, also
- * on CAPACITY).  Synchronous.  Errors: as fic_encode; ARG without a communicator; NCCL. */
+ * on CAPACITY).  Synchronous; collective: every rank of the communicator must call it with the
+ * same arguments.  A rank whose shard fails sends its status through the count all-gather, so
+ * every rank returns that status (the lowest failing rank's) rather than blocking.
+ * Errors: as fic_encode; ARG without a communicator; NCCL. */
 fic_status fic_encode_nccl(fic_ctx *ctx, const uint8_t *img, int32_t N, int32_t B_max, int32_t B_min,
                            int32_t L, const double *h_tau, const double *h_s, const int32_t *h_n_s,
                            const double *h_rms_tol, fic_record *out, int64_t capacity, int64_t *h_n_out);
+
+/* fic_encode_nccl with per-level pool sizes h_K [levels] (top-K selection, as fic_encode_topk).
+ * Errors: as fic_encode_nccl, and ARG if h_K is null or some K < 1. */
+fic_status fic_encode_nccl_topk(fic_ctx *ctx, const uint8_t *img, int32_t N, int32_t B_max, int32_t B_min,
+                                int32_t L, const int64_t *h_K, const double *h_s, const int32_t *h_n_s,
+                                const double *h_rms_tol, fic_record *out, int64_t capacity, int64_t *h_n_out);
 
 /* Merge per-shard record lists (each sorted by B desc, ry, rx) into one canonical list.
  * in: device fic_record [n_shards][stride]; h_counts: host int64 [n_shards]; out: device

@@ -285,6 +285,7 @@ fic_status level_enqueue(fic_ctx *ctx, const Pool &P, const uint8_t *img, const 
     // both search kernels (tcgen05, B = 2) choose their split count on the device, up to ns_cap
     const bool dyn = true;
     sp.b2_window = ctx->b2_window;
+    sp.num_sms = ctx->num_sms;
     sp.L = P.L;
     sp.Acnt = P.A;
     sp.kept = P.kept;
@@ -437,6 +438,7 @@ fic_status fic_serialize(fic_ctx *ctx, const fic_record *rec, int64_t n_rec, int
         if (h_n_s[l] < 1 || h_n_s[l] > 255) return fail(ctx, FIC_ERR_ARG, "s count out of range");
         head.push_back((uint8_t)h_n_s[l]);
         P.sbits[l] = nbits(h_n_s[l]);
+        P.n_s[l] = h_n_s[l];
         P.posbits[l] = N >= 2 * B ? nbits((N - 2 * B) / L + 1) : 0;
     }
     const int64_t hb = (int64_t)head.size();
@@ -446,11 +448,16 @@ fic_status fic_serialize(fic_ctx *ctx, const fic_record *rec, int64_t n_rec, int
     CK(grow(ctx, ctx->b_code, fic::code_scratch_bytes(n_rec) + sizeof(unsigned) * (size_t)max_words + 256));
     unsigned *words = reinterpret_cast<unsigned *>(static_cast<char *>(ctx->b_code.p) + fic::code_scratch_bytes(n_rec));
     unsigned long long *d_total = ptr<unsigned long long>(ctx->b_counts) + 63;
+    int32_t *d_bad = reinterpret_cast<int32_t *>(ptr<unsigned long long>(ctx->b_counts) + 62);
     CK(cudaMemsetAsync(words, 0, sizeof(unsigned) * (size_t)max_words, st));
-    CK(fic::launch_code_body(rec, n_rec, P, ctx->b_code.p, words, d_total, st));
+    CK(cudaMemsetAsync(d_bad, 0, sizeof(int32_t), st));
+    CK(fic::launch_code_body(rec, n_rec, P, ctx->b_code.p, words, d_total, d_bad, st));
     unsigned long long bits = 0;
+    int32_t bad = 0;
     CK(cudaMemcpyAsync(&bits, d_total, sizeof bits, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&bad, d_bad, sizeof bad, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    if (bad) return fail(ctx, FIC_ERR_ARG, "a record cannot be coded (out of bounds, unknown level, s index or isometry)");
     const int64_t nbytes = hb + (int64_t)((bits + 7) / 8);
     *h_nbytes = nbytes;
     if (nbytes > capacity) return fail(ctx, FIC_ERR_CAPACITY, "output capacity too small for the stream");
@@ -495,12 +502,21 @@ fic_status fic_ctx_create_nccl(int32_t device, void *cuda_stream, const uint8_t 
         if (r_ != ncclSuccess) return fail(ctx, FIC_ERR_NCCL, std::string("NCCL: ") + ncclGetErrorString(r_)); \
     } while (0)
 
+static fic_status encode_impl(fic_ctx *ctx, const uint8_t *img, int32_t N, int32_t B_max, int32_t B_min,
+                              int32_t L, const double *h_tau, const int64_t *h_topk, const double *h_s,
+                              const int32_t *h_n_s, const double *h_rms_tol, int32_t shard, int32_t n_shards,
+                              fic_record *out, int64_t capacity, int64_t *h_n_out);
+
 // Rank r encodes the top-level blocks t % nranks == r (no exchange on the data path), then one
 // all-gather of the counts and one of the records (padded to the largest shard) over the
-// communicator, and the canonical merge (B desc, ry, rx) on every rank.
-fic_status fic_encode_nccl(fic_ctx *ctx, const uint8_t *img, int32_t N, int32_t B_max, int32_t B_min, int32_t L,
-                           const double *h_tau, const double *h_s, const int32_t *h_n_s, const double *h_rms_tol,
-                           fic_record *out, int64_t capacity, int64_t *h_n_out) {
+// communicator, and the canonical merge (B desc, ry, rx) on every rank.  A rank whose local encode
+// fails still takes part in the count all-gather, sending -status in place of its count, so
+// every rank sees the failure and returns the same status (that of the lowest failing rank)
+// instead of waiting in a collective the failed rank never reaches.
+static fic_status encode_nccl_impl(fic_ctx *ctx, const uint8_t *img, int32_t N, int32_t B_max, int32_t B_min,
+                                   int32_t L, const double *h_tau, const int64_t *h_topk, const double *h_s,
+                                   const int32_t *h_n_s, const double *h_rms_tol, fic_record *out, int64_t capacity,
+                                   int64_t *h_n_out) {
     CKS(ctx_check(ctx));
     if (h_n_out) *h_n_out = 0;
     if (!ctx->comm) return fail(ctx, FIC_ERR_ARG, "context has no NCCL communicator (fic_ctx_create_nccl)");
@@ -517,14 +533,23 @@ fic_status fic_encode_nccl(fic_ctx *ctx, const uint8_t *img, int32_t N, int32_t 
     int64_t *d_counts = reinterpret_cast<int64_t *>(base + rec_bytes * (size_t)(W + 1));
     int64_t *d_mine = d_counts + W;
     int64_t n_local = 0;
-    CKS(fic_encode(ctx, img, N, B_max, B_min, L, h_tau, h_s, h_n_s, h_rms_tol, ctx->rank, W, local, cap_local,
-                   &n_local));
+    const fic_status st_local = encode_impl(ctx, img, N, B_max, B_min, L, h_tau, h_topk, h_s, h_n_s, h_rms_tol,
+                                            ctx->rank, W, local, cap_local, &n_local);
+    const std::string err_local = ctx->err;
+    const int64_t mine = st_local == FIC_OK ? n_local : -(int64_t)st_local;
     cudaStream_t st = ctx->stream;
-    CK(cudaMemcpyAsync(d_mine, &n_local, sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(d_mine, &mine, sizeof(int64_t), cudaMemcpyHostToDevice, st));
     CKN(ncclAllGather(d_mine, d_counts, 1, ncclInt64, ctx->comm, st));
     std::vector<int64_t> counts(W);
     CK(cudaMemcpyAsync(counts.data(), d_counts, sizeof(int64_t) * W, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    for (int i = 0; i < W; ++i)
+        if (counts[i] < 0) {
+            const fic_status bad = (fic_status)(-counts[i]);
+            if (i == ctx->rank) return fail(ctx, bad, err_local);
+            return fail(ctx, bad, "rank " + std::to_string(i) + " failed its shard of the encode (status " +
+                                      std::to_string((int)bad) + ")");
+        }
     int64_t stride = 1, total = 0;
     for (int i = 0; i < W; ++i) {
         stride = std::max(stride, counts[i]);
@@ -541,6 +566,24 @@ fic_status fic_encode_nccl(fic_ctx *ctx, const uint8_t *img, int32_t N, int32_t 
     CK(fic::launch_merge_shards(gathered, d_counts, W, stride, stride, out, st));
     CK(cudaStreamSynchronize(st));
     return FIC_OK;
+}
+
+fic_status fic_encode_nccl(fic_ctx *ctx, const uint8_t *img, int32_t N, int32_t B_max, int32_t B_min, int32_t L,
+                           const double *h_tau, const double *h_s, const int32_t *h_n_s, const double *h_rms_tol,
+                           fic_record *out, int64_t capacity, int64_t *h_n_out) {
+    return encode_nccl_impl(ctx, img, N, B_max, B_min, L, h_tau, nullptr, h_s, h_n_s, h_rms_tol, out, capacity,
+                            h_n_out);
+}
+
+fic_status fic_encode_nccl_topk(fic_ctx *ctx, const uint8_t *img, int32_t N, int32_t B_max, int32_t B_min,
+                                int32_t L, const int64_t *h_K, const double *h_s, const int32_t *h_n_s,
+                                const double *h_rms_tol, fic_record *out, int64_t capacity, int64_t *h_n_out) {
+    if (!h_K) {
+        if (h_n_out) *h_n_out = 0;
+        return ctx ? fail(ctx, FIC_ERR_ARG, "null pool sizes") : FIC_ERR_ARG;
+    }
+    return encode_nccl_impl(ctx, img, N, B_max, B_min, L, nullptr, h_K, h_s, h_n_s, h_rms_tol, out, capacity,
+                            h_n_out);
 }
 
 const char *fic_version(void) { return "fic-b200 0.1 (sm_100a; fp32-exact CUDA-core search)"; }
@@ -799,6 +842,7 @@ static fic_status encode_body(fic_ctx *ctx, const uint8_t *img, int32_t N, int32
     for (int l = 0; l < nl; ++l) {
         CKS(check_level(ctx, N, B_max >> l, L));
         CKS(check_s(ctx, h_s + s_off[l], h_n_s[l]));
+        if (h_topk && h_topk[l] < 1) return fail(ctx, FIC_ERR_ARG, "pool size K must be >= 1");
         s_off[l + 1] = s_off[l] + h_n_s[l];
     }
     cudaStream_t st = ctx->stream;

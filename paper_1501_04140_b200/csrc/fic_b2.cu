@@ -740,12 +740,8 @@ static size_t b2_smem() {
 template <int NP>
 static cudaError_t launch_b2_scan(const B2Params &p, cudaStream_t st) {
     const size_t smem = b2_smem<NP>();
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(b2scan_kernel<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
+    static std::atomic<unsigned long long> attr{0};
+    if (cudaError_t e = ensure_smem_attr(b2scan_kernel<NP>, (int)smem, attr)) return e;
     dim3 grid((unsigned)((p.n_r + kB2Threads * kB2RPT - 1) / (kB2Threads * kB2RPT)), (unsigned)p.nsplit);
     b2scan_kernel<NP><<<grid, kB2Threads, smem, st>>>(p);
     return cudaGetLastError();

@@ -18,6 +18,20 @@ namespace fic {
 
 __device__ __forceinline__ int ilog2(int v) { return 31 - __clz(v); }
 
+// a record the container can hold: B a level in [B_min, B_max], the range inside the image on
+// its quadtree grid, the domain origin a candidate position of its level (multiple of L,
+// 2B x 2B block inside the image), iso < 8, s_idx below the level's s count
+__device__ __forceinline__ bool leaf_valid(const fic_record &r, const CodeParams &P) {
+    if (r.B < P.B_min || r.B > P.B_max || (r.B & (r.B - 1)) != 0) return false;
+    const int li = ilog2(P.B_max) - ilog2(r.B);
+    const int64_t N = P.N, B = r.B;
+    if (r.rx < 0 || r.ry < 0 || (int64_t)r.rx > N - B || (int64_t)r.ry > N - B || r.rx % r.B || r.ry % r.B)
+        return false;
+    if (r.dx < 0 || r.dy < 0 || (int64_t)r.dx > N - 2 * B || (int64_t)r.dy > N - 2 * B || r.dx % P.L || r.dy % P.L)
+        return false;
+    return r.iso < 8 && (int)r.s_idx < P.n_s[li];
+}
+
 // bit run of one leaf: (value right-aligned, MSB first; length)
 __device__ __forceinline__ void leaf_bits(const fic_record &r, const CodeParams &P, uint64_t &v, int &len) {
     v = 0;
@@ -40,10 +54,17 @@ __device__ __forceinline__ void leaf_bits(const fic_record &r, const CodeParams 
 
 __global__ void code_key_kernel(const fic_record *__restrict__ rec, int64_t n, const CodeParams P,
                                 unsigned long long *__restrict__ keys, int32_t *__restrict__ idx,
-                                uint32_t *__restrict__ lens) {
+                                uint32_t *__restrict__ lens, int32_t *__restrict__ d_bad) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const fic_record r = rec[i];
+    if (!leaf_valid(r, P)) {  // reported as FIC_ERR_ARG; contributes no bits
+        *d_bad = 1;
+        keys[i] = ~0ull;
+        idx[i] = (int32_t)i;
+        lens[i] = 0;
+        return;
+    }
     const int G = P.N / P.B_max;
     const unsigned long long top = (unsigned long long)(r.ry / P.B_max) * G + (r.rx / P.B_max);
     const int lx = (r.rx % P.B_max) / P.B_min, ly = (r.ry % P.B_max) / P.B_min;
@@ -69,9 +90,10 @@ __global__ void code_write_kernel(const fic_record *__restrict__ rec, const int3
                                   unsigned *__restrict__ words, unsigned long long *__restrict__ d_total) {
     const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= n) return;
-    uint64_t v;
-    int len;
-    leaf_bits(rec[idx[j]], P, v, len);
+    uint64_t v = 0;
+    int len = 0;
+    const fic_record r = rec[idx[j]];
+    if (leaf_valid(r, P)) leaf_bits(r, P, v, len);
     const unsigned long long p0 = off[j];
     if (j == n - 1) *d_total = p0 + (unsigned long long)len;
     unsigned long long cur_w = ~0ull;
@@ -102,7 +124,7 @@ size_t code_scratch_bytes(int64_t n) {
 }
 
 cudaError_t launch_code_body(const fic_record *rec, int64_t n, const CodeParams &P, void *scratch,
-                             unsigned *words, unsigned long long *d_total, cudaStream_t st) {
+                             unsigned *words, unsigned long long *d_total, int32_t *d_bad, cudaStream_t st) {
     if (n == 0) return cudaMemsetAsync(d_total, 0, sizeof(unsigned long long), st);
     auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
     char *b = static_cast<char *>(scratch);
@@ -119,7 +141,7 @@ cudaError_t launch_code_body(const fic_record *rec, int64_t n, const CodeParams 
     cub::DeviceScan::ExclusiveSum(nullptr, s1, ls, off, (int)n);
     tb = s0 > s1 ? s0 : s1;
     const unsigned g = (unsigned)((n + 255) / 256);
-    code_key_kernel<<<g, 256, 0, st>>>(rec, n, P, keys, idx, lens);
+    code_key_kernel<<<g, 256, 0, st>>>(rec, n, P, keys, idx, lens, d_bad);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     e = cub::DeviceRadixSort::SortPairs(b, tb, keys, kout, idx, iout, (int)n, 0, 64, st);

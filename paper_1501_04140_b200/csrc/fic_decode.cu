@@ -31,8 +31,8 @@ __global__ void dec_prep_kernel(const fic_record *__restrict__ rec, int64_t n_re
     int l = 0;
     while (l < n_levels && (B_max >> l) > r.B) ++l;
     const bool ok = l < n_levels && (B_max >> l) == r.B && r.B >= 1 && r.s_idx < sl.n_s[l] && r.iso < 8 &&
-                    r.rx >= 0 && r.ry >= 0 && r.rx + r.B <= N && r.ry + r.B <= N && r.dx >= 0 && r.dy >= 0 &&
-                    r.dx + 2 * r.B <= N && r.dy + 2 * r.B <= N;
+                    r.rx >= 0 && r.ry >= 0 && (int64_t)r.rx + r.B <= N && (int64_t)r.ry + r.B <= N && r.dx >= 0 &&
+                    r.dy >= 0 && (int64_t)r.dx + 2 * (int64_t)r.B <= N && (int64_t)r.dy + 2 * (int64_t)r.B <= N;
     if (!ok) {
         *d_bad = 1;
         return;

@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
 #include <string>
 
 #include "fic.h"
@@ -95,6 +96,7 @@ struct SearchParams {
     int32_t b2_window;           // B = 2: Cauchy-Schwarz C windows (env FIC_B2_WINDOW=0 disables)
     int32_t L, Acnt;             // domain step and candidates per axis (threshold seeding)
     const int32_t *kept;         // kept-domain candidate indices
+    int32_t num_sms;             // SMs of the context's device (persistent grids)
 };
 
 struct FinalizeParams {
@@ -125,6 +127,21 @@ struct FinalizeParams {
     int64_t capacity;
     unsigned long long *d_level_count;
 };
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device): the attribute
+// belongs to the function in each device's context, so the cache is a per-device bit mask
+// (thread-safe; a second context on another device sets it again there).
+template <class F>
+inline cudaError_t ensure_smem_attr(F *fn, int bytes, std::atomic<unsigned long long> &done_mask) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (done_mask.load(std::memory_order_acquire) & bit) return cudaSuccess;
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e == cudaSuccess) done_mask.fetch_or(bit, std::memory_order_acq_rel);
+    return e;
+}
 
 // Dynamic mapping of a CTA to (range group, domain split) from the actual counts: the grid is
 // sized from host upper bounds; ns = min(ns_cap, ctas / groups, tiles / min_tiles) splits.
@@ -172,12 +189,13 @@ __host__ __device__ constexpr float tc_t2_fold(int B, int nsp) {
 // FIC1 body writer (fic_code.cu): per level (index 0 = B_max) the position and s-index widths
 struct CodeParams {
     int32_t N, B_max, B_min, L;
-    int32_t posbits[kMaxLevels], sbits[kMaxLevels];
+    int32_t posbits[kMaxLevels], sbits[kMaxLevels], n_s[kMaxLevels];
 };
 size_t code_scratch_bytes(int64_t n);
-// words: zeroed body buffer (>= ceil(bits / 32) words); *d_total = body length in bits
+// words: zeroed body buffer (>= ceil(bits / 32) words); *d_total = body length in bits;
+// *d_bad (zeroed by the caller) = 1 if some record cannot be coded (out of bounds, unknown level)
 cudaError_t launch_code_body(const fic_record *rec, int64_t n, const CodeParams &P, void *scratch,
-                             unsigned *words, unsigned long long *d_total, cudaStream_t st);
+                             unsigned *words, unsigned long long *d_total, int32_t *d_bad, cudaStream_t st);
 
 // ---- launchers (return cudaError_t of the launch) ---------------------------------------------
 cudaError_t launch_entropy_keys(const uint8_t *img, int32_t N, int32_t B, int32_t L, int32_t A,

@@ -128,23 +128,16 @@ cudaError_t launch_entropy_keys(const uint8_t *img, int32_t N, int32_t B, int32_
     const int side = 2 * B, m = side * side;
     if (B >= 8 && L < side / 2) {  // sliding windows pay off (>= 4x fewer histogram updates)
         const size_t smem = sizeof(int64_t) * m + 8 * 256 * sizeof(int32_t);
-        static bool attr2 = false;
-        if (!attr2) {
-            cudaFuncSetAttribute(entropy_slide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-            attr2 = true;
-        }
+        static std::atomic<unsigned long long> attr2{0};
+        if (cudaError_t e = ensure_smem_attr(entropy_slide_kernel, 64 * 1024, attr2)) return e;
         const int64_t warps = (int64_t)A * ((A + kSlideSeg - 1) / kSlideSeg);
         entropy_slide_kernel<<<(unsigned)((warps + 7) / 8), 256, smem, st>>>(img, N, side, L, A, d_delta, lut_m, T,
                                                                              use_tau, keys, keep);
         return cudaGetLastError();
     }
     const size_t smem = sizeof(int64_t) * m + 8 * 256 * sizeof(int32_t);
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(entropy_keys_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             64 * 1024);
-        attr = true;
-    }
+    static std::atomic<unsigned long long> attr{0};
+    if (cudaError_t e = ensure_smem_attr(entropy_keys_kernel, 64 * 1024, attr)) return e;
     const int64_t n_c = (int64_t)A * A;
     int64_t blocks = (n_c + 7) / 8;
     if (blocks > 148 * 8) blocks = 148 * 8;

@@ -480,6 +480,7 @@ struct TCParams {
     Partial *part;
     unsigned long long *exact_count;
     int32_t lockstep;  // full rounds in lockstep (pool larger than ~L2/2), else all flattened
+    int32_t num_sms;
 };
 
 using TCRange = TCRangeG;
@@ -993,21 +994,11 @@ template <int B, int NSP>
 static cudaError_t launch_tc_t(const TCParams &p, cudaStream_t st) {
     using Cf = TCfg<B>;
     const size_t smem = tc_smem_bytes<B, NSP>();
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(tcsearch_kernel<B, NSP>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
-    // persistent: one CTA per SM (the kernel partitions the (group, tile) space itself)
-    static int num_sms = 0;
-    if (!num_sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
-        if (num_sms <= 0) num_sms = 148;
-    }
+    static std::atomic<unsigned long long> attr{0};
+    if (cudaError_t e = ensure_smem_attr(tcsearch_kernel<B, NSP>, (int)smem, attr)) return e;
+    // persistent: one CTA per SM of the context's device (the kernel partitions the (group, tile)
+    // space itself)
+    const int num_sms = p.num_sms > 0 ? p.num_sms : 148;
     int ctas = num_sms;
     if (const char *e = getenv("FIC_TC_CTAS")) ctas = std::max(1, atoi(e));  // test hook: small grids
     tcsearch_kernel<B, NSP><<<(unsigned)ctas, Cf::THREADS, smem, st>>>(p);
@@ -1073,6 +1064,7 @@ cudaError_t launch_tc_search(int32_t B, const SearchParams &sp, const uint8_t *D
     p.has_zero = sp.has_zero; p.j_zero = sp.j_zero;
     p.smax = sp.smax;
     p.part = sp.part; p.exact_count = sp.exact_count;
+    p.num_sms = sp.num_sms;
     p.lockstep = tc_pool_bytes(B, (n_slots + kTileD - 1) / kTileD) > ((size_t)48 << 20) ? 1 : 0;
     if (const char *e = getenv("FIC_TC_LOCKSTEP")) p.lockstep = atoi(e) != 0;  // test hook
     switch (B) {

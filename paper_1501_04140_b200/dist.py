@@ -51,5 +51,6 @@ def native_context(device: int, group=None, **kw) -> Context:
 
 
 def native_sharded_encode(ctx: Context, img, cfg):
-    """fic_encode_nccl: shard, NCCL all-gather and merge inside the library."""
-    return ctx.encode_nccl(img, cfg["B_max"], cfg["B_min"], cfg["L"], cfg["tau"], cfg["s"], cfg["rms_tol"])
+    """fic_encode_nccl (fic_encode_nccl_topk for a top-K cfg): shard, NCCL all-gather and merge
+    inside the library."""
+    return ctx.encode_nccl_cfg(cfg, img)

@@ -31,7 +31,8 @@ EXPORTS = (
     "fic_ctx_set_timing", "fic_get_stats", "fic_build_domain_pool", "fic_pool_info",
     "fic_pool_destroy", "fic_encode_level", "fic_encode", "fic_encode_host", "fic_merge_shards",
     "fic_entropy_lut", "fic_version", "fic_decode", "fic_psnr", "fic_build_domain_pool_topk",
-    "fic_encode_topk", "fic_nccl_unique_id", "fic_ctx_create_nccl", "fic_encode_nccl", "fic_serialize",
+    "fic_encode_topk", "fic_nccl_unique_id", "fic_ctx_create_nccl", "fic_encode_nccl", "fic_encode_nccl_topk",
+    "fic_serialize",
 )
 
 S_MODE_CODES = {"predefined": 0, "sampled10": 1, "closed5": 2, "grid": 3}  # FIC1 header s_mode
@@ -86,6 +87,7 @@ def load(path: str = SO_PATH):
         "fic_nccl_unique_id": ([P], C.c_int),
         "fic_ctx_create_nccl": ([i32, P, P, i32, i32, P], C.c_int),
         "fic_encode_nccl": ([P, P, i32, i32, i32, i32, P, P, P, P, P, i64, P], C.c_int),
+        "fic_encode_nccl_topk": ([P, P, i32, i32, i32, i32, P, P, P, P, P, i64, P], C.c_int),
         "fic_psnr": ([P, P, P, i64, P], C.c_int),
         "fic_serialize": ([P, P, i64, i32, i32, i32, i32, P, i32, dbl, P, i64, P], C.c_int),
         "fic_version": ([], C.c_char_p),
@@ -312,9 +314,10 @@ class Context:
                                               stride, _dptr(out)), "fic_merge_shards")
         return out[: int(cnt.sum())]
 
-    def encode_nccl(self, img, B_max: int, B_min: int, L: int, tau, s_sets, rms_tol, out=None):
-        """Sharded encode over the context's NCCL communicator (fic_encode_nccl): every rank gets
-        the full canonical code (CUDA uint8 [n, 40])."""
+    def encode_nccl(self, img, B_max: int, B_min: int, L: int, tau, s_sets, rms_tol, out=None, topk=None):
+        """Sharded encode over the context's NCCL communicator (fic_encode_nccl, or
+        fic_encode_nccl_topk with per-level pool sizes): every rank gets the full canonical code
+        (CUDA uint8 [n, 40])."""
         import torch
         N = img.shape[0]
         tau, n_s, s_flat, tol = self._cfg_arrays(tau, s_sets, rms_tol)
@@ -322,10 +325,20 @@ class Context:
         if out is None or out.shape[0] < cap:
             out = torch.empty((cap, RECORD_BYTES), dtype=torch.uint8, device=img.device)
         n_out = C.c_int64()
-        self._check(self.lib.fic_encode_nccl(self.handle, _dptr(img), N, B_max, B_min, L, _ptr(tau), _ptr(s_flat),
-                                             _ptr(n_s), _ptr(tol), _dptr(out), out.shape[0], C.byref(n_out)),
-                    "fic_encode_nccl")
+        if topk is None:
+            st = self.lib.fic_encode_nccl(self.handle, _dptr(img), N, B_max, B_min, L, _ptr(tau), _ptr(s_flat),
+                                          _ptr(n_s), _ptr(tol), _dptr(out), out.shape[0], C.byref(n_out))
+            self._check(st, "fic_encode_nccl")
+        else:
+            K = np.ascontiguousarray(topk, dtype=np.int64)
+            st = self.lib.fic_encode_nccl_topk(self.handle, _dptr(img), N, B_max, B_min, L, _ptr(K), _ptr(s_flat),
+                                               _ptr(n_s), _ptr(tol), _dptr(out), out.shape[0], C.byref(n_out))
+            self._check(st, "fic_encode_nccl_topk")
         return out[: n_out.value]
+
+    def encode_nccl_cfg(self, cfg, img, out=None):
+        return self.encode_nccl(img, cfg["B_max"], cfg["B_min"], cfg["L"], cfg["tau"], cfg["s"], cfg["rms_tol"],
+                                out=out, topk=cfg.get("topk"))
 
     def decode(self, recs, N: int, B_max: int, s_sets, iterations: int = 12, init=None):
         """PIFS decode (fic_decode): CUDA uint8 [n, 40] records -> CUDA uint8 [N, N] image."""

@@ -82,3 +82,24 @@ def test_stream_of_concatenated_shards(fic):
     parts = [ctx.encode_cfg(cfg, img, shard=r, n_shards=3).clone() for r in range(3)]
     cat = torch.cat(parts, 0)
     assert ctx.serialize_cfg(cfg, cat) == full
+
+
+@pytest.mark.parametrize("field,value", [("B", 3), ("B", 64), ("rx", 2 ** 31 - 2), ("ry", -4), ("dx", 1),
+                                         ("dy", 10 ** 6), ("iso", 8), ("s_idx", 7)])
+def test_corrupt_record_rejected(fic, field, value):
+    """A record the container cannot hold (level outside [B_min, B_max], range or domain outside
+    the image or off its grid, isometry >= 8, s index past the level's list) is FIC_ERR_ARG, not
+    an out-of-bounds write; the decoder rejects the same records."""
+    p, ctx, torch = fic
+    cfg = config("C2")
+    img = torch.from_numpy(image_for(cfg)).cuda()
+    recs = p.records_to_numpy(ctx.encode_cfg(cfg, img)).copy()
+    recs[5][field] = value
+    bad = torch.from_numpy(recs.view(np.uint8).reshape(-1, 40).copy()).cuda()
+    with pytest.raises(p.FicError) as ei:
+        ctx.serialize_cfg(cfg, bad)
+    assert ei.value.status == 1
+    if field not in ("dx",):  # (dx = 1 is a valid decode position; only the container needs dx % L == 0)
+        with pytest.raises(p.FicError) as ei:
+            ctx.decode(bad, cfg["N"], cfg["B_max"], cfg["s"], 2)
+        assert ei.value.status == 1

@@ -503,3 +503,27 @@ def test_c3_full_parity(fic, smode):
     cfg = config("C3", s_mode=smode, t=8.0)
     img, got = encode_both(fic, cfg)
     assert_same(got, oracle.encode_cfg(cfg, img), f"C3 {smode} full")
+
+
+def test_native_nccl_error_status_and_topk(fic):
+    """fic_encode_nccl exchanges a failing shard's status through the count all-gather (every
+    rank returns it instead of blocking in the record all-gather): on a one-rank communicator an
+    empty pool comes back as FIC_ERR_EMPTY_POOL, and the context stays usable.  The top-K variant
+    (fic_encode_nccl_topk) returns the one-GPU top-K code."""
+    p, ctx, torch = fic
+    nctx = p.Context(0, nccl=(p.nccl_unique_id(), 1, 0))
+    try:
+        bad = dev(torch, constant_image(64, 3))
+        with pytest.raises(p.FicError) as ei:
+            nctx.encode_nccl(bad, 16, 2, 2, [0.1] * 4, [(0.5,)] * 4, [8.0] * 4)
+        assert ei.value.status == 3
+        cfg = config("C2", topk=[64, 128, 256, 512])
+        img = dev(torch, image_for(cfg))
+        ref = ctx.encode_cfg(cfg, img)
+        got = nctx.encode_nccl_cfg(cfg, img)
+        assert got.cpu().numpy().tobytes() == ref.cpu().numpy().tobytes()
+        with pytest.raises(p.FicError) as ei:
+            nctx.encode_nccl(img, 16, 2, 4, [-1.0] * 4, cfg["s"], cfg["rms_tol"], topk=[64, 0, 1, 1])
+        assert ei.value.status == 1
+    finally:
+        nctx.close()
