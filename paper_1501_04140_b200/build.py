@@ -57,6 +57,18 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return _build_locked(verbose)
 
 
+def build_variant(out_path: str, defines=(), extra=()) -> str:
+    """A diagnostics / A-B build of the same sources into out_path (e.g. -DFIC_TC_TRACE for
+    scripts/tc_trace.py); loaded with FIC_SO=out_path.  Not used by the product path."""
+    cmd = [NVCC, *NVCC_FLAGS, *[f"-D{d}" for d in defines], *extra, "-I", INCLUDE, "-I", CSRC, "-o", out_path,
+           *sources(), "-lquadmath", *nccl_link()]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        sys.stderr.write(res.stdout + res.stderr)
+        raise RuntimeError("nvcc failed for the variant build")
+    return out_path
+
+
 def _build_locked(verbose: bool) -> str:
     # NCCL (fic_ctx_create_nccl / fic_encode_nccl): the system headers; the library is the one
     # torch bundles (nvidia/nccl/lib, rpath), so whichever of torch and libfic.so loads first,

@@ -64,7 +64,18 @@ struct TCfg {
     static constexpr int ACC = QR ? 2 * N : N;             // TMEM columns per accumulator buffer
     static constexpr int NBUF = 512 / ACC >= 4 ? 4 : 2;    // TMEM accumulator buffers (MMA <-> epilogue)
     static constexpr int EWG = B == 4 ? 3 : 4;            // epilogue warpgroups
-    static constexpr int THREADS = 64 + 128 * EWG;
+    // warps: producer, MMA issuer, 4 EWG epilogue warps, the exact-path warp
+    static constexpr int XWARP = 2 + 4 * EWG;
+    static constexpr int THREADS = 64 + 128 * EWG + 32;
+    static constexpr int XQ = 512;                         // exact-path work ring (power of two)
+};
+
+// One (range, domain) pair the fp32 filter could not exclude, queued for the exact-path warp.
+struct XItem {
+    int32_t mx;    // max_k SRD_k
+    int32_t d;     // pool slot of the domain
+    int32_t sd;    // its SD
+    int32_t meta;  // range q (5 bits) | k* << 5 | domain lane m << 8
 };
 
 constexpr uint32_t kTmemCols = 512;
@@ -455,6 +466,42 @@ __global__ void __launch_bounds__(256) tc_range_prep_kernel(const uint8_t *__res
     else tc_range_meta_body<B>(img, N, ranges, d_nr, n_pad, smax, d_misc, meta, univ, blockIdx.x - nb_op);
 }
 
+// ------------------------------------------------------------------------------ pipeline trace
+// Diagnostics only (-DFIC_TC_TRACE, scripts/tc_trace.py): clock64 stamps of CTA 0's pipeline
+// events -- 0 producer copy issued, 1 MMA saw the stage full, 2 MMA saw the accumulator free,
+// 3 MMA committed the tile, 4 epilogue warp 2 saw the tile, 5 its loads done, 6 its tile done,
+// 7 the last epilogue warp's tile done, 8 + w - 2 epilogue warp w's loads done.
+#ifdef FIC_TC_TRACE
+__device__ long long g_tc_trace[32][4096];
+#define TC_TR(kind, idx)                                                           \
+    do {                                                                           \
+        if (blockIdx.x == 0 && (idx) < 4096) g_tc_trace[kind][idx] = clock64();   \
+    } while (0)
+__device__ __forceinline__ long long tc_gtime() {
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define TC_TR_SEG(kind, k)                                                                        \
+    do {                                                                                          \
+        if (blockIdx.x < 512 && (k) < 8) g_tc_trace[kind][blockIdx.x * 8 + (k)] = tc_gtime();      \
+    } while (0)
+#define TC_TR_CTA(kind)                                                      \
+    do {                                                                     \
+        if (threadIdx.x == 0 && blockIdx.x < 4096) g_tc_trace[kind][blockIdx.x] = tc_gtime(); \
+    } while (0)
+#else
+#define TC_TR(kind, idx) \
+    do {                 \
+    } while (0)
+#define TC_TR_CTA(kind) \
+    do {                \
+    } while (0)
+#define TC_TR_SEG(kind, k) \
+    do {                   \
+    } while (0)
+#endif
+
 // ------------------------------------------------------------------------------ search kernel
 struct TCParams {
     const unsigned long long *d_nr, *d_misc;  // device sizes: n_r; n_kept, Cmax
@@ -542,7 +589,10 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
     uint64_t *bbar = tempty + NBUF;  // [BBUF] range operand loaded, [BBUF] range operand free
     uint32_t *sTmem = reinterpret_cast<uint32_t *>(bbar + 4);
     Partial *sBest = reinterpret_cast<Partial *>(sTmem + 4);  // [NR][128] per (range, domain lane)
-    int2 *sQ = reinterpret_cast<int2 *>(sBest + NR * kTileD);  // [epilogue threads][4] exact queue
+    XItem *sXQ = reinterpret_cast<XItem *>(sBest + NR * kTileD);     // [XQ] exact-path ring
+    unsigned *sXSeq = reinterpret_cast<unsigned *>(sXQ + Cf::XQ);    // [XQ] slot i holds item i when = i + 1
+    unsigned *sXCtl = sXSeq + Cf::XQ;  // [0] items reserved, [1] items consumed, [2] no more items
+    float *sM2 = reinterpret_cast<float *>(sXCtl + 4);  // [NR] RU(2 margin) of the group's ranges
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int n_r = (int)*P.d_nr;
@@ -577,6 +627,7 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
     if (blockIdx.x == 0 && threadIdx.x == 0) *P.d_ns = (unsigned long long)min(nseg_max, P.ns_cap);
 
     // ---- setup: barriers, TMEM, per-range constants, the resident range operand
+    TC_TR_CTA(30);
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
             tmbar_init(&full[s], 1);
@@ -596,20 +647,17 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     if (threadIdx.x < 16) sHsn[threadIdx.x] = threadIdx.x < P.nsp ? -__double2float_rn(0.5 * P.spos[threadIdx.x]) : 0.f;
+    for (int i = threadIdx.x; i < Cf::XQ; i += blockDim.x) sXSeq[i] = 0u;
+    if (threadIdx.x < 3) sXCtl[threadIdx.x] = 0u;
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *sTmem;
 
     if (warp == 0) {
-        // ================= producer: each (tile, chunk) stage as kCopyLanes bulk copies issued by
-        // different lanes.  In isolation copies from several threads overlap
-        // (scripts/micro/bulk_rate.cu), but inside the persistent kernel, with every SM streaming
-        // the pool from L2, one copy per stage is fastest (C3: 1.90 ms vs 1.93 with 2 lanes, 1.94
-        // with 4, 2.06 with 8)
-        constexpr int kCopyLanes = 1;
-        constexpr uint32_t PART = Cf::STAGE_BYTES / kCopyLanes;
-        static_assert(Cf::STAGE_BYTES % (16 * kCopyLanes) == 0, "bulk copies need 16-byte multiples");
+        // ================= producer: lane l < STAGES owns the stages s = l and issues their bulk
+        // copies, so STAGES copies are in flight at once
+        constexpr int kCopyLanes = STAGES;
         if (lane < kCopyLanes) {
             int i = 0;
             for (int k = 0; k < nseg; ++k) {
@@ -619,11 +667,12 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
             for (int tile = ta; tile < ta + ntl; ++tile) {  // tile by tile across the CTA's segments
                 for (int ch = 0; ch < CH; ++ch, ++i) {
                     const int s = i % STAGES;
+                    if (s != lane) continue;
                     if (i >= STAGES) tmbar_wait(&empty[s], (uint32_t)(((i / STAGES) + 1) & 1));
-                    if (lane == 0) tmbar_expect_tx(&full[s], Cf::STAGE_BYTES);
-                    __syncwarp((1u << kCopyLanes) - 1);  // expect_tx before any of the stage's copies lands
-                    tbulk_g2s(sA + s * Cf::STAGE_BYTES + lane * PART,
-                              P.Dtc + ((size_t)tile * CH + ch) * Cf::STAGE_BYTES + lane * PART, PART, &full[s]);
+                    tmbar_expect_tx(&full[s], Cf::STAGE_BYTES);
+                    TC_TR(0, i);
+                    tbulk_g2s(sA + s * Cf::STAGE_BYTES, P.Dtc + ((size_t)tile * CH + ch) * Cf::STAGE_BYTES,
+                              Cf::STAGE_BYTES, &full[s]);
                 }
             }
             }
@@ -656,7 +705,9 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
                 for (int ch = 0; ch < CH; ++ch, ++i) {
                     const int s = i % STAGES;
                     tmbar_wait(&full[s], (uint32_t)((i / STAGES) & 1));
+                    if (lane == 0) TC_TR(1, i);
                     if (ch == 0 && tl >= NBUF) tmbar_wait(&tempty[buf], (uint32_t)(((tl / NBUF) + 1) & 1));
+                    if (lane == 0 && ch == 0) TC_TR(2, tl);
                     tc_fence_after();
                     if (lane == 0) {
                         // K bytes kg of the tile: QR's q plane (kg < n) accumulates S_q at column 0
@@ -673,7 +724,7 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
                             tc_mma_i8(tmem + dcol, ad, bd, idesc, kp > 0 ? 1u : 0u);
                         }
                         tc_commit(&empty[s]);
-                        if (ch == CH - 1) tc_commit(&tfull[buf]);
+                        if (ch == CH - 1) { tc_commit(&tfull[buf]); TC_TR(3, tl); }
                     }
                     __syncwarp();
                 }
@@ -681,6 +732,91 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
             if (lane == 0) tc_commit(&bbar[Cf::BBUF + kb]);  // operand free once these MMAs complete
             __syncwarp();
         }
+    } else if (warp == Cf::XWARP) {
+        // ================= exact path, off the tile pipeline: the canonical binary64 score (C7)
+        // of every queued pair for every s > 0, then -- in queue order, one lane -- the
+        // lexicographic first-min update of the (range, domain lane) best and the CAS-min of the
+        // range's threshold.  The epilogue warps only push items, so a rare pair no longer
+        // stalls its warp (and through the two-buffer TMEM ring every warp) for ~1-2k cycles.
+        unsigned head = 0, n_items = 0;
+        volatile unsigned *vseq = sXSeq, *vctl = sXCtl;
+        for (;;) {
+            const unsigned idx = head + lane;
+            const bool ready = vseq[idx & (Cf::XQ - 1)] == idx + 1;
+            const unsigned rb = __ballot_sync(0xffffffffu, ready);
+            const int cnt = rb == 0xffffffffu ? 32 : __ffs(~rb) - 1;  // leading ready slots
+            if (cnt == 0) {
+                if (vctl[2] && vctl[1] == vctl[0]) break;
+                __nanosleep(64);
+                continue;
+            }
+            __threadfence_block();
+            double eb = INFINITY;
+            int32_t kjb = INT_MAX, qg = 0, mm = 0, dd = 0;
+            if (lane < cnt) {
+                const XItem it = sXQ[idx & (Cf::XQ - 1)];
+                qg = it.meta & 31;
+                const int ks = (it.meta >> 5) & 7;
+                mm = it.meta >> 8;
+                dd = it.d;
+                const TCRange &R = sR[qg];
+                const double Bq = __dsub_rn(__dmul_rn((double)n, (double)it.mx), __dmul_rn((double)R.SR, (double)it.sd));
+                const double c16 = __dmul_rn(0.0625, (double)__ldg(P.C + it.d));
+                for (int jj = 0; jj < P.nsp; ++jj) {
+                    const double sj = P.spos[jj];
+                    const double e = __dadd_rn(__dsub_rn(R.A, __dmul_rn(__dmul_rn(0.5, sj), Bq)),
+                                               __dmul_rn(__dmul_rn(sj, sj), c16));
+                    const int32_t kj = (ks << 8) | P.jpos[jj];
+                    if (e < eb || (e == eb && kj < kjb)) { eb = e; kjb = kj; }
+                }
+            }
+            // the (range, domain lane) best is a lexicographic minimum, so the updates commute:
+            // lanes with distinct slots update in parallel; a slot queued twice in one batch is
+            // first reduced to its lowest lane (rare)
+            const bool act = lane < cnt;
+            const unsigned key = act ? (unsigned)(qg * kTileD + mm) : (0x80000000u | (unsigned)lane);
+            const unsigned grp = __match_any_sync(0xffffffffu, key);
+            if (__any_sync(0xffffffffu, act && __popc(grp) > 1)) {
+                for (int i = 0; i < 32; ++i) {
+                    const double oe = __shfl_sync(0xffffffffu, eb, i);
+                    const int32_t od = __shfl_sync(0xffffffffu, dd, i);
+                    const int32_t okj = __shfl_sync(0xffffffffu, kjb, i);
+                    if (act && i != lane && ((grp >> i) & 1) &&
+                        (oe < eb || (oe == eb && (od < dd || (od == dd && okj < kjb))))) {
+                        eb = oe; dd = od; kjb = okj;
+                    }
+                }
+            }
+            if (act && __ffs(grp) - 1 == lane) {
+                Partial *bp = &sBest[key];
+                const Partial b = *bp;
+                if (eb < b.e || (eb == b.e && (dd < b.d || (dd == b.d && kjb < b.kj)))) {
+                    Partial nb;
+                    nb.e = eb; nb.d = dd; nb.kj = kjb;
+                    *bp = nb;
+                    const TCRange &R = sR[qg];
+                    const float t = fminf(__double2float_ru(__dadd_rn(__dsub_rn(eb, R.A), R.margin)), FLT_MAX);
+                    int *ti = reinterpret_cast<int *>(&sThr[qg]);
+                    int old = *ti;
+                    while (t < __int_as_float(old)) {
+                        const int prev = atomicCAS(ti, old, __float_as_int(t));
+                        if (prev == old) break;
+                        old = prev;
+                    }
+                }
+            }
+            head += cnt;
+            n_items += cnt;
+            __syncwarp();
+            if (lane == 0) {
+                __threadfence_block();
+                vctl[1] = head;  // the updates of items < head are visible
+            }
+        }
+        if (lane == 0 && n_items && P.exact_count) atomicAdd(P.exact_count, (unsigned long long)n_items);
+#ifdef FIC_TC_TRACE
+        if (lane == 0 && blockIdx.x < 4096) { g_tc_trace[28][blockIdx.x] = n_items; g_tc_trace[27][blockIdx.x] = nseg; }
+#endif
     } else {
         // ================= epilogue: lane = domain (TMEM lane), warpgroup = a quarter (third) of
         // the ranges; segment by segment (one range group each), tiles counted across segments
@@ -697,9 +833,7 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
         for (int jj = 0; jj < NT; ++jj) nhs[jj] = sHsn[jj] * kBqScale;
         static_assert(Cf::EWG <= 5, "named barriers 1..EWG (seeding) and 6 (segments) must not collide");
         auto epi_sync = [&]() { asm volatile("bar.sync 6, %0;" ::"r"(128 * Cf::EWG) : "memory"); };
-        unsigned n_exact = 0;
-        int qn = 0;
-        const int qbase = et * 4;
+        volatile unsigned *vctl = sXCtl;
         const int64_t t2row = P.n_slots;
         // fp32 filter score of one (range, domain) pair from the max over isometries of SRD_k
         auto score = [&](int mx, int rsr, int32_t sd, const float *t2) -> float {
@@ -746,12 +880,14 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
             // ---- segment setup: this group's range constants and thresholds (the previous
             // segment's readers of sR / sThr / sRed have passed the barrier)
             epi_sync();
+            if (et == 0) TC_TR_SEG(23, k);
             if (et < NR) {
                 const TCRange R = P.rmeta[r0 + et];
                 sR[et] = R;
                 sSR[et] = R.SR;
                 const float th = P.has_zero ? fminf(__double2float_ru(R.margin), FLT_MAX) : FLT_MAX;
                 sThr[et] = R.valid ? th : -FLT_MAX;
+                sM2[et] = fminf(__double2float_ru(2.0 * R.margin), FLT_MAX);
             }
             epi_sync();
             for (int q = 0; q < HALF; ++q) {
@@ -821,6 +957,7 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
                 }
                 asm volatile("bar.sync %0, 128;" ::"r"(1 + eg) : "memory");  // the warpgroup's seeds
             }
+            if (et == 0) TC_TR_SEG(24, k);
             for (int tt = 0; tt < ntl; ++tt, ++tl) {
                 const unsigned buf = tl % NBUF;
                 const int d = (ta + tt) * kTileD + m;
@@ -836,6 +973,7 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
                     for (int jj = 0; jj < NT; ++jj) t2_n[jj] = kIdx ? __ldg(P.t2f + (di + jj * t2r)) : __ldg(t2p + jj * t2row);
                 }
                 tmbar_wait_sa(tfull_sa + 8 * buf, (tl / NBUF) & 1);
+                if (warp == 2 && lane == 0) TC_TR(4, tl);
                 tc_fence_after();
                 const uint32_t tbase = tmem + ((uint32_t)(lq * 32) << 16) + buf * Cf::ACC + eg * HALF * 8;
                 // four ranges (32 columns) per tcgen05.ld, the next group in flight while one is scored
@@ -852,6 +990,8 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) tmbar_arrive_sa(tempty_sa + 8 * buf);
+                if (warp == 2 && lane == 0) TC_TR(5, tl);
+                if (lane == 0) TC_TR(8 + warp - 2, tl);
                 if constexpr (Cf::QR) {  // SRD_k = 4 S_q + S_r (exact: < 2^31)
 #pragma unroll
                     for (int i = 0; i < 32; ++i) vv[i] = 4u * vv[i] + vv[32 + i];
@@ -871,7 +1011,7 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
                         const float g0 = score(mx, B == 8 ? sSR[eg * HALF + q] : rSR[q], sd, t2);
                         pm |= (g0 <= sThr[eg * HALF + q]) ? (1u << q4) : 0u;
                     }
-                    if (pm) {  // queue (q, k*, max SRD) of the passing ranges for the exact path
+                    if (pm) {  // queue (range, domain, k*, max SRD) of the passing pairs for the exact warp
 #pragma unroll
                         for (int q4 = 0; q4 < 4; ++q4) {
                             if (pm >> q4 & 1) {
@@ -880,47 +1020,46 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
 #pragma unroll
                                 for (int k = 6; k >= 0; --k)
                                     if ((int)v[k] == mxs[q4]) ks = k;  // lowest index attaining the max
-                                sQ[qbase + qn] = make_int2((g * 4 + q4) | (ks << 8), mxs[q4]);
-                                ++qn;
+                                // tighten the range's threshold at once from the fp32 score (the
+                                // exact warp's own update, RU(e - A + margin), comes later): with
+                                // NSP > 0, g approximates min_{s > 0} e_s - A within the margin, so
+                                // e <= A + g + margin and RU(g + 2 margin) is a valid threshold
+                                // (NSP = 0: g is only a lower bound of the grid's minimum -- no)
+                                if constexpr (NSP > 0) {
+                                    const int q = g * 4 + q4;
+                                    const float g0 = score(mxs[q4], B == 8 ? sSR[eg * HALF + q] : rSR[q], sd, t2);
+                                    const float t = fminf(__fadd_ru(g0, sM2[eg * HALF + q]), FLT_MAX);
+                                    int *ti = reinterpret_cast<int *>(&sThr[eg * HALF + q]);
+                                    int old = *ti;
+                                    while (t < __int_as_float(old)) {
+                                        const int prev = atomicCAS(ti, old, __float_as_int(t));
+                                        if (prev == old) break;
+                                        old = prev;
+                                    }
+                                }
+                                const unsigned xi = atomicAdd(&sXCtl[0], 1u);
+                                while (xi - vctl[1] >= (unsigned)Cf::XQ) __nanosleep(32);  // ring full (rare)
+                                XItem it;
+                                it.mx = mxs[q4]; it.d = d; it.sd = sd;
+                                it.meta = (eg * HALF + g * 4 + q4) | (ks << 5) | (m << 8);
+                                sXQ[xi & (Cf::XQ - 1)] = it;
+                                __threadfence_block();
+                                reinterpret_cast<volatile unsigned *>(sXSeq)[xi & (Cf::XQ - 1)] = xi + 1;
                             }
                         }
                     }
-                    // ---- exact path (rare, one rolled copy): canonical binary64 score for every s > 0,
-                    // lexicographic first-min update of this lane's best, CAS-min of the shared threshold
-                    for (int i = 0; i < qn; ++i) {
-                        const int2 ent = sQ[qbase + i];
-                        const int q = ent.x & 255, ks = ent.x >> 8, mx = ent.y;
-                        const TCRange &R = sR[eg * HALF + q];
-                        Partial *bp = &sBest[(eg * HALF + q) * kTileD + m];
-                        const double Bq = __dsub_rn(__dmul_rn((double)n, (double)mx),
-                                                    __dmul_rn((double)R.SR, (double)sd));
-                        const double c16 = __dmul_rn(0.0625, (double)P.C[d]);
-                        double e0 = bp->e;
-                        int32_t d0 = bp->d, kj0 = bp->kj;
-                        for (int jj = 0; jj < P.nsp; ++jj) {
-                            const double sj = P.spos[jj];
-                            const double e = __dadd_rn(__dsub_rn(R.A, __dmul_rn(__dmul_rn(0.5, sj), Bq)),
-                                                       __dmul_rn(__dmul_rn(sj, sj), c16));
-                            const int32_t kj = (ks << 8) | P.jpos[jj];
-                            if (e < e0 || (e == e0 && (d < d0 || (d == d0 && kj < kj0)))) { e0 = e; d0 = d; kj0 = kj; }
-                        }
-                        bp->e = e0;
-                        bp->d = d0;
-                        bp->kj = kj0;
-                        const float t = fminf(__double2float_ru(__dadd_rn(__dsub_rn(e0, R.A), R.margin)), FLT_MAX);
-                        int *ti = reinterpret_cast<int *>(&sThr[eg * HALF + q]);
-                        int old = *ti;
-                        while (t < __int_as_float(old)) {
-                            const int prev = atomicCAS(ti, old, __float_as_int(t));
-                            if (prev == old) break;
-                            old = prev;
-                        }
-                    }
-                    n_exact += qn;
-                    qn = 0;
-                    __syncwarp();  // reconverge after the (rare, divergent) exact path
                 }
+                if (warp == 2 && lane == 0) TC_TR(6, tl);
+                if (warp == Cf::THREADS / 32 - 1 && lane == 0) TC_TR(7, tl);
             }
+            // ---- every queued pair of this segment has been scored by the exact warp
+            epi_sync();
+            if (et == 0) TC_TR_SEG(25, k);
+            if (et == 0)
+                while (vctl[1] != vctl[0]) __nanosleep(32);
+            epi_sync();
+            if (et == 0) TC_TR_SEG(26, k);
+            __threadfence_block();
             // ---- reduce each range's best over the 128 domain lanes (lexicographic); the HALF
             // shuffle chains interleaved (independent ranges)
             {
@@ -970,12 +1109,11 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
                 }
             }
         }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) n_exact += __shfl_xor_sync(0xffffffffu, n_exact, o);
-        if (lane == 0 && n_exact && P.exact_count) atomicAdd(P.exact_count, (unsigned long long)n_exact);
+        if (et == 0) vctl[2] = 1u;  // the exact warp may stop once the ring is empty
     }
     tc_fence_before();
     __syncthreads();
+    TC_TR_CTA(31);
     if (warp == 0) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
@@ -987,7 +1125,7 @@ static size_t tc_smem_bytes() {
     using Cf = TCfg<B>;
     return (size_t)Cf::STAGES * Cf::STAGE_BYTES + Cf::BBUF * Cf::B_BYTES + sizeof(TCRange) * Cf::NR + 4 * Cf::NR +
            4 * 16 + 4 * Cf::NR + sizeof(Partial) * Cf::NR * 4 + 8 * (2 * Cf::STAGES + 2 * Cf::NBUF + 4) + 16 +
-           sizeof(Partial) * Cf::NR * kTileD + sizeof(int2) * 128 * Cf::EWG * 4 + 1024;
+           sizeof(Partial) * Cf::NR * kTileD + (sizeof(XItem) + 4) * Cf::XQ + 16 + 4 * Cf::NR + 1024;
 }
 
 template <int B, int NSP>
@@ -1040,6 +1178,15 @@ static cudaError_t tc_range_prep(const SearchParams &sp, uint8_t *scratch, TCPar
     p.rmeta = meta;
     return cudaGetLastError();
 }
+
+#ifdef FIC_TC_TRACE
+extern "C" int fic_debug_tc_trace(long long *h_out) {  // [32][4096], then zeroed on the device
+    cudaError_t e = cudaMemcpyFromSymbol(h_out, g_tc_trace, sizeof(long long) * 32 * 4096);
+    static long long zero[32][4096];
+    if (e == cudaSuccess) e = cudaMemcpyToSymbol(g_tc_trace, zero, sizeof zero);
+    return (int)e;
+}
+#endif
 
 cudaError_t launch_tc_search(int32_t B, const SearchParams &sp, const uint8_t *Dtc, int64_t n_slots,
                              uint8_t *scratch, cudaStream_t st) {
