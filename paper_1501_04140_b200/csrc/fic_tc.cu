@@ -136,6 +136,22 @@ __device__ __forceinline__ void tc_mma_i8(uint32_t tmem_d, uint64_t adesc, uint6
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
         : "memory");
 }
+// the same, issued by the warp's elected lane: called by the whole (converged) warp, so the
+// operands stay warp-uniform and ptxas needs no per-lane waterfall to move them to uniform registers
+__device__ __forceinline__ void tc_mma_i8_elect(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                                uint32_t accum) {
+    asm volatile(
+        "{ .reg .pred p, e; setp.ne.b32 p, %4, 0; elect.sync _|e, 0xffffffff; "
+        "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p; }" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
+        : "memory");
+}
+__device__ __forceinline__ void tc_commit_elect(uint32_t bar_sa) {
+    asm volatile(
+        "{ .reg .pred e; elect.sync _|e, 0xffffffff; "
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0]; }" ::"r"(bar_sa)
+        : "memory");
+}
 __device__ __forceinline__ void tc_ld8(uint32_t taddr, uint32_t (&v)[8]) {
     asm volatile(
         "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
@@ -693,10 +709,13 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
         // ================= MMA issuer
         constexpr uint32_t idesc = idesc_i8(NN);
         int i = 0, tl = 0;
+        const uint32_t tmem_u = __shfl_sync(0xffffffffu, tmem, 0);
+        const uint32_t sA_sa = su32(sA), empty_sa = su32(empty), tfull_sa = su32(tfull);
         for (int k = 0; k < nseg; ++k) {
             int grp, ta, ntl, slot;
             bool lastseg;
             plan_segment(&plan, k, grp, ta, ntl, slot, lastseg);
+            ntl = __shfl_sync(0xffffffffu, ntl, 0);
             const int kb = k % Cf::BBUF;
             tmbar_wait(&bbar[kb], (uint32_t)((k / Cf::BBUF) & 1));
             const uint32_t bbase = su32(sB + kb * Cf::B_BYTES);
@@ -709,10 +728,11 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
                     if (ch == 0 && tl >= NBUF) tmbar_wait(&tempty[buf], (uint32_t)(((tl / NBUF) + 1) & 1));
                     if (lane == 0 && ch == 0) TC_TR(2, tl);
                     tc_fence_after();
-                    if (lane == 0) {
+                    {
                         // K bytes kg of the tile: QR's q plane (kg < n) accumulates S_q at column 0
-                        // of the buffer, its r plane S_r at column N, both against the same B rows
-                        const uint32_t a0 = su32(sA + s * Cf::STAGE_BYTES);
+                        // of the buffer, its r plane S_r at column N, both against the same B rows;
+                        // the whole warp runs this (uniform operands), one elected lane issues
+                        const uint32_t a0 = sA_sa + s * Cf::STAGE_BYTES;
 #pragma unroll
                         for (int kk = 0; kk < KCH / 32; ++kk) {
                             const int kg = ch * KCH + kk * 32;
@@ -721,16 +741,17 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
                             const uint32_t dcol = buf * Cf::ACC + plane * NN;
                             const uint64_t ad = smem_desc(a0 + kk * 256, 128, (KCH / 16) * 128);
                             const uint64_t bd = smem_desc(bbase + kp * 8, 128, (Cf::KB / 16) * 128);
-                            tc_mma_i8(tmem + dcol, ad, bd, idesc, kp > 0 ? 1u : 0u);
+                            tc_mma_i8_elect(tmem_u + dcol, ad, bd, idesc, kp > 0 ? 1u : 0u);
                         }
-                        tc_commit(&empty[s]);
-                        if (ch == CH - 1) { tc_commit(&tfull[buf]); TC_TR(3, tl); }
+                        tc_commit_elect(empty_sa + 8 * s);
+                        if (ch == CH - 1) {
+                            tc_commit_elect(tfull_sa + 8 * buf);
+                            if (lane == 0) TC_TR(3, tl);
+                        }
                     }
-                    __syncwarp();
                 }
             }
-            if (lane == 0) tc_commit(&bbar[Cf::BBUF + kb]);  // operand free once these MMAs complete
-            __syncwarp();
+            tc_commit_elect(su32(&bbar[Cf::BBUF + kb]));  // operand free once these MMAs complete
         }
     } else if (warp == Cf::XWARP) {
         // ================= exact path, off the tile pipeline: the canonical binary64 score (C7)
