@@ -233,9 +233,10 @@ fic_status t2f_enqueue(fic_ctx *ctx, Pool &P, const double *h_s, int32_t n_s, cu
     for (int j = 0; j < n_s; ++j)
         if (h_s[j] != 0.0) sl.s[nsp++] = h_s[j];
     const int64_t slots = P.n_tiles_max * fic::kTileD;
+    const fic::SGrid grid = fic::detect_sgrid(sl.s, nsp);
     CK(grow(ctx, P.b_t2f, sizeof(float) * (size_t)slots * (nsp ? nsp : 1)));
     CK(fic::launch_t2f(P.C, &P.d_misc[0], slots, sl, nsp, reinterpret_cast<float *>(P.b_t2f.p),
-                       (P.mode == 0 && nsp > 2) ? 1 : 0, P.mode == 0 ? fic::tc_t2_fold(P.B, nsp) : 0.f, st));
+                       nsp > 2 ? (grid.on ? 2 : 1) : 0, fic::tc_t2_fold(P.B, nsp), st, grid.h));
     if (nsp > 0 && slots > 0) ctx->launches += 1;
     P.t2f_ready = 1;
     return FIC_OK;
@@ -284,6 +285,7 @@ fic_status level_enqueue(fic_ctx *ctx, const Pool &P, const uint8_t *img, const 
     sp.tiles_per_split = (int32_t)((tiles + sp.nsplit - 1) / sp.nsplit);
     // both search kernels (tcgen05, B = 2) choose their split count on the device, up to ns_cap
     const bool dyn = true;
+    sp.grid = fic::detect_sgrid(sp.spos, sp.nsp);
     sp.b2_window = ctx->b2_window;
     sp.num_sms = ctx->num_sms;
     sp.L = P.L;
@@ -303,8 +305,7 @@ fic_status level_enqueue(fic_ctx *ctx, const Pool &P, const uint8_t *img, const 
     if (P.mode == 0) {
         if (!t2f_pre) {
             CK(fic::launch_t2f(P.C, &P.d_misc[0], slots, sl, sp.nsp, ptr<float>(ctx->b_t2f),
-                               (P.mode == 0 && sp.nsp > 2) ? 1 : 0,
-                               P.mode == 0 ? fic::tc_t2_fold(P.B, sp.nsp) : 0.f, st));
+                               sp.nsp > 2 ? (sp.grid.on ? 2 : 1) : 0, fic::tc_t2_fold(P.B, sp.nsp), st, sp.grid.h));
             if (sp.nsp > 0 && slots > 0) ctx->launches += 1;
         }
         if (ctx->timing) CK(cudaEventRecord(ctx->ev[level_slot][1], st));

@@ -164,6 +164,7 @@ struct B2Params {
     const int32_t *Cs;     // [n_slots] C (sorted)
     const int32_t *ds;     // [n_slots] kept-domain rank of each sorted position
     int32_t tw;
+    SGrid grid;  // uniform grid of the positive s: NP = 0 kernels, T = (RN(C/16), RN(2 / (C h)))
     const int32_t *kept;
     const unsigned long long *d_nr, *d_misc;  // device sizes: n_r; n_kept, Cmax
     int32_t nsplit;
@@ -189,10 +190,22 @@ constexpr int kB2Unroll = 4;
 
 // filter margin of one range (e units): |Bq| <= sqrt(A C); fp32 -hs and t2 roundings and one
 // FFMA -> 4u (hs |Bq| + t2)
-__device__ __forceinline__ double b2_margin(double A, double smax, double cmax) {
+__device__ __forceinline__ double b2_margin(double A, double smax, double cmax, bool grid = false) {
     const double u = 5.9604644775390625e-08;
     const double hs = 0.5 * smax, t2m = smax * smax * cmax * 0.0625;
-    return 4.0 * u * (hs * sqrt(A * cmax) * 1.01 + t2m) + 1e-12 * (A + t2m) + 1e-30;
+    // grid: g(s) = s (s RN(C/16) - bq/4) at fp32 grid points s = fma(j, h, a) -- the s rounding
+    // (and the 1e-12 grid fit), C/16, FFMA and FMUL roundings: <= ~6u (hs |Bq| + 2 t2)
+    return (grid ? 16.0 : 4.0) * u * (hs * sqrt(A * cmax) * 1.01 + t2m) + 1e-12 * (A + t2m) + 1e-30;
+}
+
+// fp32 score of the uniform grid's two points around s* = 4 Bq / C (bq = 2 Bq here): the pair
+// brackets the nearest grid point, so min of the two = min_j (e_j - A) within the margin
+__device__ __forceinline__ float b2_grid_g(const SGrid &G, float bq, float c16, float ug) {
+    const float x = fmaf(bq, ug, -G.aoh);
+    const float j0 = fminf(fmaxf(floorf(x), 0.f), (float)(G.K - 2));
+    const float s0 = fmaf(j0, G.h, G.a), s1 = s0 + G.h;
+    const float hb = -0.25f * bq;
+    return fminf(s0 * fmaf(s0, c16, hb), s1 * fmaf(s1, c16, hb));
 }
 
 __device__ __forceinline__ float2 b2_bc(float v) { return make_float2(v, v); }
@@ -217,7 +230,7 @@ __device__ __forceinline__ B2Range b2_range(int a, int b, int c, int d) {
 // margin, which only the per-s filter has.)
 template <int NP>
 __global__ void __launch_bounds__(kB2Threads, 3) b2scan_kernel(const __grid_constant__ B2Params P) {
-    constexpr int RPT = kB2RPT, NB = kB2NB, TW = 2 * NP;
+    constexpr int RPT = kB2RPT, NB = kB2NB, TW = NP == 0 ? 2 : 2 * NP;
     constexpr int TPS = NP == 1 ? 2 : 1;  // tiles per stage
     constexpr int SDOM = TPS * kTileD;    // domains per stage
     constexpr int NWARP = kB2Threads / 32;
@@ -274,7 +287,7 @@ __global__ void __launch_bounds__(kB2Threads, 3) b2scan_kernel(const __grid_cons
         else { X[q / 2].x = R.x2; SX[q / 2].x = R.sx; DX[q / 2].x = R.dx; }
         gm[q] = INFINITY;
     }
-    float2 nh[NP];  // -(s_j / 4) (times 2 max Bq); zero on pads (t2 = +inf there)
+    float2 nh[NP == 0 ? 1 : NP];  // -(s_j / 4) (times 2 max Bq); zero on pads (t2 = +inf there)
 #pragma unroll
     for (int jp = 0; jp < NP; ++jp) {
         nh[jp].x = 2 * jp < P.nsp ? P.nhs[2 * jp] : 0.f;
@@ -290,14 +303,26 @@ __global__ void __launch_bounds__(kB2Threads, 3) b2scan_kernel(const __grid_cons
 #pragma unroll kB2Unroll
         for (int dl = 0; dl < nd; ++dl) {
             const float4 f = Fb[dl];
-            float2 t2[NP];
+            float2 t2[NP == 0 ? 1 : NP];
 #pragma unroll
-            for (int jp = 0; jp < NP; ++jp) t2[jp] = reinterpret_cast<const float2 *>(Tb + dl * TW)[jp];
+            for (int jp = 0; jp < (NP == 0 ? 1 : NP); ++jp) t2[jp] = reinterpret_cast<const float2 *>(Tb + dl * TW)[jp];
 #pragma unroll
             for (int p = 0; p < RPT / 2; ++p) {
                 float2 Q = __fmul2_rn(DX[p], b2_bc(f.z));
                 Q = __ffma2_rn(X[p], b2_bc(f.x), Q);
                 const float2 bq = __ffma2_rn(SX[p], b2_bc(f.y), make_float2(fabsf(Q.x), fabsf(Q.y)));
+                if constexpr (NP == 0) {  // uniform grid: the two points around s*, packed over the range pair
+                    const float2 x = __ffma2_rn(bq, b2_bc(t2[0].y), b2_bc(-P.grid.aoh));
+                    const float jx = fminf(fmaxf(floorf(x.x), 0.f), (float)(P.grid.K - 2));
+                    const float jy = fminf(fmaxf(floorf(x.y), 0.f), (float)(P.grid.K - 2));
+                    const float2 s0 = __ffma2_rn(make_float2(jx, jy), b2_bc(P.grid.h), b2_bc(P.grid.a));
+                    const float2 s1 = __fadd2_rn(s0, b2_bc(P.grid.h));
+                    const float2 hb = __fmul2_rn(bq, b2_bc(-0.25f));
+                    const float2 g0 = __fmul2_rn(s0, __ffma2_rn(s0, b2_bc(t2[0].x), hb));
+                    const float2 g1 = __fmul2_rn(s1, __ffma2_rn(s1, b2_bc(t2[0].x), hb));
+                    gm[2 * p] = fminf(gm[2 * p], fminf(g0.x, g1.x));
+                    gm[2 * p + 1] = fminf(gm[2 * p + 1], fminf(g0.y, g1.y));
+                }
 #pragma unroll
                 for (int jp = 0; jp < NP; ++jp) {
                     const float2 g0 = __ffma2_rn(nh[jp], b2_bc(bq.x), t2[jp]);
@@ -391,7 +416,7 @@ __global__ void __launch_bounds__(256) b2exact_kernel(const __grid_constant__ B2
     const uint8_t *p0 = P.img + (size_t)rr.y * P.N + rr.x;
     const B2Range R = b2_range(p0[0], p0[1], p0[P.N + 1], p0[P.N]);
     const double A = (double)R.A;
-    const double margin = b2_margin(A, P.smax, cmax);
+    const double margin = b2_margin(A, P.smax, cmax, P.grid.on != 0);
     float gmn = INFINITY;
     for (int i = lane; i < ns; i += 32) gmn = fminf(gmn, P.gmin[(size_t)r * P.ns_cap + i]);
 #pragma unroll
@@ -414,7 +439,9 @@ __global__ void __launch_bounds__(256) b2exact_kernel(const __grid_constant__ B2
             const float4 f = P.F[pos];
             const float bq = fmaf(R.sx, f.y, fabsf(fmaf(R.x2, f.x, R.dx * f.z)));
             float g = INFINITY;
-            for (int jj = 0; jj < P.nsp; ++jj) g = fminf(g, fmaf(P.nhs[jj], bq, P.T[pos * P.tw + jj]));
+            if (P.grid.on) g = b2_grid_g(P.grid, bq, P.T[pos * 2], P.T[pos * 2 + 1]);
+            else
+                for (int jj = 0; jj < P.nsp; ++jj) g = fminf(g, fmaf(P.nhs[jj], bq, P.T[pos * P.tw + jj]));
             if (g <= thr) {
                 ++n_exact;
                 const int32_t d = P.ds[pos];
@@ -719,12 +746,19 @@ __global__ void __launch_bounds__(256, 6) b2win_kernel(const __grid_constant__ B
 
 // t2_j per slot, [slot][tw]; +inf on pad slots and pad j
 __global__ void b2_t2_kernel(const float4 *__restrict__ F, const unsigned long long *__restrict__ d_nk,
-                             int64_t n_slots, const SList spos, int32_t nsp, int32_t tw, float *__restrict__ T) {
+                             int64_t n_slots, const SList spos, int32_t nsp, int32_t tw, float *__restrict__ T,
+                             float grid_h) {
     const int64_t d = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (d >= n_slots) return;
     const int64_t n_k = (int64_t)*d_nk;
     if (d >= ((n_k + kTileD - 1) / kTileD) * kTileD) return;
     const double c16 = __dmul_rn(0.0625, (double)F[d].w);  // C (exact in fp32, < 2^23)
+    if (grid_h > 0.f) {  // uniform grid: RN(C/16) (+inf on pads), RN(2 / (C h)) (bq = 2 Bq)
+        const double C = (double)F[d].w;
+        T[d * 2] = d < n_k ? __double2float_rn(c16) : INFINITY;
+        T[d * 2 + 1] = (d < n_k && C > 0.0) ? __double2float_rn(2.0 / (C * (double)grid_h)) : 0.f;
+        return;
+    }
     for (int j = 0; j < tw; ++j) {
         const double s = j < nsp ? spos.s[j] : 0.0;
         T[d * tw + j] = (d < n_k && j < nsp) ? __double2float_rn(__dmul_rn(__dmul_rn(s, s), c16)) : INFINITY;
@@ -734,7 +768,7 @@ __global__ void b2_t2_kernel(const float4 *__restrict__ F, const unsigned long l
 template <int NP>
 static size_t b2_smem() {
     constexpr int TPS = NP == 1 ? 2 : 1;
-    return (size_t)kB2NB * TPS * kTileD * (16 + 8 * NP) + kB2NB * 12 + 64;
+    return (size_t)kB2NB * TPS * kTileD * (16 + 8 * (NP == 0 ? 1 : NP)) + kB2NB * 12 + 64;
 }
 
 template <int NP>
@@ -762,7 +796,7 @@ int b2_nsplit_hint(int64_t n_r, int64_t n_tiles, int num_sms) {
     return (int)ns;
 }
 
-int b2_t2_width(int32_t nsp) { return nsp <= 2 ? 2 : (nsp <= 16 ? 16 : 32); }
+int b2_t2_width(int32_t nsp) { return nsp <= 2 ? 2 : (nsp <= 16 ? 16 : 32); }  // (a grid uses 2 of them)
 
 size_t b2_scratch_bytes(int64_t n_r, int32_t ns_cap) { return 64 + sizeof(float) * (size_t)n_r * ns_cap; }
 
@@ -770,13 +804,15 @@ cudaError_t launch_b2_search(const SearchParams &sp, const B2Pool &bp, float *T,
                              int32_t L, int32_t A, void *scratch, unsigned long long *scan_count,
                              cudaStream_t st) {
     if (sp.n_r == 0 || sp.nsp == 0) return cudaSuccess;
-    const int tw = b2_t2_width(sp.nsp);
+    const bool grid = sp.grid.on && !(sp.b2_window && !sp.has_zero && sp.nsp <= 2);
+    const int tw = grid ? 2 : b2_t2_width(sp.nsp);
     const int64_t slots = sp.slot_stride;
     SList sl;
     memcpy(sl.s, sp.spos, sizeof sl.s);
     const bool win = sp.b2_window && !sp.has_zero && sp.nsp <= 2;  // predefined s: C windows
     if (slots > 0 && !win) {  // (b2win forms t2 from the feature's C itself)
-        b2_t2_kernel<<<(unsigned)((slots + 255) / 256), 256, 0, st>>>(bp.F, &sp.d_misc[0], slots, sl, sp.nsp, tw, T);
+        b2_t2_kernel<<<(unsigned)((slots + 255) / 256), 256, 0, st>>>(bp.F, &sp.d_misc[0], slots, sl, sp.nsp, tw, T,
+                                                                      grid ? sp.grid.h : 0.f);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }
@@ -791,6 +827,8 @@ cudaError_t launch_b2_search(const SearchParams &sp, const B2Pool &bp, float *T,
     for (int j = 0; j < kMaxS; ++j) p.nhs[j] = j < sp.nsp ? -(float)(0.25 * sp.spos[j]) : 0.f;
     p.has_zero = sp.has_zero; p.j_zero = sp.j_zero;
     p.smax = sp.smax;
+    p.grid = sp.grid;
+    p.grid.on = grid ? 1 : 0;
     p.part = sp.part; p.exact_count = sp.exact_count; p.scan_count = scan_count;
     p.d_nscan = reinterpret_cast<unsigned long long *>(scratch);
     p.gmin = reinterpret_cast<float *>(static_cast<char *>(scratch) + 64);
@@ -798,7 +836,8 @@ cudaError_t launch_b2_search(const SearchParams &sp, const B2Pool &bp, float *T,
         b2win_kernel<<<(unsigned)((sp.n_r + 7) / 8), 256, 0, st>>>(p);
         return cudaGetLastError();
     }
-    cudaError_t e = tw == 2 ? launch_b2_scan<1>(p, st) : tw == 16 ? launch_b2_scan<8>(p, st) : launch_b2_scan<16>(p, st);
+    cudaError_t e = grid ? launch_b2_scan<0>(p, st)
+                         : tw == 2 ? launch_b2_scan<1>(p, st) : tw == 16 ? launch_b2_scan<8>(p, st) : launch_b2_scan<16>(p, st);
     if (e != cudaSuccess) return e;
     b2exact_kernel<<<(unsigned)((sp.n_r + 7) / 8), 256, 0, st>>>(p);
     return cudaGetLastError();

@@ -10,6 +10,7 @@
 #include <stdint.h>
 
 #include <atomic>
+#include <cmath>
 #include <string>
 
 #include "fic.h"
@@ -67,6 +68,31 @@ struct Partial {
     int32_t kj;  // iso | (s_idx << 8)
 };
 
+// A level's positive s values that form a uniform grid s_j = a + j h (j = 0..K-1, K >= 3, up to
+// 1e-12 relative): the 16-value grid, sampled10 and the 5-bit closed-form levels.  The fp32
+// filter then scores only the two grid points around s* = 4 Bq / C (the parabola's vertex,
+// Eq. 2), which bracket the nearest one -- a tight estimate of the minimum over the whole set
+// (not just a lower bound), so threshold seeding works as for the predefined sets.
+struct SGrid {
+    int32_t on;   // 0: not a uniform grid
+    int32_t K;
+    float a, h, aoh;  // a, h and a / h as fp32
+};
+inline SGrid detect_sgrid(const double *spos, int nsp) {
+    SGrid g;
+    g.on = 0; g.K = nsp; g.a = g.h = g.aoh = 0.f;
+    if (nsp < 3) return g;
+    const double a = spos[0], h = (spos[nsp - 1] - spos[0]) / (double)(nsp - 1);
+    if (!(h > 0.0)) return g;
+    for (int j = 0; j < nsp; ++j) {
+        const double v = a + (double)j * h;
+        if (!(fabs(spos[j] - v) <= 1e-12 * (fabs(spos[j]) + 1e-300))) return g;
+    }
+    g.on = 1;
+    g.a = (float)a; g.h = (float)h; g.aoh = (float)(a / h);
+    return g;
+}
+
 // Level sizes live on the device (no host round trip between levels): n_r = *d_nr,
 // n_kept = d_misc[0], Cmax = d_misc[1]; host fields n_r / n_tiles are UPPER BOUNDS used only
 // to size grids and buffers; a CTA's domain tiles are [split nt / nsplit, (split+1) nt / nsplit).
@@ -97,6 +123,7 @@ struct SearchParams {
     int32_t L, Acnt;             // domain step and candidates per axis (threshold seeding)
     const int32_t *kept;         // kept-domain candidate indices
     int32_t num_sms;             // SMs of the context's device (persistent grids)
+    SGrid grid;                  // the positive s form a uniform grid (nsp > 2)
 };
 
 struct FinalizeParams {
@@ -229,8 +256,11 @@ cudaError_t launch_pool_moments(const uint8_t *img, int32_t N, int32_t B, int32_
 struct SList {
     double s[kMaxS];
 };
+
+// univ: 0 one row per s (t2_j = s_j^2 C / 16, `fold` folds the magic constant), 1 the
+// s-independent filter (RN(1/C)), 2 uniform grid (rows RN(C / 16), RN(4 / (C h)))
 cudaError_t launch_t2f(const int64_t *C, const unsigned long long *d_nk, int64_t n_slots, const SList &spos,
-                       int32_t nsp, float *t2f, int32_t univ, float fold, cudaStream_t st);
+                       int32_t nsp, float *t2f, int32_t univ, float fold, cudaStream_t st, float grid_h = 0.f);
 cudaError_t launch_finalize(const FinalizeParams &p, cudaStream_t st);
 cudaError_t launch_merge_shards(const fic_record *in, const int64_t *d_counts, int32_t n_shards,
                                 int64_t stride, int64_t max_count, fic_record *out, cudaStream_t st);

@@ -402,11 +402,16 @@ cudaError_t launch_pool_moments(const uint8_t *img, int32_t N, int32_t B, int32_
 // no subtraction of the magic constant (the extra rounding is in the filter margin)
 __global__ void t2f_kernel(const int64_t *__restrict__ C, const unsigned long long *__restrict__ d_nk,
                            int64_t n_slots, const SList spos, int32_t nsp, float *__restrict__ t2f, int32_t univ,
-                           float fold) {
+                           float fold, float grid_h) {
     const int64_t d = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (d >= n_slots) return;
     const int64_t n_k = (int64_t)*d_nk;
     if (d >= ((n_k + kTileD - 1) / kTileD) * kTileD) return;
+    if (univ == 2) {  // uniform grid: RN(C / 16) (+inf on pads: never passes), RN(4 / (C h))
+        t2f[d] = d < n_k ? __double2float_rn(__dmul_rn(0.0625, (double)C[d])) : INFINITY;
+        t2f[n_slots + d] = (d < n_k && C[d] > 0) ? __double2float_rn(4.0 / ((double)C[d] * (double)grid_h)) : 0.f;
+        return;
+    }
     if (univ) {
         t2f[d] = d < n_k ? (C[d] > 0 ? __double2float_rn(1.0 / (double)C[d]) : 0.f) : __int_as_float(0x7fc00000);
         return;
@@ -424,9 +429,9 @@ __global__ void t2f_kernel(const int64_t *__restrict__ C, const unsigned long lo
 }
 
 cudaError_t launch_t2f(const int64_t *C, const unsigned long long *d_nk, int64_t n_slots, const SList &spos,
-                       int32_t nsp, float *t2f, int32_t univ, float fold, cudaStream_t st) {
+                       int32_t nsp, float *t2f, int32_t univ, float fold, cudaStream_t st, float grid_h) {
     if (n_slots == 0 || nsp == 0) return cudaSuccess;
-    t2f_kernel<<<(unsigned)((n_slots + 255) / 256), 256, 0, st>>>(C, d_nk, n_slots, spos, nsp, t2f, univ, fold);
+    t2f_kernel<<<(unsigned)((n_slots + 255) / 256), 256, 0, st>>>(C, d_nk, n_slots, spos, nsp, t2f, univ, fold, grid_h);
     return cudaGetLastError();
 }
 

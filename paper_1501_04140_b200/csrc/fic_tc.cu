@@ -50,7 +50,13 @@ struct TCfg {
     static constexpr int KB = QR ? n : KP;                 // B operand K bytes per (range, k) row
     // ranges per CTA: 8 per epilogue warp per tile; B = 4 uses 3 epilogue warpgroups (14 warps,
     // at most 4 per SM sub-partition, so 128 registers per thread instead of 96 with 18 warps)
-    static constexpr int NR = (B == 16) ? 16 : (B == 4 ? 24 : 32);
+#ifndef FIC_B4_NR
+#define FIC_B4_NR 24
+#endif
+#ifndef FIC_B4_EWG
+#define FIC_B4_EWG 3
+#endif
+    static constexpr int NR = (B == 16) ? 16 : (B == 4 ? FIC_B4_NR : 32);
     static constexpr int N = 8 * NR;                       // MMA N (columns per accumulator)
     static constexpr int KCH = QR ? 512 : (KP < 256 ? KP : 256);  // K bytes per pipeline stage
     static constexpr int CH = KP / KCH;                    // stages per domain tile
@@ -63,7 +69,7 @@ struct TCfg {
     static constexpr int BBUF = B == 4 ? 2 : 1;
     static constexpr int ACC = QR ? 2 * N : N;             // TMEM columns per accumulator buffer
     static constexpr int NBUF = 512 / ACC >= 4 ? 4 : 2;    // TMEM accumulator buffers (MMA <-> epilogue)
-    static constexpr int EWG = B == 4 ? 3 : 4;            // epilogue warpgroups
+    static constexpr int EWG = B == 4 ? FIC_B4_EWG : 4;   // epilogue warpgroups
     // warps: producer, MMA issuer, 4 EWG epilogue warps, the exact-path warp
     static constexpr int XWARP = 2 + 4 * EWG;
     static constexpr int THREADS = 64 + 128 * EWG + 32;
@@ -158,8 +164,9 @@ __device__ __forceinline__ void tc_ld8(uint32_t taddr, uint32_t (&v)[8]) {
         : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
         : "r"(taddr));
 }
-template <int O>
-__device__ __forceinline__ void tc_ld32(uint32_t taddr, uint32_t (&w)[64]) {
+template <int O, int W>
+__device__ __forceinline__ void tc_ld32(uint32_t taddr, uint32_t (&w)[W]) {
+    static_assert(O + 32 <= W, "tcgen05.ld destination");
     uint32_t *v = w + O;
     asm volatile(
         "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
@@ -464,7 +471,12 @@ __device__ __forceinline__ void tc_range_meta_body(const uint8_t *__restrict__ i
     // folded magic constant (B <= 8): t2' = RN(t2 - nhs M) adds u |t2 - nhs M| <= u (t2m + hs k M)
     if (B <= 8) R.margin += 2.0 * u * (t2m + hs * (B == 2 ? 1.0 : (B == 4 ? 2.0 : 64.0)) * 12582912.0);
     // s-independent filter (NSP = 0): Bq rounded once, squared, times RN(1/C): <= 4.04u Bq^2/C <= 4.04u A
-    if (univ) R.margin = 4.1 * u * R.A + 1e-12 * R.A + 1e-30;
+    if (univ == 1) R.margin = 4.1 * u * R.A + 1e-12 * R.A + 1e-30;
+    // uniform grid (NSP = 3): g(s) = s (s RN(C/16) - Bq/2) at two fp32 grid points s = fma(j, h, a):
+    // Bq RN conversion, s rounding (incl. the 1e-12 grid fit), C/16 rounding, the FFMA and the
+    // FMUL: |error| <= ~6u (hs |Bq| + 2 t2) -> 16u (hs |Bq|max + t2max)
+    if (univ == 2)
+        R.margin = 16.0 * u * (hs * bq + t2m) + 1e-12 * (R.A + hs * bq + t2m) + 1e-30;
     meta[r] = R;
 }
 
@@ -544,6 +556,7 @@ struct TCParams {
     unsigned long long *exact_count;
     int32_t lockstep;  // full rounds in lockstep (pool larger than ~L2/2), else all flattened
     int32_t num_sms;
+    SGrid grid;        // NSP = 3: the positive s are the uniform grid a + j h, j < K
 };
 
 using TCRange = TCRangeG;
@@ -759,7 +772,7 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
         // lexicographic first-min update of the (range, domain lane) best and the CAS-min of the
         // range's threshold.  The epilogue warps only push items, so a rare pair no longer
         // stalls its warp (and through the two-buffer TMEM ring every warp) for ~1-2k cycles.
-        unsigned head = 0, n_items = 0;
+        unsigned head = 0, n_items = 0, idle_ns = 128;
         volatile unsigned *vseq = sXSeq, *vctl = sXCtl;
         for (;;) {
             const unsigned idx = head + lane;
@@ -768,9 +781,13 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
             const int cnt = rb == 0xffffffffu ? 32 : __ffs(~rb) - 1;  // leading ready slots
             if (cnt == 0) {
                 if (vctl[2] && vctl[1] == vctl[0]) break;
-                __nanosleep(64);
+                // idle: back off (items are rare; every poll takes issue slots from the epilogue
+                // warps of this SMSP, which pace the whole TMEM ring)
+                __nanosleep(idle_ns);
+                idle_ns = min(idle_ns * 2, 2048u);
                 continue;
             }
+            idle_ns = 128;
             __threadfence_block();
             double eb = INFINITY;
             int32_t kjb = INT_MAX, qg = 0, mm = 0, dd = 0;
@@ -845,7 +862,8 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
         const int lq = warp & 3;          // TMEM lane quarter accessible by this warp
         const int m = lq * 32 + lane;     // domain lane within the tile
         const int et = threadIdx.x - 64;  // epilogue thread
-        constexpr int NT = NSP ? NSP : 1;  // t2 values per domain (u = 1/C for NSP = 0)
+        // t2f rows per domain: one per s (NSP 1, 2); u = RN(1/C) (NSP 0); RN(C/16), RN(4/(C h)) (grid)
+        constexpr int NT = NSP == 3 ? 2 : (NSP ? NSP : 1);
         float nhs[NT];
 #pragma unroll
         // the B = 4 / 8 conversions below yield Bq / 2 and Bq / 64: fold the power of two into -s/2
@@ -859,7 +877,11 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
         // fp32 filter score of one (range, domain) pair from the max over isometries of SRD_k
         auto score = [&](int mx, int rsr, int32_t sd, const float *t2) -> float {
             float bq;
-            if constexpr (NSP == 0 && B <= 8) {
+            if constexpr (NSP == 3 && B <= 8) {
+                bq = (float)(n * mx - rsr * sd);  // exact int32 Bq, one RN conversion
+            } else if constexpr (NSP == 3) {
+                bq = (float)((long long)n * mx - (long long)rsr * sd);
+            } else if constexpr (NSP == 0 && B <= 8) {
                 // exact Bq in int32 (|n SRD|, |SR SD| <= 1.06e9 at B = 8), one RN conversion
                 bq = (float)(n * mx - rsr * sd);
             } else if constexpr (NSP == 0) {
@@ -879,7 +901,17 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
                 bq = fmaf((float)n, (float)mx, -((float)rsr * (float)sd));
             }
             float g0;
-            if constexpr (NSP == 0) {
+            if constexpr (NSP == 3) {
+                // the two grid points around s* = 4 Bq / C: x = (s* - a) / h, j0 = clamp(floor x)
+                const float x = fmaf(bq, t2[1], -P.grid.aoh);
+                const float j0 = fminf(fmaxf(floorf(x), 0.f), (float)(P.grid.K - 2));
+                const float s0 = fmaf(j0, P.grid.h, P.grid.a);
+                const float2 sv = make_float2(s0, s0 + P.grid.h);
+                const float hb = -0.5f * bq;
+                const float2 tt = __ffma2_rn(sv, make_float2(t2[0], t2[0]), make_float2(hb, hb));
+                const float2 g2 = __fmul2_rn(sv, tt);  // s (s C/16 - Bq/2) = e_s - A
+                g0 = fminf(g2.x, g2.y);
+            } else if constexpr (NSP == 0) {
                 g0 = -(bq * bq) * t2[0];  // >= -(Bq^2 / C)(1 + 4.04u): continuous minimum
             } else if constexpr (NSP == 2) {  // both s in one packed FFMA2 (the same two roundings)
                 const float2 g2 = __ffma2_rn(make_float2(nhs[0], nhs[1]), make_float2(bq, bq), make_float2(t2[0], t2[1]));
@@ -979,6 +1011,11 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
                 asm volatile("bar.sync %0, 128;" ::"r"(1 + eg) : "memory");  // the warpgroup's seeds
             }
             if (et == 0) TC_TR_SEG(24, k);
+#ifdef FIC_EPI_UNROLL
+#define FIC_STR_(x) #x
+#define FIC_PRAGMA_(x) _Pragma(FIC_STR_(x))
+            FIC_PRAGMA_(unroll FIC_EPI_UNROLL)
+#endif
             for (int tt = 0; tt < ntl; ++tt, ++tl) {
                 const unsigned buf = tl % NBUF;
                 const int d = (ta + tt) * kTileD + m;
@@ -999,14 +1036,16 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
                 const uint32_t tbase = tmem + ((uint32_t)(lq * 32) << 16) + buf * Cf::ACC + eg * HALF * 8;
                 // four ranges (32 columns) per tcgen05.ld, the next group in flight while one is scored
                 constexpr int G = HALF / 4;
-                uint32_t vv[64];
+                uint32_t vv[Cf::QR ? 64 : G * 32];
                 // the tile's accumulators (<= 2 groups of 4 ranges, or QR's two planes) into
                 // registers, then the buffer goes straight back to the MMA warp: the next MMA into
                 // it overlaps this tile's scoring
-                static_assert(G <= 2 && (!Cf::QR || G == 1), "one tile's accumulators fit vv[64]");
+                static_assert(G <= 4 && (!Cf::QR || G == 1), "one tile's accumulators fit vv");
                 tc_ld32<0>(tbase, vv);
                 if constexpr (Cf::QR) tc_ld32<32>(tbase + NN, vv);
-                else if constexpr (G == 2) tc_ld32<32>(tbase + 32, vv);
+                if constexpr (!Cf::QR && G >= 2) tc_ld32<32>(tbase + 32, vv);
+                if constexpr (!Cf::QR && G >= 3) tc_ld32<64>(tbase + 64, vv);
+                if constexpr (!Cf::QR && G >= 4) tc_ld32<96>(tbase + 96, vv);
                 tc_wait_ld();
                 tc_fence_before();
                 __syncwarp();
@@ -1024,7 +1063,7 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
 #pragma unroll
                     for (int q4 = 0; q4 < 4; ++q4) {  // branch-free filter of four ranges
                         const int q = g * 4 + q4;
-                        const uint32_t *v = vv + (g & 1) * 32 + q4 * 8;
+                        const uint32_t *v = vv + g * 32 + q4 * 8;
                         const int mx = max(__vimax3_s32((int)v[0], (int)v[1], (int)v[2]),
                                            __vimax3_s32((int)v[3], (int)v[4], __vimax3_s32((int)v[5], (int)v[6], (int)v[7])));
                         mxs[q4] = mx;
@@ -1036,7 +1075,7 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
 #pragma unroll
                         for (int q4 = 0; q4 < 4; ++q4) {
                             if (pm >> q4 & 1) {
-                                const uint32_t *v = vv + (g & 1) * 32 + q4 * 8;
+                                const uint32_t *v = vv + g * 32 + q4 * 8;
                                 int ks = 7;
 #pragma unroll
                                 for (int k = 6; k >= 0; --k)
@@ -1168,10 +1207,11 @@ template <int B>
 static cudaError_t launch_tc_b(const TCParams &p, cudaStream_t st) {
     if (p.nsp <= 1) return launch_tc_t<B, 1>(p, st);
     if (p.nsp <= 2) return launch_tc_t<B, 2>(p, st);
+    if (p.grid.on) return launch_tc_t<B, 3>(p, st);
     return launch_tc_t<B, 0>(p, st);
 }
 
-int tc_ranges_per_cta(int B) { return B == 16 ? 16 : (B == 4 ? 24 : 32); }
+int tc_ranges_per_cta(int B) { return B == 16 ? TCfg<16>::NR : (B == 4 ? TCfg<4>::NR : TCfg<8>::NR); }
 
 size_t tc_range_bytes(int B, int64_t n_r) {
     switch (B) {
@@ -1194,7 +1234,7 @@ static cudaError_t tc_range_prep(const SearchParams &sp, uint8_t *scratch, TCPar
     const int nb_op = (int)((total16 + 255) / 256), nb_meta = (int)((meta_threads + 255) / 256);
     tc_range_prep_kernel<B><<<(unsigned)(nb_op + nb_meta), 256, 0, st>>>(sp.img, sp.N, sp.ranges, sp.d_nr, total16,
                                                                         Bop, nb_op, n_pad, sp.smax, sp.d_misc, meta,
-                                                                        sp.nsp > 2 ? 1 : 0);
+                                                                        sp.nsp > 2 ? (sp.grid.on ? 2 : 1) : 0);
     p.Bop = Bop;
     p.rmeta = meta;
     return cudaGetLastError();
@@ -1233,6 +1273,7 @@ cudaError_t launch_tc_search(int32_t B, const SearchParams &sp, const uint8_t *D
     p.smax = sp.smax;
     p.part = sp.part; p.exact_count = sp.exact_count;
     p.num_sms = sp.num_sms;
+    p.grid = sp.grid;
     p.lockstep = tc_pool_bytes(B, (n_slots + kTileD - 1) / kTileD) > ((size_t)48 << 20) ? 1 : 0;
     if (const char *e = getenv("FIC_TC_LOCKSTEP")) p.lockstep = atoi(e) != 0;  // test hook
     switch (B) {

@@ -1,0 +1,11 @@
+#!/bin/bash
+# GPU box: quick C3 bench of the default build and of each abvar/*.so (FIC_SO), same box
+for so in default abvar/*.so; do
+  if [ "$so" = default ]; then unset FIC_SO; else export FIC_SO=$PWD/$so; fi
+  timeout 300 python bench.py --no-cpu-baseline --no-e2e --steps ${STEPS:-30} "$@" > gpurun_out/ab.log 2>&1 || { echo "$so failed"; tail -5 gpurun_out/ab.log; continue; }
+  python - "$so" <<'PY'
+import json, sys
+d = json.loads(open("gpurun_out/ab.log").read().strip().splitlines()[-1])
+print("%-22s ms/encode %.4f " % (sys.argv[1], d["ms_per_step"]) + " ".join("B%d %.4f" % (l["B"], l["ms_search"]) for l in d["levels"]))
+PY
+done
