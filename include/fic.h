@@ -88,7 +88,8 @@ fic_status fic_get_stats(const fic_ctx *ctx, fic_level_stats *h_out, int32_t max
  *   candidates: 2B x 2B blocks at (x, y) = (aL, bL), x + 2B <= N, y + 2B <= N, row-major;
  *   entropy key of the raw block, keep iff tau < 0 or H > tau (nats, strict) [R3-R6];
  *   kept blocks decimated by 2x2 sums (D' = 4d) [R1] and their moments.
- * img: device [N*N]; B in {2,4,8,16,32}; L >= 1; 2B <= N.
+ * img: device [N*N]; B in {2,4,8,16,32} (B = 2 closed form on CUDA cores, 4..32 tcgen05);
+ * L >= 1; 2B <= N.
  * Errors: ARG, SHAPE, EMPTY_POOL (the pool is still returned for inspection), CUDA, NOMEM.
  * Synchronises the ctx stream (the kept count is returned on the host). */
 fic_status fic_build_domain_pool(fic_ctx *ctx, const uint8_t *img, int32_t N, int32_t B,

@@ -203,8 +203,7 @@ void pool_take_counts(Pool &P, const unsigned long long *h) {
 
 fic_status check_level(fic_ctx *ctx, int32_t N, int32_t B, int32_t L) {
     if (!pow2(B) || B < 2) return fail(ctx, FIC_ERR_ARG, "B must be a power of two >= 2");
-    if (B > 16)
-        return fail(ctx, FIC_ERR_ARG, "B > 16 is not supported by the CUDA search kernel yet");
+    if (B > 32) return fail(ctx, FIC_ERR_ARG, "B must be <= 32");
     if (L < 1) return fail(ctx, FIC_ERR_ARG, "L must be >= 1");
     if (N < 1 || 2 * B > N) return fail(ctx, FIC_ERR_SHAPE, "2B > N: no domain block fits");
     return FIC_OK;

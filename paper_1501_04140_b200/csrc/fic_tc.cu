@@ -31,6 +31,7 @@
 #include <climits>
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 
 #include "fic_internal.cuh"
 
@@ -45,7 +46,7 @@ struct TCfg {
     // accumulators, SRD = 4 S_q + S_r: half the MMA work, half the A bytes and a quarter of the
     // resident range operand of the 4-polyphase-plane form used at B <= 8 (where the epilogue,
     // not the MMA or the feed, is the bottleneck and a second accumulator would only add work)
-    static constexpr bool QR = (B == 16);
+    static constexpr bool QR = (B >= 16);
     static constexpr int KP = QR ? 2 * n : ((4 * n + 31) / 32) * 32;  // A K bytes per domain (padded)
     static constexpr int KB = QR ? n : KP;                 // B operand K bytes per (range, k) row
     // ranges per CTA: 8 per epilogue warp per tile; B = 4 uses 3 epilogue warpgroups (14 warps,
@@ -56,7 +57,9 @@ struct TCfg {
 #ifndef FIC_B4_EWG
 #define FIC_B4_EWG 3
 #endif
-    static constexpr int NR = (B == 16) ? 16 : (B == 4 ? FIC_B4_NR : 32);
+    // B = 32 (QR, n = 1024 K bytes per range row): 8 ranges, so the 64 KB range operand and two
+    // 64 KB A stages fit shared memory
+    static constexpr int NR = (B == 32) ? 8 : (B == 16) ? 16 : (B == 4 ? FIC_B4_NR : 32);
     static constexpr int N = 8 * NR;                       // MMA N (columns per accumulator)
     static constexpr int KCH = QR ? 512 : (KP < 256 ? KP : 256);  // K bytes per pipeline stage
     static constexpr int CH = KP / KCH;                    // stages per domain tile
@@ -69,7 +72,7 @@ struct TCfg {
     static constexpr int BBUF = B == 4 ? 2 : 1;
     static constexpr int ACC = QR ? 2 * N : N;             // TMEM columns per accumulator buffer
     static constexpr int NBUF = 512 / ACC >= 4 ? 4 : 2;    // TMEM accumulator buffers (MMA <-> epilogue)
-    static constexpr int EWG = B == 4 ? FIC_B4_EWG : 4;   // epilogue warpgroups
+    static constexpr int EWG = B == 4 ? FIC_B4_EWG : (B == 32 ? 2 : 4);   // epilogue warpgroups
     // warps: producer, MMA issuer, 4 EWG epilogue warps, the exact-path warp
     static constexpr int XWARP = 2 + 4 * EWG;
     static constexpr int THREADS = 64 + 128 * EWG + 32;
@@ -253,7 +256,9 @@ __global__ void __launch_bounds__(256) pool_tc_kernel(const uint8_t *__restrict_
         // one thread per 16 pixels writes both planes (q = D' >> 2 at K byte p, r = D' & 3 at
         // n + p) and the domain moments SD, SDD -> C = n SDD - SD^2 (reduced over the n/16 = 16
         // threads of the domain, a half warp), which replaces pool_moments_kernel at this level
-        static_assert(Cf::n / 16 == 16, "QR moments assume 16 threads per domain");
+        // B = 16: thread g = decimated row g; B = 32: decimated row g / 2, half g % 2 (16 values,
+        // 32 source bytes each); the moments are fused at B = 16 only (pool_moments_kernel else)
+        constexpr int HPR = B / 16;  // threads per decimated row
         uint32_t wq[4] = {0, 0, 0, 0}, wr[4] = {0, 0, 0, 0};
         int sd = 0;
         long long sdd = 0;
@@ -263,7 +268,7 @@ __global__ void __launch_bounds__(256) pool_tc_kernel(const uint8_t *__restrict_
             // nonzero shift, ends at or before the row's last byte) and summed two pixels per 16-bit lane
             const int32_t c = kept[d];
             const int64_t x = (int64_t)(c % A) * L, y = (int64_t)(c / A) * L;
-            const uint8_t *r0 = img + (y + 2 * g) * N + x;
+            const uint8_t *r0 = img + (y + 2 * (g / HPR)) * N + x + 32 * (g % HPR);
             const uint32_t *w0 = reinterpret_cast<const uint32_t *>(reinterpret_cast<uintptr_t>(r0) & ~(uintptr_t)3);
             const uint32_t *w1 = w0 + N / 4;
             const uint32_t sh = (uint32_t)(reinterpret_cast<uintptr_t>(r0) & 3) * 8;
@@ -297,18 +302,20 @@ __global__ void __launch_bounds__(256) pool_tc_kernel(const uint8_t *__restrict_
             store16(g * 16, wq);
             store16(Cf::n + g * 16, wr);
         }
+        if constexpr (B == 16) {
 #pragma unroll
-        for (int o = 8; o > 0; o >>= 1) {
-            sd += __shfl_xor_sync(0xffffffffu, sd, o);
-            sdd += __shfl_xor_sync(0xffffffffu, sdd, o);
+            for (int o = 8; o > 0; o >>= 1) {
+                sd += __shfl_xor_sync(0xffffffffu, sd, o);
+                sdd += __shfl_xor_sync(0xffffffffu, sdd, o);
+            }
+            const long long cc = (long long)Cf::n * sdd - (long long)sd * sd;
+            if (g == 0 && live) {
+                SD[d] = sd;
+                SDf[d] = (float)sd;
+                Cm[d] = cc;
+            }
+            block_max_atomic(g == 0 && live && d < n_k ? (unsigned long long)cc : 0ull, d_cmax);
         }
-        const long long cc = (long long)Cf::n * sdd - (long long)sd * sd;
-        if (g == 0 && live) {
-            SD[d] = sd;
-            SDf[d] = (float)sd;
-            Cm[d] = cc;
-        }
-        block_max_atomic(g == 0 && live && d < n_k ? (unsigned long long)cc : 0ull, d_cmax);
     } else {
         uint32_t w[4] = {0, 0, 0, 0};
         if (d < n_k) {
@@ -330,18 +337,19 @@ __global__ void __launch_bounds__(256) pool_tc_kernel(const uint8_t *__restrict_
     }
 }
 
-int tc_supported(int B) { return B == 4 || B == 8 || B == 16; }
+int tc_supported(int B) { return B == 4 || B == 8 || B == 16 || B == 32; }
 
 size_t tc_pool_bytes(int B, int64_t n_tiles) {
     switch (B) {
     case 4: return (size_t)n_tiles * TCfg<4>::CH * TCfg<4>::STAGE_BYTES;
     case 8: return (size_t)n_tiles * TCfg<8>::CH * TCfg<8>::STAGE_BYTES;
     case 16: return (size_t)n_tiles * TCfg<16>::CH * TCfg<16>::STAGE_BYTES;
+    case 32: return (size_t)n_tiles * TCfg<32>::CH * TCfg<32>::STAGE_BYTES;
     default: return 0;
     }
 }
 
-int tc_pool_has_moments(int B) { return TCfg<16>::QR && B == 16; }
+int tc_pool_has_moments(int B) { return B == 16; }
 
 cudaError_t launch_pool_tc(const uint8_t *img, int32_t N, int32_t B, int32_t L, int32_t A,
                            const int32_t *kept, const unsigned long long *d_nk, int64_t n_tiles_max,
@@ -351,7 +359,8 @@ cudaError_t launch_pool_tc(const uint8_t *img, int32_t N, int32_t B, int32_t L, 
     switch (B) {
     case 4: g16 = TCfg<4>::KP / 16; break;
     case 8: g16 = TCfg<8>::KP / 16; break;
-    case 16: g16 = TCfg<16>::QR ? TCfg<16>::n / 16 : TCfg<16>::KP / 16; break;
+    case 16: g16 = TCfg<16>::n / 16; break;
+    case 32: g16 = TCfg<32>::n / 16; break;
     default: return cudaErrorInvalidValue;
     }
     const int64_t total16 = n_tiles_max * kTileD * g16;
@@ -361,6 +370,7 @@ cudaError_t launch_pool_tc(const uint8_t *img, int32_t N, int32_t B, int32_t L, 
     case 4: pool_tc_kernel<4><<<blocks, 256, 0, st>>>(img, N, L, A, kept, d_nk, total16, Dtc, SD, SDf, C, d_cmax); break;
     case 8: pool_tc_kernel<8><<<blocks, 256, 0, st>>>(img, N, L, A, kept, d_nk, total16, Dtc, SD, SDf, C, d_cmax); break;
     case 16: pool_tc_kernel<16><<<blocks, 256, 0, st>>>(img, N, L, A, kept, d_nk, total16, Dtc, SD, SDf, C, d_cmax); break;
+    case 32: pool_tc_kernel<32><<<blocks, 256, 0, st>>>(img, N, L, A, kept, d_nk, total16, Dtc, SD, SDf, C, d_cmax); break;
     }
     return cudaGetLastError();
 }
@@ -377,13 +387,14 @@ __device__ __forceinline__ void tc_range_operand_body(const uint8_t *__restrict_
     // source pixel of byte p of row k: Rperm_k(p) = R(f_k^{-1}(p)); under this numbering
     // f_k^{-1} = f_{k'} with k' = [0,3,2,1,4,5,6,7][k] (rotations by 90/270 swap, the rest are
     // involutions) -- tabulated once per block
-    __shared__ uint8_t src[8][Cf::n];
+    using SrcT = typename std::conditional<(Cf::n > 256), uint16_t, uint8_t>::type;  // pixel index < n
+    __shared__ SrcT src[8][Cf::n];
     for (int t = threadIdx.x; t < 8 * Cf::n; t += blockDim.x) {
         const int kk = t / Cf::n, p = t % Cf::n;
         const int kinv = (kk == 1) ? 3 : (kk == 3 ? 1 : kk);
         int si, sj;
         tiso_src(B, kinv, p / B, p % B, si, sj);
-        src[kk][p] = (uint8_t)(si * B + sj);
+        src[kk][p] = (SrcT)(si * B + sj);
     }
     __syncthreads();
     const int64_t e = (int64_t)bx * blockDim.x + threadIdx.x;  // one 16-byte group
@@ -1211,13 +1222,16 @@ static cudaError_t launch_tc_b(const TCParams &p, cudaStream_t st) {
     return launch_tc_t<B, 0>(p, st);
 }
 
-int tc_ranges_per_cta(int B) { return B == 16 ? TCfg<16>::NR : (B == 4 ? TCfg<4>::NR : TCfg<8>::NR); }
+int tc_ranges_per_cta(int B) {
+    return B == 32 ? TCfg<32>::NR : B == 16 ? TCfg<16>::NR : (B == 4 ? TCfg<4>::NR : TCfg<8>::NR);
+}
 
 size_t tc_range_bytes(int B, int64_t n_r) {
     switch (B) {
     case 4: return (size_t)((n_r + TCfg<4>::NR - 1) / TCfg<4>::NR) * (TCfg<4>::B_BYTES + TCfg<4>::NR * sizeof(TCRangeG));
     case 8: return (size_t)((n_r + TCfg<8>::NR - 1) / TCfg<8>::NR) * (TCfg<8>::B_BYTES + TCfg<8>::NR * sizeof(TCRangeG));
     case 16: return (size_t)((n_r + TCfg<16>::NR - 1) / TCfg<16>::NR) * (TCfg<16>::B_BYTES + TCfg<16>::NR * sizeof(TCRangeG));
+    case 32: return (size_t)((n_r + TCfg<32>::NR - 1) / TCfg<32>::NR) * (TCfg<32>::B_BYTES + TCfg<32>::NR * sizeof(TCRangeG));
     default: return 0;
     }
 }
@@ -1259,6 +1273,7 @@ cudaError_t launch_tc_search(int32_t B, const SearchParams &sp, const uint8_t *D
     case 4: e0 = tc_range_prep<4>(sp, scratch, p, st); break;
     case 8: e0 = tc_range_prep<8>(sp, scratch, p, st); break;
     case 16: e0 = tc_range_prep<16>(sp, scratch, p, st); break;
+    case 32: e0 = tc_range_prep<32>(sp, scratch, p, st); break;
     default: return cudaErrorInvalidValue;
     }
     if (e0 != cudaSuccess) return e0;
@@ -1280,6 +1295,7 @@ cudaError_t launch_tc_search(int32_t B, const SearchParams &sp, const uint8_t *D
     case 4: return launch_tc_b<4>(p, st);
     case 8: return launch_tc_b<8>(p, st);
     case 16: return launch_tc_b<16>(p, st);
+    case 32: return launch_tc_b<32>(p, st);
     default: return cudaErrorInvalidValue;
     }
 }

@@ -1,7 +1,7 @@
 """Randomized end-to-end parity (GPU vs oracle) over shapes the named configs do not reach:
 image sizes that leave ragged domain tiles and few range groups, odd steps L, 1-4 levels, every
 s mode, random entropy thresholds and tolerances, and small persistent grids (FIC_TC_CTAS) so
-that the search plan splits groups across runs.  Every record field must match bit for bit.
+that the search plan splits groups across runs; B_max up to 32, occasionally an s below 2^-20.  Every record field must match bit for bit.
 FIC_FUZZ_N=n widens the sweep (n cases, n // 3 top-K + shard cases; default 48)."""
 import os
 
@@ -31,8 +31,8 @@ def fic():
 
 def case(seed):
     rng = np.random.default_rng(1000 + seed)
-    B_max = int(rng.choice([4, 8, 16]))
-    B_min = int(rng.choice([b for b in (2, 4, 8, 16) if b <= B_max]))
+    B_max = int(rng.choice([4, 8, 16, 32]))
+    B_min = int(rng.choice([b for b in (2, 4, 8, 16, 32) if b <= B_max]))
     N = B_max * int(rng.integers(2, 6))
     L = int(rng.integers(1, 4))
     levels = []
@@ -42,7 +42,9 @@ def case(seed):
         B //= 2
     mode = ["predefined", "grid", "sampled10", "closed5"][seed % 4]
     sets = {"grid": GRID_S, "sampled10": SAMPLED10_S, "closed5": CLOSED5_S}
-    s_sets = [tuple(PREDEFINED_S[B]) if mode == "predefined" else sets[mode] for B in levels]
+    s_sets = [tuple(PREDEFINED_S.get(B, (0.1,))) if mode == "predefined" else sets[mode] for B in levels]
+    if rng.random() < 0.15:  # s below the licensed floor (finalize re-derives (k, j))
+        s_sets = [(1e-15,) + tuple(x) for x in s_sets] if mode == "predefined" else s_sets
     tau = [float(rng.choice([-1.0, 0.5, 1.5])) for _ in levels]
     tol = [float(rng.choice([2.0, 6.0, 12.0]))] * len(levels)
     img = make_image(N, 77 + seed, texture=bool(seed % 2))

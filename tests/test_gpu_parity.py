@@ -355,11 +355,11 @@ def test_capacity_error_reports_count(fic):
     assert small.cpu().numpy().tobytes() == full[:10].cpu().numpy().tobytes()
 
 
-def test_b32_and_bad_args(fic):
+def test_b64_and_bad_args(fic):
     p, ctx, torch = fic
     img = dev(torch, make_image(128, 2))
-    with pytest.raises(p.FicError) as ei:  # B_max = 32 not supported on the GPU path
-        ctx.encode(img, 32, 2, 2, [-1] * 5, [(0.5,)] * 5, [8.0] * 5)
+    with pytest.raises(p.FicError) as ei:  # B_max > 32
+        ctx.encode(img, 64, 2, 2, [-1] * 6, [(0.5,)] * 6, [8.0] * 6)
     assert ei.value.status == 1
     with pytest.raises(p.FicError) as ei:  # more than 32 contrast values
         ctx.encode(img, 16, 2, 2, [-1] * 4, [tuple(np.linspace(0, 1, 33))] * 4, [8.0] * 4)
@@ -527,3 +527,38 @@ def test_native_nccl_error_status_and_topk(fic):
         assert ei.value.status == 1
     finally:
         nctx.close()
+
+
+# ------------------------------------------------------------------ B = 32 ranges ("B is a predefined parameter")
+@pytest.mark.parametrize("smode", ["predefined", "grid", "closed5"])
+@pytest.mark.parametrize("N,L,tau", [(96, 2, -1.0), (128, 3, 4.76), (80, 1, -1.0)])
+def test_level_parity_b32(fic, smode, N, L, tau):
+    img = make_image(N, 300 + N + L, texture=True)
+    s = {"predefined": (0.1,), "grid": GRID_S, "closed5": CLOSED5_S}[smode]
+    level_case(fic, img, 32, L, tau, s, tol=6.0, is_min=False)
+
+
+@pytest.mark.parametrize("t", [4.0, 16.0])
+def test_encode_b32_quadtree(fic, t):
+    """Quadtree 32 -> 2 on the C2 image (every 32x32 range searched, then split) ..."""
+    cfg = config("C2", t=t)
+    cfg["B_max"] = 32
+    cfg["tau"] = [5.2] + list(cfg["tau"])
+    cfg["s"] = [(0.1,)] + list(cfg["s"])
+    cfg["rms_tol"] = [t] * 5
+    img, got = encode_both(fic, cfg)
+    assert_same(got, oracle.encode_cfg(cfg, img), f"B_max=32 t={t}")
+
+
+def test_encode_b32_accepts_on_ramp(fic):
+    """... and on a ramp with noise-free affine copies, where 32x32 leaves are accepted."""
+    cfg = config("C2", t=1.0)
+    cfg["N"] = 128
+    cfg["B_max"] = 32
+    cfg["tau"] = [-1.0] * 5
+    cfg["s"] = [(0.5, 0.9)] * 5
+    cfg["rms_tol"] = [1.0] * 5
+    img = ramp_image(128)
+    img, got = encode_both(fic, cfg, img)
+    assert (got["B"] == 32).all() and (got["err"] == 0.0).all()
+    assert_same(got, oracle.encode_cfg(cfg, img), "B_max=32 ramp")
