@@ -59,6 +59,8 @@ def parse():
                          "(0 = sized so that the whole run takes about 2.5 minutes)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--nccl", action="store_true",
+                    help="N = 1: run the multi-GPU path anyway (fic_encode_nccl on a one-rank communicator)")
     ap.add_argument("--serial-pools", action="store_true",
                     help="build every level's pool on the critical stream (FIC_OVERLAP_POOLS=0): "
                          "ms_pool is then the serial pool cost")
@@ -271,8 +273,11 @@ def main():
     # timing 1: two events per level around the search launches (the roofline's kernel time,
     # measured live in the timed region); pool / finalize times come from an instrumented pass
     # after it (timing 2 adds three more events per level, which cost device time)
+    use_nccl = world > 1 or args.nccl
     if world > 1:
         ctx = fdist.native_context(dev.index, stream=stream, timing=1)
+    elif use_nccl:
+        ctx = fic.Context(dev.index, stream=stream, timing=1, nccl=(fic.nccl_unique_id(), 1, 0))
     else:
         ctx = fic.Context(dev.index, stream=stream, timing=1)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
@@ -280,7 +285,7 @@ def main():
     out = torch.empty((cap, fic.RECORD_BYTES), dtype=torch.uint8, device=dev)
 
     def step_on(im):
-        if world > 1:  # range blocks of the one image sharded over the ranks, gathered (NCCL)
+        if use_nccl:  # range blocks of the one image sharded over the ranks, gathered (NCCL)
             return ctx.encode_nccl_cfg(cfg, im, out=out)
         return ctx.encode_cfg(cfg, im, out=out)
 
@@ -337,7 +342,7 @@ def main():
     torch.cuda.synchronize(dev)
     rec = step().clone()
     mgpu_parity = None
-    if world > 1 and rank == 0:  # the gathered code against the one-GPU encode of the same image
+    if use_nccl and rank == 0:  # the gathered code against the one-GPU encode of the same image
         one = fic.Context(dev.index, stream=stream)
         ref1 = one.encode_cfg(cfg, img)
         mgpu_parity = {"equal_to_one_gpu_encode": bool(torch.equal(ref1, rec)), "records": int(rec.shape[0])}
@@ -387,7 +392,7 @@ def main():
         d_img = torch.empty_like(img)
 
         def hstep():
-            if world > 1 or cfg.get("topk"):  # H2D image, encode, D2H of the whole code
+            if use_nccl or cfg.get("topk"):  # H2D image, encode, D2H of the whole code
                 d_img.copy_(h_img, non_blocking=True)
                 r = step_on(d_img)
                 h_out_t[: r.numel()].copy_(r.view(-1), non_blocking=True)
@@ -457,7 +462,8 @@ def main():
                    "pool": (f"top-{args.topk}" if args.topk else "entropy tau"),
                    "entropy_tau": cfg["tau"],
                    "partition": ("one image; top-level blocks t % N to rank t, NCCL all-gather + merge "
-                                 "(fic_encode_nccl) in the timed region" if world > 1 else "one GPU"),
+                                 "(fic_encode_nccl) in the timed region" if use_nccl else "one GPU") +
+                                (" (one-rank communicator)" if use_nccl and world == 1 else ""),
                    "pools": "serialised on the critical stream" if args.serial_pools else "overlapped (side stream)",
                    "l2": "flushed between timed steps (256 MB write)",
                    "pairs_per_step": pairs_step, "evaluated_pairs_per_step": evald_step,

@@ -65,7 +65,7 @@ struct Pool {
 struct Partial {
     double e;
     int32_t d;
-    int32_t kj;  // iso | (s_idx << 8)
+    int32_t kj;  // iso << 8 | s_idx (kPendIso: iso not yet resolved)
 };
 
 // A level's positive s values that form a uniform grid s_j = a + j h (j = 0..K-1, K >= 3, up to
