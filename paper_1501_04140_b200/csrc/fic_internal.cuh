@@ -207,10 +207,17 @@ __device__ __forceinline__ bool cta_work(int n_r, int rpc, int n_tiles, int min_
     return true;
 }
 
-// scale of -s/2 in the tcgen05 epilogue's magic-number filter (B <= 8, one or two s), which the
-// t2f table folds the magic constant into; 0 = plain table
+// B = 4, 8 on the tcgen05 f16 form (fp16 operands, fp32 accumulator, exact; fic_tc.cu TCfg);
+// -DFIC_TC_F16=0 builds the u8 polyphase form with the magic-number filter instead
+#ifndef FIC_TC_F16
+#define FIC_TC_F16 1
+#endif
+// scale of -s/2 in the tcgen05 epilogue's magic-number filter (u8 form at B <= 8, one or two s),
+// which the t2f table folds the magic constant into; 0 = plain table (B = 2 keeps the fold)
 __host__ __device__ constexpr float tc_t2_fold(int B, int nsp) {
-    return (nsp >= 1 && nsp <= 2) ? (B == 2 ? 1.f : (B == 4 ? 2.f : (B == 8 ? 64.f : 0.f))) : 0.f;
+    return (nsp >= 1 && nsp <= 2)
+               ? (B == 2 ? 1.f : (FIC_TC_F16 ? 0.f : (B == 4 ? 2.f : (B == 8 ? 64.f : 0.f))))
+               : 0.f;
 }
 
 // FIC1 body writer (fic_code.cu): per level (index 0 = B_max) the position and s-index widths

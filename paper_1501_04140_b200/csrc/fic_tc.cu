@@ -33,6 +33,8 @@
 #include <cstring>
 #include <type_traits>
 
+#include <cuda_fp16.h>
+
 #include "fic_internal.cuh"
 
 namespace fic {
@@ -47,7 +49,13 @@ struct TCfg {
     // resident range operand of the 4-polyphase-plane form used at B <= 8 (where the epilogue,
     // not the MMA or the feed, is the bottleneck and a second accumulator would only add work)
     static constexpr bool QR = (B >= 16);
-    static constexpr int KP = QR ? 2 * n : ((4 * n + 31) / 32) * 32;  // A K bytes per domain (padded)
+    // B = 4, 8 (F16): the decimated D' itself (<= 1020) and the range (<= 255) as fp16, which
+    // represents them exactly, into an fp32 accumulator (kind::f16, K = 16 per instruction): every
+    // partial sum is an integer below 2^24 (SRD <= 64 * 255 * 1020 = 16,646,400 at B = 8), so the
+    // accumulation is exact and the epilogue gets SRD as floats -- a quarter of the MMA work and
+    // half the A bytes of the 4-polyphase-plane u8 form, and no int -> float conversion
+    static constexpr bool F16 = FIC_TC_F16 && (B == 4 || B == 8);
+    static constexpr int KP = QR ? 2 * n : F16 ? 2 * n : ((4 * n + 31) / 32) * 32;  // A K bytes per domain
     static constexpr int KB = QR ? n : KP;                 // B operand K bytes per (range, k) row
     // ranges per CTA: 8 per epilogue warp per tile; B = 4 uses 3 epilogue warpgroups (14 warps,
     // at most 4 per SM sub-partition, so 128 registers per thread instead of 96 with 18 warps)
@@ -61,15 +69,15 @@ struct TCfg {
     // 64 KB A stages fit shared memory
     static constexpr int NR = (B == 32) ? 8 : (B == 16) ? 16 : (B == 4 ? FIC_B4_NR : 32);
     static constexpr int N = 8 * NR;                       // MMA N (columns per accumulator)
-    static constexpr int KCH = QR ? 512 : (KP < 256 ? KP : 256);  // K bytes per pipeline stage
+    static constexpr int KCH = QR ? 512 : (KP < 256 ? KP : 256);  // K bytes per pipeline stage (F16: a tile)
     static constexpr int CH = KP / KCH;                    // stages per domain tile
     static constexpr int STAGE_BYTES = kTileD * KCH;       // A bytes per stage
     // B = 16 is fed by bulk copies (latency x bytes in flight): 8 x 16 KB stages
-    static constexpr int STAGES = QR ? 2 : (B == 8 ? 2 : 4);
+    static constexpr int STAGES = QR ? 2 : F16 ? (B == 4 ? 8 : 4) : (B == 8 ? 2 : 4);
     static constexpr int B_BYTES = N * KB;                 // resident range operand
     // range-operand buffers: 2 where shared memory allows, so the next segment's operand loads
     // while the current segment's MMAs still read the other one
-    static constexpr int BBUF = B == 4 ? 2 : 1;
+    static constexpr int BBUF = (B == 4 || F16) ? 2 : 1;
     static constexpr int ACC = QR ? 2 * N : N;             // TMEM columns per accumulator buffer
     static constexpr int NBUF = 512 / ACC >= 4 ? 4 : 2;    // TMEM accumulator buffers (MMA <-> epilogue)
     static constexpr int EWG = B == 4 ? FIC_B4_EWG : (B == 32 ? 2 : 4);   // epilogue warpgroups
@@ -196,6 +204,22 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo, uint
 __host__ __device__ constexpr uint32_t idesc_i8(int N) {
     return (2u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
 }
+// kind::f16 instruction descriptor: D f32, A f16, B f16, both K-major, M = 128, N
+__host__ __device__ constexpr uint32_t idesc_f16(int N) {
+    return (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+}
+__device__ __forceinline__ void tc_mma_f16_elect(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                                 uint32_t accum) {
+    asm volatile(
+        "{ .reg .pred p, e; setp.ne.b32 p, %4, 0; elect.sync _|e, 0xffffffff; "
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p; }" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
+        : "memory");
+}
+// two small non-negative integers (exact in fp16) packed as fp16 bits, low half first
+__device__ __forceinline__ uint32_t f16x2_int(int lo, int hi) {
+    return (uint32_t)__half_as_ushort(__int2half_rn(lo)) | ((uint32_t)__half_as_ushort(__int2half_rn(hi)) << 16);
+}
 // byte offset of element (row, kb) in a K-major no-swizzle operand with K bytes per row
 __host__ __device__ __forceinline__ uint32_t cm_off(int row, int kb, int K) {
     return (uint32_t)((row >> 3) * (K / 16) * 128 + (kb >> 4) * 128 + (row & 7) * 16 + (kb & 15));
@@ -316,6 +340,26 @@ __global__ void __launch_bounds__(256) pool_tc_kernel(const uint8_t *__restrict_
             }
             block_max_atomic(g == 0 && live && d < n_k ? (unsigned long long)cc : 0ull, d_cmax);
         }
+    } else if constexpr (Cf::F16) {
+        // 16-byte group g = decimated pixels 8g .. 8g + 7 (row-major) as fp16
+        uint32_t w[4] = {0, 0, 0, 0};
+        if (d < n_k) {
+            const int32_t c = kept[d];
+            const int64_t x = (int64_t)(c % A) * L, y = (int64_t)(c / A) * L;
+#pragma unroll
+            for (int q = 0; q < 8; q += 2) {
+                int v2[2];
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int p = g * 8 + q + h;
+                    const int i = p / B, j = p % B;
+                    const uint8_t *r0 = img + (y + 2 * i) * N + x + 2 * j;
+                    v2[h] = (int)r0[0] + (int)r0[1] + (int)r0[N] + (int)r0[N + 1];
+                }
+                w[q >> 1] = f16x2_int(v2[0], v2[1]);
+            }
+        }
+        store16(g * 16, w);
     } else {
         uint32_t w[4] = {0, 0, 0, 0};
         if (d < n_k) {
@@ -409,7 +453,15 @@ __device__ __forceinline__ void tc_range_operand_body(const uint8_t *__restrict_
     const int rl = row >> 3, k = row & 7;
     const int64_t r = grp * Cf::NR + rl;
     uint32_t w[4] = {0, 0, 0, 0};
-    if (r < n_r) {
+    if (Cf::F16 && r < n_r) {  // fp16 elements 8g .. 8g + 7 of Rperm_k
+        const int2 rr = ranges[r];
+        const uint8_t *rb = img + (size_t)rr.y * N + rr.x;
+#pragma unroll
+        for (int q = 0; q < 8; q += 2) {
+            const int s0 = src[k][g * 8 + q], s1 = src[k][g * 8 + q + 1];
+            w[q >> 1] = f16x2_int(rb[(size_t)(s0 / B) * N + s0 % B], rb[(size_t)(s1 / B) * N + s1 % B]);
+        }
+    } else if (r < n_r) {
         const int2 rr = ranges[r];
         const uint8_t *rb = img + (size_t)rr.y * N + rr.x;
 #pragma unroll
@@ -477,10 +529,16 @@ __device__ __forceinline__ void tc_range_meta_body(const uint8_t *__restrict__ i
     const double t2m = smax * smax * cmax * 0.0625;
     // + the int -> float conversion of Bq in the epilogue: exact at B = 2, |error| <= 2 at B = 4,
     // <= 64 at B = 8 (floor of Bq / 2 and Bq / 64)
-    R.margin = 8.0 * u * (hs * bq + t2m) + 1e-12 * (R.A + hs * bq + t2m) +
-               (B == 4 ? hs * 2.0 : (B == 8 ? hs * 64.0 : 0.0)) + 1e-30;
-    // folded magic constant (B <= 8): t2' = RN(t2 - nhs M) adds u |t2 - nhs M| <= u (t2m + hs k M)
-    if (B <= 8) R.margin += 2.0 * u * (t2m + hs * (B == 2 ? 1.0 : (B == 4 ? 2.0 : 64.0)) * 12582912.0);
+    if (TCfg<B>::F16) {
+        // F16: y = RN(SRD_max - SR (SD / n)) = RN(Bq / n) (one FFMA, SD / n exact), then
+        // g = RN(nhs n y + t2): conversions of s / 2 and t2, the two roundings -> 4u (hs |Bq| + t2)
+        R.margin = 8.0 * u * (hs * bq + t2m) + 1e-12 * (R.A + hs * bq + t2m) + 1e-30;
+    } else {
+        R.margin = 8.0 * u * (hs * bq + t2m) + 1e-12 * (R.A + hs * bq + t2m) +
+                   (B == 4 ? hs * 2.0 : (B == 8 ? hs * 64.0 : 0.0)) + 1e-30;
+        // folded magic constant (B <= 8): t2' = RN(t2 - nhs M) adds u |t2 - nhs M| <= u (t2m + hs k M)
+        if (B <= 8) R.margin += 2.0 * u * (t2m + hs * (B == 2 ? 1.0 : (B == 4 ? 2.0 : 64.0)) * 12582912.0);
+    }
     // s-independent filter (NSP = 0): Bq rounded once, squared, times RN(1/C): <= 4.04u Bq^2/C <= 4.04u A
     if (univ == 1) R.margin = 4.1 * u * R.A + 1e-12 * R.A + 1e-30;
     // uniform grid (NSP = 3): g(s) = s (s RN(C/16) - Bq/2) at two fp32 grid points s = fma(j, h, a):
@@ -731,7 +789,7 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
         }
     } else if (warp == 1) {
         // ================= MMA issuer
-        constexpr uint32_t idesc = idesc_i8(NN);
+        constexpr uint32_t idesc = Cf::F16 ? idesc_f16(NN) : idesc_i8(NN);
         int i = 0, tl = 0;
         const uint32_t tmem_u = __shfl_sync(0xffffffffu, tmem, 0);
         const uint32_t sA_sa = su32(sA), empty_sa = su32(empty), tfull_sa = su32(tfull);
@@ -765,7 +823,8 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
                             const uint32_t dcol = buf * Cf::ACC + plane * NN;
                             const uint64_t ad = smem_desc(a0 + kk * 256, 128, (KCH / 16) * 128);
                             const uint64_t bd = smem_desc(bbase + kp * 8, 128, (Cf::KB / 16) * 128);
-                            tc_mma_i8_elect(tmem_u + dcol, ad, bd, idesc, kp > 0 ? 1u : 0u);
+                            if constexpr (Cf::F16) tc_mma_f16_elect(tmem_u + dcol, ad, bd, idesc, kp > 0 ? 1u : 0u);
+                            else tc_mma_i8_elect(tmem_u + dcol, ad, bd, idesc, kp > 0 ? 1u : 0u);
                         }
                         tc_commit_elect(empty_sa + 8 * s);
                         if (ch == CH - 1) {
@@ -879,16 +938,22 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
 #pragma unroll
         // the B = 4 / 8 conversions below yield Bq / 2 and Bq / 64: fold the power of two into -s/2
         // (exact), so g = fma(nhs, bq, t2) keeps its rounding without the multiply
-        constexpr float kBqScale = B == 4 ? 2.0f : (B == 8 ? 64.0f : 1.0f);
+        // F16: g = (-(s/2) n) y + t2 with y = RN(Bq / n)
+        constexpr float kBqScale = Cf::F16 ? (float)n : (B == 4 ? 2.0f : (B == 8 ? 64.0f : 1.0f));
         for (int jj = 0; jj < NT; ++jj) nhs[jj] = sHsn[jj] * kBqScale;
         static_assert(Cf::EWG <= 5, "named barriers 1..EWG (seeding) and 6 (segments) must not collide");
         auto epi_sync = [&]() { asm volatile("bar.sync 6, %0;" ::"r"(128 * Cf::EWG) : "memory"); };
         volatile unsigned *vctl = sXCtl;
         const int64_t t2row = P.n_slots;
         // fp32 filter score of one (range, domain) pair from the max over isometries of SRD_k
-        auto score = [&](int mx, int rsr, int32_t sd, const float *t2) -> float {
+        // F16: mx holds the bits of the fp32 max (non-negative floats order like their bits, so
+        // the VIMNMX3 max is the float max), rsr the bits of -SR, sdn = SD / n (exact)
+        auto score = [&](int mx, int rsr, int32_t sd, float sdn, const float *t2) -> float {
             float bq;
-            if constexpr (NSP == 3 && B <= 8) {
+            if constexpr (Cf::F16) {
+                const float y = fmaf(__int_as_float(rsr), sdn, __int_as_float(mx));  // RN(Bq / n)
+                bq = (NSP == 0 || NSP == 3) ? y * (float)n : y;
+            } else if constexpr (NSP == 3 && B <= 8) {
                 bq = (float)(n * mx - rsr * sd);  // exact int32 Bq, one RN conversion
             } else if constexpr (NSP == 3) {
                 bq = (float)((long long)n * mx - (long long)rsr * sd);
@@ -948,7 +1013,7 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
             if (et < NR) {
                 const TCRange R = P.rmeta[r0 + et];
                 sR[et] = R;
-                sSR[et] = R.SR;
+                sSR[et] = Cf::F16 ? __float_as_int(-(float)R.SR) : R.SR;
                 const float th = P.has_zero ? fminf(__double2float_ru(R.margin), FLT_MAX) : FLT_MAX;
                 sThr[et] = R.valid ? th : -FLT_MAX;
                 sM2[et] = fminf(__double2float_ru(2.0 * R.margin), FLT_MAX);
@@ -962,7 +1027,8 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
             }
             int rSR[HALF];
 #pragma unroll
-            for (int q = 0; q < HALF; ++q) rSR[q] = sR[eg * HALF + q].SR;
+            for (int q = 0; q < HALF; ++q)
+                rSR[q] = Cf::F16 ? __float_as_int(-(float)sR[eg * HALF + q].SR) : sR[eg * HALF + q].SR;
             // per-domain data of this lane, walked tile by tile (pointers advanced, not recomputed);
             // NSP > 0 is chosen only when the level has exactly NSP values s > 0, so every row exists
             // B >= 8: a 32-bit slot index (one IMAD.WIDE per load instead of 64-bit pointer
@@ -1004,7 +1070,7 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
                         const uint32_t *v = sv + q4 * 8;
                         const int mx = max(__vimax3_s32((int)v[0], (int)v[1], (int)v[2]),
                                            __vimax3_s32((int)v[3], (int)v[4], __vimax3_s32((int)v[5], (int)v[6], (int)v[7])));
-                        float gm = score(mx, rSR[q], sd_n, t2_n);
+                        float gm = score(mx, rSR[q], sd_n, (float)sd_n * (1.0f / (float)n), t2_n);
 #pragma unroll
                         for (int o = 16; o > 0; o >>= 1) gm = fminf(gm, __shfl_xor_sync(0xffffffffu, gm, o));
                         if (lane == 0) {
@@ -1031,6 +1097,7 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
                 const unsigned buf = tl % NBUF;
                 const int d = (ta + tt) * kTileD + m;
                 const int32_t sd = sd_n;
+                const float sdn = (float)sd * (1.0f / (float)n);  // exact (SD < 2^24, n a power of two)
                 float t2[NT];
 #pragma unroll
                 for (int jj = 0; jj < NT; ++jj) t2[jj] = t2_n[jj];
@@ -1079,7 +1146,7 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
                                            __vimax3_s32((int)v[3], (int)v[4], __vimax3_s32((int)v[5], (int)v[6], (int)v[7])));
                         mxs[q4] = mx;
                         // (B = 8, at its 96-register ceiling: the range sums from shared memory)
-                        const float g0 = score(mx, B == 8 ? sSR[eg * HALF + q] : rSR[q], sd, t2);
+                        const float g0 = score(mx, B == 8 ? sSR[eg * HALF + q] : rSR[q], sd, sdn, t2);
                         pm |= (g0 <= sThr[eg * HALF + q]) ? (1u << q4) : 0u;
                     }
                     if (pm) {  // queue (range, domain, k*, max SRD) of the passing pairs for the exact warp
@@ -1098,7 +1165,7 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
                                 // (NSP = 0: g is only a lower bound of the grid's minimum -- no)
                                 if constexpr (NSP > 0) {
                                     const int q = g * 4 + q4;
-                                    const float g0 = score(mxs[q4], B == 8 ? sSR[eg * HALF + q] : rSR[q], sd, t2);
+                                    const float g0 = score(mxs[q4], B == 8 ? sSR[eg * HALF + q] : rSR[q], sd, sdn, t2);
                                     const float t = fminf(__fadd_ru(g0, sM2[eg * HALF + q]), FLT_MAX);
                                     int *ti = reinterpret_cast<int *>(&sThr[eg * HALF + q]);
                                     int old = *ti;
@@ -1111,7 +1178,8 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
                                 const unsigned xi = atomicAdd(&sXCtl[0], 1u);
                                 while (xi - vctl[1] >= (unsigned)Cf::XQ) __nanosleep(32);  // ring full (rare)
                                 XItem it;
-                                it.mx = mxs[q4]; it.d = d; it.sd = sd;
+                                it.mx = Cf::F16 ? (int)__int_as_float(mxs[q4]) : mxs[q4];
+                                it.d = d; it.sd = sd;
                                 it.meta = (eg * HALF + g * 4 + q4) | (ks << 5) | (m << 8);
                                 sXQ[xi & (Cf::XQ - 1)] = it;
                                 __threadfence_block();
