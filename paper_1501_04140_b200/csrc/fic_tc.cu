@@ -753,30 +753,14 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
     const uint32_t tmem = *sTmem;
 
     if (warp == 0) {
-        // ================= producer: lane l < STAGES owns the stages s = l and issues their bulk
-        // copies, so STAGES copies are in flight at once
-        constexpr int kCopyLanes = STAGES;
-        if (lane < kCopyLanes) {
+        // ================= producer: one lane issues every bulk copy in order -- each segment's
+        // range operand (once the MMAs of the segment BBUF earlier released its buffer) and the A
+        // stages (stage / phase carried incrementally; the (tile, chunk) stages of a segment are
+        // contiguous in the pool)
+        if (lane == 0) {
+            int s = 0;
+            uint32_t ph = 0;
             int i = 0;
-            for (int k = 0; k < nseg; ++k) {
-            int grp, ta, ntl, slot;
-            bool lastseg;
-            plan_segment(&plan, k, grp, ta, ntl, slot, lastseg);
-            for (int tile = ta; tile < ta + ntl; ++tile) {  // tile by tile across the CTA's segments
-                for (int ch = 0; ch < CH; ++ch, ++i) {
-                    const int s = i % STAGES;
-                    if (s != lane) continue;
-                    if (i >= STAGES) tmbar_wait(&empty[s], (uint32_t)(((i / STAGES) + 1) & 1));
-                    tmbar_expect_tx(&full[s], Cf::STAGE_BYTES);
-                    TC_TR(0, i);
-                    tbulk_g2s(sA + s * Cf::STAGE_BYTES, P.Dtc + ((size_t)tile * CH + ch) * Cf::STAGE_BYTES,
-                              Cf::STAGE_BYTES, &full[s]);
-                }
-            }
-            }
-        } else if (lane == kCopyLanes) {
-            // the resident range operand of each segment's group (tc_range_operand_kernel), once
-            // the previous segment's MMAs released it
             for (int k = 0; k < nseg; ++k) {
                 int grp, ta, ntl, slot;
                 bool lastseg;
@@ -785,6 +769,15 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
                 if (k >= Cf::BBUF) tmbar_wait(&bbar[Cf::BBUF + kb], (uint32_t)(((k / Cf::BBUF) - 1) & 1));
                 tmbar_expect_tx(&bbar[kb], Cf::B_BYTES);
                 tbulk_g2s(sB + kb * Cf::B_BYTES, P.Bop + (size_t)grp * Cf::B_BYTES, Cf::B_BYTES, &bbar[kb]);
+                const uint8_t *src = P.Dtc + (size_t)ta * CH * Cf::STAGE_BYTES;
+                for (int c = 0; c < ntl * CH; ++c, ++i) {
+                    if (i >= STAGES) tmbar_wait(&empty[s], ph ^ 1u);
+                    tmbar_expect_tx(&full[s], Cf::STAGE_BYTES);
+                    TC_TR(0, i);
+                    tbulk_g2s(sA + s * Cf::STAGE_BYTES, src, Cf::STAGE_BYTES, &full[s]);
+                    src += Cf::STAGE_BYTES;
+                    if (++s == STAGES) { s = 0; ph ^= 1u; }
+                }
             }
         }
     } else if (warp == 1) {
