@@ -381,6 +381,94 @@ __global__ void __launch_bounds__(256) pool_tc_kernel(const uint8_t *__restrict_
     }
 }
 
+// QR pool (B = 16, 32), warp per domain (grid-stride over the slots): the raw 2B x 2B block read
+// as 32 / RW rows x RW words per load (RW = B / 2 words per raw row; coalesced), the 2 x 2 sums
+// formed with one packed add per word and one shuffle between the two rows of a pair, written as
+// the q = D' >> 2 and r = D' & 3 planes (two bytes per lane per decimated row), and SD, SDD -> C
+// reduced over the warp.  (Previously each thread formed one decimated row: the 16 rows of a
+// domain per half-warp, uncoalesced.)  Rows that are not word-aligned (N % 4 != 0) are read
+// bytewise.
+template <int B>
+__global__ void __launch_bounds__(256) pool_qr_kernel(const uint8_t *__restrict__ img, int32_t N, int32_t L,
+                                                       int32_t A, const int32_t *__restrict__ kept,
+                                                       const unsigned long long *__restrict__ d_nk,
+                                                       uint8_t *__restrict__ Dtc, int32_t *__restrict__ SD,
+                                                       float *__restrict__ SDf, int64_t *__restrict__ Cm,
+                                                       unsigned long long *d_cmax) {
+    using Cf = TCfg<B>;
+    constexpr int RW = B / 2;         // words per raw row (2B bytes)
+    constexpr int RPI = 32 / RW;      // raw rows per warp load
+    constexpr int ITS = 2 * B / RPI;  // loads per domain
+    static_assert(Cf::QR && RPI % 2 == 0, "QR pool");
+    const int lane = threadIdx.x & 31;
+    const int64_t n_k = (int64_t)*d_nk;
+    const int64_t slots = ((n_k + kTileD - 1) / kTileD) * kTileD;
+    const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int rr = lane / RW, w = lane % RW;  // row in the group, word in the row
+    const bool wordwise = (N & 3) == 0 && (reinterpret_cast<uintptr_t>(img) & 3) == 0;
+    unsigned long long cmax = 0;
+    for (int64_t d = wid; d < slots; d += nw) {
+        const int64_t tile = d / kTileD;
+        const int m = (int)(d - tile * kTileD);
+        uint8_t *tb = Dtc + (size_t)tile * Cf::CH * Cf::STAGE_BYTES;  // [tile][chunk][128 x KCH]
+        auto put2 = [&](int kb, uint16_t v) {
+            *reinterpret_cast<uint16_t *>(tb + (size_t)(kb / Cf::KCH) * Cf::STAGE_BYTES + cm_off(m, kb % Cf::KCH, Cf::KCH)) = v;
+        };
+        int sd = 0;
+        long long sdd = 0;
+        if (d < n_k) {
+            const int32_t c = kept[d];
+            const int64_t x = (int64_t)(c % A) * L, y = (int64_t)(c / A) * L;
+            const uint8_t *r0 = img + y * N + x;
+            const uint32_t sh = (uint32_t)(reinterpret_cast<uintptr_t>(r0) & 3) * 8;
+            const uint32_t *wrow0 = reinterpret_cast<const uint32_t *>(reinterpret_cast<uintptr_t>(r0) & ~(uintptr_t)3);
+#pragma unroll 2
+            for (int it = 0; it < ITS; ++it) {
+                uint32_t v;
+                if (wordwise) {
+                    const uint32_t *wr = wrow0 + (size_t)(RPI * it + rr) * (N / 4);
+                    const uint32_t lo = __ldg(wr + w);
+                    uint32_t hi = __shfl_down_sync(0xffffffffu, lo, 1);
+                    if (w == RW - 1) hi = sh ? __ldg(wr + RW) : 0u;  // (N % 4 == 0: within the row)
+                    v = __funnelshift_r(lo, hi, sh);                 // pixels 4w .. 4w + 3
+                } else {
+                    const uint8_t *pb = r0 + (size_t)(RPI * it + rr) * N + 4 * w;
+                    v = (uint32_t)pb[0] | ((uint32_t)pb[1] << 8) | ((uint32_t)pb[2] << 16) | ((uint32_t)pb[3] << 24);
+                }
+                const uint32_t h = (v & 0x00FF00FFu) + ((v >> 8) & 0x00FF00FFu);  // 2 horizontal pairs
+                const uint32_t dd = h + __shfl_down_sync(0xffffffffu, h, RW);   // + the row below
+                if ((rr & 1) == 0) {
+                    const int i = (RPI / 2) * it + (rr >> 1);  // decimated row; columns 2w, 2w + 1
+                    const int a = (int)(dd & 0xFFFFu), b = (int)(dd >> 16);
+                    sd += a + b;
+                    sdd += (long long)(a * a + b * b);
+                    const int kq = B * i + 2 * w;  // K byte of (i, 2w) in the q plane; r plane at n + kq
+                    put2(kq, (uint16_t)((a >> 2) | ((b >> 2) << 8)));
+                    put2(Cf::n + kq, (uint16_t)((a & 3) | ((b & 3) << 8)));
+                }
+            }
+        } else {  // pad rows of the last tile: zero q and r planes
+            for (int kb = 16 * lane; kb < Cf::KP; kb += 16 * 32)
+                *reinterpret_cast<uint4 *>(tb + (size_t)(kb / Cf::KCH) * Cf::STAGE_BYTES + cm_off(m, kb % Cf::KCH, Cf::KCH)) =
+                    make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            sd += __shfl_xor_sync(0xffffffffu, sd, o);
+            sdd += __shfl_xor_sync(0xffffffffu, sdd, o);
+        }
+        const long long cc = (long long)Cf::n * sdd - (long long)sd * sd;
+        if (lane == 0) {
+            SD[d] = sd;
+            SDf[d] = (float)sd;
+            Cm[d] = cc;
+        }
+        if (d < n_k && (unsigned long long)cc > cmax) cmax = (unsigned long long)cc;
+    }
+    block_max_atomic(cmax, d_cmax);
+}
+
 int tc_supported(int B) { return B == 4 || B == 8 || B == 16 || B == 32; }
 
 size_t tc_pool_bytes(int B, int64_t n_tiles) {
@@ -393,7 +481,7 @@ size_t tc_pool_bytes(int B, int64_t n_tiles) {
     }
 }
 
-int tc_pool_has_moments(int B) { return B == 16; }
+int tc_pool_has_moments(int B) { return B >= 16; }
 
 cudaError_t launch_pool_tc(const uint8_t *img, int32_t N, int32_t B, int32_t L, int32_t A,
                            const int32_t *kept, const unsigned long long *d_nk, int64_t n_tiles_max,
@@ -413,8 +501,16 @@ cudaError_t launch_pool_tc(const uint8_t *img, int32_t N, int32_t B, int32_t L, 
     switch (B) {
     case 4: pool_tc_kernel<4><<<blocks, 256, 0, st>>>(img, N, L, A, kept, d_nk, total16, Dtc, SD, SDf, C, d_cmax); break;
     case 8: pool_tc_kernel<8><<<blocks, 256, 0, st>>>(img, N, L, A, kept, d_nk, total16, Dtc, SD, SDf, C, d_cmax); break;
-    case 16: pool_tc_kernel<16><<<blocks, 256, 0, st>>>(img, N, L, A, kept, d_nk, total16, Dtc, SD, SDf, C, d_cmax); break;
-    case 32: pool_tc_kernel<32><<<blocks, 256, 0, st>>>(img, N, L, A, kept, d_nk, total16, Dtc, SD, SDf, C, d_cmax); break;
+    case 16: {  // warp per domain (pool_qr_kernel)
+        const unsigned bq = (unsigned)std::min<int64_t>((n_tiles_max * kTileD + 7) / 8, 148 * 16);
+        pool_qr_kernel<16><<<bq, 256, 0, st>>>(img, N, L, A, kept, d_nk, Dtc, SD, SDf, C, d_cmax);
+        break;
+    }
+    case 32: {
+        const unsigned bq = (unsigned)std::min<int64_t>((n_tiles_max * kTileD + 7) / 8, 148 * 16);
+        pool_qr_kernel<32><<<bq, 256, 0, st>>>(img, N, L, A, kept, d_nk, Dtc, SD, SDf, C, d_cmax);
+        break;
+    }
     }
     return cudaGetLastError();
 }

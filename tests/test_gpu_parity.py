@@ -562,3 +562,13 @@ def test_encode_b32_accepts_on_ramp(fic):
     img, got = encode_both(fic, cfg, img)
     assert (got["B"] == 32).all() and (got["err"] == 0.0).all()
     assert_same(got, oracle.encode_cfg(cfg, img), "B_max=32 ramp")
+
+
+@pytest.mark.parametrize("B,N,L", [(16, 70, 3), (32, 66, 1), (16, 97, 2), (8, 75, 3), (4, 41, 1)])
+def test_level_parity_unaligned_rows(fic, B, N, L):
+    """Image widths that are not a multiple of 4 (rows not word-aligned): the pool kernels that
+    read words fall back to bytes."""
+    img = random_image(N, 11 * B + N)
+    n = (N // B) * B
+    ranges = np.array([(u * B, v * B) for v in range(n // B) for u in range(n // B)], np.int32)
+    level_case(fic, img, B, L, -1.0, (0.1, 0.6) if B >= 16 else PREDEFINED_S[B], ranges=ranges)
