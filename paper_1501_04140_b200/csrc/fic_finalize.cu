@@ -83,8 +83,11 @@ __device__ __noinline__ void srd_all_dev(const FinalizeParams &P, int2 rr, int32
 
 }  // namespace
 
-// Thread per range.
-__global__ void finalize_kernel(const __grid_constant__ FinalizeParams P) {
+// Thread per range.  Templated on B so the row loads and the partial merge unroll: the loads are
+// independent and all in flight at once (with a runtime B the loop issued them one round trip
+// at a time: 14 us at B = 16).
+template <int BT>
+__global__ void __launch_bounds__(128) finalize_kernel(const __grid_constant__ FinalizeParams P) {
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= (int)*P.d_nr) return;
     if (P.d_misc[0] == 0) {  // ranges but no domain block survived the entropy filter
@@ -92,13 +95,14 @@ __global__ void finalize_kernel(const __grid_constant__ FinalizeParams P) {
         return;
     }
     const int2 rr = P.ranges[r];
-    const int B = P.B, n = B * B;
+    constexpr int B = BT, n = B * B;
     long long sr = 0, srr = 0;
     const uint8_t *rb = P.img + (size_t)rr.y * P.N + rr.x;
     if (B >= 4 && ((reinterpret_cast<uintptr_t>(P.img) | (uintptr_t)P.N) & 15) == 0) {
         // rows of B bytes at 16-byte aligned bases (rr.x % B == 0): independent word loads and
         // byte dot products (sum <= 261120, sum of squares <= 66.6e6 at B = 32: exact in 32 bits)
         unsigned s1 = 0, s2 = 0;
+#pragma unroll
         for (int i = 0; i < B; ++i) {
             const uint32_t *row = reinterpret_cast<const uint32_t *>(rb + (size_t)i * P.N);
             if (B == 16) {
@@ -107,14 +111,17 @@ __global__ void finalize_kernel(const __grid_constant__ FinalizeParams P) {
 #pragma unroll
                 for (int q = 0; q < 4; ++q) { s1 = __dp4a(w[q], 0x01010101u, s1); s2 = __dp4a(w[q], w[q], s2); }
             } else {
+#pragma unroll
                 for (int q = 0; q < B / 4; ++q) { const uint32_t w = row[q]; s1 = __dp4a(w, 0x01010101u, s1); s2 = __dp4a(w, w, s2); }
             }
         }
         sr = s1;
         srr = s2;
     } else {
+#pragma unroll 4
         for (int i = 0; i < B; ++i) {
             const uint8_t *row = rb + (size_t)i * P.N;
+#pragma unroll 4
             for (int j = 0; j < B; ++j) {
                 const int v = row[j];
                 sr += v;
@@ -134,9 +141,15 @@ __global__ void finalize_kernel(const __grid_constant__ FinalizeParams P) {
         best.kj = INT_MAX;
     }
     const int ns = P.nsplit > 0 ? (int)*P.d_ns : 0;
-    for (int sp = 0; sp < ns; ++sp) {
-        const Partial c = P.part[(size_t)r * P.nsplit + sp];
-        if (lex_less(c.e, c.d, c.kj, best)) { best.e = c.e; best.d = c.d; best.kj = c.kj; }
+    const Partial *pr = P.part + (size_t)r * P.nsplit;
+    for (int sp0 = 0; sp0 < ns; sp0 += 4) {  // four partial loads in flight at a time
+        Partial c[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (sp0 + u < ns) c[u] = pr[sp0 + u];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (sp0 + u < ns && lex_less(c[u].e, c[u].d, c[u].kj, best)) { best.e = c[u].e; best.d = c[u].d; best.kj = c[u].kj; }
     }
     if (best.kj & kPendIso || P.fix_kj) {
         // The searches report the minimal e and the first domain attaining it exactly (for every
@@ -223,7 +236,15 @@ __global__ void finalize_kernel(const __grid_constant__ FinalizeParams P) {
 
 cudaError_t launch_finalize(const FinalizeParams &p, cudaStream_t st) {
     if (p.n_r == 0) return cudaSuccess;
-    finalize_kernel<<<(unsigned)((p.n_r + 127) / 128), 128, 0, st>>>(p);
+    const unsigned g = (unsigned)((p.n_r + 127) / 128);
+    switch (p.B) {
+    case 2: finalize_kernel<2><<<g, 128, 0, st>>>(p); break;
+    case 4: finalize_kernel<4><<<g, 128, 0, st>>>(p); break;
+    case 8: finalize_kernel<8><<<g, 128, 0, st>>>(p); break;
+    case 16: finalize_kernel<16><<<g, 128, 0, st>>>(p); break;
+    case 32: finalize_kernel<32><<<g, 128, 0, st>>>(p); break;
+    default: return cudaErrorInvalidValue;
+    }
     return cudaGetLastError();
 }
 
