@@ -85,6 +85,9 @@ struct TCfg {
     static constexpr int XWARP = 2 + 4 * EWG;
     static constexpr int THREADS = 64 + 128 * EWG + 32;
     static constexpr int XQ = 512;                         // exact-path work ring (power of two)
+    // exact-path best slots per range (slot = domain lane % RBW): 8 at B >= 16, whose 16 ranges
+    // per CTA see bursts of items of one range; 1 at B <= 8 (C3: B = 4 0.530 vs 0.537 ms with 8)
+    static constexpr int RBW = B >= 16 ? 8 : 1;
 };
 
 // One (range, domain) pair the fp32 filter could not exclude, queued for the exact-path warp.
@@ -617,11 +620,11 @@ __device__ __forceinline__ void tc_range_meta_body(const uint8_t *__restrict__ i
     }
     R.A = (double)((long long)n * srr - sr * sr);
     R.SR = (int32_t)sr;
-    // fp32 filter error: |Bq| <= sqrt(A C) (Cauchy-Schwarz); conversions, hs and t2 roundings,
-    // two FFMA roundings, SR*SD rounding at B = 16 -> 8u (hs (sqrt(A Cmax) + n 1020 SR) + t2max)
+    // fp32 filter error: |Bq| <= sqrt(A C) (Cauchy-Schwarz); the one rounding of Bq (or of Bq / n),
+    // hs and t2 roundings, two FFMA roundings -> 8u (hs sqrt(A Cmax) + t2max)
     const double u = 5.9604644775390625e-08;
     const double hs = 0.5 * smax;
-    const double bq = sqrt(R.A * cmax) * 1.01 + (B > 8 ? (double)n * 1020.0 * (double)sr : 0.0);
+    const double bq = sqrt(R.A * cmax) * 1.01;  // every form converts an exact (or RN(Bq / n)) value once
     const double t2m = smax * smax * cmax * 0.0625;
     // + the int -> float conversion of Bq in the epilogue: exact at B = 2, |error| <= 2 at B = 4,
     // <= 64 at B = 8 (floor of Bq / 2 and Bq / 64)
@@ -776,14 +779,15 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
     float *sThr = reinterpret_cast<float *>(sR + NR);          // [NR] RU(best - A + margin), CAS-min
     float *sHsn = reinterpret_cast<float *>(sThr + NR);        // [NSP]
     int *sSR = reinterpret_cast<int *>(sHsn + 16);              // [NR] range sums (B = 8 reads them here)
-    Partial *sRed = reinterpret_cast<Partial *>(sSR + NR);      // [NR][4]
+    // [NR][RBW] range bests, RBW slots per range (slot = domain lane % RBW) so the exact warp's
+    // updates of one range from different lanes rarely collide; written by the exact warp only
+    Partial *sRB = reinterpret_cast<Partial *>(sSR + NR);
     constexpr int NBUF = Cf::NBUF;
-    uint64_t *bar = reinterpret_cast<uint64_t *>(sRed + NR * 4);  // full[S], empty[S], tfull[NB], tempty[NB], bop
+    uint64_t *bar = reinterpret_cast<uint64_t *>(sRB + NR * Cf::RBW);  // full[S], empty[S], tfull[NB], tempty[NB], bop
     uint64_t *full = bar, *empty = bar + STAGES, *tfull = bar + 2 * STAGES, *tempty = tfull + NBUF;
     uint64_t *bbar = tempty + NBUF;  // [BBUF] range operand loaded, [BBUF] range operand free
     uint32_t *sTmem = reinterpret_cast<uint32_t *>(bbar + 4);
-    Partial *sBest = reinterpret_cast<Partial *>(sTmem + 4);  // [NR][128] per (range, domain lane)
-    XItem *sXQ = reinterpret_cast<XItem *>(sBest + NR * kTileD);     // [XQ] exact-path ring
+    XItem *sXQ = reinterpret_cast<XItem *>(sTmem + 4);               // [XQ] exact-path ring (16 B aligned)
     unsigned *sXSeq = reinterpret_cast<unsigned *>(sXQ + Cf::XQ);    // [XQ] slot i holds item i when = i + 1
     unsigned *sXCtl = sXSeq + Cf::XQ;  // [0] items reserved, [1] items consumed, [2] no more items
     float *sM2 = reinterpret_cast<float *>(sXCtl + 4);  // [NR] RU(2 margin) of the group's ranges
@@ -967,40 +971,36 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
                     if (e < eb || (e == eb && kj < kjb)) { eb = e; kjb = kj; }
                 }
             }
-            // the (range, domain lane) best is a lexicographic minimum, so the updates commute:
-            // lanes with distinct slots update in parallel; a slot queued twice in one batch is
-            // first reduced to its lowest lane (rare)
+            // the range's best is a lexicographic minimum, so the updates commute: in each pass
+            // the lowest pending lane of every range updates it (distinct ranges in parallel);
+            // passes = the largest number of items of one range in the batch.  This warp is the
+            // only writer of sRB during a segment.
             const bool act = lane < cnt;
-            const unsigned key = act ? (unsigned)(qg * kTileD + mm) : (0x80000000u | (unsigned)lane);
+            const unsigned key = act ? (unsigned)(qg * Cf::RBW + (mm & (Cf::RBW - 1))) : (0x80000000u | (unsigned)lane);
             const unsigned grp = __match_any_sync(0xffffffffu, key);
-            if (__any_sync(0xffffffffu, act && __popc(grp) > 1)) {
-                for (int i = 0; i < 32; ++i) {
-                    const double oe = __shfl_sync(0xffffffffu, eb, i);
-                    const int32_t od = __shfl_sync(0xffffffffu, dd, i);
-                    const int32_t okj = __shfl_sync(0xffffffffu, kjb, i);
-                    if (act && i != lane && ((grp >> i) & 1) &&
-                        (oe < eb || (oe == eb && (od < dd || (od == dd && okj < kjb))))) {
-                        eb = oe; dd = od; kjb = okj;
+            unsigned pending = __ballot_sync(0xffffffffu, act);
+            while (pending) {
+                const bool lead = ((pending >> lane) & 1u) && lane == __ffs(grp & pending) - 1;
+                if (lead) {
+                    Partial *bp = &sRB[key];
+                    const Partial b = *bp;
+                    if (eb < b.e || (eb == b.e && (dd < b.d || (dd == b.d && kjb < b.kj)))) {
+                        Partial nb;
+                        nb.e = eb; nb.d = dd; nb.kj = kjb;
+                        *bp = nb;
+                        const TCRange &R = sR[qg];
+                        const float t = fminf(__double2float_ru(__dadd_rn(__dsub_rn(eb, R.A), R.margin)), FLT_MAX);
+                        int *ti = reinterpret_cast<int *>(&sThr[qg]);
+                        int old = *ti;
+                        while (t < __int_as_float(old)) {
+                            const int prev = atomicCAS(ti, old, __float_as_int(t));
+                            if (prev == old) break;
+                            old = prev;
+                        }
                     }
                 }
-            }
-            if (act && __ffs(grp) - 1 == lane) {
-                Partial *bp = &sBest[key];
-                const Partial b = *bp;
-                if (eb < b.e || (eb == b.e && (dd < b.d || (dd == b.d && kjb < b.kj)))) {
-                    Partial nb;
-                    nb.e = eb; nb.d = dd; nb.kj = kjb;
-                    *bp = nb;
-                    const TCRange &R = sR[qg];
-                    const float t = fminf(__double2float_ru(__dadd_rn(__dsub_rn(eb, R.A), R.margin)), FLT_MAX);
-                    int *ti = reinterpret_cast<int *>(&sThr[qg]);
-                    int old = *ti;
-                    while (t < __int_as_float(old)) {
-                        const int prev = atomicCAS(ti, old, __float_as_int(t));
-                        if (prev == old) break;
-                        old = prev;
-                    }
-                }
+                pending &= ~__ballot_sync(0xffffffffu, lead);
+                __syncwarp();
             }
             head += cnt;
             n_items += cnt;
@@ -1063,7 +1063,10 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
                 // |Bq| < 2^28: magic on Bq / 64, error <= 64 (margin); M folded
                 bq = __int_as_float(((n * mx - rsr * sd) >> 6) + 0x4B400000);  // (x 64 in nhs)
             } else {
-                bq = fmaf((float)n, (float)mx, -((float)rsr * (float)sd));
+                // QR (B >= 16, one or two s): Bq exact in int64, one RN conversion (the fp32
+                // product form rounded n max and SR SD separately: a margin term n 1020 SR that
+                // let ~8x more pairs through to the exact path)
+                bq = (float)((long long)n * mx - (long long)rsr * sd);
             }
             float g0;
             if constexpr (NSP == 3) {
@@ -1096,24 +1099,23 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
             plan_segment(&plan, k, grp, ta, ntl, slot, lastseg);
             const int r0 = grp * NR;
             // ---- segment setup: this group's range constants and thresholds (the previous
-            // segment's readers of sR / sThr / sRed have passed the barrier)
+            // segment's readers of sR / sThr / sRB have passed the barrier)
             epi_sync();
             if (et == 0) TC_TR_SEG(23, k);
             if (et < NR) {
                 const TCRange R = P.rmeta[r0 + et];
                 sR[et] = R;
+                Partial pb;  // s = 0 (if listed): e = A for every (domain, k) -> (A, 0, 0, j_zero)
+                if (P.has_zero) { pb.e = R.A; pb.d = 0; pb.kj = P.j_zero; }
+                else { pb.e = INFINITY; pb.d = INT_MAX; pb.kj = INT_MAX; }
+#pragma unroll
+                for (int w = 0; w < Cf::RBW; ++w) sRB[et * Cf::RBW + w] = pb;
                 sSR[et] = Cf::F16 ? __float_as_int(-(float)R.SR) : R.SR;
                 const float th = P.has_zero ? fminf(__double2float_ru(R.margin), FLT_MAX) : FLT_MAX;
                 sThr[et] = R.valid ? th : -FLT_MAX;
                 sM2[et] = fminf(__double2float_ru(2.0 * R.margin), FLT_MAX);
             }
             epi_sync();
-            for (int q = 0; q < HALF; ++q) {
-                Partial pb;
-                if (P.has_zero) { pb.e = sR[eg * HALF + q].A; pb.d = 0; pb.kj = P.j_zero; }
-                else { pb.e = INFINITY; pb.d = INT_MAX; pb.kj = INT_MAX; }
-                sBest[(eg * HALF + q) * kTileD + m] = pb;
-            }
             int rSR[HALF];
 #pragma unroll
             for (int q = 0; q < HALF; ++q)
@@ -1288,43 +1290,11 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
             epi_sync();
             if (et == 0) TC_TR_SEG(26, k);
             __threadfence_block();
-            // ---- reduce each range's best over the 128 domain lanes (lexicographic); the HALF
-            // shuffle chains interleaved (independent ranges)
-            {
-                double e0[HALF];
-                int32_t d0[HALF], kj0[HALF];
-#pragma unroll
-                for (int q = 0; q < HALF; ++q) {
-                    const Partial mine = sBest[(eg * HALF + q) * kTileD + m];
-                    e0[q] = mine.e; d0[q] = mine.d; kj0[q] = mine.kj;
-                }
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) {
-#pragma unroll
-                    for (int q = 0; q < HALF; ++q) {
-                        const double oe = __shfl_xor_sync(0xffffffffu, e0[q], o);
-                        const int od = __shfl_xor_sync(0xffffffffu, d0[q], o);
-                        const int okj = __shfl_xor_sync(0xffffffffu, kj0[q], o);
-                        if (oe < e0[q] || (oe == e0[q] && (od < d0[q] || (od == d0[q] && okj < kj0[q])))) {
-                            e0[q] = oe; d0[q] = od; kj0[q] = okj;
-                        }
-                    }
-                }
-                if (lane == 0) {
-#pragma unroll
-                    for (int q = 0; q < HALF; ++q) {
-                        Partial pb;
-                        pb.e = e0[q]; pb.d = d0[q]; pb.kj = kj0[q];
-                        sRed[(eg * HALF + q) * 4 + lq] = pb;
-                    }
-                }
-            }
-            epi_sync();
             if (et < NR) {  // the segment's partial of each range; the group's last segment also
                 const int r = r0 + et;  // fills the unused slots
-                Partial b = sRed[et * 4];
-                for (int w = 1; w < 4; ++w) {
-                    const Partial c = sRed[et * 4 + w];
+                Partial b = sRB[et * Cf::RBW];
+                for (int w = 1; w < Cf::RBW; ++w) {
+                    const Partial c = sRB[et * Cf::RBW + w];
                     if (c.e < b.e || (c.e == b.e && (c.d < b.d || (c.d == b.d && c.kj < b.kj)))) b = c;
                 }
                 if (r < n_r) {
@@ -1352,8 +1322,8 @@ template <int B, int NSP>
 static size_t tc_smem_bytes() {
     using Cf = TCfg<B>;
     return (size_t)Cf::STAGES * Cf::STAGE_BYTES + Cf::BBUF * Cf::B_BYTES + sizeof(TCRange) * Cf::NR + 4 * Cf::NR +
-           4 * 16 + 4 * Cf::NR + sizeof(Partial) * Cf::NR * 4 + 8 * (2 * Cf::STAGES + 2 * Cf::NBUF + 4) + 16 +
-           sizeof(Partial) * Cf::NR * kTileD + (sizeof(XItem) + 4) * Cf::XQ + 16 + 4 * Cf::NR + 1024;
+           4 * 16 + 4 * Cf::NR + sizeof(Partial) * Cf::NR * Cf::RBW + 8 * (2 * Cf::STAGES + 2 * Cf::NBUF + 4) + 16 +
+           (sizeof(XItem) + 4) * Cf::XQ + 16 + 4 * Cf::NR + 1024;
 }
 
 template <int B, int NSP>
