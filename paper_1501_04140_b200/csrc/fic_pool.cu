@@ -17,6 +17,17 @@ namespace fic {
 
 // ------------------------------------------------------------------------------------ entropy
 
+// Exact warp sum of int64 values in three 22-bit limbs (each limb sum < 2^27 over 32 lanes, the
+// top limb signed): three single-instruction warp reductions instead of five 64-bit shuffle
+// rounds.
+__device__ __forceinline__ int64_t warp_sum_i64(int64_t v) {
+    const int l0 = (int)(v & 0x3FFFFF), l1 = (int)((v >> 22) & 0x3FFFFF), l2 = (int)(v >> 44);
+    const int s0 = __reduce_add_sync(0xffffffffu, l0);
+    const int s1 = __reduce_add_sync(0xffffffffu, l1);
+    const int s2 = __reduce_add_sync(0xffffffffu, l2);
+    return (int64_t)s0 + ((int64_t)s1 << 22) + ((int64_t)s2 << 44);
+}
+
 // One warp per candidate (grid-stride).  Each warp owns a 256-bin histogram in shared memory.
 // The key is accumulated while the histogram is built: inserting a pixel into a bin holding
 // `old` pixels adds delta[old] = LUT[old+1] - LUT[old], so after all m insertions the sum is
@@ -33,21 +44,22 @@ __global__ void __launch_bounds__(256) entropy_keys_kernel(
     __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     int32_t *hist = hist_all + warp * 256;
+    const int lgs = __ffs(side) - 1;
     const int64_t n_c = (int64_t)A * A;
     const int64_t wstride = (int64_t)gridDim.x * (blockDim.x >> 5);
     for (int64_t c = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp; c < n_c; c += wstride) {
         for (int v = lane; v < 256; v += 32) hist[v] = 0;
         __syncwarp();
         const int64_t x = (c % A) * L, y = (c / A) * L;
+        const uint8_t *base = img + y * N + x;
         int64_t acc = 0;
-        for (int idx = lane; idx < m; idx += 32) {
-            const int i = idx / side, j = idx - (idx / side) * side;
-            const int v = img[(y + i) * (int64_t)N + x + j];
+        for (int idx = lane; idx < m; idx += 32) {  // side = 2B is a power of two
+            const int i = idx >> lgs, j = idx & (side - 1);
+            const int v = base[i * N + j];
             const int old = atomicAdd(&hist[v], 1);
             acc += delta[old];
         }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        acc = warp_sum_i64(acc);
         if (lane == 0) {
             const int64_t key = lut_m - acc;
             keys[c] = key;
@@ -82,22 +94,38 @@ __global__ void __launch_bounds__(256) entropy_slide_kernel(
     if (w >= (int64_t)A * segs) return;
     const int b = (int)(w / segs), a0 = (int)(w % segs) * kSlideSeg, a1 = min(A, a0 + kSlideSeg);
     const int64_t y = (int64_t)b * L;
+    const uint8_t *rowbase = img + y * N;  // the warp's band of rows
     for (int v = lane; v < 256; v += 32) hist[v] = 0;
     __syncwarp();
     int64_t acc = 0;
     {
-        const int64_t x = (int64_t)a0 * L;
+        const uint8_t *base = rowbase + (int64_t)a0 * L;
+        const int lgs = __ffs(side) - 1;  // side = 2B is a power of two
         for (int idx = lane; idx < m; idx += 32) {
-            const int i = idx / side, j = idx - i * side;
-            const int old = atomicAdd(&hist[img[(y + i) * (int64_t)N + x + j]], 1);
+            const int old = atomicAdd(&hist[base[(idx >> lgs) * N + (idx & (side - 1))]], 1);
             acc += delta[old];
         }
     }
     const int nu = L * side;  // pixels leaving (and entering) per step
-    for (int a = a0;; ++a) {
-        int64_t tot = acc;
+    // this lane's pixels of a step are the same for every step (relative to x = a L): their
+    // offsets (leaving columns x .. x + L - 1, entering x + side ..) are formed once, so the step
+    // loop has no division by L and no 64-bit address arithmetic
+    constexpr int kSlots = 8;
+    int off[kSlots];
+    unsigned leaving = 0, valid = 0;
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+    for (int t = 0; t < kSlots; ++t) {
+        const int u = lane + 32 * t;
+        const bool lv = u < nu;
+        const int uu = lv ? u : u - nu;
+        const int i = uu / L, j = uu - (uu / L) * L;
+        off[t] = i * N + j + (lv ? 0 : side);
+        if (u < 2 * nu) valid |= 1u << t;
+        if (lv) leaving |= 1u << t;
+    }
+    const bool fits = 2 * nu <= 32 * kSlots;
+    for (int a = a0;; ++a) {
+        const int64_t tot = warp_sum_i64(acc);
         if (lane == 0) {
             const int64_t key = lut_m - tot;
             const int64_t c = (int64_t)b * A + a;
@@ -106,16 +134,31 @@ __global__ void __launch_bounds__(256) entropy_slide_kernel(
         }
         if (a + 1 >= a1) break;
         __syncwarp();
-        const int64_t x = (int64_t)a * L;
-        for (int u = lane; u < 2 * nu; u += 32) {
-            const int uu = u < nu ? u : u - nu;
-            const int i = uu / L, j = uu - i * L;
-            if (u < nu) {  // leaving column x + j
-                const int old = atomicSub(&hist[img[(y + i) * (int64_t)N + x + j]], 1);
-                acc -= delta[old - 1];
-            } else {       // entering column x + side + j
-                const int old = atomicAdd(&hist[img[(y + i) * (int64_t)N + x + side + j]], 1);
-                acc += delta[old];
+        const uint8_t *base = rowbase + (int64_t)a * L;
+        if (fits) {
+#pragma unroll
+            for (int t = 0; t < kSlots; ++t) {
+                if (!((valid >> t) & 1u)) continue;
+                const int v = base[off[t]];
+                if ((leaving >> t) & 1u) {  // leaving column x + j
+                    const int old = atomicSub(&hist[v], 1);
+                    acc -= delta[old - 1];
+                } else {                    // entering column x + side + j
+                    const int old = atomicAdd(&hist[v], 1);
+                    acc += delta[old];
+                }
+            }
+        } else {
+            for (int u = lane; u < 2 * nu; u += 32) {
+                const int uu = u < nu ? u : u - nu;
+                const int i = uu / L, j = uu - i * L;
+                if (u < nu) {
+                    const int old = atomicSub(&hist[base[i * N + j]], 1);
+                    acc -= delta[old - 1];
+                } else {
+                    const int old = atomicAdd(&hist[base[i * N + side + j]], 1);
+                    acc += delta[old];
+                }
             }
         }
         __syncwarp();
