@@ -109,7 +109,7 @@ void free_buf(Buf &b) {
 void free_pool(Pool &P) {
     free_buf(P.b_keys); free_buf(P.b_keep); free_buf(P.b_kept);
     free_buf(P.b_SDf); free_buf(P.b_SD); free_buf(P.b_C); free_buf(P.b_misc);
-    free_buf(P.b_Dtc); free_buf(P.b_F2); free_buf(P.b_blocksum); free_buf(P.b_topk); free_buf(P.b_t2f);
+    free_buf(P.b_Dtc); free_buf(P.b_D2); free_buf(P.b_F2); free_buf(P.b_blocksum); free_buf(P.b_topk); free_buf(P.b_t2f);
 }
 
 bool pow2(int32_t v) { return v > 0 && (v & (v - 1)) == 0; }
@@ -150,6 +150,7 @@ fic_status pool_enqueue(fic_ctx *ctx, Pool &P, const uint8_t *img, int32_t N, in
     CK(grow(ctx, P.b_kept, sizeof(int32_t) * P.n_c));
     P.mode = B == 2 ? 3 : 0;  // B = 2: closed form on CUDA cores (fic_b2.cu); else tcgen05 (fic_tc.cu)
     if (P.mode == 0) CK(grow(ctx, P.b_Dtc, fic::tc_pool_bytes(B, tiles_max)));
+    if (P.mode == 0 && fic::tc_pool_d2_bytes(B, N, L)) CK(grow(ctx, P.b_D2, fic::tc_pool_d2_bytes(B, N, L)));
     if (P.mode == 3) CK(grow(ctx, P.b_F2, fic::b2_pool_bytes(slots)));
     CK(grow(ctx, P.b_SDf, sizeof(float) * slots));
     CK(grow(ctx, P.b_SD, sizeof(int32_t) * slots));
@@ -177,14 +178,15 @@ fic_status pool_enqueue(fic_ctx *ctx, Pool &P, const uint8_t *img, int32_t N, in
                                 d_kept_mirror));
     if (P.mode == 0)
         CK(fic::launch_pool_tc(img, N, B, L, P.A, P.kept, &P.d_misc[0], tiles_max, P.Dtc, P.SD, P.SDf, P.C,
-                               &P.d_misc[1], st));
+                               &P.d_misc[1], fic::tc_pool_d2_bytes(B, N, L) ? ptr<uint16_t>(P.b_D2) : nullptr, st));
     else
         CK(fic::launch_b2_pool(img, N, L, P.A, P.kept, &P.d_misc[0], slots, P.b_F2.p, &P.b2, st));
     const bool fused = P.mode == 0 && fic::tc_pool_has_moments(B);
     if (!fused)
         CK(fic::launch_pool_moments(img, N, B, L, P.A, P.kept, &P.d_misc[0], slots, P.SD, P.SDf, P.C,
                                     &P.d_misc[1], st));
-    ctx->launches += 6 + (P.mode == 3 ? 1 : 0) - (fused ? 1 : 0);  // entropy, select x3, gather, moments
+    // entropy, select x3, gather, moments (+ the decimated image of the QR pools)
+    ctx->launches += 6 + (P.mode == 3 ? 1 : 0) - (fused ? 1 : 0) + (fic::tc_pool_d2_bytes(B, N, L) ? 1 : 0);
     return FIC_OK;
 }
 

@@ -55,7 +55,7 @@ struct Pool {
     int64_t *C = nullptr;
     unsigned long long *d_misc = nullptr;  // [0] = n_kept, [1] = Cmax, [2] = max |dh|_2 (float bits)
     double dnmax = 0.0;
-    Buf b_keys, b_keep, b_kept, b_SDf, b_SD, b_C, b_misc, b_Dtc, b_F2, b_blocksum, b_topk;
+    Buf b_keys, b_keep, b_kept, b_SDf, b_SD, b_C, b_misc, b_Dtc, b_F2, b_blocksum, b_topk, b_D2;
     Buf b_t2f;           // fp32 filter table of this level, enqueued with the pool (fic_encode)
     int t2f_ready = 0;   // b_t2f holds the table for the level's s set (reset after the level)
     int device = 0;
@@ -304,10 +304,12 @@ size_t tc_pool_bytes(int B, int64_t n_tiles);
 int tc_nsplit_hint(int32_t B, int64_t n_r, int64_t n_tiles, int num_sms);
 // also writes SD, SDf, C and Cmax when tc_pool_has_moments(B) (pool_moments_kernel is skipped)
 int tc_pool_has_moments(int B);
+// D2: workspace of tc_pool_d2_bytes(B, N, L) bytes (the 2 x 2 decimated image, B >= 16), else null
+size_t tc_pool_d2_bytes(int B, int32_t N, int32_t L);
 cudaError_t launch_pool_tc(const uint8_t *img, int32_t N, int32_t B, int32_t L, int32_t A,
                            const int32_t *kept, const unsigned long long *d_nk, int64_t n_tiles_max,
                            uint8_t *Dtc, int32_t *SD, float *SDf, int64_t *C, unsigned long long *d_cmax,
-                           cudaStream_t st);
+                           uint16_t *D2, cudaStream_t st);
 size_t tc_range_bytes(int B, int64_t n_r);  // scratch for the prepared range operand + metadata
 cudaError_t launch_tc_search(int32_t B, const SearchParams &sp, const uint8_t *Dtc, int64_t n_slots,
                              uint8_t *scratch, cudaStream_t st);

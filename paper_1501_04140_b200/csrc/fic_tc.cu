@@ -62,6 +62,16 @@ struct TCfg {
 #ifndef FIC_B4_NR
 #define FIC_B4_NR 24
 #endif
+#ifndef FIC_PROD_WARP
+#define FIC_PROD_WARP 0
+#define FIC_MMA_WARP 1
+#endif
+#ifndef FIC_PROD_NS
+#define FIC_PROD_NS 0
+#endif
+#ifndef FIC_MMA_NS
+#define FIC_MMA_NS 0
+#endif
 #ifndef FIC_B4_EWG
 #define FIC_B4_EWG 3
 #endif
@@ -73,7 +83,10 @@ struct TCfg {
     static constexpr int CH = KP / KCH;                    // stages per domain tile
     static constexpr int STAGE_BYTES = kTileD * KCH;       // A bytes per stage
     // B = 16 is fed by bulk copies (latency x bytes in flight): 8 x 16 KB stages
-    static constexpr int STAGES = QR ? 2 : F16 ? (B == 4 ? 8 : 4) : (B == 8 ? 2 : 4);
+#ifndef FIC_B4_STAGES
+#define FIC_B4_STAGES 8
+#endif
+    static constexpr int STAGES = QR ? 2 : F16 ? (B == 4 ? FIC_B4_STAGES : 4) : (B == 8 ? 2 : 4);
     static constexpr int B_BYTES = N * KB;                 // resident range operand
     // range-operand buffers: 2 where shared memory allows, so the next segment's operand loads
     // while the current segment's MMAs still read the other one
@@ -133,6 +146,21 @@ __device__ __forceinline__ void tmbar_wait(uint64_t *bar, uint32_t parity) {
             : "=r"(done)
             : "r"(su32(bar)), "r"(parity)
             : "memory");
+    }
+}
+// the producer's and MMA warp's waits: probe, then sleep ns between probes -- a spinning control
+// warp takes issue slots from the three epilogue warps of its SM sub-partition, which then lag
+// the others and (through the shared TMEM buffers) pace the whole tile ring
+__device__ __forceinline__ void tmbar_wait_sleep(uint64_t *bar, uint32_t parity, uint32_t ns) {
+    uint32_t done = 0;
+    for (;;) {
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+            : "=r"(done)
+            : "r"(su32(bar)), "r"(parity)
+            : "memory");
+        if (done) break;
+        __nanosleep(ns);
     }
 }
 __device__ __forceinline__ void tbulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
@@ -384,92 +412,137 @@ __global__ void __launch_bounds__(256) pool_tc_kernel(const uint8_t *__restrict_
     }
 }
 
-// QR pool (B = 16, 32), warp per domain (grid-stride over the slots): the raw 2B x 2B block read
-// as 32 / RW rows x RW words per load (RW = B / 2 words per raw row; coalesced), the 2 x 2 sums
-// formed with one packed add per word and one shuffle between the two rows of a pair, written as
-// the q = D' >> 2 and r = D' & 3 planes (two bytes per lane per decimated row), and SD, SDD -> C
-// reduced over the warp.  (Previously each thread formed one decimated row: the 16 rows of a
-// domain per half-warp, uncoalesced.)  Rows that are not word-aligned (N % 4 != 0) are read
-// bytewise.
+// QR pool (B = 16, 32) in two launches.  (1) decimate_kernel: the 2 x 2 sums of the whole image
+// once per parity class (y & 1, x & 1) -- one class when L is even (every domain corner is even),
+// four when L is odd -- as uint16 planes D2_p[u][v] = the 2 x 2 block at (2u + oy, 2v + ox), so
+// D'(i, j) of the domain at (x, y) is D2_{(y&1, x&1)}[(y >> 1) + i][(x >> 1) + j].  (2)
+// pool_qr_kernel: warp per domain (grid-stride over the slots), each lane one or four chunks of 8
+// consecutive D' of a row: q = D' >> 2 and r = D' & 3 packed to 8 bytes each (one 8-byte store per
+// plane into the K-major core-matrix layout), SD, SDD in int32 (< 2^31 at n = 1024) reduced with
+// REDUX.  The 2 x 2 sums, previously formed per domain from the raw 2B x 2B block (each image pixel
+// of a C3 pool read ~(2B / L)^2 = 256 times, 333 warp instructions per domain), are formed once.
+__host__ __device__ __forceinline__ int d2_pitch(int32_t N) { return ((N / 2 + 7) & ~7) + 8; }  // elements
+__global__ void __launch_bounds__(256) decimate_kernel(const uint8_t *__restrict__ img, int32_t N, int32_t planes,
+                                                       uint16_t *__restrict__ D2) {
+    const int H = N / 2, W = d2_pitch(N);  // rows of W elements (16-byte aligned, zero padded)
+    const int64_t per = (int64_t)H * W;
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= per * planes) return;
+    const int p = (int)(e / per);
+    const int rem = (int)(e - (int64_t)p * per);
+    const int u = rem / W, v = rem - (rem / W) * W;
+    const int oy = p >> 1, ox = p & 1;
+    const int y = 2 * u + oy, x = 2 * v + ox;
+    uint16_t s = 0;
+    if (v < H && y + 1 < N && x + 1 < N) {
+        const uint8_t *r0 = img + (size_t)y * N + x;
+        s = (uint16_t)(r0[0] + r0[1] + r0[N] + r0[N + 1]);
+    }
+    D2[e] = s;
+}
+
 template <int B>
-__global__ void __launch_bounds__(256) pool_qr_kernel(const uint8_t *__restrict__ img, int32_t N, int32_t L,
+__global__ void __launch_bounds__(256) pool_qr_kernel(const uint16_t *__restrict__ D2, int32_t N, int32_t L,
                                                        int32_t A, const int32_t *__restrict__ kept,
                                                        const unsigned long long *__restrict__ d_nk,
                                                        uint8_t *__restrict__ Dtc, int32_t *__restrict__ SD,
                                                        float *__restrict__ SDf, int64_t *__restrict__ Cm,
                                                        unsigned long long *d_cmax) {
     using Cf = TCfg<B>;
-    constexpr int RW = B / 2;         // words per raw row (2B bytes)
-    constexpr int RPI = 32 / RW;      // raw rows per warp load
-    constexpr int ITS = 2 * B / RPI;  // loads per domain
-    static_assert(Cf::QR && RPI % 2 == 0, "QR pool");
-    const int lane = threadIdx.x & 31;
+    constexpr int CPR = B / 8;            // 8-column chunks per decimated row
+    constexpr int CPL = B * CPR / 32;     // chunks per lane (1 at B = 16, 4 at B = 32)
+    constexpr int GB = 8 * Cf::KCH;       // bytes of one 8-domain group in one stage (contiguous)
+    constexpr int CMP = 144;              // padded core matrix in shared memory (128 B + 16)
+    static_assert(Cf::QR && CPL >= 1, "QR pool (launched with 256 threads: 8 warps = 8 domains)");
+    // the CTA's 8 domains (one per warp) staged in the core-matrix layout of their 8 rows, so the
+    // tile is written with coalesced 16-byte stores of whole 128-byte core matrices (writing each
+    // domain's rows straight to global memory touched 64 partial sectors per domain)
+    __shared__ __align__(16) uint8_t stg[Cf::CH * (GB / 128) * CMP];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int H = N / 2, W = d2_pitch(N);
     const int64_t n_k = (int64_t)*d_nk;
     const int64_t slots = ((n_k + kTileD - 1) / kTileD) * kTileD;
-    const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    const int rr = lane / RW, w = lane % RW;  // row in the group, word in the row
-    const bool wordwise = (N & 3) == 0 && (reinterpret_cast<uintptr_t>(img) & 3) == 0;
     unsigned long long cmax = 0;
-    for (int64_t d = wid; d < slots; d += nw) {
-        const int64_t tile = d / kTileD;
-        const int m = (int)(d - tile * kTileD);
-        uint8_t *tb = Dtc + (size_t)tile * Cf::CH * Cf::STAGE_BYTES;  // [tile][chunk][128 x KCH]
-        auto put2 = [&](int kb, uint16_t v) {
-            *reinterpret_cast<uint16_t *>(tb + (size_t)(kb / Cf::KCH) * Cf::STAGE_BYTES + cm_off(m, kb % Cf::KCH, Cf::KCH)) = v;
+    for (int64_t g0 = (int64_t)blockIdx.x * 8; g0 < slots; g0 += (int64_t)gridDim.x * 8) {
+        const int64_t d = g0 + w;
+        int sd = 0, sdd = 0;
+        auto put8 = [&](int kb, uint2 v) {  // 8 bytes at K byte kb of this warp's domain
+            const int ch = kb / Cf::KCH, kc = kb % Cf::KCH;
+            *reinterpret_cast<uint2 *>(stg + (ch * (GB / 128) + (kc >> 4)) * CMP + w * 16 + (kc & 15)) = v;
         };
-        int sd = 0;
-        long long sdd = 0;
         if (d < n_k) {
             const int32_t c = kept[d];
-            const int64_t x = (int64_t)(c % A) * L, y = (int64_t)(c / A) * L;
-            const uint8_t *r0 = img + y * N + x;
-            const uint32_t sh = (uint32_t)(reinterpret_cast<uintptr_t>(r0) & 3) * 8;
-            const uint32_t *wrow0 = reinterpret_cast<const uint32_t *>(reinterpret_cast<uintptr_t>(r0) & ~(uintptr_t)3);
-#pragma unroll 2
-            for (int it = 0; it < ITS; ++it) {
-                uint32_t v;
-                if (wordwise) {
-                    const uint32_t *wr = wrow0 + (size_t)(RPI * it + rr) * (N / 4);
-                    const uint32_t lo = __ldg(wr + w);
-                    uint32_t hi = __shfl_down_sync(0xffffffffu, lo, 1);
-                    if (w == RW - 1) hi = sh ? __ldg(wr + RW) : 0u;  // (N % 4 == 0: within the row)
-                    v = __funnelshift_r(lo, hi, sh);                 // pixels 4w .. 4w + 3
-                } else {
-                    const uint8_t *pb = r0 + (size_t)(RPI * it + rr) * N + 4 * w;
-                    v = (uint32_t)pb[0] | ((uint32_t)pb[1] << 8) | ((uint32_t)pb[2] << 16) | ((uint32_t)pb[3] << 24);
+            const int x = (c % A) * L, y = (c / A) * L;
+            // the 8 D' of a chunk are 16 bytes at an even byte offset sh within a 16-byte-aligned
+            // 32-byte window: two aligned 16-byte loads, then words q .. q + 4 selected and
+            // funnel-shifted by (sh & 3) bytes (the same shift for every chunk of the domain)
+            const int col = x >> 1;
+            const uint16_t *base = D2 + (size_t)(((y & 1) << 1) | (x & 1)) * H * W + (size_t)(y >> 1) * W + (col & ~7);
+            const int sh = (col & 7) * 2, qs = sh >> 2;
+            const uint32_t fs = (uint32_t)(sh & 3) * 8;
+#pragma unroll
+            for (int t = 0; t < CPL; ++t) {
+                const int chk = lane + 32 * t;
+                const int i = chk / CPR, h = chk % CPR;
+                const uint4 *src = reinterpret_cast<const uint4 *>(base + (size_t)i * W + 8 * h);
+                const uint4 lo = __ldg(src), hi = __ldg(src + 1);
+                const uint32_t wv[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+                uint32_t sel[5];
+#pragma unroll
+                for (int k = 0; k < 5; ++k)
+                    sel[k] = qs == 0 ? wv[k] : qs == 1 ? wv[k + 1] : qs == 2 ? wv[k + 2] : wv[(k + 3) & 7];
+                uint32_t pr[4];  // D' pairs (2 x 16 bits)
+#pragma unroll
+                for (int k = 0; k < 4; ++k) pr[k] = __funnelshift_r(sel[k], sel[k + 1], fs);
+                uint32_t qv[4], rv[4];
+                uint32_t s2 = 0;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    qv[k] = (pr[k] >> 2) & 0x00FF00FFu;
+                    rv[k] = pr[k] & 0x00030003u;
+                    s2 += pr[k];  // two 16-bit lanes, each <= 4 * 1020
+                    const int a = (int)(pr[k] & 0xFFFFu), b = (int)(pr[k] >> 16);
+                    sdd += a * a + b * b;
                 }
-                const uint32_t h = (v & 0x00FF00FFu) + ((v >> 8) & 0x00FF00FFu);  // 2 horizontal pairs
-                const uint32_t dd = h + __shfl_down_sync(0xffffffffu, h, RW);   // + the row below
-                if ((rr & 1) == 0) {
-                    const int i = (RPI / 2) * it + (rr >> 1);  // decimated row; columns 2w, 2w + 1
-                    const int a = (int)(dd & 0xFFFFu), b = (int)(dd >> 16);
-                    sd += a + b;
-                    sdd += (long long)(a * a + b * b);
-                    const int kq = B * i + 2 * w;  // K byte of (i, 2w) in the q plane; r plane at n + kq
-                    put2(kq, (uint16_t)((a >> 2) | ((b >> 2) << 8)));
-                    put2(Cf::n + kq, (uint16_t)((a & 3) | ((b & 3) << 8)));
-                }
+                sd += (int)(s2 & 0xFFFFu) + (int)(s2 >> 16);
+                const int kb = B * i + 8 * h;  // K byte of (i, 8h) in the q plane; the r plane at n + kb
+                put8(kb, make_uint2(__byte_perm(qv[0], qv[1], 0x6420), __byte_perm(qv[2], qv[3], 0x6420)));
+                put8(Cf::n + kb, make_uint2(__byte_perm(rv[0], rv[1], 0x6420), __byte_perm(rv[2], rv[3], 0x6420)));
             }
         } else {  // pad rows of the last tile: zero q and r planes
-            for (int kb = 16 * lane; kb < Cf::KP; kb += 16 * 32)
-                *reinterpret_cast<uint4 *>(tb + (size_t)(kb / Cf::KCH) * Cf::STAGE_BYTES + cm_off(m, kb % Cf::KCH, Cf::KCH)) =
-                    make_uint4(0, 0, 0, 0);
-        }
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            sd += __shfl_xor_sync(0xffffffffu, sd, o);
-            sdd += __shfl_xor_sync(0xffffffffu, sdd, o);
+            for (int t = 0; t < 2 * CPL; ++t) put8(8 * (lane + 32 * t), make_uint2(0u, 0u));
         }
-        const long long cc = (long long)Cf::n * sdd - (long long)sd * sd;
-        if (lane == 0) {
-            SD[d] = sd;
-            SDf[d] = (float)sd;
-            Cm[d] = cc;
+        sd = __reduce_add_sync(0xffffffffu, sd);
+        sdd = (int)__reduce_add_sync(0xffffffffu, (unsigned)sdd);
+        if (d < slots) {
+            const long long cc = (long long)Cf::n * sdd - (long long)sd * sd;
+            if (lane == 0) {
+                SD[d] = sd;
+                SDf[d] = (float)sd;
+                Cm[d] = cc;
+            }
+            if (d < n_k && (unsigned long long)cc > cmax) cmax = (unsigned long long)cc;
         }
-        if (d < n_k && (unsigned long long)cc > cmax) cmax = (unsigned long long)cc;
+        __syncthreads();
+        {  // the group's CH x GB bytes, 16 per thread per pass (slots are a multiple of kTileD = 128)
+            const int64_t tile = g0 / kTileD;
+            const int grp = (int)((g0 - tile * kTileD) >> 3);
+            uint8_t *dst = Dtc + (size_t)tile * Cf::CH * Cf::STAGE_BYTES + (size_t)grp * GB;
+            for (int e = threadIdx.x; e < Cf::CH * GB / 16; e += blockDim.x) {
+                const int ch = e / (GB / 16), r = e % (GB / 16);
+                const uint4 v = *reinterpret_cast<const uint4 *>(stg + (ch * (GB / 128) + (r >> 3)) * CMP + (r & 7) * 16);
+                *reinterpret_cast<uint4 *>(dst + (size_t)ch * Cf::STAGE_BYTES + (size_t)r * 16) = v;
+            }
+        }
+        __syncthreads();
     }
     block_max_atomic(cmax, d_cmax);
+}
+
+size_t tc_pool_d2_bytes(int B, int32_t N, int32_t L) {
+    if (B < 16) return 0;
+    return (L % 2 == 0 ? 1 : 4) * (size_t)(N / 2) * (size_t)d2_pitch(N) * sizeof(uint16_t);
 }
 
 int tc_supported(int B) { return B == 4 || B == 8 || B == 16 || B == 32; }
@@ -489,7 +562,7 @@ int tc_pool_has_moments(int B) { return B >= 16; }
 cudaError_t launch_pool_tc(const uint8_t *img, int32_t N, int32_t B, int32_t L, int32_t A,
                            const int32_t *kept, const unsigned long long *d_nk, int64_t n_tiles_max,
                            uint8_t *Dtc, int32_t *SD, float *SDf, int64_t *C, unsigned long long *d_cmax,
-                           cudaStream_t st) {
+                           uint16_t *D2, cudaStream_t st) {
     int g16 = 0;
     switch (B) {
     case 4: g16 = TCfg<4>::KP / 16; break;
@@ -504,14 +577,15 @@ cudaError_t launch_pool_tc(const uint8_t *img, int32_t N, int32_t B, int32_t L, 
     switch (B) {
     case 4: pool_tc_kernel<4><<<blocks, 256, 0, st>>>(img, N, L, A, kept, d_nk, total16, Dtc, SD, SDf, C, d_cmax); break;
     case 8: pool_tc_kernel<8><<<blocks, 256, 0, st>>>(img, N, L, A, kept, d_nk, total16, Dtc, SD, SDf, C, d_cmax); break;
-    case 16: {  // warp per domain (pool_qr_kernel)
-        const unsigned bq = (unsigned)std::min<int64_t>((n_tiles_max * kTileD + 7) / 8, 148 * 16);
-        pool_qr_kernel<16><<<bq, 256, 0, st>>>(img, N, L, A, kept, d_nk, Dtc, SD, SDf, C, d_cmax);
-        break;
-    }
-    case 32: {
-        const unsigned bq = (unsigned)std::min<int64_t>((n_tiles_max * kTileD + 7) / 8, 148 * 16);
-        pool_qr_kernel<32><<<bq, 256, 0, st>>>(img, N, L, A, kept, d_nk, Dtc, SD, SDf, C, d_cmax);
+    case 16:
+    case 32: {  // decimated image, then warp per domain (pool_qr_kernel)
+        if (!D2) return cudaErrorInvalidValue;
+        const int64_t d2n = (int64_t)(tc_pool_d2_bytes(B, N, L) / sizeof(uint16_t));
+        decimate_kernel<<<(unsigned)((d2n + 255) / 256), 256, 0, st>>>(img, N, L % 2 == 0 ? 1 : 4, D2);
+        // one wave (6 CTAs of 256 threads per SM at <= 40 registers), grid-stride over the groups
+        const unsigned bq = (unsigned)std::min<int64_t>((n_tiles_max * kTileD + 7) / 8, 148 * 6);
+        if (B == 16) pool_qr_kernel<16><<<bq, 256, 0, st>>>(D2, N, L, A, kept, d_nk, Dtc, SD, SDf, C, d_cmax);
+        else pool_qr_kernel<32><<<bq, 256, 0, st>>>(D2, N, L, A, kept, d_nk, Dtc, SD, SDf, C, d_cmax);
         break;
     }
     }
@@ -666,7 +740,9 @@ __global__ void __launch_bounds__(256) tc_range_prep_kernel(const uint8_t *__res
 // Diagnostics only (-DFIC_TC_TRACE, scripts/tc_trace.py): clock64 stamps of CTA 0's pipeline
 // events -- 0 producer copy issued, 1 MMA saw the stage full, 2 MMA saw the accumulator free,
 // 3 MMA committed the tile, 4 epilogue warp 2 saw the tile, 5 its loads done, 6 its tile done,
-// 7 the last epilogue warp's tile done, 8 + w - 2 epilogue warp w's loads done.
+// 7 the last epilogue warp's tile done, 8 + w - 2 epilogue warp w's loads done; row 29: per
+// epilogue warp w, [2w] cycles of tile work, [2w + 1] cycles waiting for tiles, [64 + 2w] cycles
+// in push blocks, [64 + 2w + 1] push blocks.
 #ifdef FIC_TC_TRACE
 __device__ long long g_tc_trace[32][4096];
 #define TC_TR(kind, idx)                                                           \
@@ -852,7 +928,7 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
     tc_fence_after();
     const uint32_t tmem = *sTmem;
 
-    if (warp == 0) {
+    if (warp == FIC_PROD_WARP) {
         // ================= producer: one lane issues every bulk copy in order -- each segment's
         // range operand (once the MMAs of the segment BBUF earlier released its buffer) and the A
         // stages (stage / phase carried incrementally; the (tile, chunk) stages of a segment are
@@ -871,7 +947,11 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
                 tbulk_g2s(sB + kb * Cf::B_BYTES, P.Bop + (size_t)grp * Cf::B_BYTES, Cf::B_BYTES, &bbar[kb]);
                 const uint8_t *src = P.Dtc + (size_t)ta * CH * Cf::STAGE_BYTES;
                 for (int c = 0; c < ntl * CH; ++c, ++i) {
+#if FIC_PROD_NS
+                    if (i >= STAGES) tmbar_wait_sleep(&empty[s], ph ^ 1u, FIC_PROD_NS);
+#else
                     if (i >= STAGES) tmbar_wait(&empty[s], ph ^ 1u);
+#endif
                     tmbar_expect_tx(&full[s], Cf::STAGE_BYTES);
                     TC_TR(0, i);
                     tbulk_g2s(sA + s * Cf::STAGE_BYTES, src, Cf::STAGE_BYTES, &full[s]);
@@ -880,7 +960,7 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
                 }
             }
         }
-    } else if (warp == 1) {
+    } else if (warp == FIC_MMA_WARP) {
         // ================= MMA issuer
         constexpr uint32_t idesc = Cf::F16 ? idesc_f16(NN) : idesc_i8(NN);
         int i = 0, tl = 0;
@@ -898,9 +978,15 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
                 const int buf = tl % NBUF;
                 for (int ch = 0; ch < CH; ++ch, ++i) {
                     const int s = i % STAGES;
+#if FIC_MMA_NS
+                    tmbar_wait_sleep(&full[s], (uint32_t)((i / STAGES) & 1), FIC_MMA_NS);
+                    if (lane == 0) TC_TR(1, i);
+                    if (ch == 0 && tl >= NBUF) tmbar_wait_sleep(&tempty[buf], (uint32_t)(((tl / NBUF) + 1) & 1), FIC_MMA_NS);
+#else
                     tmbar_wait(&full[s], (uint32_t)((i / STAGES) & 1));
                     if (lane == 0) TC_TR(1, i);
                     if (ch == 0 && tl >= NBUF) tmbar_wait(&tempty[buf], (uint32_t)(((tl / NBUF) + 1) & 1));
+#endif
                     if (lane == 0 && ch == 0) TC_TR(2, tl);
                     tc_fence_after();
                     {
@@ -1093,6 +1179,10 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
         };
         unsigned tl = 0;  // tiles consumed by this CTA (TMEM buffer ring position)
         const uint32_t tfull_sa = su32(tfull), tempty_sa = su32(tempty);
+#ifdef FIC_TC_TRACE
+        long long acc_wait = 0, acc_busy = 0;  // per epilogue warp: tfull waits, tile work (cycles)
+        long long acc_push = 0, n_push = 0;    // cycles in (and count of) push blocks
+#endif
         for (int k = 0; k < nseg; ++k) {
             int grp, ta, ntl, slot;
             bool lastseg;
@@ -1199,7 +1289,14 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
 #pragma unroll
                     for (int jj = 0; jj < NT; ++jj) t2_n[jj] = kIdx ? __ldg(P.t2f + (di + jj * t2r)) : __ldg(t2p + jj * t2row);
                 }
+#ifdef FIC_TC_TRACE
+                const long long tw0 = clock64();
+#endif
                 tmbar_wait_sa(tfull_sa + 8 * buf, (tl / NBUF) & 1);
+#ifdef FIC_TC_TRACE
+                const long long tw1 = clock64();
+                acc_wait += tw1 - tw0;
+#endif
                 if (warp == 2 && lane == 0) TC_TR(4, tl);
                 tc_fence_after();
                 const uint32_t tbase = tmem + ((uint32_t)(lq * 32) << 16) + buf * Cf::ACC + eg * HALF * 8;
@@ -1240,6 +1337,9 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
                         const float g0 = score(mx, B == 8 ? sSR[eg * HALF + q] : rSR[q], sd, sdn, t2);
                         pm |= (g0 <= sThr[eg * HALF + q]) ? (1u << q4) : 0u;
                     }
+#ifdef FIC_TC_TRACE
+                    const long long tp0 = clock64();
+#endif
                     if (pm) {  // queue (range, domain, k*, max SRD) of the passing pairs for the exact warp
 #pragma unroll
                         for (int q4 = 0; q4 < 4; ++q4) {
@@ -1278,9 +1378,15 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
                             }
                         }
                     }
+#ifdef FIC_TC_TRACE
+                    if (pm) { acc_push += clock64() - tp0; ++n_push; }
+#endif
                 }
                 if (warp == 2 && lane == 0) TC_TR(6, tl);
-                if (warp == Cf::THREADS / 32 - 1 && lane == 0) TC_TR(7, tl);
+                if (warp == Cf::XWARP - 1 && lane == 0) TC_TR(7, tl);
+#ifdef FIC_TC_TRACE
+                acc_busy += clock64() - tw1;
+#endif
             }
             // ---- every queued pair of this segment has been scored by the exact warp
             epi_sync();
@@ -1308,6 +1414,12 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
             }
         }
         if (et == 0) vctl[2] = 1u;  // the exact warp may stop once the ring is empty
+#ifdef FIC_TC_TRACE
+        if (blockIdx.x == 0 && lane == 0) {
+            g_tc_trace[29][2 * warp] = acc_busy; g_tc_trace[29][2 * warp + 1] = acc_wait;
+            g_tc_trace[29][64 + 2 * warp] = acc_push; g_tc_trace[29][64 + 2 * warp + 1] = n_push;
+        }
+#endif
     }
     tc_fence_before();
     __syncthreads();

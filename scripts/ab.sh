@@ -1,6 +1,6 @@
 #!/bin/bash
 # GPU box: quick C3 bench of the default build and of each abvar/*.so (FIC_SO), same box
-for so in default abvar/*.so; do
+for so in default $(ls abvar/*.so 2>/dev/null); do
   if [ "$so" = default ]; then unset FIC_SO; else export FIC_SO=$PWD/$so; fi
   timeout 300 python bench.py --no-cpu-baseline --no-e2e --steps ${STEPS:-30} "$@" > gpurun_out/ab.log 2>&1 || { echo "$so failed"; tail -5 gpurun_out/ab.log; continue; }
   python - "$so" <<'PY'

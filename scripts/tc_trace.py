@@ -26,7 +26,7 @@ SO = os.path.join(ROOT, "paper_1501_04140_b200", "libfic_trace.so")
 def main():
     from paper_1501_04140_b200 import build as b
     if not os.path.exists(SO) or os.environ.get("FIC_TRACE_REBUILD"):
-        b.build_variant(SO, defines=["FIC_TC_TRACE"])
+        b.build_variant(SO, defines=["FIC_TC_TRACE"] + os.environ.get("FIC_TRACE_DEFS", "").split())
     os.environ["FIC_SO"] = SO
     import torch
     from paper_1501_04140_b200 import fic
@@ -46,6 +46,7 @@ def main():
         dr = torch.from_numpy(ranges).cuda()
         tr = np.zeros((32, 4096), np.int64)
         for rep in range(3):
+            tr[:] = 0
             ctx.encode_level(img, pool, dr, cfg["s"][li], 8.0, False)
             torch.cuda.synchronize()
             lib.fic_debug_tc_trace(tr.ctypes.data_as(C.c_void_p))
@@ -70,6 +71,14 @@ def main():
                         print(f"   CTA {c} seg {kk}: start {(s23[kk] - st[c]) / 1e3:.1f} us, setup+seed {(s24[kk] - s23[kk]) / 1e3:.1f},"
                               f" tiles {(s25[kk] - s24[kk]) / 1e3:.1f}, drain {(s26[kk] - s25[kk]) / 1e3:.1f}")
                     print(f"   CTA {c} end {(en[c] - st[c]) / 1e3:.1f} us")
+        wb = tr[29][0:64:2]; ww = tr[29][1:64:2]
+        live_w = np.nonzero(wb > 0)[0]
+        if len(live_w):
+            print("   per epilogue warp (warp: SMSP busy/wait kcycles):",
+                  " ".join(f"w{w}:{w % 4} {wb[w] / 1e3:.0f}/{ww[w] / 1e3:.0f}" for w in live_w))
+            pc, pn = tr[29][64:128:2], tr[29][65:128:2]
+            print("   push blocks per warp (kcycles / count / cycles each):",
+                  " ".join(f"w{w} {pc[w] / 1e3:.0f}/{pn[w]}/{pc[w] / max(pn[w], 1):.0f}" for w in live_w))
         n_t = int((tr[6] > 0).sum())
         n_i = int((tr[0] > 0).sum())
         med = lambda a: float(np.median(a)) if len(a) else float("nan")  # noqa: E731
@@ -82,6 +91,15 @@ def main():
               f"mma: free->commit {med(t3 - t2):.0f}  commit gap {med(np.diff(t3)):.0f}")
         print(f"  epi2: tfull wait {med(t4[1:] - t6[:-1]):.0f}  ld {med(t5 - t4):.0f}  compute {med(t6 - t5):.0f}  "
               f"tile {med(np.diff(t6)):.0f}  last warp lag {med(t7 - t6):.0f}  commit->seen {med(t4 - t3):.0f}")
+        nw = int((tr[8:20, 100] > 0).sum()) if n_t > 100 else 0
+        if nw:
+            ld = tr[8:8 + nw, :n_t].astype(np.float64)  # per epilogue warp, per tile: loads done
+            lag = ld - np.median(ld, axis=0)
+            last = np.argmax(ld, axis=0)
+            print("   per warp (w:SMSP): mean lag vs median warp (cycles) / share of tiles it loads last:")
+            print("   " + " ".join(f"w{w + 2}:{(w + 2) % 4} {lag[w].mean():.0f}/{(last == w).mean():.2f}" for w in range(nw)))
+            spread = ld.max(axis=0) - ld.min(axis=0)
+            print(f"   load spread across warps per tile: p10 {np.percentile(spread, 10):.0f} p50 {np.median(spread):.0f} p90 {np.percentile(spread, 90):.0f}")
         if os.environ.get("FIC_TRACE_DUMP") and n_t > 110 and n_i == n_t:
             base = t4[100]
             print("  tile  copy  full  free  commit  seen  loaded  done  lastdone   (cycles from tile 100 seen)")
