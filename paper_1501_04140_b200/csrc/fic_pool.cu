@@ -76,7 +76,10 @@ __global__ void __launch_bounds__(256) entropy_keys_kernel(
 // adds LUT[old-1] - LUT[old] = -delta[old-1]; per bin the contributions telescope to
 // LUT[final] - LUT[initial] in any order (a removed pixel is always present, so no count goes
 // negative), so every key is the same exact integer as the direct build.
-constexpr int kSlideSeg = 16;
+#ifndef FIC_SLIDE_SEG
+#define FIC_SLIDE_SEG 12
+#endif
+constexpr int kSlideSeg = FIC_SLIDE_SEG;
 __global__ void __launch_bounds__(256) entropy_slide_kernel(
     const uint8_t *__restrict__ img, int32_t N, int32_t side, int32_t L, int32_t A,
     const int64_t *__restrict__ g_delta, int64_t lut_m, int64_t T, int use_tau,

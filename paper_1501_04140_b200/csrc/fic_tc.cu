@@ -1206,6 +1206,7 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
                 sM2[et] = fminf(__double2float_ru(2.0 * R.margin), FLT_MAX);
             }
             epi_sync();
+            if (et == 0) TC_TR_SEG(20, k);
             int rSR[HALF];
 #pragma unroll
             for (int q = 0; q < HALF; ++q)
@@ -1231,11 +1232,17 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
                 // sends every pair better than s = 0 to the exact path
                 const unsigned buf0 = tl % NBUF;
                 tmbar_wait_sa(tfull_sa + 8 * buf0, (tl / NBUF) & 1);
+                if (et == 0) TC_TR_SEG(21, k);
                 tc_fence_after();
                 const uint32_t tb0 = tmem + ((uint32_t)(lq * 32) << 16) + buf0 * Cf::ACC + eg * HALF * 8;
-#pragma unroll 1
+                // all HALF ranges scored first, then their warp minima as interleaved butterflies,
+                // then lane q (< HALF) lowers range q's threshold -- independent chains (scoring,
+                // reducing and CAS-ing the ranges one after another took ~5k cycles per segment)
+                float gq[HALF];
+                const float sdn0 = (float)sd_n * (1.0f / (float)n);
+#pragma unroll
                 for (int g = 0; g < HALF / 4; ++g) {
-                    uint32_t sv[64];
+                    uint32_t sv[Cf::QR ? 64 : 32];
                     tc_ld32<0>(tb0 + g * 32, sv);
                     if constexpr (Cf::QR) {
                         tc_ld32<32>(tb0 + NN, sv);
@@ -1247,25 +1254,32 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
                     }
 #pragma unroll
                     for (int q4 = 0; q4 < 4; ++q4) {
-                        const int q = g * 4 + q4;
                         const uint32_t *v = sv + q4 * 8;
                         const int mx = max(__vimax3_s32((int)v[0], (int)v[1], (int)v[2]),
                                            __vimax3_s32((int)v[3], (int)v[4], __vimax3_s32((int)v[5], (int)v[6], (int)v[7])));
-                        float gm = score(mx, rSR[q], sd_n, (float)sd_n * (1.0f / (float)n), t2_n);
-#pragma unroll
-                        for (int o = 16; o > 0; o >>= 1) gm = fminf(gm, __shfl_xor_sync(0xffffffffu, gm, o));
-                        if (lane == 0) {
-                            const float t = fminf(__fadd_ru(gm, __double2float_ru(2.0 * sR[eg * HALF + q].margin)), FLT_MAX);
-                            int *ti = reinterpret_cast<int *>(&sThr[eg * HALF + q]);
-                            int old = *ti;
-                            while (t < __int_as_float(old)) {  // (NaN / +inf pads never lower it)
-                                const int prev = atomicCAS(ti, old, __float_as_int(t));
-                                if (prev == old) break;
-                                old = prev;
-                            }
-                        }
+                        gq[g * 4 + q4] = score(mx, rSR[g * 4 + q4], sd_n, sdn0, t2_n);
                     }
                 }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+                    for (int q = 0; q < HALF; ++q) gq[q] = fminf(gq[q], __shfl_xor_sync(0xffffffffu, gq[q], o));
+                }
+                float mine = gq[0];
+#pragma unroll
+                for (int q = 1; q < HALF; ++q) mine = lane == q ? gq[q] : mine;
+                if (lane < HALF) {
+                    const int r = eg * HALF + lane;
+                    const float t = fminf(__fadd_ru(mine, sM2[r]), FLT_MAX);
+                    int *ti = reinterpret_cast<int *>(&sThr[r]);
+                    int old = *ti;
+                    while (t < __int_as_float(old)) {  // (NaN / +inf pads never lower it)
+                        const int prev = atomicCAS(ti, old, __float_as_int(t));
+                        if (prev == old) break;
+                        old = prev;
+                    }
+                }
+                if (et == 0) TC_TR_SEG(22, k);
                 asm volatile("bar.sync %0, 128;" ::"r"(1 + eg) : "memory");  // the warpgroup's seeds
             }
             if (et == 0) TC_TR_SEG(24, k);

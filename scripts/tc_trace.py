@@ -68,7 +68,9 @@ def main():
                     row = lambda kd: tr[kd][c * 8: c * 8 + 8]  # noqa: E731
                     s23, s24, s25, s26 = row(23), row(24), row(25), row(26)
                     for kk in range(int(tr[27][c])):
-                        print(f"   CTA {c} seg {kk}: start {(s23[kk] - st[c]) / 1e3:.1f} us, setup+seed {(s24[kk] - s23[kk]) / 1e3:.1f},"
+                        s20, s21, s22 = row(20), row(21), row(22)
+                        print(f"   CTA {c} seg {kk}: start {(s23[kk] - st[c]) / 1e3:.1f} us, setup {(s20[kk] - s23[kk]) / 1e3:.2f}"
+                              f" seed wait {(s21[kk] - s20[kk]) / 1e3:.2f} own seed {(s22[kk] - s21[kk]) / 1e3:.2f} wg bar {(s24[kk] - s22[kk]) / 1e3:.2f},"
                               f" tiles {(s25[kk] - s24[kk]) / 1e3:.1f}, drain {(s26[kk] - s25[kk]) / 1e3:.1f}")
                     print(f"   CTA {c} end {(en[c] - st[c]) / 1e3:.1f} us")
         wb = tr[29][0:64:2]; ww = tr[29][1:64:2]
