@@ -92,8 +92,11 @@ struct TCfg {
     // while the current segment's MMAs still read the other one
     static constexpr int BBUF = (B == 4 || F16) ? 2 : 1;
     static constexpr int ACC = QR ? 2 * N : N;             // TMEM columns per accumulator buffer
-    static constexpr int NBUF = 512 / ACC >= 4 ? 4 : 2;    // TMEM accumulator buffers (MMA <-> epilogue)
+    static constexpr int NBUF = 512 / ACC >= 4 ? 4 : 512 / ACC;  // TMEM accumulator buffers (MMA <-> epilogue)
     static constexpr int EWG = B == 4 ? FIC_B4_EWG : (B == 32 ? 2 : 4);   // epilogue warpgroups
+    // ranges per warpgroup, in groups of 4 (one 32-column tcgen05.ld); when EWG does not divide
+    // NR / 4 the last warpgroup's trailing groups are empty (skipped)
+    static constexpr int HALF = ((NR + 4 * EWG - 1) / (4 * EWG)) * 4;
     // warps: producer, MMA issuer, 4 EWG epilogue warps, the exact-path warp
     static constexpr int XWARP = 2 + 4 * EWG;
     static constexpr int THREADS = 64 + 128 * EWG + 32;
@@ -847,7 +850,10 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
     using Cf = TCfg<B>;
     constexpr int n = Cf::n, KP = Cf::KP, NR = Cf::NR, NN = Cf::N, KCH = Cf::KCH, CH = Cf::CH;
     constexpr int STAGES = Cf::STAGES;
-    constexpr int HALF = NR / Cf::EWG;  // ranges per epilogue warpgroup
+    constexpr int HALF = Cf::HALF;  // ranges per epilogue warpgroup (the last may have fewer)
+    constexpr bool UNEVEN = HALF * Cf::EWG != NR;
+    static_assert(NR % 4 == 0 && Cf::NBUF >= 2 && (Cf::EWG - 1) * HALF < NR,
+                  "range groups of 4, >= 2 accumulator buffers, every warpgroup has ranges");
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t *sA = smem;                                        // [STAGES][128 x KCH]
     uint8_t *sB = sA + STAGES * Cf::STAGE_BYTES;               // [N x KP]
@@ -1210,7 +1216,9 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
             int rSR[HALF];
 #pragma unroll
             for (int q = 0; q < HALF; ++q)
-                rSR[q] = Cf::F16 ? __float_as_int(-(float)sR[eg * HALF + q].SR) : sR[eg * HALF + q].SR;
+                rSR[q] = (!UNEVEN || eg * HALF + q < NR)
+                             ? (Cf::F16 ? __float_as_int(-(float)sR[eg * HALF + q].SR) : sR[eg * HALF + q].SR)
+                             : 0;
             // per-domain data of this lane, walked tile by tile (pointers advanced, not recomputed);
             // NSP > 0 is chosen only when the level has exactly NSP values s > 0, so every row exists
             // B >= 8: a 32-bit slot index (one IMAD.WIDE per load instead of 64-bit pointer
@@ -1242,6 +1250,11 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
                 const float sdn0 = (float)sd_n * (1.0f / (float)n);
 #pragma unroll
                 for (int g = 0; g < HALF / 4; ++g) {
+                    if (UNEVEN && eg * HALF + g * 4 >= NR) {  // an empty group
+#pragma unroll
+                        for (int q4 = 0; q4 < 4; ++q4) gq[g * 4 + q4] = INFINITY;
+                        continue;
+                    }
                     uint32_t sv[Cf::QR ? 64 : 32];
                     tc_ld32<0>(tb0 + g * 32, sv);
                     if constexpr (Cf::QR) {
@@ -1268,7 +1281,7 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
                 float mine = gq[0];
 #pragma unroll
                 for (int q = 1; q < HALF; ++q) mine = lane == q ? gq[q] : mine;
-                if (lane < HALF) {
+                if (lane < HALF && (!UNEVEN || eg * HALF + lane < NR)) {
                     const int r = eg * HALF + lane;
                     const float t = fminf(__fadd_ru(mine, sM2[r]), FLT_MAX);
                     int *ti = reinterpret_cast<int *>(&sThr[r]);
@@ -1323,9 +1336,9 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
                 static_assert(G <= 4 && (!Cf::QR || G == 1), "one tile's accumulators fit vv");
                 tc_ld32<0>(tbase, vv);
                 if constexpr (Cf::QR) tc_ld32<32>(tbase + NN, vv);
-                if constexpr (!Cf::QR && G >= 2) tc_ld32<32>(tbase + 32, vv);
-                if constexpr (!Cf::QR && G >= 3) tc_ld32<64>(tbase + 64, vv);
-                if constexpr (!Cf::QR && G >= 4) tc_ld32<96>(tbase + 96, vv);
+                if constexpr (!Cf::QR && G >= 2) if (!UNEVEN || eg * HALF + 4 < NR) tc_ld32<32>(tbase + 32, vv);
+                if constexpr (!Cf::QR && G >= 3) if (!UNEVEN || eg * HALF + 8 < NR) tc_ld32<64>(tbase + 64, vv);
+                if constexpr (!Cf::QR && G >= 4) if (!UNEVEN || eg * HALF + 12 < NR) tc_ld32<96>(tbase + 96, vv);
                 tc_wait_ld();
                 tc_fence_before();
                 __syncwarp();
@@ -1338,6 +1351,7 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
                 }
 #pragma unroll
                 for (int g = 0; g < G; ++g) {
+                    if (UNEVEN && eg * HALF + g * 4 >= NR) continue;  // an empty group
                     unsigned pm = 0;
                     int mxs[4];
 #pragma unroll
