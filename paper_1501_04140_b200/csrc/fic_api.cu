@@ -180,8 +180,9 @@ fic_status pool_enqueue(fic_ctx *ctx, Pool &P, const uint8_t *img, int32_t N, in
         CK(fic::launch_pool_tc(img, N, B, L, P.A, P.kept, &P.d_misc[0], tiles_max, P.Dtc, P.SD, P.SDf, P.C,
                                &P.d_misc[1], fic::tc_pool_d2_bytes(B, N, L) ? ptr<uint16_t>(P.b_D2) : nullptr, st));
     else
-        CK(fic::launch_b2_pool(img, N, L, P.A, P.kept, &P.d_misc[0], slots, P.b_F2.p, &P.b2, st));
-    const bool fused = P.mode == 0 && fic::tc_pool_has_moments(B);
+        CK(fic::launch_b2_pool(img, N, L, P.A, P.kept, &P.d_misc[0], slots, P.b_F2.p, &P.b2, P.SD, P.SDf, P.C,
+                               &P.d_misc[1], st));
+    const bool fused = P.mode == 3 || fic::tc_pool_has_moments(B);
     if (!fused)
         CK(fic::launch_pool_moments(img, N, B, L, P.A, P.kept, &P.d_misc[0], slots, P.SD, P.SDf, P.C,
                                     &P.d_misc[1], st));

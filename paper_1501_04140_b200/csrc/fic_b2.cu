@@ -55,31 +55,41 @@ __device__ __forceinline__ void b2_wait(uint64_t *bar, uint32_t parity) {
 // them).  The pool is stored sorted by C (stable: ties keep the kept-domain rank order), with
 // ds[pos] = kept-domain rank and Cs[pos] = C, so the search can bound a range's admissible
 // domains to C windows (Cauchy-Schwarz, see b2win_kernel).
-__global__ void b2_pool_kernel(const uint8_t *__restrict__ img, int32_t N, int32_t L, int32_t A,
-                               const int32_t *__restrict__ kept, const unsigned long long *__restrict__ d_nk,
-                               int64_t n_slots, float4 *__restrict__ F, uint32_t *__restrict__ key,
-                               int32_t *__restrict__ val) {
+// also the pool moments of the level (SD, SDf, C, Cmax; pool_moments_kernel is not run for B = 2)
+__global__ void __launch_bounds__(256) b2_pool_kernel(const uint8_t *__restrict__ img, int32_t N, int32_t L, int32_t A,
+                                                      const int32_t *__restrict__ kept,
+                                                      const unsigned long long *__restrict__ d_nk, int64_t n_slots,
+                                                      float4 *__restrict__ F, uint32_t *__restrict__ key,
+                                                      int32_t *__restrict__ val, int32_t *__restrict__ SD,
+                                                      float *__restrict__ SDf, int64_t *__restrict__ Cm,
+                                                      unsigned long long *d_cmax) {
     const int64_t d = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (d >= n_slots) return;
     const int64_t n_k = (int64_t)*d_nk;
-    val[d] = (int32_t)d;
-    if (d >= n_k) {
-        F[d] = make_float4(0.f, 0.f, 0.f, 0.f);
-        key[d] = 0xffffffu;  // pads sort last (C < 2^23)
-        return;
+    unsigned long long cm = 0;  // (no early return: block_max_atomic)
+    if (d < n_slots) {
+        val[d] = (int32_t)d;
+        if (d >= n_k) {
+            F[d] = make_float4(0.f, 0.f, 0.f, 0.f);
+            key[d] = 0xffffffu;  // pads sort last (C < 2^23)
+            SD[d] = 0; SDf[d] = 0.f; Cm[d] = 0;
+        } else {
+            const int32_t c = kept[d];
+            const int64_t x0 = (int64_t)(c % A) * L, y0 = (int64_t)(c / A) * L;
+            auto dp = [&](int i, int j) {
+                const uint8_t *q = img + (y0 + 2 * i) * N + x0 + 2 * j;
+                return (int)q[0] + (int)q[1] + (int)q[N] + (int)q[N + 1];
+            };
+            const int w = dp(0, 0), x = dp(0, 1), y = dp(1, 1), z = dp(1, 0);
+            const int sd = w + x + y + z;
+            const int cc = 4 * (w * w + x * x + y * y + z * z) - sd * sd;  // C = n SDD - SD^2 < 2^23
+            const int yr = abs(w - y), yi = abs(x - z);
+            F[d] = make_float4((float)(w - x + y - z), (float)(yr + yi), (float)(yr - yi), (float)cc);
+            key[d] = (uint32_t)cc;
+            SD[d] = sd; SDf[d] = (float)sd; Cm[d] = cc;
+            cm = (unsigned long long)cc;
+        }
     }
-    const int32_t c = kept[d];
-    const int64_t x0 = (int64_t)(c % A) * L, y0 = (int64_t)(c / A) * L;
-    auto dp = [&](int i, int j) {
-        const uint8_t *q = img + (y0 + 2 * i) * N + x0 + 2 * j;
-        return (int)q[0] + (int)q[1] + (int)q[N] + (int)q[N + 1];
-    };
-    const int w = dp(0, 0), x = dp(0, 1), y = dp(1, 1), z = dp(1, 0);
-    const int sd = w + x + y + z;
-    const int cc = 4 * (w * w + x * x + y * y + z * z) - sd * sd;  // C = n SDD - SD^2 < 2^23
-    const int yr = abs(w - y), yi = abs(x - z);
-    F[d] = make_float4((float)(w - x + y - z), (float)(yr + yi), (float)(yr - yi), (float)cc);
-    key[d] = (uint32_t)cc;
+    block_max_atomic(cm, d_cmax);
 }
 
 __global__ void b2_gather_kernel(const float4 *__restrict__ Fu, const int32_t *__restrict__ ds, int64_t n_slots,
@@ -113,7 +123,7 @@ size_t b2_pool_bytes(int64_t n_slots) { return b2_layout(n_slots).total; }
 
 cudaError_t launch_b2_pool(const uint8_t *img, int32_t N, int32_t L, int32_t A, const int32_t *kept,
                            const unsigned long long *d_nk, int64_t n_slots, void *store, B2Pool *out,
-                           cudaStream_t st) {
+                           int32_t *SD, float *SDf, int64_t *C, unsigned long long *d_cmax, cudaStream_t st) {
     const B2PoolLayout Ly = b2_layout(n_slots);
     char *base = static_cast<char *>(store);
     out->F = reinterpret_cast<float4 *>(base + Ly.F);
@@ -124,7 +134,7 @@ cudaError_t launch_b2_pool(const uint8_t *img, int32_t N, int32_t L, int32_t A, 
     uint32_t *key = reinterpret_cast<uint32_t *>(base + Ly.key);
     int32_t *val = reinterpret_cast<int32_t *>(base + Ly.val);
     const unsigned g = (unsigned)((n_slots + 255) / 256);
-    b2_pool_kernel<<<g, 256, 0, st>>>(img, N, L, A, kept, d_nk, n_slots, Fu, key, val);
+    b2_pool_kernel<<<g, 256, 0, st>>>(img, N, L, A, kept, d_nk, n_slots, Fu, key, val, SD, SDf, C, d_cmax);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     size_t tb = Ly.tmp_bytes;

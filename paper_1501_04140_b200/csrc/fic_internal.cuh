@@ -276,7 +276,7 @@ cudaError_t launch_merge_shards(const fic_record *in, const int64_t *d_counts, i
 size_t b2_pool_bytes(int64_t n_slots);
 cudaError_t launch_b2_pool(const uint8_t *img, int32_t N, int32_t L, int32_t A, const int32_t *kept,
                            const unsigned long long *d_nk, int64_t n_slots, void *store, B2Pool *out,
-                           cudaStream_t st);
+                           int32_t *SD, float *SDf, int64_t *C, unsigned long long *d_cmax, cudaStream_t st);
 int b2_nsplit_hint(int64_t n_r, int64_t n_tiles, int num_sms);
 int b2_t2_width(int32_t nsp);  // floats per slot of the B = 2 t2 table
 size_t b2_scratch_bytes(int64_t n_r, int32_t ns_cap);  // pass-1 minima + split count

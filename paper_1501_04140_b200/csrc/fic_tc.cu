@@ -283,25 +283,46 @@ __device__ __forceinline__ float ord2f(uint32_t o) {
 
 // ------------------------------------------------------------------------------ pool (A operand)
 // Tile t, chunk c: 128 domains x KCH bytes in the core-matrix layout (one bulk copy per stage).
-// K byte kb of domain d = plane (kb / n) = (a, b) = (plane >> 1, plane & 1), pixel p = kb % n:
-// I(y + 2i + a, x + 2j + b); zero for kb >= 4n.
+// All forms read the 2 x 2 sums D' from the once-decimated image D2 (decimate_kernel below: plane
+// p = (y & 1, x & 1) holds D2_p[u][v] = the 2 x 2 block at (2u + oy, 2v + ox), rows of
+// d2_pitch(N) elements, so D'(i, j) of the domain at (x, y) is D2_p[(y >> 1) + i][(x >> 1) + j]).
+__host__ __device__ __forceinline__ int d2_pitch(int32_t N) { return ((N / 2 + 7) & ~7) + 8; }  // elements
+// The 8 D' at element col .. col + 7 of a D2 row (16 bytes at an even byte offset within a
+// 16-byte-aligned 32-byte window): two aligned 16-byte loads, words q .. q + 4 selected and
+// funnel-shifted by (sh & 3) bytes; returned as 4 pairs (2 x 16 bits)
+__device__ __forceinline__ void d2_load8(const uint16_t *row, int col, uint32_t (&pr)[4]) {
+    const uint4 *src = reinterpret_cast<const uint4 *>(row + (col & ~7));
+    const uint4 lo = __ldg(src), hi = __ldg(src + 1);
+    const uint32_t wv[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+    const int sh = (col & 7) * 2, qs = sh >> 2;
+    const uint32_t fs = (uint32_t)(sh & 3) * 8;
+    uint32_t sel[5];
+#pragma unroll
+    for (int k = 0; k < 5; ++k) sel[k] = qs == 0 ? wv[k] : qs == 1 ? wv[k + 1] : qs == 2 ? wv[k + 2] : wv[(k + 3) & 7];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) pr[k] = __funnelshift_r(sel[k], sel[k + 1], fs);
+}
+
+// B = 4, 8 (f16 form): thread per 16-byte K group g = the decimated pixels 8g .. 8g + 7
+// (row-major) as fp16, and the domain moments SD, SDD -> C = n SDD - SD^2 reduced over the
+// domain's KP / 16 threads (consecutive lanes), which replaces pool_moments_kernel.  u8 form
+// (FIC_TC_F16 = 0): the four polyphase planes of the raw block, moments by pool_moments_kernel.
 template <int B>
-__global__ void __launch_bounds__(256) pool_tc_kernel(const uint8_t *__restrict__ img, int32_t N, int32_t L,
-                                                      int32_t A, const int32_t *__restrict__ kept,
+__global__ void __launch_bounds__(256) pool_tc_kernel(const uint8_t *__restrict__ img, const uint16_t *__restrict__ D2,
+                                                      int32_t N, int32_t L, int32_t A,
+                                                      const int32_t *__restrict__ kept,
                                                       const unsigned long long *__restrict__ d_nk,
                                                       int64_t total16, uint8_t *__restrict__ Dtc,
                                                       int32_t *__restrict__ SD, float *__restrict__ SDf,
                                                       int64_t *__restrict__ Cm, unsigned long long *d_cmax) {
     using Cf = TCfg<B>;
+    static_assert(!Cf::QR, "QR pools: pool_qr_kernel");
     const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // one 16-byte group
     const int64_t n_k = (int64_t)*d_nk;
     const int64_t ntiles = (n_k + kTileD - 1) / kTileD;
-    // QR: n/16 threads per domain (16 pixels each, both planes); else one per 16-byte K group
-    constexpr int G16 = Cf::QR ? Cf::n / 16 : Cf::KP / 16;
+    constexpr int G16 = Cf::KP / 16;
     const int64_t tile = e / ((int64_t)kTileD * G16);
-    // (QR: no early return -- the block reduces Cmax with one atomic)
-    if (!Cf::QR && (e >= total16 || tile >= ntiles)) return;
-    const bool live = e < total16 && tile < ntiles;
+    const bool live = e < total16 && tile < ntiles;  // (no early return: block_max_atomic)
     const int rem = (int)(e - tile * kTileD * G16);
     const int m = rem / G16, g = rem % G16;
     const int64_t d = tile * kTileD + m;
@@ -310,91 +331,49 @@ __global__ void __launch_bounds__(256) pool_tc_kernel(const uint8_t *__restrict_
         uint8_t *dst = Dtc + ((size_t)tile * Cf::CH + ch) * Cf::STAGE_BYTES + cm_off(m, kc, Cf::KCH);
         *reinterpret_cast<uint4 *>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
     };
-    if constexpr (Cf::QR) {
-        // one thread per 16 pixels writes both planes (q = D' >> 2 at K byte p, r = D' & 3 at
-        // n + p) and the domain moments SD, SDD -> C = n SDD - SD^2 (reduced over the n/16 = 16
-        // threads of the domain, a half warp), which replaces pool_moments_kernel at this level
-        // B = 16: thread g = decimated row g; B = 32: decimated row g / 2, half g % 2 (16 values,
-        // 32 source bytes each); the moments are fused at B = 16 only (pool_moments_kernel else)
-        constexpr int HPR = B / 16;  // threads per decimated row
-        uint32_t wq[4] = {0, 0, 0, 0}, wr[4] = {0, 0, 0, 0};
-        int sd = 0;
-        long long sdd = 0;
-        if (live && d < n_k) {
-            // thread g = decimated row g: source rows y + 2g, y + 2g + 1, bytes x .. x + 31, read as
-            // aligned 32-bit words (byte shift x % 4; with N % 4 == 0 the 9th word, read only for a
-            // nonzero shift, ends at or before the row's last byte) and summed two pixels per 16-bit lane
-            const int32_t c = kept[d];
-            const int64_t x = (int64_t)(c % A) * L, y = (int64_t)(c / A) * L;
-            const uint8_t *r0 = img + (y + 2 * (g / HPR)) * N + x + 32 * (g % HPR);
-            const uint32_t *w0 = reinterpret_cast<const uint32_t *>(reinterpret_cast<uintptr_t>(r0) & ~(uintptr_t)3);
-            const uint32_t *w1 = w0 + N / 4;
-            const uint32_t sh = (uint32_t)(reinterpret_cast<uintptr_t>(r0) & 3) * 8;
-            uint32_t u0[9], u1[9];
-#pragma unroll
-            for (int k = 0; k < 8; ++k) { u0[k] = __ldg(w0 + k); u1[k] = __ldg(w1 + k); }
-            u0[8] = sh ? __ldg(w0 + 8) : 0u;
-            u1[8] = sh ? __ldg(w1 + 8) : 0u;
-#pragma unroll
-            for (int k = 0; k < 8; k += 2) {
-                uint32_t sq[2], sr2[2];
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const uint32_t v0 = __funnelshift_r(u0[k + h], u0[k + h + 1], sh);
-                    const uint32_t v1 = __funnelshift_r(u1[k + h], u1[k + h + 1], sh);
-                    // 16-bit lanes: D'_{2(k+h)}, D'_{2(k+h)+1} (<= 1020)
-                    const uint32_t dd = (v0 & 0x00FF00FFu) + ((v0 >> 8) & 0x00FF00FFu) +
-                                        (v1 & 0x00FF00FFu) + ((v1 >> 8) & 0x00FF00FFu);
-                    const int da = (int)(dd & 0xFFFFu), db = (int)(dd >> 16);
-                    sd += da + db;
-                    sdd += (long long)(da * da + db * db);
-                    sq[h] = (dd >> 2) & 0x00FF00FFu;
-                    sr2[h] = dd & 0x00030003u;
-                }
-                // bytes in K order: [lo(h0), hi(h0), lo(h1), hi(h1)]
-                wq[k >> 1] = __byte_perm(sq[0], sq[1], 0x6420);
-                wr[k >> 1] = __byte_perm(sr2[0], sr2[1], 0x6420);
-            }
-        }
-        if (live) {
-            store16(g * 16, wq);
-            store16(Cf::n + g * 16, wr);
-        }
-        if constexpr (B == 16) {
-#pragma unroll
-            for (int o = 8; o > 0; o >>= 1) {
-                sd += __shfl_xor_sync(0xffffffffu, sd, o);
-                sdd += __shfl_xor_sync(0xffffffffu, sdd, o);
-            }
-            const long long cc = (long long)Cf::n * sdd - (long long)sd * sd;
-            if (g == 0 && live) {
-                SD[d] = sd;
-                SDf[d] = (float)sd;
-                Cm[d] = cc;
-            }
-            block_max_atomic(g == 0 && live && d < n_k ? (unsigned long long)cc : 0ull, d_cmax);
-        }
-    } else if constexpr (Cf::F16) {
-        // 16-byte group g = decimated pixels 8g .. 8g + 7 (row-major) as fp16
+    if constexpr (Cf::F16) {
         uint32_t w[4] = {0, 0, 0, 0};
-        if (d < n_k) {
+        int sd = 0, sdd = 0;
+        if (live && d < n_k) {
             const int32_t c = kept[d];
-            const int64_t x = (int64_t)(c % A) * L, y = (int64_t)(c / A) * L;
+            const int x = (c % A) * L, y = (c / A) * L;
+            const int H = N / 2, W = d2_pitch(N);
+            const uint16_t *base = D2 + (size_t)(((y & 1) << 1) | (x & 1)) * H * W + (size_t)(y >> 1) * W;
+            const int col = x >> 1;
+            uint32_t pr[4];  // D' pairs: pixels 8g + 2k, 8g + 2k + 1
+            if constexpr (B == 8) {
+                d2_load8(base + (size_t)g * W, col, pr);
+            } else {  // B = 4: rows 2g, 2g + 1, four pixels each
 #pragma unroll
-            for (int q = 0; q < 8; q += 2) {
-                int v2[2];
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const int p = g * 8 + q + h;
-                    const int i = p / B, j = p % B;
-                    const uint8_t *r0 = img + (y + 2 * i) * N + x + 2 * j;
-                    v2[h] = (int)r0[0] + (int)r0[1] + (int)r0[N] + (int)r0[N + 1];
+                for (int r = 0; r < 2; ++r) {
+                    const uint16_t *row = base + (size_t)(2 * g + r) * W + col;
+                    pr[2 * r] = (uint32_t)__ldg(row) | ((uint32_t)__ldg(row + 1) << 16);
+                    pr[2 * r + 1] = (uint32_t)__ldg(row + 2) | ((uint32_t)__ldg(row + 3) << 16);
                 }
-                w[q >> 1] = f16x2_int(v2[0], v2[1]);
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int a = (int)(pr[k] & 0xFFFFu), b = (int)(pr[k] >> 16);
+                sd += a + b;
+                sdd += a * a + b * b;
+                w[k] = f16x2_int(a, b);
             }
         }
-        store16(g * 16, w);
+        if (live) store16(g * 16, w);
+#pragma unroll
+        for (int o = 1; o < G16; o <<= 1) {
+            sd += __shfl_xor_sync(0xffffffffu, sd, o);
+            sdd += __shfl_xor_sync(0xffffffffu, sdd, o);
+        }
+        const long long cc = (long long)Cf::n * sdd - (long long)sd * sd;
+        if (g == 0 && live) {
+            SD[d] = sd;
+            SDf[d] = (float)sd;
+            Cm[d] = cc;
+        }
+        block_max_atomic(g == 0 && live && d < n_k ? (unsigned long long)cc : 0ull, d_cmax);
     } else {
+        if (!live) return;
         uint32_t w[4] = {0, 0, 0, 0};
         if (d < n_k) {
             const int32_t c = kept[d];
@@ -424,7 +403,6 @@ __global__ void __launch_bounds__(256) pool_tc_kernel(const uint8_t *__restrict_
 // plane into the K-major core-matrix layout), SD, SDD in int32 (< 2^31 at n = 1024) reduced with
 // REDUX.  The 2 x 2 sums, previously formed per domain from the raw 2B x 2B block (each image pixel
 // of a C3 pool read ~(2B / L)^2 = 256 times, 333 warp instructions per domain), are formed once.
-__host__ __device__ __forceinline__ int d2_pitch(int32_t N) { return ((N / 2 + 7) & ~7) + 8; }  // elements
 __global__ void __launch_bounds__(256) decimate_kernel(const uint8_t *__restrict__ img, int32_t N, int32_t planes,
                                                        uint16_t *__restrict__ D2) {
     const int H = N / 2, W = d2_pitch(N);  // rows of W elements (16-byte aligned, zero padded)
@@ -476,27 +454,14 @@ __global__ void __launch_bounds__(256) pool_qr_kernel(const uint16_t *__restrict
         if (d < n_k) {
             const int32_t c = kept[d];
             const int x = (c % A) * L, y = (c / A) * L;
-            // the 8 D' of a chunk are 16 bytes at an even byte offset sh within a 16-byte-aligned
-            // 32-byte window: two aligned 16-byte loads, then words q .. q + 4 selected and
-            // funnel-shifted by (sh & 3) bytes (the same shift for every chunk of the domain)
             const int col = x >> 1;
-            const uint16_t *base = D2 + (size_t)(((y & 1) << 1) | (x & 1)) * H * W + (size_t)(y >> 1) * W + (col & ~7);
-            const int sh = (col & 7) * 2, qs = sh >> 2;
-            const uint32_t fs = (uint32_t)(sh & 3) * 8;
+            const uint16_t *base = D2 + (size_t)(((y & 1) << 1) | (x & 1)) * H * W + (size_t)(y >> 1) * W;
 #pragma unroll
             for (int t = 0; t < CPL; ++t) {
                 const int chk = lane + 32 * t;
                 const int i = chk / CPR, h = chk % CPR;
-                const uint4 *src = reinterpret_cast<const uint4 *>(base + (size_t)i * W + 8 * h);
-                const uint4 lo = __ldg(src), hi = __ldg(src + 1);
-                const uint32_t wv[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
-                uint32_t sel[5];
-#pragma unroll
-                for (int k = 0; k < 5; ++k)
-                    sel[k] = qs == 0 ? wv[k] : qs == 1 ? wv[k + 1] : qs == 2 ? wv[k + 2] : wv[(k + 3) & 7];
                 uint32_t pr[4];  // D' pairs (2 x 16 bits)
-#pragma unroll
-                for (int k = 0; k < 4; ++k) pr[k] = __funnelshift_r(sel[k], sel[k + 1], fs);
+                d2_load8(base + (size_t)i * W, col + 8 * h, pr);
                 uint32_t qv[4], rv[4];
                 uint32_t s2 = 0;
 #pragma unroll
@@ -543,8 +508,17 @@ __global__ void __launch_bounds__(256) pool_qr_kernel(const uint16_t *__restrict
     block_max_atomic(cmax, d_cmax);
 }
 
+// the pools built from D2 with fused moments: QR (B = 16, 32) and the f16 form (B = 4, 8)
+static bool TCfg_QR_or_F16(int B) {
+    switch (B) {
+    case 4: return TCfg<4>::F16;
+    case 8: return TCfg<8>::F16;
+    case 16: case 32: return true;
+    default: return false;
+    }
+}
 size_t tc_pool_d2_bytes(int B, int32_t N, int32_t L) {
-    if (B < 16) return 0;
+    if (!TCfg_QR_or_F16(B)) return 0;
     return (L % 2 == 0 ? 1 : 4) * (size_t)(N / 2) * (size_t)d2_pitch(N) * sizeof(uint16_t);
 }
 
@@ -560,37 +534,29 @@ size_t tc_pool_bytes(int B, int64_t n_tiles) {
     }
 }
 
-int tc_pool_has_moments(int B) { return B >= 16; }
+int tc_pool_has_moments(int B) { return TCfg_QR_or_F16(B) ? 1 : 0; }
 
 cudaError_t launch_pool_tc(const uint8_t *img, int32_t N, int32_t B, int32_t L, int32_t A,
                            const int32_t *kept, const unsigned long long *d_nk, int64_t n_tiles_max,
                            uint8_t *Dtc, int32_t *SD, float *SDf, int64_t *C, unsigned long long *d_cmax,
                            uint16_t *D2, cudaStream_t st) {
-    int g16 = 0;
-    switch (B) {
-    case 4: g16 = TCfg<4>::KP / 16; break;
-    case 8: g16 = TCfg<8>::KP / 16; break;
-    case 16: g16 = TCfg<16>::n / 16; break;
-    case 32: g16 = TCfg<32>::n / 16; break;
-    default: return cudaErrorInvalidValue;
-    }
-    const int64_t total16 = n_tiles_max * kTileD * g16;
-    if (total16 == 0) return cudaSuccess;
-    const unsigned blocks = (unsigned)((total16 + 255) / 256);
-    switch (B) {
-    case 4: pool_tc_kernel<4><<<blocks, 256, 0, st>>>(img, N, L, A, kept, d_nk, total16, Dtc, SD, SDf, C, d_cmax); break;
-    case 8: pool_tc_kernel<8><<<blocks, 256, 0, st>>>(img, N, L, A, kept, d_nk, total16, Dtc, SD, SDf, C, d_cmax); break;
-    case 16:
-    case 32: {  // decimated image, then warp per domain (pool_qr_kernel)
+    if (B != 4 && B != 8 && B != 16 && B != 32) return cudaErrorInvalidValue;
+    if (n_tiles_max == 0) return cudaSuccess;
+    if (tc_pool_d2_bytes(B, N, L)) {  // the decimated image (all parity classes the domains use)
         if (!D2) return cudaErrorInvalidValue;
         const int64_t d2n = (int64_t)(tc_pool_d2_bytes(B, N, L) / sizeof(uint16_t));
         decimate_kernel<<<(unsigned)((d2n + 255) / 256), 256, 0, st>>>(img, N, L % 2 == 0 ? 1 : 4, D2);
-        // one wave (6 CTAs of 256 threads per SM at <= 40 registers), grid-stride over the groups
+    }
+    if (B <= 8) {
+        const int64_t total16 = n_tiles_max * kTileD * (B == 4 ? TCfg<4>::KP / 16 : TCfg<8>::KP / 16);
+        const unsigned blocks = (unsigned)((total16 + 255) / 256);
+        if (B == 4) pool_tc_kernel<4><<<blocks, 256, 0, st>>>(img, D2, N, L, A, kept, d_nk, total16, Dtc, SD, SDf, C, d_cmax);
+        else pool_tc_kernel<8><<<blocks, 256, 0, st>>>(img, D2, N, L, A, kept, d_nk, total16, Dtc, SD, SDf, C, d_cmax);
+    } else {  // warp per domain (pool_qr_kernel), one wave (6 CTAs of 256 threads per SM at <= 40
+              // registers), grid-stride over the 8-domain groups
         const unsigned bq = (unsigned)std::min<int64_t>((n_tiles_max * kTileD + 7) / 8, 148 * 6);
         if (B == 16) pool_qr_kernel<16><<<bq, 256, 0, st>>>(D2, N, L, A, kept, d_nk, Dtc, SD, SDf, C, d_cmax);
         else pool_qr_kernel<32><<<bq, 256, 0, st>>>(D2, N, L, A, kept, d_nk, Dtc, SD, SDf, C, d_cmax);
-        break;
-    }
     }
     return cudaGetLastError();
 }
