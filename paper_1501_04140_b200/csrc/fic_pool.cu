@@ -199,12 +199,12 @@ constexpr int kSelBlock = 4096;  // flags per CTA (select_chain_kernel); one scr
 size_t select_blocksum_len(int64_t n) { return (size_t)((n + kSelBlock - 1) / kSelBlock) + 1; }
 
 struct EmitIndex {
-    static constexpr bool kClear = false;
+    static constexpr bool kClear = false, kBlockCopy = false;
     int32_t *out;
     __device__ void operator()(int64_t i, int64_t pos) const { out[pos] = (int32_t)i; }
 };
 struct EmitGrid {  // the child bitmap is cleared as it is consumed (ready for the next level)
-    static constexpr bool kClear = true;
+    static constexpr bool kClear = true, kBlockCopy = false;
     int2 *out;
     int64_t G;
     int32_t B;
@@ -221,15 +221,26 @@ __device__ __forceinline__ void copy_record(fic_record *dst, const fic_record *s
     for (int q = 0; q < 5; ++q) d[q] = s[q];
 }
 
+// records: the CTA lists its selected indices in shared memory, then copies the records as
+// consecutive 8-byte words (coalesced stores; one thread copying its own records wrote 40-byte
+// strided words -- 21.7 us for the ~200k records of C3's B = 4 level)
 struct EmitRecord {
-    static constexpr bool kClear = false;
+    static constexpr bool kClear = false, kBlockCopy = true;
     const fic_record *in;
     fic_record *out;
     const unsigned long long *base;
     int64_t cap;
-    __device__ void operator()(int64_t i, int64_t pos) const {
-        const int64_t o = (int64_t)*base + pos;
-        if (o < cap) copy_record(out + o, in + i);
+    // record j of the CTA's selection (index blk0 + idx[j]) to position *base + excl + j
+    __device__ void block_copy(const int *idx, int cnt, int64_t blk0, int64_t excl, int t, int nt) const {
+        const int64_t o0 = (int64_t)*base + excl;
+        const uint64_t *src = reinterpret_cast<const uint64_t *>(in);
+        uint64_t *dst = reinterpret_cast<uint64_t *>(out);
+        constexpr int WPR = sizeof(fic_record) / 8;  // 8-byte words per record
+        static_assert(sizeof(fic_record) % 8 == 0, "records move as 8-byte words");
+        for (int wd = t; wd < cnt * WPR; wd += nt) {
+            const int j = wd / WPR, k = wd - j * WPR;
+            if (o0 + j < cap) dst[(o0 + j) * WPR + k] = src[(blk0 + idx[j]) * WPR + k];
+        }
     }
 };
 
@@ -246,6 +257,8 @@ __global__ void __launch_bounds__(kChainThreads) select_chain_kernel(const uint8
                                                                      unsigned long long *d_total2) {
     __shared__ int wsum[kChainThreads / 32];
     __shared__ long long s_excl;
+    __shared__ int s_tot;
+    __shared__ int s_idx[Emit::kBlockCopy ? kChainBlock : 1];
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     const int64_t b0 = (int64_t)blockIdx.x * kChainBlock + (int64_t)t * kChainItems;
     uint32_t w[kChainItems / 4];
@@ -281,46 +294,88 @@ __global__ void __launch_bounds__(kChainThreads) select_chain_kernel(const uint8
     }
     if (lane == 31) wsum[warp] = incl;
     __syncthreads();
-    if (t == 0) {
+    if (warp == 0) {
+        // warp 0: the CTA's exclusive warp offsets and total, then a warp-wide look-back over 32
+        // predecessors at a time (the nearest one holding an inclusive prefix ends it; the
+        // aggregates before it are summed) -- one dependent round of loads per 32 predecessors
+        // instead of one per predecessor
         long long tot = 0;
-        for (int i = 0; i < kChainThreads / 32; ++i) {
-            const int ws = wsum[i];
-            wsum[i] = (int)tot;
-            tot += ws;
+        if (lane == 0) {
+            for (int i = 0; i < kChainThreads / 32; ++i) {
+                const int ws = wsum[i];
+                wsum[i] = (int)tot;
+                tot += ws;
+            }
         }
+        tot = __shfl_sync(0xffffffffu, tot, 0);
         const unsigned long long T = (unsigned long long)tag << 34;
         volatile unsigned long long *vs = state;
         long long excl = 0;
         if (blockIdx.x == 0) {
-            vs[0] = T | (2ull << 32) | (unsigned long long)tot;
+            if (lane == 0) vs[0] = T | (2ull << 32) | (unsigned long long)tot;
         } else {
-            vs[blockIdx.x] = T | (1ull << 32) | (unsigned long long)tot;  // aggregate
-            __threadfence();
-            for (int j = (int)blockIdx.x - 1;;) {
-                const unsigned long long v = vs[j];
-                if ((v >> 34) != tag) continue;  // predecessor not published yet
-                excl += (long long)(v & 0xffffffffull);
-                if (((v >> 32) & 3ull) == 2ull) break;  // inclusive prefix: done
-                --j;
+            if (lane == 0) {
+                vs[blockIdx.x] = T | (1ull << 32) | (unsigned long long)tot;  // aggregate
+                __threadfence();
             }
-            __threadfence();
-            vs[blockIdx.x] = T | (2ull << 32) | (unsigned long long)(excl + tot);
+            __syncwarp();
+            for (int j0 = (int)blockIdx.x - 1;;) {
+                const int j = j0 - lane;
+                unsigned long long v = 0;
+                bool ready = true;
+                if (j >= 0) {
+                    v = vs[j];
+                    ready = (v >> 34) == tag;  // published in this call
+                }
+                if (!__all_sync(0xffffffffu, ready)) continue;
+                const bool inc = j < 0 || ((v >> 32) & 3ull) == 2ull;
+                const unsigned im = __ballot_sync(0xffffffffu, inc);
+                const int stop = im ? __ffs(im) - 1 : 31;  // nearest inclusive prefix (or the window)
+                long long c = lane <= stop && j >= 0 ? (long long)(v & 0xffffffffull) : 0;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+                excl += c;
+                if (im) break;
+                j0 -= 32;
+            }
+            if (lane == 0) {
+                __threadfence();
+                vs[blockIdx.x] = T | (2ull << 32) | (unsigned long long)(excl + tot);
+            }
         }
-        s_excl = excl;
-        if (blockIdx.x == gridDim.x - 1) {
-            *d_total = (unsigned long long)(excl + tot);
-            if (d_total2) *d_total2 = (unsigned long long)(excl + tot);
+        if (lane == 0) {
+            s_excl = excl;
+            s_tot = (int)tot;
+            if (blockIdx.x == gridDim.x - 1) {
+                *d_total = (unsigned long long)(excl + tot);
+                if (d_total2) *d_total2 = (unsigned long long)(excl + tot);
+            }
         }
     }
     __syncthreads();
-    int64_t pos = s_excl + wsum[warp] + incl - cnt;
+    if constexpr (Emit::kBlockCopy) {
+        int lp = wsum[warp] + incl - cnt;  // position within the CTA's selection
 #pragma unroll
-    for (int q = 0; q < kChainItems / 4; ++q) {
-        uint32_t x = w[q];
-        while (x) {
-            const int bit = __ffs(x) - 1;  // lowest set flag byte first: index order
-            emit(b0 + 4 * q + (bit >> 3), pos++);
-            x &= x - 1;
+        for (int q = 0; q < kChainItems / 4; ++q) {
+            uint32_t x = w[q];
+            while (x) {
+                const int bit = __ffs(x) - 1;
+                s_idx[lp++] = (int)(t * kChainItems + 4 * q + (bit >> 3));
+                x &= x - 1;
+            }
+        }
+        __syncthreads();
+        emit.block_copy(s_idx, s_tot, (int64_t)blockIdx.x * kChainBlock, s_excl, t, kChainThreads);
+    } else {
+        int64_t pos = s_excl + wsum[warp] + incl - cnt;
+#pragma unroll
+        for (int q = 0; q < kChainItems / 4; ++q) {
+            uint32_t x = w[q];
+            while (x) {
+                const int bit = __ffs(x) - 1;  // lowest set flag byte first: index order
+                emit(b0 + 4 * q + (bit >> 3), pos++);
+                x &= x - 1;
+            }
         }
     }
 }
