@@ -42,12 +42,14 @@ struct fic_ctx {
     cudaStream_t crit = nullptr;                 // the encode's critical path (highest priority)
     bool child_clean = false;                    // b_child is all zero (see encode_body)
     cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
-    int overlap_pools = 0;                       // env FIC_OVERLAP_POOLS=1
+    int overlap_pools = 1;                       // env FIC_OVERLAP_POOLS=0: every pool on the main stream
     cudaEvent_t pool_ready[fic::kMaxLevels] = {};
     cudaEvent_t level_done[fic::kMaxLevels] = {};  // finalize of level l done (records ready)
     Buf b_blocksum2;  // compaction scratch of the side-stream record gathering
     Buf b_code;       // FIC1 writer scratch (fic_serialize)
     cudaEvent_t main_ready = nullptr;
+    Buf b_d2;                       // the decimated image, shared by the levels' pools (fic_encode)
+    cudaEvent_t d2_ready = nullptr;
     int b2_window = 1;    // env FIC_B2_WINDOW=0: B = 2 full scan instead of the C windows
     Buf b_u, b_gthr, b_rop, b_dec, b_nccl;
     ncclComm_t comm = nullptr;  // fic_ctx_create_nccl: one rank per GPU
@@ -136,9 +138,12 @@ int64_t entropy_threshold(double tau, int32_t m) {
 }
 
 // ------------------------------------------------------------------------- pool building
+// d2_shared: the decimated image of img built once for every level (fic_encode; d2_ready is
+// recorded after it), else the pool decimates into its own buffer
 fic_status pool_enqueue(fic_ctx *ctx, Pool &P, const uint8_t *img, int32_t N, int32_t B,
                         int32_t L, double tau, int64_t topk, cudaStream_t st,
-                        unsigned long long *d_kept_mirror = nullptr) {
+                        unsigned long long *d_kept_mirror = nullptr, const uint16_t *d2_shared = nullptr,
+                        cudaEvent_t d2_ready = nullptr) {
     P.device = ctx->device;
     P.N = N; P.B = B; P.L = L; P.n = B * B;
     P.A = (N - 2 * B) / L + 1;
@@ -150,7 +155,8 @@ fic_status pool_enqueue(fic_ctx *ctx, Pool &P, const uint8_t *img, int32_t N, in
     CK(grow(ctx, P.b_kept, sizeof(int32_t) * P.n_c));
     P.mode = B == 2 ? 3 : 0;  // B = 2: closed form on CUDA cores (fic_b2.cu); else tcgen05 (fic_tc.cu)
     if (P.mode == 0) CK(grow(ctx, P.b_Dtc, fic::tc_pool_bytes(B, tiles_max)));
-    if (P.mode == 0 && fic::tc_pool_d2_bytes(B, N, L)) CK(grow(ctx, P.b_D2, fic::tc_pool_d2_bytes(B, N, L)));
+    const bool own_d2 = P.mode == 0 && fic::tc_pool_d2_bytes(B, N, L) && !d2_shared;
+    if (own_d2) CK(grow(ctx, P.b_D2, fic::tc_pool_d2_bytes(B, N, L)));
     if (P.mode == 3) CK(grow(ctx, P.b_F2, fic::b2_pool_bytes(slots)));
     CK(grow(ctx, P.b_SDf, sizeof(float) * slots));
     CK(grow(ctx, P.b_SD, sizeof(int32_t) * slots));
@@ -176,9 +182,18 @@ fic_status pool_enqueue(fic_ctx *ctx, Pool &P, const uint8_t *img, int32_t N, in
     }
     CK(fic::launch_select_index(P.keep, P.n_c, ptr<int64_t>(P.b_blocksum), P.kept, &P.d_misc[0], st,
                                 d_kept_mirror));
-    if (P.mode == 0)
+    if (P.mode == 0) {
+        const uint16_t *D2 = nullptr;
+        if (own_d2) {
+            CK(fic::launch_decimate(img, N, L, ptr<uint16_t>(P.b_D2), st));
+            D2 = ptr<uint16_t>(P.b_D2);
+        } else if (fic::tc_pool_d2_bytes(B, N, L)) {
+            if (d2_ready) CK(cudaStreamWaitEvent(st, d2_ready, 0));
+            D2 = d2_shared;
+        }
         CK(fic::launch_pool_tc(img, N, B, L, P.A, P.kept, &P.d_misc[0], tiles_max, P.Dtc, P.SD, P.SDf, P.C,
-                               &P.d_misc[1], fic::tc_pool_d2_bytes(B, N, L) ? ptr<uint16_t>(P.b_D2) : nullptr, st));
+                               &P.d_misc[1], D2, st));
+    }
     else
         CK(fic::launch_b2_pool(img, N, L, P.A, P.kept, &P.d_misc[0], slots, P.b_F2.p, &P.b2, P.SD, P.SDf, P.C,
                                &P.d_misc[1], st));
@@ -187,7 +202,7 @@ fic_status pool_enqueue(fic_ctx *ctx, Pool &P, const uint8_t *img, int32_t N, in
         CK(fic::launch_pool_moments(img, N, B, L, P.A, P.kept, &P.d_misc[0], slots, P.SD, P.SDf, P.C,
                                     &P.d_misc[1], st));
     // entropy, select x3, gather, moments (+ the decimated image of the QR pools)
-    ctx->launches += 6 + (P.mode == 3 ? 1 : 0) - (fused ? 1 : 0) + (fic::tc_pool_d2_bytes(B, N, L) ? 1 : 0);
+    ctx->launches += 6 + (P.mode == 3 ? 1 : 0) - (fused ? 1 : 0) + (own_d2 ? 1 : 0);
     return FIC_OK;
 }
 
@@ -640,6 +655,7 @@ fic_status fic_ctx_create(int32_t device, void *cuda_stream, fic_ctx **out) {
     for (int l = 0; l < fic::kMaxLevels && e == cudaSuccess; ++l)
         e = cudaEventCreateWithFlags(&ctx->level_done[l], cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->main_ready, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->d2_ready, cudaEventDisableTiming);
     if (e != cudaSuccess) {
         fic_ctx_destroy(ctx);
         return FIC_ERR_CUDA;
@@ -680,8 +696,10 @@ fic_status fic_ctx_destroy(fic_ctx *ctx) {
     for (auto &e : ctx->level_done)
         if (e) cudaEventDestroy(e);
     free_buf(ctx->b_blocksum2);
+    free_buf(ctx->b_d2);
     free_buf(ctx->b_code);
     if (ctx->main_ready) cudaEventDestroy(ctx->main_ready);
+    if (ctx->d2_ready) cudaEventDestroy(ctx->d2_ready);
     if (ctx->side) {
         cudaStreamSynchronize(ctx->side);
         cudaStreamDestroy(ctx->side);
@@ -888,13 +906,23 @@ static fic_status encode_body(fic_ctx *ctx, const uint8_t *img, int32_t N, int32
     //    level-0 search (pools depend only on the image)
     CK(cudaEventRecord(ctx->main_ready, st));  // the image is ready (caller's stream order)
     CK(cudaStreamWaitEvent(ctx->side, ctx->main_ready, 0));
+    // the decimated image, once for every level, on the side stream: it overlaps the level-0
+    // entropy filter (the level-0 pool waits for d2_ready; the side-stream pools follow it)
+    const size_t d2_bytes = fic::tc_pool_d2_bytes(16, N, L);
+    const uint16_t *d2 = nullptr;
+    if (d2_bytes && B_max >= 4) {
+        CK(grow(ctx, ctx->b_d2, d2_bytes));
+        d2 = ptr<uint16_t>(ctx->b_d2);
+        CK(fic::launch_decimate(img, N, L, ptr<uint16_t>(ctx->b_d2), ctx->side));
+        CK(cudaEventRecord(ctx->d2_ready, ctx->side));
+    }
     for (int l = 0; l < nl; ++l) {
         cudaStream_t ps = (l == 0 || !ctx->overlap_pools) ? st : ctx->side;
-        ctx->launches = 0;
+        ctx->launches = l == 0 && d2 ? 1 : 0;
         if (ctx->timing >= 2) CK(cudaEventRecord(ctx->ev[l][0], ps));
         // (n_kept is also written next to the other counters: one device -> host copy at the end)
         CKS(pool_enqueue(ctx, ctx->levels[l], img, N, B_max >> l, L, h_topk ? -1.0 : h_tau[l],
-                         h_topk ? h_topk[l] : 0, ps, d_counts + 48 + l));
+                         h_topk ? h_topk[l] : 0, ps, d_counts + 48 + l, d2, ps == ctx->side ? nullptr : ctx->d2_ready));
         CKS(t2f_enqueue(ctx, ctx->levels[l], h_s + s_off[l], h_n_s[l], ps));
         if (ctx->timing >= 2) CK(cudaEventRecord(ctx->ev[l][4], ps));
         if (l > 0) CK(cudaEventRecord(ctx->pool_ready[l], ps));

@@ -306,10 +306,14 @@ int tc_nsplit_hint(int32_t B, int64_t n_r, int64_t n_tiles, int num_sms);
 int tc_pool_has_moments(int B);
 // D2: workspace of tc_pool_d2_bytes(B, N, L) bytes (the 2 x 2 decimated image, B >= 16), else null
 size_t tc_pool_d2_bytes(int B, int32_t N, int32_t L);
+// the decimated image D2 (tc_pool_d2_bytes(B, N, L) bytes, any tc pool B) of img
+cudaError_t launch_decimate(const uint8_t *img, int32_t N, int32_t L, uint16_t *D2, cudaStream_t st);
+// D2 must hold the decimated image (launch_decimate, earlier in stream order) when
+// tc_pool_d2_bytes(B, N, L) != 0
 cudaError_t launch_pool_tc(const uint8_t *img, int32_t N, int32_t B, int32_t L, int32_t A,
                            const int32_t *kept, const unsigned long long *d_nk, int64_t n_tiles_max,
                            uint8_t *Dtc, int32_t *SD, float *SDf, int64_t *C, unsigned long long *d_cmax,
-                           uint16_t *D2, cudaStream_t st);
+                           const uint16_t *D2, cudaStream_t st);
 size_t tc_range_bytes(int B, int64_t n_r);  // scratch for the prepared range operand + metadata
 cudaError_t launch_tc_search(int32_t B, const SearchParams &sp, const uint8_t *Dtc, int64_t n_slots,
                              uint8_t *scratch, cudaStream_t st);

@@ -536,17 +536,20 @@ size_t tc_pool_bytes(int B, int64_t n_tiles) {
 
 int tc_pool_has_moments(int B) { return TCfg_QR_or_F16(B) ? 1 : 0; }
 
+cudaError_t launch_decimate(const uint8_t *img, int32_t N, int32_t L, uint16_t *D2, cudaStream_t st) {
+    const int64_t d2n = (int64_t)(tc_pool_d2_bytes(16, N, L) / sizeof(uint16_t));  // (size independent of B)
+    if (d2n == 0) return cudaSuccess;
+    decimate_kernel<<<(unsigned)((d2n + 255) / 256), 256, 0, st>>>(img, N, L % 2 == 0 ? 1 : 4, D2);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_pool_tc(const uint8_t *img, int32_t N, int32_t B, int32_t L, int32_t A,
                            const int32_t *kept, const unsigned long long *d_nk, int64_t n_tiles_max,
                            uint8_t *Dtc, int32_t *SD, float *SDf, int64_t *C, unsigned long long *d_cmax,
-                           uint16_t *D2, cudaStream_t st) {
+                           const uint16_t *D2, cudaStream_t st) {
     if (B != 4 && B != 8 && B != 16 && B != 32) return cudaErrorInvalidValue;
     if (n_tiles_max == 0) return cudaSuccess;
-    if (tc_pool_d2_bytes(B, N, L)) {  // the decimated image (all parity classes the domains use)
-        if (!D2) return cudaErrorInvalidValue;
-        const int64_t d2n = (int64_t)(tc_pool_d2_bytes(B, N, L) / sizeof(uint16_t));
-        decimate_kernel<<<(unsigned)((d2n + 255) / 256), 256, 0, st>>>(img, N, L % 2 == 0 ? 1 : 4, D2);
-    }
+    if (tc_pool_d2_bytes(B, N, L) && !D2) return cudaErrorInvalidValue;
     if (B <= 8) {
         const int64_t total16 = n_tiles_max * kTileD * (B == 4 ? TCfg<4>::KP / 16 : TCfg<8>::KP / 16);
         const unsigned blocks = (unsigned)((total16 + 255) / 256);
