@@ -36,8 +36,8 @@ struct fic_ctx {
         b_scounts;
     unsigned long long *h_counts = nullptr;  // pinned [64]
     std::vector<fic_level_stats> stats;
-    cudaEvent_t ev[fic::kMaxLevels][5] = {};
-    int64_t launches = 0;
+    cudaEvent_t ev[fic::kMaxLevels][5] = {};  // pool start, search start, search end, finalize end, pool end
+    int64_t launches = 0;                      // libfic kernels enqueued (fic_level_stats.kernel_launches)
     cudaStream_t side = nullptr;                 // pool builds of levels >= 1 overlap the searches
     cudaStream_t crit = nullptr;                 // the encode's critical path (highest priority)
     bool child_clean = false;                    // b_child is all zero (see encode_body)
@@ -53,8 +53,18 @@ struct fic_ctx {
     int b2_window = 1;    // env FIC_B2_WINDOW=0: B = 2 full scan instead of the C windows
     Buf b_u, b_gthr, b_rop, b_dec, b_nccl;
     ncclComm_t comm = nullptr;  // fic_ctx_create_nccl: one rank per GPU
-    int32_t nranks = 1, rank = 0;  // libfic kernels enqueued (for fic_level_stats.kernel_launches)  // pool start, search start, search end, finalize end, pool end
+    int32_t nranks = 1, rank = 0;
 };
+
+namespace fic {
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char *v = getenv("FIC_PDL");
+        return !(v && strcmp(v, "0") == 0);
+    }();
+    return on;
+}
+}  // namespace fic
 
 namespace {
 
@@ -646,6 +656,10 @@ fic_status fic_ctx_create(int32_t device, void *cuda_stream, fic_ctx **out) {
     // path's small kernels are scheduled first
     int prio_lo = 0, prio_hi = 0;
     if (e == cudaSuccess) e = cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+    {
+        const char *sp = getenv("FIC_SIDE_PRIO");  // (A/B experiments: "hi" = the critical path's priority)
+        if (sp && strcmp(sp, "hi") == 0) prio_lo = prio_hi;
+    }
     if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&ctx->side, cudaStreamNonBlocking, prio_lo);
     if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&ctx->crit, cudaStreamNonBlocking, prio_hi);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->fork_ev, cudaEventDisableTiming);

@@ -556,6 +556,8 @@ constexpr int kStash = 64;  // phase-1 candidates kept per warp (overflow: full 
 __global__ void __launch_bounds__(256, 6) b2win_kernel(const __grid_constant__ B2Params P) {
     __shared__ int sStash[8][kStash];
     __shared__ int sNst[8];
+    pdl_wait();
+    pdl_trigger();
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     if (lane == 0) sNst[wib] = 0;
     __syncwarp();
@@ -843,7 +845,7 @@ cudaError_t launch_b2_search(const SearchParams &sp, const B2Pool &bp, float *T,
     p.d_nscan = reinterpret_cast<unsigned long long *>(scratch);
     p.gmin = reinterpret_cast<float *>(static_cast<char *>(scratch) + 64);
     if (win) {  // predefined s: Cauchy-Schwarz windows
-        b2win_kernel<<<(unsigned)((sp.n_r + 7) / 8), 256, 0, st>>>(p);
+        if (cudaError_t e = launch_pdl(b2win_kernel, dim3((unsigned)((sp.n_r + 7) / 8)), dim3(256), 0, st, p)) return e;
         return cudaGetLastError();
     }
     cudaError_t e = grid ? launch_b2_scan<0>(p, st)

@@ -88,6 +88,8 @@ __device__ __noinline__ void srd_all_dev(const FinalizeParams &P, int2 rr, int32
 // at a time: 14 us at B = 16).
 template <int BT>
 __global__ void __launch_bounds__(128) finalize_kernel(const __grid_constant__ FinalizeParams P) {
+    pdl_wait();
+    pdl_trigger();
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= (int)*P.d_nr) return;
     if (P.d_misc[0] == 0) {  // ranges but no domain block survived the entropy filter
@@ -238,14 +240,13 @@ cudaError_t launch_finalize(const FinalizeParams &p, cudaStream_t st) {
     if (p.n_r == 0) return cudaSuccess;
     const unsigned g = (unsigned)((p.n_r + 127) / 128);
     switch (p.B) {
-    case 2: finalize_kernel<2><<<g, 128, 0, st>>>(p); break;
-    case 4: finalize_kernel<4><<<g, 128, 0, st>>>(p); break;
-    case 8: finalize_kernel<8><<<g, 128, 0, st>>>(p); break;
-    case 16: finalize_kernel<16><<<g, 128, 0, st>>>(p); break;
-    case 32: finalize_kernel<32><<<g, 128, 0, st>>>(p); break;
+    case 2: return launch_pdl(finalize_kernel<2>, dim3(g), dim3(128), 0, st, p);
+    case 4: return launch_pdl(finalize_kernel<4>, dim3(g), dim3(128), 0, st, p);
+    case 8: return launch_pdl(finalize_kernel<8>, dim3(g), dim3(128), 0, st, p);
+    case 16: return launch_pdl(finalize_kernel<16>, dim3(g), dim3(128), 0, st, p);
+    case 32: return launch_pdl(finalize_kernel<32>, dim3(g), dim3(128), 0, st, p);
     default: return cudaErrorInvalidValue;
     }
-    return cudaGetLastError();
 }
 
 }  // namespace fic

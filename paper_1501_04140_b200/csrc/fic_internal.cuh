@@ -12,6 +12,7 @@
 #include <atomic>
 #include <cmath>
 #include <string>
+#include <utility>
 
 #include "fic.h"
 
@@ -168,6 +169,32 @@ inline cudaError_t ensure_smem_attr(F *fn, int bytes, std::atomic<unsigned long 
     e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     if (e == cudaSuccess) done_mask.fetch_or(bit, std::memory_order_acq_rel);
     return e;
+}
+
+// Programmatic dependent launch along the quadtree's critical path (finalize -> compaction ->
+// range preparation -> search -> ...): each kernel there is launched with programmatic stream
+// serialisation, lets its dependents launch as soon as all of its CTAs are running
+// (pdl_trigger), and waits for its predecessor's completion and memory (pdl_wait) before it
+// reads anything the predecessor wrote -- the dependent's launch and CTA placement overlap the
+// predecessor's tail instead of following it.  Outside such a launch both are no-ops.
+// FIC_PDL=0 launches them plainly.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args &&...args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
 // Dynamic mapping of a CTA to (range group, domain split) from the actual counts: the grid is

@@ -259,6 +259,8 @@ __global__ void __launch_bounds__(kChainThreads) select_chain_kernel(const uint8
     __shared__ long long s_excl;
     __shared__ int s_tot;
     __shared__ int s_idx[Emit::kBlockCopy ? kChainBlock : 1];
+    pdl_wait();
+    pdl_trigger();
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     const int64_t b0 = (int64_t)blockIdx.x * kChainBlock + (int64_t)t * kChainItems;
     uint32_t w[kChainItems / 4];
@@ -399,9 +401,8 @@ static cudaError_t select_run(const uint8_t *flags, int64_t n, int64_t *blocksum
         return cudaMemsetAsync(d_total, 0, sizeof(unsigned long long), st);
     }
     static_assert(kChainBlock == kSelBlock, "blocksum scratch holds one word per chain block");
-    select_chain_kernel<Emit><<<(unsigned)nb, kChainThreads, 0, st>>>(
-        flags, n, emit, reinterpret_cast<unsigned long long *>(blocksum), next_chain_tag(), d_total, d_total2);
-    return cudaGetLastError();
+    return launch_pdl(select_chain_kernel<Emit>, dim3((unsigned)nb), dim3(kChainThreads), 0, st, flags, n, emit,
+                      reinterpret_cast<unsigned long long *>(blocksum), next_chain_tag(), d_total, d_total2);
 }
 
 cudaError_t launch_select_index(const uint8_t *flags, int64_t n, int64_t *blocksum, int32_t *out,
@@ -433,6 +434,8 @@ cudaError_t launch_accumulate(unsigned long long *d_acc, const unsigned long lon
 }
 
 __global__ void top_flags_kernel(uint8_t *flags, int64_t n, int32_t shard, int32_t n_shards) {
+    pdl_wait();
+    pdl_trigger();
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) flags[i] = (uint8_t)((i % n_shards) == shard);
 }
@@ -440,8 +443,7 @@ __global__ void top_flags_kernel(uint8_t *flags, int64_t n, int32_t shard, int32
 cudaError_t launch_top_flags(uint8_t *flags, int64_t G, int32_t shard, int32_t n_shards,
                              cudaStream_t st) {
     const int64_t n = G * G;
-    top_flags_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(flags, n, shard, n_shards);
-    return cudaGetLastError();
+    return launch_pdl(top_flags_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, st, flags, n, shard, n_shards);
 }
 
 // Warp per domain slot: SD, SDD (int), C = n SDD - SD^2 (int64); pads get zeros.

@@ -704,6 +704,8 @@ __global__ void __launch_bounds__(256) tc_range_prep_kernel(const uint8_t *__res
                                                             int32_t n_pad, double smax,
                                                             const unsigned long long *__restrict__ d_misc,
                                                             TCRangeG *__restrict__ meta, int32_t univ) {
+    pdl_wait();
+    pdl_trigger();
     if ((int)blockIdx.x < nb_op) tc_range_operand_body<B>(img, N, ranges, d_nr, total16, Bop, blockIdx.x);
     else tc_range_meta_body<B>(img, N, ranges, d_nr, n_pad, smax, d_misc, meta, univ, blockIdx.x - nb_op);
 }
@@ -816,6 +818,8 @@ __device__ __forceinline__ void plan_segment(const SegPlan *sp, int k, int &grp,
 
 template <int B, int NSP>
 __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __grid_constant__ TCParams P) {
+    pdl_wait();
+    pdl_trigger();
     using Cf = TCfg<B>;
     constexpr int n = Cf::n, KP = Cf::KP, NR = Cf::NR, NN = Cf::N, KCH = Cf::KCH, CH = Cf::CH;
     constexpr int STAGES = Cf::STAGES;
@@ -1446,8 +1450,7 @@ static cudaError_t launch_tc_t(const TCParams &p, cudaStream_t st) {
     const int num_sms = p.num_sms > 0 ? p.num_sms : 148;
     int ctas = num_sms;
     if (const char *e = getenv("FIC_TC_CTAS")) ctas = std::max(1, atoi(e));  // test hook: small grids
-    tcsearch_kernel<B, NSP><<<(unsigned)ctas, Cf::THREADS, smem, st>>>(p);
-    return cudaGetLastError();
+    return launch_pdl(tcsearch_kernel<B, NSP>, dim3((unsigned)ctas), dim3(Cf::THREADS), smem, st, p);
 }
 
 template <int B>
@@ -1482,9 +1485,10 @@ static cudaError_t tc_range_prep(const SearchParams &sp, uint8_t *scratch, TCPar
     const int n_pad = (int)(groups * Cf::NR);
     const int64_t meta_threads = (int64_t)n_pad * (B >= 8 ? 32 : 1);
     const int nb_op = (int)((total16 + 255) / 256), nb_meta = (int)((meta_threads + 255) / 256);
-    tc_range_prep_kernel<B><<<(unsigned)(nb_op + nb_meta), 256, 0, st>>>(sp.img, sp.N, sp.ranges, sp.d_nr, total16,
-                                                                        Bop, nb_op, n_pad, sp.smax, sp.d_misc, meta,
-                                                                        sp.nsp > 2 ? (sp.grid.on ? 2 : 1) : 0);
+    if (cudaError_t e = launch_pdl(tc_range_prep_kernel<B>, dim3((unsigned)(nb_op + nb_meta)), dim3(256), 0, st,
+                                   sp.img, sp.N, sp.ranges, sp.d_nr, total16, Bop, nb_op, n_pad, sp.smax, sp.d_misc,
+                                   meta, (int32_t)(sp.nsp > 2 ? (sp.grid.on ? 2 : 1) : 0)))
+        return e;
     p.Bop = Bop;
     p.rmeta = meta;
     return cudaGetLastError();
