@@ -470,7 +470,8 @@ def main():
                    "records_per_step": n_rec},
         "roofline": {"bound": "alu" if 4.0 * n / pk["int8"] < 2.0 / pk["int32"] + 0.5 * nS / pk["fp64"] else "tensor",
                      "kernel": ("b2win_kernel (B=2 closed form, C windows, CUDA cores)" if dom["B"] == 2
-                                else f"tcsearch_kernel<B={dom['B']}> (tcgen05 kind::i8)"),
+                                else f"tcsearch_kernel<B={dom['B']}> (tcgen05 "
+                                     + ("kind::f16, exact fp32 accumulation)" if dom["B"] <= 8 else "kind::i8)")),
                      "achieved": achieved, "peak": peak, "unit": "Gpairs/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "peak_note": "SURVEY 8(d): 1/max(4n/P_int8, 2/P_int32 + 0.5|S|/P_fp64) pairs/s with "
