@@ -546,14 +546,21 @@ __device__ __forceinline__ double b2_canon(const B2Params &P, double A, float bq
     return e0;
 }
 
-constexpr int kWinStep = 64;  // domains per frontier per round
+#ifndef FIC_B2_WINSTEP
+#define FIC_B2_WINSTEP 128
+#endif
+#ifndef FIC_B2_MINB
+#define FIC_B2_MINB 4
+#endif
+constexpr int kWinStep = FIC_B2_WINSTEP;  // domains per frontier per round
+constexpr int kWinPer = 4 * (kWinStep / 32);  // features per lane per round
 
 constexpr int kStash = 64;  // phase-1 candidates kept per warp (overflow: full phase-2 sweep)
 
 // 6 CTAs (48 warps) per SM: the rounds are L2-latency bound, and more resident warps beat the
 // few spills of the 40-register budget (C3 B = 2: 74 regs 0.312 ms, 64 0.273, 48 0.260, 40 0.251,
 // 32 0.265)
-__global__ void __launch_bounds__(256, 6) b2win_kernel(const __grid_constant__ B2Params P) {
+__global__ void __launch_bounds__(256, FIC_B2_MINB) b2win_kernel(const __grid_constant__ B2Params P) {
     __shared__ int sStash[8][kStash];
     __shared__ int sNst[8];
     pdl_wait();
@@ -627,11 +634,11 @@ __global__ void __launch_bounds__(256, 6) b2win_kernel(const __grid_constant__ B
         if (lane == 3 && q3 < n_k) cn = __ldg(P.Cs + q3);
         // all of this lane's loads of the round first (up to 8 domains, L2-latency bound), then
         // the arithmetic; absent slots read position 0 and are masked to +inf
-        float4 fv[8];
-        bool ok8[8];
+        float4 fv[kWinPer];
+        bool ok8[kWinPer];
         const int nf[4] = {n0, n1, n2, n3}, bf[4] = {b0, b1, b2, b3};
 #pragma unroll
-        for (int k = 0; k < 2; ++k) {
+        for (int k = 0; k < kWinStep / 32; ++k) {
 #pragma unroll
             for (int f = 0; f < 4; ++f) {
                 const int o = lane + 32 * k;
@@ -640,9 +647,9 @@ __global__ void __launch_bounds__(256, 6) b2win_kernel(const __grid_constant__ B
                 fv[k * 4 + f] = __ldg(P.F + pos);
             }
         }
-        float g = INFINITY, gv[8];
+        float g = INFINITY, gv[kWinPer];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
+        for (int i = 0; i < kWinPer; ++i) {
             float bq;
             const float gi = gof(fv[i], bq);
             gv[i] = ok8[i] ? gi : INFINITY;
@@ -656,7 +663,7 @@ __global__ void __launch_bounds__(256, 6) b2win_kernel(const __grid_constant__ B
             const float ts = fminf(__fadd_ru(gmin, marg2_ru), FLT_MAX);
             if (__any_sync(0xffffffffu, g <= ts)) {  // (g: this lane's minimum of the round)
 #pragma unroll
-                for (int i = 0; i < 8; ++i) {
+                for (int i = 0; i < kWinPer; ++i) {
                     if (gv[i] <= ts) {
                         const int slot = atomicAdd(&sNst[wib], 1);
                         if (slot < kStash) sStash[wib][slot] = bf[i & 3] + lane + 32 * (i >> 2);
