@@ -75,9 +75,21 @@ struct TCfg {
 #ifndef FIC_B4_EWG
 #define FIC_B4_EWG 3
 #endif
+#ifndef FIC_B8_NR
+#define FIC_B8_NR 32
+#endif
+#ifndef FIC_B8_EWG
+#define FIC_B8_EWG 4
+#endif
+#ifndef FIC_B16_NR
+#define FIC_B16_NR 16
+#endif
+#ifndef FIC_B16_EWG
+#define FIC_B16_EWG 4
+#endif
     // B = 32 (QR, n = 1024 K bytes per range row): 8 ranges, so the 64 KB range operand and two
     // 64 KB A stages fit shared memory
-    static constexpr int NR = (B == 32) ? 8 : (B == 16) ? 16 : (B == 4 ? FIC_B4_NR : 32);
+    static constexpr int NR = (B == 32) ? 8 : (B == 16) ? FIC_B16_NR : (B == 4 ? FIC_B4_NR : FIC_B8_NR);
     static constexpr int N = 8 * NR;                       // MMA N (columns per accumulator)
     static constexpr int KCH = QR ? 512 : (KP < 256 ? KP : 256);  // K bytes per pipeline stage (F16: a tile)
     static constexpr int CH = KP / KCH;                    // stages per domain tile
@@ -93,7 +105,7 @@ struct TCfg {
     static constexpr int BBUF = (B == 4 || F16) ? 2 : 1;
     static constexpr int ACC = QR ? 2 * N : N;             // TMEM columns per accumulator buffer
     static constexpr int NBUF = 512 / ACC >= 4 ? 4 : 512 / ACC;  // TMEM accumulator buffers (MMA <-> epilogue)
-    static constexpr int EWG = B == 4 ? FIC_B4_EWG : (B == 32 ? 2 : 4);   // epilogue warpgroups
+    static constexpr int EWG = B == 4 ? FIC_B4_EWG : (B == 32 ? 2 : B == 8 ? FIC_B8_EWG : FIC_B16_EWG);  // epilogue warpgroups
     // ranges per warpgroup, in groups of 4 (one 32-column tcgen05.ld); when EWG does not divide
     // NR / 4 the last warpgroup's trailing groups are empty (skipped)
     static constexpr int HALF = ((NR + 4 * EWG - 1) / (4 * EWG)) * 4;
