@@ -587,48 +587,60 @@ __device__ __forceinline__ void tc_range_operand_body(const uint8_t *__restrict_
     using Cf = TCfg<B>;
     // source pixel of byte p of row k: Rperm_k(p) = R(f_k^{-1}(p)); under this numbering
     // f_k^{-1} = f_{k'} with k' = [0,3,2,1,4,5,6,7][k] (rotations by 90/270 swap, the rest are
-    // involutions) -- tabulated once per block
-    using SrcT = typename std::conditional<(Cf::n > 256), uint16_t, uint8_t>::type;  // pixel index < n
-    __shared__ SrcT src[8][Cf::n];
-    for (int t = threadIdx.x; t < 8 * Cf::n; t += blockDim.x) {
-        const int kk = t / Cf::n, p = t % Cf::n;
-        const int kinv = (kk == 1) ? 3 : (kk == 3 ? 1 : kk);
-        int si, sj;
-        tiso_src(B, kinv, p / B, p % B, si, sj);
-        src[kk][p] = (SrcT)(si * B + sj);
+    // involutions).  The block's ranges are first staged in shared memory (row-contiguous
+    // loads); each thread then forms its 16 bytes from there, the source index in closed form
+    // (mirror, then k' & 3 quarter turns) -- instead of a per-block table and 16 scattered
+    // global byte loads per thread.
+    constexpr int G16 = Cf::KB / 16;
+    constexpr int RPB = (256 / G16 + 7) / 8 + 1;  // ranges a 256-thread block can touch
+    __shared__ uint8_t sR[RPB][Cf::n];
+    const int64_t e0 = (int64_t)bx * blockDim.x;
+    const int64_t e = e0 + threadIdx.x;  // one 16-byte group
+    const int64_t n_r = (int64_t)*d_nr;
+    auto range_of = [&](int64_t ee) {  // range index of group ee's row
+        const int64_t rg = ee / G16;
+        return (rg / Cf::N) * Cf::NR + (int)(rg % Cf::N) / 8;
+    };
+    const int64_t r_first = range_of(e0);
+    for (int t = threadIdx.x; t < RPB * Cf::n; t += blockDim.x) {
+        const int q = t / Cf::n, p = t % Cf::n;
+        const int64_t r = r_first + q;
+        uint8_t v = 0;
+        if (r < n_r && e0 < total16) {
+            const int2 rr = ranges[r];
+            v = img[(size_t)(rr.y + p / B) * N + rr.x + p % B];
+        }
+        sR[q][p] = v;
     }
     __syncthreads();
-    const int64_t e = (int64_t)bx * blockDim.x + threadIdx.x;  // one 16-byte group
     if (e >= total16) return;
-    const int64_t n_r = (int64_t)*d_nr;
     if (e / ((int64_t)Cf::N * (Cf::KB / 16)) > (n_r + Cf::NR - 1) / Cf::NR) return;  // past the last group
-    constexpr int G16 = Cf::KB / 16;
     const int64_t row_g = e / G16;  // global row = group * N + row
     const int g = (int)(e % G16);
     const int64_t grp = row_g / Cf::N;
     const int row = (int)(row_g % Cf::N);
     const int rl = row >> 3, k = row & 7;
     const int64_t r = grp * Cf::NR + rl;
+    const uint8_t *rs = sR[r - r_first];
+    const int kinv = (k == 1) ? 3 : (k == 3 ? 1 : k), rot = kinv & 3;
+    constexpr int b = B - 1;
+    auto src = [&](int p) {  // pixel index of byte p of row k
+        const int i = p / B, j0 = p % B;
+        const int j = kinv >= 4 ? b - j0 : j0;
+        const int si = rot == 0 ? i : rot == 1 ? b - j : rot == 2 ? b - i : j;
+        const int sj = rot == 0 ? j : rot == 1 ? i : rot == 2 ? b - j : b - i;
+        return si * B + sj;
+    };
     uint32_t w[4] = {0, 0, 0, 0};
     if (Cf::F16 && r < n_r) {  // fp16 elements 8g .. 8g + 7 of Rperm_k
-        const int2 rr = ranges[r];
-        const uint8_t *rb = img + (size_t)rr.y * N + rr.x;
 #pragma unroll
-        for (int q = 0; q < 8; q += 2) {
-            const int s0 = src[k][g * 8 + q], s1 = src[k][g * 8 + q + 1];
-            w[q >> 1] = f16x2_int(rb[(size_t)(s0 / B) * N + s0 % B], rb[(size_t)(s1 / B) * N + s1 % B]);
-        }
+        for (int q = 0; q < 8; q += 2) w[q >> 1] = f16x2_int(rs[src(g * 8 + q)], rs[src(g * 8 + q + 1)]);
     } else if (r < n_r) {
-        const int2 rr = ranges[r];
-        const uint8_t *rb = img + (size_t)rr.y * N + rr.x;
 #pragma unroll
         for (int q = 0; q < 16; ++q) {
             const int kb = g * 16 + q;
             uint32_t v = 0;
-            if (kb < (Cf::QR ? Cf::n : 4 * Cf::n)) {  // 4 polyphase copies, or once (QR)
-                const int sp = src[k][kb % Cf::n];
-                v = rb[(size_t)(sp / B) * N + sp % B];
-            }
+            if (kb < (Cf::QR ? Cf::n : 4 * Cf::n)) v = rs[src(kb % Cf::n)];  // 4 polyphase copies, or once (QR)
             w[q >> 2] |= v << (8 * (q & 3));
         }
     }
