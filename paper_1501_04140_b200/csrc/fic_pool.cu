@@ -85,6 +85,8 @@ __global__ void __launch_bounds__(256) entropy_slide_kernel(
     const int64_t *__restrict__ g_delta, int64_t lut_m, int64_t T, int use_tau,
     int64_t *__restrict__ keys, uint8_t *__restrict__ keep) {
     extern __shared__ __align__(16) unsigned char sm[];
+    pdl_wait();
+    pdl_trigger();
     const int m = side * side;
     int64_t *delta = reinterpret_cast<int64_t *>(sm);
     int32_t *hist_all = reinterpret_cast<int32_t *>(sm + sizeof(int64_t) * m);
@@ -177,9 +179,8 @@ cudaError_t launch_entropy_keys(const uint8_t *img, int32_t N, int32_t B, int32_
         static std::atomic<unsigned long long> attr2{0};
         if (cudaError_t e = ensure_smem_attr(entropy_slide_kernel, 64 * 1024, attr2)) return e;
         const int64_t warps = (int64_t)A * ((A + kSlideSeg - 1) / kSlideSeg);
-        entropy_slide_kernel<<<(unsigned)((warps + 7) / 8), 256, smem, st>>>(img, N, side, L, A, d_delta, lut_m, T,
-                                                                             use_tau, keys, keep);
-        return cudaGetLastError();
+        return launch_pdl(entropy_slide_kernel, dim3((unsigned)((warps + 7) / 8)), dim3(256), smem, st, img, N, side, L,
+                          A, d_delta, lut_m, T, use_tau, keys, keep);
     }
     const size_t smem = sizeof(int64_t) * m + 8 * 256 * sizeof(int32_t);
     static std::atomic<unsigned long long> attr{0};
@@ -506,6 +507,8 @@ cudaError_t launch_pool_moments(const uint8_t *img, int32_t N, int32_t B, int32_
 __global__ void t2f_kernel(const int64_t *__restrict__ C, const unsigned long long *__restrict__ d_nk,
                            int64_t n_slots, const SList spos, int32_t nsp, float *__restrict__ t2f, int32_t univ,
                            float fold, float grid_h) {
+    pdl_wait();
+    pdl_trigger();
     const int64_t d = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (d >= n_slots) return;
     const int64_t n_k = (int64_t)*d_nk;
@@ -534,8 +537,8 @@ __global__ void t2f_kernel(const int64_t *__restrict__ C, const unsigned long lo
 cudaError_t launch_t2f(const int64_t *C, const unsigned long long *d_nk, int64_t n_slots, const SList &spos,
                        int32_t nsp, float *t2f, int32_t univ, float fold, cudaStream_t st, float grid_h) {
     if (n_slots == 0 || nsp == 0) return cudaSuccess;
-    t2f_kernel<<<(unsigned)((n_slots + 255) / 256), 256, 0, st>>>(C, d_nk, n_slots, spos, nsp, t2f, univ, fold, grid_h);
-    return cudaGetLastError();
+    return launch_pdl(t2f_kernel, dim3((unsigned)((n_slots + 255) / 256)), dim3(256), 0, st, C, d_nk, n_slots, spos,
+                      nsp, t2f, univ, fold, grid_h);
 }
 
 // ----------------------------------------------------------------------------- shard merge
