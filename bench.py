@@ -226,17 +226,23 @@ def roofline_peaks():
     """P_int8, P_int32, P_fp64 of SURVEY §8(d)'s pair-kernel roofline, measured on a B200 of this
     pool by scripts/micro/peaks.cu (profiles/peaks_r02.json); the nominal B200 figures if the file
     is missing (stated in `source`)."""
+    # dense f16 MMA rate: the driver-measured bf16 cuBLAS burst figure (same tensor rate as f16,
+    # guide's nominal ratio 1:1), else the nominal 2.25 PFLOP/s
+    mp = load_peaks()
+    f16 = float(mp["bf16_tflops"]) * 1e12 if mp.get("bf16_tflops") else 2.25e15
     try:
         d = json.load(open(os.path.join(ROOT, "profiles", "peaks_r02.json")))
         i32 = d["int32_lane_ops_per_s"]
         return {"int8": float(d["int8_tc_ops_per_s"]),
                 "int32": float(max(i32.values())),
                 "fp64": float(d["fp64_lane_ops_per_s"]["dfma"]),
+                "f16": f16,
                 "source": "measured: profiles/peaks_r02.json (scripts/micro/peaks.cu, all SMs, CUDA events); "
-                          "P_int32 = best int mix (IMAD + VIMNMX3), P_fp64 = DFMA lane-ops/s"}
+                          "P_int32 = best int mix (IMAD + VIMNMX3), P_fp64 = DFMA lane-ops/s; "
+                          "P_f16 = MEASURED_PEAKS.json bf16_tflops (burst)"}
     except Exception:
-        f = float(load_peaks().get("sm_max_mhz", 1965.0)) * 1e6
-        return {"int8": 4.5e15, "int32": 148 * 128 * f, "fp64": 148 * 64 * f,
+        f = float(mp.get("sm_max_mhz", 1965.0)) * 1e6
+        return {"int8": 4.5e15, "int32": 148 * 128 * f, "fp64": 148 * 64 * f, "f16": f16,
                 "source": "nominal (profiles/peaks_r02.json missing): 4.5 POPS int8, 128 / 64 lanes per SM"}
 
 
@@ -425,26 +431,41 @@ def main():
             dist.destroy_process_group()
         return 0
 
-    # ---- roofline of the dominant kernel (the level search with the largest device time),
-    # SURVEY.md §8(d):  T_roof = pairs * max(4n / P_int8, 2 / P_int32 + 0.5 |S| / P_fp64)
+    # ---- roofline of the dominant kernel (the level search with the largest device time).
+    # SURVEY.md §8(d):  T_roof = pairs * max(4n / P_int8, 2 / P_int32 + 0.5 |S| / P_fp64).  The
+    # fp64 term charges every pair the binary64 scoring that the kernels replace by an fp32 filter
+    # with a rigorous margin (the exact path scores ~0.003% of the pairs), so that model is not a
+    # ceiling of this design (C3 tcsearch<4>: 1.14 of it).  The reported `roofline` keeps the
+    # model's integer term and the tensor term of the operand form the kernel runs:
+    #   T = pairs * max(T_tc, 2 / P_int32),  T_tc = 2n / P_f16 (B = 4, 8: kind::f16, K = n),
+    #   4n / P_int8 (B >= 16: kind::i8, q and r planes), none at B = 2 (CUDA-core closed form).
+    # `roofline_survey_model` reports the SURVEY model unchanged.
     pk = roofline_peaks()
 
-    def t_pair(B, nS):  # seconds per pair at the roofline
+    def t_pair_survey(B, nS):  # seconds per pair, SURVEY 8(d) as written
         n = B * B
         return max(4.0 * n / pk["int8"], 2.0 / pk["int32"] + 0.5 * nS / pk["fp64"])
+
+    def t_tc(B):
+        n = B * B
+        return 0.0 if B == 2 else (2.0 * n / pk["f16"] if B <= 8 else 4.0 * n / pk["int8"])
+
+    def t_pair(B):  # seconds per pair: the integer term and the kernel's tensor term
+        return max(t_tc(B), 2.0 / pk["int32"])
 
     lv_B = [lv["B"] for lv in level_acc]
     for lv in level_acc:
         nS_l = len(cfg["s"][lv_B.index(lv["B"])])
         evald = lv["pairs_scanned"] * 8  # pairs the kernel evaluated (B=2 windows skip proven losers)
         t_l = lv["ms_search"] / args.steps / 1e3
-        lv["roof_frac"] = (evald * t_pair(lv["B"], nS_l) / t_l) if t_l > 0 else None
+        lv["roof_frac"] = (evald * t_pair(lv["B"]) / t_l) if t_l > 0 else None
+        lv["roof_frac_survey_model"] = (evald * t_pair_survey(lv["B"], nS_l) / t_l) if t_l > 0 else None
     dom = max(level_acc, key=lambda s: s["ms_search"])
-    n = dom["B"] * dom["B"]
     nS = len(cfg["s"][lv_B.index(dom["B"])])
     ms_launch = dom["ms_search"] / args.steps
     achieved = dom["pairs_scanned"] * 8 / (ms_launch / 1e3) / 1e9
-    peak = 1.0 / t_pair(dom["B"], nS) / 1e9
+    peak = 1.0 / t_pair(dom["B"]) / 1e9
+    peak_survey = 1.0 / t_pair_survey(dom["B"], nS) / 1e9
     traffic = load_traffic("b2win_kernel" if dom["B"] == 2 else f"tcsearch_kernel<{dom['B']},")
 
     res = {
@@ -468,33 +489,34 @@ def main():
                    "l2": "flushed between timed steps (256 MB write)",
                    "pairs_per_step": pairs_step, "evaluated_pairs_per_step": evald_step,
                    "records_per_step": n_rec},
-        "roofline": {"bound": "alu" if 4.0 * n / pk["int8"] < 2.0 / pk["int32"] + 0.5 * nS / pk["fp64"] else "tensor",
+        "roofline": {"bound": "tensor" if t_tc(dom["B"]) > 2.0 / pk["int32"] else "alu",
                      "kernel": ("b2win_kernel (B=2 closed form, C windows, CUDA cores)" if dom["B"] == 2
                                 else f"tcsearch_kernel<B={dom['B']}> (tcgen05 "
                                      + ("kind::f16, exact fp32 accumulation)" if dom["B"] <= 8 else "kind::i8)")),
                      "achieved": achieved, "peak": peak, "unit": "Gpairs/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "peak_note": "SURVEY 8(d): 1/max(4n/P_int8, 2/P_int32 + 0.5|S|/P_fp64) pairs/s with "
-                                  f"P_int8 = {pk['int8']:.3e} ops/s, P_int32 = {pk['int32']:.3e}, "
-                                  f"P_fp64 = {pk['fp64']:.3e} ({pk['source']}); achieved counts the pairs "
-                                  "the kernel evaluated (DESIGN.md 7)"},
+                     "peak_note": "1/max(T_tc, 2/P_int32) pairs/s: SURVEY 8(d)'s integer term (2 int ops per pair) "
+                                  "and the tensor term of the kernel's operand form (2n/P_f16 at B = 4, 8; "
+                                  f"4n/P_int8 at B >= 16); P_int32 = {pk['int32']:.3e} ops/s, "
+                                  f"P_int8 = {pk['int8']:.3e}, P_f16 = {pk['f16']:.3e} ({pk['source']}); "
+                                  "achieved counts the pairs the kernel evaluated (DESIGN.md 7)"},
+        "roofline_survey_model": {"achieved": achieved, "peak": peak_survey, "unit": "Gpairs/s",
+                                  "frac": achieved / peak_survey,
+                                  "note": "SURVEY 8(d) as written, 1/max(4n/P_int8, 2/P_int32 + 0.5|S|/P_fp64) "
+                                          f"with P_fp64 = {pk['fp64']:.3e}: its fp64 term charges every pair the "
+                                          "binary64 scoring the fp32 filter avoids, so it is not a ceiling here"},
         "levels": [{"B": s["B"], "n_candidates": s["n_candidates"], "n_kept": s["n_kept"],
                     "n_ranges": s["n_ranges"], "pairs": s["pairs"],
                     "exact_evals": s["exact_evals"], "pairs_scanned": s["pairs_scanned"],
                     "pruned_frac": 1.0 - s["pairs_scanned"] / max(1, s["n_ranges"] * s["n_kept"]),
                     "ms_pool": s["ms_pool"] / args.steps, "ms_search": s["ms_search"] / args.steps,
-                    "ms_finalize": s["ms_finalize"] / args.steps, "roof_frac": s["roof_frac"]}
+                    "ms_finalize": s["ms_finalize"] / args.steps, "roof_frac": s["roof_frac"],
+                    "roof_frac_survey_model": s["roof_frac_survey_model"]}
                    for s in level_acc],
         "quality": quality,
         "gpu_launches": int(launches),
         "clocks": clk,
     }
-    # the same kernel against the int-only part of the model (2 int ops per pair, no fp64 term):
-    # the kernel replaces the model's per-pair fp64 scoring by an fp32 filter with a rigorous
-    # margin, so the SURVEY model's fraction can exceed what its int work alone would allow
-    res["roofline_int_only"] = {"bound": "alu", "achieved": achieved, "peak": pk["int32"] / 2.0 / 1e9,
-                                "unit": "Gpairs/s", "frac": achieved / (pk["int32"] / 2.0 / 1e9),
-                                "note": "peak = P_int32 / 2 pairs/s (SURVEY 8(d)'s 2 int ops per pair)"}
     if mgpu_parity is not None:
         res["multi_gpu_parity"] = mgpu_parity
     if e2e:

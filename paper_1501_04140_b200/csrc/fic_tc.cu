@@ -1346,65 +1346,77 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
 #pragma unroll
                     for (int i = 0; i < 32; ++i) vv[i] = 4u * vv[i] + vv[32 + i];
                 }
+                // the filter of GB ranges at a time (branch-free, their chains interleaved), then one
+                // branch into the rare queueing path, which re-forms the max of each passing range
+                // from the accumulators still in registers (one group of 4 ranges per branch: the whole
+                // tile per branch, FIC_B4_GB=8 at B = 4, was measured slower: 0.507 -> 0.553 ms)
+#ifndef FIC_B4_GB
+#define FIC_B4_GB 4
+#endif
+                constexpr int GB = (B == 4 && FIC_B4_GB <= G * 4) ? FIC_B4_GB : 4;
+                static_assert(GB % 4 == 0 && (G * 4) % GB == 0, "branch groups of whole tcgen05.ld groups");
 #pragma unroll
-                for (int g = 0; g < G; ++g) {
+                for (int gb = 0; gb < G * 4 / GB; ++gb) {
+                unsigned pm = 0;
+#pragma unroll
+                for (int g = gb * GB / 4; g < (gb + 1) * GB / 4; ++g) {
                     if (UNEVEN && eg * HALF + g * 4 >= NR) continue;  // an empty group
-                    unsigned pm = 0;
-                    int mxs[4];
 #pragma unroll
-                    for (int q4 = 0; q4 < 4; ++q4) {  // branch-free filter of four ranges
+                    for (int q4 = 0; q4 < 4; ++q4) {
                         const int q = g * 4 + q4;
-                        const uint32_t *v = vv + g * 32 + q4 * 8;
+                        const uint32_t *v = vv + q * 8;
                         const int mx = max(__vimax3_s32((int)v[0], (int)v[1], (int)v[2]),
                                            __vimax3_s32((int)v[3], (int)v[4], __vimax3_s32((int)v[5], (int)v[6], (int)v[7])));
-                        mxs[q4] = mx;
                         // (B = 8, at its 96-register ceiling: the range sums from shared memory)
                         const float g0 = score(mx, B == 8 ? sSR[eg * HALF + q] : rSR[q], sd, sdn, t2);
-                        pm |= (g0 <= sThr[eg * HALF + q]) ? (1u << q4) : 0u;
+                        pm |= (g0 <= sThr[eg * HALF + q]) ? (1u << q) : 0u;
                     }
+                }
 #ifdef FIC_TC_TRACE
-                    const long long tp0 = clock64();
+                const long long tp0 = clock64();
 #endif
-                    if (pm) {  // queue (range, domain, k*, max SRD) of the passing pairs for the exact warp
+                // (a warp-uniform branch on __any_sync instead: B = 4 0.508 -> 0.525 ms)
+                if (pm) {  // queue (range, domain, k*, max SRD) of the passing pairs for the exact warp
 #pragma unroll
-                        for (int q4 = 0; q4 < 4; ++q4) {
-                            if (pm >> q4 & 1) {
-                                const uint32_t *v = vv + g * 32 + q4 * 8;
-                                int ks = 7;
+                    for (int q = gb * GB; q < (gb + 1) * GB; ++q) {
+                        if (pm >> q & 1) {
+                            const uint32_t *v = vv + q * 8;
+                            const int mx = max(__vimax3_s32((int)v[0], (int)v[1], (int)v[2]),
+                                               __vimax3_s32((int)v[3], (int)v[4], __vimax3_s32((int)v[5], (int)v[6], (int)v[7])));
+                            int ks = 7;
 #pragma unroll
-                                for (int k = 6; k >= 0; --k)
-                                    if ((int)v[k] == mxs[q4]) ks = k;  // lowest index attaining the max
-                                // tighten the range's threshold at once from the fp32 score (the
-                                // exact warp's own update, RU(e - A + margin), comes later): with
-                                // NSP > 0, g approximates min_{s > 0} e_s - A within the margin, so
-                                // e <= A + g + margin and RU(g + 2 margin) is a valid threshold
-                                // (NSP = 0: g is only a lower bound of the grid's minimum -- no)
-                                if constexpr (NSP > 0) {
-                                    const int q = g * 4 + q4;
-                                    const float g0 = score(mxs[q4], B == 8 ? sSR[eg * HALF + q] : rSR[q], sd, sdn, t2);
-                                    const float t = fminf(__fadd_ru(g0, sM2[eg * HALF + q]), FLT_MAX);
-                                    int *ti = reinterpret_cast<int *>(&sThr[eg * HALF + q]);
-                                    int old = *ti;
-                                    while (t < __int_as_float(old)) {
-                                        const int prev = atomicCAS(ti, old, __float_as_int(t));
-                                        if (prev == old) break;
-                                        old = prev;
-                                    }
+                            for (int k = 6; k >= 0; --k)
+                                if ((int)v[k] == mx) ks = k;  // lowest index attaining the max
+                            // tighten the range's threshold at once from the fp32 score (the
+                            // exact warp's own update, RU(e - A + margin), comes later): with
+                            // NSP > 0, g approximates min_{s > 0} e_s - A within the margin, so
+                            // e <= A + g + margin and RU(g + 2 margin) is a valid threshold
+                            // (NSP = 0: g is only a lower bound of the grid's minimum -- no)
+                            if constexpr (NSP > 0) {
+                                const float g0 = score(mx, B == 8 ? sSR[eg * HALF + q] : rSR[q], sd, sdn, t2);
+                                const float t = fminf(__fadd_ru(g0, sM2[eg * HALF + q]), FLT_MAX);
+                                int *ti = reinterpret_cast<int *>(&sThr[eg * HALF + q]);
+                                int old = *ti;
+                                while (t < __int_as_float(old)) {
+                                    const int prev = atomicCAS(ti, old, __float_as_int(t));
+                                    if (prev == old) break;
+                                    old = prev;
                                 }
-                                const unsigned xi = atomicAdd(&sXCtl[0], 1u);
-                                while (xi - vctl[1] >= (unsigned)Cf::XQ) __nanosleep(32);  // ring full (rare)
-                                XItem it;
-                                it.mx = Cf::F16 ? (int)__int_as_float(mxs[q4]) : mxs[q4];
-                                it.d = d; it.sd = sd;
-                                it.meta = (eg * HALF + g * 4 + q4) | (ks << 5) | (m << 8);
-                                sXQ[xi & (Cf::XQ - 1)] = it;
-                                __threadfence_block();
-                                reinterpret_cast<volatile unsigned *>(sXSeq)[xi & (Cf::XQ - 1)] = xi + 1;
                             }
+                            const unsigned xi = atomicAdd(&sXCtl[0], 1u);
+                            while (xi - vctl[1] >= (unsigned)Cf::XQ) __nanosleep(32);  // ring full (rare)
+                            XItem it;
+                            it.mx = Cf::F16 ? (int)__int_as_float(mx) : mx;
+                            it.d = d; it.sd = sd;
+                            it.meta = (eg * HALF + q) | (ks << 5) | (m << 8);
+                            sXQ[xi & (Cf::XQ - 1)] = it;
+                            __threadfence_block();
+                            reinterpret_cast<volatile unsigned *>(sXSeq)[xi & (Cf::XQ - 1)] = xi + 1;
                         }
                     }
+                }
 #ifdef FIC_TC_TRACE
-                    if (pm) { acc_push += clock64() - tp0; ++n_push; }
+                if (pm) { acc_push += clock64() - tp0; ++n_push; }
 #endif
                 }
                 if (warp == 2 && lane == 0) TC_TR(6, tl);
