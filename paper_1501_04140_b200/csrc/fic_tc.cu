@@ -1181,16 +1181,16 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
             return g0;
         };
         unsigned tl = 0;  // tiles consumed by this CTA (TMEM buffer ring position)
-        uint32_t tfull_sa = su32(tfull), tempty_sa = su32(tempty);
+        uint32_t tfull_sa = su32(tfull);
 #ifndef FIC_OPAQUE_SA
 #define FIC_OPAQUE_SA 1
 #endif
-        if (FIC_OPAQUE_SA && B == 4) {
-            // opaque to the compiler: at the register ceiling it otherwise re-forms the barriers'
-            // shared addresses in every tile (S2UR SR_CgaCtaId, ~6% of the B = 4 stall samples;
-            // B = 4 0.512 -> 0.504 ms; at B = 8 the two registers cost spills, 0.159 -> 0.171)
-            asm volatile("" : "+r"(tfull_sa), "+r"(tempty_sa));
-        }
+        // held opaque to the compiler (FIC_OPAQUE_SA bit 0: B = 4, bit 1: B >= 8): at the register
+        // ceiling it otherwise re-forms the barrier's shared address in every tile (S2UR
+        // SR_CgaCtaId: ~6% of the B = 4 stall samples, 0.512 -> 0.504 ms; at B = 8 the register
+        // costs spills: 0.159 -> 0.165 ms); tempty follows tfull
+        if (FIC_OPAQUE_SA & (B == 4 ? 1 : 2)) asm volatile("" : "+r"(tfull_sa));
+        const uint32_t tempty_sa = tfull_sa + 8u * NBUF;
 #ifdef FIC_TC_TRACE
         long long acc_wait = 0, acc_busy = 0;  // per epilogue warp: tfull waits, tile work (cycles)
         long long acc_push = 0, n_push = 0;    // cycles in (and count of) push blocks
