@@ -212,7 +212,8 @@ fic_status pool_enqueue(fic_ctx *ctx, Pool &P, const uint8_t *img, int32_t N, in
         CK(fic::launch_pool_moments(img, N, B, L, P.A, P.kept, &P.d_misc[0], slots, P.SD, P.SDf, P.C,
                                     &P.d_misc[1], st));
     // entropy, select x3, gather, moments (+ the decimated image of the QR pools)
-    ctx->launches += 6 + (P.mode == 3 ? 1 : 0) - (fused ? 1 : 0) + (own_d2 ? 1 : 0);
+    // (B = 2: + the coarse C index of the sorted pool)
+    ctx->launches += 6 + (P.mode == 3 ? 2 : 0) - (fused ? 1 : 0) + (own_d2 ? 1 : 0);
     return FIC_OK;
 }
 
@@ -348,7 +349,7 @@ fic_status level_enqueue(fic_ctx *ctx, const Pool &P, const uint8_t *img, const 
         CK(fic::launch_b2_search(sp, P.b2, ptr<float>(ctx->b_u), P.kept, P.L, P.A, ctx->b_gthr.p,
                                  ptr<unsigned long long>(ctx->b_counts) + 40 + level_slot, st));
         // t2 table, pass 1 scan, pass 2 exact -- or the single window kernel
-        const bool win = sp.b2_window && !sp.has_zero && sp.nsp <= 2;
+        const bool win = (sp.b2_window && !sp.has_zero && sp.nsp <= 2) || fic::b2_wink_applies(sp);
         ctx->launches += sp.nsp > 0 && n_r_max > 0 ? (win ? 1 : 3) : 0;
     }
     if (ctx->timing) CK(cudaEventRecord(ctx->ev[level_slot][2], st));

@@ -98,8 +98,27 @@ __global__ void b2_gather_kernel(const float4 *__restrict__ Fu, const int32_t *_
     if (i < n_slots) F[i] = Fu[ds[i]];
 }
 
+// Coarse index of the C-sorted pool: ctab[t] = first sorted position whose C (as fp32) is
+// >= (t dl)^2, dl = sqrt(Cmax) / kB2CtabN -- monotone in t; b2wink_kernel starts its frontiers
+// there instead of binary-searching every window centre
+__global__ void b2_ctab_kernel(const int32_t *__restrict__ Cs, const unsigned long long *__restrict__ d_nk,
+                               const unsigned long long *__restrict__ d_cmax, int32_t *__restrict__ ctab) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= kB2CtabN) return;
+    const int n = (int)*d_nk;
+    const float dl = sqrtf((float)*d_cmax) / (float)kB2CtabN;
+    const float v = ((float)t * dl) * ((float)t * dl);
+    int lo = 0, hi = n;
+    while (lo < hi) {
+        const int m = (lo + hi) >> 1;
+        if ((float)__ldg(Cs + m) >= v) hi = m;
+        else lo = m + 1;
+    }
+    ctab[t] = lo;
+}
+
 struct B2PoolLayout {
-    size_t F, Fu, Cs, key, ds, val, tmp, tmp_bytes, total;
+    size_t F, Fu, Cs, key, ds, val, ctab, tmp, tmp_bytes, total;
 };
 static B2PoolLayout b2_layout(int64_t slots) {
     B2PoolLayout L;
@@ -111,6 +130,7 @@ static B2PoolLayout b2_layout(int64_t slots) {
     L.key = o; o += al(sizeof(uint32_t) * slots);
     L.ds = o; o += al(sizeof(int32_t) * slots);
     L.val = o; o += al(sizeof(int32_t) * slots);
+    L.ctab = o; o += al(sizeof(int32_t) * kB2CtabN);
     L.tmp_bytes = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, L.tmp_bytes, (const uint32_t *)nullptr, (uint32_t *)nullptr,
                                     (const int32_t *)nullptr, (int32_t *)nullptr, (int)slots, 0, 24);
@@ -129,6 +149,7 @@ cudaError_t launch_b2_pool(const uint8_t *img, int32_t N, int32_t L, int32_t A, 
     out->F = reinterpret_cast<float4 *>(base + Ly.F);
     out->Cs = reinterpret_cast<int32_t *>(base + Ly.Cs);
     out->ds = reinterpret_cast<int32_t *>(base + Ly.ds);
+    out->ctab = reinterpret_cast<int32_t *>(base + Ly.ctab);
     if (n_slots == 0) return cudaSuccess;
     float4 *Fu = reinterpret_cast<float4 *>(base + Ly.Fu);
     uint32_t *key = reinterpret_cast<uint32_t *>(base + Ly.key);
@@ -142,6 +163,7 @@ cudaError_t launch_b2_pool(const uint8_t *img, int32_t N, int32_t L, int32_t A, 
                                         (int)n_slots, 0, 24, st);
     if (e != cudaSuccess) return e;
     b2_gather_kernel<<<g, 256, 0, st>>>(Fu, out->ds, n_slots, out->F);
+    b2_ctab_kernel<<<kB2CtabN / 256, 256, 0, st>>>(out->Cs, d_nk, d_cmax, out->ctab);
     return cudaGetLastError();
 }
 
@@ -173,6 +195,7 @@ struct B2Params {
     const float *T;        // [n_slots][tw] t2_j = RN((s_j s_j)(C/16)), +inf on pads (sorted order)
     const int32_t *Cs;     // [n_slots] C (sorted)
     const int32_t *ds;     // [n_slots] kept-domain rank of each sorted position
+    const int32_t *ctab;   // [kB2CtabN] coarse index of Cs (b2_ctab_kernel)
     int32_t tw;
     SGrid grid;  // uniform grid of the positive s: NP = 0 kernels, T = (RN(C/16), RN(2 / (C h)))
     const int32_t *kept;
@@ -763,6 +786,239 @@ __global__ void __launch_bounds__(256, FIC_B2_MINB) b2win_kernel(const __grid_co
     }
 }
 
+// ---------------------------------------------------------------------------------------------
+// Windowed search for a uniform grid of s (the 16-value grid, sampled10, the closed-form levels:
+// up to 31 positive values; s = 0 may be listed), one warp per range.
+//
+// b2win_kernel's bound per s: a domain can only win or tie if lb_s(C) = (sqrt(A) - s sqrt(C)/4)^2
+// <= best for some s, i.e. sqrt(C) in W_s = [(4/s)(sqrt(A) - sqrt(best)), (4/s)(sqrt(A) +
+// sqrt(best))], a window around the centre C*_s = 16 A / s^2.  Both ends of W_s decrease as s
+// grows, so the centres (s descending = C* ascending) cut the C-sorted pool into K + 1 gaps and
+// inside gap i (between centres i - 1 and i) the union of the windows is W_{i-1}'s part above
+// centre i - 1 plus W_i's part below centre i.  Lane i owns gap i: an up frontier (from centre
+// i - 1, stops past W_{i-1}'s upper end) and a down frontier (from centre i, stops past W_i's lower
+// end) consume it from both ends and stop when they meet.  A frontier tests only its far end,
+// so the start positions need only be monotone in i, not exact: they come from the coarse index
+// of the sorted C (one load per lane instead of K binary searches).  Rounds take up to 512 / kWkStep
+// frontiers (rotating), 128 domains each; filter, stash and phase 2 as in b2win_kernel, with the
+// uniform-grid bracket of tcsearch_kernel<B, 3> as the fp32 score (the bracket's RN(2 / (C h))
+// only picks the two grid points around s*: an approximate quotient, off by far less than half a
+// grid step, picks the same nearest point) and the s = 0 seed (A; 0, 0, j_zero) when listed.
+#ifndef FIC_B2WK_STEP
+#define FIC_B2WK_STEP 128
+#endif
+constexpr int kWkStep = FIC_B2WK_STEP;         // domains per frontier task (a multiple of 32)
+constexpr int kWkTasks = 512 / kWkStep;         // tasks per round: 16 features per lane
+__global__ void __launch_bounds__(256, FIC_B2_MINB) b2wink_kernel(const __grid_constant__ B2Params P) {
+    __shared__ int sStash[8][kStash];
+    __shared__ int sNst[8];
+    pdl_wait();
+    pdl_trigger();
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    if (lane == 0) sNst[wib] = 0;
+    __syncwarp();
+    const int r = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    if (blockIdx.x == 0 && threadIdx.x == 0) *P.d_ns = 1ull;
+    const int n_r = (int)*P.d_nr;
+    if (r >= n_r) return;
+    const int n_k = (int)P.d_misc[0];
+    const double cmax = (double)P.d_misc[1];
+    const int2 rr = P.ranges[r];
+    const uint8_t *p0 = P.img + (size_t)rr.y * P.N + rr.x;
+    const B2Range R = b2_range(p0[0], p0[1], p0[P.N + 1], p0[P.N]);
+    const double A = (double)R.A;
+    const double margin = b2_margin(A, P.smax, cmax, true);
+    const int K = P.nsp;  // positive s, ascending (a uniform grid); centre i <-> spos[K - 1 - i]
+    const float g2h = (float)(2.0 / (double)P.grid.h);
+    auto gof = [&](const float4 fv, float &bq) {
+        bq = fmaf(R.sx, fv.y, fabsf(fmaf(R.x2, fv.x, R.dx * fv.z)));
+        const float ug = fv.w > 0.f ? __fdividef(g2h, fv.w) : 0.f;
+        return b2_grid_g(P.grid, bq, fv.w * 0.0625f, ug);  // (C / 16 exact: C < 2^23)
+    };
+    const float sqAf = sqrtf((float)R.A);
+    // gap `lane` (0 .. K): [lo0, hi0), consumed from both ends
+    int c = n_k;
+    if (lane < K) {
+        const float dl = sqrtf((float)cmax) / (float)kB2CtabN;
+        const float x = 4.f * sqAf / (float)P.spos[K - 1 - lane];  // sqrt(C*) of centre `lane`
+        const int t = dl > 0.f ? (int)fminf(x / dl, (float)(kB2CtabN - 1)) : 0;
+        c = min(__ldg(P.ctab + t), n_k);
+    }
+    const int cprev = __shfl_up_sync(0xffffffffu, c, 1);
+    const int lo0 = (lane == 0 || lane > K) ? 0 : cprev;
+    const int hi0 = lane < K ? c : (lane == K ? n_k : 0);
+    int lo = lo0, hi = hi0;
+    // window factors 4 / s: up frontier <-> centre lane - 1, down frontier <-> centre lane
+    const float ku = (lane >= 1 && lane <= K) ? (float)(4.0 / P.spos[K - lane]) : 0.f;
+    const float kd = lane < K ? (float)(4.0 / P.spos[K - 1 - lane]) : 0.f;
+    bool upA = lane >= 1 && lane <= K && lo < hi;
+    bool dnA = lane < K && lo < hi;
+    const float A_ru = __double2float_ru(A), marg_ru = __double2float_ru(margin);
+    const float marg2_ru = __double2float_ru(2.0 * margin);
+    const float zcap = P.has_zero ? marg_ru : FLT_MAX;  // s = 0 listed: best <= A
+    float gmin = INFINITY;
+    unsigned scanned = 0, rot = 0;
+    for (;;) {
+        const unsigned mu = __ballot_sync(0xffffffffu, upA), md = __ballot_sync(0xffffffffu, dnA);
+        if (!(mu | md)) break;
+        // up to 4 tasks: bit g = up frontier of gap g, bit 32 + g = its down frontier
+        const unsigned long long all = (unsigned long long)mu | ((unsigned long long)md << 32);
+        const unsigned long long rotd = rot ? ((all >> rot) | (all << (64 - rot))) : all;
+        int tb[kWkTasks], tn[kWkTasks];
+        unsigned long long left = rotd;
+#pragma unroll
+        for (int t = 0; t < kWkTasks; ++t) {
+            tb[t] = 0; tn[t] = 0;
+            if (!left) continue;
+            const int bit = __ffsll((long long)left) - 1;
+            left &= left - 1;
+            const int task = (bit + (int)rot) & 63, g = task & 31;
+            int base = 0, n = 0;
+            if (lane == g) {
+                n = min(kWkStep, hi - lo);
+                if (task < 32) { base = lo; lo += n; }
+                else { base = hi - n; hi -= n; }
+            }
+            tb[t] = __shfl_sync(0xffffffffu, base, g);
+            tn[t] = __shfl_sync(0xffffffffu, n, g);
+        }
+        {
+            // next rotation offset: after the last task of this round
+            unsigned long long l2 = rotd;
+            int last = -1;
+#pragma unroll
+            for (int t = 0; t < kWkTasks; ++t) {
+                if (!l2) break;
+                last = __ffsll((long long)l2) - 1;
+                l2 &= l2 - 1;
+            }
+            if (last >= 0) rot = (unsigned)((last + (int)rot + 1) & 63);
+        }
+        // the frontiers' next C values (in flight with the features)
+        int cnu = 0, cnd = 0;
+        if (upA && lo < hi) cnu = __ldg(P.Cs + lo);
+        if (dnA && lo < hi) cnd = __ldg(P.Cs + hi - 1);
+        constexpr int NPL = kWkTasks * (kWkStep / 32);  // features per lane per round
+        float4 fv[NPL];
+        bool ok8[NPL];
+#pragma unroll
+        for (int k = 0; k < kWkStep / 32; ++k) {
+#pragma unroll
+            for (int t = 0; t < kWkTasks; ++t) {
+                const int o = lane + 32 * k;
+                ok8[k * kWkTasks + t] = o < tn[t];
+                const int pos = ok8[k * kWkTasks + t] ? tb[t] + o : 0;
+                fv[k * kWkTasks + t] = __ldg(P.F + pos);
+            }
+        }
+#pragma unroll
+        for (int t = 0; t < kWkTasks; ++t) scanned += (unsigned)tn[t];
+        float g = INFINITY, gv[NPL];
+#pragma unroll
+        for (int i = 0; i < NPL; ++i) {
+            float bq;
+            const float gi = gof(fv[i], bq);
+            gv[i] = ok8[i] ? gi : INFINITY;
+            g = fminf(g, gv[i]);
+        }
+        gmin = fminf(gmin, b2_fdec(__reduce_min_sync(0xffffffffu, b2_fkey(g))));
+        {
+            // stash every domain with g <= the current phase-2 threshold bound (never below the
+            // final threshold: gmin only decreases)
+            const float ts = fminf(fminf(__fadd_ru(gmin, marg2_ru), FLT_MAX), zcap);
+            if (__any_sync(0xffffffffu, g <= ts)) {
+#pragma unroll
+                for (int i = 0; i < NPL; ++i) {
+                    if (gv[i] <= ts) {
+                        const int slot = atomicAdd(&sNst[wib], 1);
+                        if (slot < kStash) sStash[wib][slot] = tb[i % kWkTasks] + lane + 32 * (i / kWkTasks);
+                    }
+                }
+            }
+        }
+        float ub = gmin < INFINITY ? __fadd_ru(__fadd_ru(A_ru, gmin), marg_ru) : INFINITY;
+        if (P.has_zero) ub = fminf(ub, A_ru);
+        const float u = sqrtf(fmaxf(ub, 0.f)) * 1.0001f + 1e-3f * (1.f + sqAf);
+        const float cl = kd * (sqAf - u);
+        const float clo = cl > 0.f ? cl * cl * 0.9999f : -1.f;
+        const float ch = ku * (sqAf + u);
+        const float chi = ch * ch * 1.0001f;
+        upA = upA && lo < hi && (float)cnu <= chi;
+        dnA = dnA && lo < hi && (float)cnd >= clo;
+    }
+    // phase 2 (as b2win_kernel / b2exact_kernel): stashed candidates, or the visited runs
+    float thr = gmin < INFINITY ? fminf(__double2float_ru(__dadd_rn((double)gmin, 2.0 * margin)), FLT_MAX) : -FLT_MAX;
+    double be;
+    int32_t bd, bkj;
+    if (P.has_zero) {  // s = 0: e = A for every (domain, k); first is (0, 0, j_zero)
+        be = A; bd = 0; bkj = P.j_zero;
+        thr = gmin < INFINITY ? fminf(thr, zcap) : zcap;
+    } else {
+        be = INFINITY; bd = INT_MAX; bkj = INT_MAX;
+    }
+    unsigned n_exact = 0;
+    auto exact = [&](int pos, float bq, float cf) {
+        ++n_exact;
+        const int32_t d = __ldg(P.ds + pos);
+        const double Bq = 0.5 * (double)bq, c16 = __dmul_rn(0.0625, (double)cf);
+        double e0 = INFINITY;
+        int j0 = 0;
+        for (int jj = 0; jj < P.nsp; ++jj) {
+            const double sv = P.spos[jj];
+            const double e = __dadd_rn(__dsub_rn(A, __dmul_rn(__dmul_rn(0.5, sv), Bq)), __dmul_rn(__dmul_rn(sv, sv), c16));
+            if (e < e0) { e0 = e; j0 = jj; }  // lowest j among equal e (same k* for every s > 0)
+        }
+        int32_t kj = P.jpos[j0] | kPendIso;
+        if (e0 == be && d == bd)  // only the zero-s seed (d = 0, k = 0) ties here
+            kj = (b2_kstar(P, rr, d) << 8) | P.jpos[j0];
+        if (b2_less(e0, d, kj, be, bd, bkj)) {
+            be = e0; bd = d; bkj = kj;
+            thr = fminf(thr, fminf(__double2float_ru(__dadd_rn(__dsub_rn(e0, A), margin)), FLT_MAX));
+        }
+    };
+    __syncwarp();
+    const int nst = sNst[wib];
+    if (nst <= kStash) {
+        for (int i = lane; i < nst; i += 32) {
+            const int pos = sStash[wib][i];
+            const float4 fv = __ldg(P.F + pos);
+            float bq;
+            if (gof(fv, bq) <= thr) exact(pos, bq, fv.w);
+        }
+    } else {
+        // the visited runs of every gap: [lo0, lo) and [hi, hi0)
+        for (int g = 0; g <= K; ++g) {
+            const int l0 = __shfl_sync(0xffffffffu, lo0, g), l1 = __shfl_sync(0xffffffffu, lo, g);
+            const int h1 = __shfl_sync(0xffffffffu, hi, g), h0 = __shfl_sync(0xffffffffu, hi0, g);
+            for (int w = 0; w < 2; ++w) {
+                const int a0 = w == 0 ? l0 : h1, a1 = w == 0 ? l1 : h0;
+                for (int pos = a0 + lane; pos < a1; pos += 32) {
+                    const float4 fv = __ldg(P.F + pos);
+                    float bq;
+                    if (gof(fv, bq) <= thr) exact(pos, bq, fv.w);
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double oe = __shfl_xor_sync(0xffffffffu, be, o);
+        const int32_t od = __shfl_xor_sync(0xffffffffu, bd, o);
+        const int32_t okj = __shfl_xor_sync(0xffffffffu, bkj, o);
+        if (b2_less(oe, od, okj, be, bd, bkj)) { be = oe; bd = od; bkj = okj; }
+        n_exact += __shfl_xor_sync(0xffffffffu, n_exact, o);
+    }
+    if (lane == 0) {
+        Partial pb;
+        pb.e = be;
+        pb.d = bd;
+        pb.kj = bkj;
+        P.part[(size_t)r * P.ns_cap] = pb;
+        if (n_exact && P.exact_count) atomicAdd(P.exact_count, (unsigned long long)n_exact);
+        if (P.scan_count) atomicAdd(P.scan_count, (unsigned long long)scanned);
+    }
+}
+
 // t2_j per slot, [slot][tw]; +inf on pad slots and pad j
 __global__ void b2_t2_kernel(const float4 *__restrict__ F, const unsigned long long *__restrict__ d_nk,
                              int64_t n_slots, const SList spos, int32_t nsp, int32_t tw, float *__restrict__ T,
@@ -815,6 +1071,20 @@ int b2_nsplit_hint(int64_t n_r, int64_t n_tiles, int num_sms) {
     return (int)ns;
 }
 
+// b2wink_kernel: windows enabled, a uniform grid of 3 .. 16 positive s (ascending; one gap per
+// lane), env FIC_B2_WINK=0 keeps the two-pass scan.  C3 B = 2 (ms, scan -> windows): grid 1.04 ->
+// 0.76 (18% of the pairs scanned), sampled10 1.02 -> 0.57 (13%); the 31 closed-form levels scan
+// 33% of the pairs and stay on the scan (1.22 -> 1.26 with windows).  Frontier steps of 32 / 64
+// domains (more tasks per round) scanned less but ran slower (grid 0.76 -> 1.10 / 0.82)
+
+bool b2_wink_applies(const SearchParams &sp) {
+    static const bool on = [] {
+        const char *e = getenv("FIC_B2_WINK");
+        return !(e && strcmp(e, "0") == 0);
+    }();
+    return on && sp.b2_window && sp.grid.on && sp.nsp >= 3 && sp.nsp <= 16;
+}
+
 int b2_t2_width(int32_t nsp) { return nsp <= 2 ? 2 : (nsp <= 16 ? 16 : 32); }  // (a grid uses 2 of them)
 
 size_t b2_scratch_bytes(int64_t n_r, int32_t ns_cap) { return 64 + sizeof(float) * (size_t)n_r * ns_cap; }
@@ -829,7 +1099,9 @@ cudaError_t launch_b2_search(const SearchParams &sp, const B2Pool &bp, float *T,
     SList sl;
     memcpy(sl.s, sp.spos, sizeof sl.s);
     const bool win = sp.b2_window && !sp.has_zero && sp.nsp <= 2;  // predefined s: C windows
-    if (slots > 0 && !win) {  // (b2win forms t2 from the feature's C itself)
+    // a uniform grid of s (the large sets): per-s C windows over the gaps between the centres
+    const bool wink = !win && b2_wink_applies(sp);
+    if (slots > 0 && !win && !wink) {  // (the window kernels form t2 from the feature's C itself)
         b2_t2_kernel<<<(unsigned)((slots + 255) / 256), 256, 0, st>>>(bp.F, &sp.d_misc[0], slots, sl, sp.nsp, tw, T,
                                                                       grid ? sp.grid.h : 0.f);
         cudaError_t e = cudaGetLastError();
@@ -853,6 +1125,12 @@ cudaError_t launch_b2_search(const SearchParams &sp, const B2Pool &bp, float *T,
     p.gmin = reinterpret_cast<float *>(static_cast<char *>(scratch) + 64);
     if (win) {  // predefined s: Cauchy-Schwarz windows
         if (cudaError_t e = launch_pdl(b2win_kernel, dim3((unsigned)((sp.n_r + 7) / 8)), dim3(256), 0, st, p)) return e;
+        return cudaGetLastError();
+    }
+    if (wink) {
+        p.ctab = bp.ctab;
+        p.grid.on = 1;
+        if (cudaError_t e = launch_pdl(b2wink_kernel, dim3((unsigned)((sp.n_r + 7) / 8)), dim3(256), 0, st, p)) return e;
         return cudaGetLastError();
     }
     cudaError_t e = grid ? launch_b2_scan<0>(p, st)

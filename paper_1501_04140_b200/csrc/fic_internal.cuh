@@ -38,7 +38,9 @@ struct B2Pool {          // B = 2 pool, sorted by C (stable)
     float4 *F = nullptr;    // [slots] features (Y2, yr + yi, yr - yi, C) in sorted order
     int32_t *Cs = nullptr;  // [slots] C in sorted order (pads 0xffffff)
     int32_t *ds = nullptr;  // [slots] kept-domain rank of each sorted position
+    int32_t *ctab = nullptr;  // [kB2CtabN] first sorted position with C >= (t sqrt(Cmax) / kB2CtabN)^2
 };
+constexpr int kB2CtabN = 4096;  // coarse index of the sorted C (b2_ctab_kernel)
 
 // One level's entropy-filtered domain pool (fic_pool).
 struct Pool {
@@ -306,6 +308,7 @@ cudaError_t launch_b2_pool(const uint8_t *img, int32_t N, int32_t L, int32_t A, 
                            int32_t *SD, float *SDf, int64_t *C, unsigned long long *d_cmax, cudaStream_t st);
 int b2_nsplit_hint(int64_t n_r, int64_t n_tiles, int num_sms);
 int b2_t2_width(int32_t nsp);  // floats per slot of the B = 2 t2 table
+bool b2_wink_applies(const SearchParams &sp);  // B = 2 uniform-grid windows (b2wink_kernel)
 size_t b2_scratch_bytes(int64_t n_r, int32_t ns_cap);  // pass-1 minima + split count
 // scan_count: (range, domain) pairs the search evaluated (the windowed path proves the rest
 // non-competitive); may be null
