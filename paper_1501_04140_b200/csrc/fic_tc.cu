@@ -22,7 +22,7 @@
 // Persistent CTAs, one per SM (SegPlan: lockstep rounds of range groups for pools larger than
 // ~L2/2, then a flattened (group, tile) tail in equal runs).  Roles: warp 0 = TMEM allocator +
 // bulk-copy producer (lane 0 the A stages, lane 1 the per-segment range operand), warp 1 = MMA
-// issuer (one elected thread), then EWG epilogue warpgroups (3 at B = 4, else 4), each a share
+// issuer (one elected thread), then EWG epilogue warpgroups (4; 2 at B = 32), each a share
 // of the ranges; warp w reads TMEM lanes 32 (w % 4) ...  Pipelines: A stages full/empty
 // (producer <-> MMA), two TMEM accumulator buffers full/empty (MMA <-> epilogue, released right
 // after the tile's loads), range operand loaded/free (producer <-> MMA).
@@ -57,10 +57,12 @@ struct TCfg {
     static constexpr bool F16 = FIC_TC_F16 && (B == 4 || B == 8);
     static constexpr int KP = QR ? 2 * n : F16 ? 2 * n : ((4 * n + 31) / 32) * 32;  // A K bytes per domain
     static constexpr int KB = QR ? n : KP;                 // B operand K bytes per (range, k) row
-    // ranges per CTA: 8 per epilogue warp per tile; B = 4 uses 3 epilogue warpgroups (14 warps,
-    // at most 4 per SM sub-partition, so 128 registers per thread instead of 96 with 18 warps)
+    // ranges per CTA: 8 per epilogue warp per tile, 4 epilogue warpgroups.  B = 4 loads each
+    // group's accumulators just before scoring it (FIC_SPLIT_LD), which keeps it under the 96
+    // registers of 19 warps: 32 ranges x 4 warpgroups 0.472 ms against 24 x 3 at 128 registers
+    // (all loads first) 0.504 ms
 #ifndef FIC_B4_NR
-#define FIC_B4_NR 24
+#define FIC_B4_NR 32
 #endif
 #ifndef FIC_PROD_WARP
 #define FIC_PROD_WARP 0
@@ -73,7 +75,7 @@ struct TCfg {
 #define FIC_MMA_NS 0
 #endif
 #ifndef FIC_B4_EWG
-#define FIC_B4_EWG 3
+#define FIC_B4_EWG 4
 #endif
 #ifndef FIC_B8_NR
 #define FIC_B8_NR 32
@@ -1183,12 +1185,12 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
         unsigned tl = 0;  // tiles consumed by this CTA (TMEM buffer ring position)
         uint32_t tfull_sa = su32(tfull);
 #ifndef FIC_OPAQUE_SA
-#define FIC_OPAQUE_SA 1
+#define FIC_OPAQUE_SA 3
 #endif
         // held opaque to the compiler (FIC_OPAQUE_SA bit 0: B = 4, bit 1: B >= 8): at the register
         // ceiling it otherwise re-forms the barrier's shared address in every tile (S2UR
-        // SR_CgaCtaId: ~6% of the B = 4 stall samples, 0.512 -> 0.504 ms; at B = 8 the register
-        // costs spills: 0.159 -> 0.165 ms); tempty follows tfull
+        // SR_CgaCtaId: ~6% of the B = 4 stall samples, 0.512 -> 0.504 ms; B = 8, with the split
+        // loads, 0.154 -> 0.152 ms); tempty follows tfull
         if (FIC_OPAQUE_SA & (B == 4 ? 1 : 2)) asm volatile("" : "+r"(tfull_sa));
         const uint32_t tempty_sa = tfull_sa + 8u * NBUF;
 #ifdef FIC_TC_TRACE
@@ -1340,15 +1342,26 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
                 // registers, then the buffer goes straight back to the MMA warp: the next MMA into
                 // it overlaps this tile's scoring
                 static_assert(G <= 4 && (!Cf::QR || G == 1), "one tile's accumulators fit vv");
-                tc_ld32<0>(tbase, vv);
-                if constexpr (Cf::QR) tc_ld32<32>(tbase + NN, vv);
-                if constexpr (!Cf::QR && G >= 2) if (!UNEVEN || eg * HALF + 4 < NR) tc_ld32<32>(tbase + 32, vv);
-                if constexpr (!Cf::QR && G >= 3) if (!UNEVEN || eg * HALF + 8 < NR) tc_ld32<64>(tbase + 64, vv);
-                if constexpr (!Cf::QR && G >= 4) if (!UNEVEN || eg * HALF + 12 < NR) tc_ld32<96>(tbase + 96, vv);
-                tc_wait_ld();
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) tmbar_arrive_sa(tempty_sa + 8 * buf);
+                // FIC_SPLIT_LD (bit 0: B = 4, bit 1: B = 8): each group's 32 columns loaded just
+                // before it is scored, the buffer released after the last load (one group's
+                // accumulators live at a time, the release later by a group's scoring): B = 8
+                // 0.1555 -> 0.154 ms and no spills; at B = 4 it is what lets 4 warpgroups fit
+                // (0.504 -> 0.472 ms; with 3 warpgroups alone it cost 0.504 -> 0.513)
+#ifndef FIC_SPLIT_LD
+#define FIC_SPLIT_LD 3
+#endif
+                constexpr bool kSplit = (FIC_SPLIT_LD & (B == 4 ? 1 : B == 8 ? 2 : 0)) != 0 && !Cf::QR && G >= 2;
+                if constexpr (!kSplit) {
+                    tc_ld32<0>(tbase, vv);
+                    if constexpr (Cf::QR) tc_ld32<32>(tbase + NN, vv);
+                    if constexpr (!Cf::QR && G >= 2) if (!UNEVEN || eg * HALF + 4 < NR) tc_ld32<32>(tbase + 32, vv);
+                    if constexpr (!Cf::QR && G >= 3) if (!UNEVEN || eg * HALF + 8 < NR) tc_ld32<64>(tbase + 64, vv);
+                    if constexpr (!Cf::QR && G >= 4) if (!UNEVEN || eg * HALF + 12 < NR) tc_ld32<96>(tbase + 96, vv);
+                    tc_wait_ld();
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) tmbar_arrive_sa(tempty_sa + 8 * buf);
+                }
                 if (warp == 2 && lane == 0) TC_TR(5, tl);
                 if (lane == 0) TC_TR(8 + warp - 2, tl);
                 if constexpr (Cf::QR) {  // SRD_k = 4 S_q + S_r (exact: < 2^31)
@@ -1366,6 +1379,21 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
                 static_assert(GB % 4 == 0 && (G * 4) % GB == 0, "branch groups of whole tcgen05.ld groups");
 #pragma unroll
                 for (int gb = 0; gb < G * 4 / GB; ++gb) {
+                if constexpr (kSplit) {
+                    static_assert(GB == 4, "split loads: one group per branch group");
+                    if (!UNEVEN || eg * HALF + gb * 4 < NR) {
+                        if (gb == 0) tc_ld32<0>(tbase, vv);
+                        else if (gb == 1) { if constexpr (G >= 2) tc_ld32<32>(tbase + 32, vv); }
+                        else if (gb == 2) { if constexpr (G >= 3) tc_ld32<64>(tbase + 64, vv); }
+                        else { if constexpr (G >= 4) tc_ld32<96>(tbase + 96, vv); }
+                    }
+                    tc_wait_ld();
+                    if (gb == G - 1) {
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) tmbar_arrive_sa(tempty_sa + 8 * buf);
+                    }
+                }
                 unsigned pm = 0;
 #pragma unroll
                 for (int g = gb * GB / 4; g < (gb + 1) * GB / 4; ++g) {
