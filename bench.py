@@ -77,8 +77,41 @@ class ClockSampler:
         self.gpu = gpu_index
         self.proc = None
         self.path = None
+        self.nvml = None
 
     def start(self):
+        # NVML polled from a thread (~1 ms period: a 50-step C3 region lasts ~55 ms, which the
+        # nvidia-smi process below samples only a few times); nvidia-smi if NVML is missing
+        self.nvml = None
+        try:
+            import threading
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
+            self.nvml = {"sm": [], "smax": [], "reasons": set(), "stop": False}
+            bits = {"hw_slowdown": pynvml.nvmlClocksEventReasonHwSlowdown,
+                    "hw_thermal_slowdown": pynvml.nvmlClocksEventReasonHwThermalSlowdown,
+                    "sw_thermal_slowdown": pynvml.nvmlClocksEventReasonSwThermalSlowdown,
+                    "sw_power_cap": pynvml.nvmlClocksEventReasonSwPowerCap}
+            smax = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+
+            def poll(st=self.nvml):
+                while not st["stop"]:
+                    try:
+                        st["sm"].append(float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)))
+                        st["smax"].append(float(smax))
+                        r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                        for nm, b in bits.items():
+                            if r & b:
+                                st["reasons"].add(nm)
+                    except Exception:
+                        pass
+                    time.sleep(0.001)
+            self.thread = threading.Thread(target=poll, daemon=True)
+            self.thread.start()
+            return
+        except Exception:
+            self.nvml = None
         try:
             fd, self.path = tempfile.mkstemp(prefix="clocks_", suffix=".csv")
             os.close(fd)
@@ -90,6 +123,15 @@ class ClockSampler:
             self.proc = None
 
     def stop(self):
+        if self.nvml is not None:
+            self.nvml["stop"] = True
+            self.thread.join(timeout=2)
+            sm = self.nvml["sm"]
+            if not sm:
+                return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"], "source": "nvml"}
+            loaded = [x for x in sm if x > 0.5 * max(sm)] or sm
+            return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": max(self.nvml["smax"]),
+                    "reasons": sorted(self.nvml["reasons"]), "samples": len(sm), "source": "nvml"}
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
         self.proc.terminate()
