@@ -851,7 +851,7 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
     constexpr int STAGES = Cf::STAGES;
     constexpr int HALF = Cf::HALF;  // ranges per epilogue warpgroup (the last may have fewer)
     constexpr bool UNEVEN = HALF * Cf::EWG != NR;
-    static_assert(NR % 4 == 0 && Cf::NBUF >= 2 && (Cf::EWG - 1) * HALF < NR,
+    static_assert(NR % 4 == 0 && Cf::NBUF >= (Cf::QR ? 1 : 2) && (Cf::EWG - 1) * HALF < NR,
                   "range groups of 4, >= 2 accumulator buffers, every warpgroup has ranges");
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t *sA = smem;                                        // [STAGES][128 x KCH]
@@ -1266,7 +1266,7 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
                     uint32_t sv[Cf::QR ? 64 : 32];
                     tc_ld32<0>(tb0 + g * 32, sv);
                     if constexpr (Cf::QR) {
-                        tc_ld32<32>(tb0 + NN, sv);
+                        tc_ld32<32>(tb0 + NN + g * 32, sv);
                         tc_wait_ld();
 #pragma unroll
                         for (int i = 0; i < 32; ++i) sv[i] = 4u * sv[i] + sv[32 + i];
@@ -1341,7 +1341,7 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
                 // the tile's accumulators (<= 2 groups of 4 ranges, or QR's two planes) into
                 // registers, then the buffer goes straight back to the MMA warp: the next MMA into
                 // it overlaps this tile's scoring
-                static_assert(G <= 4 && (!Cf::QR || G == 1), "one tile's accumulators fit vv");
+
                 // FIC_SPLIT_LD (bit 0: B = 4, bit 1: B = 8): each group's 32 columns loaded just
                 // before it is scored, the buffer released after the last load (one group's
                 // accumulators live at a time, the release later by a group's scoring): B = 8
@@ -1350,7 +1350,11 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
 #ifndef FIC_SPLIT_LD
 #define FIC_SPLIT_LD 3
 #endif
-                constexpr bool kSplit = (FIC_SPLIT_LD & (B == 4 ? 1 : B == 8 ? 2 : 0)) != 0 && !Cf::QR && G >= 2;
+                // (bit 2: the QR form, B >= 16, with two groups -- each group's q and r planes)
+                constexpr bool kSplit = (FIC_SPLIT_LD & (B == 4 ? 1 : B == 8 ? 2 : 4)) != 0 && G >= 2;
+                constexpr bool kQRS = kSplit && Cf::QR;  // QR split: a group's combined sums in vv[0, 32)
+                auto vgrp = [&](int q) -> const uint32_t * { return kQRS ? vv + (q & 3) * 8 : vv + q * 8; };
+                static_assert(G <= 4 && (!Cf::QR || G == 1 || kQRS), "one tile's accumulators fit vv");
                 if constexpr (!kSplit) {
                     tc_ld32<0>(tbase, vv);
                     if constexpr (Cf::QR) tc_ld32<32>(tbase + NN, vv);
@@ -1364,7 +1368,7 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
                 }
                 if (warp == 2 && lane == 0) TC_TR(5, tl);
                 if (lane == 0) TC_TR(8 + warp - 2, tl);
-                if constexpr (Cf::QR) {  // SRD_k = 4 S_q + S_r (exact: < 2^31)
+                if constexpr (Cf::QR && !kSplit) {  // SRD_k = 4 S_q + S_r (exact: < 2^31)
 #pragma unroll
                     for (int i = 0; i < 32; ++i) vv[i] = 4u * vv[i] + vv[32 + i];
                 }
@@ -1382,16 +1386,25 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
                 if constexpr (kSplit) {
                     static_assert(GB == 4, "split loads: one group per branch group");
                     if (!UNEVEN || eg * HALF + gb * 4 < NR) {
-                        if (gb == 0) tc_ld32<0>(tbase, vv);
-                        else if (gb == 1) { if constexpr (G >= 2) tc_ld32<32>(tbase + 32, vv); }
-                        else if (gb == 2) { if constexpr (G >= 3) tc_ld32<64>(tbase + 64, vv); }
-                        else { if constexpr (G >= 4) tc_ld32<96>(tbase + 96, vv); }
+                        if constexpr (kQRS) {
+                            tc_ld32<0>(tbase + gb * 32, vv);
+                            tc_ld32<32>(tbase + NN + gb * 32, vv);
+                        } else {
+                            if (gb == 0) tc_ld32<0>(tbase, vv);
+                            else if (gb == 1) { if constexpr (G >= 2) tc_ld32<32>(tbase + 32, vv); }
+                            else if (gb == 2) { if constexpr (G >= 3) tc_ld32<64>(tbase + 64, vv); }
+                            else { if constexpr (G >= 4) tc_ld32<96>(tbase + 96, vv); }
+                        }
                     }
                     tc_wait_ld();
                     if (gb == G - 1) {
                         tc_fence_before();
                         __syncwarp();
                         if (lane == 0) tmbar_arrive_sa(tempty_sa + 8 * buf);
+                    }
+                    if constexpr (kQRS) {  // SRD_k = 4 S_q + S_r (exact: < 2^31)
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) vv[i] = 4u * vv[i] + vv[32 + i];
                     }
                 }
                 unsigned pm = 0;
@@ -1401,7 +1414,7 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
 #pragma unroll
                     for (int q4 = 0; q4 < 4; ++q4) {
                         const int q = g * 4 + q4;
-                        const uint32_t *v = vv + q * 8;
+                        const uint32_t *v = vgrp(q);
                         const int mx = max(__vimax3_s32((int)v[0], (int)v[1], (int)v[2]),
                                            __vimax3_s32((int)v[3], (int)v[4], __vimax3_s32((int)v[5], (int)v[6], (int)v[7])));
                         // (B = 8, at its 96-register ceiling: the range sums from shared memory)
@@ -1417,7 +1430,7 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
 #pragma unroll
                     for (int q = gb * GB; q < (gb + 1) * GB; ++q) {
                         if (pm >> q & 1) {
-                            const uint32_t *v = vv + q * 8;
+                            const uint32_t *v = vgrp(q);
                             const int mx = max(__vimax3_s32((int)v[0], (int)v[1], (int)v[2]),
                                                __vimax3_s32((int)v[3], (int)v[4], __vimax3_s32((int)v[5], (int)v[6], (int)v[7])));
                             int ks = 7;
