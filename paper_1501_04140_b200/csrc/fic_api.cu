@@ -50,7 +50,9 @@ struct fic_ctx {
     cudaEvent_t main_ready = nullptr;
     Buf b_d2;                       // the decimated image, shared by the levels' pools (fic_encode)
     cudaEvent_t d2_ready = nullptr;
+    cudaEvent_t top_ready = nullptr;  // the top-level range list, selected on the side stream
     int b2_window = 1;    // env FIC_B2_WINDOW=0: B = 2 full scan instead of the C windows
+    int top_side = 1;     // env FIC_TOP_SIDE=0: top-level range selection on the critical stream
     Buf b_u, b_gthr, b_rop, b_dec, b_nccl;
     ncclComm_t comm = nullptr;  // fic_ctx_create_nccl: one rank per GPU
     int32_t nranks = 1, rank = 0;
@@ -647,6 +649,8 @@ fic_status fic_ctx_create(int32_t device, void *cuda_stream, fic_ctx **out) {
     {
         const char *bw = getenv("FIC_B2_WINDOW");
         ctx->b2_window = bw && strcmp(bw, "0") == 0 ? 0 : 1;
+        const char *tsd = getenv("FIC_TOP_SIDE");
+        ctx->top_side = tsd && strcmp(tsd, "0") == 0 ? 0 : 1;
         const char *ov = getenv("FIC_OVERLAP_POOLS");
         ctx->overlap_pools = ov ? atoi(ov) != 0 : 1;
     }
@@ -671,6 +675,7 @@ fic_status fic_ctx_create(int32_t device, void *cuda_stream, fic_ctx **out) {
         e = cudaEventCreateWithFlags(&ctx->level_done[l], cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->main_ready, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->d2_ready, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->top_ready, cudaEventDisableTiming);
     if (e != cudaSuccess) {
         fic_ctx_destroy(ctx);
         return FIC_ERR_CUDA;
@@ -715,6 +720,7 @@ fic_status fic_ctx_destroy(fic_ctx *ctx) {
     free_buf(ctx->b_code);
     if (ctx->main_ready) cudaEventDestroy(ctx->main_ready);
     if (ctx->d2_ready) cudaEventDestroy(ctx->d2_ready);
+    if (ctx->top_ready) cudaEventDestroy(ctx->top_ready);
     if (ctx->side) {
         cudaStreamSynchronize(ctx->side);
         cudaStreamDestroy(ctx->side);
@@ -921,6 +927,17 @@ static fic_status encode_body(fic_ctx *ctx, const uint8_t *img, int32_t N, int32
     //    level-0 search (pools depend only on the image)
     CK(cudaEventRecord(ctx->main_ready, st));  // the image is ready (caller's stream order)
     CK(cudaStreamWaitEvent(ctx->side, ctx->main_ready, 0));
+    // 2. top-level ranges of this shard (row-major), selected on the side stream while the
+    //    level-0 pool builds on the critical one (the level-0 search waits for top_ready)
+    uint8_t *child = ptr<uint8_t>(ctx->b_child);
+    const bool top_side = ctx->top_side;
+    {
+        cudaStream_t ts = top_side ? ctx->side : st;
+        CK(fic::launch_top_flags(child, G, shard, n_shards, ts));
+        CK(fic::launch_select_grid(child, G, B_max, ptr<int64_t>(ctx->b_blocksum), ptr<int2>(ctx->b_rng[0]),
+                                   d_counts + 32, ts));
+        if (top_side) CK(cudaEventRecord(ctx->top_ready, ts));
+    }
     // the decimated image, once for every level, on the side stream: it overlaps the level-0
     // entropy filter (the level-0 pool waits for d2_ready; the side-stream pools follow it)
     const size_t d2_bytes = fic::tc_pool_d2_bytes(16, N, L);
@@ -943,13 +960,7 @@ static fic_status encode_body(fic_ctx *ctx, const uint8_t *img, int32_t N, int32
         if (l > 0) CK(cudaEventRecord(ctx->pool_ready[l], ps));
         ctx->stats[l].kernel_launches = ctx->launches;
     }
-    ctx->launches = 0;
-    // 2. top-level ranges of this shard (row-major)
-    uint8_t *child = ptr<uint8_t>(ctx->b_child);
-    CK(fic::launch_top_flags(child, G, shard, n_shards, st));
-    CK(fic::launch_select_grid(child, G, B_max, ptr<int64_t>(ctx->b_blocksum), ptr<int2>(ctx->b_rng[0]),
-                               d_counts + 32, st));
-    ctx->launches += 4;  // top flags + select x3
+    ctx->launches = 4;  // top flags + select x3 (step 2)
     int64_t n_r_max = G * G > shard ? (G * G - shard + n_shards - 1) / n_shards : 0;
     std::vector<int64_t> bound(nl, 0);
 
@@ -963,6 +974,7 @@ static fic_status encode_body(fic_ctx *ctx, const uint8_t *img, int32_t N, int32
         const int64_t Gc = N / (B / 2 > 0 ? B / 2 : 1);
         bound[l] = n_r_max;
         if (l > 0) CK(cudaStreamWaitEvent(st, ctx->pool_ready[l], 0));
+        if (l == 0 && top_side) CK(cudaStreamWaitEvent(st, ctx->top_ready, 0));
         fic_record *rec_l = ptr<fic_record>(ctx->b_rec) + rec_off[l];
         uint8_t *acc_l = ptr<uint8_t>(ctx->b_acc) + rec_off[l];
         if (last) {
