@@ -622,8 +622,27 @@ __global__ void __launch_bounds__(256, FIC_B2_MINB) b2win_kernel(const __grid_co
     // s_a >= s_b, centres c_a <= c_b
     const int ia = (P.nsp > 1 && P.spos[1] > P.spos[0]) ? 1 : 0, ib = P.nsp > 1 ? 1 - ia : ia;
     const double sa = P.spos[ia], sb = P.spos[ib];
-    const int ca = n_k > 0 ? b2_lower_bound(P.Cs, n_k, 16.0 * A / (sa * sa), lane) : 0;
-    const int cb = n_k > 0 ? max(ca, b2_lower_bound(P.Cs, n_k, 16.0 * A / (sb * sb), lane)) : 0;
+#ifndef FIC_B2_CTAB
+#define FIC_B2_CTAB 1
+#endif
+    // the window centres' positions: a frontier tests only its far end, so any start positions
+    // monotone in the centre serve (b2wink_kernel): the coarse index of the sorted C, one load
+    // per centre, instead of two warp-wide searches of ~3 dependent rounds each
+    int ca, cb;
+    if (FIC_B2_CTAB) {
+        const float dl = sqrtf((float)cmax) / (float)kB2CtabN;
+        int c = 0;
+        if (lane < 2 && n_k > 0) {
+            const float x = 4.f * sqrtf((float)R.A) / (float)(lane == 0 ? sa : sb);
+            const int t = dl > 0.f ? (int)fminf(x / dl, (float)(kB2CtabN - 1)) : 0;
+            c = min(__ldg(P.ctab + t), n_k);
+        }
+        ca = __shfl_sync(0xffffffffu, c, 0);
+        cb = max(ca, __shfl_sync(0xffffffffu, c, 1));
+    } else {
+        ca = n_k > 0 ? b2_lower_bound(P.Cs, n_k, 16.0 * A / (sa * sa), lane) : 0;
+        cb = n_k > 0 ? max(ca, b2_lower_bound(P.Cs, n_k, 16.0 * A / (sb * sb), lane)) : 0;
+    }
     // window bounds in C (fp32, widened by 1e-4 relative and 1e-3 (1 + sqrt A) absolute in
     // sqrt C -- far above the fp32 rounding of these few operations, so never too narrow)
     const float sqAf = sqrtf((float)R.A);
@@ -1124,6 +1143,7 @@ cudaError_t launch_b2_search(const SearchParams &sp, const B2Pool &bp, float *T,
     p.d_nscan = reinterpret_cast<unsigned long long *>(scratch);
     p.gmin = reinterpret_cast<float *>(static_cast<char *>(scratch) + 64);
     if (win) {  // predefined s: Cauchy-Schwarz windows
+        p.ctab = bp.ctab;
         if (cudaError_t e = launch_pdl(b2win_kernel, dim3((unsigned)((sp.n_r + 7) / 8)), dim3(256), 0, st, p)) return e;
         return cudaGetLastError();
     }
