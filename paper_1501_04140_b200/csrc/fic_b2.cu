@@ -99,14 +99,15 @@ __global__ void b2_gather_kernel(const float4 *__restrict__ Fu, const int32_t *_
 }
 
 // Coarse index of the C-sorted pool: ctab[t] = first sorted position whose C (as fp32) is
-// >= (t dl)^2, dl = sqrt(Cmax) / kB2CtabN -- monotone in t; b2wink_kernel starts its frontiers
+// >= (t dl)^2, dl = sqrt(Cmax) / n_tab -- monotone in t; b2wink_kernel starts its frontiers
 // there instead of binary-searching every window centre
 __global__ void b2_ctab_kernel(const int32_t *__restrict__ Cs, const unsigned long long *__restrict__ d_nk,
-                               const unsigned long long *__restrict__ d_cmax, int32_t *__restrict__ ctab) {
+                               const unsigned long long *__restrict__ d_cmax, int32_t *__restrict__ ctab,
+                               int32_t n_tab) {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= kB2CtabN) return;
+    if (t >= n_tab) return;
     const int n = (int)*d_nk;
-    const float dl = sqrtf((float)*d_cmax) / (float)kB2CtabN;
+    const float dl = sqrtf((float)*d_cmax) / (float)n_tab;
     const float v = ((float)t * dl) * ((float)t * dl);
     int lo = 0, hi = n;
     while (lo < hi) {
@@ -130,7 +131,7 @@ static B2PoolLayout b2_layout(int64_t slots) {
     L.key = o; o += al(sizeof(uint32_t) * slots);
     L.ds = o; o += al(sizeof(int32_t) * slots);
     L.val = o; o += al(sizeof(int32_t) * slots);
-    L.ctab = o; o += al(sizeof(int32_t) * kB2CtabN);
+    L.ctab = o; o += al(sizeof(int32_t) * b2_ctab_entries(slots));
     L.tmp_bytes = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, L.tmp_bytes, (const uint32_t *)nullptr, (uint32_t *)nullptr,
                                     (const int32_t *)nullptr, (int32_t *)nullptr, (int)slots, 0, 24);
@@ -150,6 +151,7 @@ cudaError_t launch_b2_pool(const uint8_t *img, int32_t N, int32_t L, int32_t A, 
     out->Cs = reinterpret_cast<int32_t *>(base + Ly.Cs);
     out->ds = reinterpret_cast<int32_t *>(base + Ly.ds);
     out->ctab = reinterpret_cast<int32_t *>(base + Ly.ctab);
+    out->ctab_n = b2_ctab_entries(n_slots);
     if (n_slots == 0) return cudaSuccess;
     float4 *Fu = reinterpret_cast<float4 *>(base + Ly.Fu);
     uint32_t *key = reinterpret_cast<uint32_t *>(base + Ly.key);
@@ -163,7 +165,7 @@ cudaError_t launch_b2_pool(const uint8_t *img, int32_t N, int32_t L, int32_t A, 
                                         (int)n_slots, 0, 24, st);
     if (e != cudaSuccess) return e;
     b2_gather_kernel<<<g, 256, 0, st>>>(Fu, out->ds, n_slots, out->F);
-    b2_ctab_kernel<<<kB2CtabN / 256, 256, 0, st>>>(out->Cs, d_nk, d_cmax, out->ctab);
+    b2_ctab_kernel<<<(unsigned)(out->ctab_n / 256), 256, 0, st>>>(out->Cs, d_nk, d_cmax, out->ctab, out->ctab_n);
     return cudaGetLastError();
 }
 
@@ -195,7 +197,8 @@ struct B2Params {
     const float *T;        // [n_slots][tw] t2_j = RN((s_j s_j)(C/16)), +inf on pads (sorted order)
     const int32_t *Cs;     // [n_slots] C (sorted)
     const int32_t *ds;     // [n_slots] kept-domain rank of each sorted position
-    const int32_t *ctab;   // [kB2CtabN] coarse index of Cs (b2_ctab_kernel)
+    const int32_t *ctab;   // [ctab_n] coarse index of Cs (b2_ctab_kernel)
+    int32_t ctab_n;
     int32_t tw;
     SGrid grid;  // uniform grid of the positive s: NP = 0 kernels, T = (RN(C/16), RN(2 / (C h)))
     const int32_t *kept;
@@ -630,11 +633,11 @@ __global__ void __launch_bounds__(256, FIC_B2_MINB) b2win_kernel(const __grid_co
     // per centre, instead of two warp-wide searches of ~3 dependent rounds each
     int ca, cb;
     if (FIC_B2_CTAB) {
-        const float dl = sqrtf((float)cmax) / (float)kB2CtabN;
+        const float dl = sqrtf((float)cmax) / (float)P.ctab_n;
         int c = 0;
         if (lane < 2 && n_k > 0) {
             const float x = 4.f * sqrtf((float)R.A) / (float)(lane == 0 ? sa : sb);
-            const int t = dl > 0.f ? (int)fminf(x / dl, (float)(kB2CtabN - 1)) : 0;
+            const int t = dl > 0.f ? (int)fminf(x / dl, (float)(P.ctab_n - 1)) : 0;
             c = min(__ldg(P.ctab + t), n_k);
         }
         ca = __shfl_sync(0xffffffffu, c, 0);
@@ -858,9 +861,9 @@ __global__ void __launch_bounds__(256, FIC_B2_MINB) b2wink_kernel(const __grid_c
     // gap `lane` (0 .. K): [lo0, hi0), consumed from both ends
     int c = n_k;
     if (lane < K) {
-        const float dl = sqrtf((float)cmax) / (float)kB2CtabN;
+        const float dl = sqrtf((float)cmax) / (float)P.ctab_n;
         const float x = 4.f * sqAf / (float)P.spos[K - 1 - lane];  // sqrt(C*) of centre `lane`
-        const int t = dl > 0.f ? (int)fminf(x / dl, (float)(kB2CtabN - 1)) : 0;
+        const int t = dl > 0.f ? (int)fminf(x / dl, (float)(P.ctab_n - 1)) : 0;
         c = min(__ldg(P.ctab + t), n_k);
     }
     const int cprev = __shfl_up_sync(0xffffffffu, c, 1);
@@ -1143,12 +1146,12 @@ cudaError_t launch_b2_search(const SearchParams &sp, const B2Pool &bp, float *T,
     p.d_nscan = reinterpret_cast<unsigned long long *>(scratch);
     p.gmin = reinterpret_cast<float *>(static_cast<char *>(scratch) + 64);
     if (win) {  // predefined s: Cauchy-Schwarz windows
-        p.ctab = bp.ctab;
+        p.ctab = bp.ctab; p.ctab_n = bp.ctab_n;
         if (cudaError_t e = launch_pdl(b2win_kernel, dim3((unsigned)((sp.n_r + 7) / 8)), dim3(256), 0, st, p)) return e;
         return cudaGetLastError();
     }
     if (wink) {
-        p.ctab = bp.ctab;
+        p.ctab = bp.ctab; p.ctab_n = bp.ctab_n;
         p.grid.on = 1;
         if (cudaError_t e = launch_pdl(b2wink_kernel, dim3((unsigned)((sp.n_r + 7) / 8)), dim3(256), 0, st, p)) return e;
         return cudaGetLastError();

@@ -38,9 +38,15 @@ struct B2Pool {          // B = 2 pool, sorted by C (stable)
     float4 *F = nullptr;    // [slots] features (Y2, yr + yi, yr - yi, C) in sorted order
     int32_t *Cs = nullptr;  // [slots] C in sorted order (pads 0xffffff)
     int32_t *ds = nullptr;  // [slots] kept-domain rank of each sorted position
-    int32_t *ctab = nullptr;  // [kB2CtabN] first sorted position with C >= (t sqrt(Cmax) / kB2CtabN)^2
+    int32_t *ctab = nullptr;  // [ctab_n] first sorted position with C >= (t sqrt(Cmax) / ctab_n)^2
+    int32_t ctab_n = 0;       // entries: a power of two >= slots / 16, at least 4096
 };
-constexpr int kB2CtabN = 4096;  // coarse index of the sorted C (b2_ctab_kernel)
+// entries of the coarse index of the sorted C (b2_ctab_kernel): ~16 domains per bin on average
+inline int32_t b2_ctab_entries(int64_t slots) {
+    int64_t e = 4096;
+    while (e < slots / 16 && e < (1 << 22)) e *= 2;
+    return (int32_t)e;
+}
 
 // One level's entropy-filtered domain pool (fic_pool).
 struct Pool {
