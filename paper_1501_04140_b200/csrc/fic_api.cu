@@ -277,7 +277,8 @@ fic_status level_enqueue(fic_ctx *ctx, const Pool &P, const uint8_t *img, const 
                          double rms_tol, int is_min, fic_record *rec, uint8_t *acc, uint8_t *child,
                          int level_slot, int32_t *d_err, fic_record *out_direct = nullptr,
                          const unsigned long long *d_base = nullptr, int64_t capacity = 0,
-                         unsigned long long *d_level_count = nullptr, cudaEvent_t before_finalize = nullptr) {
+                         unsigned long long *d_level_count = nullptr, cudaEvent_t before_finalize = nullptr,
+                         int prep_done = 0) {
     cudaStream_t st = ctx->stream;
     if (n_r_max == 0) return FIC_OK;
     fic::SearchParams sp;
@@ -307,6 +308,7 @@ fic_status level_enqueue(fic_ctx *ctx, const Pool &P, const uint8_t *img, const 
         }
         if (h_s[j] > sp.smax) sp.smax = h_s[j];
     }
+    sp.prep_done = prep_done;
     if (P.mode == 0)
         sp.nsplit = fic::tc_nsplit_hint(P.B, n_r_max, tiles, ctx->num_sms);
     else
@@ -936,6 +938,14 @@ static fic_status encode_body(fic_ctx *ctx, const uint8_t *img, int32_t N, int32
         CK(fic::launch_top_flags(child, G, shard, n_shards, ts));
         CK(fic::launch_select_grid(child, G, B_max, ptr<int64_t>(ctx->b_blocksum), ptr<int2>(ctx->b_rng[0]),
                                    d_counts + 32, ts));
+        // and the level-0 range preparation (operand + moments: image and ranges only), off the
+        // critical stream too -- the level-0 search then follows its pool directly
+        if (top_side && B_max >= 4) {
+            const int64_t nr0 = G * G > shard ? (G * G - shard + n_shards - 1) / n_shards : 0;
+            CK(grow(ctx, ctx->b_rop, fic::tc_range_bytes(B_max, nr0)));
+            CK(fic::launch_tc_prep(B_max, img, N, ptr<int2>(ctx->b_rng[0]), d_counts + 32, nr0,
+                                   ptr<uint8_t>(ctx->b_rop), ts));
+        }
         if (top_side) CK(cudaEventRecord(ctx->top_ready, ts));
     }
     // the decimated image, once for every level, on the side stream: it overlaps the level-0
@@ -984,11 +994,13 @@ static fic_status encode_body(fic_ctx *ctx, const uint8_t *img, int32_t N, int32
             CK(cudaEventRecord(ctx->main_ready, ctx->side));
             CKS(level_enqueue(ctx, P, img, ptr<int2>(ctx->b_rng[cur]), d_counts + 32 + l, n_r_max,
                               h_s + s_off[l], h_n_s[l], h_rms_tol[l], 1, rec_l, acc_l, nullptr, l, d_err, out,
-                              d_counts + 0, capacity, d_counts + 16 + l, ctx->main_ready));
+                              d_counts + 0, capacity, d_counts + 16 + l, ctx->main_ready,
+                              (l == 0 && top_side && B >= 4) ? 1 : 0));
             last_direct = l;  // (the host adds this level's count to the total after the copy)
         } else {
             CKS(level_enqueue(ctx, P, img, ptr<int2>(ctx->b_rng[cur]), d_counts + 32 + l, n_r_max,
-                              h_s + s_off[l], h_n_s[l], h_rms_tol[l], 0, rec_l, acc_l, child, l, d_err));
+                              h_s + s_off[l], h_n_s[l], h_rms_tol[l], 0, rec_l, acc_l, child, l, d_err,
+                              nullptr, nullptr, 0, nullptr, nullptr, (l == 0 && top_side && B >= 4) ? 1 : 0));
             // the accepted records of this level go to `out` on the side stream (in level order,
             // after the pools there), off the critical path of the next level's search
             CK(cudaEventRecord(ctx->level_done[l], st));

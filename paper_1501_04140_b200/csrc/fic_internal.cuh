@@ -133,6 +133,7 @@ struct SearchParams {
     const int32_t *kept;         // kept-domain candidate indices
     int32_t num_sms;             // SMs of the context's device (persistent grids)
     SGrid grid;                  // the positive s form a uniform grid (nsp > 2)
+    int32_t prep_done;           // the range preparation was enqueued ahead (launch_tc_prep)
 };
 
 struct FinalizeParams {
@@ -351,6 +352,10 @@ cudaError_t launch_pool_tc(const uint8_t *img, int32_t N, int32_t B, int32_t L, 
                            uint8_t *Dtc, int32_t *SD, float *SDf, int64_t *C, unsigned long long *d_cmax,
                            const uint16_t *D2, cudaStream_t st);
 size_t tc_range_bytes(int B, int64_t n_r);  // scratch for the prepared range operand + metadata
+// the range operand and moments of a level's ranges alone (they need only the image and the
+// range list), ahead of launch_tc_search with sp.prep_done = 1 and the same scratch
+cudaError_t launch_tc_prep(int32_t B, const uint8_t *img, int32_t N, const int2 *ranges,
+                           const unsigned long long *d_nr, int64_t n_r, uint8_t *scratch, cudaStream_t st);
 cudaError_t launch_tc_search(int32_t B, const SearchParams &sp, const uint8_t *Dtc, int64_t n_slots,
                              uint8_t *scratch, cudaStream_t st);
 

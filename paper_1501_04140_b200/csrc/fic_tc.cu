@@ -656,7 +656,40 @@ struct TCRangeG {
     int32_t valid;
 };
 
-// Thread per range: SR, A = n SRR - SR^2 and the filter margin
+// The fp32 filter's margin of one range (DESIGN.md §6 "Exactness"), from its A, the level's
+// largest s and the pool's largest C
+template <int B>
+__device__ __forceinline__ double tc_margin(double A, double smax, double cmax, int univ) {
+    double m;
+    // fp32 filter error: |Bq| <= sqrt(A C) (Cauchy-Schwarz); the one rounding of Bq (or of Bq / n),
+    // hs and t2 roundings, two FFMA roundings -> 8u (hs sqrt(A Cmax) + t2max)
+    const double u = 5.9604644775390625e-08;
+    const double hs = 0.5 * smax;
+    const double bq = sqrt(A * cmax) * 1.01;  // every form converts an exact (or RN(Bq / n)) value once
+    const double t2m = smax * smax * cmax * 0.0625;
+    // + the int -> float conversion of Bq in the epilogue: exact at B = 2, |error| <= 2 at B = 4,
+    // <= 64 at B = 8 (floor of Bq / 2 and Bq / 64)
+    if (TCfg<B>::F16) {
+        // F16: y = RN(SRD_max - SR (SD / n)) = RN(Bq / n) (one FFMA, SD / n exact), then
+        // g = RN(nhs n y + t2): conversions of s / 2 and t2, the two roundings -> 4u (hs |Bq| + t2)
+        m = 8.0 * u * (hs * bq + t2m) + 1e-12 * (A + hs * bq + t2m) + 1e-30;
+    } else {
+        m = 8.0 * u * (hs * bq + t2m) + 1e-12 * (A + hs * bq + t2m) +
+                   (B == 4 ? hs * 2.0 : (B == 8 ? hs * 64.0 : 0.0)) + 1e-30;
+        // folded magic constant (B <= 8): t2' = RN(t2 - nhs M) adds u |t2 - nhs M| <= u (t2m + hs k M)
+        if (B <= 8) m += 2.0 * u * (t2m + hs * (B == 2 ? 1.0 : (B == 4 ? 2.0 : 64.0)) * 12582912.0);
+    }
+    // s-independent filter (NSP = 0): Bq rounded once, squared, times RN(1/C): <= 4.04u Bq^2/C <= 4.04u A
+    if (univ == 1) m = 4.1 * u * A + 1e-12 * A + 1e-30;
+    // uniform grid (NSP = 3): g(s) = s (s RN(C/16) - Bq/2) at two fp32 grid points s = fma(j, h, a):
+    // Bq RN conversion, s rounding (incl. the 1e-12 grid fit), C/16 rounding, the FFMA and the
+    // FMUL: |error| <= ~6u (hs |Bq| + 2 t2) -> 16u (hs |Bq|max + t2max)
+    if (univ == 2)
+        m = 16.0 * u * (hs * bq + t2m) + 1e-12 * (A + hs * bq + t2m) + 1e-30;
+    return m;
+}
+
+// Thread per range: SR, A = n SRR - SR^2 (the filter margin is the search's: tc_margin)
 template <int B>
 __device__ __forceinline__ void tc_range_meta_body(const uint8_t *__restrict__ img, int32_t N,
                                                    const int2 *__restrict__ ranges,
@@ -669,7 +702,6 @@ __device__ __forceinline__ void tc_range_meta_body(const uint8_t *__restrict__ i
     const int r = gt / TPR, sub = gt % TPR;
     if (r >= n_pad) return;
     const int n_r = (int)*d_nr;
-    const double cmax = (double)d_misc[1];
     constexpr int n = B * B;
     TCRangeG R;
     long long sr = 0, srr = 0;
@@ -692,31 +724,8 @@ __device__ __forceinline__ void tc_range_meta_body(const uint8_t *__restrict__ i
     }
     R.A = (double)((long long)n * srr - sr * sr);
     R.SR = (int32_t)sr;
-    // fp32 filter error: |Bq| <= sqrt(A C) (Cauchy-Schwarz); the one rounding of Bq (or of Bq / n),
-    // hs and t2 roundings, two FFMA roundings -> 8u (hs sqrt(A Cmax) + t2max)
-    const double u = 5.9604644775390625e-08;
-    const double hs = 0.5 * smax;
-    const double bq = sqrt(R.A * cmax) * 1.01;  // every form converts an exact (or RN(Bq / n)) value once
-    const double t2m = smax * smax * cmax * 0.0625;
-    // + the int -> float conversion of Bq in the epilogue: exact at B = 2, |error| <= 2 at B = 4,
-    // <= 64 at B = 8 (floor of Bq / 2 and Bq / 64)
-    if (TCfg<B>::F16) {
-        // F16: y = RN(SRD_max - SR (SD / n)) = RN(Bq / n) (one FFMA, SD / n exact), then
-        // g = RN(nhs n y + t2): conversions of s / 2 and t2, the two roundings -> 4u (hs |Bq| + t2)
-        R.margin = 8.0 * u * (hs * bq + t2m) + 1e-12 * (R.A + hs * bq + t2m) + 1e-30;
-    } else {
-        R.margin = 8.0 * u * (hs * bq + t2m) + 1e-12 * (R.A + hs * bq + t2m) +
-                   (B == 4 ? hs * 2.0 : (B == 8 ? hs * 64.0 : 0.0)) + 1e-30;
-        // folded magic constant (B <= 8): t2' = RN(t2 - nhs M) adds u |t2 - nhs M| <= u (t2m + hs k M)
-        if (B <= 8) R.margin += 2.0 * u * (t2m + hs * (B == 2 ? 1.0 : (B == 4 ? 2.0 : 64.0)) * 12582912.0);
-    }
-    // s-independent filter (NSP = 0): Bq rounded once, squared, times RN(1/C): <= 4.04u Bq^2/C <= 4.04u A
-    if (univ == 1) R.margin = 4.1 * u * R.A + 1e-12 * R.A + 1e-30;
-    // uniform grid (NSP = 3): g(s) = s (s RN(C/16) - Bq/2) at two fp32 grid points s = fma(j, h, a):
-    // Bq RN conversion, s rounding (incl. the 1e-12 grid fit), C/16 rounding, the FFMA and the
-    // FMUL: |error| <= ~6u (hs |Bq| + 2 t2) -> 16u (hs |Bq|max + t2max)
-    if (univ == 2)
-        R.margin = 16.0 * u * (hs * bq + t2m) + 1e-12 * (R.A + hs * bq + t2m) + 1e-30;
+    R.margin = 0.0;  // formed by the search from the pool's Cmax (tc_margin): the preparation
+                     // needs only the image and the ranges, so it can run before the pool exists
     meta[r] = R;
 }
 
@@ -1115,11 +1124,11 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
         // t2f rows per domain: one per s (NSP 1, 2); u = RN(1/C) (NSP 0); RN(C/16), RN(4/(C h)) (grid)
         constexpr int NT = NSP == 3 ? 2 : (NSP ? NSP : 1);
         float nhs[NT];
-#pragma unroll
         // the B = 4 / 8 conversions below yield Bq / 2 and Bq / 64: fold the power of two into -s/2
         // (exact), so g = fma(nhs, bq, t2) keeps its rounding without the multiply
         // F16: g = (-(s/2) n) y + t2 with y = RN(Bq / n)
         constexpr float kBqScale = Cf::F16 ? (float)n : (B == 4 ? 2.0f : (B == 8 ? 64.0f : 1.0f));
+#pragma unroll
         for (int jj = 0; jj < NT; ++jj) nhs[jj] = sHsn[jj] * kBqScale;
         static_assert(Cf::EWG <= 5, "named barriers 1..EWG (seeding) and 6 (segments) must not collide");
         auto epi_sync = [&]() { asm volatile("bar.sync 6, %0;" ::"r"(128 * Cf::EWG) : "memory"); };
@@ -1207,7 +1216,8 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
             epi_sync();
             if (et == 0) TC_TR_SEG(23, k);
             if (et < NR) {
-                const TCRange R = P.rmeta[r0 + et];
+                TCRange R = P.rmeta[r0 + et];
+                R.margin = tc_margin<B>(R.A, P.smax, (double)P.d_misc[1], NSP == 0 ? 1 : (NSP == 3 ? 2 : 0));
                 sR[et] = R;
                 Partial pb;  // s = 0 (if listed): e = A for every (domain, k) -> (A, 0, 0, j_zero)
                 if (P.has_zero) { pb.e = R.A; pb.d = 0; pb.kj = P.j_zero; }
@@ -1561,23 +1571,40 @@ size_t tc_range_bytes(int B, int64_t n_r) {
     }
 }
 
+// the operand and the moments of a level's ranges (scratch: [groups][B_BYTES] operand, then the
+// [groups * NR] moments); launch = false only derives the pointers (prepared ahead)
 template <int B>
-static cudaError_t tc_range_prep(const SearchParams &sp, uint8_t *scratch, TCParams &p, cudaStream_t st) {
+static cudaError_t tc_range_prep(const uint8_t *img, int32_t N, const int2 *ranges, const unsigned long long *d_nr,
+                                 int64_t n_r, uint8_t *scratch, TCParams &p, cudaStream_t st, bool launch) {
     using Cf = TCfg<B>;
-    const int64_t groups = (sp.n_r + Cf::NR - 1) / Cf::NR;
+    const int64_t groups = (n_r + Cf::NR - 1) / Cf::NR;
     uint8_t *Bop = scratch;
     TCRangeG *meta = reinterpret_cast<TCRangeG *>(scratch + (size_t)groups * Cf::B_BYTES);
+    p.Bop = Bop;
+    p.rmeta = meta;
+    if (!launch) return cudaSuccess;
     const int64_t total16 = groups * Cf::N * (Cf::KB / 16);
     const int n_pad = (int)(groups * Cf::NR);
     const int64_t meta_threads = (int64_t)n_pad * (B >= 8 ? 32 : 1);
     const int nb_op = (int)((total16 + 255) / 256), nb_meta = (int)((meta_threads + 255) / 256);
     if (cudaError_t e = launch_pdl(tc_range_prep_kernel<B>, dim3((unsigned)(nb_op + nb_meta)), dim3(256), 0, st,
-                                   sp.img, sp.N, sp.ranges, sp.d_nr, total16, Bop, nb_op, n_pad, sp.smax, sp.d_misc,
-                                   meta, (int32_t)(sp.nsp > 2 ? (sp.grid.on ? 2 : 1) : 0)))
+                                   img, N, ranges, d_nr, total16, Bop, nb_op, n_pad, 0.0,
+                                   (const unsigned long long *)nullptr, meta, (int32_t)0))
         return e;
-    p.Bop = Bop;
-    p.rmeta = meta;
     return cudaGetLastError();
+}
+
+cudaError_t launch_tc_prep(int32_t B, const uint8_t *img, int32_t N, const int2 *ranges,
+                           const unsigned long long *d_nr, int64_t n_r, uint8_t *scratch, cudaStream_t st) {
+    if (n_r == 0) return cudaSuccess;
+    TCParams p;
+    switch (B) {
+    case 4: return tc_range_prep<4>(img, N, ranges, d_nr, n_r, scratch, p, st, true);
+    case 8: return tc_range_prep<8>(img, N, ranges, d_nr, n_r, scratch, p, st, true);
+    case 16: return tc_range_prep<16>(img, N, ranges, d_nr, n_r, scratch, p, st, true);
+    case 32: return tc_range_prep<32>(img, N, ranges, d_nr, n_r, scratch, p, st, true);
+    default: return cudaErrorInvalidValue;
+    }
 }
 
 #ifdef FIC_TC_TRACE
@@ -1595,11 +1622,12 @@ cudaError_t launch_tc_search(int32_t B, const SearchParams &sp, const uint8_t *D
     TCParams p;
     memset(&p, 0, sizeof p);
     cudaError_t e0 = cudaSuccess;
+    const bool launch = !sp.prep_done;
     switch (B) {
-    case 4: e0 = tc_range_prep<4>(sp, scratch, p, st); break;
-    case 8: e0 = tc_range_prep<8>(sp, scratch, p, st); break;
-    case 16: e0 = tc_range_prep<16>(sp, scratch, p, st); break;
-    case 32: e0 = tc_range_prep<32>(sp, scratch, p, st); break;
+    case 4: e0 = tc_range_prep<4>(sp.img, sp.N, sp.ranges, sp.d_nr, sp.n_r, scratch, p, st, launch); break;
+    case 8: e0 = tc_range_prep<8>(sp.img, sp.N, sp.ranges, sp.d_nr, sp.n_r, scratch, p, st, launch); break;
+    case 16: e0 = tc_range_prep<16>(sp.img, sp.N, sp.ranges, sp.d_nr, sp.n_r, scratch, p, st, launch); break;
+    case 32: e0 = tc_range_prep<32>(sp.img, sp.N, sp.ranges, sp.d_nr, sp.n_r, scratch, p, st, launch); break;
     default: return cudaErrorInvalidValue;
     }
     if (e0 != cudaSuccess) return e0;
