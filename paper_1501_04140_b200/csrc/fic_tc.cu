@@ -856,7 +856,7 @@ __global__ void __launch_bounds__(TCfg<B>::THREADS, 1) tcsearch_kernel(const __g
     pdl_wait();
     pdl_trigger();
     using Cf = TCfg<B>;
-    constexpr int n = Cf::n, KP = Cf::KP, NR = Cf::NR, NN = Cf::N, KCH = Cf::KCH, CH = Cf::CH;
+    constexpr int n = Cf::n, NR = Cf::NR, NN = Cf::N, KCH = Cf::KCH, CH = Cf::CH;
     constexpr int STAGES = Cf::STAGES;
     constexpr int HALF = Cf::HALF;  // ranges per epilogue warpgroup (the last may have fewer)
     constexpr bool UNEVEN = HALF * Cf::EWG != NR;
