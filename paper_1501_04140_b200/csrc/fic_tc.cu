@@ -93,14 +93,23 @@ struct TCfg {
     // 64 KB A stages fit shared memory
     static constexpr int NR = (B == 32) ? 8 : (B == 16) ? FIC_B16_NR : (B == 4 ? FIC_B4_NR : FIC_B8_NR);
     static constexpr int N = 8 * NR;                       // MMA N (columns per accumulator)
-    static constexpr int KCH = QR ? 512 : (KP < 256 ? KP : 256);  // K bytes per pipeline stage (F16: a tile)
+    // B = 16: one 64 KB stage per tile (q and r planes), two stages.  Finer stages (KCH = 256, 4 or
+    // 5 stages: FIC_B16_KCH / FIC_B16_STAGES) were measured slower (C3 B16 0.105 -> 0.107 /
+    // 0.108 ms): the feed is bounded by the bulk-copy throughput, not by the bytes in flight
+#ifndef FIC_B16_KCH
+#define FIC_B16_KCH 512
+#endif
+#ifndef FIC_B16_STAGES
+#define FIC_B16_STAGES 2
+#endif
+    static constexpr int KCH = QR ? (B == 16 ? FIC_B16_KCH : 512) : (KP < 256 ? KP : 256);  // K bytes per pipeline stage (F16: a tile)
     static constexpr int CH = KP / KCH;                    // stages per domain tile
     static constexpr int STAGE_BYTES = kTileD * KCH;       // A bytes per stage
-    // B = 16 is fed by bulk copies (latency x bytes in flight): 8 x 16 KB stages
+    // A stages (one tile each in the f16 form): B = 4 8 x 4 KB, B = 8 4 x 16 KB; QR 2 x 64 KB (above)
 #ifndef FIC_B4_STAGES
 #define FIC_B4_STAGES 8
 #endif
-    static constexpr int STAGES = QR ? 2 : F16 ? (B == 4 ? FIC_B4_STAGES : 4) : (B == 8 ? 2 : 4);
+    static constexpr int STAGES = QR ? (B == 16 ? FIC_B16_STAGES : 2) : F16 ? (B == 4 ? FIC_B4_STAGES : 4) : (B == 8 ? 2 : 4);
     static constexpr int B_BYTES = N * KB;                 // resident range operand
     // range-operand buffers: 2 where shared memory allows, so the next segment's operand loads
     // while the current segment's MMAs still read the other one
