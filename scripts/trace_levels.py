@@ -1,7 +1,7 @@
 #!/usr/bin/env python3
 """Per-level timeline of a few encodes (timing 2 events): FIC_TRACE=1 python scripts/trace_levels.py [C3].
 Prints when each level's search starts, the gap after the previous finalize, and the join / counter copy."""
-import sys, time, torch
+import os, sys, time, torch
 sys.path.insert(0, ".")
 from fic_inputs.configs import config, image_for
 from paper_1501_04140_b200 import fic
@@ -12,6 +12,8 @@ out = torch.empty(((cfg["N"] // cfg["B_min"]) ** 2, fic.RECORD_BYTES), dtype=tor
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 for i in range(6):
     flush.fill_(1)
+    if os.environ.get("TRACE_SLEEP"):  # host runs ahead: the whole encode queued before the GPU reaches it
+        torch.cuda._sleep(6_000_000)
     e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
     e0.record(); ctx.encode_cfg(cfg, img, out=out); e1.record(); e1.synchronize()
     print("total %.3f" % e0.elapsed_time(e1), file=sys.stderr)
