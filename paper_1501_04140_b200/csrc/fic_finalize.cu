@@ -86,13 +86,21 @@ __device__ __noinline__ void srd_all_dev(const FinalizeParams &P, int2 rr, int32
 // Thread per range.  Templated on B so the row loads and the partial merge unroll: the loads are
 // independent and all in flight at once (with a runtime B the loop issued them one round trip
 // at a time: 14 us at B = 16).
+// The range list, its count and the pool's kept count come from kernels that completed before
+// the search passed its own griddepcontrol.wait (the range compaction and preparation, the pool
+// behind an event), so the range moments are formed before this kernel waits for the search:
+// their loads overlap the search's tail (FIC_FIN_EARLY=0: wait first).
+#ifndef FIC_FIN_EARLY
+#define FIC_FIN_EARLY 1
+#endif
 template <int BT>
 __global__ void __launch_bounds__(128) finalize_kernel(const __grid_constant__ FinalizeParams P) {
-    pdl_wait();
+    if (!FIC_FIN_EARLY) pdl_wait();
     pdl_trigger();
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= (int)*P.d_nr) return;
     if (P.d_misc[0] == 0) {  // ranges but no domain block survived the entropy filter
+        if (FIC_FIN_EARLY) pdl_wait();
         if (r == 0) *P.d_err = FIC_ERR_EMPTY_POOL;
         return;
     }
@@ -132,6 +140,7 @@ __global__ void __launch_bounds__(128) finalize_kernel(const __grid_constant__ F
         }
     }
     const double A = (double)((long long)n * srr - sr * sr);
+    if (FIC_FIN_EARLY) pdl_wait();  // the search's partials, split count and records from here on
     Best best;
     if (P.has_zero) {
         best.e = A;
