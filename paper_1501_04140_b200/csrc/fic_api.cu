@@ -53,6 +53,7 @@ struct fic_ctx {
     cudaEvent_t top_ready = nullptr;  // the top-level range list, selected on the side stream
     int b2_window = 1;    // env FIC_B2_WINDOW=0: B = 2 full scan instead of the C windows
     int top_side = 1;     // env FIC_TOP_SIDE=0: top-level range selection on the critical stream
+    int counts_kernel = 1;  // env FIC_COUNTS_KERNEL=0: the counters by cudaMemcpyAsync (A/B)
     Buf b_u, b_gthr, b_rop, b_dec, b_nccl;
     ncclComm_t comm = nullptr;  // fic_ctx_create_nccl: one rank per GPU
     int32_t nranks = 1, rank = 0;
@@ -646,7 +647,9 @@ fic_status fic_ctx_create(int32_t device, void *cuda_stream, fic_ctx **out) {
     e = cudaMalloc(&ctx->d_delta, sizeof(int64_t) * 4096);
     if (e == cudaSuccess)
         e = cudaMemcpy(ctx->d_delta, delta.data(), sizeof(int64_t) * 4096, cudaMemcpyHostToDevice);
-    if (e == cudaSuccess) e = cudaMallocHost(&ctx->h_counts, 64 * sizeof(unsigned long long));
+    if (e == cudaSuccess)  // (mapped: the counters' kernel writes it, FIC_COUNTS_KERNEL)
+        e = cudaHostAlloc(reinterpret_cast<void **>(&ctx->h_counts), 64 * sizeof(unsigned long long),
+                          cudaHostAllocPortable | cudaHostAllocMapped);
     if (e == cudaSuccess) e = grow(nullptr, ctx->b_counts, 64 * sizeof(unsigned long long));
     {
         const char *bw = getenv("FIC_B2_WINDOW");
@@ -655,6 +658,12 @@ fic_status fic_ctx_create(int32_t device, void *cuda_stream, fic_ctx **out) {
         ctx->top_side = tsd && strcmp(tsd, "0") == 0 ? 0 : 1;
         const char *ov = getenv("FIC_OVERLAP_POOLS");
         ctx->overlap_pools = ov ? atoi(ov) != 0 : 1;
+        const char *ck = getenv("FIC_COUNTS_KERNEL");
+        ctx->counts_kernel = ck && strcmp(ck, "0") == 0 ? 0 : 1;
+        // the counters' kernel writes the pinned host buffer through UVA (device-accessible)
+        int uva = 0;
+        if (e == cudaSuccess) e = cudaDeviceGetAttribute(&uva, cudaDevAttrUnifiedAddressing, device);
+        if (!uva) ctx->counts_kernel = 0;
     }
     for (int l = 0; l < fic::kMaxLevels && e == cudaSuccess; ++l)
         for (int q = 0; q < 5 && e == cudaSuccess; ++q) e = cudaEventCreate(&ctx->ev[l][q]);
@@ -1028,7 +1037,11 @@ static fic_status encode_body(fic_ctx *ctx, const uint8_t *img, int32_t N, int32
     CK(cudaStreamWaitEvent(st, ctx->main_ready, 0));
     const bool trace = ctx->timing >= 2 && getenv("FIC_TRACE");
     if (trace) CK(cudaEventRecord(ctx->ev[fic::kMaxLevels - 1][0], st));
-    CK(cudaMemcpyAsync(ctx->h_counts, d_counts, 64 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    if (ctx->counts_kernel) {
+        CK(fic::launch_copy_counts(d_counts, ctx->h_counts, 64, st));
+        ctx->stats[0].kernel_launches += 1;
+    } else
+        CK(cudaMemcpyAsync(ctx->h_counts, d_counts, 64 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
     if (trace) CK(cudaEventRecord(ctx->ev[fic::kMaxLevels - 1][1], st));
     const auto hs0 = std::chrono::steady_clock::now();
     CK(cudaStreamSynchronize(st));

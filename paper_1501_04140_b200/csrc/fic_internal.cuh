@@ -288,6 +288,7 @@ cudaError_t launch_select_records(const uint8_t *flags, int64_t n, int64_t *bloc
 cudaError_t launch_set_u64(unsigned long long *d, unsigned long long v, cudaStream_t st);
 // *d_acc += *d_add (single thread)
 cudaError_t launch_accumulate(unsigned long long *d_acc, const unsigned long long *d_add, cudaStream_t st);
+cudaError_t launch_copy_counts(const unsigned long long *d_src, unsigned long long *h_dst, int n, cudaStream_t st);
 
 size_t select_blocksum_len(int64_t n);
 cudaError_t launch_top_flags(uint8_t *flags, int64_t G, int32_t shard, int32_t n_shards,

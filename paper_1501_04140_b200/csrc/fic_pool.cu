@@ -429,6 +429,18 @@ cudaError_t launch_set_u64(unsigned long long *d, unsigned long long v, cudaStre
 
 __global__ void accumulate_kernel(unsigned long long *acc, const unsigned long long *add) { *acc += *add; }
 
+// The encode's counters straight into page-locked host memory (mapped under UVA): one tiny kernel
+// after the join instead of a device -> host copy-engine transfer.
+__global__ void copy_counts_kernel(const unsigned long long *__restrict__ src, unsigned long long *dst, int n) {
+    const int i = threadIdx.x;
+    if (i < n) dst[i] = src[i];
+}
+
+cudaError_t launch_copy_counts(const unsigned long long *d_src, unsigned long long *h_dst, int n, cudaStream_t st) {
+    copy_counts_kernel<<<1, 64, 0, st>>>(d_src, h_dst, n);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_accumulate(unsigned long long *d_acc, const unsigned long long *d_add, cudaStream_t st) {
     accumulate_kernel<<<1, 1, 0, st>>>(d_acc, d_add);
     return cudaGetLastError();
